@@ -1,0 +1,223 @@
+/*
+ * gcctb.h -- C ABI of the B200-native batched-OLTP concurrency-control library
+ * (libgcctb.so).  Re-designs the hot path measured by the gCCTB testbed of
+ * "GPU-Accelerated OLTP: An In-Depth Analysis of Concurrency Control Schemes"
+ * (arXiv 2406.10158).  Citations are PAPER.md / SPEC.md line numbers.
+ *
+ * Problem statement: tables and indexes are resident in device
+ * memory; transactions consist only of reads and writes whose read/write sets are
+ * known before execution; a batch is executed with one worker per transaction under
+ * one concurrency-control (CC) scheme until every transaction commits; results stay
+ * in device memory.
+ *
+ * Conventions for every entry point:
+ *   - Plain C types only; every call returns cc_status; no C++ exception crosses the ABI.
+ *   - Argument / configuration errors return before anything is enqueued.
+ *   - Device work is asynchronous on the db's stream.  Asynchronous faults (a CUDA
+ *     error, the device watchdog, timestamp overflow) surface at the next cc_sync() /
+ *     cc_submit(); after a CUDA fault the db is sticky-failed (CC_ERR_STATE).
+ *   - Ownership: the db owns every device allocation it makes (tables, indexes, CC
+ *     metadata, version arena, queues, batches).  The caller owns result buffers and
+ *     any host / device source buffers it passes in (they are read before return for
+ *     host sources, or before the next stream operation completes for device sources).
+ *   - A db is not re-entrant: one host thread at a time.
+ *   - cc_last_error(db) returns a message for the last failing call (valid until the
+ *     next call on that db).
+ */
+#ifndef GCCTB_H
+#define GCCTB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CC_OK = 0,
+    CC_ERR_INVALID_ARG = 1,
+    CC_ERR_CONFIG = 2,            /* ConfigError */
+    CC_ERR_OOM = 3,
+    CC_ERR_CUDA = 4,
+    CC_ERR_NCCL = 5,
+    CC_ERR_KEY_NOT_FOUND = 6,     /* KeyNotFound */
+    CC_ERR_TS_OVERFLOW = 7,       /* TimestampOverflow at 2^31-1 */
+    CC_ERR_VERSION_EXHAUSTED = 8, /* VersionExhausted */
+    CC_ERR_WATCHDOG = 9,          /* WatchdogTimeout */
+    CC_ERR_STATE = 10,            /* sticky after a device fault */
+    CC_ERR_UNSUPPORTED = 11
+} cc_status;
+
+/* The eight schemes of PAPER.md Table I. */
+typedef enum {
+    CC_TPL_NW = 0,  /* 2PL no-wait */
+    CC_TPL_WD = 1,  /* 2PL wait-die */
+    CC_TO = 2,      /* basic timestamp ordering */
+    CC_MVCC = 3,    /* multi-version TO */
+    CC_SILO = 4,    /* OCC */
+    CC_TICTOC = 5,  /* OCC */
+    CC_GPUTX = 6,   /* conflict-graph ranks / K-sets */
+    CC_GACCO = 7    /* preprocessed lock table */
+} cc_scheme;
+
+#define CC_NUM_SCHEMES 8
+
+typedef struct cc_db_s *cc_db;
+typedef struct cc_batch_s *cc_batch;
+
+/* ---------------------------------------------------------------- db lifetime */
+typedef struct {
+    int device;        /* CUDA device ordinal */
+    void *stream;      /* cudaStream_t to run on; NULL = the library creates one */
+    int rank;          /* partition id of this process (0 for a single GPU) */
+    int world;         /* number of partitions (1 for a single GPU) */
+} cc_db_desc;
+
+/* Create a db bound to (device, stream).  *out receives the handle. */
+cc_status cc_db_create(const cc_db_desc *desc, cc_db *out);
+/* Free every device allocation of the db (waits for its stream first). */
+cc_status cc_db_destroy(cc_db db);
+/* Message of the last failing call on db (never NULL; "" when none). */
+const char *cc_last_error(cc_db db);
+/* Library build string (arch, version).  Never NULL. */
+const char *cc_version(void);
+
+/* ------------------------------------------------------- tables and indexes
+ * Row store: one fixed-size array of tuples per table; all CC-managed tables share
+ * one monotonically increasing record id space.
+ * Table size is fixed for the life of the db (no insert/delete). */
+
+/* Create a table of `rows` rows of `row_bytes` bytes (multiple of 8), zero-filled.
+ * *table_id receives its id.  Errors: INVALID_ARG (row_bytes==0 or not a multiple of
+ * 8, rows==0), OOM. */
+cc_status cc_table_create(cc_db db, const char *name, uint32_t row_bytes, uint64_t rows,
+                          uint32_t *table_id);
+/* Copy n rows from src (host if src_on_device==0, else device) into rows
+ * [first_row, first_row+n).  Synchronous for host sources. */
+cc_status cc_table_load(cc_db db, uint32_t table_id, uint64_t first_row, uint64_t n,
+                        const void *src, int src_on_device);
+/* Copy rows [first_row, first_row+n) to dst (host or device).  Waits for the db
+ * stream, so it observes every submitted batch. */
+cc_status cc_table_read(cc_db db, uint32_t table_id, uint64_t first_row, uint64_t n,
+                        void *dst, int dst_on_device);
+/* Number of rows / row bytes of a table. */
+cc_status cc_table_info(cc_db db, uint32_t table_id, uint64_t *rows, uint32_t *row_bytes);
+
+/* Sorted-array index over table_id: sorted_keys[i] strictly ascending,
+ * row_ids[i] < rows(table).  A lookup is a binary search.  INVALID_ARG unless strictly
+ * ascending.  *index_id receives the id. */
+cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_keys,
+                          const uint64_t *row_ids, uint64_t n, int src_on_device,
+                          uint32_t *index_id);
+
+/* ----------------------------------------------------------------- YCSB
+ * YCSB table: n_rows rows of 16 x u64 (128 B); word j of row k is
+ * mix64(seed ^ (16k + j)) for j < 15 and word 15 (a write counter) is 0, where mix64
+ * is the splitmix64 finaliser (reading Z11).  Creates table "usertable" and
+ * its primary-key index (key k -> row k), generated on the device. */
+typedef struct {
+    uint64_t n_rows;
+    uint64_t seed;
+} cc_ycsb_db_desc;
+cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *desc);
+
+/* On-device YCSB batch generator.
+ * thresholds: u64[n_rows] Zipf inverse-CDF table (see inputs/ycsb.py), host or device
+ * per thresholds_on_device; it is read during the call (device) or copied (host).
+ * Key = ((rank-1) * scramble_mult) mod n_rows; duplicates within a transaction are
+ * resampled; each transaction's keys are sorted ascending; each access writes with
+ * probability write_frac; field in [0, 15). */
+typedef struct {
+    uint32_t n_txn;
+    uint32_t ops_per_txn;      /* K, 1..16 */
+    double write_frac;         /* W in [0, 1] */
+    uint64_t seed;
+    const uint64_t *thresholds;
+    int thresholds_on_device;
+    uint64_t scramble_mult;    /* must be coprime with n_rows */
+} cc_ycsb_gen_desc;
+cc_status cc_batch_gen_ycsb(cc_db db, const cc_ycsb_gen_desc *g, cc_batch *out);
+
+/* Import a YCSB-form batch: keys u32[n_txn*K] (primary keys of "usertable", sorted
+ * ascending and distinct within each transaction), ops u8[n_txn*K] (bit7 = write,
+ * bits 0..3 = field < 15).  KEY_NOT_FOUND surfaces at submit for unknown keys. */
+cc_status cc_batch_import_ycsb(cc_db db, const uint32_t *keys, const uint8_t *ops,
+                               uint32_t n_txn, uint32_t ops_per_txn, int src_on_device,
+                               cc_batch *out);
+/* Export a YCSB batch to host buffers (keys u32[n*K], ops u8[n*K]). */
+cc_status cc_batch_export_ycsb(cc_db db, cc_batch b, uint32_t *keys, uint8_t *ops);
+/* Batch geometry. */
+cc_status cc_batch_info(cc_db db, cc_batch b, uint32_t *n_txn, uint32_t *ops_per_txn,
+                        uint32_t *kind);
+cc_status cc_batch_free(cc_db db, cc_batch b);
+
+/* ------------------------------------------------------------ execution */
+#define CC_FLAG_IMMEDIATE_RETRY 0x1u /* paper mode: the worker re-runs its own aborted
+                                        transaction at once instead of
+                                        appending it to the retry queue */
+#define CC_FLAG_TIMING 0x2u          /* record CUDA events around each phase; read them
+                                        with cc_timing_read() */
+
+typedef struct {
+    cc_scheme scheme;
+    uint32_t wd;            /* warp density: 2^wd working lanes per warp, 0..5 */
+    uint32_t bs;            /* block size: warps per block, 1..32 */
+    uint32_t flags;         /* CC_FLAG_* */
+    uint32_t grid;          /* blocks; 0 = resident capacity (persistent grid) */
+    double watchdog_s;      /* device watchdog in seconds (0 = 30 s) */
+} cc_exec_desc;
+
+/* Per-transaction results, all DEVICE pointers owned by the caller.  Any may be NULL
+ * except committed.  n = n_txn of the batch, K = ops_per_txn.
+ *   committed u8[n]   1 iff the transaction committed
+ *   restarts  u32[n]  number of aborted attempts
+ *   order_hi/lo u64[n] the scheme's serialization-order key;
+ *                     ascending (hi, lo) is a valid serial order of the committed set
+ *   commit_pos u32[n] dense position of the transaction in that order
+ *   read_out  u64[n*K] per-op value read (YCSB: fingerprint of the row read)
+ *   stats     u64[CC_STATS_WORDS] device counters (see cc_stats)               */
+#define CC_STATS_WORDS 16
+typedef struct {
+    uint8_t *committed;
+    uint32_t *restarts;
+    uint64_t *order_hi;
+    uint64_t *order_lo;
+    uint32_t *commit_pos;
+    uint64_t *read_out;
+    uint64_t *stats;
+} cc_result;
+
+/* Host view of the stats words. */
+typedef struct {
+    uint64_t commits;       /* committed transactions */
+    uint64_t aborts;        /* sum of restarts (abort rate = aborts / commits) */
+    uint64_t attempts;
+    uint64_t error;         /* device-side cc_status (0 = ok) */
+    uint64_t max_rank;      /* GPUTx: number of K-sets - 1 */
+    uint64_t ts_last;       /* TO/MVCC: last timestamp drawn */
+    uint64_t reserved[10];
+} cc_stats;
+
+/* Run batch b under desc->scheme: reset the scheme's CC state (a2), preprocess
+ * (GPUTx/GaccO, a3), execute with compaction of aborts into a retry queue until every
+ * transaction commits (a4-a6), then emit results (a7).  Asynchronous on the db stream. */
+cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res);
+/* Wait for the db stream; surface asynchronous errors; if st != NULL copy the stats of
+ * the last submit into it. */
+cc_status cc_sync(cc_db db, cc_stats *st);
+
+/* Phase timing (CC_FLAG_TIMING): accumulated milliseconds per phase over the submits
+ * since the last reset: ms[0]=reset(a2) ms[1]=prep(a3) ms[2]=exec(a4-a6)
+ * ms[3]=emit(a7) ms[4]=whole submit; *n_submits receives the count.  Waits for the
+ * stream.  reset != 0 clears the accumulators. */
+cc_status cc_timing_read(cc_db db, double ms[5], uint64_t *n_submits, int reset);
+
+/* Device-side snapshot of every table's bytes: save=1 copies tables -> snapshot,
+ * save=0 restores.  Used to reset the db between measurement repetitions. */
+cc_status cc_snapshot(cc_db db, int save);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCCTB_H */

@@ -1,0 +1,176 @@
+"""Python convenience layer over the C ABI: torch tensors as caller-owned device result
+buffers, the db stream = the current torch stream.  Marshalling only."""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import gcctb as G
+
+
+@dataclass
+class Result:
+    committed: torch.Tensor
+    restarts: torch.Tensor
+    order_hi: torch.Tensor
+    order_lo: torch.Tensor
+    commit_pos: torch.Tensor
+    read_out: torch.Tensor | None
+    stats: torch.Tensor
+
+    @staticmethod
+    def alloc(n_txn: int, K: int, device, read_out=True) -> "Result":
+        z = dict(device=device)
+        return Result(
+            committed=torch.zeros(n_txn, dtype=torch.uint8, **z),
+            restarts=torch.zeros(n_txn, dtype=torch.int32, **z),
+            order_hi=torch.zeros(n_txn, dtype=torch.int64, **z),
+            order_lo=torch.zeros(n_txn, dtype=torch.int64, **z),
+            commit_pos=torch.zeros(n_txn, dtype=torch.int32, **z),
+            read_out=torch.zeros(n_txn * K, dtype=torch.int64, **z) if read_out else None,
+            stats=torch.zeros(G.CC_STATS_WORDS, dtype=torch.int64, **z),
+        )
+
+    def c(self) -> G.cc_result:
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        return G.cc_result(p(self.committed), p(self.restarts), p(self.order_hi), p(self.order_lo),
+                           p(self.commit_pos), p(self.read_out), p(self.stats))
+
+    def host(self) -> dict:
+        u = lambda t: t.cpu().numpy()  # noqa: E731
+        d = {
+            "committed": u(self.committed),
+            "restarts": u(self.restarts).view(np.uint32),
+            "order_hi": u(self.order_hi).view(np.uint64),
+            "order_lo": u(self.order_lo).view(np.uint64),
+            "commit_pos": u(self.commit_pos).view(np.uint32),
+        }
+        if self.read_out is not None:
+            d["read_out"] = u(self.read_out).view(np.uint64)
+        return d
+
+
+class Batch:
+    def __init__(self, db: "DB", handle):
+        self.db = db
+        self.h = handle
+        n, k, kind = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        G.check(db.h, G.lib().cc_batch_info(db.h, handle, ctypes.byref(n), ctypes.byref(k),
+                                            ctypes.byref(kind)))
+        self.n_txn, self.K, self.kind = n.value, k.value, kind.value
+
+    def export_ycsb(self):
+        keys = np.zeros(self.n_txn * self.K, dtype=np.uint32)
+        ops = np.zeros(self.n_txn * self.K, dtype=np.uint8)
+        G.check(self.db.h, G.lib().cc_batch_export_ycsb(self.db.h, self.h, keys.ctypes.data,
+                                                        ops.ctypes.data))
+        return keys, ops
+
+    def free(self):
+        if self.h:
+            G.lib().cc_batch_free(self.db.h, self.h)
+            self.h = None
+
+
+class DB:
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1):
+        L = G.lib()
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        self.device = device
+        d = G.cc_db_desc(device, ctypes.c_void_p(stream.cuda_stream), rank, world)
+        h = ctypes.c_void_p()
+        G.check(None, L.cc_db_create(ctypes.byref(d), ctypes.byref(h)))
+        self.h = h
+        self.ycsb_rows = 0
+
+    def close(self):
+        if self.h:
+            G.lib().cc_db_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        G.check(self.h, st)
+
+    # ----------------------------------------------------------- YCSB
+    def load_ycsb(self, n_rows: int, seed: int):
+        d = G.cc_ycsb_db_desc(n_rows, seed)
+        self._chk(G.lib().cc_load_ycsb(self.h, ctypes.byref(d)))
+        self.ycsb_rows = n_rows
+        self.ycsb_table = 0
+
+    def gen_ycsb(self, n_txn: int, K: int, W: float, seed: int, thresholds, mult: int) -> Batch:
+        """thresholds: torch uint64/int64 cuda tensor or numpy uint64 array."""
+        if isinstance(thresholds, torch.Tensor):
+            ptr, on_dev = thresholds.data_ptr(), 1
+            keep = thresholds
+        else:
+            keep = np.ascontiguousarray(thresholds, dtype=np.uint64)
+            ptr, on_dev = keep.ctypes.data, 0
+        g = G.cc_ycsb_gen_desc(n_txn, K, float(W), seed, ctypes.c_void_p(ptr), on_dev, mult)
+        h = ctypes.c_void_p()
+        self._chk(G.lib().cc_batch_gen_ycsb(self.h, ctypes.byref(g), ctypes.byref(h)))
+        del keep
+        return Batch(self, h)
+
+    def import_ycsb(self, keys, ops, K: int) -> Batch:
+        h = ctypes.c_void_p()
+        if isinstance(keys, torch.Tensor):
+            st = G.lib().cc_batch_import_ycsb(self.h, keys.data_ptr(), ops.data_ptr(),
+                                              keys.numel() // K, K, 1, ctypes.byref(h))
+        else:
+            k = np.ascontiguousarray(keys, dtype=np.uint32)
+            o = np.ascontiguousarray(ops, dtype=np.uint8)
+            st = G.lib().cc_batch_import_ycsb(self.h, k.ctypes.data, o.ctypes.data, k.size // K, K,
+                                              0, ctypes.byref(h))
+        self._chk(st)
+        return Batch(self, h)
+
+    def read_table(self, table_id: int = 0) -> np.ndarray:
+        rows, rb = ctypes.c_uint64(), ctypes.c_uint32()
+        self._chk(G.lib().cc_table_info(self.h, table_id, ctypes.byref(rows), ctypes.byref(rb)))
+        out = np.zeros(rows.value * rb.value // 8, dtype=np.uint64)
+        self._chk(G.lib().cc_table_read(self.h, table_id, 0, rows.value, out.ctypes.data, 0))
+        return out.reshape(rows.value, rb.value // 8)
+
+    def load_table(self, table_id: int, rows: np.ndarray, first: int = 0):
+        r = np.ascontiguousarray(rows)
+        rb = r.shape[1] * r.itemsize if r.ndim == 2 else None
+        n = r.shape[0]
+        self._chk(G.lib().cc_table_load(self.h, table_id, first, n, r.ctypes.data, 0))
+
+    # ----------------------------------------------------------- execution
+    def submit(self, batch: Batch, scheme, wd: int = 0, bs: int = 32, flags: int = 0,
+               grid: int = 0, watchdog_s: float = 30.0, result: Result | None = None,
+               read_out=True) -> Result:
+        sid = G.SCHEME_ID[scheme] if isinstance(scheme, str) else int(scheme)
+        if result is None:
+            result = Result.alloc(batch.n_txn, batch.K, torch.device("cuda", self.device), read_out)
+        d = G.cc_exec_desc(sid, wd, bs, flags, grid, watchdog_s)
+        r = result.c()
+        self._chk(G.lib().cc_submit(self.h, batch.h, ctypes.byref(d), ctypes.byref(r)))
+        return result
+
+    def sync(self) -> G.cc_stats:
+        s = G.cc_stats()
+        self._chk(G.lib().cc_sync(self.h, ctypes.byref(s)))
+        return s
+
+    def timing(self, reset: bool = False):
+        ms = (ctypes.c_double * 5)()
+        n = ctypes.c_uint64()
+        self._chk(G.lib().cc_timing_read(self.h, ctypes.byref(ms), ctypes.byref(n), int(reset)))
+        return list(ms), n.value
+
+    def snapshot(self, save: bool):
+        self._chk(G.lib().cc_snapshot(self.h, 1 if save else 0))

@@ -1,0 +1,639 @@
+// db.cu -- host driver behind the C ABI (include/gcctb.h).  It owns every device
+// allocation, enqueues the a1..a7 kernels on the db stream, and turns device errors
+// into cc_status.  No torch types anywhere: plain pointers and sizes.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace gcctb {
+cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, unsigned long long *ohi,
+                            unsigned long long *olo, uint32_t n, cudaStream_t s);
+int rank_kernel_grid();
+}  // namespace gcctb
+
+using namespace gcctb;
+typedef unsigned long long u64;
+
+struct Table {
+    std::string name;
+    uint32_t row_bytes;
+    uint64_t rows;
+    uint64_t base;   // first record id
+    void *d;
+};
+struct Index {
+    uint32_t table;
+    uint64_t n;
+    u64 *keys;
+    u64 *rowids;
+};
+
+struct cc_batch_s {
+    uint32_t kind;
+    uint32_t n_txn;
+    uint32_t K;
+    uint32_t *keys;
+    uint8_t *ops;
+};
+
+struct Pending {
+    cudaEvent_t ev[5];
+};
+
+struct cc_db_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int rank = 0, world = 1;
+    int num_sms = 148;
+    std::string err;
+    cc_status sticky = CC_OK;
+    std::vector<Table> tables;
+    std::vector<Index> indexes;
+    uint64_t n_records = 0;
+    u64 *meta = nullptr;
+    uint64_t meta_records = 0;
+    int ycsb_table = -1, ycsb_index = -1;
+    // per-submit scratch (grown on demand)
+    Ctl *ctl = nullptr;
+    u64 *stats_scratch = nullptr;
+    u64 *sticky_dev = nullptr;
+    uint32_t cap_txn = 0;
+    uint64_t cap_acc = 0;
+    uint8_t *committed = nullptr;
+    uint32_t *restarts = nullptr;
+    u64 *ohi = nullptr, *olo = nullptr;
+    u64 *ring = nullptr;
+    uint32_t ring_cap = 0;
+    u64 *arena = nullptr;
+    uint64_t arena_nodes = 0;
+    uint32_t arena_row_words = 0;
+    PrepBufs prep{};
+    std::vector<void *> prep_allocs;
+    std::vector<void *> snap;
+    std::vector<Pending> pending;
+    std::vector<Pending> free_events;
+    double acc[5] = {0, 0, 0, 0, 0};
+    uint64_t n_timed = 0;
+    cc_stats last{};
+    std::vector<cc_batch_s *> batches;
+};
+
+static cc_status fail(cc_db db, cc_status st, const char *fmt, ...) {
+    if (db) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        db->err = buf;
+        if (st == CC_ERR_CUDA) db->sticky = CC_ERR_STATE;
+    }
+    return st;
+}
+
+#define CUDA_TRY(db, x)                                                                   \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(db, e_ == cudaErrorMemoryAllocation ? CC_ERR_OOM : CC_ERR_CUDA,   \
+                        "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define CHECK_DB(db)                                                         \
+    do {                                                                     \
+        if (!(db)) return CC_ERR_INVALID_ARG;                                \
+        if ((db)->sticky != CC_OK) return (db)->sticky;                      \
+        if (cudaSetDevice((db)->device) != cudaSuccess)                      \
+            return fail(db, CC_ERR_CUDA, "cudaSetDevice(%d) failed", (db)->device); \
+    } while (0)
+
+template <class T>
+static cudaError_t dalloc(T **p, size_t bytes) {
+    return cudaMalloc((void **)p, bytes ? bytes : 16);
+}
+
+extern "C" {
+
+const char *cc_version(void) { return "gcctb-b200 0.1 (sm_100a, CUDA " "12.9)"; }
+
+const char *cc_last_error(cc_db db) { return db ? db->err.c_str() : "null db"; }
+
+cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
+    if (!desc || !out) return CC_ERR_INVALID_ARG;
+    if (desc->world < 1 || desc->rank < 0 || desc->rank >= desc->world) return CC_ERR_INVALID_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return CC_ERR_CUDA;
+    if (desc->device < 0 || desc->device >= ndev) return CC_ERR_INVALID_ARG;
+    cc_db db = new cc_db_s();
+    db->device = desc->device;
+    db->rank = desc->rank;
+    db->world = desc->world;
+    if (cudaSetDevice(db->device) != cudaSuccess) { delete db; return CC_ERR_CUDA; }
+    cudaDeviceGetAttribute(&db->num_sms, cudaDevAttrMultiProcessorCount, db->device);
+    if (desc->stream) {
+        db->stream = (cudaStream_t)desc->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete db;
+            return CC_ERR_CUDA;
+        }
+        db->own_stream = true;
+    }
+    if (dalloc(&db->ctl, sizeof(Ctl)) || dalloc(&db->stats_scratch, 8 * CC_STATS_WORDS) ||
+        dalloc(&db->sticky_dev, 8)) {
+        delete db;
+        return CC_ERR_OOM;
+    }
+    cudaMemset(db->sticky_dev, 0, 8);
+    cudaMemset(db->ctl, 0, sizeof(Ctl));
+    *out = db;
+    return CC_OK;
+}
+
+static void free_scratch(cc_db db) {
+    cudaFree(db->committed); cudaFree(db->restarts); cudaFree(db->ohi); cudaFree(db->olo);
+    cudaFree(db->ring);
+    for (void *p : db->prep_allocs) cudaFree(p);
+    db->prep_allocs.clear();
+    db->committed = nullptr; db->restarts = nullptr; db->ohi = db->olo = nullptr; db->ring = nullptr;
+    db->cap_txn = 0;
+    db->cap_acc = 0;
+}
+
+cc_status cc_db_destroy(cc_db db) {
+    if (!db) return CC_ERR_INVALID_ARG;
+    cudaSetDevice(db->device);
+    cudaStreamSynchronize(db->stream);
+    for (auto &t : db->tables) cudaFree(t.d);
+    for (auto &i : db->indexes) { cudaFree(i.keys); cudaFree(i.rowids); }
+    for (void *p : db->snap) cudaFree(p);
+    for (auto *b : db->batches) { cudaFree(b->keys); cudaFree(b->ops); delete b; }
+    for (auto &pe : db->pending) for (auto &e : pe.ev) cudaEventDestroy(e);
+    for (auto &pe : db->free_events) for (auto &e : pe.ev) cudaEventDestroy(e);
+    free_scratch(db);
+    cudaFree(db->arena);
+    cudaFree(db->meta);
+    cudaFree(db->ctl);
+    cudaFree(db->stats_scratch);
+    cudaFree(db->sticky_dev);
+    if (db->own_stream) cudaStreamDestroy(db->stream);
+    delete db;
+    return CC_OK;
+}
+
+// ---------------------------------------------------------------- tables
+cc_status cc_table_create(cc_db db, const char *name, uint32_t row_bytes, uint64_t rows,
+                          uint32_t *table_id) {
+    CHECK_DB(db);
+    if (!table_id || row_bytes == 0 || row_bytes % 8 || rows == 0)
+        return fail(db, CC_ERR_INVALID_ARG, "cc_table_create: bad row_bytes/rows");
+    if (db->n_records + rows > (1ull << 32))
+        return fail(db, CC_ERR_CONFIG, "cc_table_create: more than 2^32 records");
+    Table t;
+    t.name = name ? name : "";
+    t.row_bytes = row_bytes;
+    t.rows = rows;
+    t.base = db->n_records;
+    CUDA_TRY(db, dalloc(&t.d, (size_t)row_bytes * rows));
+    CUDA_TRY(db, cudaMemsetAsync(t.d, 0, (size_t)row_bytes * rows, db->stream));
+    // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B)
+    const uint64_t need = db->n_records + rows;
+    u64 *meta = nullptr;
+    CUDA_TRY(db, dalloc(&meta, need * 16));
+    if (db->meta) cudaFree(db->meta);
+    db->meta = meta;
+    db->meta_records = need;
+    db->n_records = need;
+    db->tables.push_back(t);
+    *table_id = (uint32_t)db->tables.size() - 1;
+    return CC_OK;
+}
+
+cc_status cc_table_info(cc_db db, uint32_t table_id, uint64_t *rows, uint32_t *row_bytes) {
+    CHECK_DB(db);
+    if (table_id >= db->tables.size()) return fail(db, CC_ERR_INVALID_ARG, "bad table id");
+    if (rows) *rows = db->tables[table_id].rows;
+    if (row_bytes) *row_bytes = db->tables[table_id].row_bytes;
+    return CC_OK;
+}
+
+cc_status cc_table_load(cc_db db, uint32_t table_id, uint64_t first_row, uint64_t n,
+                        const void *src, int src_on_device) {
+    CHECK_DB(db);
+    if (table_id >= db->tables.size() || !src) return fail(db, CC_ERR_INVALID_ARG, "bad args");
+    Table &t = db->tables[table_id];
+    if (first_row + n > t.rows) return fail(db, CC_ERR_INVALID_ARG, "row range out of table");
+    char *dst = (char *)t.d + first_row * t.row_bytes;
+    CUDA_TRY(db, cudaMemcpyAsync(dst, src, n * t.row_bytes,
+                                 src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 db->stream));
+    if (!src_on_device) CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    return CC_OK;
+}
+
+cc_status cc_table_read(cc_db db, uint32_t table_id, uint64_t first_row, uint64_t n, void *dst,
+                        int dst_on_device) {
+    CHECK_DB(db);
+    if (table_id >= db->tables.size() || !dst) return fail(db, CC_ERR_INVALID_ARG, "bad args");
+    Table &t = db->tables[table_id];
+    if (first_row + n > t.rows) return fail(db, CC_ERR_INVALID_ARG, "row range out of table");
+    const char *src = (const char *)t.d + first_row * t.row_bytes;
+    CUDA_TRY(db, cudaMemcpyAsync(dst, src, n * t.row_bytes,
+                                 dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    return CC_OK;
+}
+
+cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_keys,
+                          const uint64_t *row_ids, uint64_t n, int src_on_device,
+                          uint32_t *index_id) {
+    CHECK_DB(db);
+    if (table_id >= db->tables.size() || !sorted_keys || !row_ids || !index_id || n == 0)
+        return fail(db, CC_ERR_INVALID_ARG, "cc_index_create: bad args");
+    std::vector<uint64_t> hk, hr;
+    const uint64_t *k = sorted_keys, *r = row_ids;
+    if (src_on_device) {
+        hk.resize(n); hr.resize(n);
+        CUDA_TRY(db, cudaMemcpy(hk.data(), sorted_keys, n * 8, cudaMemcpyDeviceToHost));
+        CUDA_TRY(db, cudaMemcpy(hr.data(), row_ids, n * 8, cudaMemcpyDeviceToHost));
+        k = hk.data(); r = hr.data();
+    }
+    for (uint64_t i = 0; i < n; i++) {
+        if (i && k[i] <= k[i - 1]) return fail(db, CC_ERR_INVALID_ARG, "index keys not strictly ascending");
+        if (r[i] >= db->tables[table_id].rows) return fail(db, CC_ERR_INVALID_ARG, "row id out of table");
+    }
+    Index ix{table_id, n, nullptr, nullptr};
+    CUDA_TRY(db, dalloc(&ix.keys, n * 8));
+    CUDA_TRY(db, dalloc(&ix.rowids, n * 8));
+    CUDA_TRY(db, cudaMemcpy(ix.keys, k, n * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(db, cudaMemcpy(ix.rowids, r, n * 8, cudaMemcpyHostToDevice));
+    db->indexes.push_back(ix);
+    *index_id = (uint32_t)db->indexes.size() - 1;
+    return CC_OK;
+}
+
+// ---------------------------------------------------------------- YCSB
+cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *d) {
+    CHECK_DB(db);
+    if (!d || d->n_rows == 0 || d->n_rows > 0xFFFFFFFFull)
+        return fail(db, CC_ERR_INVALID_ARG, "cc_load_ycsb: bad n_rows");
+    if (db->ycsb_table >= 0) return fail(db, CC_ERR_CONFIG, "YCSB table already loaded");
+    uint32_t tid;
+    cc_status st = cc_table_create(db, "usertable", 128, d->n_rows, &tid);
+    if (st) return st;
+    Table &t = db->tables[tid];
+    CUDA_TRY(db, launch_ycsb_init_rows((u64 *)t.d, 0, d->n_rows, d->seed, db->stream));
+    Index ix{tid, d->n_rows, nullptr, nullptr};
+    CUDA_TRY(db, dalloc(&ix.keys, d->n_rows * 8));
+    CUDA_TRY(db, dalloc(&ix.rowids, d->n_rows * 8));
+    CUDA_TRY(db, launch_identity_index(ix.keys, ix.rowids, d->n_rows, db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    db->indexes.push_back(ix);
+    db->ycsb_table = (int)tid;
+    db->ycsb_index = (int)db->indexes.size() - 1;
+    return CC_OK;
+}
+
+static cc_status new_batch(cc_db db, uint32_t n_txn, uint32_t K, cc_batch *out) {
+    cc_batch b = new cc_batch_s();
+    b->kind = KIND_YCSB;
+    b->n_txn = n_txn;
+    b->K = K;
+    if (dalloc(&b->keys, (size_t)n_txn * K * 4) || dalloc(&b->ops, (size_t)n_txn * K)) {
+        cudaFree(b->keys);
+        delete b;
+        return fail(db, CC_ERR_OOM, "batch allocation failed");
+    }
+    db->batches.push_back(b);
+    *out = b;
+    return CC_OK;
+}
+
+cc_status cc_batch_gen_ycsb(cc_db db, const cc_ycsb_gen_desc *g, cc_batch *out) {
+    CHECK_DB(db);
+    if (!g || !out || !g->thresholds) return fail(db, CC_ERR_INVALID_ARG, "cc_batch_gen_ycsb: null");
+    if (db->ycsb_table < 0) return fail(db, CC_ERR_CONFIG, "no YCSB table loaded");
+    const uint64_t n = db->tables[db->ycsb_table].rows;
+    if (g->ops_per_txn == 0 || g->ops_per_txn > 16 || g->ops_per_txn > n || g->n_txn == 0 ||
+        g->n_txn > (1u << 21) || !(g->write_frac >= 0.0 && g->write_frac <= 1.0))
+        return fail(db, CC_ERR_CONFIG, "cc_batch_gen_ycsb: bad geometry (K 1..16, n_txn <= 2^21, W in [0,1])");
+    cc_batch b;
+    cc_status st = new_batch(db, g->n_txn, g->ops_per_txn, &b);
+    if (st) return st;
+    const u64 *T = (const u64 *)g->thresholds;
+    u64 *tmp = nullptr;
+    if (!g->thresholds_on_device) {
+        CUDA_TRY(db, dalloc(&tmp, n * 8));
+        CUDA_TRY(db, cudaMemcpyAsync(tmp, g->thresholds, n * 8, cudaMemcpyHostToDevice, db->stream));
+        T = tmp;
+    }
+    CUDA_TRY(db, cudaMemsetAsync(db->ctl, 0, sizeof(Ctl), db->stream));
+    CUDA_TRY(db, launch_ycsb_gen(b->keys, b->ops, g->n_txn, g->ops_per_txn, n, g->write_frac,
+                                 g->seed, T, g->scramble_mult % n, db->ctl, db->stream));
+    if (tmp) {
+        CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+        cudaFree(tmp);
+    }
+    *out = b;
+    return CC_OK;
+}
+
+cc_status cc_batch_import_ycsb(cc_db db, const uint32_t *keys, const uint8_t *ops, uint32_t n_txn,
+                               uint32_t K, int src_on_device, cc_batch *out) {
+    CHECK_DB(db);
+    if (!keys || !ops || !out || n_txn == 0 || K == 0 || K > 16 || n_txn > (1u << 21))
+        return fail(db, CC_ERR_INVALID_ARG, "cc_batch_import_ycsb: bad args (K 1..16, n_txn <= 2^21)");
+    if (db->ycsb_table < 0) return fail(db, CC_ERR_CONFIG, "no YCSB table loaded");
+    cc_batch b;
+    cc_status st = new_batch(db, n_txn, K, &b);
+    if (st) return st;
+    const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CUDA_TRY(db, cudaMemcpyAsync(b->keys, keys, (size_t)n_txn * K * 4, kind, db->stream));
+    CUDA_TRY(db, cudaMemcpyAsync(b->ops, ops, (size_t)n_txn * K, kind, db->stream));
+    if (!src_on_device) CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    *out = b;
+    return CC_OK;
+}
+
+cc_status cc_batch_export_ycsb(cc_db db, cc_batch b, uint32_t *keys, uint8_t *ops) {
+    CHECK_DB(db);
+    if (!b || !keys || !ops || b->kind != KIND_YCSB) return fail(db, CC_ERR_INVALID_ARG, "bad batch");
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, cudaMemcpy(keys, b->keys, (size_t)b->n_txn * b->K * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(db, cudaMemcpy(ops, b->ops, (size_t)b->n_txn * b->K, cudaMemcpyDeviceToHost));
+    return CC_OK;
+}
+
+cc_status cc_batch_info(cc_db db, cc_batch b, uint32_t *n_txn, uint32_t *K, uint32_t *kind) {
+    if (!db || !b) return CC_ERR_INVALID_ARG;
+    if (n_txn) *n_txn = b->n_txn;
+    if (K) *K = b->K;
+    if (kind) *kind = b->kind;
+    return CC_OK;
+}
+
+cc_status cc_batch_free(cc_db db, cc_batch b) {
+    if (!db || !b) return CC_ERR_INVALID_ARG;
+    for (size_t i = 0; i < db->batches.size(); i++)
+        if (db->batches[i] == b) {
+            cudaStreamSynchronize(db->stream);
+            cudaFree(b->keys);
+            cudaFree(b->ops);
+            delete b;
+            db->batches.erase(db->batches.begin() + i);
+            return CC_OK;
+        }
+    return fail(db, CC_ERR_INVALID_ARG, "unknown batch");
+}
+
+// ---------------------------------------------------------------- execution
+static cc_status ensure_scratch(cc_db db, uint32_t n_txn, uint64_t n_acc) {
+    if (n_txn <= db->cap_txn && n_acc <= db->cap_acc) return CC_OK;
+    cudaStreamSynchronize(db->stream);
+    free_scratch(db);
+    const uint32_t nt = n_txn;
+    const uint64_t na = n_acc < nt ? nt : n_acc;
+    CUDA_TRY(db, dalloc(&db->committed, nt));
+    CUDA_TRY(db, dalloc(&db->restarts, (size_t)nt * 4));
+    CUDA_TRY(db, dalloc(&db->ohi, (size_t)nt * 8));
+    CUDA_TRY(db, dalloc(&db->olo, (size_t)nt * 8));
+    uint32_t cap = 1024;
+    while (cap < 2 * nt) cap <<= 1;
+    CUDA_TRY(db, dalloc(&db->ring, (size_t)cap * 8));
+    db->ring_cap = cap;
+    PrepBufs &b = db->prep;
+    auto A = [&](auto **p, size_t bytes) -> cudaError_t {
+        cudaError_t e = dalloc(p, bytes);
+        if (e == cudaSuccess) db->prep_allocs.push_back((void *)*p);
+        return e;
+    };
+    CUDA_TRY(db, A(&b.keys_in, na * 8));
+    CUDA_TRY(db, A(&b.keys_out, na * 8));
+    CUDA_TRY(db, A(&b.acc_rec, na * 4));
+    CUDA_TRY(db, A(&b.acc_seg, na * 4));
+    CUDA_TRY(db, A(&b.acc_pos, na * 4));
+    CUDA_TRY(db, A(&b.sorted_pos, na * 4));
+    CUDA_TRY(db, A(&b.head_flag, na * 4));
+    CUDA_TRY(db, A(&b.seg_id, na * 4));
+    CUDA_TRY(db, A(&b.seg_start, na * 4));
+    CUDA_TRY(db, A(&b.lw, na * 4));
+    CUDA_TRY(db, A(&b.cursor, na * 4));
+    CUDA_TRY(db, A(&b.rank, (size_t)nt * 4));
+    CUDA_TRY(db, A(&b.rank_sorted, (size_t)nt * 4));
+    CUDA_TRY(db, A(&b.gid_in, (size_t)nt * 4));
+    CUDA_TRY(db, A(&b.rank_order, (size_t)nt * 4));
+    CUDA_TRY(db, A(&b.rank_count, (size_t)nt * 4));
+    CUDA_TRY(db, A(&b.rank_done, (size_t)nt * 4));
+    CUDA_TRY(db, A(&b.rank_start, (size_t)nt * 4));
+    b.cub_bytes = prep_cub_bytes(na, nt);
+    CUDA_TRY(db, A((char **)&b.cub_tmp, b.cub_bytes));
+    db->cap_txn = nt;
+    db->cap_acc = na;
+    return CC_OK;
+}
+
+static cc_status ensure_arena(cc_db db, uint64_t nodes, uint32_t row_words) {
+    if (nodes <= db->arena_nodes && row_words == db->arena_row_words) return CC_OK;
+    cudaStreamSynchronize(db->stream);
+    cudaFree(db->arena);
+    db->arena = nullptr;
+    db->arena_nodes = 0;
+    CUDA_TRY(db, dalloc(&db->arena, nodes * (2 + row_words) * 8));
+    db->arena_nodes = nodes;
+    db->arena_row_words = row_words;
+    return CC_OK;
+}
+
+static Pending get_events(cc_db db) {
+    Pending p;
+    if (!db->free_events.empty()) {
+        p = db->free_events.back();
+        db->free_events.pop_back();
+        return p;
+    }
+    for (auto &e : p.ev) cudaEventCreate(&e);
+    return p;
+}
+
+cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res) {
+    CHECK_DB(db);
+    if (!b || !desc || !res || !res->committed)
+        return fail(db, CC_ERR_INVALID_ARG, "cc_submit: null batch/desc/result");
+    if ((unsigned)desc->scheme >= CC_NUM_SCHEMES) return fail(db, CC_ERR_INVALID_ARG, "bad scheme");
+    if (desc->wd > 5 || desc->bs < 1 || desc->bs > 32)
+        return fail(db, CC_ERR_INVALID_ARG, "wd must be 0..5 and bs 1..32 (PAPER.md:480-484)");
+    if (b->kind != KIND_YCSB) return fail(db, CC_ERR_UNSUPPORTED, "batch kind not supported");
+    const int scheme = (int)desc->scheme;
+    const bool det = scheme == CC_GPUTX || scheme == CC_GACCO;
+    const uint64_t n_acc = (uint64_t)b->n_txn * b->K;
+    cc_status st = ensure_scratch(db, b->n_txn, n_acc);
+    if (st) return st;
+    if (scheme == CC_MVCC) {
+        st = ensure_arena(db, n_acc, 16);   // one history node per write op
+        if (st) return st;
+    }
+    const Table &t = db->tables[db->ycsb_table];
+    const Index &ix = db->indexes[db->ycsb_index];
+
+    ExecParams p{};
+    p.scheme = scheme;
+    p.n_txn = b->n_txn;
+    p.K = b->K;
+    p.wd = desc->wd;
+    p.flags = desc->flags;
+    p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
+    p.ctl = db->ctl;
+    p.meta = db->meta;
+    p.arena = db->arena;
+    p.ring = db->ring;
+    p.ring_cap = db->ring_cap;
+    p.committed = db->committed;
+    p.restarts = db->restarts;
+    p.order_hi = db->ohi;
+    p.order_lo = db->olo;
+    p.read_out = (u64 *)res->read_out;
+    YcsbParams y{};
+    y.keys = b->keys;
+    y.ops = b->ops;
+    y.idx_keys = ix.keys;
+    y.idx_rows = ix.rowids;
+    y.idx_n = ix.n;
+    y.rows = (u64 *)t.d;
+    y.n_rows = t.rows;
+
+    const bool timing = desc->flags & CC_FLAG_TIMING;
+    Pending ev{};
+    if (timing) {
+        ev = get_events(db);
+        CUDA_TRY(db, cudaEventRecord(ev.ev[0], db->stream));
+    }
+    // a2: reset CC state (every record of every table)
+    CUDA_TRY(db, launch_reset_meta(scheme, db->meta, db->n_records, db->ring, db->ring_cap, db->ctl,
+                                   db->stream));
+    CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
+    if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[1], db->stream));
+    // a3: preprocessing for the conflict-graph schemes
+    if (det) {
+        CUDA_TRY(db, launch_ycsb_gather(p, y, db->prep, db->stream));
+        CUDA_TRY(db, launch_prep_common(p, db->prep, db->n_records, scheme == CC_GPUTX,
+                                        rank_kernel_grid(), db->stream));
+        p.acc_rec = db->prep.acc_rec;
+        p.acc_seg = db->prep.acc_seg;
+        p.acc_pos = db->prep.acc_pos;
+        p.cursor = db->prep.cursor;
+        p.rank_order = db->prep.rank_order;
+        p.rank_of = db->prep.rank;
+        p.rank_done = db->prep.rank_done;
+        p.rank_count = db->prep.rank_count;
+    }
+    if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[2], db->stream));
+    // a4-a6: persistent executor
+    const int block = 32 * (int)desc->bs;
+    int grid = (int)desc->grid;
+    if (grid <= 0) {
+        const int per_sm = ycsb_exec_max_blocks_per_sm(scheme, block);
+        if (per_sm <= 0) return fail(db, CC_ERR_CONFIG, "executor cannot launch %d threads/block", block);
+        grid = per_sm * db->num_sms;
+    }
+    CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, db->stream));
+    if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
+    // a7: commit positions + result copy-out
+    cc_result r = *res;
+    if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
+    CUDA_TRY(db, launch_finalize(p, r, db->prep, det, db->stream));
+    if ((void *)r.stats != (void *)db->stats_scratch)
+        CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS,
+                                     cudaMemcpyDeviceToDevice, db->stream));
+    if (timing) {
+        CUDA_TRY(db, cudaEventRecord(ev.ev[4], db->stream));
+        db->pending.push_back(ev);
+    }
+    return CC_OK;
+}
+
+static cc_status drain_timing(cc_db db) {
+    for (auto &pe : db->pending) {
+        float ms[4];
+        for (int i = 0; i < 4; i++) CUDA_TRY(db, cudaEventElapsedTime(&ms[i], pe.ev[i], pe.ev[i + 1]));
+        float tot;
+        CUDA_TRY(db, cudaEventElapsedTime(&tot, pe.ev[0], pe.ev[4]));
+        for (int i = 0; i < 4; i++) db->acc[i] += ms[i];
+        db->acc[4] += tot;
+        db->n_timed++;
+        db->free_events.push_back(pe);
+    }
+    db->pending.clear();
+    return CC_OK;
+}
+
+cc_status cc_sync(cc_db db, cc_stats *out) {
+    CHECK_DB(db);
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, cudaGetLastError());
+    u64 w[CC_STATS_WORDS];
+    CUDA_TRY(db, cudaMemcpy(w, db->stats_scratch, sizeof w, cudaMemcpyDeviceToHost));
+    cc_stats s{};
+    s.commits = w[0];
+    s.aborts = w[1];
+    s.attempts = w[2];
+    s.error = w[3];
+    s.max_rank = w[4];
+    s.ts_last = w[5];
+    db->last = s;
+    if (out) *out = s;
+    Ctl c;
+    CUDA_TRY(db, cudaMemcpy(&c, db->ctl, sizeof c, cudaMemcpyDeviceToHost));
+    const u64 e = c.err ? c.err : w[3];
+    if (e) {
+        static const char *names[] = {"ok", "invalid arg", "config", "oom", "cuda", "nccl",
+                                      "key not found", "timestamp overflow", "version exhausted",
+                                      "watchdog timeout", "state", "unsupported"};
+        return fail(db, (cc_status)e, "device reported: %s", e < 12 ? names[e] : "?");
+    }
+    return CC_OK;
+}
+
+cc_status cc_timing_read(cc_db db, double ms[5], uint64_t *n_submits, int reset) {
+    CHECK_DB(db);
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    cc_status st = drain_timing(db);
+    if (st) return st;
+    if (ms) for (int i = 0; i < 5; i++) ms[i] = db->acc[i];
+    if (n_submits) *n_submits = db->n_timed;
+    if (reset) {
+        for (double &a : db->acc) a = 0;
+        db->n_timed = 0;
+    }
+    return CC_OK;
+}
+
+cc_status cc_snapshot(cc_db db, int save) {
+    CHECK_DB(db);
+    if (save) {
+        for (void *p : db->snap) cudaFree(p);
+        db->snap.clear();
+        for (auto &t : db->tables) {
+            void *p = nullptr;
+            CUDA_TRY(db, dalloc(&p, (size_t)t.row_bytes * t.rows));
+            db->snap.push_back(p);
+            CUDA_TRY(db, cudaMemcpyAsync(p, t.d, (size_t)t.row_bytes * t.rows, cudaMemcpyDeviceToDevice,
+                                         db->stream));
+        }
+    } else {
+        if (db->snap.size() != db->tables.size()) return fail(db, CC_ERR_CONFIG, "no snapshot saved");
+        for (size_t i = 0; i < db->tables.size(); i++) {
+            auto &t = db->tables[i];
+            CUDA_TRY(db, cudaMemcpyAsync(t.d, db->snap[i], (size_t)t.row_bytes * t.rows,
+                                         cudaMemcpyDeviceToDevice, db->stream));
+        }
+    }
+    return CC_OK;
+}
+
+}  // extern "C"

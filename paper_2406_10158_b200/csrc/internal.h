@@ -1,0 +1,104 @@
+// internal.h -- structures shared by the host driver (db.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gcctb.h"
+
+namespace gcctb {
+
+// Device control block of one submit (all counters reset by the a2 reset kernel).
+struct Ctl {
+    unsigned long long head;     // claim counter over [0, n_txn) then the retry ring
+    unsigned long long tail;     // retry-ring append counter
+    unsigned long long done;     // committed transactions
+    unsigned long long ts;       // TO/MVCC timestamp allocator (first ts = 1)
+    unsigned long long ticket;   // lock-point / serialization-point ticket
+    unsigned long long err;      // first device error (cc_status), 0 = none
+    unsigned long long aborts;
+    unsigned long long attempts;
+    unsigned long long max_rank;
+    unsigned long long rank_head;  // GPUTx rank-pass claim counter
+    unsigned long long pad[6];
+};
+
+enum { KIND_YCSB = 1, KIND_TPCC = 2 };
+
+// Workload-independent execution parameters.
+struct ExecParams {
+    int scheme;
+    uint32_t n_txn;
+    uint32_t K;                  // accesses per transaction slot (YCSB ops_per_txn)
+    uint32_t wd;
+    uint32_t flags;
+    unsigned long long watchdog_ns;
+    Ctl *ctl;
+    unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
+    unsigned long long *arena;   // MVCC version nodes
+    unsigned long long *ring;    // retry queue
+    uint32_t ring_cap;           // power of two
+    // per-transaction internal results
+    uint8_t *committed;
+    uint32_t *restarts;
+    unsigned long long *order_hi;
+    unsigned long long *order_lo;
+    unsigned long long *read_out;  // caller buffer (may be null)
+    // deterministic-scheme tables (a3)
+    const uint32_t *acc_rec;     // resolved record of each access (n_txn*K) or null
+    const uint32_t *acc_seg;     // GaccO: segment (item) id of each access
+    const uint32_t *acc_pos;     // GaccO: queue position of each access
+    uint32_t *cursor;            // GaccO: per-segment owner cursor
+    const uint32_t *rank_order;  // GPUTx: transactions sorted by rank
+    const uint32_t *rank_of;     // GPUTx: rank of each transaction
+    uint32_t *rank_done;         // GPUTx: completed count per rank
+    const uint32_t *rank_count;  // GPUTx: size of each rank (K-set)
+};
+
+// YCSB workload parameters.
+struct YcsbParams {
+    const uint32_t *keys;        // n_txn*K primary keys
+    const uint8_t *ops;          // n_txn*K op bytes: bit7 write, bits 0..3 field
+    const unsigned long long *idx_keys;  // sorted-array index
+    const unsigned long long *idx_rows;
+    unsigned long long idx_n;
+    unsigned long long *rows;    // 16 x u64 per row
+    unsigned long long n_rows;
+};
+
+// Deterministic-scheme preprocessing buffers (a3), sized n_acc = n_txn*K.
+struct PrepBufs {
+    unsigned long long *keys_in, *keys_out;   // (rec << 27) | (gid << 6) | (i << 1) | w
+    uint32_t *acc_rec, *acc_seg, *acc_pos, *sorted_pos;
+    uint32_t *head_flag, *seg_id, *seg_start;
+    uint32_t *lw;          // last-write position (+1) at or before each sorted entry
+    uint32_t *cursor;
+    uint32_t *rank, *rank_sorted, *gid_in, *rank_order, *rank_count, *rank_done, *rank_start;
+    void *cub_tmp;
+    size_t cub_bytes;
+};
+
+// launchers (defined in the .cu files)
+cudaError_t launch_reset_meta(int scheme, unsigned long long *meta, uint64_t n_records,
+                              unsigned long long *ring, uint32_t ring_cap, Ctl *ctl,
+                              cudaStream_t s);
+cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
+                             cudaStream_t s);
+int ycsb_exec_max_blocks_per_sm(int scheme, int block);
+cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBufs &b,
+                               cudaStream_t s);
+cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,
+                               bool gputx, int grid, cudaStream_t s);
+cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
+                            bool deterministic, cudaStream_t s);
+size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
+
+cudaError_t launch_ycsb_init_rows(unsigned long long *rows, uint64_t first, uint64_t n,
+                                  uint64_t seed, cudaStream_t s);
+cudaError_t launch_identity_index(unsigned long long *keys, unsigned long long *rows,
+                                  uint64_t n, cudaStream_t s);
+cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
+                            uint64_t n_rows, double W, uint64_t seed,
+                            const unsigned long long *T, uint64_t mult, Ctl *ctl,
+                            cudaStream_t s);
+
+}  // namespace gcctb

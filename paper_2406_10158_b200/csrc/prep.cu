@@ -1,0 +1,306 @@
+// prep.cu -- a2 CC-state reset, a3 preprocessing for the deterministic schemes
+// (access table, GaccO lock table, GPUTx ranks / K-sets) and a7 result emission.
+//
+// Access table: every access becomes the 64-bit sort key
+//   (rec << 27) | (gid << 6) | (i << 1) | is_write
+// so one radix sort groups accesses per item with transaction ids ascending; segment
+// boundaries come from a head-flag prefix sum (the paper uses thrust sort + scan; we
+// use CUB from the toolkit).
+#include <cub/cub.cuh>
+
+#include "exec.cuh"
+
+namespace gcctb {
+
+constexpr int KEY_SHIFT = 27;
+constexpr u64 GID_MASK = (1ull << 21) - 1;
+
+// ------------------------------------------------------------------ a2 reset
+// Reset the scheme's CC words (the throughput window starts "from the initialization
+// of the CC method", Z19), the retry ring and the control block.
+__global__ void reset_kernel(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
+                             uint32_t ring_cap, Ctl *ctl) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (scheme == CC_MVCC) {
+        for (uint64_t r = tid; r < n_records; r += stride) {
+            // lo = 0 (RTS = WTS = 0, not pending); hi = head begins at ts 0, no history
+            reinterpret_cast<ulonglong2 *>(meta)[r] = make_ulonglong2(0ull, VNONE);
+        }
+    } else {
+        for (uint64_t r = tid; r < n_records; r += stride) meta[r] = 0ull;
+    }
+    for (uint64_t r = tid; r < ring_cap; r += stride) ring[r] = 0ull;
+    if (tid < sizeof(Ctl) / 8) reinterpret_cast<u64 *>(ctl)[tid] = 0ull;
+}
+
+__global__ void zero_txn_kernel(uint8_t *committed, uint32_t *restarts, u64 *ohi, u64 *olo,
+                                uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        committed[i] = 0;
+        restarts[i] = 0;
+        ohi[i] = ~0ull;
+        olo[i] = ~0ull;
+    }
+}
+
+cudaError_t launch_reset_meta(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
+                              uint32_t ring_cap, Ctl *ctl, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    reset_kernel<<<sms * 4, 512, 0, s>>>(scheme, meta, n_records, ring, ring_cap, ctl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, u64 *ohi, u64 *olo,
+                            uint32_t n, cudaStream_t s) {
+    zero_txn_kernel<<<(n + 255) / 256, 256, 0, s>>>(committed, restarts, ohi, olo, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a3 kernels
+__global__ void head_flag_kernel(const u64 *keys, uint32_t *head, uint32_t *wpos, uint64_t n) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const u64 k = keys[p];
+    head[p] = (p == 0 || (keys[p - 1] >> KEY_SHIFT) != (k >> KEY_SHIFT)) ? 1u : 0u;
+    wpos[p] = (k & 1ull) ? (uint32_t)(p + 1) : 0u;   // write marker for the last-write scan
+}
+
+__global__ void seg_start_kernel(const uint32_t *head, const uint32_t *seg_id, uint32_t *seg_start,
+                                 uint32_t *cursor, uint64_t n) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    if (head[p]) {
+        seg_start[seg_id[p] - 1] = (uint32_t)p;
+        cursor[seg_id[p] - 1] = 0u;
+    }
+}
+
+// GaccO lock table: queue position of each access inside its item's segment
+// ("recording which transaction currently owns each data item").
+__global__ void positions_kernel(const u64 *keys, const uint32_t *seg_id, const uint32_t *seg_start,
+                                 uint32_t K, uint32_t *acc_seg, uint32_t *acc_pos,
+                                 uint32_t *sorted_pos, uint64_t n) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const u64 k = keys[p];
+    const uint64_t gid = (k >> 6) & GID_MASK, i = (k >> 1) & 31u;
+    const uint64_t a = gid * K + i;
+    const uint32_t seg = seg_id[p] - 1;
+    acc_seg[a] = seg;
+    acc_pos[a] = (uint32_t)p - seg_start[seg];
+    sorted_pos[a] = (uint32_t)p;
+}
+
+// GPUTx ranks (PAPER.md:218 read per Z1): rank(T) = 1 + max rank over the conflicting
+// earlier transactions.  In each item's id-ordered segment a read depends on the last
+// earlier write; a write on the last earlier write and every read since (Z2: reads do
+// not conflict).  Dataflow pass: lanes claim transactions in increasing id (so every
+// predecessor is claimed by a running lane) and wait for predecessor ranks.
+constexpr uint32_t RANK_UNSET = 0xFFFFFFFFu;
+
+__global__ void __launch_bounds__(256) gputx_rank_kernel(
+    const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_id, const uint32_t *seg_start,
+    const uint32_t *lw, uint32_t *rank, uint32_t n_txn, uint32_t K, Ctl *ctl,
+    u64 watchdog_ns) {
+    const u64 deadline = globaltimer_ns() + watchdog_ns;
+    for (;;) {
+        const u64 s = agg_fetch_add(&ctl->rank_head);
+        if (s >= n_txn) return;
+        const uint32_t gid = (uint32_t)s;
+        uint32_t r = 0;
+        for (uint32_t i = 0; i < K; i++) {
+            const uint32_t p = sorted_pos[(u64)gid * K + i];
+            const uint32_t s0 = seg_start[seg_id[p] - 1];
+            const bool w = keys[p] & 1ull;
+            const uint32_t q = (p > s0) ? lw[p - 1] : 0u;    // last write before p (+1)
+            const bool has_q = q > s0;                          // inside this segment
+            uint32_t lo = has_q ? q - 1 : s0;                   // first predecessor to visit
+            uint32_t hi = w ? p : (has_q ? q : s0);             // reads: only the write
+            for (uint32_t x = lo; x < hi; x++) {
+                const uint32_t u = (uint32_t)((keys[x] >> 6) & GID_MASK);
+                uint32_t ru;
+                unsigned ns = 20;
+                while ((ru = ld_acquire32(&rank[u])) == RANK_UNSET) {
+                    if (ld_relaxed(&ctl->err) || globaltimer_ns() > deadline) {
+                        atomicCAS(&ctl->err, 0ull, (u64)CC_ERR_WATCHDOG);
+                        return;
+                    }
+                    __nanosleep(ns);
+                    ns = ns < 320 ? ns * 2 : 320;
+                }
+                r = max(r, ru + 1);
+            }
+        }
+        st_release32(&rank[gid], r);
+        atomicMax(&ctl->max_rank, (u64)r);
+    }
+}
+
+__global__ void fill_u32_kernel(uint32_t *a, uint32_t v, uint64_t n) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = v;
+}
+__global__ void iota_kernel(uint32_t *a, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = i;
+}
+
+// K-set boundaries over the rank-sorted transactions
+__global__ void rank_bounds_kernel(const uint32_t *rs, uint32_t *start, uint32_t *count,
+                                   uint32_t *done, uint32_t n) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint32_t r = rs[p];
+    if (p == 0 || rs[p - 1] != r) { start[r] = p; done[r] = 0; }
+}
+__global__ void rank_count_kernel(const uint32_t *rs, const uint32_t *start, uint32_t *count,
+                                  uint32_t n) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint32_t r = rs[p];
+    if (p == n - 1 || rs[p + 1] != r) count[r] = p + 1 - start[r];
+}
+
+int rank_kernel_grid() {
+    int dev = 0, sms = 148, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gputx_rank_kernel, 256, 0);
+    return (nb > 0 ? nb : 1) * sms;
+}
+
+static int bits_for(uint64_t x) {
+    int b = 1;
+    while (b < 64 && (1ull << b) <= x) b++;
+    return b;
+}
+
+size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn) {
+    size_t a = 0, b = 0, c = 0, d = 0, e = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, a, (const u64 *)nullptr, (u64 *)nullptr, (int)n_acc);
+    cub::DeviceScan::InclusiveSum(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_acc);
+    cub::DeviceScan::InclusiveScan(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                   cub::Max(), (int)n_acc);
+    cub::DeviceRadixSort::SortPairs(nullptr, d, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_txn);
+    cub::DeviceRadixSort::SortPairs(nullptr, e, (const u64 *)nullptr, (u64 *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_txn);
+    size_t m = a;
+    m = m > b ? m : b;
+    m = m > c ? m : c;
+    m = m > d ? m : d;
+    m = m > e ? m : e;
+    return m + 256;
+}
+
+cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records, bool gputx,
+                               int grid, cudaStream_t s) {
+    const uint64_t n = (uint64_t)p.n_txn * p.K;
+    const int blk = 256;
+    const unsigned g = (unsigned)((n + blk - 1) / blk);
+    size_t bytes = b.cub_bytes;
+    cudaError_t e;
+    const int end_bit = KEY_SHIFT + bits_for(n_records);
+    e = cub::DeviceRadixSort::SortKeys(b.cub_tmp, bytes, b.keys_in, b.keys_out, (int)n, 0,
+                                       end_bit > 64 ? 64 : end_bit, s);
+    if (e) return e;
+    head_flag_kernel<<<g, blk, 0, s>>>(b.keys_out, b.head_flag, b.lw, n);
+    bytes = b.cub_bytes;
+    e = cub::DeviceScan::InclusiveSum(b.cub_tmp, bytes, b.head_flag, b.seg_id, (int)n, s);
+    if (e) return e;
+    seg_start_kernel<<<g, blk, 0, s>>>(b.head_flag, b.seg_id, b.seg_start, b.cursor, n);
+    positions_kernel<<<g, blk, 0, s>>>(b.keys_out, b.seg_id, b.seg_start, p.K, b.acc_seg,
+                                       b.acc_pos, b.sorted_pos, n);
+    if (!gputx) return cudaGetLastError();
+    // last write at or before each sorted position (+1): inclusive max-scan of markers
+    bytes = b.cub_bytes;
+    // (head_flag is dead after the positions pass; it receives the scan output)
+    e = cub::DeviceScan::InclusiveScan(b.cub_tmp, bytes, b.lw, b.head_flag, cub::Max(), (int)n, s);
+    if (e) return e;
+    fill_u32_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank, RANK_UNSET, p.n_txn);
+    gputx_rank_kernel<<<grid, 256, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start, b.head_flag,
+                                           b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
+    iota_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.gid_in, p.n_txn);
+    bytes = b.cub_bytes;
+    e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.rank, b.rank_sorted, b.gid_in,
+                                        b.rank_order, (int)p.n_txn, 0, bits_for(p.n_txn), s);
+    if (e) return e;
+    rank_bounds_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank_sorted, b.rank_start,
+                                                                 b.rank_count, b.rank_done, p.n_txn);
+    rank_count_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank_sorted, b.rank_start,
+                                                                b.rank_count, p.n_txn);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a7 emission
+__global__ void commit_pos_kernel(const uint32_t *sorted_gid, const uint8_t *committed,
+                                  uint32_t *pos_out, uint32_t n) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const uint32_t g = sorted_gid[p];
+    pos_out[g] = committed[g] ? p : 0xFFFFFFFFu;
+}
+
+__global__ void gather_hi_kernel(const u64 *hi, const uint32_t *perm, u64 *out, uint32_t n) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) out[p] = hi[perm[p]];
+}
+
+__global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t *pos) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < p.n_txn) {
+        r.committed[i] = p.committed[i];
+        if (r.restarts) r.restarts[i] = p.restarts[i];
+        if (r.order_hi) r.order_hi[i] = p.order_hi[i];
+        if (r.order_lo) r.order_lo[i] = p.order_lo[i];
+        if (r.commit_pos) r.commit_pos[i] = pos[i];
+    }
+    if (i == 0 && r.stats) {
+        const Ctl *c = p.ctl;
+        r.stats[0] = c->done;
+        r.stats[1] = c->aborts;
+        r.stats[2] = c->done + c->aborts;
+        r.stats[3] = c->err;
+        r.stats[4] = c->max_rank;
+        r.stats[5] = c->ts;
+        for (int k = 6; k < CC_STATS_WORDS; k++) r.stats[k] = 0;
+    }
+}
+
+cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
+                            bool deterministic, cudaStream_t s) {
+    const uint32_t n = p.n_txn;
+    const int blk = 256;
+    const unsigned g = (n + blk - 1) / blk;
+    // commit positions: a stable radix sort of the order keys (lo, then hi when used)
+    uint32_t *pos = b.acc_pos;   // reuse as n-sized scratch after execution
+    if (deterministic) {
+        iota_kernel<<<g, blk, 0, s>>>(b.rank_order, n);
+        commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
+    } else {
+        iota_kernel<<<g, blk, 0, s>>>(b.gid_in, n);
+        size_t bytes = b.cub_bytes;
+        u64 *k1 = b.keys_in, *k2 = b.keys_out;   // n_acc >= n scratch
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, p.order_lo, k1, b.gid_in,
+                                                        b.rank_order, (int)n, 0, 64, s);
+        if (e) return e;
+        if (p.scheme == CC_TICTOC) {
+            gather_hi_kernel<<<g, blk, 0, s>>>(p.order_hi, b.rank_order, k1, n);
+            bytes = b.cub_bytes;
+            e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, k1, k2, b.rank_order, b.gid_in,
+                                                (int)n, 0, 64, s);
+            if (e) return e;
+            commit_pos_kernel<<<g, blk, 0, s>>>(b.gid_in, p.committed, pos, n);
+        } else {
+            commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
+        }
+    }
+    copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);
+    return cudaGetLastError();
+}
+
+}  // namespace gcctb

@@ -1,0 +1,286 @@
+// ycsb.cu -- YCSB workload on the device: table initialiser, primary-key index,
+// a1 batch generator, the workload policy the executor is instantiated with, and the
+// a3 access gather for the deterministic schemes.
+//
+// YCSB: 2^20*10 rows, 16 single-tuple accesses per transaction,
+// Zipfian keys (theta), write fraction W.  Row = 16 x u64 (128 B, one L2 line pair
+// of sectors; reading Z11).  Op semantics (Z11): out = fp(row) = sum_j rotl(r[j], j);
+// a write also sets r[f] = r[f]*0x9E3779B97F4A7C15 + ((gid<<4)|i) + 1 and r[15] += 1.
+#include "exec.cuh"
+
+namespace gcctb {
+
+struct YcsbWL {
+    static constexpr int MAXK = 16;
+    static constexpr int ROW_WORDS = 16;
+    using Params = YcsbParams;
+    struct Txn {
+        u32 gid;
+        u32 n;
+        u32 wmask;
+        u32 rec[MAXK];
+        uint8_t field[MAXK];
+        u64 key_hi, key_lo;
+    };
+    struct Ws {
+        u64 out[MAXK];
+        u64 nf[MAXK];
+        u64 n15[MAXK];
+    };
+
+    // Resolve every access up front: the read/write set is predetermined
+    // (PAPER.md:446).  Index lookups are binary searches in the sorted array
+    // (PAPER.md:344), run in lockstep over the K keys for memory-level parallelism.
+    static GC_DEV bool load(const ExecParams &p, const YcsbParams &y, u32 gid, Txn &t) {
+        t.gid = gid;
+        t.n = p.K;
+        t.wmask = 0;
+        const u64 base = (u64)gid * p.K;
+        if (p.acc_rec) {   // deterministic schemes: resolved during preprocessing (a3)
+#pragma unroll
+            for (int i = 0; i < MAXK; i++)
+                if (i < (int)p.K) {
+                    t.rec[i] = p.acc_rec[base + i];
+                    const uint8_t op = y.ops[base + i];
+                    t.field[i] = op & 0x0F;
+                    t.wmask |= (u32)(op >> 7) << i;
+                }
+            return true;
+        }
+        u64 key[MAXK];
+        const u64 *b[MAXK];
+#pragma unroll
+        for (int i = 0; i < MAXK; i++) {
+            if (i < (int)p.K) {
+                key[i] = y.keys[base + i];
+                const uint8_t op = y.ops[base + i];
+                t.field[i] = op & 0x0F;
+                t.wmask |= (u32)(op >> 7) << i;
+            } else {
+                key[i] = 0;
+            }
+            b[i] = y.idx_keys;
+        }
+        u64 n = y.idx_n;
+        while (n > 1) {
+            const u64 half = n >> 1;
+#pragma unroll
+            for (int i = 0; i < MAXK; i++)
+                if (i < (int)p.K) b[i] = (__ldg(b[i] + half) < key[i]) ? b[i] + half : b[i];
+            n -= half;
+        }
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < MAXK; i++)
+            if (i < (int)p.K) {
+                u64 pos = (u64)(b[i] - y.idx_keys);
+                u64 kv = __ldg(b[i]);
+                if (kv < key[i]) { pos++; kv = pos < y.idx_n ? __ldg(y.idx_keys + pos) : ~0ull; }
+                if (pos >= y.idx_n || kv != key[i]) ok = false;   // KeyNotFound
+                else t.rec[i] = (u32)__ldg(y.idx_rows + pos);
+            }
+        return ok;
+    }
+
+    static GC_DEV u64 *row(const YcsbParams &y, u32 rec) { return y.rows + (u64)rec * 16u; }
+
+    static GC_DEV void read_op(const YcsbParams &, const Txn &t, int i, const u64 *src, Ws &ws) {
+        u64 r[16];
+#pragma unroll
+        for (int j = 0; j < 8; j++) ld_cg_v2(src + 2 * j, r[2 * j], r[2 * j + 1]);
+        u64 fp = 0, rf = 0;
+        const unsigned f = t.field[i];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            fp += rotl64(r[j], j);
+            rf = (j == (int)f) ? r[j] : rf;
+        }
+        ws.out[i] = fp;
+        if ((t.wmask >> i) & 1) {
+            ws.nf[i] = rf * 0x9E3779B97F4A7C15ull + ((((u64)t.gid) << 4) | (u64)i) + 1ull;
+            ws.n15[i] = r[15] + 1ull;
+        }
+    }
+
+    static GC_DEV void install(const YcsbParams &, const Txn &t, int i, u64 *dst, const Ws &ws) {
+        st_cg(dst + t.field[i], ws.nf[i]);
+        st_cg(dst + 15, ws.n15[i]);
+    }
+
+    static GC_DEV void copy_row(const u64 *src, u64 *dst) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            u64 a, b;
+            ld_cg_v2(src + 2 * j, a, b);
+            st_cg_v2(dst + 2 * j, a, b);
+        }
+    }
+
+    static GC_DEV void emit(const ExecParams &p, const YcsbParams &, const Txn &t, const Ws &ws) {
+        if (!p.read_out) return;
+        const u64 base = (u64)t.gid * p.K;
+#pragma unroll
+        for (int i = 0; i < MAXK; i++)
+            if (i < (int)t.n) p.read_out[base + i] = ws.out[i];
+    }
+};
+
+// ---------------------------------------------------------------- executor launch
+template <int S>
+static cudaError_t launch_one(const ExecParams &p, const YcsbParams &y, int grid, int block,
+                              cudaStream_t s) {
+    exec_kernel<S, YcsbWL><<<grid, block, 0, s>>>(p, y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
+                             cudaStream_t s) {
+    switch (p.scheme) {
+        case CC_TPL_NW: return launch_one<CC_TPL_NW>(p, y, grid, block, s);
+        case CC_TPL_WD: return launch_one<CC_TPL_WD>(p, y, grid, block, s);
+        case CC_TO: return launch_one<CC_TO>(p, y, grid, block, s);
+        case CC_MVCC: return launch_one<CC_MVCC>(p, y, grid, block, s);
+        case CC_SILO: return launch_one<CC_SILO>(p, y, grid, block, s);
+        case CC_TICTOC: return launch_one<CC_TICTOC>(p, y, grid, block, s);
+        case CC_GPUTX: return launch_one<CC_GPUTX>(p, y, grid, block, s);
+        case CC_GACCO: return launch_one<CC_GACCO>(p, y, grid, block, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int S>
+static int occ_one(int block) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, exec_kernel<S, YcsbWL>, block, 0);
+    return nb;
+}
+
+int ycsb_exec_max_blocks_per_sm(int scheme, int block) {
+    switch (scheme) {
+        case CC_TPL_NW: return occ_one<CC_TPL_NW>(block);
+        case CC_TPL_WD: return occ_one<CC_TPL_WD>(block);
+        case CC_TO: return occ_one<CC_TO>(block);
+        case CC_MVCC: return occ_one<CC_MVCC>(block);
+        case CC_SILO: return occ_one<CC_SILO>(block);
+        case CC_TICTOC: return occ_one<CC_TICTOC>(block);
+        case CC_GPUTX: return occ_one<CC_GPUTX>(block);
+        case CC_GACCO: return occ_one<CC_GACCO>(block);
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------- a3 gather
+// One thread per transaction: resolve its accesses and emit the access-table sort
+// keys (rec << 27) | (gid << 6) | (i << 1) | is_write.
+__global__ void ycsb_gather_kernel(ExecParams p, YcsbParams y, uint32_t *acc_rec,
+                                   unsigned long long *keys_out) {
+    const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= p.n_txn) return;
+    YcsbWL::Txn t;
+    ExecParams q = p;
+    q.acc_rec = nullptr;
+    if (!YcsbWL::load(q, y, gid, t)) {
+        atomicCAS(&p.ctl->err, 0ull, (u64)CC_ERR_KEY_NOT_FOUND);
+        return;
+    }
+    const u64 base = (u64)gid * p.K;
+    for (u32 i = 0; i < p.K; i++) {
+        acc_rec[base + i] = t.rec[i];
+        keys_out[base + i] = ((u64)t.rec[i] << 27) | ((u64)gid << 6) | ((u64)i << 1) | ((t.wmask >> i) & 1u);
+    }
+}
+
+cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBufs &b,
+                               cudaStream_t s) {
+    const int blk = 256;
+    ycsb_gather_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(p, y, b.acc_rec, b.keys_in);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- table + index init
+// Row initialiser: the device copy of the seeded input generator (inputs/ycsb.py):
+// word j of row k = mix64(seed ^ (16k + j)) for j < 15, word 15 = 0.
+__global__ void ycsb_init_rows_kernel(u64 *rows, uint64_t first, uint64_t n, uint64_t seed) {
+    const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;   // word index
+    if (w >= n * 16) return;
+    const uint64_t k = first + w / 16, j = w % 16;
+    rows[w] = (j == 15) ? 0ull : mix64(seed ^ (16ull * k + j));
+}
+
+cudaError_t launch_ycsb_init_rows(u64 *rows, uint64_t first, uint64_t n, uint64_t seed,
+                                  cudaStream_t s) {
+    const uint64_t words = n * 16;
+    ycsb_init_rows_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(rows, first, n, seed);
+    return cudaGetLastError();
+}
+
+__global__ void identity_index_kernel(u64 *keys, u64 *rowids, uint64_t n) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { keys[i] = i; rowids[i] = i; }
+}
+
+cudaError_t launch_identity_index(u64 *keys, u64 *rowids, uint64_t n, cudaStream_t s) {
+    identity_index_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, rowids, n);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- a1 generator
+// One thread per transaction (readings Z12, Z13):
+//   op i: draw k = 0,1,..: u = rng(seed, gid, 1<<56 | i<<24 | k), rank = Zipf(u) by
+//   binary search in the threshold table, key = ((rank-1)*A) mod n, until distinct;
+//   sort keys ascending; write iff (rng(seed,gid,2<<56|i) >> 11) < floor(W*2^53);
+//   field = rng(seed,gid,3<<56|i) mod 15.
+__global__ void ycsb_gen_kernel(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
+                                uint64_t n, u64 wthr, uint64_t seed, const u64 *T,
+                                uint64_t A, Ctl *ctl) {
+    const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= n_txn) return;
+    u32 kk[16];
+    for (u32 i = 0; i < K; i++) {
+        for (u64 k = 0;; k++) {
+            if (k >= (1u << 24)) {
+                atomicCAS(&ctl->err, 0ull, (u64)CC_ERR_CONFIG);
+                return;
+            }
+            const u64 u = rng3(seed, gid, (1ull << 56) | ((u64)i << 24) | k);
+            // count = #{j : T[j] <= u}
+            u64 lo = 0, hi = n;
+            while (lo < hi) {
+                const u64 mid = lo + (hi - lo) / 2;
+                if (__ldg(T + mid) <= u) lo = mid + 1; else hi = mid;
+            }
+            if (lo > n - 1) lo = n - 1;
+            const u64 key = (lo * A) % n;   // (rank - 1) * A mod n
+            bool dup = false;
+            for (u32 j = 0; j < i; j++) dup |= (kk[j] == (u32)key);
+            if (!dup) { kk[i] = (u32)key; break; }
+        }
+    }
+    for (u32 i = 1; i < K; i++) {
+        const u32 v = kk[i];
+        int j = (int)i - 1;
+        while (j >= 0 && kk[j] > v) { kk[j + 1] = kk[j]; j--; }
+        kk[j + 1] = v;
+    }
+    const u64 base = (u64)gid * K;
+    for (u32 i = 0; i < K; i++) {
+        const u64 um = rng3(seed, gid, (2ull << 56) | i);
+        const u64 uf = rng3(seed, gid, (3ull << 56) | i);
+        uint8_t op = (uint8_t)(uf % 15u);
+        if ((um >> 11) < wthr) op |= 0x80u;
+        keys[base + i] = kk[i];
+        ops[base + i] = op;
+    }
+}
+
+cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
+                            uint64_t n_rows, double W, uint64_t seed, const u64 *T,
+                            uint64_t mult, Ctl *ctl, cudaStream_t s) {
+    const u64 wthr = (u64)(W * 9007199254740992.0);
+    const int blk = 128;
+    ycsb_gen_kernel<<<(n_txn + blk - 1) / blk, blk, 0, s>>>(keys, ops, n_txn, K, n_rows, wthr,
+                                                            seed, T, mult, ctl);
+    return cudaGetLastError();
+}
+
+}  // namespace gcctb

@@ -1,0 +1,175 @@
+"""-m gpu: parity of the CUDA path (through the C ABI) against the CPU oracle on YCSB.
+
+Bar: bit-exact.  For every scheme the GPU's read outputs and final
+table equal the oracle's serial replay of the committed set in the GPU-reported order;
+GPUTx and GaccO must also report ascending batch order with zero aborts."""
+import numpy as np
+import pytest
+
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc", "gputx", "gacco"]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def c1(torch_cuda, orc):
+    """BASELINE.json configs[0]: 1,024 rows, 1,024 txns x 4 ops, W=0.5, theta=0.8."""
+    from paper_2406_10158_b200.api import DB
+    db = DB(0)
+    db.load_ycsb(1024, 11)
+    S0 = db.read_table(0)
+    db.snapshot(True)
+    yield db, S0
+    db.close()
+
+
+def test_device_rows_equal_input_generator(c1):
+    db, S0 = c1
+    assert np.array_equal(S0, inputs.ycsb_rows(11, 1024))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_a1_generator_bitexact(c1, orc, seed):
+    db, _ = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, seed, T, A)
+    k, o = b.export_ycsb()
+    ek, eo = orc.ycsb_gen(seed, 1024, 1024, 4, 0.5, T, A)
+    assert np.array_equal(k, ek) and np.array_equal(o, eo)
+    b.free()
+
+
+CORNERS = [(0, 32), (5, 1), (0, 1), (5, 32), (2, 8)]
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("wd,bs", CORNERS)
+def test_c1_parity(c1, orc, scheme, wd, bs):
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    for seed in (5, 6):
+        b = db.gen_ycsb(1024, 4, 0.5, seed, T, A)
+        keys, ops = orc.ycsb_gen(seed, 1024, 1024, 4, 0.5, T, A)
+        db.snapshot(False)
+        res = db.submit(b, scheme, wd=wd, bs=bs)
+        st = db.sync()
+        assert st.commits == 1024
+        h = res.host()
+        assert int(h["restarts"].astype(np.int64).sum()) == st.aborts
+        orc.check_ycsb(scheme, S0, keys, ops, 4, h, db.read_table(0))
+        if scheme == "gputx":
+            assert st.max_rank == int(orc.gputx_ranks(keys, ops, 4, 1024).max())
+        b.free()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_immediate_retry_mode(c1, orc, scheme):
+    from paper_2406_10158_b200.gcctb import CC_FLAG_IMMEDIATE_RETRY
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 9, T, A)
+    keys, ops = orc.ycsb_gen(9, 1024, 1024, 4, 0.5, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=32, flags=CC_FLAG_IMMEDIATE_RETRY)
+    db.sync()
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(), db.read_table(0))
+    b.free()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_read_only_never_aborts(c1, orc, scheme):
+    """RO preset: no scheme aborts, state unchanged."""
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.99)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.0, 3, T, A)
+    keys, ops = orc.ycsb_gen(3, 1024, 1024, 4, 0.0, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=5, bs=32)
+    st = db.sync()
+    assert st.aborts == 0
+    h = res.host()
+    orc.check_ycsb(scheme, S0, keys, ops, 4, h, db.read_table(0))
+    assert np.array_equal(db.read_table(0), S0)
+    b.free()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_brute_force_tiny(c1, orc, scheme):
+    """<=7 txns x <=3 ops over <=5 rows, W=0.5: the GPU outcome is one of the n! serial
+    outcomes, and the reported order reproduces it."""
+    db, S0 = c1
+    rng = np.random.default_rng(1234 + len(scheme))
+    for it in range(40):
+        n = int(rng.integers(2, 8))
+        k = int(rng.integers(1, 4))
+        keys, ops = inputs.random_batch(int(rng.integers(1 << 30)), n, k, 1024, 0.5, hot=5)
+        b = db.import_ycsb(keys, ops, k)
+        db.snapshot(False)
+        res = db.submit(b, scheme, wd=int(rng.integers(0, 6)), bs=int(rng.integers(1, 5)))
+        db.sync()
+        h = res.host()
+        after = db.read_table(0)
+        orc.check_ycsb(scheme, S0, keys, ops, k, h, after)
+        outs = orc.ycsb_serial_outcomes(S0[:5].copy(), keys, ops, k, list(range(n)))
+        got = (after[:5].tobytes(), h["read_out"].reshape(n, k).tobytes())
+        assert got in outs
+        b.free()
+
+
+def test_key_not_found(c1):
+    from paper_2406_10158_b200.gcctb import CCError
+    db, _ = c1
+    b = db.import_ycsb(np.array([1, 5000], np.uint32), np.array([0, 0], np.uint8), 2)
+    db.submit(b, "silo")
+    with pytest.raises(CCError, match="KEY_NOT_FOUND"):
+        db.sync()
+    b.free()
+
+
+@pytest.fixture(scope="module")
+def c2(torch_cuda, orc):
+    """BASELINE.json configs[1]: 10,485,760-row table, 64K x 16 ops."""
+    from paper_2406_10158_b200.api import DB
+    n = 10 * (1 << 20)
+    db = DB(0)
+    db.load_ycsb(n, 5)
+    S0 = db.read_table(0)
+    assert np.array_equal(S0[:4096], inputs.ycsb_rows(5, 4096))
+    assert np.array_equal(S0[-4096:], inputs.ycsb_rows(5, 4096, n - 4096))
+    db.snapshot(True)
+    yield db, S0, n
+    db.close()
+
+
+@pytest.mark.parametrize("theta", [0.8, 0.99])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c2_full_size_parity(c2, orc, scheme, theta):
+    """Full-size parity in the bench launch configuration (wd=0, bs=32 default)."""
+    db, S0, n = c2
+    T = inputs.zipf_thresholds(n, theta)
+    A = inputs.scramble_mult(n)
+    B, K, W = 1 << 16, 16, 0.1
+    b = db.gen_ycsb(B, K, W, 77, T, A)
+    keys, ops = orc.ycsb_gen(77, n, B, K, W, T, A)
+    k2, o2 = b.export_ycsb()
+    assert np.array_equal(keys, k2) and np.array_equal(ops, o2)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=32)
+    st = db.sync()
+    assert st.commits == B
+    orc.check_ycsb(scheme, S0, keys, ops, K, res.host(), db.read_table(0))
+    b.free()

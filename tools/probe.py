@@ -1,0 +1,53 @@
+"""Quick perf probe (not the bench): C2-shaped YCSB, every scheme, a few thetas."""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+from paper_2406_10158_b200.api import DB  # noqa: E402
+from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING, SCHEMES  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", type=int, default=10 * (1 << 20))
+    ap.add_argument("--batch", type=int, default=1 << 16)
+    ap.add_argument("--K", type=int, default=16)
+    ap.add_argument("--W", type=float, default=0.1)
+    ap.add_argument("--thetas", default="0,0.6,0.8,0.99")
+    ap.add_argument("--schemes", default=",".join(SCHEMES))
+    ap.add_argument("--wd", type=int, default=0)
+    ap.add_argument("--bs", type=int, default=32)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    db = DB(0)
+    db.load_ycsb(a.rows, 1)
+    A = inputs.scramble_mult(a.rows)
+    out = []
+    for th in [float(x) for x in a.thetas.split(",")]:
+        T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
+        b = db.gen_ycsb(a.batch, a.K, a.W, 3, T, A)
+        for s in a.schemes.split(","):
+            db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20)
+            db.sync()
+            db.timing(reset=True)
+            for _ in range(a.reps):
+                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING, watchdog_s=20)
+            st = db.sync()
+            ms, n = db.timing(reset=True)
+            per = [m / n for m in ms]
+            row = dict(theta=th, scheme=s, txn_s=a.batch / (per[4] / 1e3), abort_rate=st.aborts / st.commits,
+                       ms_reset=per[0], ms_prep=per[1], ms_exec=per[2], ms_emit=per[3], ms_total=per[4])
+            out.append(row)
+            print(json.dumps(row), flush=True)
+        b.free()
+
+
+if __name__ == "__main__":
+    main()
