@@ -1,0 +1,394 @@
+"""bench.py -- committed txn/s + abort rate per CC scheme on YCSB (BASELINE.json
+metric; workload = configs[1]: 10,485,760-row table, batch 64K x 16 ops).
+
+One step = one pass of the whole hot path over one synthetic batch: a1 on-device batch
+generation, then for each of the 8 schemes a2 reset, a3 preprocessing (GPUTx/GaccO),
+a4-a6 execution with abort compaction, a7 result emission.  value = committed
+transactions of all schemes / step time (whole job, summed over ranks).
+
+YCSB does not shard: with N GPUs every rank runs an independent
+replica on its own batch ("replicas only", weak scaling); no data-path collective.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCHEMES = ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc", "gputx", "gacco"]
+METRIC = "committed txn/s + abort rate per CC scheme, YCSB & TPC-C, at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=10 * (1 << 20))
+    ap.add_argument("--batch", type=int, default=1 << 16)
+    ap.add_argument("--ops", type=int, default=16)
+    ap.add_argument("--theta", type=float, default=0.6)   # MC preset
+    ap.add_argument("--write-frac", type=float, default=0.1)
+    ap.add_argument("--wd", type=int, default=0)          # paper launch wd=0, bs=32
+    ap.add_argument("--bs", type=int, default=32)
+    ap.add_argument("--schemes", default=",".join(SCHEMES))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[1]) for s in self.samples if len(s) >= 9 and s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if len(s) >= 9 and s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) >= 9:
+                for n, v in zip(names, s[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def algorithmic_bytes(n_txn, K, n_writes, scheme):
+    """SURVEY.md §8(d) per-op bytes: read = 8 (CC word) + 128 (row) + 8 (out); a write
+    adds 16 (two updated row words) + 8 (word release); MVCC adds 144 per write
+    (history node); + 5 B per op of batch input (u32 key + u8 op)."""
+    reads = n_txn * K - n_writes
+    b = reads * 144 + n_writes * 168 + n_txn * K * 5
+    if scheme == "mvcc":
+        b += n_writes * 144
+    return b
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def load_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_replay_timed(args, seconds, max_batches=None):
+    """The oracle as it stands (oracle/: plain C serial executor), one host core.
+    Generates S0 (inputs) and batches with the oracle's own generator, then times only
+    the serial replay loop.  Returns (txn/s, txns replayed, seconds, sample string)."""
+    import numpy as np
+    import inputs
+    import oracle
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    S = inputs.ycsb_rows(1, args.rows)
+    T = inputs.zipf_thresholds(args.rows, args.theta)
+    A = inputs.scramble_mult(args.rows)
+    keys, ops = oracle.ycsb_gen(123, args.rows, args.batch, args.ops, args.write_frac, T, A)
+    order = np.arange(args.batch, dtype=np.uint32)
+    out = np.zeros(args.batch * args.ops, dtype=np.uint64)
+    L = oracle.lib()
+    done = 0
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        st = L.orc_ycsb_replay(oracle._ptr(S), args.rows, args.batch, args.ops, oracle._ptr(keys),
+                               oracle._ptr(ops), oracle._ptr(order), args.batch, oracle._ptr(out))
+        assert st == 0
+        done += args.batch
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (max_batches and n >= max_batches):
+            break
+    sample = (f"serial replay of {n} x {args.batch}-txn YCSB batches (K={args.ops}, theta={args.theta}, "
+              f"W={args.write_frac}) over the {args.rows}-row table, 1 core")
+    return done / el, done, el, sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    # each step: serial replay of one step's worth of transactions (8 schemes x batch),
+    # bounded so --steps K --warmup W finishes in minutes
+    import numpy as np  # noqa: F401
+    per_step = len(args.schemes.split(",")) * args.batch
+    tps, done, el, sample = oracle_replay_timed(args, seconds=min(args.cpu_seconds, 30.0))
+    ms_per_step = per_step / tps * 1e3
+    line = {
+        "metric": METRIC, "value": tps, "unit": "txn/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic", "impl": "reference",
+        "config": config_of(args, world),
+        "cpu_baseline": {"value": tps, "unit": "txn/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": tps, "unit": "txn/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, world):
+    return {"workload": "ycsb_configs1_10Mrows_64Kx16", "rows": args.rows, "batch": args.batch,
+            "ops_per_txn": args.ops, "theta": args.theta, "write_frac": args.write_frac,
+            "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs,
+            "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (1.34 GB table, 168 MB CC words)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    from paper_2406_10158_b200.api import DB, Result
+    from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    schemes = args.schemes.split(",")
+    db = DB(local)
+    db.load_ycsb(args.rows, 1 + rank)
+    T = torch.from_numpy(inputs.zipf_thresholds(args.rows, args.theta).view(np.int64)).to(dev)
+    A = inputs.scramble_mult(args.rows)
+    res = {s: Result.alloc(args.batch, args.ops, dev) for s in schemes}
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, timing=False):
+        b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
+        for s in schemes:
+            db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING if timing else 0,
+                      result=res[s], watchdog_s=60)
+        return b
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for i in range(args.warmup):
+        b = step(i)
+        db.sync()
+        b.free()
+    barrier()
+    # ---- timed region
+    clocks = Clocks(local)
+    clocks.start()
+    db.timing(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    batches = []
+    barrier()
+    e0.record(stream)
+    for i in range(args.steps):
+        batches.append(step(args.warmup + i, timing=True))
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    st = db.sync()
+    ms = e0.elapsed_time(e1)
+    phase_ms, n_sub = db.timing(reset=True)
+    # per-scheme stats from the last step (committed + aborts), checked complete
+    per = {}
+    last = batches[-1]
+    for s in schemes:
+        h = res[s].stats.cpu().numpy().view(np.uint64)
+        per[s] = {"commits": int(h[0]), "aborts": int(h[1]), "abort_rate": float(h[1]) / max(1, int(h[0]))}
+        assert int(h[0]) == args.batch, (s, int(h[0]))
+    keys, ops = last.export_ycsb()
+    n_writes = int(((ops & 0x80) != 0).sum())
+    for b in batches:
+        b.free()
+    # per-scheme exec timing (one extra timed pass per scheme on a fresh batch, untimed overall)
+    b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 999_999 + rank, T, A)
+    bk, bo = b.export_ycsb()
+    nw2 = int(((bo & 0x80) != 0).sum())
+    exec_ms_total, alg_bytes_total = 0.0, 0
+    for s in schemes:
+        db.timing(reset=True)
+        db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING, result=res[s], watchdog_s=60)
+        db.sync()
+        pm, _ = db.timing(reset=True)
+        per[s]["exec_ms"] = pm[2]
+        per[s]["submit_ms"] = pm[4]
+        per[s]["txn_s"] = args.batch / (pm[4] / 1e3)
+        ab = algorithmic_bytes(args.batch, args.ops, nw2, s)
+        per[s]["exec_GBps"] = ab / (pm[2] / 1e3) / 1e9
+        exec_ms_total += pm[2]
+        alg_bytes_total += ab
+    # ---- e2e through the public API with host buffers
+    e2e = run_e2e(args, db, bk, bo, schemes, res, dev, stream, barrier, world)
+    b.free()
+
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_commits = args.steps * args.batch * len(schemes) * world
+    value = total_commits / (ms_max / 1e3)
+    if rank == 0:
+        peaks = load_peaks()
+        peak = peaks["hbm_gbs"] if peaks else 6650.0
+        achieved = alg_bytes_total / (exec_ms_total / 1e3) / 1e9
+        tr = load_traffic()
+        traffic = None
+        if tr and tr.get("config") == config_key(args):
+            traffic = tr.get("dram_bytes_per_launch")
+        exec_share = phase_ms[2] / phase_ms[4] if phase_ms[4] else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "txn/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": config_of(args, world),
+            "abort_rate": sum(p["aborts"] for p in per.values()) / max(1, sum(p["commits"] for p in per.values())),
+            "per_scheme": per,
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step(schemes) * args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "exec_kernel (a4-a6), all schemes",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
+                         "exec_share_of_step": exec_share},
+        }
+        if not args.no_cpu_baseline and world >= 1:
+            tps, done, el, sample = oracle_replay_timed(args, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": tps, "unit": "txn/s", "cores": 1, "kind": "oracle",
+                                    "sample": sample}
+        print(json.dumps(line), flush=True)
+    db.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def config_key(args):
+    return f"ycsb rows={args.rows} batch={args.batch} K={args.ops} theta={args.theta} W={args.write_frac} wd={args.wd} bs={args.bs}"
+
+
+def launches_per_step(schemes):
+    """Kernel launches issued by libgcctb per step: 1 generator + per scheme: reset 2,
+    exec 1, finalize (non-deterministic: iota + CUB radix sort (counted 1) + commit_pos
+    + copy_out = 4, TicToc +2; deterministic: iota + commit_pos + copy_out = 3), plus
+    GaccO prep 6 (gather, sort, flags, scan, starts, positions) and GPUTx prep 13."""
+    n = 1
+    for s in schemes:
+        n += 3
+        if s in ("gputx", "gacco"):
+            n += 3 + (6 if s == "gacco" else 13)
+        else:
+            n += 4 + (2 if s == "tictoc" else 0)
+    return n
+
+
+def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world):
+    """Same metric through the public C-ABI with HOST buffers: every step imports the
+    batch from pinned host memory (cc_batch_import_ycsb, src_on_device=0), runs all
+    schemes, and reads each scheme's commit flags, commit positions and read outputs
+    back to pinned host memory."""
+    import torch
+    pk = torch.from_numpy(keys).pin_memory()
+    po = torch.from_numpy(ops).pin_memory()
+    outs = {s: (torch.empty(args.batch, dtype=torch.uint8).pin_memory(),
+                torch.empty(args.batch, dtype=torch.int32).pin_memory(),
+                torch.empty(args.batch * args.ops, dtype=torch.int64).pin_memory()) for s in schemes}
+    n_steps = max(2, min(args.steps, 5))
+
+    def one():
+        b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
+        for s in schemes:
+            db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60)
+            c, p_, r = outs[s]
+            c.copy_(res[s].committed, non_blocking=True)
+            p_.copy_(res[s].commit_pos, non_blocking=True)
+            r.copy_(res[s].read_out, non_blocking=True)
+        db.sync()
+        b.free()
+
+    one()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        one()
+    barrier()
+    el = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    h2d = keys.nbytes + ops.nbytes
+    d2h = len(schemes) * (args.batch * (1 + 4) + args.batch * args.ops * 8)
+    return {"value": n_steps * args.batch * len(schemes) * world / el, "unit": "txn/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_steps,
+            "note": "host wall clock around import(H2D) + submit x schemes + D2H of results"}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

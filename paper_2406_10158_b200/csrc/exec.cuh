@@ -588,6 +588,22 @@ GC_DEV bool ring_take(Th &th, u64 k, u32 &gid) {
     }
 }
 
+// Randomised, bounded exponential backoff after an abort.  Lanes of one warp run in
+// lockstep, so two transactions with crossed read/write sets can otherwise lock,
+// fail each other's validation and retry in perfect symmetry forever (an OCC livelock
+// the paper's immediate restart, is exposed to as well).  Delay is
+// uniform in [0, min(64 ns << restarts, 16 us)) from a hash of (gid, restarts).
+GC_DEV void abort_backoff(u32 gid, u32 restarts) {
+    const u32 sh = restarts < 8 ? restarts : 8;
+    const u32 cap = 64u << sh;
+    u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % cap);
+    while (d > 0) {
+        const u32 s = d < 1000u ? d : 1000u;
+        __nanosleep(s);
+        d -= s;
+    }
+}
+
 // ------------------------------------------------------------------ the kernel
 template <int S, class WL>
 __global__ void __launch_bounds__(1024) exec_kernel(ExecParams p, typename WL::Params y) {
@@ -624,8 +640,10 @@ __global__ void __launch_bounds__(1024) exec_kernel(ExecParams p, typename WL::P
                 break;
             }
             if (r == RES_FATAL) return;
-            p.restarts[gid] += 1;    // single owner of gid at a time; ring gives ordering
+            const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
+            p.restarts[gid] = nr;
             agg_add(&p.ctl->aborts);
+            abort_backoff(gid, nr);
             if (p.flags & CC_FLAG_IMMEDIATE_RETRY) continue;
             ring_push(th, gid);
             break;
