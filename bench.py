@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--write-frac", type=float, default=0.1)
     ap.add_argument("--wd", type=int, default=0)          # paper launch wd=0, bs=32
     ap.add_argument("--bs", type=int, default=32)
+    ap.add_argument("--lanes", type=int, default=1)       # 1 = thread per txn; 4/8/16 = tile mode
     ap.add_argument("--schemes", default=",".join(SCHEMES))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -186,7 +187,7 @@ def run_reference(args, rank, world):
 def config_of(args, world):
     return {"workload": "ycsb_configs1_10Mrows_64Kx16", "rows": args.rows, "batch": args.batch,
             "ops_per_txn": args.ops, "theta": args.theta, "write_frac": args.write_frac,
-            "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs,
+            "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs, "lanes_per_txn": args.lanes,
             "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (1.34 GB table, 168 MB CC words)"}
 
 
@@ -216,7 +217,7 @@ def run_ours(args, rank, world, local):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
         for s in schemes:
             db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING if timing else 0,
-                      result=res[s], watchdog_s=60)
+                      result=res[s], watchdog_s=60, lanes=args.lanes)
         return b
 
     def barrier():
@@ -264,7 +265,7 @@ def run_ours(args, rank, world, local):
     exec_ms_total, alg_bytes_total = 0.0, 0
     for s in schemes:
         db.timing(reset=True)
-        db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING, result=res[s], watchdog_s=60)
+        db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING, result=res[s], watchdog_s=60, lanes=args.lanes)
         db.sync()
         pm, _ = db.timing(reset=True)
         per[s]["exec_ms"] = pm[2]
@@ -320,7 +321,8 @@ def run_ours(args, rank, world, local):
 
 
 def config_key(args):
-    return f"ycsb rows={args.rows} batch={args.batch} K={args.ops} theta={args.theta} W={args.write_frac} wd={args.wd} bs={args.bs}"
+    return (f"ycsb rows={args.rows} batch={args.batch} K={args.ops} theta={args.theta} W={args.write_frac} "
+            f"wd={args.wd} bs={args.bs} lanes={args.lanes}")
 
 
 def launches_per_step(schemes):
@@ -354,7 +356,7 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world):
     def one():
         b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
         for s in schemes:
-            db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60)
+            db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes)
             c, p_, r = outs[s]
             c.copy_(res[s].committed, non_blocking=True)
             p_.copy_(res[s].commit_pos, non_blocking=True)

@@ -165,6 +165,10 @@ typedef struct {
     uint32_t bs;            /* block size: warps per block, 1..32 */
     uint32_t flags;         /* CC_FLAG_* */
     uint32_t grid;          /* blocks; 0 = resident capacity (persistent grid) */
+    uint32_t lanes_per_txn; /* 0/1: one lane per transaction (the paper's model, wd and bs
+                               apply); 4/8/16: a tile of that many lanes runs one
+                               transaction, lane i owning access i (must be >= ops per
+                               transaction; wd is ignored) */
     double watchdog_s;      /* device watchdog in seconds (0 = 30 s) */
 } cc_exec_desc;
 

@@ -469,6 +469,11 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (desc->wd > 5 || desc->bs < 1 || desc->bs > 32)
         return fail(db, CC_ERR_INVALID_ARG, "wd must be 0..5 and bs 1..32 (PAPER.md:480-484)");
     if (b->kind != KIND_YCSB) return fail(db, CC_ERR_UNSUPPORTED, "batch kind not supported");
+    {
+        const uint32_t L = desc->lanes_per_txn;
+        if (!(L <= 1 || L == 4 || L == 8 || L == 16) || (L > 1 && L < b->K))
+            return fail(db, CC_ERR_INVALID_ARG, "lanes_per_txn must be 0/1 or 4/8/16 and >= ops per txn");
+    }
     const int scheme = (int)desc->scheme;
     const bool det = scheme == CC_GPUTX || scheme == CC_GACCO;
     const uint64_t n_acc = (uint64_t)b->n_txn * b->K;
@@ -487,6 +492,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.K = b->K;
     p.wd = desc->wd;
     p.flags = desc->flags;
+    p.lanes = desc->lanes_per_txn <= 1 ? 1 : desc->lanes_per_txn;
     p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
     p.ctl = db->ctl;
     p.meta = db->meta;
@@ -537,7 +543,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     const int block = 32 * (int)desc->bs;
     int grid = (int)desc->grid;
     if (grid <= 0) {
-        const int per_sm = ycsb_exec_max_blocks_per_sm(scheme, block);
+        const int per_sm = ycsb_exec_max_blocks_per_sm(scheme, (int)p.lanes, block);
         if (per_sm <= 0) return fail(db, CC_ERR_CONFIG, "executor cannot launch %d threads/block", block);
         grid = per_sm * db->num_sms;
     }
@@ -589,7 +595,7 @@ cc_status cc_sync(cc_db db, cc_stats *out) {
     if (out) *out = s;
     Ctl c;
     CUDA_TRY(db, cudaMemcpy(&c, db->ctl, sizeof c, cudaMemcpyDeviceToHost));
-    const u64 e = c.err ? c.err : w[3];
+    const u64 e = c.err.v ? c.err.v : w[3];
     if (e) {
         static const char *names[] = {"ok", "invalid arg", "config", "oom", "cuda", "nccl",
                                       "key not found", "timestamp overflow", "version exhausted",

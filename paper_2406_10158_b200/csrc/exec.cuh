@@ -1,20 +1,25 @@
 // exec.cuh -- the persistent transaction executor and the
 // eight CC schemes, generic over a workload policy WL.
 //
-// Execution model (B200 design):
-//  * one persistent grid at resident capacity; every working lane (2^wd per warp,
-//    PAPER.md:480) claims transactions in increasing id from a device ticket, so
-//    every transaction anyone waits on is already running on a resident lane (H1);
-//  * an aborted attempt releases its CC state, bumps restarts[gid] and appends gid to
-//    a device retry ring with a warp-aggregated atomic (a6), from which lanes claim
-//    again after the fresh ids are exhausted; CC_FLAG_IMMEDIATE_RETRY restores the
-//    paper's "the thread immediately restarts";
-//  * each committing attempt emits its serialization-order key.
+// Two execution modes share the queue and the control-word protocols:
+//  * thread mode (lanes = 1): one lane per transaction, 2^wd working lanes per warp,
+//    bs warps per block -- the paper's launch model;
+//  * tile mode (lanes = G in {4,8,16,32}): a tile of G lanes runs one transaction,
+//    lane i owns access i.  Index lookups, CC words and rows of all accesses are issued
+//    in parallel; commit / abort / wait decisions are tile ballots (vote.any/all), the
+//    warp-level structure the north star asks for.  Same protocols, same order keys.
 //
-// WL must provide: MAXK, Txn {gid, n, wmask, rec[]}, Ws, load(), row(), read_op(),
-// install(), copy_row(), emit(), ROW_WORDS.
+// Queue (a6): lanes (or tile leaders) claim fresh ids in increasing order from a
+// device ticket.  An aborted attempt releases its CC state, bumps restarts[gid],
+// backs off, and -- while fresh ids remain -- appends gid to a bounded MPMC retry
+// ring (warp-aggregated append) and claims new work; once fresh ids are exhausted the
+// worker re-runs its own transaction.  Workers take retry-ring entries
+// before fresh ids and exit when both are empty, so no lane ever polls for work that
+// does not exist.  Every transaction a worker waits on has a smaller id or is held by
+// a running worker, so nothing waits on an unscheduled block.
 #pragma once
 #include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -23,29 +28,31 @@ namespace gcctb {
 namespace cg = cooperative_groups;
 
 enum { RES_OK = 0, RES_ABORT = 1, RES_FATAL = 2 };
+constexpr u32 NO_TXN = 0xFFFFFFFFu;
 
 // ------------------------------------------------------------------ thread context
 struct Th {
     u64 deadline;
     const ExecParams *p;
+    u32 polls;
 };
 
-GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err, 0ull, code); }
+GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err.v, 0ull, code); }
 
 GC_DEV bool dead(Th &th) {
-    if (ld_relaxed(&th.p->ctl->err) != 0) return true;
     if (globaltimer_ns() > th.deadline) {
         set_err(th.p->ctl, CC_ERR_WATCHDOG);
         return true;
     }
+    if ((++th.polls & 15u) == 0 && ld_relaxed(&th.p->ctl->err.v) != 0) return true;
     return false;
 }
 
 struct Spin {
-    unsigned ns = 20;
+    unsigned ns = 16;
     GC_DEV bool wait(Th &th) {   // false -> give up (error / watchdog)
         __nanosleep(ns);
-        ns = ns < 320 ? ns + ns / 2 + 8 : 320;
+        ns = ns < 256 ? ns * 2 : 256;
         return !dead(th);
     }
 };
@@ -57,535 +64,6 @@ GC_DEV u64 agg_fetch_add(u64 *ctr) {
     if (g.thread_rank() == 0) base = atomicAdd(ctr, (u64)g.size());
     base = g.shfl(base, 0);
     return base + g.thread_rank();
-}
-GC_DEV void agg_add(u64 *ctr) {
-    cg::coalesced_group g = cg::coalesced_threads();
-    if (g.thread_rank() == 0) atom_add_acqrel(ctr, (u64)g.size());
-}
-
-// ------------------------------------------------------------------ 2PL (Table II)
-// word = [62] shared | [61:31] holder count | [30:0] holder (wait-die: min age of the
-// holders, Z7; age = gid + 1).  0 = free.
-constexpr u64 TPL_S = 1ull << 62;
-constexpr u64 M31 = 0x7FFFFFFFull;
-GC_DEV u32 tpl_cnt(u64 v) { return (u32)((v >> 31) & M31); }
-GC_DEV u32 tpl_holder(u64 v) { return (u32)(v & M31); }
-GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
-    return (s ? TPL_S : 0ull) | ((cnt & M31) << 31) | (holder & M31);
-}
-
-template <bool WD>
-GC_DEV int tpl_acquire(u64 *w, bool ex, u32 age, Th &th) {
-    u64 v = ld_relaxed(w);
-    Spin sp;
-    for (;;) {
-        u64 nv;
-        bool conflict;
-        if (ex) {
-            conflict = (v != 0);
-            nv = tpl_make(false, 1, age);
-        } else {
-            conflict = (v != 0) && !(v & TPL_S);
-            nv = (v == 0) ? tpl_make(true, 1, age)
-                          : tpl_make(true, tpl_cnt(v) + 1, min(age, tpl_holder(v)));
-        }
-        if (conflict) {
-            // no-wait: abort at once (PAPER.md:176).  wait-die: an older requester
-            // (smaller age) waits, a younger one dies (PAPER.md:176, SPEC.md:254).
-            if (!WD || !(age < tpl_holder(v))) return RES_ABORT;
-            if (!sp.wait(th)) return RES_FATAL;
-            v = ld_relaxed(w);
-            continue;
-        }
-        u64 old = cas_acqrel(w, v, nv);
-        if (old == v) return RES_OK;
-        v = old;
-    }
-}
-
-GC_DEV void tpl_release(u64 *w, bool ex) {
-    if (ex) {
-        st_release(w, 0ull);
-        return;
-    }
-    u64 v = ld_relaxed(w);
-    for (;;) {
-        u64 nv = (tpl_cnt(v) <= 1) ? 0ull : v - (1ull << 31);
-        u64 old = cas_acqrel(w, v, nv);
-        if (old == v) return;
-        v = old;
-    }
-}
-
-template <bool WD, class WL>
-GC_DEV int run_tpl(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    const u32 age = t.gid + 1;
-    int i = 0, r = RES_OK;
-    for (; i < (int)t.n; i++) {
-        const bool ex = (t.wmask >> i) & 1;
-        r = tpl_acquire<WD>(&p.meta[t.rec[i]], ex, age, th);
-        if (r != RES_OK) break;
-        WL::read_op(y, t, i, WL::row(y, t.rec[i]), ws);  // row is stable under the lock
-    }
-    if (r != RES_OK) {
-        for (int j = 0; j < i; j++) tpl_release(&p.meta[t.rec[j]], (t.wmask >> j) & 1);
-        return r;
-    }
-    // lock point: every lock held, none released -> ticket is a valid serial order (strict 2PL)
-    const u64 ticket = agg_fetch_add(&p.ctl->ticket);
-    for (int j = 0; j < (int)t.n; j++)
-        if ((t.wmask >> j) & 1) WL::install(y, t, j, WL::row(y, t.rec[j]), ws);
-    for (int j = 0; j < (int)t.n; j++) tpl_release(&p.meta[t.rec[j]], (t.wmask >> j) & 1);
-    t.key_hi = 0;
-    t.key_lo = ticket;
-    return RES_OK;
-}
-
-// ------------------------------------------------------------------ TO (Table II)
-// word = [62] pending (uncommitted write) | [61:31] RTS | [30:0] WTS.
-// While pending, WTS holds the pending writer's ts (the writer keeps the committed
-// word to restore on abort).  Reading rules follow PAPER.md:188 with reading Z4.
-constexpr u64 TO_P = 1ull << 62;
-GC_DEV u64 to_rts(u64 v) { return (v >> 31) & M31; }
-GC_DEV u64 to_wts(u64 v) { return v & M31; }
-GC_DEV u64 to_make(bool pend, u64 rts, u64 wts) {
-    return (pend ? TO_P : 0ull) | ((rts & M31) << 31) | (wts & M31);
-}
-
-GC_DEV bool draw_ts(Th &th, u64 &ts) {
-    ts = agg_fetch_add(&th.p->ctl->ts) + 1;   // a fresh timestamp per attempt
-    if (ts > M31) {                            // 31-bit field
-        set_err(th.p->ctl, CC_ERR_TS_OVERFLOW);
-        return false;
-    }
-    return true;
-}
-
-template <class WL>
-GC_DEV int run_to(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    u64 ts;
-    if (!draw_ts(th, ts)) return RES_FATAL;
-    u64 saved[WL::MAXK];
-    u32 pend = 0;
-    int r = RES_OK;
-    for (int i = 0; i < (int)t.n && r == RES_OK; i++) {
-        u64 *w = &p.meta[t.rec[i]];
-        const u64 *row = WL::row(y, t.rec[i]);
-        Spin sp;
-        if ((t.wmask >> i) & 1) {
-            // write (read-modify-write): ts must be newer than RTS and WTS
-            u64 v = ld_acquire(w);
-            for (;;) {
-                if (v & TO_P) {
-                    if (to_wts(v) < ts) {   // older pending writer: wait for it (Z4)
-                        if (!sp.wait(th)) { r = RES_FATAL; break; }
-                        v = ld_acquire(w);
-                        continue;
-                    }
-                    r = RES_ABORT;
-                    break;
-                }
-                if (ts < to_rts(v) || ts < to_wts(v)) { r = RES_ABORT; break; }
-                u64 old = cas_acqrel(w, v, to_make(true, to_rts(v), ts));
-                if (old == v) break;
-                v = old;
-            }
-            if (r != RES_OK) break;
-            saved[i] = v;
-            pend |= 1u << i;
-            WL::read_op(y, t, i, row, ws);     // stable: we own the pending bit
-        } else {
-            // read: ts must be newer than WTS; wait on an older pending writer; then read
-            // the row between two loads of the word and raise RTS with a CAS
-            for (;;) {
-                u64 v = ld_acquire(w);
-                if (ts < to_wts(v)) { r = RES_ABORT; break; }
-                if (v & TO_P) {
-                    if (!sp.wait(th)) { r = RES_FATAL; break; }
-                    continue;
-                }
-                WL::read_op(y, t, i, row, ws);
-                fence_acqrel();
-                if (to_rts(v) >= ts) {
-                    if (ld_relaxed(w) == v) break;
-                    continue;
-                }
-                if (cas_acqrel(w, v, to_make(false, ts, to_wts(v))) == v) break;
-            }
-        }
-    }
-    if (r != RES_OK) {
-        for (int j = 0; j < (int)t.n; j++)
-            if ((pend >> j) & 1) st_release(&p.meta[t.rec[j]], saved[j]);
-        return r;
-    }
-    for (int j = 0; j < (int)t.n; j++)
-        if ((pend >> j) & 1) {
-            WL::install(y, t, j, WL::row(y, t.rec[j]), ws);
-            st_release(&p.meta[t.rec[j]], to_make(false, ts, ts));
-        }
-    t.key_hi = 0;
-    t.key_lo = ts;
-    return RES_OK;
-}
-
-// ------------------------------------------------------------------ MVCC (Table II)
-// meta[2r]   lo = TO word (pending | RTS | WTS); while pending WTS = pending writer ts
-// meta[2r+1] hi = version pointer word: [63:32] begin ts of the in-place head version,
-//                 [31:0] arena index of the previous version (NONE = 0xFFFFFFFF).
-// History nodes (arena, one per write op of the batch):
-//   word0 = (begin << 32) | prev, word1 = 0, words 2.. = row content (immutable once
-//   published).  Writes are buffered and installed at commit (Z6).
-constexpr u64 VNONE = 0xFFFFFFFFull;
-
-template <class WL>
-GC_DEV int run_mvcc(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    u64 ts;
-    if (!draw_ts(th, ts)) return RES_FATAL;
-    u64 saved_wts[WL::MAXK];
-    u32 pend = 0;
-    int r = RES_OK;
-    for (int i = 0; i < (int)t.n && r == RES_OK; i++) {
-        u64 *lo = &p.meta[2ull * t.rec[i]];
-        u64 *hi = lo + 1;
-        const u64 *row = WL::row(y, t.rec[i]);
-        Spin sp;
-        if ((t.wmask >> i) & 1) {
-            // writes append only at the head: ts > head WTS and ts >= RTS (Z6)
-            u64 v = ld_acquire(lo);
-            for (;;) {
-                if (v & TO_P) {
-                    if (to_wts(v) < ts) {
-                        if (!sp.wait(th)) { r = RES_FATAL; break; }
-                        v = ld_acquire(lo);
-                        continue;
-                    }
-                    r = RES_ABORT;
-                    break;
-                }
-                if (ts < to_rts(v) || ts < to_wts(v)) { r = RES_ABORT; break; }
-                u64 old = cas_acqrel(lo, v, to_make(true, to_rts(v), ts));
-                if (old == v) break;
-                v = old;
-            }
-            if (r != RES_OK) break;
-            saved_wts[i] = to_wts(v);
-            pend |= 1u << i;
-            WL::read_op(y, t, i, row, ws);
-        } else {
-            // read the version whose interval holds ts; never aborts
-            for (;;) {
-                u64 v = ld_acquire(lo);
-                if ((v & TO_P) && to_wts(v) < ts) {   // older pending writer: its version is ours
-                    if (!sp.wait(th)) { r = RES_FATAL; break; }
-                    continue;
-                }
-                u64 h = ld_acquire(hi);
-                if ((h >> 32) <= ts) {   // head visible: read in place, validate, raise RTS
-                    WL::read_op(y, t, i, row, ws);
-                    fence_acqrel();
-                    if (ld_relaxed(hi) != h) continue;
-                    if (to_rts(v) >= ts) {
-                        if (ld_relaxed(lo) == v) break;
-                        continue;
-                    }
-                    u64 nv = (v & ~(M31 << 31)) | ((ts & M31) << 31);
-                    if (cas_acqrel(lo, v, nv) == v) break;
-                    continue;
-                }
-                // walk the history chain for the newest version with begin <= ts
-                u64 idx = h & VNONE;
-                bool found = false;
-                while (idx != VNONE) {
-                    const u64 *node = p.arena + idx * (2 + WL::ROW_WORDS);
-                    u64 h0 = ld_cg(node);
-                    if ((h0 >> 32) <= ts) {
-                        WL::read_op(y, t, i, node + 2, ws);
-                        found = true;
-                        break;
-                    }
-                    idx = h0 & VNONE;
-                }
-                if (!found) {
-                    set_err(p.ctl, CC_ERR_VERSION_EXHAUSTED);
-                    r = RES_FATAL;
-                }
-                break;
-            }
-        }
-    }
-    if (r != RES_OK) {
-        for (int j = 0; j < (int)t.n; j++)
-            if ((pend >> j) & 1) {   // restore the committed word, keeping raised RTS
-                u64 *lo = &p.meta[2ull * t.rec[j]];
-                u64 v = ld_relaxed(lo);
-                for (;;) {
-                    u64 old = cas_acqrel(lo, v, to_make(false, to_rts(v), saved_wts[j]));
-                    if (old == v) break;
-                    v = old;
-                }
-            }
-        return r;
-    }
-    for (int j = 0; j < (int)t.n; j++)
-        if ((pend >> j) & 1) {
-            u64 *lo = &p.meta[2ull * t.rec[j]];
-            u64 *hi = lo + 1;
-            u64 *row = WL::row(y, t.rec[j]);
-            const u64 nidx = (u64)t.gid * p.K + j;
-            u64 *node = p.arena + nidx * (2 + WL::ROW_WORDS);
-            const u64 h = ld_relaxed(hi);
-            st_cg(node, ((h >> 32) << 32) | (h & VNONE));   // old head -> history node
-            WL::copy_row(row, node + 2);
-            fence_acqrel();
-            st_release(hi, (ts << 32) | nidx);                // publish, then install
-            fence_acqrel();
-            WL::install(y, t, j, row, ws);
-            st_release(lo, to_make(false, ts, ts));
-        }
-    t.key_hi = 0;
-    t.key_lo = ts;
-    return RES_OK;
-}
-
-// ------------------------------------------------------------------ Silo (Table II)
-// word = [63] lock | [62:0] TID.  Read phase snapshots (word, row, word); commit locks
-// the write set no-wait, draws the serialization-point ticket,
-// validates the read set, installs with TID = 1 + max observed (epoch dropped,
-// PAPER.md:416; Z8).
-constexpr u64 LOCKB = 1ull << 63;
-
-template <class WL>
-GC_DEV bool occ_read_phase(Th &th, typename WL::Txn &t, typename WL::Ws &ws,
-                           const typename WL::Params &y, u64 *obs) {
-    const ExecParams &p = *th.p;
-    for (int i = 0; i < (int)t.n; i++) {
-        u64 *w = &p.meta[t.rec[i]];
-        const u64 *row = WL::row(y, t.rec[i]);
-        Spin sp;
-        for (;;) {
-            u64 v1 = ld_acquire(w);
-            if (v1 & LOCKB) {   // a committer holds it: wait (Z10)
-                if (!sp.wait(th)) return false;
-                continue;
-            }
-            WL::read_op(y, t, i, row, ws);
-            fence_acqrel();
-            if (ld_relaxed(w) == v1) {
-                obs[i] = v1;
-                break;
-            }
-        }
-    }
-    return true;
-}
-
-template <class WL>
-GC_DEV int occ_lock_writes(Th &th, typename WL::Txn &t, u64 *pre, u32 &locked) {
-    const ExecParams &p = *th.p;
-    locked = 0;
-    for (int i = 0; i < (int)t.n; i++) {
-        if (!((t.wmask >> i) & 1)) continue;
-        u64 *w = &p.meta[t.rec[i]];
-        u64 v = ld_relaxed(w);
-        for (;;) {
-            if (v & LOCKB) return RES_ABORT;   // no-wait in the write phase
-            u64 old = cas_acqrel(w, v, v | LOCKB);
-            if (old == v) break;
-            v = old;
-        }
-        pre[i] = v;
-        locked |= 1u << i;
-    }
-    return RES_OK;
-}
-
-template <class WL>
-GC_DEV void occ_unlock(const ExecParams &p, typename WL::Txn &t, const u64 *pre, u32 locked) {
-    for (int j = 0; j < (int)t.n; j++)
-        if ((locked >> j) & 1) st_release(&p.meta[t.rec[j]], pre[j]);
-}
-
-template <class WL>
-GC_DEV int run_silo(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    u64 obs[WL::MAXK], pre[WL::MAXK];
-    if (!occ_read_phase<WL>(th, t, ws, y, obs)) return RES_FATAL;
-    u32 locked;
-    if (occ_lock_writes<WL>(th, t, pre, locked) != RES_OK) {
-        occ_unlock<WL>(p, t, pre, locked);
-        return RES_ABORT;
-    }
-    const u64 ticket = agg_fetch_add(&p.ctl->ticket);   // serialization point
-    fence_acqrel();
-    u64 tid = 0;
-    for (int i = 0; i < (int)t.n; i++) {
-        const bool wr = (t.wmask >> i) & 1;
-        const u64 cur = wr ? pre[i] : ld_acquire(&p.meta[t.rec[i]]);
-        if (cur != obs[i]) {   // TID changed, or locked by another transaction
-            occ_unlock<WL>(p, t, pre, locked);
-            return RES_ABORT;
-        }
-        tid = max(tid, obs[i]);
-    }
-    tid = (tid + 1) & ~LOCKB;
-    for (int j = 0; j < (int)t.n; j++)
-        if ((t.wmask >> j) & 1) {
-            WL::install(y, t, j, WL::row(y, t.rec[j]), ws);
-            st_release(&p.meta[t.rec[j]], tid);
-        }
-    t.key_hi = 0;
-    t.key_lo = ticket;
-    return RES_OK;
-}
-
-// ------------------------------------------------------------------ TicToc (Table II)
-// word = [63] lock | [62:48] delta | [47:0] WTS, RTS = WTS + delta.
-constexpr u64 M48 = (1ull << 48) - 1;
-constexpr u64 DMAX = 0x7FFFull;
-GC_DEV u64 tt_wts(u64 v) { return v & M48; }
-GC_DEV u64 tt_rts(u64 v) { return (v & M48) + ((v >> 48) & DMAX); }
-
-template <class WL>
-GC_DEV int run_tictoc(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    u64 obs[WL::MAXK], pre[WL::MAXK];
-    if (!occ_read_phase<WL>(th, t, ws, y, obs)) return RES_FATAL;
-    u32 locked;
-    if (occ_lock_writes<WL>(th, t, pre, locked) != RES_OK) {
-        occ_unlock<WL>(p, t, pre, locked);
-        return RES_ABORT;
-    }
-    // commit_ts = max(max over writes of RTS+1, max over reads of WTS)
-    u64 cts = 0;
-    for (int i = 0; i < (int)t.n; i++) {
-        if ((t.wmask >> i) & 1) cts = max(cts, tt_rts(pre[i]) + 1);
-        cts = max(cts, tt_wts(obs[i]));
-    }
-    for (int i = 0; i < (int)t.n; i++) {
-        if ((t.wmask >> i) & 1) {
-            if (tt_wts(pre[i]) != tt_wts(obs[i])) {
-                occ_unlock<WL>(p, t, pre, locked);
-                return RES_ABORT;
-            }
-            continue;
-        }
-        if (tt_rts(obs[i]) >= cts) continue;   // version valid through cts already
-        u64 *w = &p.meta[t.rec[i]];
-        u64 v = ld_acquire(w);
-        for (;;) {
-            if (tt_wts(v) != tt_wts(obs[i]) || (v & LOCKB)) {
-                occ_unlock<WL>(p, t, pre, locked);
-                return RES_ABORT;
-            }
-            if (tt_rts(v) >= cts) break;
-            u64 nw = tt_wts(v);
-            if (cts - nw > DMAX) nw = cts - DMAX;   // delta overflow: shift WTS up (Z9)
-            u64 old = cas_acqrel(w, v, ((cts - nw) << 48) | nw);
-            if (old == v) break;
-            v = old;
-        }
-    }
-    const u64 ticket = agg_fetch_add(&p.ctl->ticket);   // after validation, before install
-    for (int j = 0; j < (int)t.n; j++)
-        if ((t.wmask >> j) & 1) {
-            WL::install(y, t, j, WL::row(y, t.rec[j]), ws);
-            st_release(&p.meta[t.rec[j]], cts & M48);
-        }
-    t.key_hi = cts;
-    t.key_lo = ticket;
-    return RES_OK;
-}
-
-// ------------------------------------------------------------------ GaccO
-// Every access waits until the item's cursor reaches its preprocessed queue position,
-// performs the access, then advances the cursor (release after the op, Z3).
-template <class WL>
-GC_DEV int run_gacco(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    const u64 base = (u64)t.gid * p.K;
-    for (int i = 0; i < (int)t.n; i++) {
-        const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
-        u32 *cur = &p.cursor[seg];
-        Spin sp;
-        while (ld_acquire32(cur) != pos)
-            if (!sp.wait(th)) return RES_FATAL;
-        u64 *row = WL::row(y, t.rec[i]);
-        WL::read_op(y, t, i, row, ws);
-        if ((t.wmask >> i) & 1) WL::install(y, t, i, row, ws);
-        st_release32(cur, pos + 1);
-    }
-    t.key_hi = 0;
-    t.key_lo = t.gid;
-    return RES_OK;
-}
-
-// ------------------------------------------------------------------ GPUTx
-// K-set k runs once every transaction of K-set k-1 has completed; inside a K-set there
-// is no concurrency control.
-template <class WL>
-GC_DEV int run_gputx(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    const ExecParams &p = *th.p;
-    const u32 k = p.rank_of[t.gid];
-    if (k > 0) {
-        Spin sp;
-        while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
-            if (!sp.wait(th)) return RES_FATAL;
-    }
-    for (int i = 0; i < (int)t.n; i++) {
-        u64 *row = WL::row(y, t.rec[i]);
-        WL::read_op(y, t, i, row, ws);
-        if ((t.wmask >> i) & 1) WL::install(y, t, i, row, ws);
-    }
-    atom_add_release32(&p.rank_done[k], 1u);
-    t.key_hi = 0;
-    t.key_lo = t.gid;
-    return RES_OK;
-}
-
-template <int S, class WL>
-GC_DEV int run_scheme(Th &th, typename WL::Txn &t, typename WL::Ws &ws, const typename WL::Params &y) {
-    if constexpr (S == CC_TPL_NW) return run_tpl<false, WL>(th, t, ws, y);
-    else if constexpr (S == CC_TPL_WD) return run_tpl<true, WL>(th, t, ws, y);
-    else if constexpr (S == CC_TO) return run_to<WL>(th, t, ws, y);
-    else if constexpr (S == CC_MVCC) return run_mvcc<WL>(th, t, ws, y);
-    else if constexpr (S == CC_SILO) return run_silo<WL>(th, t, ws, y);
-    else if constexpr (S == CC_TICTOC) return run_tictoc<WL>(th, t, ws, y);
-    else if constexpr (S == CC_GACCO) return run_gacco<WL>(th, t, ws, y);
-    else return run_gputx<WL>(th, t, ws, y);
-}
-
-// ------------------------------------------------------------------ retry ring (a6)
-// Bounded MPMC ring of (seq << 32 | gid) slots; slot k of the retry sequence lives at
-// ring[k & (cap-1)], its consumer clears it after reading.
-GC_DEV void ring_push(Th &th, u32 gid) {
-    const ExecParams &p = *th.p;
-    const u64 r = agg_fetch_add(&p.ctl->tail);
-    u64 *slot = p.ring + (r & (p.ring_cap - 1));
-    Spin sp;
-    while (ld_relaxed(slot) != 0)   // previous lap not consumed yet
-        if (!sp.wait(th)) return;
-    st_release(slot, (((r + 1) & 0xFFFFFFFFull) << 32) | gid);
-}
-
-GC_DEV bool ring_take(Th &th, u64 k, u32 &gid) {
-    const ExecParams &p = *th.p;
-    u64 *slot = p.ring + (k & (p.ring_cap - 1));
-    const u64 want = (k + 1) & 0xFFFFFFFFull;
-    Spin sp;
-    for (;;) {
-        const u64 v = ld_acquire(slot);
-        if ((v >> 32) == want) {
-            gid = (u32)v;
-            st_relaxed(slot, 0ull);
-            return true;
-        }
-        if (ld_acquire(&p.ctl->done) >= p.n_txn) return false;
-        if (!sp.wait(th)) return false;
-    }
 }
 
 // Randomised, bounded exponential backoff after an abort.  Lanes of one warp run in
@@ -604,49 +82,692 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
     }
 }
 
-// ------------------------------------------------------------------ the kernel
+// ------------------------------------------------------------------ queue (a6)
+// Retry ring: bounded MPMC of (seq << 32 | gid) slots; slot r of the retry sequence
+// lives at ring[r & (cap-1)]; its consumer clears it after reading.
+GC_DEV void ring_push_one(Th &th, u64 r, u32 gid) {
+    const ExecParams &p = *th.p;
+    u64 *slot = p.ring + (r & (p.ring_cap - 1));
+    Spin sp;
+    while (ld_relaxed(slot) != 0)   // previous lap not consumed yet
+        if (!sp.wait(th)) return;
+    st_release(slot, (((r + 1) & 0xFFFFFFFFull) << 32) | gid);
+}
+
+// Claim work for one worker: the oldest retry-ring entry, else a fresh id, else NO_TXN.
+template <int S>
+GC_DEV u32 claim_work(Th &th, bool &fresh_exhausted) {
+    const ExecParams &p = *th.p;
+    Ctl *c = p.ctl;
+    constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
+    if (!DET) {
+        for (;;) {
+            const u64 r = ld_relaxed(&c->rhead.v);
+            const u64 t = ld_acquire(&c->tail.v);
+            if (r >= t) break;
+            if (atomicCAS(&c->rhead.v, r, r + 1) != r) continue;
+            u64 *slot = p.ring + (r & (p.ring_cap - 1));
+            const u64 want = (r + 1) & 0xFFFFFFFFull;
+            Spin sp;
+            for (;;) {
+                const u64 v = ld_acquire(slot);
+                if ((v >> 32) == want) {
+                    st_relaxed(slot, 0ull);
+                    return (u32)v;
+                }
+                if (!sp.wait(th)) return NO_TXN;
+            }
+        }
+    }
+    if (!fresh_exhausted) {
+        const u64 s = atomicAdd(&c->head.v, 1ull);
+        if (s < p.n_txn) return (S == CC_GPUTX) ? p.rank_order[s] : (u32)s;
+        fresh_exhausted = true;
+    }
+    return NO_TXN;
+}
+
+GC_DEV bool fresh_left(const ExecParams &p) { return ld_relaxed(&p.ctl->head.v) < p.n_txn; }
+
+// ------------------------------------------------------------------ 2PL (Table II)
+// word = [62] shared | [61:31] holder count | [30:0] holder (wait-die: min age of the
+// holders, Z7; age = gid + 1).  Free <=> count == 0 (shared releases are a single
+// atomic subtract and may leave stale shared/holder bits behind).
+constexpr u64 TPL_S = 1ull << 62;
+constexpr u64 M31 = 0x7FFFFFFFull;
+constexpr u64 TPL_ONE = 1ull << 31;
+GC_DEV u32 tpl_cnt(u64 v) { return (u32)((v >> 31) & M31); }
+GC_DEV u32 tpl_holder(u64 v) { return (u32)(v & M31); }
+GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
+    return (s ? TPL_S : 0ull) | ((cnt & M31) << 31) | (holder & M31);
+}
+
+// One acquisition step.  Returns 0 granted, 1 wait (wait-die older requester, or the
+// CAS lost a race), 2 die (conflict under no-wait, or younger requester).
+template <bool WD>
+GC_DEV int tpl_try(u64 *w, bool ex, u32 age) {
+    u64 v = ld_relaxed(w);
+    for (int k = 0; k < 4; k++) {
+        const u32 cnt = tpl_cnt(v);
+        bool conflict;
+        u64 nv;
+        if (ex) {
+            conflict = cnt != 0;
+            nv = tpl_make(false, 1, age);
+        } else {
+            conflict = cnt != 0 && !(v & TPL_S);
+            nv = cnt == 0 ? tpl_make(true, 1, age) : tpl_make(true, cnt + 1, min(age, tpl_holder(v)));
+        }
+        if (conflict) {
+            // no-wait: abort at once (PAPER.md:176).  wait-die: an older requester
+            // (smaller age) waits, a younger one dies (PAPER.md:176, SPEC.md:254).
+            return (WD && age < tpl_holder(v)) ? 1 : 2;
+        }
+        const u64 old = cas_acqrel(w, v, nv);
+        if (old == v) return 0;
+        v = old;
+    }
+    return 1;
+}
+
+GC_DEV void tpl_release_relaxed(u64 *w, bool ex) {
+    if (ex) st_relaxed(w, 0ull);
+    else atom_add_relaxed(w, (u64)(-(long long)TPL_ONE));
+}
+
+// ------------------------------------------------------------------ TO (Table II)
+// word = [62] pending (uncommitted write) | [61:31] RTS | [30:0] WTS.  While pending,
+// WTS holds the pending writer's ts (the writer keeps the committed word to restore
+// on abort).  Reading rules follow PAPER.md:188 with reading Z4.
+constexpr u64 TO_P = 1ull << 62;
+GC_DEV u64 to_rts(u64 v) { return (v >> 31) & M31; }
+GC_DEV u64 to_wts(u64 v) { return v & M31; }
+GC_DEV u64 to_make(bool pend, u64 rts, u64 wts) {
+    return (pend ? TO_P : 0ull) | ((rts & M31) << 31) | (wts & M31);
+}
+
+// ------------------------------------------------------------------ MVCC (Table II)
+// meta[2r]   lo = TO word (pending | RTS | WTS); while pending WTS = pending writer ts
+// meta[2r+1] hi = version pointer word: [63:32] begin ts of the in-place head version,
+//                 [31:0] arena index of the previous version (NONE = 0xFFFFFFFF).
+// History nodes (one per write op of the batch): word0 = the hi word
+// of the version they replaced ((begin << 32) | prev), word1 = 0, then the row content.
+constexpr u64 VNONE = 0xFFFFFFFFull;
+
+// ------------------------------------------------------------------ OCC (Table II)
+constexpr u64 LOCKB = 1ull << 63;    // Silo: [63] lock | [62:0] TID
+constexpr u64 M48 = (1ull << 48) - 1; // TicToc: [63] lock | [62:48] delta | [47:0] WTS
+constexpr u64 DMAX = 0x7FFFull;
+GC_DEV u64 tt_wts(u64 v) { return v & M48; }
+GC_DEV u64 tt_rts(u64 v) { return (v & M48) + ((v >> 48) & DMAX); }
+
+// Per-access step outcomes used by both modes
+enum { ST_DONE = 0, ST_WAIT = 1, ST_ABORT = 2 };
+
+// TO access step for one item (write = read-modify-write).  On success for a write the
+// row is read under the pending bit; for a read it is read between two word loads.
+template <class WL>
+GC_DEV int to_step(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+                   u32 gid, u32 i, u64 ts, bool &pend, u64 &saved) {
+    u64 *w = &p.meta[L.rec];
+    const u64 *row = WL::row(y, L);
+    const u64 v = ld_acquire(w);
+    if (L.w) {
+        if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;   // older pending: wait (Z4)
+        if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
+        if (cas_acqrel(w, v, to_make(true, to_rts(v), ts)) != v) return ST_WAIT;
+        pend = true;
+        saved = v;
+        WL::read(y, L, gid, i, row);   // stable: we own the pending bit
+        return ST_DONE;
+    }
+    if (ts < to_wts(v)) return ST_ABORT;
+    if (v & TO_P) return ST_WAIT;
+    WL::read(y, L, gid, i, row);
+    fence_acqrel();
+    if (to_rts(v) >= ts) return ld_relaxed(w) == v ? ST_DONE : ST_WAIT;
+    return cas_acqrel(w, v, to_make(false, ts, to_wts(v))) == v ? ST_DONE : ST_WAIT;
+}
+
+template <class WL>
+GC_DEV void to_commit(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L, u64 ts) {
+    WL::install(y, L, WL::row(y, L));
+    fence_acqrel();
+    st_relaxed(&p.meta[L.rec], to_make(false, ts, ts));
+}
+
+// MVCC access step (Z6): writes append at the head only; reads never abort.
+template <class WL>
+GC_DEV int mvcc_step(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+                     u32 gid, u32 i, u64 ts, bool &pend, u64 &saved_wts) {
+    u64 *lo = &p.meta[2ull * L.rec];
+    u64 *hi = lo + 1;
+    const u64 *row = WL::row(y, L);
+    const u64 v = ld_acquire(lo);
+    if (L.w) {
+        if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;
+        if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
+        if (cas_acqrel(lo, v, to_make(true, to_rts(v), ts)) != v) return ST_WAIT;
+        pend = true;
+        saved_wts = to_wts(v);
+        WL::read(y, L, gid, i, row);
+        return ST_DONE;
+    }
+    if ((v & TO_P) && to_wts(v) < ts) return ST_WAIT;   // older pending writer: its version is ours
+    const u64 h = ld_acquire(hi);
+    if ((h >> 32) <= ts) {   // head visible: read in place, validate, raise RTS
+        WL::read(y, L, gid, i, row);
+        fence_acqrel();
+        if (ld_relaxed(hi) != h) return ST_WAIT;
+        if (to_rts(v) >= ts) return ld_relaxed(lo) == v ? ST_DONE : ST_WAIT;
+        const u64 nv = (v & ~(M31 << 31)) | ((ts & M31) << 31);
+        return cas_acqrel(lo, v, nv) == v ? ST_DONE : ST_WAIT;
+    }
+    // walk the history chain for the newest version with begin <= ts
+    u64 idx = h & VNONE;
+    while (idx != VNONE) {
+        const u64 *node = p.arena + idx * (2 + WL::ROW_WORDS);
+        const u64 h0 = ld_cg(node);
+        if ((h0 >> 32) <= ts) {
+            WL::read(y, L, gid, i, node + 2);
+            return ST_DONE;
+        }
+        idx = h0 & VNONE;
+    }
+    set_err(p.ctl, CC_ERR_VERSION_EXHAUSTED);
+    return ST_ABORT;
+}
+
+template <class WL>
+GC_DEV void mvcc_restore(const ExecParams &p, typename WL::Lane &L, u64 saved_wts) {
+    u64 *lo = &p.meta[2ull * L.rec];
+    u64 v = ld_relaxed(lo);
+    for (;;) {   // keep RTS raised by readers while we were pending
+        const u64 old = cas_acqrel(lo, v, to_make(false, to_rts(v), saved_wts));
+        if (old == v) return;
+        v = old;
+    }
+}
+
+template <class WL>
+GC_DEV void mvcc_commit(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+                        u32 gid, u32 i, u64 ts) {
+    u64 *lo = &p.meta[2ull * L.rec];
+    u64 *hi = lo + 1;
+    u64 *row = WL::row(y, L);
+    const u64 nidx = (u64)gid * p.K + i;
+    u64 *node = p.arena + nidx * (2 + WL::ROW_WORDS);
+    st_cg(node, ld_relaxed(hi));   // old head -> history node (begin, prev)
+    WL::copy_row(row, node + 2);
+    fence_acqrel();
+    st_release(hi, (ts << 32) | nidx);   // publish the history, then install in place
+    fence_acqrel();
+    WL::install(y, L, row);
+    fence_acqrel();
+    st_relaxed(lo, to_make(false, ts, ts));
+}
+
+// OCC read-phase step: snapshot (word, row, word); spin while locked (Z10).
+template <class WL>
+GC_DEV int occ_snap_step(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+                         u32 gid, u32 i, u64 &obs) {
+    u64 *w = &p.meta[L.rec];
+    const u64 v1 = ld_acquire(w);
+    if (v1 & LOCKB) return ST_WAIT;
+    WL::read(y, L, gid, i, WL::row(y, L));
+    fence_acqrel();
+    if (ld_relaxed(w) != v1) return ST_WAIT;
+    obs = v1;
+    return ST_DONE;
+}
+
+// no-wait write lock
+GC_DEV bool occ_lock(u64 *w, u64 &pre) {
+    u64 v = ld_relaxed(w);
+    for (int k = 0; k < 8; k++) {
+        if (v & LOCKB) return false;
+        const u64 old = cas_acqrel(w, v, v | LOCKB);
+        if (old == v) {
+            pre = v;
+            return true;
+        }
+        v = old;
+    }
+    return false;
+}
+
+// TicToc read-set validation of one item against commit_ts (Z9)
+GC_DEV bool tictoc_validate(u64 *w, u64 obs, u64 cts) {
+    if (tt_rts(obs) >= cts) return true;   // version valid through cts already
+    u64 v = ld_acquire(w);
+    for (;;) {
+        if (tt_wts(v) != tt_wts(obs) || (v & LOCKB)) return false;
+        if (tt_rts(v) >= cts) return true;
+        u64 nw = tt_wts(v);
+        if (cts - nw > DMAX) nw = cts - DMAX;   // delta overflow: shift WTS up (Z9)
+        const u64 old = cas_acqrel(w, v, ((cts - nw) << 48) | nw);
+        if (old == v) return true;
+        v = old;
+    }
+}
+
+GC_DEV bool draw_ts_overflow(u64 ts, const ExecParams &p) {
+    if (ts > M31) {   // 31-bit field
+        set_err(p.ctl, CC_ERR_TS_OVERFLOW);
+        return true;
+    }
+    return false;
+}
+
+// ===================================================================== thread mode
+// One lane per transaction; accesses processed in ascending key order.
 template <int S, class WL>
-__global__ void __launch_bounds__(1024) exec_kernel(ExecParams p, typename WL::Params y) {
+GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typename WL::Params &y,
+                      u64 &key_hi, u64 &key_lo) {
+    const ExecParams &p = *th.p;
+    if constexpr (S == CC_TPL_NW || S == CC_TPL_WD) {
+        constexpr bool WD = S == CC_TPL_WD;
+        const u32 age = gid + 1;
+        u32 i = 0;
+        int r = RES_OK;
+        for (; i < n; i++) {
+            Spin sp;
+            int st;
+            while ((st = tpl_try<WD>(&p.meta[L[i].rec], L[i].w, age)) == ST_WAIT)
+                if (!sp.wait(th)) { st = -1; break; }
+            if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
+            WL::read(y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
+        }
+        if (r != RES_OK) {
+            fence_acqrel();
+            for (u32 j = 0; j < i; j++) tpl_release_relaxed(&p.meta[L[j].rec], L[j].w);
+            return r;
+        }
+        // lock point: every lock held, none released -> a valid serial order (strict 2PL)
+        key_lo = agg_fetch_add(&p.ctl->ticket.v);
+        key_hi = 0;
+        for (u32 j = 0; j < n; j++)
+            if (L[j].w) WL::install(y, L[j], WL::row(y, L[j]));
+        fence_acqrel();
+        for (u32 j = 0; j < n; j++) tpl_release_relaxed(&p.meta[L[j].rec], L[j].w);
+        return RES_OK;
+    } else if constexpr (S == CC_TO || S == CC_MVCC) {
+        const u64 ts = agg_fetch_add(&p.ctl->ts.v) + 1;   // fresh ts per attempt
+        if (draw_ts_overflow(ts, p)) return RES_FATAL;
+        u32 pendm = 0;
+        u64 saved[WL::MAXK];
+        int r = RES_OK;
+        for (u32 i = 0; i < n && r == RES_OK; i++) {
+            Spin sp;
+            for (;;) {
+                bool pend = false;
+                const int st = (S == CC_TO) ? to_step<WL>(p, y, L[i], gid, i, ts, pend, saved[i])
+                                            : mvcc_step<WL>(p, y, L[i], gid, i, ts, pend, saved[i]);
+                if (pend) pendm |= 1u << i;
+                if (st == ST_DONE) break;
+                if (st == ST_ABORT) { r = RES_ABORT; break; }
+                if (!sp.wait(th)) { r = RES_FATAL; break; }
+            }
+        }
+        if (r != RES_OK) {
+            for (u32 j = 0; j < n; j++)
+                if ((pendm >> j) & 1) {
+                    if (S == CC_TO) st_release(&p.meta[L[j].rec], saved[j]);
+                    else mvcc_restore<WL>(p, L[j], saved[j]);
+                }
+            return r;
+        }
+        for (u32 j = 0; j < n; j++)
+            if ((pendm >> j) & 1) {
+                if (S == CC_TO) to_commit<WL>(p, y, L[j], ts);
+                else mvcc_commit<WL>(p, y, L[j], gid, j, ts);
+            }
+        key_hi = 0;
+        key_lo = ts;
+        return RES_OK;
+    } else if constexpr (S == CC_SILO || S == CC_TICTOC) {
+        u64 obs[WL::MAXK], pre[WL::MAXK];
+        for (u32 i = 0; i < n; i++) {
+            Spin sp;
+            while (occ_snap_step<WL>(p, y, L[i], gid, i, obs[i]) != ST_DONE)
+                if (!sp.wait(th)) return RES_FATAL;
+        }
+        u32 locked = 0;
+        bool ok = true;
+        for (u32 i = 0; i < n && ok; i++)
+            if (L[i].w) {
+                if (occ_lock(&p.meta[L[i].rec], pre[i])) locked |= 1u << i;
+                else ok = false;
+            }
+        u64 ticket = 0, cts = 0;
+        if (ok && S == CC_SILO) {
+            ticket = agg_fetch_add(&p.ctl->ticket.v);   // serialization point
+            fence_acqrel();
+            for (u32 i = 0; i < n && ok; i++)
+                ok = L[i].w ? (pre[i] == obs[i]) : (ld_acquire(&p.meta[L[i].rec]) == obs[i]);
+        }
+        if (ok && S == CC_TICTOC) {
+            for (u32 i = 0; i < n; i++) {   // commit_ts
+                if (L[i].w) cts = max(cts, tt_rts(pre[i]) + 1);
+                cts = max(cts, tt_wts(obs[i]));
+            }
+            for (u32 i = 0; i < n && ok; i++)
+                ok = L[i].w ? (tt_wts(pre[i]) == tt_wts(obs[i]))
+                            : tictoc_validate(&p.meta[L[i].rec], obs[i], cts);
+            if (ok) ticket = agg_fetch_add(&p.ctl->ticket.v);   // after validation
+        }
+        if (!ok) {
+            fence_acqrel();
+            for (u32 j = 0; j < n; j++)
+                if ((locked >> j) & 1) st_relaxed(&p.meta[L[j].rec], pre[j]);
+            return RES_ABORT;
+        }
+        u64 nw;
+        if (S == CC_SILO) {
+            u64 tid = 0;
+            for (u32 i = 0; i < n; i++) tid = max(tid, obs[i]);
+            nw = (tid + 1) & ~LOCKB;   // TID = 1 + max observed (epoch dropped)
+            key_hi = 0;
+        } else {
+            nw = cts & M48;
+            key_hi = cts;
+        }
+        key_lo = ticket;
+        for (u32 j = 0; j < n; j++)
+            if (L[j].w) WL::install(y, L[j], WL::row(y, L[j]));
+        fence_acqrel();
+        for (u32 j = 0; j < n; j++)
+            if (L[j].w) st_relaxed(&p.meta[L[j].rec], nw);
+        return RES_OK;
+    } else if constexpr (S == CC_GACCO) {
+        // wait for the turn, access, advance the cursor (release after the op, Z3)
+        const u64 base = (u64)gid * p.K;
+        for (u32 i = 0; i < n; i++) {
+            const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
+            u32 *cur = &p.cursor[seg];
+            Spin sp;
+            while (ld_acquire32(cur) != pos)
+                if (!sp.wait(th)) return RES_FATAL;
+            u64 *row = WL::row(y, L[i]);
+            WL::read(y, L[i], gid, i, row);
+            if (L[i].w) WL::install(y, L[i], row);
+            st_release32(cur, pos + 1);
+        }
+        key_hi = 0;
+        key_lo = gid;
+        return RES_OK;
+    } else {   // GPUTx: K-set k runs after K-set k-1 completes; no CC inside
+        const u32 k = p.rank_of[gid];
+        if (k > 0) {
+            Spin sp;
+            while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
+                if (!sp.wait(th)) return RES_FATAL;
+        }
+        for (u32 i = 0; i < n; i++) {
+            u64 *row = WL::row(y, L[i]);
+            WL::read(y, L[i], gid, i, row);
+            if (L[i].w) WL::install(y, L[i], row);
+        }
+        atom_add_release32(&p.rank_done[k], 1u);
+        key_hi = 0;
+        key_lo = gid;
+        return RES_OK;
+    }
+}
+
+template <int S, class WL>
+__global__ void __launch_bounds__(1024) exec_thread_kernel(ExecParams p, typename WL::Params y) {
     const u32 lane = threadIdx.x & 31u;
     if (lane >= (1u << p.wd)) return;   // idle lanes exit at once
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
     Th th;
     th.p = &p;
+    th.polls = 0;
     th.deadline = globaltimer_ns() + p.watchdog_ns;
-    typename WL::Txn t;
-    typename WL::Ws ws;
+    typename WL::Lane L[WL::MAXK];
+    bool exhausted = false;
     for (;;) {
-        if (dead(th)) return;
-        const u64 s = agg_fetch_add(&p.ctl->head);
-        u32 gid;
-        if (s < p.n_txn) {
-            gid = (S == CC_GPUTX) ? p.rank_order[s] : (u32)s;
-        } else {
-            if (DET || (p.flags & CC_FLAG_IMMEDIATE_RETRY)) return;
-            if (!ring_take(th, s - p.n_txn, gid)) return;
-        }
-        if (!WL::load(p, y, gid, t)) {
+        const u32 gid = claim_work<S>(th, exhausted);
+        if (gid == NO_TXN) return;
+        const u32 n = WL::load_all(p, y, gid, L);
+        if (n == 0xFFFFFFFFu) {
             set_err(p.ctl, CC_ERR_KEY_NOT_FOUND);
             return;
         }
         for (;;) {
-            const int r = run_scheme<S, WL>(th, t, ws, y);
+            u64 kh, kl;
+            const int r = run_thread<S, WL>(th, gid, L, n, y, kh, kl);
             if (r == RES_OK) {
-                WL::emit(p, y, t, ws);
-                p.order_hi[gid] = t.key_hi;
-                p.order_lo[gid] = t.key_lo;
+                for (u32 i = 0; i < n; i++) WL::emit(p, y, L[i], gid, i);
+                p.order_hi[gid] = kh;
+                p.order_lo[gid] = kl;
                 p.committed[gid] = 1;
-                agg_add(&p.ctl->done);
                 break;
             }
-            if (r == RES_FATAL) return;
+            if (r == RES_FATAL || DET) return;
             const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
             p.restarts[gid] = nr;
-            agg_add(&p.ctl->aborts);
             abort_backoff(gid, nr);
-            if (p.flags & CC_FLAG_IMMEDIATE_RETRY) continue;
-            ring_push(th, gid);
-            break;
+            if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && fresh_left(p)) {
+                ring_push_one(th, agg_fetch_add(&p.ctl->tail.v), gid);   // compaction (a6)
+                break;
+            }
+        }
+    }
+}
+
+// ===================================================================== tile mode
+// G lanes per transaction; lane i owns access i.  Every loop below is tile-uniform:
+// the exit conditions are tile votes, so all lanes execute the same collectives.
+template <int S, class WL, class Tile>
+GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
+                    const typename WL::Params &y, u64 &key_hi, u64 &key_lo) {
+    const ExecParams &p = *th.p;
+    const u32 li = tile.thread_rank();
+    const bool act = L.act;
+    if constexpr (S == CC_TPL_NW || S == CC_TPL_WD) {
+        constexpr bool WD = S == CC_TPL_WD;
+        const u32 age = gid + 1;
+        bool held = false;
+        Spin sp;
+        for (;;) {
+            int st = ST_DONE;
+            if (act && !held) {
+                st = tpl_try<WD>(&p.meta[L.rec], L.w, age);
+                held = st == ST_DONE;
+            }
+            if (tile.any(st == ST_ABORT)) {
+                if (held) tpl_release_relaxed(&p.meta[L.rec], L.w);
+                return RES_ABORT;
+            }
+            if (tile.all(!act || held)) break;
+            if (tile.any(!sp.wait(th))) {
+                if (held) tpl_release_relaxed(&p.meta[L.rec], L.w);
+                return RES_FATAL;
+            }
+        }
+        if (act) WL::read(y, L, gid, li, WL::row(y, L));   // stable under the lock
+        u64 ticket = 0;
+        if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // lock point
+        key_lo = tile.shfl(ticket, 0);
+        key_hi = 0;
+        if (act && L.w) WL::install(y, L, WL::row(y, L));
+        fence_acqrel();
+        if (act) tpl_release_relaxed(&p.meta[L.rec], L.w);
+        return RES_OK;
+    } else if constexpr (S == CC_TO || S == CC_MVCC) {
+        u64 ts = 0;
+        if (li == 0) ts = atomicAdd(&p.ctl->ts.v, 1ull) + 1;
+        ts = tile.shfl(ts, 0);
+        if (draw_ts_overflow(ts, p)) return RES_FATAL;
+        bool done = !act, pend = false;
+        u64 saved = 0;
+        Spin sp;
+        for (;;) {
+            int st = ST_DONE;
+            if (!done) {
+                st = (S == CC_TO) ? to_step<WL>(p, y, L, gid, li, ts, pend, saved)
+                                  : mvcc_step<WL>(p, y, L, gid, li, ts, pend, saved);
+                done = st == ST_DONE;
+            }
+            if (tile.any(st == ST_ABORT)) {
+                if (pend) {
+                    if (S == CC_TO) st_release(&p.meta[L.rec], saved);
+                    else mvcc_restore<WL>(p, L, saved);
+                }
+                return RES_ABORT;
+            }
+            if (tile.all(done)) break;
+            if (tile.any(!sp.wait(th))) {
+                if (pend) {
+                    if (S == CC_TO) st_release(&p.meta[L.rec], saved);
+                    else mvcc_restore<WL>(p, L, saved);
+                }
+                return RES_FATAL;
+            }
+        }
+        if (pend) {
+            if (S == CC_TO) to_commit<WL>(p, y, L, ts);
+            else mvcc_commit<WL>(p, y, L, gid, li, ts);
+        }
+        key_hi = 0;
+        key_lo = ts;
+        return RES_OK;
+    } else if constexpr (S == CC_SILO || S == CC_TICTOC) {
+        u64 obs = 0, pre = 0;
+        bool done = !act;
+        Spin sp;
+        for (;;) {   // read phase
+            if (!done) done = occ_snap_step<WL>(p, y, L, gid, li, obs) == ST_DONE;
+            if (tile.all(done)) break;
+            if (tile.any(!sp.wait(th))) return RES_FATAL;
+        }
+        bool locked = false, bad = false;
+        if (act && L.w) {
+            locked = occ_lock(&p.meta[L.rec], pre);
+            bad = !locked;
+        }
+        u64 ticket = 0, cts = 0;
+        if (!tile.any(bad)) {
+            if (S == CC_SILO) {
+                if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // serialization point
+                ticket = tile.shfl(ticket, 0);
+                fence_acqrel();
+                if (act) bad = L.w ? (pre != obs) : (ld_acquire(&p.meta[L.rec]) != obs);
+            } else {
+                u64 c = 0;
+                if (act) c = max(L.w ? tt_rts(pre) + 1 : 0ull, tt_wts(obs));
+                cts = cg::reduce(tile, c, cg::greater<u64>());
+                if (act) bad = L.w ? (tt_wts(pre) != tt_wts(obs)) : !tictoc_validate(&p.meta[L.rec], obs, cts);
+                if (!tile.any(bad)) {
+                    if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // after validation
+                    ticket = tile.shfl(ticket, 0);
+                }
+            }
+        }
+        if (tile.any(bad)) {
+            if (locked) st_release(&p.meta[L.rec], pre);
+            return RES_ABORT;
+        }
+        u64 nw;
+        if (S == CC_SILO) {
+            const u64 tid = cg::reduce(tile, act ? obs : 0ull, cg::greater<u64>());
+            nw = (tid + 1) & ~LOCKB;
+            key_hi = 0;
+        } else {
+            nw = cts & M48;
+            key_hi = cts;
+        }
+        key_lo = ticket;
+        if (act && L.w) WL::install(y, L, WL::row(y, L));
+        fence_acqrel();
+        if (act && L.w) st_relaxed(&p.meta[L.rec], nw);
+        return RES_OK;
+    } else if constexpr (S == CC_GACCO) {
+        int st = ST_DONE;
+        if (act) {   // each lane waits for its own item's turn: overlapped across items
+            const u64 a = (u64)gid * p.K + li;
+            const u32 seg = p.acc_seg[a], pos = p.acc_pos[a];
+            u32 *cur = &p.cursor[seg];
+            Spin sp;
+            while (ld_acquire32(cur) != pos)
+                if (!sp.wait(th)) { st = ST_ABORT; break; }
+            if (st == ST_DONE) {
+                u64 *row = WL::row(y, L);
+                WL::read(y, L, gid, li, row);
+                if (L.w) WL::install(y, L, row);
+                st_release32(cur, pos + 1);
+            }
+        }
+        if (tile.any(st != ST_DONE)) return RES_FATAL;
+        key_hi = 0;
+        key_lo = gid;
+        return RES_OK;
+    } else {   // GPUTx
+        const u32 k = p.rank_of[gid];
+        int st = ST_DONE;
+        if (li == 0 && k > 0) {
+            Spin sp;
+            while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
+                if (!sp.wait(th)) { st = ST_ABORT; break; }
+        }
+        if (tile.any(st != ST_DONE)) return RES_FATAL;
+        if (act) {
+            u64 *row = WL::row(y, L);
+            WL::read(y, L, gid, li, row);
+            if (L.w) WL::install(y, L, row);
+        }
+        tile.sync();   // every lane's install precedes the K-set release
+        if (li == 0) atom_add_release32(&p.rank_done[k], 1u);
+        key_hi = 0;
+        key_lo = gid;
+        return RES_OK;
+    }
+}
+
+template <int S, class WL, int G>
+__global__ void __launch_bounds__(1024) exec_tile_kernel(ExecParams p, typename WL::Params y) {
+    auto tile = cg::tiled_partition<G>(cg::this_thread_block());
+    const u32 li = tile.thread_rank();
+    constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
+    Th th;
+    th.p = &p;
+    th.polls = 0;
+    th.deadline = globaltimer_ns() + p.watchdog_ns;
+    typename WL::Lane L;
+    bool exhausted = false;
+    for (;;) {
+        u32 gid = NO_TXN;
+        if (li == 0) gid = claim_work<S>(th, exhausted);
+        gid = tile.shfl(gid, 0);
+        if (gid == NO_TXN) return;
+        const bool ok = WL::load_lane(p, y, gid, li, L);
+        if (!tile.all(ok)) {
+            if (li == 0) set_err(p.ctl, CC_ERR_KEY_NOT_FOUND);
+            return;
+        }
+        for (;;) {
+            u64 kh = 0, kl = 0;
+            const int r = run_tile<S, WL>(tile, th, gid, L, y, kh, kl);
+            if (r == RES_OK) {
+                if (L.act) WL::emit(p, y, L, gid, li);
+                if (li == 0) {
+                    p.order_hi[gid] = kh;
+                    p.order_lo[gid] = kl;
+                    p.committed[gid] = 1;
+                }
+                break;
+            }
+            if (r == RES_FATAL || DET) return;
+            int push = 0;
+            if (li == 0) {
+                const u32 nr = p.restarts[gid] + 1;
+                p.restarts[gid] = nr;
+                abort_backoff(gid, nr);
+                push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && fresh_left(p);
+                if (push) ring_push_one(th, atomicAdd(&p.ctl->tail.v, 1ull), gid);
+            }
+            if (tile.shfl(push, 0)) break;
         }
     }
 }

@@ -7,19 +7,24 @@
 
 namespace gcctb {
 
-// Device control block of one submit (all counters reset by the a2 reset kernel).
+// Device control block of one submit (reset by the a2 reset kernel).  Every hot
+// counter lives in its own 256 B block so that claims, tickets, timestamps and the
+// error word never share an L2 line (and usually not an L2 slice).
+struct alignas(256) Counter {
+    unsigned long long v;
+    unsigned long long pad[31];
+};
 struct Ctl {
-    unsigned long long head;     // claim counter over [0, n_txn) then the retry ring
-    unsigned long long tail;     // retry-ring append counter
-    unsigned long long done;     // committed transactions
-    unsigned long long ts;       // TO/MVCC timestamp allocator (first ts = 1)
-    unsigned long long ticket;   // lock-point / serialization-point ticket
-    unsigned long long err;      // first device error (cc_status), 0 = none
-    unsigned long long aborts;
-    unsigned long long attempts;
-    unsigned long long max_rank;
-    unsigned long long rank_head;  // GPUTx rank-pass claim counter
-    unsigned long long pad[6];
+    Counter head;       // claim counter over [0, n_txn)
+    Counter tail;       // retry-ring append counter (producers)
+    Counter rhead;      // retry-ring claim counter (consumers)
+    Counter done;       // committed transactions (counted at emission)
+    Counter ts;         // TO/MVCC timestamp allocator (first ts = 1)
+    Counter ticket;     // lock-point / serialization-point ticket
+    Counter err;        // first device error (cc_status), 0 = none
+    Counter aborts;     // sum of restarts (counted at emission)
+    Counter max_rank;   // GPUTx: number of K-sets - 1
+    Counter rank_head;  // GPUTx rank-pass claim counter
 };
 
 enum { KIND_YCSB = 1, KIND_TPCC = 2 };
@@ -31,6 +36,7 @@ struct ExecParams {
     uint32_t K;                  // accesses per transaction slot (YCSB ops_per_txn)
     uint32_t wd;
     uint32_t flags;
+    uint32_t lanes;              // lanes per transaction (1 = thread per txn)
     unsigned long long watchdog_ns;
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
@@ -83,7 +89,7 @@ cudaError_t launch_reset_meta(int scheme, unsigned long long *meta, uint64_t n_r
                               cudaStream_t s);
 cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
                              cudaStream_t s);
-int ycsb_exec_max_blocks_per_sm(int scheme, int block);
+int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block);
 cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBufs &b,
                                cudaStream_t s);
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,

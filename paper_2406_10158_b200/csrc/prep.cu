@@ -31,7 +31,7 @@ __global__ void reset_kernel(int scheme, u64 *meta, uint64_t n_records, u64 *rin
         for (uint64_t r = tid; r < n_records; r += stride) meta[r] = 0ull;
     }
     for (uint64_t r = tid; r < ring_cap; r += stride) ring[r] = 0ull;
-    if (tid < sizeof(Ctl) / 8) reinterpret_cast<u64 *>(ctl)[tid] = 0ull;
+    for (uint64_t r = tid; r < sizeof(Ctl) / 8; r += stride) reinterpret_cast<u64 *>(ctl)[r] = 0ull;
 }
 
 __global__ void zero_txn_kernel(uint8_t *committed, uint32_t *restarts, u64 *ohi, u64 *olo,
@@ -102,41 +102,53 @@ __global__ void positions_kernel(const u64 *keys, const uint32_t *seg_id, const 
 // predecessor is claimed by a running lane) and wait for predecessor ranks.
 constexpr uint32_t RANK_UNSET = 0xFFFFFFFFu;
 
+template <int G>
 __global__ void __launch_bounds__(256) gputx_rank_kernel(
     const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_id, const uint32_t *seg_start,
     const uint32_t *lw, uint32_t *rank, uint32_t n_txn, uint32_t K, Ctl *ctl,
     u64 watchdog_ns) {
+    // a tile of G lanes per transaction, lane i resolves the predecessors of access i
+    auto tile = cg::tiled_partition<G>(cg::this_thread_block());
+    const uint32_t li = tile.thread_rank();
     const u64 deadline = globaltimer_ns() + watchdog_ns;
     for (;;) {
-        const u64 s = agg_fetch_add(&ctl->rank_head);
+        u64 s = 0;
+        if (li == 0) s = atomicAdd(&ctl->rank_head.v, 1ull);
+        s = tile.shfl(s, 0);
         if (s >= n_txn) return;
         const uint32_t gid = (uint32_t)s;
         uint32_t r = 0;
-        for (uint32_t i = 0; i < K; i++) {
-            const uint32_t p = sorted_pos[(u64)gid * K + i];
+        bool fail = false;
+        if (li < K) {
+            const uint32_t p = sorted_pos[(u64)gid * K + li];
             const uint32_t s0 = seg_start[seg_id[p] - 1];
             const bool w = keys[p] & 1ull;
-            const uint32_t q = (p > s0) ? lw[p - 1] : 0u;    // last write before p (+1)
-            const bool has_q = q > s0;                          // inside this segment
-            uint32_t lo = has_q ? q - 1 : s0;                   // first predecessor to visit
-            uint32_t hi = w ? p : (has_q ? q : s0);             // reads: only the write
-            for (uint32_t x = lo; x < hi; x++) {
+            const uint32_t q = (p > s0) ? lw[p - 1] : 0u;   // last write before p (+1)
+            const bool has_q = q > s0;                        // inside this segment
+            const uint32_t lo = has_q ? q - 1 : s0;           // first predecessor to visit
+            const uint32_t hi = w ? p : (has_q ? q : s0);     // reads: only that write
+            for (uint32_t x = lo; x < hi && !fail; x++) {
                 const uint32_t u = (uint32_t)((keys[x] >> 6) & GID_MASK);
                 uint32_t ru;
-                unsigned ns = 20;
+                unsigned ns = 8;
                 while ((ru = ld_acquire32(&rank[u])) == RANK_UNSET) {
-                    if (ld_relaxed(&ctl->err) || globaltimer_ns() > deadline) {
-                        atomicCAS(&ctl->err, 0ull, (u64)CC_ERR_WATCHDOG);
-                        return;
+                    if (globaltimer_ns() > deadline || ld_relaxed(&ctl->err.v)) {
+                        atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_WATCHDOG);
+                        fail = true;
+                        break;
                     }
                     __nanosleep(ns);
-                    ns = ns < 320 ? ns * 2 : 320;
+                    ns = ns < 128 ? ns * 2 : 128;
                 }
                 r = max(r, ru + 1);
             }
         }
-        st_release32(&rank[gid], r);
-        atomicMax(&ctl->max_rank, (u64)r);
+        if (tile.any(fail)) return;
+        r = cg::reduce(tile, r, cg::greater<uint32_t>());
+        if (li == 0) {
+            st_release32(&rank[gid], r);
+            atomicMax(&ctl->max_rank.v, (u64)r);
+        }
     }
 }
 
@@ -169,7 +181,7 @@ int rank_kernel_grid() {
     int dev = 0, sms = 148, nb = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gputx_rank_kernel, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gputx_rank_kernel<32>, 256, 0);
     return (nb > 0 ? nb : 1) * sms;
 }
 
@@ -205,7 +217,9 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     size_t bytes = b.cub_bytes;
     cudaError_t e;
     const int end_bit = KEY_SHIFT + bits_for(n_records);
-    e = cub::DeviceRadixSort::SortKeys(b.cub_tmp, bytes, b.keys_in, b.keys_out, (int)n, 0,
+    // keys arrive in (gid, i) order; a stable LSD sort on the record bits alone keeps
+    // transaction ids ascending within each item (3 passes for 2^24 records, not 7)
+    e = cub::DeviceRadixSort::SortKeys(b.cub_tmp, bytes, b.keys_in, b.keys_out, (int)n, KEY_SHIFT,
                                        end_bit > 64 ? 64 : end_bit, s);
     if (e) return e;
     head_flag_kernel<<<g, blk, 0, s>>>(b.keys_out, b.head_flag, b.lw, n);
@@ -222,8 +236,12 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     e = cub::DeviceScan::InclusiveScan(b.cub_tmp, bytes, b.lw, b.head_flag, cub::Max(), (int)n, s);
     if (e) return e;
     fill_u32_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank, RANK_UNSET, p.n_txn);
-    gputx_rank_kernel<<<grid, 256, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start, b.head_flag,
-                                           b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
+    if (p.K <= 16)
+        gputx_rank_kernel<16><<<grid, 256, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
+                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
+    else
+        gputx_rank_kernel<32><<<grid, 256, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
+                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
     iota_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.gid_in, p.n_txn);
     bytes = b.cub_bytes;
     e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.rank, b.rank_sorted, b.gid_in,
@@ -252,23 +270,32 @@ __global__ void gather_hi_kernel(const u64 *hi, const uint32_t *perm, u64 *out, 
 
 __global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t *pos) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t c = 0, a = 0;
     if (i < p.n_txn) {
-        r.committed[i] = p.committed[i];
-        if (r.restarts) r.restarts[i] = p.restarts[i];
+        c = p.committed[i];
+        a = p.restarts[i];
+        r.committed[i] = (uint8_t)c;
+        if (r.restarts) r.restarts[i] = a;
         if (r.order_hi) r.order_hi[i] = p.order_hi[i];
         if (r.order_lo) r.order_lo[i] = p.order_lo[i];
         if (r.commit_pos) r.commit_pos[i] = pos[i];
     }
-    if (i == 0 && r.stats) {
-        const Ctl *c = p.ctl;
-        r.stats[0] = c->done;
-        r.stats[1] = c->aborts;
-        r.stats[2] = c->done + c->aborts;
-        r.stats[3] = c->err;
-        r.stats[4] = c->max_rank;
-        r.stats[5] = c->ts;
-        for (int k = 6; k < CC_STATS_WORDS; k++) r.stats[k] = 0;
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    a = __reduce_add_sync(0xFFFFFFFFu, a);
+    if ((threadIdx.x & 31) == 0) {
+        if (c) atomicAdd(&p.ctl->done.v, (u64)c);
+        if (a) atomicAdd(&p.ctl->aborts.v, (u64)a);
     }
+}
+
+__global__ void stats_kernel(const Ctl *c, uint64_t *stats) {
+    stats[0] = c->done.v;
+    stats[1] = c->aborts.v;
+    stats[2] = c->done.v + c->aborts.v;
+    stats[3] = c->err.v;
+    stats[4] = c->max_rank.v;
+    stats[5] = c->ts.v;
+    for (int k = 6; k < CC_STATS_WORDS; k++) stats[k] = 0;
 }
 
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
@@ -300,6 +327,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         }
     }
     copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);
+    stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats);
     return cudaGetLastError();
 }
 

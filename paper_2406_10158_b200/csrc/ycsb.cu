@@ -14,53 +14,55 @@ struct YcsbWL {
     static constexpr int MAXK = 16;
     static constexpr int ROW_WORDS = 16;
     using Params = YcsbParams;
-    struct Txn {
-        u32 gid;
-        u32 n;
-        u32 wmask;
-        u32 rec[MAXK];
-        uint8_t field[MAXK];
-        u64 key_hi, key_lo;
-    };
-    struct Ws {
-        u64 out[MAXK];
-        u64 nf[MAXK];
-        u64 n15[MAXK];
+    // One access of a transaction and its private workspace ("private
+    // workspace"): the value read and the buffered new values of a write.
+    struct Lane {
+        u32 rec;
+        bool act, w;
+        uint8_t field;
+        u64 out, nf, n15;
     };
 
-    // Resolve every access up front: the read/write set is predetermined
-    // (PAPER.md:446).  Index lookups are binary searches in the sorted array
-    // (PAPER.md:344), run in lockstep over the K keys for memory-level parallelism.
-    static GC_DEV bool load(const ExecParams &p, const YcsbParams &y, u32 gid, Txn &t) {
-        t.gid = gid;
-        t.n = p.K;
-        t.wmask = 0;
-        const u64 base = (u64)gid * p.K;
-        if (p.acc_rec) {   // deterministic schemes: resolved during preprocessing (a3)
-#pragma unroll
-            for (int i = 0; i < MAXK; i++)
-                if (i < (int)p.K) {
-                    t.rec[i] = p.acc_rec[base + i];
-                    const uint8_t op = y.ops[base + i];
-                    t.field[i] = op & 0x0F;
-                    t.wmask |= (u32)(op >> 7) << i;
-                }
-            return true;
+    // Sorted-array index lookup: branch-free binary search; returns the
+    // row or ~0 for KeyNotFound.
+    static GC_DEV u64 lookup(const YcsbParams &y, u64 key) {
+        const u64 *b = y.idx_keys;
+        u64 n = y.idx_n;
+        while (n > 1) {
+            const u64 half = n >> 1;
+            b = (__ldg(b + half) < key) ? b + half : b;
+            n -= half;
         }
+        u64 pos = (u64)(b - y.idx_keys);
+        u64 kv = __ldg(b);
+        if (kv < key) {
+            pos++;
+            kv = pos < y.idx_n ? __ldg(y.idx_keys + pos) : ~0ull;
+        }
+        return (pos >= y.idx_n || kv != key) ? ~0ull : __ldg(y.idx_rows + pos);
+    }
+
+    // Thread mode: resolve every access up front (read/write sets are predetermined,
+    // PAPER.md:446); the K binary searches run in lockstep for memory-level parallelism.
+    static GC_DEV u32 load_all(const ExecParams &p, const YcsbParams &y, u32 gid, Lane *L) {
+        const u64 base = (u64)gid * p.K;
         u64 key[MAXK];
         const u64 *b[MAXK];
 #pragma unroll
         for (int i = 0; i < MAXK; i++) {
-            if (i < (int)p.K) {
-                key[i] = y.keys[base + i];
+            L[i].act = i < (int)p.K;
+            if (L[i].act) {
                 const uint8_t op = y.ops[base + i];
-                t.field[i] = op & 0x0F;
-                t.wmask |= (u32)(op >> 7) << i;
+                L[i].field = op & 0x0F;
+                L[i].w = op >> 7;
+                key[i] = y.keys[base + i];
+                if (p.acc_rec) L[i].rec = p.acc_rec[base + i];   // resolved by a3
             } else {
                 key[i] = 0;
             }
             b[i] = y.idx_keys;
         }
+        if (p.acc_rec) return p.K;
         u64 n = y.idx_n;
         while (n > 1) {
             const u64 half = n >> 1;
@@ -75,36 +77,57 @@ struct YcsbWL {
             if (i < (int)p.K) {
                 u64 pos = (u64)(b[i] - y.idx_keys);
                 u64 kv = __ldg(b[i]);
-                if (kv < key[i]) { pos++; kv = pos < y.idx_n ? __ldg(y.idx_keys + pos) : ~0ull; }
-                if (pos >= y.idx_n || kv != key[i]) ok = false;   // KeyNotFound
-                else t.rec[i] = (u32)__ldg(y.idx_rows + pos);
+                if (kv < key[i]) {
+                    pos++;
+                    kv = pos < y.idx_n ? __ldg(y.idx_keys + pos) : ~0ull;
+                }
+                if (pos >= y.idx_n || kv != key[i]) ok = false;
+                else L[i].rec = (u32)__ldg(y.idx_rows + pos);
             }
-        return ok;
+        return ok ? p.K : 0xFFFFFFFFu;
     }
 
-    static GC_DEV u64 *row(const YcsbParams &y, u32 rec) { return y.rows + (u64)rec * 16u; }
+    // Tile mode: lane i resolves access i.
+    static GC_DEV bool load_lane(const ExecParams &p, const YcsbParams &y, u32 gid, u32 i, Lane &L) {
+        L.act = i < p.K;
+        if (!L.act) return true;
+        const u64 a = (u64)gid * p.K + i;
+        const uint8_t op = y.ops[a];
+        L.field = op & 0x0F;
+        L.w = op >> 7;
+        if (p.acc_rec) {
+            L.rec = p.acc_rec[a];
+            return true;
+        }
+        const u64 r = lookup(y, y.keys[a]);
+        L.rec = (u32)r;
+        return r != ~0ull;
+    }
 
-    static GC_DEV void read_op(const YcsbParams &, const Txn &t, int i, const u64 *src, Ws &ws) {
+    static GC_DEV u64 *row(const YcsbParams &y, const Lane &L) { return y.rows + (u64)L.rec * 16u; }
+
+    // op semantics (Z11): out = fp(row); a write buffers r[f]*G + ((gid<<4)|i) + 1 and
+    // r[15] + 1 (installed at commit by the scheme).
+    static GC_DEV void read(const YcsbParams &, Lane &L, u32 gid, u32 i, const u64 *src) {
         u64 r[16];
 #pragma unroll
         for (int j = 0; j < 8; j++) ld_cg_v2(src + 2 * j, r[2 * j], r[2 * j + 1]);
         u64 fp = 0, rf = 0;
-        const unsigned f = t.field[i];
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             fp += rotl64(r[j], j);
-            rf = (j == (int)f) ? r[j] : rf;
+            rf = (j == (int)L.field) ? r[j] : rf;
         }
-        ws.out[i] = fp;
-        if ((t.wmask >> i) & 1) {
-            ws.nf[i] = rf * 0x9E3779B97F4A7C15ull + ((((u64)t.gid) << 4) | (u64)i) + 1ull;
-            ws.n15[i] = r[15] + 1ull;
+        L.out = fp;
+        if (L.w) {
+            L.nf = rf * 0x9E3779B97F4A7C15ull + ((((u64)gid) << 4) | (u64)i) + 1ull;
+            L.n15 = r[15] + 1ull;
         }
     }
 
-    static GC_DEV void install(const YcsbParams &, const Txn &t, int i, u64 *dst, const Ws &ws) {
-        st_cg(dst + t.field[i], ws.nf[i]);
-        st_cg(dst + 15, ws.n15[i]);
+    static GC_DEV void install(const YcsbParams &, const Lane &L, u64 *dst) {
+        st_cg(dst + L.field, L.nf);
+        st_cg(dst + 15, L.n15);
     }
 
     static GC_DEV void copy_row(const u64 *src, u64 *dst) {
@@ -116,55 +139,66 @@ struct YcsbWL {
         }
     }
 
-    static GC_DEV void emit(const ExecParams &p, const YcsbParams &, const Txn &t, const Ws &ws) {
-        if (!p.read_out) return;
-        const u64 base = (u64)t.gid * p.K;
-#pragma unroll
-        for (int i = 0; i < MAXK; i++)
-            if (i < (int)t.n) p.read_out[base + i] = ws.out[i];
+    static GC_DEV void emit(const ExecParams &p, const YcsbParams &, const Lane &L, u32 gid, u32 i) {
+        if (p.read_out) p.read_out[(u64)gid * p.K + i] = L.out;
     }
 };
 
 // ---------------------------------------------------------------- executor launch
 template <int S>
-static cudaError_t launch_one(const ExecParams &p, const YcsbParams &y, int grid, int block,
-                              cudaStream_t s) {
-    exec_kernel<S, YcsbWL><<<grid, block, 0, s>>>(p, y);
+static cudaError_t launch_s(const ExecParams &p, const YcsbParams &y, int grid, int block,
+                            cudaStream_t s) {
+    switch (p.lanes) {
+        case 4: exec_tile_kernel<S, YcsbWL, 4><<<grid, block, 0, s>>>(p, y); break;
+        case 8: exec_tile_kernel<S, YcsbWL, 8><<<grid, block, 0, s>>>(p, y); break;
+        case 16: exec_tile_kernel<S, YcsbWL, 16><<<grid, block, 0, s>>>(p, y); break;
+        default: exec_thread_kernel<S, YcsbWL><<<grid, block, 0, s>>>(p, y); break;
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
                              cudaStream_t s) {
     switch (p.scheme) {
-        case CC_TPL_NW: return launch_one<CC_TPL_NW>(p, y, grid, block, s);
-        case CC_TPL_WD: return launch_one<CC_TPL_WD>(p, y, grid, block, s);
-        case CC_TO: return launch_one<CC_TO>(p, y, grid, block, s);
-        case CC_MVCC: return launch_one<CC_MVCC>(p, y, grid, block, s);
-        case CC_SILO: return launch_one<CC_SILO>(p, y, grid, block, s);
-        case CC_TICTOC: return launch_one<CC_TICTOC>(p, y, grid, block, s);
-        case CC_GPUTX: return launch_one<CC_GPUTX>(p, y, grid, block, s);
-        case CC_GACCO: return launch_one<CC_GACCO>(p, y, grid, block, s);
+        case CC_TPL_NW: return launch_s<CC_TPL_NW>(p, y, grid, block, s);
+        case CC_TPL_WD: return launch_s<CC_TPL_WD>(p, y, grid, block, s);
+        case CC_TO: return launch_s<CC_TO>(p, y, grid, block, s);
+        case CC_MVCC: return launch_s<CC_MVCC>(p, y, grid, block, s);
+        case CC_SILO: return launch_s<CC_SILO>(p, y, grid, block, s);
+        case CC_TICTOC: return launch_s<CC_TICTOC>(p, y, grid, block, s);
+        case CC_GPUTX: return launch_s<CC_GPUTX>(p, y, grid, block, s);
+        case CC_GACCO: return launch_s<CC_GACCO>(p, y, grid, block, s);
     }
     return cudaErrorInvalidValue;
 }
 
-template <int S>
-static int occ_one(int block) {
+template <class F>
+static int occ_of(F f, int block) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, exec_kernel<S, YcsbWL>, block, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, block, 0);
     return nb;
 }
 
-int ycsb_exec_max_blocks_per_sm(int scheme, int block) {
+template <int S>
+static int occ_s(int lanes, int block) {
+    switch (lanes) {
+        case 4: return occ_of(exec_tile_kernel<S, YcsbWL, 4>, block);
+        case 8: return occ_of(exec_tile_kernel<S, YcsbWL, 8>, block);
+        case 16: return occ_of(exec_tile_kernel<S, YcsbWL, 16>, block);
+        default: return occ_of(exec_thread_kernel<S, YcsbWL>, block);
+    }
+}
+
+int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block) {
     switch (scheme) {
-        case CC_TPL_NW: return occ_one<CC_TPL_NW>(block);
-        case CC_TPL_WD: return occ_one<CC_TPL_WD>(block);
-        case CC_TO: return occ_one<CC_TO>(block);
-        case CC_MVCC: return occ_one<CC_MVCC>(block);
-        case CC_SILO: return occ_one<CC_SILO>(block);
-        case CC_TICTOC: return occ_one<CC_TICTOC>(block);
-        case CC_GPUTX: return occ_one<CC_GPUTX>(block);
-        case CC_GACCO: return occ_one<CC_GACCO>(block);
+        case CC_TPL_NW: return occ_s<CC_TPL_NW>(lanes, block);
+        case CC_TPL_WD: return occ_s<CC_TPL_WD>(lanes, block);
+        case CC_TO: return occ_s<CC_TO>(lanes, block);
+        case CC_MVCC: return occ_s<CC_MVCC>(lanes, block);
+        case CC_SILO: return occ_s<CC_SILO>(lanes, block);
+        case CC_TICTOC: return occ_s<CC_TICTOC>(lanes, block);
+        case CC_GPUTX: return occ_s<CC_GPUTX>(lanes, block);
+        case CC_GACCO: return occ_s<CC_GACCO>(lanes, block);
     }
     return 0;
 }
@@ -174,26 +208,23 @@ int ycsb_exec_max_blocks_per_sm(int scheme, int block) {
 // keys (rec << 27) | (gid << 6) | (i << 1) | is_write.
 __global__ void ycsb_gather_kernel(ExecParams p, YcsbParams y, uint32_t *acc_rec,
                                    unsigned long long *keys_out) {
-    const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= p.n_txn) return;
-    YcsbWL::Txn t;
-    ExecParams q = p;
-    q.acc_rec = nullptr;
-    if (!YcsbWL::load(q, y, gid, t)) {
-        atomicCAS(&p.ctl->err, 0ull, (u64)CC_ERR_KEY_NOT_FOUND);
+    const u64 a = (u64)blockIdx.x * blockDim.x + threadIdx.x;   // one thread per access
+    if (a >= (u64)p.n_txn * p.K) return;
+    const u32 gid = (u32)(a / p.K), i = (u32)(a % p.K);
+    const u64 r = YcsbWL::lookup(y, y.keys[a]);
+    if (r == ~0ull) {
+        atomicCAS(&p.ctl->err.v, 0ull, (u64)CC_ERR_KEY_NOT_FOUND);
         return;
     }
-    const u64 base = (u64)gid * p.K;
-    for (u32 i = 0; i < p.K; i++) {
-        acc_rec[base + i] = t.rec[i];
-        keys_out[base + i] = ((u64)t.rec[i] << 27) | ((u64)gid << 6) | ((u64)i << 1) | ((t.wmask >> i) & 1u);
-    }
+    acc_rec[a] = (uint32_t)r;
+    keys_out[a] = (r << 27) | ((u64)gid << 6) | ((u64)i << 1) | (u64)(y.ops[a] >> 7);
 }
 
 cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBufs &b,
                                cudaStream_t s) {
     const int blk = 256;
-    ycsb_gather_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(p, y, b.acc_rec, b.keys_in);
+    const u64 n = (u64)p.n_txn * p.K;
+    ycsb_gather_kernel<<<(unsigned)((n + blk - 1) / blk), blk, 0, s>>>(p, y, b.acc_rec, b.keys_in);
     return cudaGetLastError();
 }
 
@@ -239,7 +270,7 @@ __global__ void ycsb_gen_kernel(uint32_t *keys, uint8_t *ops, uint32_t n_txn, ui
     for (u32 i = 0; i < K; i++) {
         for (u64 k = 0;; k++) {
             if (k >= (1u << 24)) {
-                atomicCAS(&ctl->err, 0ull, (u64)CC_ERR_CONFIG);
+                atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_CONFIG);
                 return;
             }
             const u64 u = rng3(seed, gid, (1ull << 56) | ((u64)i << 24) | k);

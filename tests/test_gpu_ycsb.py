@@ -50,12 +50,13 @@ def test_a1_generator_bitexact(c1, orc, seed):
     b.free()
 
 
-CORNERS = [(0, 32), (5, 1), (0, 1), (5, 32), (2, 8)]
+# (wd, bs, lanes): thread mode corners of the paper's launch grid + tile modes
+CORNERS = [(0, 32, 1), (5, 1, 1), (0, 1, 1), (5, 32, 1), (2, 8, 1), (0, 32, 4), (0, 8, 8), (0, 32, 16)]
 
 
 @pytest.mark.parametrize("scheme", SCHEMES)
-@pytest.mark.parametrize("wd,bs", CORNERS)
-def test_c1_parity(c1, orc, scheme, wd, bs):
+@pytest.mark.parametrize("wd,bs,lanes", CORNERS)
+def test_c1_parity(c1, orc, scheme, wd, bs, lanes):
     db, S0 = c1
     T = inputs.zipf_thresholds(1024, 0.8)
     A = inputs.scramble_mult(1024)
@@ -63,7 +64,7 @@ def test_c1_parity(c1, orc, scheme, wd, bs):
         b = db.gen_ycsb(1024, 4, 0.5, seed, T, A)
         keys, ops = orc.ycsb_gen(seed, 1024, 1024, 4, 0.5, T, A)
         db.snapshot(False)
-        res = db.submit(b, scheme, wd=wd, bs=bs)
+        res = db.submit(b, scheme, wd=wd, bs=bs, lanes=lanes)
         st = db.sync()
         assert st.commits == 1024
         h = res.host()
@@ -74,8 +75,9 @@ def test_c1_parity(c1, orc, scheme, wd, bs):
         b.free()
 
 
+@pytest.mark.parametrize("lanes", [1, 4])
 @pytest.mark.parametrize("scheme", SCHEMES)
-def test_immediate_retry_mode(c1, orc, scheme):
+def test_immediate_retry_mode(c1, orc, scheme, lanes):
     from paper_2406_10158_b200.gcctb import CC_FLAG_IMMEDIATE_RETRY
     db, S0 = c1
     T = inputs.zipf_thresholds(1024, 0.8)
@@ -83,14 +85,15 @@ def test_immediate_retry_mode(c1, orc, scheme):
     b = db.gen_ycsb(1024, 4, 0.5, 9, T, A)
     keys, ops = orc.ycsb_gen(9, 1024, 1024, 4, 0.5, T, A)
     db.snapshot(False)
-    res = db.submit(b, scheme, wd=0, bs=32, flags=CC_FLAG_IMMEDIATE_RETRY)
+    res = db.submit(b, scheme, wd=0, bs=32, flags=CC_FLAG_IMMEDIATE_RETRY, lanes=lanes)
     db.sync()
     orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(), db.read_table(0))
     b.free()
 
 
+@pytest.mark.parametrize("lanes", [1, 4])
 @pytest.mark.parametrize("scheme", SCHEMES)
-def test_read_only_never_aborts(c1, orc, scheme):
+def test_read_only_never_aborts(c1, orc, scheme, lanes):
     """RO preset: no scheme aborts, state unchanged."""
     db, S0 = c1
     T = inputs.zipf_thresholds(1024, 0.99)
@@ -98,7 +101,7 @@ def test_read_only_never_aborts(c1, orc, scheme):
     b = db.gen_ycsb(1024, 4, 0.0, 3, T, A)
     keys, ops = orc.ycsb_gen(3, 1024, 1024, 4, 0.0, T, A)
     db.snapshot(False)
-    res = db.submit(b, scheme, wd=5, bs=32)
+    res = db.submit(b, scheme, wd=5, bs=32, lanes=lanes)
     st = db.sync()
     assert st.aborts == 0
     h = res.host()
@@ -119,7 +122,8 @@ def test_brute_force_tiny(c1, orc, scheme):
         keys, ops = inputs.random_batch(int(rng.integers(1 << 30)), n, k, 1024, 0.5, hot=5)
         b = db.import_ycsb(keys, ops, k)
         db.snapshot(False)
-        res = db.submit(b, scheme, wd=int(rng.integers(0, 6)), bs=int(rng.integers(1, 5)))
+        lanes = [1, 4][it % 2]
+        res = db.submit(b, scheme, wd=int(rng.integers(0, 6)), bs=int(rng.integers(1, 5)), lanes=lanes)
         db.sync()
         h = res.host()
         after = db.read_table(0)
@@ -155,10 +159,12 @@ def c2(torch_cuda, orc):
     db.close()
 
 
-@pytest.mark.parametrize("theta", [0.8, 0.99])
+@pytest.mark.parametrize("lanes", [1, 16])
+@pytest.mark.parametrize("theta", [0.6, 0.99])
 @pytest.mark.parametrize("scheme", SCHEMES)
-def test_c2_full_size_parity(c2, orc, scheme, theta):
-    """Full-size parity in the bench launch configuration (wd=0, bs=32 default)."""
+def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
+    """Full-size parity in the bench launch configurations (thread mode wd=0, bs=32 and
+    tile mode 16 lanes)."""
     db, S0, n = c2
     T = inputs.zipf_thresholds(n, theta)
     A = inputs.scramble_mult(n)
@@ -168,7 +174,7 @@ def test_c2_full_size_parity(c2, orc, scheme, theta):
     k2, o2 = b.export_ycsb()
     assert np.array_equal(keys, k2) and np.array_equal(ops, o2)
     db.snapshot(False)
-    res = db.submit(b, scheme, wd=0, bs=32)
+    res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes)
     st = db.sync()
     assert st.commits == B
     orc.check_ycsb(scheme, S0, keys, ops, K, res.host(), db.read_table(0))
