@@ -210,8 +210,8 @@ def run_ours(args, rank, world, local):
     db.load_ycsb(args.rows, 1 + rank)
     T = torch.from_numpy(inputs.zipf_thresholds(args.rows, args.theta).view(np.int64)).to(dev)
     A = inputs.scramble_mult(args.rows)
-    res = {s: Result.alloc(args.batch, args.ops, dev) for s in schemes}
-    stream = torch.cuda.current_stream(dev)
+    res = {s: Result.alloc(args.batch, args.ops, dev, stream=db.stream) for s in schemes}
+    stream = db.stream   # every library launch goes to this stream; events are recorded on it
 
     def step(i, timing=False):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
@@ -251,7 +251,7 @@ def run_ours(args, rank, world, local):
     per = {}
     last = batches[-1]
     for s in schemes:
-        h = res[s].stats.cpu().numpy().view(np.uint64)
+        h = res[s].stats.cpu().numpy().view(np.uint64)   # after db.sync()
         per[s] = {"commits": int(h[0]), "aborts": int(h[1]), "abort_rate": float(h[1]) / max(1, int(h[0]))}
         assert int(h[0]) == args.batch, (s, int(h[0]))
     keys, ops = last.export_ycsb()
@@ -355,12 +355,13 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world):
 
     def one():
         b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
-        for s in schemes:
-            db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes)
-            c, p_, r = outs[s]
-            c.copy_(res[s].committed, non_blocking=True)
-            p_.copy_(res[s].commit_pos, non_blocking=True)
-            r.copy_(res[s].read_out, non_blocking=True)
+        with torch.cuda.stream(stream):
+            for s in schemes:
+                db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes)
+                c, p_, r = outs[s]
+                c.copy_(res[s].committed, non_blocking=True)
+                p_.copy_(res[s].commit_pos, non_blocking=True)
+                r.copy_(res[s].read_out, non_blocking=True)
         db.sync()
         b.free()
 

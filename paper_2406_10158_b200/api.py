@@ -22,7 +22,12 @@ class Result:
     stats: torch.Tensor
 
     @staticmethod
-    def alloc(n_txn: int, K: int, device, read_out=True) -> "Result":
+    def alloc(n_txn: int, K: int, device, read_out=True, stream=None) -> "Result":
+        """Allocate on `stream` (the db's stream) so the zero-fill is ordered before
+        the library's kernels on that stream."""
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                return Result.alloc(n_txn, K, device, read_out)
         z = dict(device=device)
         return Result(
             committed=torch.zeros(n_txn, dtype=torch.uint8, **z),
@@ -39,7 +44,9 @@ class Result:
         return G.cc_result(p(self.committed), p(self.restarts), p(self.order_hi), p(self.order_lo),
                            p(self.commit_pos), p(self.read_out), p(self.stats))
 
-    def host(self) -> dict:
+    def host(self, stream=None) -> dict:
+        if stream is not None:
+            stream.synchronize()
         u = lambda t: t.cpu().numpy()  # noqa: E731
         d = {
             "committed": u(self.committed),
@@ -76,10 +83,16 @@ class Batch:
 
 
 class DB:
+    """One db on one device.  All library work runs on ``self.stream`` (an explicit
+    torch stream, never the legacy default stream, which would make the library create
+    an unordered stream of its own).  Result buffers are allocated on it; callers that
+    touch results with torch ops must use ``with torch.cuda.stream(db.stream)`` or
+    synchronise first (``sync()``)."""
+
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1):
         L = G.lib()
-        if stream is None:
-            stream = torch.cuda.current_stream(device)
+        if stream is None or stream.cuda_stream == 0:
+            stream = torch.cuda.Stream(device)
         self.stream = stream
         self.device = device
         d = G.cc_db_desc(device, ctypes.c_void_p(stream.cuda_stream), rank, world)
@@ -112,6 +125,7 @@ class DB:
     def gen_ycsb(self, n_txn: int, K: int, W: float, seed: int, thresholds, mult: int) -> Batch:
         """thresholds: torch uint64/int64 cuda tensor or numpy uint64 array."""
         if isinstance(thresholds, torch.Tensor):
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
             ptr, on_dev = thresholds.data_ptr(), 1
             keep = thresholds
         else:
@@ -126,6 +140,7 @@ class DB:
     def import_ycsb(self, keys, ops, K: int) -> Batch:
         h = ctypes.c_void_p()
         if isinstance(keys, torch.Tensor):
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
             st = G.lib().cc_batch_import_ycsb(self.h, keys.data_ptr(), ops.data_ptr(),
                                               keys.numel() // K, K, 1, ctypes.byref(h))
         else:
@@ -155,7 +170,8 @@ class DB:
                read_out=True, lanes: int = 1) -> Result:
         sid = G.SCHEME_ID[scheme] if isinstance(scheme, str) else int(scheme)
         if result is None:
-            result = Result.alloc(batch.n_txn, batch.K, torch.device("cuda", self.device), read_out)
+            result = Result.alloc(batch.n_txn, batch.K, torch.device("cuda", self.device), read_out,
+                                  stream=self.stream)
         d = G.cc_exec_desc(sid, wd, bs, flags, grid, lanes, watchdog_s)
         r = result.c()
         self._chk(G.lib().cc_submit(self.h, batch.h, ctypes.byref(d), ctypes.byref(r)))

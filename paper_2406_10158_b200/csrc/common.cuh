@@ -72,6 +72,7 @@ GC_DEV u32 atom_add_release32(u32 *p, u32 v) {
     return old;
 }
 GC_DEV void fence_acqrel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+GC_DEV void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
 
 // Row payload access through L2 (coherent point), 16 B vectors.
 GC_DEV void ld_cg_v2(const u64 *p, u64 &a, u64 &b) {

@@ -403,8 +403,7 @@ static cc_status ensure_scratch(cc_db db, uint32_t n_txn, uint64_t n_acc) {
     CUDA_TRY(db, dalloc(&db->restarts, (size_t)nt * 4));
     CUDA_TRY(db, dalloc(&db->ohi, (size_t)nt * 8));
     CUDA_TRY(db, dalloc(&db->olo, (size_t)nt * 8));
-    uint32_t cap = 1024;
-    while (cap < 2 * nt) cap <<= 1;
+    const uint32_t cap = nt;   // each id is appended to the retry batch at most once
     CUDA_TRY(db, dalloc(&db->ring, (size_t)cap * 8));
     db->ring_cap = cap;
     PrepBufs &b = db->prep;

@@ -9,14 +9,12 @@
 //    in parallel; commit / abort / wait decisions are tile ballots (vote.any/all), the
 //    warp-level structure the north star asks for.  Same protocols, same order keys.
 //
-// Queue (a6): lanes (or tile leaders) claim fresh ids in increasing order from a
-// device ticket.  An aborted attempt releases its CC state, bumps restarts[gid],
-// backs off, and -- while fresh ids remain -- appends gid to a bounded MPMC retry
-// ring (warp-aggregated append) and claims new work; once fresh ids are exhausted the
-// worker re-runs its own transaction.  Workers take retry-ring entries
-// before fresh ids and exit when both are empty, so no lane ever polls for work that
-// does not exist.  Every transaction a worker waits on has a smaller id or is held by
-// a running worker, so nothing waits on an unscheduled block.
+// Queue (a6): round 1 claims fresh ids in increasing order from a device ticket; an
+// abort while fresh ids remain releases the CC state, bumps restarts[gid], backs off
+// and compacts gid into the retry batch; round 2 drains that batch once it is sealed;
+// aborts after that retry in place.  Every transaction a worker waits
+// on has a smaller id or is held by a running worker, so nothing waits on an
+// unscheduled block.
 #pragma once
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
@@ -83,51 +81,62 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
 }
 
 // ------------------------------------------------------------------ queue (a6)
-// Retry ring: bounded MPMC of (seq << 32 | gid) slots; slot r of the retry sequence
-// lives at ring[r & (cap-1)]; its consumer clears it after reading.
-GC_DEV void ring_push_one(Th &th, u64 r, u32 gid) {
+// Round 1 is the fresh batch, claimed in increasing id.  While fresh ids remain, an
+// aborted transaction is compacted into the retry batch (`ring`, appended with one
+// atomic per converged group); each id is appended at most once before the fresh ids
+// run out, so n_txn slots always suffice.  When a worker finds the fresh ids exhausted
+// it seals the retry batch -- it waits until no append is in flight, then every later
+// append attempt sees the exhaustion and retries in place -- and round 2 consumes the
+// sealed batch with one atomicAdd per claim.  Aborts after exhaustion retry in place
+// after their backoff.  Workers exit when both rounds are drained: no worker ever
+// polls for work that may not exist.
+GC_DEV bool try_append_retry(Th &th, u32 gid) {
     const ExecParams &p = *th.p;
-    u64 *slot = p.ring + (r & (p.ring_cap - 1));
-    Spin sp;
-    while (ld_relaxed(slot) != 0)   // previous lap not consumed yet
-        if (!sp.wait(th)) return;
-    st_release(slot, (((r + 1) & 0xFFFFFFFFull) << 32) | gid);
+    Ctl *c = p.ctl;
+    atomicAdd(&c->inflight.v, 1ull);
+    fence_sc();   // Dekker pair with the sealer: one of us sees the other
+    bool ok = false;
+    if (ld_relaxed(&c->head.v) < p.n_txn) {
+        const u64 r = atomicAdd(&c->tail.v, 1ull);
+        st_relaxed(p.ring + r, (u64)gid);
+        ok = true;
+    }
+    fence_acqrel();
+    atomicAdd(&c->inflight.v, (u64)-1ll);
+    return ok;
 }
 
-// Claim work for one worker: the oldest retry-ring entry, else a fresh id, else NO_TXN.
+struct Claim {
+    bool exhausted = false;
+    bool sealed = false;
+    u64 tail = 0;
+};
+
+// Claim work for one worker: a fresh id, else a retry-batch entry, else NO_TXN.
 template <int S>
-GC_DEV u32 claim_work(Th &th, bool &fresh_exhausted) {
+GC_DEV u32 claim_work(Th &th, Claim &cl) {
     const ExecParams &p = *th.p;
     Ctl *c = p.ctl;
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
-    if (!DET) {
-        for (;;) {
-            const u64 r = ld_relaxed(&c->rhead.v);
-            const u64 t = ld_acquire(&c->tail.v);
-            if (r >= t) break;
-            if (atomicCAS(&c->rhead.v, r, r + 1) != r) continue;
-            u64 *slot = p.ring + (r & (p.ring_cap - 1));
-            const u64 want = (r + 1) & 0xFFFFFFFFull;
-            Spin sp;
-            for (;;) {
-                const u64 v = ld_acquire(slot);
-                if ((v >> 32) == want) {
-                    st_relaxed(slot, 0ull);
-                    return (u32)v;
-                }
-                if (!sp.wait(th)) return NO_TXN;
-            }
-        }
-    }
-    if (!fresh_exhausted) {
+    if (!cl.exhausted) {
         const u64 s = atomicAdd(&c->head.v, 1ull);
         if (s < p.n_txn) return (S == CC_GPUTX) ? p.rank_order[s] : (u32)s;
-        fresh_exhausted = true;
+        cl.exhausted = true;
     }
-    return NO_TXN;
+    if (DET || (p.flags & CC_FLAG_IMMEDIATE_RETRY)) return NO_TXN;
+    if (!cl.sealed) {
+        fence_sc();
+        Spin sp;
+        while (ld_acquire(&c->inflight.v) != 0)
+            if (!sp.wait(th)) return NO_TXN;
+        cl.tail = ld_acquire(&c->tail.v);
+        cl.sealed = true;
+    }
+    if (cl.tail == 0 || ld_relaxed(&c->rhead.v) >= cl.tail) return NO_TXN;
+    const u64 r = atomicAdd(&c->rhead.v, 1ull);
+    if (r >= cl.tail) return NO_TXN;
+    return (u32)ld_relaxed(p.ring + r);
 }
-
-GC_DEV bool fresh_left(const ExecParams &p) { return ld_relaxed(&p.ctl->head.v) < p.n_txn; }
 
 // ------------------------------------------------------------------ 2PL (Table II)
 // word = [62] shared | [61:31] holder count | [30:0] holder (wait-die: min age of the
@@ -147,7 +156,7 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 template <bool WD>
 GC_DEV int tpl_try(u64 *w, bool ex, u32 age) {
     u64 v = ld_relaxed(w);
-    for (int k = 0; k < 4; k++) {
+    for (;;) {   // latch-free read-transform-CAS loop
         const u32 cnt = tpl_cnt(v);
         bool conflict;
         u64 nv;
@@ -167,7 +176,6 @@ GC_DEV int tpl_try(u64 *w, bool ex, u32 age) {
         if (old == v) return 0;
         v = old;
     }
-    return 1;
 }
 
 GC_DEV void tpl_release_relaxed(u64 *w, bool ex) {
@@ -202,7 +210,7 @@ GC_DEV u64 tt_wts(u64 v) { return v & M48; }
 GC_DEV u64 tt_rts(u64 v) { return (v & M48) + ((v >> 48) & DMAX); }
 
 // Per-access step outcomes used by both modes
-enum { ST_DONE = 0, ST_WAIT = 1, ST_ABORT = 2 };
+enum { ST_DONE = 0, ST_WAIT = 1, ST_ABORT = 2, ST_RETRY = 3 };   // RETRY: lost a CAS race, go again at once
 
 // TO access step for one item (write = read-modify-write).  On success for a write the
 // row is read under the pending bit; for a read it is read between two word loads.
@@ -215,7 +223,7 @@ GC_DEV int to_step(const ExecParams &p, const typename WL::Params &y, typename W
     if (L.w) {
         if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;   // older pending: wait (Z4)
         if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
-        if (cas_acqrel(w, v, to_make(true, to_rts(v), ts)) != v) return ST_WAIT;
+        if (cas_acqrel(w, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
         pend = true;
         saved = v;
         WL::read(y, L, gid, i, row);   // stable: we own the pending bit
@@ -225,8 +233,8 @@ GC_DEV int to_step(const ExecParams &p, const typename WL::Params &y, typename W
     if (v & TO_P) return ST_WAIT;
     WL::read(y, L, gid, i, row);
     fence_acqrel();
-    if (to_rts(v) >= ts) return ld_relaxed(w) == v ? ST_DONE : ST_WAIT;
-    return cas_acqrel(w, v, to_make(false, ts, to_wts(v))) == v ? ST_DONE : ST_WAIT;
+    if (to_rts(v) >= ts) return ld_relaxed(w) == v ? ST_DONE : ST_RETRY;
+    return cas_acqrel(w, v, to_make(false, ts, to_wts(v))) == v ? ST_DONE : ST_RETRY;
 }
 
 template <class WL>
@@ -247,7 +255,7 @@ GC_DEV int mvcc_step(const ExecParams &p, const typename WL::Params &y, typename
     if (L.w) {
         if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;
         if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
-        if (cas_acqrel(lo, v, to_make(true, to_rts(v), ts)) != v) return ST_WAIT;
+        if (cas_acqrel(lo, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
         pend = true;
         saved_wts = to_wts(v);
         WL::read(y, L, gid, i, row);
@@ -258,10 +266,10 @@ GC_DEV int mvcc_step(const ExecParams &p, const typename WL::Params &y, typename
     if ((h >> 32) <= ts) {   // head visible: read in place, validate, raise RTS
         WL::read(y, L, gid, i, row);
         fence_acqrel();
-        if (ld_relaxed(hi) != h) return ST_WAIT;
-        if (to_rts(v) >= ts) return ld_relaxed(lo) == v ? ST_DONE : ST_WAIT;
+        if (ld_relaxed(hi) != h) return ST_RETRY;
+        if (to_rts(v) >= ts) return ld_relaxed(lo) == v ? ST_DONE : ST_RETRY;
         const u64 nv = (v & ~(M31 << 31)) | ((ts & M31) << 31);
-        return cas_acqrel(lo, v, nv) == v ? ST_DONE : ST_WAIT;
+        return cas_acqrel(lo, v, nv) == v ? ST_DONE : ST_RETRY;
     }
     // walk the history chain for the newest version with begin <= ts
     u64 idx = h & VNONE;
@@ -316,7 +324,7 @@ GC_DEV int occ_snap_step(const ExecParams &p, const typename WL::Params &y, type
     if (v1 & LOCKB) return ST_WAIT;
     WL::read(y, L, gid, i, WL::row(y, L));
     fence_acqrel();
-    if (ld_relaxed(w) != v1) return ST_WAIT;
+    if (ld_relaxed(w) != v1) return ST_RETRY;
     obs = v1;
     return ST_DONE;
 }
@@ -406,6 +414,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
                 if (pend) pendm |= 1u << i;
                 if (st == ST_DONE) break;
                 if (st == ST_ABORT) { r = RES_ABORT; break; }
+                if (st == ST_RETRY) continue;
                 if (!sp.wait(th)) { r = RES_FATAL; break; }
             }
         }
@@ -429,8 +438,9 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         u64 obs[WL::MAXK], pre[WL::MAXK];
         for (u32 i = 0; i < n; i++) {
             Spin sp;
-            while (occ_snap_step<WL>(p, y, L[i], gid, i, obs[i]) != ST_DONE)
-                if (!sp.wait(th)) return RES_FATAL;
+            int st;
+            while ((st = occ_snap_step<WL>(p, y, L[i], gid, i, obs[i])) != ST_DONE)
+                if (st == ST_WAIT && !sp.wait(th)) return RES_FATAL;
         }
         u32 locked = 0;
         bool ok = true;
@@ -525,9 +535,9 @@ __global__ void __launch_bounds__(1024) exec_thread_kernel(ExecParams p, typenam
     th.polls = 0;
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L[WL::MAXK];
-    bool exhausted = false;
+    Claim cl;
     for (;;) {
-        const u32 gid = claim_work<S>(th, exhausted);
+        const u32 gid = claim_work<S>(th, cl);
         if (gid == NO_TXN) return;
         const u32 n = WL::load_all(p, y, gid, L);
         if (n == 0xFFFFFFFFu) {
@@ -548,10 +558,7 @@ __global__ void __launch_bounds__(1024) exec_thread_kernel(ExecParams p, typenam
             const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
             p.restarts[gid] = nr;
             abort_backoff(gid, nr);
-            if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && fresh_left(p)) {
-                ring_push_one(th, agg_fetch_add(&p.ctl->tail.v), gid);   // compaction (a6)
-                break;
-            }
+            if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) break;   // a6
         }
     }
 }
@@ -618,6 +625,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 return RES_ABORT;
             }
             if (tile.all(done)) break;
+            if (tile.any(st == ST_RETRY)) continue;   // lost a CAS race: go again at once
             if (tile.any(!sp.wait(th))) {
                 if (pend) {
                     if (S == CC_TO) st_release(&p.meta[L.rec], saved);
@@ -638,8 +646,13 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         bool done = !act;
         Spin sp;
         for (;;) {   // read phase
-            if (!done) done = occ_snap_step<WL>(p, y, L, gid, li, obs) == ST_DONE;
+            int st = ST_DONE;
+            if (!done) {
+                st = occ_snap_step<WL>(p, y, L, gid, li, obs);
+                done = st == ST_DONE;
+            }
             if (tile.all(done)) break;
+            if (tile.any(st == ST_RETRY)) continue;
             if (tile.any(!sp.wait(th))) return RES_FATAL;
         }
         bool locked = false, bad = false;
@@ -735,10 +748,10 @@ __global__ void __launch_bounds__(1024) exec_tile_kernel(ExecParams p, typename 
     th.polls = 0;
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L;
-    bool exhausted = false;
+    Claim cl;
     for (;;) {
         u32 gid = NO_TXN;
-        if (li == 0) gid = claim_work<S>(th, exhausted);
+        if (li == 0) gid = claim_work<S>(th, cl);
         gid = tile.shfl(gid, 0);
         if (gid == NO_TXN) return;
         const bool ok = WL::load_lane(p, y, gid, li, L);
@@ -764,8 +777,7 @@ __global__ void __launch_bounds__(1024) exec_tile_kernel(ExecParams p, typename 
                 const u32 nr = p.restarts[gid] + 1;
                 p.restarts[gid] = nr;
                 abort_backoff(gid, nr);
-                push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && fresh_left(p);
-                if (push) ring_push_one(th, atomicAdd(&p.ctl->tail.v, 1ull), gid);
+                push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
             }
             if (tile.shfl(push, 0)) break;
         }

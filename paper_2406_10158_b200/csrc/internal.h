@@ -25,6 +25,7 @@ struct Ctl {
     Counter aborts;     // sum of restarts (counted at emission)
     Counter max_rank;   // GPUTx: number of K-sets - 1
     Counter rank_head;  // GPUTx rank-pass claim counter
+    Counter inflight;   // retry-batch appends in flight (sealing protocol)
 };
 
 enum { KIND_YCSB = 1, KIND_TPCC = 2 };
@@ -41,8 +42,8 @@ struct ExecParams {
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
     unsigned long long *arena;   // MVCC version nodes
-    unsigned long long *ring;    // retry queue
-    uint32_t ring_cap;           // power of two
+    unsigned long long *ring;    // retry batch (compacted aborted ids), n_txn slots
+    uint32_t ring_cap;
     // per-transaction internal results
     uint8_t *committed;
     uint32_t *restarts;

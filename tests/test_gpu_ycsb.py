@@ -67,7 +67,7 @@ def test_c1_parity(c1, orc, scheme, wd, bs, lanes):
         res = db.submit(b, scheme, wd=wd, bs=bs, lanes=lanes)
         st = db.sync()
         assert st.commits == 1024
-        h = res.host()
+        h = res.host(db.stream)
         assert int(h["restarts"].astype(np.int64).sum()) == st.aborts
         orc.check_ycsb(scheme, S0, keys, ops, 4, h, db.read_table(0))
         if scheme == "gputx":
@@ -87,7 +87,7 @@ def test_immediate_retry_mode(c1, orc, scheme, lanes):
     db.snapshot(False)
     res = db.submit(b, scheme, wd=0, bs=32, flags=CC_FLAG_IMMEDIATE_RETRY, lanes=lanes)
     db.sync()
-    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(), db.read_table(0))
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
     b.free()
 
 
@@ -104,7 +104,7 @@ def test_read_only_never_aborts(c1, orc, scheme, lanes):
     res = db.submit(b, scheme, wd=5, bs=32, lanes=lanes)
     st = db.sync()
     assert st.aborts == 0
-    h = res.host()
+    h = res.host(db.stream)
     orc.check_ycsb(scheme, S0, keys, ops, 4, h, db.read_table(0))
     assert np.array_equal(db.read_table(0), S0)
     b.free()
@@ -125,7 +125,7 @@ def test_brute_force_tiny(c1, orc, scheme):
         lanes = [1, 4][it % 2]
         res = db.submit(b, scheme, wd=int(rng.integers(0, 6)), bs=int(rng.integers(1, 5)), lanes=lanes)
         db.sync()
-        h = res.host()
+        h = res.host(db.stream)
         after = db.read_table(0)
         orc.check_ycsb(scheme, S0, keys, ops, k, h, after)
         outs = orc.ycsb_serial_outcomes(S0[:5].copy(), keys, ops, k, list(range(n)))
@@ -177,5 +177,5 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes)
     st = db.sync()
     assert st.commits == B
-    orc.check_ycsb(scheme, S0, keys, ops, K, res.host(), db.read_table(0))
+    orc.check_ycsb(scheme, S0, keys, ops, K, res.host(db.stream), db.read_table(0))
     b.free()
