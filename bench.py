@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--write-frac", type=float, default=0.1)
     ap.add_argument("--wd", type=int, default=0)          # paper launch wd=0, bs=32
     ap.add_argument("--bs", type=int, default=32)
-    ap.add_argument("--lanes", type=int, default=1)       # 1 = thread per txn; 4/8/16 = tile mode
+    ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

