@@ -196,7 +196,7 @@ def test_ts_overflow_is_reported(c1):
     ops = np.full(keys.size, 0x81, np.uint8)
     b = db.import_ycsb(keys, ops, 4)
     db.snapshot(False)
-    res = db.submit(b, "to", wd=5, bs=32, watchdog_s=20)
+    res = db.submit(b, "to", wd=5, bs=32, watchdog_s=5)
     try:
         st = db.sync()
         assert st.commits == 1024    # finished before overflow: must then be correct
