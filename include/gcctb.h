@@ -152,6 +152,43 @@ cc_status cc_batch_info(cc_db db, cc_batch b, uint32_t *n_txn, uint32_t *ops_per
                         uint32_t *kind);
 cc_status cc_batch_free(cc_db db, cc_batch b);
 
+/* ----------------------------------------------------------------- TPC-C
+ * TPC-C NewOrder + Payment.  Creates, in this order, the CC-managed
+ * tables WAREHOUSE, DISTRICT, CUSTOMER, STOCK for warehouses [w_first, w_first+w_count)
+ * of `warehouses` (record ids consecutive), the immutable ITEM table
+ * (outside CC, Z16), the reserved-slot tables ORDER, NEW_ORDER, ORDER_LINE (15 per
+ * transaction), HISTORY for max_txn transactions (inserts become private slot writes,
+ * Z15), and the immutable customer last-name index.  Population per TPC-C §4.3.3 from
+ * `seed` (row layouts: inputs/tpcc.py), generated on the device. */
+typedef struct {
+    uint32_t warehouses;   /* total W */
+    uint32_t w_first;      /* first warehouse held by this db (partitioning), 0 for 1 GPU */
+    uint32_t w_count;      /* warehouses held (w_count = warehouses for 1 GPU) */
+    uint32_t max_txn;      /* capacity of the reserved-slot tables */
+    uint64_t seed;
+} cc_tpcc_db_desc;
+cc_status cc_load_tpcc(cc_db db, const cc_tpcc_db_desc *desc);
+
+/* Table ids of the TPC-C tables: ids[0..8] = W, D, C, S, I, O, NO, OL, H. */
+cc_status cc_tpcc_tables(cc_db db, uint32_t ids[9]);
+
+/* On-device TPC-C generator: NewOrder with probability
+ * neworder_permyriad/10,000 (else Payment), home warehouse uniform in [w_lo, w_hi),
+ * TPC-C §2.4.1 / §2.5.1 inputs (NURand customers/items/last names, 1% remote supply,
+ * 15% remote Payment, 60% by name), NewOrder lines distinct and sorted by stock key.
+ * Transaction descriptors are 40 x u32. */
+typedef struct {
+    uint32_t n_txn;
+    uint32_t neworder_permyriad;
+    uint64_t seed;
+    uint32_t w_lo, w_hi;
+} cc_tpcc_gen_desc;
+cc_status cc_batch_gen_tpcc(cc_db db, const cc_tpcc_gen_desc *g, cc_batch *out);
+/* Import / export TPC-C descriptors (u32[n_txn*40]). */
+cc_status cc_batch_import_tpcc(cc_db db, const uint32_t *tx, uint32_t n_txn, int src_on_device,
+                               cc_batch *out);
+cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
+
 /* ------------------------------------------------------------ execution */
 #define CC_FLAG_IMMEDIATE_RETRY 0x1u /* paper mode: the worker re-runs its own aborted
                                         transaction at once instead of
@@ -168,7 +205,8 @@ typedef struct {
     uint32_t lanes_per_txn; /* 0/1: one lane per transaction (the paper's model, wd and bs
                                apply); 4/8/16: a tile of that many lanes runs one
                                transaction, lane i owning access i (must be >= ops per
-                               transaction; wd is ignored) */
+                               transaction; wd is ignored).  TPC-C batches use 32-lane
+                               tiles for any value > 1 */
     double watchdog_s;      /* device watchdog in seconds (0 = 30 s) */
 } cc_exec_desc;
 
@@ -179,7 +217,9 @@ typedef struct {
  *   order_hi/lo u64[n] the scheme's serialization-order key;
  *                     ascending (hi, lo) is a valid serial order of the committed set
  *   commit_pos u32[n] dense position of the transaction in that order
- *   read_out  u64[n*K] per-op value read (YCSB: fingerprint of the row read)
+ *   read_out  u64[n*K] per-op value read (YCSB: fingerprint of the row read);
+ *             TPC-C: u64[n*48] per transaction (NewOrder: o_id, total, then per line
+ *             s_quantity before, 'B'/'G', ol_amount; Payment: c_id, c_balance, c_credit)
  *   stats     u64[CC_STATS_WORDS] device counters (see cc_stats)               */
 #define CC_STATS_WORDS 16
 typedef struct {

@@ -22,12 +22,12 @@ class Result:
     stats: torch.Tensor
 
     @staticmethod
-    def alloc(n_txn: int, K: int, device, read_out=True, stream=None) -> "Result":
+    def alloc(n_txn: int, K: int, device, read_out=True, stream=None, out_words=None) -> "Result":
         """Allocate on `stream` (the db's stream) so the zero-fill is ordered before
         the library's kernels on that stream."""
         if stream is not None:
             with torch.cuda.stream(stream):
-                return Result.alloc(n_txn, K, device, read_out)
+                return Result.alloc(n_txn, K, device, read_out, out_words=out_words)
         z = dict(device=device)
         return Result(
             committed=torch.zeros(n_txn, dtype=torch.uint8, **z),
@@ -35,7 +35,7 @@ class Result:
             order_hi=torch.zeros(n_txn, dtype=torch.int64, **z),
             order_lo=torch.zeros(n_txn, dtype=torch.int64, **z),
             commit_pos=torch.zeros(n_txn, dtype=torch.int32, **z),
-            read_out=torch.zeros(n_txn * K, dtype=torch.int64, **z) if read_out else None,
+            read_out=torch.zeros(n_txn * (out_words or K), dtype=torch.int64, **z) if read_out else None,
             stats=torch.zeros(G.CC_STATS_WORDS, dtype=torch.int64, **z),
         )
 
@@ -75,6 +75,15 @@ class Batch:
         G.check(self.db.h, G.lib().cc_batch_export_ycsb(self.db.h, self.h, keys.ctypes.data,
                                                         ops.ctypes.data))
         return keys, ops
+
+    def export_tpcc(self):
+        tx = np.zeros(self.n_txn * G.TPCC_TX_WORDS, dtype=np.uint32)
+        G.check(self.db.h, G.lib().cc_batch_export_tpcc(self.db.h, self.h, tx.ctypes.data))
+        return tx
+
+    @property
+    def out_words(self):
+        return G.TPCC_OUT_WORDS if self.kind == 2 else self.K
 
     def free(self):
         if self.h:
@@ -151,6 +160,33 @@ class DB:
         self._chk(st)
         return Batch(self, h)
 
+    # ----------------------------------------------------------- TPC-C
+    def load_tpcc(self, warehouses: int, seed: int, max_txn: int, w_first: int = 0, w_count: int | None = None):
+        d = G.cc_tpcc_db_desc(warehouses, w_first, warehouses if w_count is None else w_count, max_txn, seed)
+        self._chk(G.lib().cc_load_tpcc(self.h, ctypes.byref(d)))
+        ids = (ctypes.c_uint32 * 9)()
+        self._chk(G.lib().cc_tpcc_tables(self.h, ctypes.byref(ids)))
+        self.tpcc_ids = dict(zip(G.TPCC_TABLES, list(ids)))
+
+    def gen_tpcc(self, n_txn: int, seed: int, neworder_permyriad: int = 5000, w_lo: int = 0, w_hi=None) -> Batch:
+        if w_hi is None:
+            rows = ctypes.c_uint64()
+            self._chk(G.lib().cc_table_info(self.h, self.tpcc_ids["warehouse"], ctypes.byref(rows), None))
+            w_hi = w_lo + rows.value
+        g = G.cc_tpcc_gen_desc(n_txn, neworder_permyriad, seed, w_lo, w_hi)
+        h = ctypes.c_void_p()
+        self._chk(G.lib().cc_batch_gen_tpcc(self.h, ctypes.byref(g), ctypes.byref(h)))
+        return Batch(self, h)
+
+    def import_tpcc(self, tx) -> Batch:
+        t = np.ascontiguousarray(tx, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        self._chk(G.lib().cc_batch_import_tpcc(self.h, t.ctypes.data, t.size // G.TPCC_TX_WORDS, 0, ctypes.byref(h)))
+        return Batch(self, h)
+
+    def read_tpcc(self, names=None) -> dict:
+        return {k: self.read_table(self.tpcc_ids[k]) for k in (names or G.TPCC_TABLES)}
+
     def read_table(self, table_id: int = 0) -> np.ndarray:
         rows, rb = ctypes.c_uint64(), ctypes.c_uint32()
         self._chk(G.lib().cc_table_info(self.h, table_id, ctypes.byref(rows), ctypes.byref(rb)))
@@ -171,7 +207,7 @@ class DB:
         sid = G.SCHEME_ID[scheme] if isinstance(scheme, str) else int(scheme)
         if result is None:
             result = Result.alloc(batch.n_txn, batch.K, torch.device("cuda", self.device), read_out,
-                                  stream=self.stream)
+                                  stream=self.stream, out_words=batch.out_words)
         d = G.cc_exec_desc(sid, wd, bs, flags, grid, lanes, watchdog_s)
         r = result.c()
         self._chk(G.lib().cc_submit(self.h, batch.h, ctypes.byref(d), ctypes.byref(r)))

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "tpcc.h"
 
 namespace gcctb {
 cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, unsigned long long *ohi,
@@ -22,7 +23,8 @@ struct Table {
     std::string name;
     uint32_t row_bytes;
     uint64_t rows;
-    uint64_t base;   // first record id
+    uint64_t base;   // first record id (CC-managed tables)
+    bool cc;         // has CC words (false: immutable or private reserved slots)
     void *d;
 };
 struct Index {
@@ -36,8 +38,18 @@ struct cc_batch_s {
     uint32_t kind;
     uint32_t n_txn;
     uint32_t K;
-    uint32_t *keys;
-    uint8_t *ops;
+    uint32_t *keys;   // YCSB
+    uint8_t *ops;     // YCSB
+    uint32_t *tx;     // TPC-C descriptors
+};
+
+struct TpccState {
+    bool loaded = false;
+    uint32_t W = 0, w_first = 0, w_count = 0, max_txn = 0;
+    uint64_t seed = 0;
+    uint32_t c_load = 0, c_run = 0, c_id = 0, c_item = 0;
+    uint32_t ids[9] = {0};
+    uint32_t *nidx_start = nullptr, *nidx_count = nullptr, *nidx_rows = nullptr;
 };
 
 struct Pending {
@@ -58,6 +70,7 @@ struct cc_db_s {
     u64 *meta = nullptr;
     uint64_t meta_records = 0;
     int ycsb_table = -1, ycsb_index = -1;
+    TpccState tpcc;
     // per-submit scratch (grown on demand)
     Ctl *ctl = nullptr;
     u64 *stats_scratch = nullptr;
@@ -172,7 +185,8 @@ cc_status cc_db_destroy(cc_db db) {
     for (auto &t : db->tables) cudaFree(t.d);
     for (auto &i : db->indexes) { cudaFree(i.keys); cudaFree(i.rowids); }
     for (void *p : db->snap) cudaFree(p);
-    for (auto *b : db->batches) { cudaFree(b->keys); cudaFree(b->ops); delete b; }
+    for (auto *b : db->batches) { cudaFree(b->keys); cudaFree(b->ops); cudaFree(b->tx); delete b; }
+    cudaFree(db->tpcc.nidx_start); cudaFree(db->tpcc.nidx_count); cudaFree(db->tpcc.nidx_rows);
     for (auto &pe : db->pending) for (auto &e : pe.ev) cudaEventDestroy(e);
     for (auto &pe : db->free_events) for (auto &e : pe.ev) cudaEventDestroy(e);
     free_scratch(db);
@@ -187,31 +201,40 @@ cc_status cc_db_destroy(cc_db db) {
 }
 
 // ---------------------------------------------------------------- tables
-cc_status cc_table_create(cc_db db, const char *name, uint32_t row_bytes, uint64_t rows,
-                          uint32_t *table_id) {
-    CHECK_DB(db);
+static cc_status create_table(cc_db db, const char *name, uint32_t row_bytes, uint64_t rows, bool cc,
+                              uint32_t *table_id) {
     if (!table_id || row_bytes == 0 || row_bytes % 8 || rows == 0)
         return fail(db, CC_ERR_INVALID_ARG, "cc_table_create: bad row_bytes/rows");
-    if (db->n_records + rows > (1ull << 32))
+    if (cc && db->n_records + rows > (1ull << 32))
         return fail(db, CC_ERR_CONFIG, "cc_table_create: more than 2^32 records");
     Table t;
     t.name = name ? name : "";
     t.row_bytes = row_bytes;
     t.rows = rows;
     t.base = db->n_records;
+    t.cc = cc;
     CUDA_TRY(db, dalloc(&t.d, (size_t)row_bytes * rows));
     CUDA_TRY(db, cudaMemsetAsync(t.d, 0, (size_t)row_bytes * rows, db->stream));
-    // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B)
-    const uint64_t need = db->n_records + rows;
-    u64 *meta = nullptr;
-    CUDA_TRY(db, dalloc(&meta, need * 16));
-    if (db->meta) cudaFree(db->meta);
-    db->meta = meta;
-    db->meta_records = need;
-    db->n_records = need;
+    if (cc) {
+        // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B)
+        const uint64_t need = db->n_records + rows;
+        u64 *meta = nullptr;
+        CUDA_TRY(db, dalloc(&meta, need * 16));
+        CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+        if (db->meta) cudaFree(db->meta);
+        db->meta = meta;
+        db->meta_records = need;
+        db->n_records = need;
+    }
     db->tables.push_back(t);
     *table_id = (uint32_t)db->tables.size() - 1;
     return CC_OK;
+}
+
+cc_status cc_table_create(cc_db db, const char *name, uint32_t row_bytes, uint64_t rows,
+                          uint32_t *table_id) {
+    CHECK_DB(db);
+    return create_table(db, name, row_bytes, rows, true, table_id);
 }
 
 cc_status cc_table_info(cc_db db, uint32_t table_id, uint64_t *rows, uint32_t *row_bytes) {
@@ -300,13 +323,21 @@ cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *d) {
     return CC_OK;
 }
 
-static cc_status new_batch(cc_db db, uint32_t n_txn, uint32_t K, cc_batch *out) {
+static cc_status new_batch(cc_db db, uint32_t n_txn, uint32_t K, cc_batch *out, uint32_t kind = KIND_YCSB) {
     cc_batch b = new cc_batch_s();
-    b->kind = KIND_YCSB;
+    b->kind = kind;
     b->n_txn = n_txn;
     b->K = K;
-    if (dalloc(&b->keys, (size_t)n_txn * K * 4) || dalloc(&b->ops, (size_t)n_txn * K)) {
+    b->keys = nullptr;
+    b->ops = nullptr;
+    b->tx = nullptr;
+    cudaError_t e = kind == KIND_YCSB
+                        ? (dalloc(&b->keys, (size_t)n_txn * K * 4) ?: dalloc(&b->ops, (size_t)n_txn * K))
+                        : dalloc(&b->tx, (size_t)n_txn * TPCC_TX_WORDS * 4);
+    if (e) {
         cudaFree(b->keys);
+        cudaFree(b->ops);
+        cudaFree(b->tx);
         delete b;
         return fail(db, CC_ERR_OOM, "batch allocation failed");
     }
@@ -385,11 +416,139 @@ cc_status cc_batch_free(cc_db db, cc_batch b) {
             cudaStreamSynchronize(db->stream);
             cudaFree(b->keys);
             cudaFree(b->ops);
+            cudaFree(b->tx);
             delete b;
             db->batches.erase(db->batches.begin() + i);
             return CC_OK;
         }
     return fail(db, CC_ERR_INVALID_ARG, "unknown batch");
+}
+
+
+// ---------------------------------------------------------------- TPC-C
+static uint64_t host_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint64_t host_prand(uint64_t seed, uint64_t table, uint64_t row, uint64_t field) {
+    return host_mix64(seed ^ (table << 56) ^ (row << 8) ^ field);
+}
+
+cc_status cc_load_tpcc(cc_db db, const cc_tpcc_db_desc *d) {
+    CHECK_DB(db);
+    if (!d || d->warehouses == 0 || d->w_count == 0 || d->w_first + d->w_count > d->warehouses ||
+        d->max_txn == 0 || d->warehouses > 65535)
+        return fail(db, CC_ERR_INVALID_ARG, "cc_load_tpcc: bad warehouse range / max_txn");
+    if (db->tpcc.loaded) return fail(db, CC_ERR_CONFIG, "TPC-C already loaded");
+    TpccState &T = db->tpcc;
+    T.W = d->warehouses;
+    T.w_first = d->w_first;
+    T.w_count = d->w_count;
+    T.max_txn = d->max_txn;
+    T.seed = d->seed;
+    // NURand constants (TPC-C §2.1.6; inputs/tpcc.py nurand_consts)
+    uint64_t c[4];
+    for (int k = 0; k < 4; k++) c[k] = host_prand(d->seed, TPCC_T_CONST, 0, k);
+    T.c_load = (uint32_t)(c[0] % 256);
+    T.c_run = (uint32_t)((T.c_load + 65 + c[1] % 55) % 256);
+    T.c_id = (uint32_t)(c[2] % 1024);
+    T.c_item = (uint32_t)(c[3] % 8192);
+    const uint64_t wc = d->w_count;
+    const struct { const char *n; uint32_t words; uint64_t rows; bool cc; } spec[9] = {
+        {"warehouse", TPCC_W_WORDS, wc, true},
+        {"district", TPCC_D_WORDS, wc * TPCC_DIST, true},
+        {"customer", TPCC_C_WORDS, wc * TPCC_DIST * TPCC_CUST, true},
+        {"stock", TPCC_S_WORDS, wc * TPCC_STOCK, true},
+        {"item", TPCC_I_WORDS, TPCC_ITEMS, false},
+        {"order", TPCC_O_WORDS, d->max_txn, false},
+        {"new_order", TPCC_NO_WORDS, d->max_txn, false},
+        {"order_line", TPCC_OL_WORDS, (uint64_t)d->max_txn * TPCC_MAXOL, false},
+        {"history", TPCC_H_WORDS, d->max_txn, false}};
+    for (int k = 0; k < 9; k++) {
+        cc_status st = create_table(db, spec[k].n, spec[k].words * 8, spec[k].rows, spec[k].cc, &T.ids[k]);
+        if (st) return st;
+    }
+    const int pop_tab[5] = {TPCC_T_W, TPCC_T_D, TPCC_T_C, TPCC_T_S, TPCC_T_I};
+    const uint64_t first[5] = {d->w_first, (uint64_t)d->w_first * TPCC_DIST,
+                               (uint64_t)d->w_first * TPCC_DIST * TPCC_CUST, (uint64_t)d->w_first * TPCC_STOCK, 0};
+    for (int k = 0; k < 5; k++)
+        CUDA_TRY(db, launch_tpcc_pop(pop_tab[k], (u64 *)db->tables[T.ids[k]].d, first[k],
+                                     db->tables[T.ids[k]].rows, d->seed, T.c_load, db->stream));
+    const uint32_t n_cust = (uint32_t)(wc * TPCC_DIST * TPCC_CUST), n_groups = (uint32_t)(wc * TPCC_DIST * 1000);
+    CUDA_TRY(db, dalloc(&T.nidx_start, n_groups * 4ull));
+    CUDA_TRY(db, dalloc(&T.nidx_count, n_groups * 4ull));
+    CUDA_TRY(db, dalloc(&T.nidx_rows, n_cust * 4ull));
+    CUDA_TRY(db, build_name_index((const u64 *)db->tables[T.ids[2]].d, n_cust, first[2], d->seed, T.c_load,
+                                  T.nidx_start, T.nidx_count, T.nidx_rows, n_groups, db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    T.loaded = true;
+    return CC_OK;
+}
+
+cc_status cc_tpcc_tables(cc_db db, uint32_t ids[9]) {
+    CHECK_DB(db);
+    if (!db->tpcc.loaded || !ids) return fail(db, CC_ERR_CONFIG, "TPC-C not loaded");
+    for (int k = 0; k < 9; k++) ids[k] = db->tpcc.ids[k];
+    return CC_OK;
+}
+
+cc_status cc_batch_gen_tpcc(cc_db db, const cc_tpcc_gen_desc *g, cc_batch *out) {
+    CHECK_DB(db);
+    const TpccState &T = db->tpcc;
+    if (!g || !out) return fail(db, CC_ERR_INVALID_ARG, "null args");
+    if (!T.loaded) return fail(db, CC_ERR_CONFIG, "TPC-C not loaded");
+    if (g->n_txn == 0 || g->n_txn > T.max_txn || g->n_txn > (1u << 21) || g->w_hi <= g->w_lo ||
+        g->w_hi > T.W || g->neworder_permyriad > 10000)
+        return fail(db, CC_ERR_CONFIG, "cc_batch_gen_tpcc: bad n_txn (<= max_txn, 2^21) / warehouse range");
+    cc_batch b;
+    cc_status st = new_batch(db, g->n_txn, TPCC_K, &b, KIND_TPCC);
+    if (st) return st;
+    CUDA_TRY(db, cudaMemsetAsync(db->ctl, 0, sizeof(Ctl), db->stream));
+    CUDA_TRY(db, launch_tpcc_gen(b->tx, g->n_txn, g->seed, T.W, g->w_lo, g->w_hi, g->neworder_permyriad,
+                                 T.c_run, T.c_id, T.c_item, db->ctl, db->stream));
+    *out = b;
+    return CC_OK;
+}
+
+cc_status cc_batch_import_tpcc(cc_db db, const uint32_t *tx, uint32_t n_txn, int src_on_device, cc_batch *out) {
+    CHECK_DB(db);
+    if (!tx || !out || n_txn == 0) return fail(db, CC_ERR_INVALID_ARG, "null args");
+    if (!db->tpcc.loaded) return fail(db, CC_ERR_CONFIG, "TPC-C not loaded");
+    if (n_txn > db->tpcc.max_txn || n_txn > (1u << 21)) return fail(db, CC_ERR_CONFIG, "n_txn > max_txn");
+    if (!src_on_device) {   // validate ranges of host descriptors before anything is enqueued
+        for (uint32_t g = 0; g < n_txn; g++) {
+            const uint32_t *t = tx + (uint64_t)g * TPCC_TX_WORDS;
+            const TpccState &T = db->tpcc;
+            auto local = [&](uint32_t w) { return w >= T.w_first && w < T.w_first + T.w_count; };
+            bool ok = t[TX_TYPE] <= 1 && local(t[TX_W]) && t[TX_D] < TPCC_DIST && t[TX_CD] < TPCC_DIST;
+            if (t[TX_TYPE] == 0) {
+                ok = ok && t[TX_OLCNT] >= 1 && t[TX_OLCNT] <= TPCC_MAXOL && t[TX_C] < TPCC_CUST;
+                for (uint32_t j = 0; ok && j < t[TX_OLCNT]; j++)
+                    ok = t[TX_ITEM + j] < TPCC_ITEMS && local(t[TX_SUPQ + j] >> 8);
+            } else {
+                ok = ok && local(t[TX_CW]) && (t[TX_C] < TPCC_CUST || (t[TX_C] == 0xFFFFFFFFu && t[TX_CLAST] < 1000));
+            }
+            if (!ok) return fail(db, CC_ERR_KEY_NOT_FOUND, "TPC-C descriptor %u out of range", g);
+        }
+    }
+    cc_batch b;
+    cc_status st = new_batch(db, n_txn, TPCC_K, &b, KIND_TPCC);
+    if (st) return st;
+    CUDA_TRY(db, cudaMemcpyAsync(b->tx, tx, (size_t)n_txn * TPCC_TX_WORDS * 4,
+                                 src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, db->stream));
+    if (!src_on_device) CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    *out = b;
+    return CC_OK;
+}
+
+cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx) {
+    CHECK_DB(db);
+    if (!b || !tx || b->kind != KIND_TPCC) return fail(db, CC_ERR_INVALID_ARG, "bad batch");
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, cudaMemcpy(tx, b->tx, (size_t)b->n_txn * TPCC_TX_WORDS * 4, cudaMemcpyDeviceToHost));
+    return CC_OK;
 }
 
 // ---------------------------------------------------------------- execution
@@ -467,11 +626,12 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if ((unsigned)desc->scheme >= CC_NUM_SCHEMES) return fail(db, CC_ERR_INVALID_ARG, "bad scheme");
     if (desc->wd > 5 || desc->bs < 1 || desc->bs > 32)
         return fail(db, CC_ERR_INVALID_ARG, "wd must be 0..5 and bs 1..32 (PAPER.md:480-484)");
-    if (b->kind != KIND_YCSB) return fail(db, CC_ERR_UNSUPPORTED, "batch kind not supported");
+    const bool is_tpcc = b->kind == KIND_TPCC;
     {
         const uint32_t L = desc->lanes_per_txn;
-        if (!(L <= 1 || L == 4 || L == 8 || L == 16) || (L > 1 && L < b->K))
-            return fail(db, CC_ERR_INVALID_ARG, "lanes_per_txn must be 0/1 or 4/8/16 and >= ops per txn");
+        if (is_tpcc ? !(L <= 1 || L == 4 || L == 8 || L == 16 || L == 32)
+                    : (!(L <= 1 || L == 4 || L == 8 || L == 16) || (L > 1 && L < b->K)))
+            return fail(db, CC_ERR_INVALID_ARG, "lanes_per_txn must be 0/1 or 4/8/16 (>= ops per txn); TPC-C uses 32-lane tiles");
     }
     const int scheme = (int)desc->scheme;
     const bool det = scheme == CC_GPUTX || scheme == CC_GACCO;
@@ -479,11 +639,9 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     cc_status st = ensure_scratch(db, b->n_txn, n_acc);
     if (st) return st;
     if (scheme == CC_MVCC) {
-        st = ensure_arena(db, n_acc, 16);   // one history node per write op
+        st = ensure_arena(db, n_acc, is_tpcc ? TPCC_C_WORDS : 16);   // one history node per access slot
         if (st) return st;
     }
-    const Table &t = db->tables[db->ycsb_table];
-    const Index &ix = db->indexes[db->ycsb_index];
 
     ExecParams p{};
     p.scheme = scheme;
@@ -491,7 +649,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.K = b->K;
     p.wd = desc->wd;
     p.flags = desc->flags;
-    p.lanes = desc->lanes_per_txn <= 1 ? 1 : desc->lanes_per_txn;
+    p.lanes = desc->lanes_per_txn <= 1 ? 1 : (is_tpcc ? 32 : desc->lanes_per_txn);
     p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
     p.ctl = db->ctl;
     p.meta = db->meta;
@@ -504,13 +662,41 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.order_lo = db->olo;
     p.read_out = (u64 *)res->read_out;
     YcsbParams y{};
-    y.keys = b->keys;
-    y.ops = b->ops;
-    y.idx_keys = ix.keys;
-    y.idx_rows = ix.rowids;
-    y.idx_n = ix.n;
-    y.rows = (u64 *)t.d;
-    y.n_rows = t.rows;
+    TpccParams tp{};
+    if (is_tpcc) {
+        const TpccState &T = db->tpcc;
+        tp.tx = b->tx;
+        tp.wh = (u64 *)db->tables[T.ids[0]].d;
+        tp.di = (u64 *)db->tables[T.ids[1]].d;
+        tp.cu = (u64 *)db->tables[T.ids[2]].d;
+        tp.st = (u64 *)db->tables[T.ids[3]].d;
+        tp.it = (const u64 *)db->tables[T.ids[4]].d;
+        tp.o = (u64 *)db->tables[T.ids[5]].d;
+        tp.no = (u64 *)db->tables[T.ids[6]].d;
+        tp.ol = (u64 *)db->tables[T.ids[7]].d;
+        tp.h = (u64 *)db->tables[T.ids[8]].d;
+        tp.bW = db->tables[T.ids[0]].base;
+        tp.bD = db->tables[T.ids[1]].base;
+        tp.bC = db->tables[T.ids[2]].base;
+        tp.bS = db->tables[T.ids[3]].base;
+        tp.W = T.W;
+        tp.w_first = T.w_first;
+        tp.nidx_start = T.nidx_start;
+        tp.nidx_count = T.nidx_count;
+        tp.nidx_rows = T.nidx_rows;
+        tp.entry_date = 20240601;   // per-submit constant date (no wall clock)
+    } else {
+        if (db->ycsb_table < 0) return fail(db, CC_ERR_CONFIG, "no YCSB table loaded");
+        const Table &t = db->tables[db->ycsb_table];
+        const Index &ix = db->indexes[db->ycsb_index];
+        y.keys = b->keys;
+        y.ops = b->ops;
+        y.idx_keys = ix.keys;
+        y.idx_rows = ix.rowids;
+        y.idx_n = ix.n;
+        y.rows = (u64 *)t.d;
+        y.n_rows = t.rows;
+    }
 
     const bool timing = desc->flags & CC_FLAG_TIMING;
     Pending ev{};
@@ -525,7 +711,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[1], db->stream));
     // a3: preprocessing for the conflict-graph schemes
     if (det) {
-        CUDA_TRY(db, launch_ycsb_gather(p, y, db->prep, db->stream));
+        if (is_tpcc) CUDA_TRY(db, launch_tpcc_gather(p, tp, db->prep, db->n_records, db->stream));
+        else CUDA_TRY(db, launch_ycsb_gather(p, y, db->prep, db->stream));
         CUDA_TRY(db, launch_prep_common(p, db->prep, db->n_records, scheme == CC_GPUTX,
                                         rank_kernel_grid(), db->stream));
         p.acc_rec = db->prep.acc_rec;
@@ -542,11 +729,13 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     const int block = 32 * (int)desc->bs;
     int grid = (int)desc->grid;
     if (grid <= 0) {
-        const int per_sm = ycsb_exec_max_blocks_per_sm(scheme, (int)p.lanes, block);
+        const int per_sm = is_tpcc ? tpcc_exec_max_blocks_per_sm(scheme, (int)p.lanes, block)
+                                   : ycsb_exec_max_blocks_per_sm(scheme, (int)p.lanes, block);
         if (per_sm <= 0) return fail(db, CC_ERR_CONFIG, "executor cannot launch %d threads/block", block);
         grid = per_sm * db->num_sms;
     }
-    CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, db->stream));
+    if (is_tpcc) CUDA_TRY(db, launch_tpcc_exec(p, tp, grid, block, db->stream));
+    else CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, db->stream));
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
     // a7: commit positions + result copy-out
     cc_result r = *res;

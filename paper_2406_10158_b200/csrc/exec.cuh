@@ -308,7 +308,7 @@ GC_DEV void mvcc_commit(const ExecParams &p, const typename WL::Params &y, typen
     const u64 nidx = (u64)gid * p.K + i;
     u64 *node = p.arena + nidx * (2 + WL::ROW_WORDS);
     st_cg(node, ld_relaxed(hi));   // old head -> history node (begin, prev)
-    WL::copy_row(row, node + 2);
+    WL::copy_row(L, row, node + 2);
     fence_acqrel();
     st_release(hi, (ts << 32) | nidx);   // publish the history, then install in place
     fence_acqrel();
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(1024) exec_thread_kernel(ExecParams p, typenam
             u64 kh, kl;
             const int r = run_thread<S, WL>(th, gid, L, n, y, kh, kl);
             if (r == RES_OK) {
-                for (u32 i = 0; i < n; i++) WL::emit(p, y, L[i], gid, i);
+                WL::emit_txn(p, y, gid, L, n);   // outputs + private reserved-slot writes
                 p.order_hi[gid] = kh;
                 p.order_lo[gid] = kl;
                 p.committed[gid] = 1;
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(1024) exec_tile_kernel(ExecParams p, typename 
             u64 kh = 0, kl = 0;
             const int r = run_tile<S, WL>(tile, th, gid, L, y, kh, kl);
             if (r == RES_OK) {
-                if (L.act) WL::emit(p, y, L, gid, li);
+                WL::emit_tile(tile, p, y, gid, L, li);   // outputs + private reserved-slot writes
                 if (li == 0) {
                     p.order_hi[gid] = kh;
                     p.order_lo[gid] = kl;

@@ -99,6 +99,23 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
                             bool deterministic, cudaStream_t s);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
 
+struct TpccParams;
+cudaError_t launch_tpcc_exec(const ExecParams &p, const TpccParams &y, int grid, int block,
+                             cudaStream_t s);
+int tpcc_exec_max_blocks_per_sm(int scheme, int lanes, int block);
+cudaError_t launch_tpcc_gather(const ExecParams &p, const TpccParams &y, PrepBufs &b,
+                               uint64_t n_records, cudaStream_t s);
+cudaError_t launch_tpcc_pop(int table, unsigned long long *rows, unsigned long long first,
+                            unsigned long long n, unsigned long long seed, uint32_t c_load,
+                            cudaStream_t s);
+cudaError_t build_name_index(const unsigned long long *cu, uint32_t n_cust,
+                             unsigned long long first_row, unsigned long long seed,
+                             uint32_t c_load, uint32_t *idx_start, uint32_t *idx_count,
+                             uint32_t *idx_rows, uint32_t n_groups, cudaStream_t s);
+cudaError_t launch_tpcc_gen(uint32_t *tx, uint32_t n_txn, unsigned long long seed, uint32_t W,
+                            uint32_t w_lo, uint32_t w_hi, uint32_t no_pm, uint32_t c_last_run,
+                            uint32_t c_id_c, uint32_t c_item_c, Ctl *ctl, cudaStream_t s);
+
 cudaError_t launch_ycsb_init_rows(unsigned long long *rows, uint64_t first, uint64_t n,
                                   uint64_t seed, cudaStream_t s);
 cudaError_t launch_identity_index(unsigned long long *keys, unsigned long long *rows,

@@ -1,0 +1,33 @@
+// tpcc.h -- TPC-C layout constants (inputs/tpcc.py docstring is the specification) and
+// the workload parameters the executor receives.  Device library side only.
+#pragma once
+#include <cstdint>
+
+namespace gcctb {
+
+constexpr int TPCC_W_WORDS = 16, TPCC_D_WORDS = 16, TPCC_C_WORDS = 88, TPCC_S_WORDS = 40,
+              TPCC_I_WORDS = 12, TPCC_O_WORDS = 8, TPCC_NO_WORDS = 4, TPCC_OL_WORDS = 8,
+              TPCC_H_WORDS = 8;
+constexpr uint32_t TPCC_DIST = 10, TPCC_CUST = 3000, TPCC_STOCK = 100000, TPCC_ITEMS = 100000,
+                   TPCC_MAXOL = 15;
+constexpr int TPCC_K = 18;               // access slots per transaction: W, D, C + 15 lines
+constexpr int TPCC_OUT_WORDS = 48;       // read_out words per transaction
+constexpr int TPCC_CDATA_OFF = 25, TPCC_CDATA_WORDS = 63;
+constexpr int TPCC_TX_WORDS = 40;
+enum { TPCC_T_W = 1, TPCC_T_D = 2, TPCC_T_C = 3, TPCC_T_S = 4, TPCC_T_I = 5, TPCC_T_CONST = 15 };
+enum { TX_TYPE = 0, TX_W, TX_D, TX_CW, TX_CD, TX_C, TX_CLAST, TX_HAMT, TX_OLCNT, TX_ALLLOCAL,
+       TX_ITEM = 10, TX_SUPQ = 25 };
+
+struct TpccParams {
+    const uint32_t *tx;                  // n_txn x 40 descriptors
+    unsigned long long *wh, *di, *cu, *st;   // CC tables (local partition)
+    const unsigned long long *it;        // items (immutable, replicated)
+    unsigned long long *o, *no, *ol, *h; // reserved slots
+    unsigned long long bW, bD, bC, bS;   // record-id bases of W, D, C, S
+    uint32_t W;                          // total warehouses
+    uint32_t w_first;                    // first warehouse held by this db
+    const uint32_t *nidx_start, *nidx_count, *nidx_rows;   // last-name index
+    unsigned long long entry_date;
+};
+
+}  // namespace gcctb

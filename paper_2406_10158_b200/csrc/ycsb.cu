@@ -130,7 +130,7 @@ struct YcsbWL {
         st_cg(dst + 15, L.n15);
     }
 
-    static GC_DEV void copy_row(const u64 *src, u64 *dst) {
+    static GC_DEV void copy_row(const Lane &, const u64 *src, u64 *dst) {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             u64 a, b;
@@ -139,8 +139,13 @@ struct YcsbWL {
         }
     }
 
-    static GC_DEV void emit(const ExecParams &p, const YcsbParams &, const Lane &L, u32 gid, u32 i) {
-        if (p.read_out) p.read_out[(u64)gid * p.K + i] = L.out;
+    static GC_DEV void emit_txn(const ExecParams &p, const YcsbParams &, u32 gid, const Lane *L, u32 n) {
+        if (!p.read_out) return;
+        for (u32 i = 0; i < n; i++) p.read_out[(u64)gid * p.K + i] = L[i].out;
+    }
+    template <class Tile>
+    static GC_DEV void emit_tile(Tile &, const ExecParams &p, const YcsbParams &, u32 gid, const Lane &L, u32 i) {
+        if (p.read_out && L.act) p.read_out[(u64)gid * p.K + i] = L.out;
     }
 };
 

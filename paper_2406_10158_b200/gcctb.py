@@ -41,6 +41,16 @@ class cc_ycsb_gen_desc(ctypes.Structure):
                 ("scramble_mult", ctypes.c_uint64)]
 
 
+class cc_tpcc_db_desc(ctypes.Structure):
+    _fields_ = [("warehouses", ctypes.c_uint32), ("w_first", ctypes.c_uint32), ("w_count", ctypes.c_uint32),
+                ("max_txn", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+
+
+class cc_tpcc_gen_desc(ctypes.Structure):
+    _fields_ = [("n_txn", ctypes.c_uint32), ("neworder_permyriad", ctypes.c_uint32), ("seed", ctypes.c_uint64),
+                ("w_lo", ctypes.c_uint32), ("w_hi", ctypes.c_uint32)]
+
+
 class cc_exec_desc(ctypes.Structure):
     _fields_ = [("scheme", ctypes.c_int), ("wd", ctypes.c_uint32), ("bs", ctypes.c_uint32),
                 ("flags", ctypes.c_uint32), ("grid", ctypes.c_uint32),
@@ -93,7 +103,16 @@ _SIGS = {
     "cc_timing_read": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double * 5),
                                       ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]),
     "cc_snapshot": (ctypes.c_int, [_P, ctypes.c_int]),
+    "cc_load_tpcc": (ctypes.c_int, [_P, ctypes.POINTER(cc_tpcc_db_desc)]),
+    "cc_tpcc_tables": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32 * 9)]),
+    "cc_batch_gen_tpcc": (ctypes.c_int, [_P, ctypes.POINTER(cc_tpcc_gen_desc), ctypes.POINTER(_P)]),
+    "cc_batch_import_tpcc": (ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(_P)]),
+    "cc_batch_export_tpcc": (ctypes.c_int, [_P, _P, _P]),
 }
+
+TPCC_TX_WORDS = 40
+TPCC_OUT_WORDS = 48
+TPCC_TABLES = ["warehouse", "district", "customer", "stock", "item", "order", "new_order", "order_line", "history"]
 
 EXPORTED = sorted(_SIGS)
 

@@ -1,0 +1,106 @@
+"""-m gpu: TPC-C NewOrder/Payment parity of the CUDA path against the oracle
+(BASELINE.json configs[2..3]): device population == input generator, a1 generator
+bit-exact, and for every scheme the outputs, CC tables and reserved slots equal the
+oracle's serial replay in the reported order (GPUTx/GaccO: batch order)."""
+import numpy as np
+import pytest
+
+import inputs
+from inputs import tpcc as IT
+
+pytestmark = pytest.mark.gpu
+SCHEMES = ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc", "gputx", "gacco"]
+POP = ["warehouse", "district", "customer", "stock", "item"]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+def _db(W, seed, max_txn):
+    from paper_2406_10158_b200.api import DB
+    db = DB(0)
+    db.load_tpcc(W, seed, max_txn)
+    return db
+
+
+@pytest.fixture(scope="module")
+def w4(torch_cuda, orc):
+    db = _db(4, 21, 8192)
+    S0 = IT.population(21, 4)
+    got = db.read_tpcc(POP)
+    for k in POP:
+        assert np.array_equal(got[k], S0[k]), f"device population differs in {k}"
+    db.snapshot(True)
+    yield db, S0
+    db.close()
+
+
+def _run(db, S0, W, tx_batch, scheme, lanes, orc):
+    from oracle import tpcc as OT
+    tx = tx_batch.export_tpcc()
+    db.snapshot(False)
+    res = db.submit(tx_batch, scheme, wd=0, bs=32 if lanes == 1 else 8, lanes=lanes, watchdog_s=60)
+    st = db.sync()
+    assert st.commits == tx_batch.n_txn
+    h = res.host(db.stream)
+    S_gpu = db.read_tpcc(list(OT.TABLES + OT.SLOTS))
+    n = tx_batch.n_txn
+    S_gpu = {k: (v[:n * 15] if k == "order_line" else v[:n]) if k in OT.SLOTS else v for k, v in S_gpu.items()}
+    OT.check(scheme, S0, tx, W, h, S_gpu)
+    return st
+
+
+def test_generator_bitexact(w4, orc):
+    from oracle import tpcc as OT
+    db, _ = w4
+    for seed, pm in [(1, 5000), (2, 5114), (3, 10000), (4, 0)]:
+        b = db.gen_tpcc(4096, seed, pm)
+        exp = OT.gen(seed, 4, 4096, pm, IT.nurand_consts(21))
+        assert np.array_equal(b.export_tpcc(), exp)
+        b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 32])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_w4_parity(w4, orc, scheme, lanes):
+    db, S0 = w4
+    for seed in (7, 8):
+        b = db.gen_tpcc(4096, seed, 5114)
+        _run(db, S0, 4, b, scheme, lanes, orc)
+        b.free()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_payment_only_by_name_heavy(w4, orc, scheme):
+    """All Payments (60% by last name, 15% remote): W/D hot rows and BC c_data shifts."""
+    db, S0 = w4
+    b = db.gen_tpcc(4096, 99, 0)
+    _run(db, S0, 4, b, scheme, 32, orc)
+    b.free()
+
+
+@pytest.fixture(scope="module")
+def c3(torch_cuda, orc):
+    """BASELINE.json configs[2]: 1 warehouse, NewOrder/Payment 50/50, batch 16K."""
+    db = _db(1, 5, 16384)
+    S0 = IT.population(5, 1)
+    got = db.read_tpcc(POP)
+    for k in POP:
+        assert np.array_equal(got[k], S0[k])
+    db.snapshot(True)
+    yield db, S0
+    db.close()
+
+
+@pytest.mark.parametrize("lanes", [1, 32])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c3_full_size_parity(c3, orc, scheme, lanes):
+    db, S0 = c3
+    b = db.gen_tpcc(16384, 31, 5000)
+    _run(db, S0, 1, b, scheme, lanes, orc)
+    b.free()
