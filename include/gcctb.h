@@ -195,6 +195,12 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         appending it to the retry queue */
 #define CC_FLAG_TIMING 0x2u          /* record CUDA events around each phase; read them
                                         with cc_timing_read() */
+#define CC_FLAG_PARTITIONED 0x4u     /* TPC-C over warehouse partitions (a8): cc_submit runs
+                                        phase A (local transactions, chosen scheme) and
+                                        packs phase-B requests; finish with cc_part_send /
+                                        cc_part_apply / cc_part_finish */
+#define CC_FLAG_PART_ALL 0x8u        /* as PARTITIONED, but every transaction takes phase B
+                                        (exercises phase B on one partition) */
 
 typedef struct {
     cc_scheme scheme;
@@ -247,6 +253,26 @@ typedef struct {
  * (GPUTx/GaccO, a3), execute with compaction of aborts into a retry queue until every
  * transaction commits (a4-a6), then emit results (a7).  Asynchronous on the db stream. */
 cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res);
+/* ------------------------------------------- partitioned TPC-C (a8)
+ * Rank r of `world` (cc_db_desc) holds warehouses [r*W/world, (r+1)*W/world).  After a
+ * cc_submit with CC_FLAG_PARTITIONED:
+ *   cc_part_send   waits, returns the device buffer of phase-B requests (48-byte records,
+ *                  grouped by destination rank in rank order) and counts[world] on the host;
+ *   -- the caller exchanges requests with an all-to-all (NCCL via torch.distributed) --
+ *   cc_part_apply  applies n received requests (device) on the items this rank owns: per
+ *                  item, in global transaction order (every TPC-C write is a
+ *                  read-modify-write of one item), writing n 48-byte responses (device, same
+ *                  order as received);
+ *   -- the caller returns responses with the reverse all-to-all --
+ *   cc_part_finish takes the responses aligned with this rank's send buffer, assembles the
+ *                  outputs and reserved slots of its distributed transactions and completes
+ *                  the submit (a7).  Order keys: phase A (rank << 48 | scheme key, key_lo),
+ *                  phase B (1 << 63, global gid = rank * n_txn + gid).
+ * Buffers passed in are caller-owned device memory. */
+cc_status cc_part_send(cc_db db, const void **send, uint64_t *counts);
+cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp);
+cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent);
+
 /* Wait for the db stream; surface asynchronous errors; if st != NULL copy the stats of
  * the last submit into it. */
 cc_status cc_sync(cc_db db, cc_stats *st);

@@ -60,6 +60,18 @@ class Result:
         return d
 
 
+class _CudaBytes:
+    """__cuda_array_interface__ view of library-owned device memory (no copy)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3}
+
+
+def _device_bytes(ptr: int, nbytes: int, device: int) -> torch.Tensor:
+    return torch.as_tensor(_CudaBytes(ptr, nbytes), device=torch.device("cuda", device))
+
+
 class Batch:
     def __init__(self, db: "DB", handle):
         self.db = db
@@ -105,6 +117,7 @@ class DB:
         self.stream = stream
         self.device = device
         d = G.cc_db_desc(device, ctypes.c_void_p(stream.cuda_stream), rank, world)
+        self.rank, self.world = rank, world
         h = ctypes.c_void_p()
         G.check(None, L.cc_db_create(ctypes.byref(d), ctypes.byref(h)))
         self.h = h
@@ -212,6 +225,30 @@ class DB:
         r = result.c()
         self._chk(G.lib().cc_submit(self.h, batch.h, ctypes.byref(d), ctypes.byref(r)))
         return result
+
+    # ----------------------------------------------------------- partitioned TPC-C (a8)
+    def part_send(self):
+        """(device uint8 tensor of the phase-B requests grouped by destination, counts list)."""
+        ptr = ctypes.c_void_p()
+        counts = np.zeros(self.world, dtype=np.uint64)
+        self._chk(G.lib().cc_part_send(self.h, ctypes.byref(ptr), counts.ctypes.data))
+        n = int(counts.sum())
+        buf = _device_bytes(ptr.value, n * G.PART_REC_BYTES, self.device) if n else \
+            torch.empty(0, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return buf, [int(c) for c in counts]
+
+    def part_apply(self, recv: torch.Tensor) -> torch.Tensor:
+        n = recv.numel() // G.PART_REC_BYTES
+        with torch.cuda.stream(self.stream):
+            resp = torch.empty(n * G.PART_REC_BYTES, dtype=torch.uint8, device=recv.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._chk(G.lib().cc_part_apply(self.h, recv.data_ptr() if n else None, n, resp.data_ptr() if n else None))
+        return resp
+
+    def part_finish(self, resp: torch.Tensor):
+        n = resp.numel() // G.PART_REC_BYTES
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._chk(G.lib().cc_part_finish(self.h, resp.data_ptr() if n else None, n))
 
     def sync(self) -> G.cc_stats:
         s = G.cc_stats()

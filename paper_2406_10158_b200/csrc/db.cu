@@ -11,6 +11,9 @@
 #include "tpcc.h"
 
 namespace gcctb {
+cudaError_t launch_part_all(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                            uint8_t *skip, unsigned long long *cnt, unsigned long long *off,
+                            unsigned long long *cursor, PartReq *out, cudaStream_t s);
 cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, unsigned long long *ohi,
                             unsigned long long *olo, uint32_t n, cudaStream_t s);
 int rank_kernel_grid();
@@ -71,6 +74,26 @@ struct cc_db_s {
     uint64_t meta_records = 0;
     int ycsb_table = -1, ycsb_index = -1;
     TpccState tpcc;
+    struct Part {
+        bool pending = false;         // a partitioned submit awaits cc_part_finish
+        bool all = false;             // CC_FLAG_PART_ALL: every transaction is distributed
+        uint32_t cap_txn = 0;
+        uint8_t *skip = nullptr;
+        PartReq *send = nullptr;
+        PartResp *stage = nullptr;
+        unsigned long long *cnt = nullptr, *off = nullptr, *cursor = nullptr;   // [world + 1]
+        uint64_t recv_cap = 0;
+        unsigned long long *k1 = nullptr, *k2 = nullptr;
+        uint32_t *i1 = nullptr, *i2 = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_bytes = 0;
+        ExecParams p{};
+        TpccParams tp{};
+        cc_result res{};
+        cc_batch b = nullptr;
+        bool timing = false;
+        Pending ev{};
+    } part;
     // per-submit scratch (grown on demand)
     Ctl *ctl = nullptr;
     u64 *stats_scratch = nullptr;
@@ -190,6 +213,10 @@ cc_status cc_db_destroy(cc_db db) {
     for (auto &pe : db->pending) for (auto &e : pe.ev) cudaEventDestroy(e);
     for (auto &pe : db->free_events) for (auto &e : pe.ev) cudaEventDestroy(e);
     free_scratch(db);
+    cudaFree(db->part.skip); cudaFree(db->part.send); cudaFree(db->part.stage);
+    cudaFree(db->part.cnt); cudaFree(db->part.off); cudaFree(db->part.cursor);
+    cudaFree(db->part.k1); cudaFree(db->part.k2); cudaFree(db->part.i1); cudaFree(db->part.i2);
+    cudaFree(db->part.tmp);
     cudaFree(db->arena);
     cudaFree(db->meta);
     cudaFree(db->ctl);
@@ -619,6 +646,23 @@ static Pending get_events(cc_db db) {
     return p;
 }
 
+static cc_status ensure_part(cc_db db, uint32_t n_txn) {
+    auto &P = db->part;
+    if (!P.cnt) {
+        CUDA_TRY(db, dalloc(&P.cnt, (db->world + 1) * 8ull));
+        CUDA_TRY(db, dalloc(&P.off, (db->world + 1) * 8ull));
+        CUDA_TRY(db, dalloc(&P.cursor, (db->world + 1) * 8ull));
+    }
+    if (n_txn <= P.cap_txn) return CC_OK;
+    cudaStreamSynchronize(db->stream);
+    cudaFree(P.skip); cudaFree(P.send); cudaFree(P.stage);
+    CUDA_TRY(db, dalloc(&P.skip, n_txn));
+    CUDA_TRY(db, dalloc(&P.send, (size_t)n_txn * TPCC_K * sizeof(PartReq)));
+    CUDA_TRY(db, dalloc(&P.stage, (size_t)n_txn * TPCC_K * sizeof(PartResp)));
+    P.cap_txn = n_txn;
+    return CC_OK;
+}
+
 cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res) {
     CHECK_DB(db);
     if (!b || !desc || !res || !res->committed)
@@ -699,6 +743,18 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
 
     const bool timing = desc->flags & CC_FLAG_TIMING;
+    const bool partitioned = (desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) != 0;
+    if (partitioned) {
+        const TpccState &T = db->tpcc;
+        if (!is_tpcc) return fail(db, CC_ERR_UNSUPPORTED, "partitioned execution is TPC-C only (YCSB: replicas)");
+        if (db->part.pending) return fail(db, CC_ERR_STATE, "previous partitioned submit not finished");
+        if (T.W % db->world || T.w_count != T.W / db->world || T.w_first != db->rank * T.w_count)
+            return fail(db, CC_ERR_CONFIG, "partitioning needs equal contiguous warehouse ranges per rank");
+        if ((uint64_t)db->world * b->n_txn > (1ull << 24))
+            return fail(db, CC_ERR_CONFIG, "world * n_txn must be <= 2^24 (global gid bits)");
+        st = ensure_part(db, b->n_txn);
+        if (st) return st;
+    }
     Pending ev{};
     if (timing) {
         ev = get_events(db);
@@ -708,6 +764,16 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     CUDA_TRY(db, launch_reset_meta(scheme, db->meta, db->n_records, db->ring, db->ring_cap, db->ctl,
                                    db->stream));
     CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
+    if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
+        const uint32_t wpr = db->tpcc.W / db->world;
+        CUDA_TRY(db, part_classify_pack(tp, db->rank, db->world, wpr, b->n_txn, db->part.skip, db->part.cnt,
+                                        db->part.off, db->part.cursor, db->part.send, db->stream));
+        if (desc->flags & CC_FLAG_PART_ALL) {
+            CUDA_TRY(db, launch_part_all(tp, db->rank, db->world, wpr, b->n_txn, db->part.skip, db->part.cnt,
+                                         db->part.off, db->part.cursor, db->part.send, db->stream));
+        }
+        p.skip = db->part.skip;
+    }
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[1], db->stream));
     // a3: preprocessing for the conflict-graph schemes
     if (det) {
@@ -737,10 +803,20 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (is_tpcc) CUDA_TRY(db, launch_tpcc_exec(p, tp, grid, block, db->stream));
     else CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, db->stream));
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
+    if (partitioned) {   // phase B happens in cc_part_apply / cc_part_finish
+        db->part.pending = true;
+        db->part.p = p;
+        db->part.tp = tp;
+        db->part.res = *res;
+        db->part.b = b;
+        db->part.timing = timing;
+        db->part.ev = ev;
+        return CC_OK;
+    }
     // a7: commit positions + result copy-out
     cc_result r = *res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
-    CUDA_TRY(db, launch_finalize(p, r, db->prep, det, db->stream));
+    CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream));
     if ((void *)r.stats != (void *)db->stats_scratch)
         CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS,
                                      cudaMemcpyDeviceToDevice, db->stream));
@@ -748,6 +824,62 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         CUDA_TRY(db, cudaEventRecord(ev.ev[4], db->stream));
         db->pending.push_back(ev);
     }
+    return CC_OK;
+}
+
+
+cc_status cc_part_send(cc_db db, const void **send, uint64_t *counts) {
+    CHECK_DB(db);
+    if (!db->part.pending || !send || !counts) return fail(db, CC_ERR_STATE, "no partitioned submit pending");
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    std::vector<unsigned long long> c(db->world);
+    CUDA_TRY(db, cudaMemcpy(c.data(), db->part.cnt, db->world * 8ull, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < db->world; k++) counts[k] = c[k];
+    *send = db->part.send;
+    return CC_OK;
+}
+
+cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp) {
+    CHECK_DB(db);
+    auto &P = db->part;
+    if (!P.pending) return fail(db, CC_ERR_STATE, "no partitioned submit pending");
+    if (n && (!recv || !resp)) return fail(db, CC_ERR_INVALID_ARG, "null buffers");
+    if (n > P.recv_cap) {
+        cudaStreamSynchronize(db->stream);
+        cudaFree(P.k1); cudaFree(P.k2); cudaFree(P.i1); cudaFree(P.i2); cudaFree(P.tmp);
+        CUDA_TRY(db, dalloc(&P.k1, n * 8));
+        CUDA_TRY(db, dalloc(&P.k2, n * 8));
+        CUDA_TRY(db, dalloc(&P.i1, n * 4));
+        CUDA_TRY(db, dalloc(&P.i2, n * 4));
+        P.tmp_bytes = part_sort_bytes(n);
+        CUDA_TRY(db, dalloc((char **)&P.tmp, P.tmp_bytes));
+        P.recv_cap = n;
+    }
+    CUDA_TRY(db, part_apply((PartReq *)recv, n, P.tp, (PartResp *)resp, P.k1, P.k2, P.i1, P.i2, P.tmp,
+                            P.tmp_bytes, db->ctl, db->stream));
+    return CC_OK;
+}
+
+cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent) {
+    CHECK_DB(db);
+    auto &P = db->part;
+    if (!P.pending) return fail(db, CC_ERR_STATE, "no partitioned submit pending");
+    const uint32_t wpr = db->tpcc.W / db->world;
+    CUDA_TRY(db, part_finish(P.tp, db->rank, db->world, wpr, P.b->n_txn, P.skip, P.send, (const PartResp *)resp,
+                             n_sent, P.stage, P.p.committed, P.p.order_hi, P.p.order_lo, P.p.read_out,
+                             db->stream));
+    if (P.timing) CUDA_TRY(db, cudaEventRecord(P.ev.ev[3], db->stream));
+    cc_result r = P.res;
+    if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
+    CUDA_TRY(db, launch_finalize(P.p, r, db->prep, false, true, db->stream));
+    if ((void *)r.stats != (void *)db->stats_scratch)
+        CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS, cudaMemcpyDeviceToDevice,
+                                     db->stream));
+    if (P.timing) {
+        CUDA_TRY(db, cudaEventRecord(P.ev.ev[4], db->stream));
+        db->pending.push_back(P.ev);
+    }
+    P.pending = false;
     return CC_OK;
 }
 

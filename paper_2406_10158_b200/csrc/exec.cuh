@@ -541,6 +541,10 @@ __global__ void __launch_bounds__(1024) exec_thread_kernel(ExecParams p, typenam
     for (;;) {
         const u32 gid = claim_work<S>(th, cl);
         if (gid == NO_TXN) return;
+        if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
+            if (S == CC_GPUTX) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);
+            continue;
+        }
         const u32 n = WL::load_all(p, y, gid, L);
         if (n == 0xFFFFFFFFu) {
             set_err(p.ctl, CC_ERR_KEY_NOT_FOUND);
@@ -756,6 +760,10 @@ __global__ void __launch_bounds__(1024) exec_tile_kernel(ExecParams p, typename 
         if (li == 0) gid = claim_work<S>(th, cl);
         gid = tile.shfl(gid, 0);
         if (gid == NO_TXN) return;
+        if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
+            if (S == CC_GPUTX && li == 0) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);
+            continue;
+        }
         const bool ok = WL::load_lane(p, y, gid, li, L);
         if (!tile.all(ok)) {
             if (li == 0) set_err(p.ctl, CC_ERR_KEY_NOT_FOUND);

@@ -59,6 +59,7 @@ struct ExecParams {
     const uint32_t *rank_of;     // GPUTx: rank of each transaction
     uint32_t *rank_done;         // GPUTx: completed count per rank
     const uint32_t *rank_count;  // GPUTx: size of each rank (K-set)
+    const uint8_t *skip;         // partitioned TPC-C: 1 = distributed txn, left to phase B
 };
 
 // YCSB workload parameters.
@@ -96,7 +97,7 @@ cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBuf
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,
                                bool gputx, int grid, cudaStream_t s);
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, cudaStream_t s);
+                            bool deterministic, bool two_pass, cudaStream_t s);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
 
 struct TpccParams;
@@ -115,6 +116,22 @@ cudaError_t build_name_index(const unsigned long long *cu, uint32_t n_cust,
 cudaError_t launch_tpcc_gen(uint32_t *tx, uint32_t n_txn, unsigned long long seed, uint32_t W,
                             uint32_t w_lo, uint32_t w_hi, uint32_t no_pm, uint32_t c_last_run,
                             uint32_t c_id_c, uint32_t c_item_c, Ctl *ctl, cudaStream_t s);
+
+struct PartReq;
+struct PartResp;
+cudaError_t part_classify_pack(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr,
+                               uint32_t n_txn, uint8_t *skip, unsigned long long *cnt,
+                               unsigned long long *off, unsigned long long *cursor, PartReq *out,
+                               cudaStream_t s);
+cudaError_t part_apply(PartReq *req, uint64_t n, const TpccParams &y, PartResp *resp,
+                       unsigned long long *k1, unsigned long long *k2, uint32_t *i1, uint32_t *i2,
+                       void *tmp, size_t tmp_bytes, Ctl *ctl, cudaStream_t s);
+size_t part_sort_bytes(uint64_t n);
+cudaError_t part_finish(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr,
+                        uint32_t n_txn, const uint8_t *skip, const PartReq *sent,
+                        const PartResp *resp, uint64_t n_sent, PartResp *stage,
+                        uint8_t *committed, unsigned long long *ohi, unsigned long long *olo,
+                        unsigned long long *read_out, cudaStream_t s);
 
 cudaError_t launch_ycsb_init_rows(unsigned long long *rows, uint64_t first, uint64_t n,
                                   uint64_t seed, cudaStream_t s);

@@ -299,7 +299,7 @@ __global__ void stats_kernel(const Ctl *c, uint64_t *stats) {
 }
 
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, cudaStream_t s) {
+                            bool deterministic, bool two_pass, cudaStream_t s) {
     const uint32_t n = p.n_txn;
     const int blk = 256;
     const unsigned g = (n + blk - 1) / blk;
@@ -315,7 +315,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         cudaError_t e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, p.order_lo, k1, b.gid_in,
                                                         b.rank_order, (int)n, 0, 64, s);
         if (e) return e;
-        if (p.scheme == CC_TICTOC) {
+        if (two_pass) {
             gather_hi_kernel<<<g, blk, 0, s>>>(p.order_hi, b.rank_order, k1, n);
             bytes = b.cub_bytes;
             e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, k1, k2, b.rank_order, b.gid_in,

@@ -652,7 +652,7 @@ __global__ void tpcc_gather_kernel(ExecParams p, TpccParams y, uint32_t *acc_rec
     q.acc_rec = nullptr;
     const u64 base = (u64)gid * p.K;
     const uint32_t *t = y.tx + (u64)gid * TPCC_TX_WORDS;
-    const u32 n = t[TX_TYPE] == 0 ? 3 + t[TX_OLCNT] : 3;
+    const u32 n = (p.skip && p.skip[gid]) ? 0 : (t[TX_TYPE] == 0 ? 3 + t[TX_OLCNT] : 3);
     for (u32 i = 0; i < (u32)p.K; i++) {
         if (i < n) {
             TpccWL::Lane L;

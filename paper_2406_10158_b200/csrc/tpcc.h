@@ -31,3 +31,26 @@ struct TpccParams {
 };
 
 }  // namespace gcctb
+
+namespace gcctb {
+// ---- warehouse-partitioned TPC-C ----
+// One request per access of a distributed transaction, sent to the owner of the item.
+struct PartReq {
+    uint32_t gid;        // global transaction id (rank * n_local + local gid)
+    uint32_t home;       // home rank (lo16) | access lane (hi16)
+    uint32_t kind;       // 0 W, 1 D, 2 C, 3 S
+    uint32_t row;        // local row on the owner (C by name: 0xFFFFFFFF)
+    uint32_t type_d;     // txn type (bit0) | home district << 8 | remote-line flag << 16
+    uint32_t amount;     // NewOrder line qty, or Payment h_amount
+    uint32_t cust;       // by-name Payment: (c_w - w_first_owner) << 16 | c_d << 8 ... see pack
+    uint32_t last;       // by-name c_last number, or 0xFFFFFFFF
+    uint32_t c_ids;      // Payment customer: c_w (lo16) | c_d (hi16) (global ids, for the BC record)
+    uint32_t home_w;     // home warehouse (global) | home district << 16
+    uint32_t pad[2];
+};
+static_assert(sizeof(PartReq) == 48, "PartReq is 48 bytes");
+// Response: the value read by the access at its point in the gid-ordered chain.
+struct PartResp {
+    unsigned long long v[6];
+};
+}  // namespace gcctb

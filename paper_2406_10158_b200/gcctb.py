@@ -22,6 +22,9 @@ SCHEME_ID = {s: i for i, s in enumerate(SCHEMES)}
 
 CC_FLAG_IMMEDIATE_RETRY = 0x1
 CC_FLAG_TIMING = 0x2
+CC_FLAG_PARTITIONED = 0x4
+CC_FLAG_PART_ALL = 0x8
+PART_REC_BYTES = 48
 CC_STATS_WORDS = 16
 
 
@@ -108,6 +111,9 @@ _SIGS = {
     "cc_batch_gen_tpcc": (ctypes.c_int, [_P, ctypes.POINTER(cc_tpcc_gen_desc), ctypes.POINTER(_P)]),
     "cc_batch_import_tpcc": (ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(_P)]),
     "cc_batch_export_tpcc": (ctypes.c_int, [_P, _P, _P]),
+    "cc_part_send": (ctypes.c_int, [_P, ctypes.POINTER(_P), _P]),
+    "cc_part_apply": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P]),
+    "cc_part_finish": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),
 }
 
 TPCC_TX_WORDS = 40

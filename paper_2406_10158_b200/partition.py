@@ -1,0 +1,88 @@
+"""Warehouse-partitioned TPC-C orchestration.
+
+Per round each rank: cc_submit(PARTITIONED) -> phase A under the chosen scheme + packed
+phase-B requests; all-to-all #1 (requests to item owners); cc_part_apply (owners apply
+each item's chain in global gid order); all-to-all #2 (responses back, reverse splits);
+cc_part_finish (home assembles outputs / reserved slots, a7).  The collectives are NCCL
+all_to_all_single through torch.distributed (plumbing); `loopback_round` runs G
+partitions held by G dbs on one GPU with the same kernels, the exchange being a
+device-side permutation (concatenation of the per-destination slices).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import gcctb as G
+
+REC = G.PART_REC_BYTES
+
+
+def exchange(send: torch.Tensor, send_counts, group=None, via_cpu: bool = False):
+    """All-to-all of 48-byte records grouped by destination.  Returns (recv, recv_counts)."""
+    import torch.distributed as dist
+    dev = send.device if not via_cpu else torch.device("cpu")
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(x) for x in rc.tolist()]
+    src = send if not via_cpu else send.cpu()
+    recv = torch.empty(sum(recv_counts) * REC, dtype=torch.uint8, device=dev)
+    dist.all_to_all_single(recv, src, [c * REC for c in recv_counts], [c * REC for c in send_counts], group=group)
+    return (recv if not via_cpu else recv.to(send.device)), recv_counts
+
+
+def give_back(resp: torch.Tensor, recv_counts, send_counts, group=None, via_cpu: bool = False):
+    """Reverse all-to-all: responses (aligned with the received requests) return to the
+    senders, aligned with their send buffers."""
+    import torch.distributed as dist
+    dev = resp.device if not via_cpu else torch.device("cpu")
+    out = torch.empty(sum(send_counts) * REC, dtype=torch.uint8, device=dev)
+    src = resp if not via_cpu else resp.cpu()
+    dist.all_to_all_single(out, src, [c * REC for c in send_counts], [c * REC for c in recv_counts], group=group)
+    return out if not via_cpu else out.to(resp.device)
+
+
+def dist_round(db, batch, scheme, result=None, group=None, via_cpu=False, **kw):
+    """One partitioned submit on this rank (all ranks call it collectively)."""
+    flags = kw.pop("flags", 0) | G.CC_FLAG_PARTITIONED
+    res = db.submit(batch, scheme, flags=flags, result=result, **kw)
+    send, counts = db.part_send()
+    recv, recv_counts = exchange(send, counts, group, via_cpu)
+    resp = db.part_apply(recv)
+    db.stream.synchronize()
+    back = give_back(resp, recv_counts, counts, group, via_cpu)
+    db.part_finish(back)
+    return res
+
+
+def loopback_round(dbs, batches, scheme, results=None, **kw):
+    """G partitions on one GPU: the same protocol, the all-to-all being slicing and
+    concatenation of device buffers."""
+    flags = kw.pop("flags", 0) | G.CC_FLAG_PARTITIONED
+    res = [db.submit(b, scheme, flags=flags, result=None if results is None else results[i], **kw)
+           for i, (db, b) in enumerate(zip(dbs, batches))]
+    sends = [db.part_send() for db in dbs]
+    world = len(dbs)
+    offs = []
+    for buf, counts in sends:
+        o = [0]
+        for c in counts:
+            o.append(o[-1] + c * REC)
+        offs.append(o)
+    recvs, recv_parts = [], []
+    for d in range(world):
+        parts = [sends[s][0][offs[s][d]:offs[s][d + 1]] for s in range(world)]
+        recv_parts.append([p.numel() for p in parts])
+        recvs.append(torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8))
+    resps = []
+    for d, db in enumerate(dbs):
+        resps.append(db.part_apply(recvs[d]))
+        db.stream.synchronize()
+    for s, db in enumerate(dbs):
+        pieces = []
+        for d in range(world):
+            start = sum(recv_parts[d][:s])
+            pieces.append(resps[d][start:start + recv_parts[d][s]])
+        back = torch.cat(pieces)
+        db.part_finish(back)
+    return res
