@@ -44,6 +44,11 @@ def parse():
     ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="ycsb", choices=["ycsb", "tpcc"],
+                    help="ycsb = configs[1] (default); tpcc = configs[4]: W warehouses partitioned over the ranks")
+    ap.add_argument("--warehouses", type=int, default=512)
+    ap.add_argument("--tpcc-batch", type=int, default=65536, help="transactions per rank per step")
+    ap.add_argument("--tpcc-mix", type=int, default=5114, help="NewOrder share in 1/10,000 (45:43, PAPER.md:468)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -384,11 +389,96 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world):
             "note": "host wall clock around import(H2D) + submit x schemes + D2H of results"}
 
 
+def run_tpcc(args, rank, world, local):
+    """configs[4]: TPC-C with W warehouses partitioned by contiguous ranges over the
+    ranks; each rank runs its own batch of home transactions; cross-partition
+    transactions go through phase B (two NCCL all-to-alls per step)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_10158_b200.api import DB, Result
+    from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
+    from paper_2406_10158_b200.partition import dist_round
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    schemes = args.schemes.split(",")
+    W = args.warehouses
+    wpr = W // world
+    n = args.tpcc_batch
+    db = DB(local, rank=rank, world=world)
+    db.load_tpcc(W, 1, n, w_first=rank * wpr, w_count=wpr)
+    res = {s: Result.alloc(n, 18, dev, stream=db.stream, out_words=48) for s in schemes}
+
+    def step(i):
+        b = db.gen_tpcc(n, 7919 * (rank + 1) + i, args.tpcc_mix, w_lo=rank * wpr, w_hi=(rank + 1) * wpr)
+        for s in schemes:
+            if world > 1:
+                dist_round(db, b, s, result=res[s], bs=8, lanes=32, watchdog_s=60)
+            else:
+                db.submit(b, s, bs=8, lanes=32, result=res[s], watchdog_s=60)
+        return b
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for i in range(args.warmup):
+        bb = step(i)
+        db.sync()
+        bb.free()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bs_ = []
+    barrier()
+    e0.record(db.stream)
+    for i in range(args.steps):
+        bs_.append(step(args.warmup + i))
+    e1.record(db.stream)
+    barrier()
+    clk = clocks.stop()
+    db.sync()
+    ms = e0.elapsed_time(e1)
+    per = {}
+    for s in schemes:
+        h = res[s].stats.cpu().numpy().view(np.uint64)
+        per[s] = {"commits": int(h[0]), "aborts": int(h[1]), "abort_rate": float(h[1]) / max(1, int(h[0]))}
+    for bb in bs_:
+        bb.free()
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = args.steps * n * len(schemes) * world / (ms / 1e3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "txn/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "tpcc_configs4_partitioned", "warehouses": W, "batch_per_rank": n,
+                       "neworder_permyriad": args.tpcc_mix, "schemes": schemes, "lanes_per_txn": 32,
+                       "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else "")},
+            "per_scheme": per, "clocks": clk}), flush=True)
+    db.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "tpcc":
+        run_tpcc(args, rank, world, local)
         return
     run_ours(args, rank, world, local)
 
