@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--bs", type=int, default=32)
     ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
+    ap.add_argument("--index", default="tree", choices=["tree", "binary"],
+                    help="tree = cache-line search tree over the sorted keys (default); binary = PAPER.md:344")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="ycsb", choices=["ycsb", "tpcc"],
                     help="ycsb = configs[1] (default); tpcc = configs[4]: W warehouses partitioned over the ranks")
@@ -192,7 +194,7 @@ def run_reference(args, rank, world):
 def config_of(args, world):
     return {"workload": "ycsb_configs1_10Mrows_64Kx16", "rows": args.rows, "batch": args.batch,
             "ops_per_txn": args.ops, "theta": args.theta, "write_frac": args.write_frac,
-            "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs, "lanes_per_txn": args.lanes,
+            "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs, "lanes_per_txn": args.lanes, "index": args.index,
             "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (1.34 GB table, 168 MB CC words)"}
 
 
@@ -218,10 +220,13 @@ def run_ours(args, rank, world, local):
     res = {s: Result.alloc(args.batch, args.ops, dev, stream=db.stream) for s in schemes}
     stream = db.stream   # every library launch goes to this stream; events are recorded on it
 
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY
+    xflags = CC_FLAG_INDEX_BINARY if args.index == "binary" else 0
+
     def step(i, timing=False):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
         for s in schemes:
-            db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING if timing else 0,
+            db.submit(b, s, wd=args.wd, bs=args.bs, flags=xflags | (CC_FLAG_TIMING if timing else 0),
                       result=res[s], watchdog_s=60, lanes=args.lanes)
         return b
 
@@ -270,7 +275,8 @@ def run_ours(args, rank, world, local):
     exec_ms_total, alg_bytes_total = 0.0, 0
     for s in schemes:
         db.timing(reset=True)
-        db.submit(b, s, wd=args.wd, bs=args.bs, flags=CC_FLAG_TIMING, result=res[s], watchdog_s=60, lanes=args.lanes)
+        db.submit(b, s, wd=args.wd, bs=args.bs, flags=xflags | CC_FLAG_TIMING, result=res[s], watchdog_s=60,
+                  lanes=args.lanes)
         db.sync()
         pm, _ = db.timing(reset=True)
         per[s]["exec_ms"] = pm[2]
@@ -281,7 +287,7 @@ def run_ours(args, rank, world, local):
         exec_ms_total += pm[2]
         alg_bytes_total += ab
     # ---- e2e through the public API with host buffers
-    e2e = run_e2e(args, db, bk, bo, schemes, res, dev, stream, barrier, world)
+    e2e = run_e2e(args, db, bk, bo, schemes, res, dev, stream, barrier, world, xflags)
     b.free()
 
     ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -327,7 +333,7 @@ def run_ours(args, rank, world, local):
 
 def config_key(args):
     return (f"ycsb rows={args.rows} batch={args.batch} K={args.ops} theta={args.theta} W={args.write_frac} "
-            f"wd={args.wd} bs={args.bs} lanes={args.lanes}")
+            f"wd={args.wd} bs={args.bs} lanes={args.lanes} index={args.index}")
 
 
 def launches_per_step(schemes):
@@ -345,7 +351,7 @@ def launches_per_step(schemes):
     return n
 
 
-def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world):
+def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xflags=0):
     """Same metric through the public C-ABI with HOST buffers: every step imports the
     batch from pinned host memory (cc_batch_import_ycsb, src_on_device=0), runs all
     schemes, and reads each scheme's commit flags, commit positions and read outputs
@@ -362,7 +368,8 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world):
         b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
         with torch.cuda.stream(stream):
             for s in schemes:
-                db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes)
+                db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes,
+                          flags=xflags)
                 c, p_, r = outs[s]
                 c.copy_(res[s].committed, non_blocking=True)
                 p_.copy_(res[s].commit_pos, non_blocking=True)

@@ -111,6 +111,13 @@ cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_ke
                           const uint64_t *row_ids, uint64_t n, int src_on_device,
                           uint32_t *index_id);
 
+/* Batch index lookup (SPEC.md:47 index_lookup): rows_out[i] = row id of keys[i], or
+ * 2^64-1 when the key is absent (KeyNotFound).  keys / rows_out are device
+ * arrays of n u64 (caller-owned).  flags: CC_FLAG_INDEX_BINARY selects the paper's
+ * binary search, otherwise the cache-line tree; results are identical.  Async. */
+cc_status cc_index_lookup(cc_db db, uint32_t index_id, const uint64_t *keys, uint64_t n,
+                          uint64_t *rows_out, uint32_t flags);
+
 /* ----------------------------------------------------------------- YCSB
  * YCSB table: n_rows rows of 16 x u64 (128 B); word j of row k is
  * mix64(seed ^ (16k + j)) for j < 15 and word 15 (a write counter) is 0, where mix64
@@ -201,6 +208,10 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         cc_part_apply / cc_part_finish */
 #define CC_FLAG_PART_ALL 0x8u        /* as PARTITIONED, but every transaction takes phase B
                                         (exercises phase B on one partition) */
+#define CC_FLAG_INDEX_BINARY 0x10u   /* index lookups by plain binary search over the sorted
+                                        array (the paper's index) instead of the
+                                        default cache-line search tree over the same array
+                                        (identical results) */
 
 typedef struct {
     cc_scheme scheme;

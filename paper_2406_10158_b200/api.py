@@ -200,6 +200,29 @@ class DB:
     def read_tpcc(self, names=None) -> dict:
         return {k: self.read_table(self.tpcc_ids[k]) for k in (names or G.TPCC_TABLES)}
 
+    def create_table(self, name: str, row_bytes: int, rows: int) -> int:
+        tid = ctypes.c_uint32()
+        self._chk(G.lib().cc_table_create(self.h, name.encode(), row_bytes, rows, ctypes.byref(tid)))
+        return tid.value
+
+    def create_index(self, table_id: int, sorted_keys, row_ids) -> int:
+        k = np.ascontiguousarray(sorted_keys, dtype=np.uint64)
+        r = np.ascontiguousarray(row_ids, dtype=np.uint64)
+        iid = ctypes.c_uint32()
+        self._chk(G.lib().cc_index_create(self.h, table_id, k.ctypes.data, r.ctypes.data, k.size, 0,
+                                          ctypes.byref(iid)))
+        return iid.value
+
+    def index_lookup(self, index_id: int, keys, binary: bool = False) -> np.ndarray:
+        dev = torch.device("cuda", self.device)
+        with torch.cuda.stream(self.stream):
+            k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
+            out = torch.empty_like(k)
+        self._chk(G.lib().cc_index_lookup(self.h, index_id, k.data_ptr(), k.numel(), out.data_ptr(),
+                                          G.CC_FLAG_INDEX_BINARY if binary else 0))
+        self.stream.synchronize()
+        return out.cpu().numpy().view(np.uint64)
+
     def read_table(self, table_id: int = 0) -> np.ndarray:
         rows, rb = ctypes.c_uint64(), ctypes.c_uint32()
         self._chk(G.lib().cc_table_info(self.h, table_id, ctypes.byref(rows), ctypes.byref(rb)))

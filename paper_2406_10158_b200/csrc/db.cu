@@ -33,9 +33,46 @@ struct Table {
 struct Index {
     uint32_t table;
     uint64_t n;
-    u64 *keys;
+    u64 *keys;     // sorted keys, padded with ~0 to a multiple of 16 (tree leaves)
     u64 *rowids;
+    std::vector<u64 *> levels;   // cache-line tree levels above the leaves
+    std::vector<uint64_t> lens;
 };
+
+// Build the separator levels of the cache-line search tree over ix.keys (device).
+static cudaError_t build_tree(Index &ix, cudaStream_t s) {
+    uint64_t n_in = ix.n;
+    const u64 *in = ix.keys;
+    uint64_t padded = (n_in + 15) / 16 * 16;
+    ix.lens.push_back(padded);
+    while (padded > 16) {
+        const uint64_t nodes = padded / 16;
+        const uint64_t out_padded = (nodes + 15) / 16 * 16;
+        u64 *out = nullptr;
+        cudaError_t e = cudaMalloc((void **)&out, out_padded * 8);
+        if (e) return e;
+        e = launch_tree_level(in, n_in, out, out_padded, s);
+        if (e) return e;
+        ix.levels.push_back(out);
+        ix.lens.push_back(out_padded);
+        in = out;
+        n_in = nodes;
+        padded = out_padded;
+    }
+    return cudaStreamSynchronize(s);
+}
+
+static TreeIndex tree_of(const Index &ix) {
+    TreeIndex t{};
+    t.n_levels = 1 + (int)ix.levels.size();
+    t.lv[0] = ix.keys;
+    t.len[0] = ix.lens[0];
+    for (size_t k = 0; k < ix.levels.size() && k + 1 < (size_t)IDX_MAX_LEVELS; k++) {
+        t.lv[k + 1] = ix.levels[k];
+        t.len[k + 1] = ix.lens[k + 1];
+    }
+    return t;
+}
 
 struct cc_batch_s {
     uint32_t kind;
@@ -206,7 +243,11 @@ cc_status cc_db_destroy(cc_db db) {
     cudaSetDevice(db->device);
     cudaStreamSynchronize(db->stream);
     for (auto &t : db->tables) cudaFree(t.d);
-    for (auto &i : db->indexes) { cudaFree(i.keys); cudaFree(i.rowids); }
+    for (auto &i : db->indexes) {
+        cudaFree(i.keys);
+        cudaFree(i.rowids);
+        for (u64 *l : i.levels) cudaFree(l);
+    }
     for (void *p : db->snap) cudaFree(p);
     for (auto *b : db->batches) { cudaFree(b->keys); cudaFree(b->ops); cudaFree(b->tx); delete b; }
     cudaFree(db->tpcc.nidx_start); cudaFree(db->tpcc.nidx_count); cudaFree(db->tpcc.nidx_rows);
@@ -316,15 +357,35 @@ cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_ke
     }
     for (uint64_t i = 0; i < n; i++) {
         if (i && k[i] <= k[i - 1]) return fail(db, CC_ERR_INVALID_ARG, "index keys not strictly ascending");
+        if (k[i] == ~0ull) return fail(db, CC_ERR_INVALID_ARG, "key 2^64-1 is reserved");
         if (r[i] >= db->tables[table_id].rows) return fail(db, CC_ERR_INVALID_ARG, "row id out of table");
     }
-    Index ix{table_id, n, nullptr, nullptr};
-    CUDA_TRY(db, dalloc(&ix.keys, n * 8));
+    Index ix{table_id, n, nullptr, nullptr, {}, {}};
+    const uint64_t padded = (n + 15) / 16 * 16;
+    CUDA_TRY(db, dalloc(&ix.keys, padded * 8));
     CUDA_TRY(db, dalloc(&ix.rowids, n * 8));
-    CUDA_TRY(db, cudaMemcpy(ix.keys, k, n * 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(db, cudaMemcpy(ix.rowids, r, n * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(db, launch_fill_u64(ix.keys + n, ~0ull, padded - n, db->stream));
+    CUDA_TRY(db, cudaMemcpyAsync(ix.keys, k, n * 8, cudaMemcpyHostToDevice, db->stream));
+    CUDA_TRY(db, cudaMemcpyAsync(ix.rowids, r, n * 8, cudaMemcpyHostToDevice, db->stream));
+    CUDA_TRY(db, build_tree(ix, db->stream));
     db->indexes.push_back(ix);
     *index_id = (uint32_t)db->indexes.size() - 1;
+    return CC_OK;
+}
+
+cc_status cc_index_lookup(cc_db db, uint32_t index_id, const uint64_t *keys, uint64_t n, uint64_t *rows_out,
+                          uint32_t flags) {
+    CHECK_DB(db);
+    if (index_id >= db->indexes.size() || (n && (!keys || !rows_out)))
+        return fail(db, CC_ERR_INVALID_ARG, "cc_index_lookup: bad args");
+    const Index &ix = db->indexes[index_id];
+    YcsbParams y{};
+    y.idx_keys = ix.keys;
+    y.idx_rows = ix.rowids;
+    y.idx_n = ix.n;
+    y.tree = tree_of(ix);
+    y.binary = (flags & CC_FLAG_INDEX_BINARY) ? 1 : 0;
+    CUDA_TRY(db, launch_index_lookup(y, (const u64 *)keys, n, (u64 *)rows_out, db->stream));
     return CC_OK;
 }
 
@@ -339,11 +400,13 @@ cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *d) {
     if (st) return st;
     Table &t = db->tables[tid];
     CUDA_TRY(db, launch_ycsb_init_rows((u64 *)t.d, 0, d->n_rows, d->seed, db->stream));
-    Index ix{tid, d->n_rows, nullptr, nullptr};
-    CUDA_TRY(db, dalloc(&ix.keys, d->n_rows * 8));
+    Index ix{tid, d->n_rows, nullptr, nullptr, {}, {}};
+    const uint64_t padded = (d->n_rows + 15) / 16 * 16;
+    CUDA_TRY(db, dalloc(&ix.keys, padded * 8));
     CUDA_TRY(db, dalloc(&ix.rowids, d->n_rows * 8));
+    CUDA_TRY(db, launch_fill_u64(ix.keys + d->n_rows, ~0ull, padded - d->n_rows, db->stream));
     CUDA_TRY(db, launch_identity_index(ix.keys, ix.rowids, d->n_rows, db->stream));
-    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, build_tree(ix, db->stream));
     db->indexes.push_back(ix);
     db->ycsb_table = (int)tid;
     db->ycsb_index = (int)db->indexes.size() - 1;
@@ -738,6 +801,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         y.idx_keys = ix.keys;
         y.idx_rows = ix.rowids;
         y.idx_n = ix.n;
+        y.tree = tree_of(ix);
+        y.binary = (desc->flags & CC_FLAG_INDEX_BINARY) ? 1 : 0;
         y.rows = (u64 *)t.d;
         y.n_rows = t.rows;
     }

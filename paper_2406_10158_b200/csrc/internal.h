@@ -62,6 +62,17 @@ struct ExecParams {
     const uint8_t *skip;         // partitioned TPC-C: 1 = distributed txn, left to phase B
 };
 
+// Cache-line search tree over a sorted key array (same lower-bound result as the
+// binary search of PAPER.md:344): the sorted array, padded with ~0 to a multiple of 16,
+// is the leaf level; level l+1 holds the last key of every 16-entry node of level l;
+// the top level has <= 16 entries.  levels[0] = leaves.
+constexpr int IDX_MAX_LEVELS = 10;
+struct TreeIndex {
+    const unsigned long long *lv[IDX_MAX_LEVELS];
+    unsigned long long len[IDX_MAX_LEVELS];   // padded lengths (multiples of 16)
+    int n_levels;
+};
+
 // YCSB workload parameters.
 struct YcsbParams {
     const uint32_t *keys;        // n_txn*K primary keys
@@ -69,6 +80,8 @@ struct YcsbParams {
     const unsigned long long *idx_keys;  // sorted-array index
     const unsigned long long *idx_rows;
     unsigned long long idx_n;
+    TreeIndex tree;              // same keys, cache-line tree layout (f-3)
+    int binary;                  // 1 = the paper's plain binary search
     unsigned long long *rows;    // 16 x u64 per row
     unsigned long long n_rows;
 };
@@ -137,6 +150,11 @@ cudaError_t launch_ycsb_init_rows(unsigned long long *rows, uint64_t first, uint
                                   uint64_t seed, cudaStream_t s);
 cudaError_t launch_identity_index(unsigned long long *keys, unsigned long long *rows,
                                   uint64_t n, cudaStream_t s);
+cudaError_t launch_tree_level(const unsigned long long *in, uint64_t n_in, unsigned long long *out,
+                              uint64_t n_out_padded, cudaStream_t s);
+cudaError_t launch_index_lookup(const YcsbParams &y, const unsigned long long *keys, uint64_t n,
+                                unsigned long long *out, cudaStream_t s);
+cudaError_t launch_fill_u64(unsigned long long *p, unsigned long long v, uint64_t n, cudaStream_t s);
 cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                             uint64_t n_rows, double W, uint64_t seed,
                             const unsigned long long *T, uint64_t mult, Ctl *ctl,

@@ -23,9 +23,33 @@ struct YcsbWL {
         u64 out, nf, n15;
     };
 
-    // Sorted-array index lookup: branch-free binary search; returns the
-    // row or ~0 for KeyNotFound.
+    // Index lookup: lower bound of key in the sorted key array, returns
+    // the row or ~0 for KeyNotFound.  Default: descend the cache-line tree
+    // (one 128 B node of 16 keys per level: count keys < key); CC_FLAG_INDEX_BINARY:
+    // the paper's branch-free binary search.
     static GC_DEV u64 lookup(const YcsbParams &y, u64 key) {
+        if (!y.binary) return tree_lookup(y, key);
+        return binary_lookup(y, key);
+    }
+    static GC_DEV u64 tree_lookup(const YcsbParams &y, u64 key) {
+        u64 node = 0;
+        for (int l = y.tree.n_levels - 1; l >= 0; l--) {
+            const u64 *nd = y.tree.lv[l] + node * 16;
+            u32 j = 0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) {
+                u64 a, b;
+                asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(nd + 2 * w));
+                j += (a < key) + (b < key);
+            }
+            if (j == 16) return ~0ull;   // key above every key
+            node = node * 16 + j;
+        }
+        const u64 pos = node;
+        if (pos >= y.idx_n || __ldg(y.idx_keys + pos) != key) return ~0ull;
+        return __ldg(y.idx_rows + pos);
+    }
+    static GC_DEV u64 binary_lookup(const YcsbParams &y, u64 key) {
         const u64 *b = y.idx_keys;
         u64 n = y.idx_n;
         while (n > 1) {
@@ -63,6 +87,36 @@ struct YcsbWL {
             b[i] = y.idx_keys;
         }
         if (p.acc_rec) return p.K;
+        if (!y.binary) {   // tree: the K descents in lockstep, one level at a time
+            u64 node[MAXK];
+#pragma unroll
+            for (int i = 0; i < MAXK; i++) node[i] = 0;
+            bool ok = true;
+            for (int l = y.tree.n_levels - 1; l >= 0; l--) {
+                const u64 *lv = y.tree.lv[l];
+#pragma unroll
+                for (int i = 0; i < MAXK; i++)
+                    if (i < (int)p.K) {
+                        const u64 *nd = lv + node[i] * 16;
+                        u32 j = 0;
+#pragma unroll
+                        for (int w = 0; w < 8; w++) {
+                            u64 a, b;
+                            asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(nd + 2 * w));
+                            j += (a < key[i]) + (b < key[i]);
+                        }
+                        ok &= j < 16;
+                        node[i] = node[i] * 16 + (j < 16 ? j : 0);
+                    }
+            }
+#pragma unroll
+            for (int i = 0; i < MAXK; i++)
+                if (i < (int)p.K) {
+                    if (node[i] >= y.idx_n || __ldg(y.idx_keys + node[i]) != key[i]) ok = false;
+                    else L[i].rec = (u32)__ldg(y.idx_rows + node[i]);
+                }
+            return ok ? p.K : 0xFFFFFFFFu;
+        }
         u64 n = y.idx_n;
         while (n > 1) {
             const u64 half = n >> 1;
@@ -319,4 +373,34 @@ cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32
     return cudaGetLastError();
 }
 
+}  // namespace gcctb
+
+namespace gcctb {
+__global__ void index_lookup_kernel(YcsbParams y, const u64 *keys, uint64_t n, u64 *out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = YcsbWL::lookup(y, keys[i]);
+}
+cudaError_t launch_index_lookup(const YcsbParams &y, const u64 *keys, uint64_t n, u64 *out, cudaStream_t s) {
+    if (n) index_lookup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(y, keys, n, out);
+    return cudaGetLastError();
+}
+// one tree level: out[c] = in[min(16c + 15, n_in - 1)] (the last key of node c), ~0 padding
+__global__ void tree_level_kernel(const u64 *in, uint64_t n_in, u64 *out, uint64_t n_out_padded) {
+    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_out_padded) return;
+    const uint64_t n_nodes = (n_in + 15) / 16;
+    out[c] = c < n_nodes ? in[min(16 * c + 15, n_in - 1)] : ~0ull;
+}
+cudaError_t launch_tree_level(const u64 *in, uint64_t n_in, u64 *out, uint64_t n_out_padded, cudaStream_t s) {
+    tree_level_kernel<<<(unsigned)((n_out_padded + 255) / 256), 256, 0, s>>>(in, n_in, out, n_out_padded);
+    return cudaGetLastError();
+}
+__global__ void fill_u64_kernel(u64 *p, u64 v, uint64_t n) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+cudaError_t launch_fill_u64(u64 *p, u64 v, uint64_t n, cudaStream_t s) {
+    if (n) fill_u64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, v, n);
+    return cudaGetLastError();
+}
 }  // namespace gcctb

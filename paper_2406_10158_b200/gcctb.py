@@ -24,6 +24,7 @@ CC_FLAG_IMMEDIATE_RETRY = 0x1
 CC_FLAG_TIMING = 0x2
 CC_FLAG_PARTITIONED = 0x4
 CC_FLAG_PART_ALL = 0x8
+CC_FLAG_INDEX_BINARY = 0x10
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16
 
@@ -94,6 +95,7 @@ _SIGS = {
     "cc_index_create": (ctypes.c_int, [_P, ctypes.c_uint32, _P, _P, ctypes.c_uint64, ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_uint32)]),
     "cc_load_ycsb": (ctypes.c_int, [_P, ctypes.POINTER(cc_ycsb_db_desc)]),
+    "cc_index_lookup": (ctypes.c_int, [_P, ctypes.c_uint32, _P, ctypes.c_uint64, _P, ctypes.c_uint32]),
     "cc_batch_gen_ycsb": (ctypes.c_int, [_P, ctypes.POINTER(cc_ycsb_gen_desc), ctypes.POINTER(_P)]),
     "cc_batch_import_ycsb": (ctypes.c_int, [_P, _P, _P, ctypes.c_uint32, ctypes.c_uint32,
                                             ctypes.c_int, ctypes.POINTER(_P)]),

@@ -203,3 +203,43 @@ def test_ts_overflow_is_reported(c1):
     except CCError as e:
         assert "TS_OVERFLOW" in str(e) or "WATCHDOG" in str(e)
     b.free()
+
+
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 255, 4097, 300001])
+def test_index_lookup_tree_and_binary(torch_cuda, n):
+    """the row of a present key, KeyNotFound (2^64-1) otherwise; the
+    cache-line tree and the paper's binary search agree with numpy.searchsorted."""
+    from paper_2406_10158_b200.api import DB
+    rng = np.random.default_rng(n)
+    keys = np.unique(rng.integers(0, 1 << 62, size=n * 2, dtype=np.uint64))[:n]
+    keys.sort()
+    n = keys.size
+    rows = rng.permutation(n).astype(np.uint64)
+    db = DB(0)
+    tid = db.create_table("t", 8, n)
+    iid = db.create_index(tid, keys, rows)
+    probe = np.concatenate([keys, keys + np.uint64(1), np.array([0, (1 << 63)], np.uint64), keys[:3] - np.uint64(1)])
+    pos = np.searchsorted(keys, probe)
+    hit = (pos < n) & (keys[np.minimum(pos, n - 1)] == probe)
+    exp = np.where(hit, rows[np.minimum(pos, n - 1)], np.uint64((1 << 64) - 1))
+    for binary in (False, True):
+        got = db.index_lookup(iid, probe, binary=binary)
+        assert np.array_equal(got, exp), binary
+    db.close()
+
+
+@pytest.mark.parametrize("scheme", ["tpl_nw", "silo", "mvcc", "gacco"])
+def test_c1_parity_binary_index(c1, orc, scheme):
+    """The paper's binary-search index (CC_FLAG_INDEX_BINARY) gives the same results."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 44, T, A)
+    keys, ops = orc.ycsb_gen(44, 1024, 1024, 4, 0.5, T, A)
+    for lanes in (1, 4):
+        db.snapshot(False)
+        res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, flags=CC_FLAG_INDEX_BINARY)
+        db.sync()
+        orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    b.free()
