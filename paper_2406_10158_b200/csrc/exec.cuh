@@ -528,7 +528,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
 }
 
 template <int S, class WL>
-__global__ void __launch_bounds__(1024) exec_thread_kernel(ExecParams p, typename WL::Params y) {
+__global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, typename WL::Params y) {
     const u32 lane = threadIdx.x & 31u;
     if (lane >= (1u << p.wd)) return;   // idle lanes exit at once
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
@@ -745,7 +745,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
 }
 
 template <int S, class WL, int G>
-__global__ void __launch_bounds__(1024) exec_tile_kernel(ExecParams p, typename WL::Params y) {
+__global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typename WL::Params y) {
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const u32 li = tile.thread_rank();
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);

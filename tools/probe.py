@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--binary", action="store_true")
+    ap.add_argument("--grid", type=int, default=0)
     a = ap.parse_args()
     db = DB(0)
     db.load_ycsb(a.rows, 1)
@@ -36,15 +37,15 @@ def main():
         T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
         b = db.gen_ycsb(a.batch, a.K, a.W, 3, T, A)
         for s in a.schemes.split(","):
-            db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=0x10 if a.binary else 0)
+            db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=0x10 if a.binary else 0, grid=a.grid)
             db.sync()
             db.timing(reset=True)
             for _ in range(a.reps):
-                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | (0x10 if a.binary else 0), watchdog_s=20, lanes=a.lanes)
+                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | (0x10 if a.binary else 0), watchdog_s=20, lanes=a.lanes, grid=a.grid)
             st = db.sync()
             ms, n = db.timing(reset=True)
             per = [m / n for m in ms]
-            row = dict(theta=th, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, index='binary' if a.binary else 'tree', txn_s=a.batch / (per[4] / 1e3), abort_rate=st.aborts / st.commits,
+            row = dict(theta=th, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid, index='binary' if a.binary else 'tree', txn_s=a.batch / (per[4] / 1e3), abort_rate=st.aborts / st.commits,
                        ms_reset=per[0], ms_prep=per[1], ms_exec=per[2], ms_emit=per[3], ms_total=per[4])
             out.append(row)
             print(json.dumps(row), flush=True)
