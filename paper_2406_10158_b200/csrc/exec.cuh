@@ -68,11 +68,11 @@ GC_DEV u64 agg_fetch_add(u64 *ctr) {
 // lockstep, so two transactions with crossed read/write sets can otherwise lock,
 // fail each other's validation and retry in perfect symmetry forever (an OCC livelock
 // the paper's immediate restart, is exposed to as well).  Delay is
-// uniform in [0, 64 ns << min(restarts, 14)) from a hash of (gid, restarts): <= 16 us
-// for the first 8 restarts, growing to 1 ms only for pathological retry storms (basic
-// TO under a read-hot key), which otherwise burn 31-bit timestamps.
+// uniform in [0, 64 ns << min(restarts, 10)) from a hash of (gid, restarts): at most
+// ~65 us, which also rate-limits retry storms (basic TO under a read-hot key) that
+// would otherwise burn 31-bit timestamps without stretching a batch tail.
 GC_DEV void abort_backoff(u32 gid, u32 restarts) {
-    const u32 sh = restarts < 14 ? restarts : 14;
+    const u32 sh = restarts < 10 ? restarts : 10;
     const u32 cap = 64u << sh;
     u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % cap);
     while (d > 0) {
