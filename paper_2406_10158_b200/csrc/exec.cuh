@@ -68,11 +68,16 @@ GC_DEV u64 agg_fetch_add(u64 *ctr) {
 // lockstep, so two transactions with crossed read/write sets can otherwise lock,
 // fail each other's validation and retry in perfect symmetry forever (an OCC livelock
 // the paper's immediate restart, is exposed to as well).  Delay is
-// uniform in [0, 64 ns << min(restarts, 10)) from a hash of (gid, restarts): at most
-// ~65 us, which also rate-limits retry storms (basic TO under a read-hot key) that
-// would otherwise burn 31-bit timestamps without stretching a batch tail.
+// uniform in [0, 64 ns << sh) from a hash of (gid, restarts), sh = min(restarts, cap).
+// cap = 10 (~65 us) keeps batch tails short for lock / OCC schemes; timestamp schemes
+// (TO, MVCC) and any transaction past 12 restarts (a retry storm, e.g. basic TO under a
+// read-hot key, which would otherwise burn 31-bit timestamps) use cap 14
+// (~1 ms).  Measured: profiles/r01_probe_v7*.jsonl vs v6.
+template <int S>
 GC_DEV void abort_backoff(u32 gid, u32 restarts) {
-    const u32 sh = restarts < 10 ? restarts : 10;
+    constexpr u32 CAP = (S == CC_TO || S == CC_MVCC) ? 14u : 10u;
+    const u32 cap_sh = restarts < 12 ? CAP : 14u;
+    const u32 sh = restarts < cap_sh ? restarts : cap_sh;
     const u32 cap = 64u << sh;
     u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % cap);
     while (d > 0) {
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
             if (r == RES_FATAL || DET) return;
             const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
             p.restarts[gid] = nr;
-            abort_backoff(gid, nr);
+            abort_backoff<S>(gid, nr);
             if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) break;   // a6
         }
     }
@@ -786,7 +791,7 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
             if (li == 0) {
                 const u32 nr = p.restarts[gid] + 1;
                 p.restarts[gid] = nr;
-                abort_backoff(gid, nr);
+                abort_backoff<S>(gid, nr);
                 push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
             }
             if (tile.shfl(push, 0)) break;
