@@ -33,6 +33,8 @@ struct Th {
     u64 deadline;
     const ExecParams *p;
     u32 polls;
+    u64 *cw;   // lock word whose holder caused the last abort (nullptr: none)
+    u64 cv;    // its value at that moment
 };
 
 GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err.v, 0ull, code); }
@@ -85,6 +87,28 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
         __nanosleep(s);
         d -= s;
     }
+}
+
+// Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
+// no-wait / OCC semantics are unchanged -- until that lock word changes (its holder
+// committed or aborted), bounded by the backoff cap, then add a little jitter;
+// otherwise fall back to the randomised backoff.  This replaces a blind sleep (during
+// which the lock is often already free) by one L2 round trip.
+template <int S>
+GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
+    if (th.cw) {
+        const u32 sh = restarts < 10 ? restarts : 10;
+        const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
+        unsigned ns = 32;
+        while (ld_relaxed(th.cw) == th.cv && globaltimer_ns() < limit) {
+            __nanosleep(ns);
+            ns = ns < 256 ? ns * 2 : 256;
+        }
+        __nanosleep((u32)(mix64(((u64)gid << 32) | restarts) & 255u));
+        th.cw = nullptr;
+        return;
+    }
+    abort_backoff<S>(gid, restarts);
 }
 
 // ------------------------------------------------------------------ queue (a6)
@@ -161,7 +185,7 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 // One acquisition step.  Returns 0 granted, 1 wait (wait-die older requester, or the
 // CAS lost a race), 2 die (conflict under no-wait, or younger requester).
 template <bool WD>
-GC_DEV int tpl_try(u64 *w, bool ex, u32 age) {
+GC_DEV int tpl_try(u64 *w, bool ex, u32 age, u64 &seen) {
     u64 v = ld_relaxed(w);
     for (;;) {   // latch-free read-transform-CAS loop
         const u32 cnt = tpl_cnt(v);
@@ -177,6 +201,7 @@ GC_DEV int tpl_try(u64 *w, bool ex, u32 age) {
         if (conflict) {
             // no-wait: abort at once.  wait-die: an older requester
             // (smaller age) waits, a younger one dies.
+            seen = v;
             return (WD && age < tpl_holder(v)) ? 1 : 2;
         }
         const u64 old = cas_acqrel(w, v, nv);
@@ -337,9 +362,10 @@ GC_DEV int occ_snap_step(const ExecParams &p, const typename WL::Params &y, type
 }
 
 // no-wait write lock
-GC_DEV bool occ_lock(u64 *w, u64 &pre) {
+GC_DEV bool occ_lock(u64 *w, u64 &pre, u64 &seen) {
     u64 v = ld_relaxed(w);
     for (int k = 0; k < 8; k++) {
+        seen = v;
         if (v & LOCKB) return false;
         const u64 old = cas_acqrel(w, v, v | LOCKB);
         if (old == v) {
@@ -388,8 +414,10 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (; i < n; i++) {
             Spin sp;
             int st;
-            while ((st = tpl_try<WD>(&p.meta[L[i].rec], L[i].w, age)) == ST_WAIT)
+            u64 seen = 0;
+            while ((st = tpl_try<WD>(&p.meta[L[i].rec], L[i].w, age, seen)) == ST_WAIT)
                 if (!sp.wait(th)) { st = -1; break; }
+            if (st == ST_ABORT) { th.cw = &p.meta[L[i].rec]; th.cv = seen; }
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
             WL::read(y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
         }
@@ -453,8 +481,12 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         bool ok = true;
         for (u32 i = 0; i < n && ok; i++)
             if (L[i].w) {
-                if (occ_lock(&p.meta[L[i].rec], pre[i])) locked |= 1u << i;
-                else ok = false;
+                u64 seen = 0;
+                if (occ_lock(&p.meta[L[i].rec], pre[i], seen)) locked |= 1u << i;
+                else {
+                    ok = false;
+                    if (seen & LOCKB) { th.cw = &p.meta[L[i].rec]; th.cv = seen; }
+                }
             }
         u64 ticket = 0, cts = 0;
         if (ok && S == CC_SILO) {
@@ -540,6 +572,8 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
     Th th;
     th.p = &p;
     th.polls = 0;
+    th.cw = nullptr;
+    th.cv = 0;
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L[WL::MAXK];
     Claim cl;
@@ -568,7 +602,7 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
             if (r == RES_FATAL || DET) return;
             const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
             p.restarts[gid] = nr;
-            abort_backoff<S>(gid, nr);
+            retry_pace<S>(th, gid, nr);
             if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) break;   // a6
         }
     }
@@ -590,12 +624,17 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         Spin sp;
         for (;;) {
             int st = ST_DONE;
+            u64 seen = 0;
             if (act && !held) {
-                st = tpl_try<WD>(&p.meta[L.rec], L.w, age);
+                st = tpl_try<WD>(&p.meta[L.rec], L.w, age, seen);
                 held = st == ST_DONE;
             }
-            if (tile.any(st == ST_ABORT)) {
+            const unsigned dying = tile.ballot(st == ST_ABORT);
+            if (dying) {
                 if (held) tpl_release_relaxed(&p.meta[L.rec], L.w);
+                const int src = __ffs(dying) - 1;   // remember one conflicting lock for the retry
+                th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
+                th.cv = tile.shfl(seen, src);
                 return RES_ABORT;
             }
             if (tile.all(!act || held)) break;
@@ -667,9 +706,18 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (tile.any(!sp.wait(th))) return RES_FATAL;
         }
         bool locked = false, bad = false;
+        u64 seen = 0;
         if (act && L.w) {
-            locked = occ_lock(&p.meta[L.rec], pre);
+            locked = occ_lock(&p.meta[L.rec], pre, seen);
             bad = !locked;
+        }
+        {
+            const unsigned busy = tile.ballot(bad && (seen & LOCKB));
+            if (busy) {
+                const int src = __ffs(busy) - 1;
+                th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
+                th.cv = tile.shfl(seen, src);
+            }
         }
         u64 ticket = 0, cts = 0;
         if (!tile.any(bad)) {
@@ -757,6 +805,8 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
     Th th;
     th.p = &p;
     th.polls = 0;
+    th.cw = nullptr;
+    th.cv = 0;
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L;
     Claim cl;
@@ -791,7 +841,7 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
             if (li == 0) {
                 const u32 nr = p.restarts[gid] + 1;
                 p.restarts[gid] = nr;
-                abort_backoff<S>(gid, nr);
+                retry_pace<S>(th, gid, nr);
                 push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
             }
             if (tile.shfl(push, 0)) break;

@@ -39,14 +39,24 @@ def main():
         for s in a.schemes.split(","):
             db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=0x10 if a.binary else 0, grid=a.grid)
             db.sync()
-            db.timing(reset=True)
+            tots, execs = [], []
+            aborts = commits = 0
             for _ in range(a.reps):
-                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | (0x10 if a.binary else 0), watchdog_s=20, lanes=a.lanes, grid=a.grid)
-            st = db.sync()
-            ms, n = db.timing(reset=True)
-            per = [m / n for m in ms]
-            row = dict(theta=th, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid, index='binary' if a.binary else 'tree', txn_s=a.batch / (per[4] / 1e3), abort_rate=st.aborts / st.commits,
-                       ms_reset=per[0], ms_prep=per[1], ms_exec=per[2], ms_emit=per[3], ms_total=per[4])
+                db.timing(reset=True)
+                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | (0x10 if a.binary else 0), watchdog_s=20,
+                          lanes=a.lanes, grid=a.grid)
+                st = db.sync()
+                ms, n = db.timing(reset=True)
+                tots.append(ms[4])
+                execs.append(ms[2])
+                aborts += st.aborts
+                commits += st.commits
+            import statistics
+            med = statistics.median(tots)
+            row = dict(theta=th, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid,
+                       index='binary' if a.binary else 'tree', txn_s=a.batch / (med / 1e3),
+                       abort_rate=aborts / commits, ms_total_median=med, ms_total_min=min(tots),
+                       ms_total_max=max(tots), ms_exec_median=statistics.median(execs), reps=a.reps)
             out.append(row)
             print(json.dumps(row), flush=True)
         b.free()
