@@ -34,7 +34,7 @@ struct Th {
     const ExecParams *p;
     u32 polls;
     u64 *cw;   // lock word whose holder caused the last abort (nullptr: none)
-    u64 cv;    // its value at that moment
+    u64 cv;    // wait until (*cw & cv) == 0: the conflicting lock is free
 };
 
 GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err.v, 0ull, code); }
@@ -90,17 +90,18 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
 }
 
 // Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
-// no-wait / OCC semantics are unchanged -- until that lock word changes (its holder
-// committed or aborted), bounded by the backoff cap, then add a little jitter;
-// otherwise fall back to the randomised backoff.  This replaces a blind sleep (during
-// which the lock is often already free) by one L2 round trip.
+// no-wait / OCC semantics are unchanged -- until that lock is free (2PL holder count 0,
+// OCC lock bit clear), bounded by the backoff cap, add a little jitter, and retry;
+// otherwise use the randomised backoff.  This replaces a blind sleep (during which the
+// lock is often already free) by one L2 round trip, without turning a busy shared lock
+// into a retry storm.
 template <int S>
 GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
     if (th.cw) {
         const u32 sh = restarts < 10 ? restarts : 10;
         const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
         unsigned ns = 32;
-        while (ld_relaxed(th.cw) == th.cv && globaltimer_ns() < limit) {
+        while ((ld_relaxed(th.cw) & th.cv) != 0 && globaltimer_ns() < limit) {
             __nanosleep(ns);
             ns = ns < 256 ? ns * 2 : 256;
         }
@@ -417,7 +418,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             u64 seen = 0;
             while ((st = tpl_try<WD>(&p.meta[L[i].rec], L[i].w, age, seen)) == ST_WAIT)
                 if (!sp.wait(th)) { st = -1; break; }
-            if (st == ST_ABORT) { th.cw = &p.meta[L[i].rec]; th.cv = seen; }
+            if (st == ST_ABORT) { th.cw = &p.meta[L[i].rec]; th.cv = M31 << 31; }   // until free
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
             WL::read(y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
         }
@@ -485,7 +486,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
                 if (occ_lock(&p.meta[L[i].rec], pre[i], seen)) locked |= 1u << i;
                 else {
                     ok = false;
-                    if (seen & LOCKB) { th.cw = &p.meta[L[i].rec]; th.cv = seen; }
+                    if (seen & LOCKB) { th.cw = &p.meta[L[i].rec]; th.cv = LOCKB; }   // until unlocked
                 }
             }
         u64 ticket = 0, cts = 0;
@@ -634,7 +635,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 if (held) tpl_release_relaxed(&p.meta[L.rec], L.w);
                 const int src = __ffs(dying) - 1;   // remember one conflicting lock for the retry
                 th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
-                th.cv = tile.shfl(seen, src);
+                th.cv = M31 << 31;                   // wait until its holder count is 0
                 return RES_ABORT;
             }
             if (tile.all(!act || held)) break;
@@ -716,7 +717,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (busy) {
                 const int src = __ffs(busy) - 1;
                 th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
-                th.cv = tile.shfl(seen, src);
+                th.cv = LOCKB;                       // wait until unlocked
             }
         }
         u64 ticket = 0, cts = 0;
