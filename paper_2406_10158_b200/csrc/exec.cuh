@@ -97,7 +97,7 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
 // into a retry storm.
 template <int S>
 GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
-    if (th.cw) {
+    if (th.cw && restarts < 12) {   // past 12 restarts: a storm, use the long backoff
         const u32 sh = restarts < 10 ? restarts : 10;
         const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
         unsigned ns = 32;
@@ -109,6 +109,7 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         th.cw = nullptr;
         return;
     }
+    th.cw = nullptr;
     abort_backoff<S>(gid, restarts);
 }
 
