@@ -208,6 +208,10 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         cc_part_apply / cc_part_finish */
 #define CC_FLAG_PART_ALL 0x8u        /* as PARTITIONED, but every transaction takes phase B
                                         (exercises phase B on one partition) */
+#define CC_FLAG_LATCHED 0x20u        /* Exp-7: every control-word mutation
+                                        under a 32-bit per-word latch instead of one 64-bit CAS */
+#define CC_FLAG_STAGES 0x40u         /* Exp-6: per-stage cycle
+                                        accounting into cc_stats.stage_cycles */
 #define CC_FLAG_INDEX_BINARY 0x10u   /* index lookups by plain binary search over the sorted
                                         array (the paper's index) instead of the
                                         default cache-line search tree over the same array
@@ -257,7 +261,14 @@ typedef struct {
     uint64_t error;         /* device-side cc_status (0 = ok) */
     uint64_t max_rank;      /* GPUTx: number of K-sets - 1 */
     uint64_t ts_last;       /* TO/MVCC: last timestamp drawn */
-    uint64_t reserved[10];
+    uint64_t reserved[2];
+    /* CC_FLAG_STAGES: SM cycles summed over workers (tile mode: each tile's leader lane):
+     * [0] index lookup  [1] timestamp allocation  [2] waiting  [3] CC manager (rest of
+     * committed attempts)  [4] aborted attempts minus their ts allocation, plus retry
+     * pacing  [5] useful row work  [6] attempts.  Preprocessing time is the a3 phase of
+     * cc_timing_read. */
+    uint64_t stage_cycles[7];
+    uint64_t sm_clock_khz;  /* nominal SM clock, to convert cycles */
 } cc_stats;
 
 /* Run batch b under desc->scheme: reset the scheme's CC state (a2), preprocess

@@ -101,6 +101,12 @@ GC_DEV u64 globaltimer_ns() {
     return t;
 }
 
+GC_DEV u64 clk64() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+}
+
 GC_DEV void backoff(unsigned &ns) {
     __nanosleep(ns);
     ns = ns < 256 ? ns * 2 : 256;

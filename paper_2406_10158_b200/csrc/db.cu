@@ -107,6 +107,10 @@ struct cc_db_s {
     std::vector<Table> tables;
     std::vector<Index> indexes;
     uint64_t n_records = 0;
+    uint32_t *latch = nullptr;          // CC_FLAG_LATCHED
+    uint64_t latch_records = 0;
+    u64 *stages = nullptr;              // CC_FLAG_STAGES accumulators
+    int clock_khz = 0;
     u64 *meta = nullptr;
     uint64_t meta_records = 0;
     int ycsb_table = -1, ycsb_index = -1;
@@ -208,6 +212,7 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
     db->world = desc->world;
     if (cudaSetDevice(db->device) != cudaSuccess) { delete db; return CC_ERR_CUDA; }
     cudaDeviceGetAttribute(&db->num_sms, cudaDevAttrMultiProcessorCount, db->device);
+    cudaDeviceGetAttribute(&db->clock_khz, cudaDevAttrClockRate, db->device);
     if (desc->stream) {
         db->stream = (cudaStream_t)desc->stream;
     } else {
@@ -259,6 +264,8 @@ cc_status cc_db_destroy(cc_db db) {
     cudaFree(db->part.k1); cudaFree(db->part.k2); cudaFree(db->part.i1); cudaFree(db->part.i2);
     cudaFree(db->part.tmp);
     cudaFree(db->arena);
+    cudaFree(db->latch);
+    cudaFree(db->stages);
     cudaFree(db->meta);
     cudaFree(db->ctl);
     cudaFree(db->stats_scratch);
@@ -807,6 +814,23 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         y.n_rows = t.rows;
     }
 
+    if (desc->flags & CC_FLAG_LATCHED) {   // one 32-bit latch per control word (Exp-7)
+        if (db->latch_records < db->n_records) {
+            cudaStreamSynchronize(db->stream);
+            cudaFree(db->latch);
+            db->latch = nullptr;
+            CUDA_TRY(db, dalloc(&db->latch, db->n_records * 8));
+            db->latch_records = db->n_records;
+        }
+        CUDA_TRY(db, launch_fill_u64((u64 *)db->latch, 0ull, db->n_records, db->stream));
+        p.latch = db->latch;
+    }
+    if (desc->flags & CC_FLAG_STAGES) {   // 8 totals + 8 words per thread of the grid (<= 2^21 threads)
+        const uint64_t words = 8ull + 8ull * (1ull << 21);
+        if (!db->stages) CUDA_TRY(db, dalloc(&db->stages, words * 8));
+        CUDA_TRY(db, launch_fill_u64(db->stages, 0ull, words, db->stream));
+        p.stages = db->stages;
+    }
     const bool timing = desc->flags & CC_FLAG_TIMING;
     const bool partitioned = (desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) != 0;
     if (partitioned) {
@@ -865,8 +889,10 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         if (per_sm <= 0) return fail(db, CC_ERR_CONFIG, "executor cannot launch %d threads/block", block);
         grid = per_sm * db->num_sms;
     }
+    if ((uint64_t)grid * block > (1ull << 21)) return fail(db, CC_ERR_CONFIG, "grid x block > 2^21 threads");
     if (is_tpcc) CUDA_TRY(db, launch_tpcc_exec(p, tp, grid, block, db->stream));
     else CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, db->stream));
+    if (p.stages) CUDA_TRY(db, launch_stages_reduce(p.stages, (uint64_t)grid * block, db->stream));
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
     if (partitioned) {   // phase B happens in cc_part_apply / cc_part_finish
         db->part.pending = true;
@@ -976,6 +1002,8 @@ cc_status cc_sync(cc_db db, cc_stats *out) {
     s.error = w[3];
     s.max_rank = w[4];
     s.ts_last = w[5];
+    for (int k = 0; k < 7; k++) s.stage_cycles[k] = w[8 + k];
+    s.sm_clock_khz = (uint64_t)db->clock_khz;
     db->last = s;
     if (out) *out = s;
     Ctl c;

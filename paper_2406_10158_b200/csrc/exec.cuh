@@ -33,6 +33,8 @@ struct Th {
     u64 deadline;
     const ExecParams *p;
     u32 polls;
+    bool timing;          // CC_FLAG_STAGES
+    u64 *st;              // this worker's STAGE_WORDS accumulators (global memory), or null
     u64 *cw;   // lock word whose holder caused the last abort (nullptr: none)
     u64 cv;    // wait until (*cw & cv) == 0: the conflicting lock is free
 };
@@ -51,11 +53,76 @@ GC_DEV bool dead(Th &th) {
 struct Spin {
     unsigned ns = 16;
     GC_DEV bool wait(Th &th) {   // false -> give up (error / watchdog)
+        const u64 t0 = th.timing ? clk64() : 0;
         __nanosleep(ns);
         ns = ns < 256 ? ns * 2 : 256;
-        return !dead(th);
+        const bool alive = !dead(th);
+        if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
+        return alive;
     }
 };
+
+// stage timer: adds the elapsed cycles of its scope to one accumulator
+struct StageClock {
+    Th &th;
+    int k;
+    u64 t0;
+    GC_DEV StageClock(Th &t, int stage) : th(t), k(stage), t0(t.timing ? clk64() : 0) {}
+    GC_DEV ~StageClock() {
+        if (th.timing) th.st[k] += clk64() - t0;
+    }
+};
+
+// row work (the "useful" stage) done through these wrappers
+template <class WL>
+GC_DEV void rd(Th &th, const typename WL::Params &y, typename WL::Lane &L, u32 gid, u32 i, const u64 *src) {
+    StageClock c(th, STAGE_USEFUL);
+    WL::read(y, L, gid, i, src);
+}
+template <class WL>
+GC_DEV void inst(Th &th, const typename WL::Params &y, const typename WL::Lane &L, u64 *dst) {
+    StageClock c(th, STAGE_USEFUL);
+    WL::install(y, L, dst);
+}
+
+// per-attempt attribution: a committed attempt's time not spent in row
+// work, waits or timestamp allocation is CC-manager time; an aborted attempt's whole time
+// minus its timestamp allocation is abort time (its row work and waits included).
+struct AttemptClock {
+    Th &th;
+    u64 t0, u0, w0, s0;
+    GC_DEV explicit AttemptClock(Th &t) : th(t), t0(0), u0(0), w0(0), s0(0) {
+        if (t.timing) {
+            t0 = clk64();
+            u0 = t.st[STAGE_USEFUL];
+            w0 = t.st[STAGE_WAIT];
+            s0 = t.st[STAGE_TS];
+        }
+    }
+    GC_DEV void done(bool committed) {
+        if (!th.timing) return;
+        const u64 el = clk64() - t0;
+        const u64 du = th.st[STAGE_USEFUL] - u0, dw = th.st[STAGE_WAIT] - w0, ds = th.st[STAGE_TS] - s0;
+        th.st[STAGE_ATTEMPTS] += 1;
+        if (committed) {
+            th.st[STAGE_CC] += el > du + dw + ds ? el - du - dw - ds : 0;
+        } else {
+            th.st[STAGE_USEFUL] = u0;
+            th.st[STAGE_WAIT] = w0;
+            th.st[STAGE_ABORT] += el > ds ? el - ds : 0;
+        }
+    }
+};
+
+GC_DEV void stages_init(Th &th, const ExecParams &p, bool on) {
+    th.timing = p.stages != nullptr && on;
+    th.st = nullptr;
+    if (th.timing) {   // per-thread slot, reduced by stages_reduce after the kernel
+        const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+        th.st = p.stages + STAGE_WORDS + tid * STAGE_WORDS;
+        for (int k = 0; k < STAGE_WORDS; k++) th.st[k] = 0;
+    }
+}
 
 // warp-aggregated fetch-add over the currently converged lanes
 GC_DEV u64 agg_fetch_add(u64 *ctr) {
@@ -64,6 +131,52 @@ GC_DEV u64 agg_fetch_add(u64 *ctr) {
     if (g.thread_rank() == 0) base = atomicAdd(ctr, (u64)g.size());
     base = g.shfl(base, 0);
     return base + g.thread_rank();
+}
+
+// ------------------------------------------------------------------ control-word ops
+// Latch-free by default: every read-transform-update of a control word is one 64-bit
+// CAS.  With CC_FLAG_LATCHED (Exp-7) every
+// mutation of a control word happens under a 32-bit per-word latch instead (acquire
+// spin, read, compare, write, release); reads stay plain loads.
+GC_DEV void latch_acquire(uint32_t *l) {
+    unsigned ns = 8;
+    for (;;) {
+        uint32_t old;
+        asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(l) : "memory");
+        if (old == 0) return;
+        __nanosleep(ns);
+        ns = ns < 128 ? ns * 2 : 128;
+    }
+}
+GC_DEV void latch_release(uint32_t *l) { st_release32(l, 0u); }
+GC_DEV uint32_t *latch_of(const ExecParams &p, const u64 *w) { return p.latch + (w - p.meta); }
+
+GC_DEV u64 w_cas(const ExecParams &p, u64 *w, u64 expect, u64 desired) {
+    if (!p.latch) return cas_acqrel(w, expect, desired);
+    uint32_t *l = latch_of(p, w);
+    latch_acquire(l);
+    const u64 old = ld_relaxed(w);
+    if (old == expect) st_relaxed(w, desired);
+    latch_release(l);
+    return old;
+}
+GC_DEV void w_store(const ExecParams &p, u64 *w, u64 v) {   // release store
+    if (!p.latch) { st_release(w, v); return; }
+    uint32_t *l = latch_of(p, w);
+    latch_acquire(l);
+    st_relaxed(w, v);
+    latch_release(l);
+}
+GC_DEV void w_store_relaxed(const ExecParams &p, u64 *w, u64 v) {   // after an explicit fence
+    if (!p.latch) { st_relaxed(w, v); return; }
+    w_store(p, w, v);
+}
+GC_DEV void w_add(const ExecParams &p, u64 *w, u64 v) {
+    if (!p.latch) { atom_add_relaxed(w, v); return; }
+    uint32_t *l = latch_of(p, w);
+    latch_acquire(l);
+    st_relaxed(w, ld_relaxed(w) + v);
+    latch_release(l);
 }
 
 // Randomised, bounded exponential backoff after an abort.  Lanes of one warp run in
@@ -187,7 +300,7 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 // One acquisition step.  Returns 0 granted, 1 wait (wait-die older requester, or the
 // CAS lost a race), 2 die (conflict under no-wait, or younger requester).
 template <bool WD>
-GC_DEV int tpl_try(u64 *w, bool ex, u32 age, u64 &seen) {
+GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen) {
     u64 v = ld_relaxed(w);
     for (;;) {   // latch-free read-transform-CAS loop
         const u32 cnt = tpl_cnt(v);
@@ -206,15 +319,15 @@ GC_DEV int tpl_try(u64 *w, bool ex, u32 age, u64 &seen) {
             seen = v;
             return (WD && age < tpl_holder(v)) ? 1 : 2;
         }
-        const u64 old = cas_acqrel(w, v, nv);
+        const u64 old = w_cas(p, w, v, nv);
         if (old == v) return 0;
         v = old;
     }
 }
 
-GC_DEV void tpl_release_relaxed(u64 *w, bool ex) {
-    if (ex) st_relaxed(w, 0ull);
-    else atom_add_relaxed(w, (u64)(-(long long)TPL_ONE));
+GC_DEV void tpl_release_relaxed(const ExecParams &p, u64 *w, bool ex) {
+    if (ex) w_store_relaxed(p, w, 0ull);
+    else w_add(p, w, (u64)(-(long long)TPL_ONE));
 }
 
 // ------------------------------------------------------------------ TO (Table II)
@@ -249,7 +362,7 @@ enum { ST_DONE = 0, ST_WAIT = 1, ST_ABORT = 2, ST_RETRY = 3 };   // RETRY: lost 
 // TO access step for one item (write = read-modify-write).  On success for a write the
 // row is read under the pending bit; for a read it is read between two word loads.
 template <class WL>
-GC_DEV int to_step(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+GC_DEV int to_step(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                    u32 gid, u32 i, u64 ts, bool &pend, u64 &saved) {
     u64 *w = &p.meta[L.rec];
     const u64 *row = WL::row(y, L);
@@ -257,30 +370,30 @@ GC_DEV int to_step(const ExecParams &p, const typename WL::Params &y, typename W
     if (L.w) {
         if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;   // older pending: wait (Z4)
         if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
-        if (cas_acqrel(w, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
+        if (w_cas(p, w, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
         pend = true;
         saved = v;
-        WL::read(y, L, gid, i, row);   // stable: we own the pending bit
+        rd<WL>(th, y, L, gid, i, row);   // stable: we own the pending bit
         return ST_DONE;
     }
     if (ts < to_wts(v)) return ST_ABORT;
     if (v & TO_P) return ST_WAIT;
-    WL::read(y, L, gid, i, row);
+    rd<WL>(th, y, L, gid, i, row);
     fence_acqrel();
     if (to_rts(v) >= ts) return ld_relaxed(w) == v ? ST_DONE : ST_RETRY;
-    return cas_acqrel(w, v, to_make(false, ts, to_wts(v))) == v ? ST_DONE : ST_RETRY;
+    return w_cas(p, w, v, to_make(false, ts, to_wts(v))) == v ? ST_DONE : ST_RETRY;
 }
 
 template <class WL>
-GC_DEV void to_commit(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L, u64 ts) {
-    WL::install(y, L, WL::row(y, L));
+GC_DEV void to_commit(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L, u64 ts) {
+    inst<WL>(th, y, L, WL::row(y, L));
     fence_acqrel();
-    st_relaxed(&p.meta[L.rec], to_make(false, ts, ts));
+    w_store_relaxed(p, &p.meta[L.rec], to_make(false, ts, ts));
 }
 
 // MVCC access step (Z6): writes append at the head only; reads never abort.
 template <class WL>
-GC_DEV int mvcc_step(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                      u32 gid, u32 i, u64 ts, bool &pend, u64 &saved_wts) {
     u64 *lo = &p.meta[2ull * L.rec];
     u64 *hi = lo + 1;
@@ -289,21 +402,21 @@ GC_DEV int mvcc_step(const ExecParams &p, const typename WL::Params &y, typename
     if (L.w) {
         if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;
         if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
-        if (cas_acqrel(lo, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
+        if (w_cas(p, lo, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
         pend = true;
         saved_wts = to_wts(v);
-        WL::read(y, L, gid, i, row);
+        rd<WL>(th, y, L, gid, i, row);
         return ST_DONE;
     }
     if ((v & TO_P) && to_wts(v) < ts) return ST_WAIT;   // older pending writer: its version is ours
     const u64 h = ld_acquire(hi);
     if ((h >> 32) <= ts) {   // head visible: read in place, validate, raise RTS
-        WL::read(y, L, gid, i, row);
+        rd<WL>(th, y, L, gid, i, row);
         fence_acqrel();
         if (ld_relaxed(hi) != h) return ST_RETRY;
         if (to_rts(v) >= ts) return ld_relaxed(lo) == v ? ST_DONE : ST_RETRY;
         const u64 nv = (v & ~(M31 << 31)) | ((ts & M31) << 31);
-        return cas_acqrel(lo, v, nv) == v ? ST_DONE : ST_RETRY;
+        return w_cas(p, lo, v, nv) == v ? ST_DONE : ST_RETRY;
     }
     // walk the history chain for the newest version with begin <= ts
     u64 idx = h & VNONE;
@@ -311,7 +424,7 @@ GC_DEV int mvcc_step(const ExecParams &p, const typename WL::Params &y, typename
         const u64 *node = p.arena + idx * (2 + WL::ROW_WORDS);
         const u64 h0 = ld_cg(node);
         if ((h0 >> 32) <= ts) {
-            WL::read(y, L, gid, i, node + 2);
+            rd<WL>(th, y, L, gid, i, node + 2);
             return ST_DONE;
         }
         idx = h0 & VNONE;
@@ -325,14 +438,14 @@ GC_DEV void mvcc_restore(const ExecParams &p, typename WL::Lane &L, u64 saved_wt
     u64 *lo = &p.meta[2ull * L.rec];
     u64 v = ld_relaxed(lo);
     for (;;) {   // keep RTS raised by readers while we were pending
-        const u64 old = cas_acqrel(lo, v, to_make(false, to_rts(v), saved_wts));
+        const u64 old = w_cas(p, lo, v, to_make(false, to_rts(v), saved_wts));
         if (old == v) return;
         v = old;
     }
 }
 
 template <class WL>
-GC_DEV void mvcc_commit(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+GC_DEV void mvcc_commit(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                         u32 gid, u32 i, u64 ts) {
     u64 *lo = &p.meta[2ull * L.rec];
     u64 *hi = lo + 1;
@@ -342,21 +455,21 @@ GC_DEV void mvcc_commit(const ExecParams &p, const typename WL::Params &y, typen
     st_cg(node, ld_relaxed(hi));   // old head -> history node (begin, prev)
     WL::copy_row(L, row, node + 2);
     fence_acqrel();
-    st_release(hi, (ts << 32) | nidx);   // publish the history, then install in place
+    w_store(p, hi, (ts << 32) | nidx);   // publish the history, then install in place
     fence_acqrel();
-    WL::install(y, L, row);
+    inst<WL>(th, y, L, row);
     fence_acqrel();
-    st_relaxed(lo, to_make(false, ts, ts));
+    w_store_relaxed(p, lo, to_make(false, ts, ts));
 }
 
 // OCC read-phase step: snapshot (word, row, word); spin while locked (Z10).
 template <class WL>
-GC_DEV int occ_snap_step(const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
+GC_DEV int occ_snap_step(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                          u32 gid, u32 i, u64 &obs) {
     u64 *w = &p.meta[L.rec];
     const u64 v1 = ld_acquire(w);
     if (v1 & LOCKB) return ST_WAIT;
-    WL::read(y, L, gid, i, WL::row(y, L));
+    rd<WL>(th, y, L, gid, i, WL::row(y, L));
     fence_acqrel();
     if (ld_relaxed(w) != v1) return ST_RETRY;
     obs = v1;
@@ -364,12 +477,12 @@ GC_DEV int occ_snap_step(const ExecParams &p, const typename WL::Params &y, type
 }
 
 // no-wait write lock
-GC_DEV bool occ_lock(u64 *w, u64 &pre, u64 &seen) {
+GC_DEV bool occ_lock(const ExecParams &p, u64 *w, u64 &pre, u64 &seen) {
     u64 v = ld_relaxed(w);
     for (int k = 0; k < 8; k++) {
         seen = v;
         if (v & LOCKB) return false;
-        const u64 old = cas_acqrel(w, v, v | LOCKB);
+        const u64 old = w_cas(p, w, v, v | LOCKB);
         if (old == v) {
             pre = v;
             return true;
@@ -380,7 +493,7 @@ GC_DEV bool occ_lock(u64 *w, u64 &pre, u64 &seen) {
 }
 
 // TicToc read-set validation of one item against commit_ts (Z9)
-GC_DEV bool tictoc_validate(u64 *w, u64 obs, u64 cts) {
+GC_DEV bool tictoc_validate(const ExecParams &p, u64 *w, u64 obs, u64 cts) {
     if (tt_rts(obs) >= cts) return true;   // version valid through cts already
     u64 v = ld_acquire(w);
     for (;;) {
@@ -388,7 +501,7 @@ GC_DEV bool tictoc_validate(u64 *w, u64 obs, u64 cts) {
         if (tt_rts(v) >= cts) return true;
         u64 nw = tt_wts(v);
         if (cts - nw > DMAX) nw = cts - DMAX;   // delta overflow: shift WTS up (Z9)
-        const u64 old = cas_acqrel(w, v, ((cts - nw) << 48) | nw);
+        const u64 old = w_cas(p, w, v, ((cts - nw) << 48) | nw);
         if (old == v) return true;
         v = old;
     }
@@ -417,27 +530,31 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             Spin sp;
             int st;
             u64 seen = 0;
-            while ((st = tpl_try<WD>(&p.meta[L[i].rec], L[i].w, age, seen)) == ST_WAIT)
+            while ((st = tpl_try<WD>(p, &p.meta[L[i].rec], L[i].w, age, seen)) == ST_WAIT)
                 if (!sp.wait(th)) { st = -1; break; }
             if (st == ST_ABORT) { th.cw = &p.meta[L[i].rec]; th.cv = M31 << 31; }   // until free
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
-            WL::read(y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
+            rd<WL>(th, y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
         }
         if (r != RES_OK) {
             fence_acqrel();
-            for (u32 j = 0; j < i; j++) tpl_release_relaxed(&p.meta[L[j].rec], L[j].w);
+            for (u32 j = 0; j < i; j++) tpl_release_relaxed(p, &p.meta[L[j].rec], L[j].w);
             return r;
         }
         // lock point: every lock held, none released -> a valid serial order (strict 2PL)
         key_lo = agg_fetch_add(&p.ctl->ticket.v);
         key_hi = 0;
         for (u32 j = 0; j < n; j++)
-            if (L[j].w) WL::install(y, L[j], WL::row(y, L[j]));
+            if (L[j].w) inst<WL>(th, y, L[j], WL::row(y, L[j]));
         fence_acqrel();
-        for (u32 j = 0; j < n; j++) tpl_release_relaxed(&p.meta[L[j].rec], L[j].w);
+        for (u32 j = 0; j < n; j++) tpl_release_relaxed(p, &p.meta[L[j].rec], L[j].w);
         return RES_OK;
     } else if constexpr (S == CC_TO || S == CC_MVCC) {
-        const u64 ts = agg_fetch_add(&p.ctl->ts.v) + 1;   // fresh ts per attempt
+        u64 ts;
+        {
+            StageClock c(th, STAGE_TS);
+            ts = agg_fetch_add(&p.ctl->ts.v) + 1;   // fresh ts per attempt
+        }
         if (draw_ts_overflow(ts, p)) return RES_FATAL;
         u32 pendm = 0;
         u64 saved[WL::MAXK];
@@ -446,8 +563,8 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             Spin sp;
             for (;;) {
                 bool pend = false;
-                const int st = (S == CC_TO) ? to_step<WL>(p, y, L[i], gid, i, ts, pend, saved[i])
-                                            : mvcc_step<WL>(p, y, L[i], gid, i, ts, pend, saved[i]);
+                const int st = (S == CC_TO) ? to_step<WL>(th, p, y, L[i], gid, i, ts, pend, saved[i])
+                                            : mvcc_step<WL>(th, p, y, L[i], gid, i, ts, pend, saved[i]);
                 if (pend) pendm |= 1u << i;
                 if (st == ST_DONE) break;
                 if (st == ST_ABORT) { r = RES_ABORT; break; }
@@ -458,15 +575,15 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         if (r != RES_OK) {
             for (u32 j = 0; j < n; j++)
                 if ((pendm >> j) & 1) {
-                    if (S == CC_TO) st_release(&p.meta[L[j].rec], saved[j]);
+                    if (S == CC_TO) w_store(p, &p.meta[L[j].rec], saved[j]);
                     else mvcc_restore<WL>(p, L[j], saved[j]);
                 }
             return r;
         }
         for (u32 j = 0; j < n; j++)
             if ((pendm >> j) & 1) {
-                if (S == CC_TO) to_commit<WL>(p, y, L[j], ts);
-                else mvcc_commit<WL>(p, y, L[j], gid, j, ts);
+                if (S == CC_TO) to_commit<WL>(th, p, y, L[j], ts);
+                else mvcc_commit<WL>(th, p, y, L[j], gid, j, ts);
             }
         key_hi = 0;
         key_lo = ts;
@@ -476,7 +593,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 i = 0; i < n; i++) {
             Spin sp;
             int st;
-            while ((st = occ_snap_step<WL>(p, y, L[i], gid, i, obs[i])) != ST_DONE)
+            while ((st = occ_snap_step<WL>(th, p, y, L[i], gid, i, obs[i])) != ST_DONE)
                 if (st == ST_WAIT && !sp.wait(th)) return RES_FATAL;
         }
         u32 locked = 0;
@@ -484,7 +601,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 i = 0; i < n && ok; i++)
             if (L[i].w) {
                 u64 seen = 0;
-                if (occ_lock(&p.meta[L[i].rec], pre[i], seen)) locked |= 1u << i;
+                if (occ_lock(p, &p.meta[L[i].rec], pre[i], seen)) locked |= 1u << i;
                 else {
                     ok = false;
                     if (seen & LOCKB) { th.cw = &p.meta[L[i].rec]; th.cv = LOCKB; }   // until unlocked
@@ -504,13 +621,13 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             }
             for (u32 i = 0; i < n && ok; i++)
                 ok = L[i].w ? (tt_wts(pre[i]) == tt_wts(obs[i]))
-                            : tictoc_validate(&p.meta[L[i].rec], obs[i], cts);
+                            : tictoc_validate(p, &p.meta[L[i].rec], obs[i], cts);
             if (ok) ticket = agg_fetch_add(&p.ctl->ticket.v);   // after validation
         }
         if (!ok) {
             fence_acqrel();
             for (u32 j = 0; j < n; j++)
-                if ((locked >> j) & 1) st_relaxed(&p.meta[L[j].rec], pre[j]);
+                if ((locked >> j) & 1) w_store_relaxed(p, &p.meta[L[j].rec], pre[j]);
             return RES_ABORT;
         }
         u64 nw;
@@ -525,10 +642,10 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         }
         key_lo = ticket;
         for (u32 j = 0; j < n; j++)
-            if (L[j].w) WL::install(y, L[j], WL::row(y, L[j]));
+            if (L[j].w) inst<WL>(th, y, L[j], WL::row(y, L[j]));
         fence_acqrel();
         for (u32 j = 0; j < n; j++)
-            if (L[j].w) st_relaxed(&p.meta[L[j].rec], nw);
+            if (L[j].w) w_store_relaxed(p, &p.meta[L[j].rec], nw);
         return RES_OK;
     } else if constexpr (S == CC_GACCO) {
         // wait for the turn, access, advance the cursor (release after the op, Z3)
@@ -540,8 +657,8 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             while (ld_acquire32(cur) != pos)
                 if (!sp.wait(th)) return RES_FATAL;
             u64 *row = WL::row(y, L[i]);
-            WL::read(y, L[i], gid, i, row);
-            if (L[i].w) WL::install(y, L[i], row);
+            rd<WL>(th, y, L[i], gid, i, row);
+            if (L[i].w) inst<WL>(th, y, L[i], row);
             st_release32(cur, pos + 1);
         }
         key_hi = 0;
@@ -556,8 +673,8 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         }
         for (u32 i = 0; i < n; i++) {
             u64 *row = WL::row(y, L[i]);
-            WL::read(y, L[i], gid, i, row);
-            if (L[i].w) WL::install(y, L[i], row);
+            rd<WL>(th, y, L[i], gid, i, row);
+            if (L[i].w) inst<WL>(th, y, L[i], row);
         }
         atom_add_release32(&p.rank_done[k], 1u);
         key_hi = 0;
@@ -576,37 +693,52 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
     th.polls = 0;
     th.cw = nullptr;
     th.cv = 0;
+    stages_init(th, p, true);
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L[WL::MAXK];
     Claim cl;
     for (;;) {
         const u32 gid = claim_work<S>(th, cl);
-        if (gid == NO_TXN) return;
+        if (gid == NO_TXN) break;
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
             if (S == CC_GPUTX) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);
             continue;
         }
-        const u32 n = WL::load_all(p, y, gid, L);
+        u32 n;
+        {
+            StageClock c(th, STAGE_INDEX);
+            n = WL::load_all(p, y, gid, L);
+        }
         if (n == 0xFFFFFFFFu) {
             set_err(p.ctl, CC_ERR_KEY_NOT_FOUND);
-            return;
+            break;
         }
-        for (;;) {
+        bool stop = false, next = false;
+        while (!stop && !next) {
             u64 kh, kl;
+            AttemptClock ac(th);
             const int r = run_thread<S, WL>(th, gid, L, n, y, kh, kl);
+            ac.done(r == RES_OK);
             if (r == RES_OK) {
-                WL::emit_txn(p, y, gid, L, n);   // outputs + private reserved-slot writes
+                {
+                    StageClock c(th, STAGE_USEFUL);
+                    WL::emit_txn(p, y, gid, L, n);   // outputs + private reserved-slot writes
+                }
                 p.order_hi[gid] = kh;
                 p.order_lo[gid] = kl;
                 p.committed[gid] = 1;
-                break;
+                next = true;
+            } else if (r == RES_FATAL || DET) {
+                stop = true;
+            } else {
+                const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
+                p.restarts[gid] = nr;
+                StageClock c(th, STAGE_ABORT);
+                retry_pace<S>(th, gid, nr);
+                if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) next = true;   // a6
             }
-            if (r == RES_FATAL || DET) return;
-            const u32 nr = p.restarts[gid] + 1;   // single owner of gid at a time
-            p.restarts[gid] = nr;
-            retry_pace<S>(th, gid, nr);
-            if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) break;   // a6
         }
+        if (stop) break;
     }
 }
 
@@ -628,12 +760,12 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             int st = ST_DONE;
             u64 seen = 0;
             if (act && !held) {
-                st = tpl_try<WD>(&p.meta[L.rec], L.w, age, seen);
+                st = tpl_try<WD>(p, &p.meta[L.rec], L.w, age, seen);
                 held = st == ST_DONE;
             }
             const unsigned dying = tile.ballot(st == ST_ABORT);
             if (dying) {
-                if (held) tpl_release_relaxed(&p.meta[L.rec], L.w);
+                if (held) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
                 const int src = __ffs(dying) - 1;   // remember one conflicting lock for the retry
                 th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
                 th.cv = M31 << 31;                   // wait until its holder count is 0
@@ -641,23 +773,26 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
             if (tile.all(!act || held)) break;
             if (tile.any(!sp.wait(th))) {
-                if (held) tpl_release_relaxed(&p.meta[L.rec], L.w);
+                if (held) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
                 return RES_FATAL;
             }
         }
-        if (act) WL::read(y, L, gid, li, WL::row(y, L));   // stable under the lock
+        if (act) rd<WL>(th, y, L, gid, li, WL::row(y, L));   // stable under the lock
         u64 ticket = 0;
         if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // lock point
         key_lo = tile.shfl(ticket, 0);
         key_hi = 0;
-        if (act && L.w) WL::install(y, L, WL::row(y, L));
+        if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         fence_acqrel();
-        if (act) tpl_release_relaxed(&p.meta[L.rec], L.w);
+        if (act) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
         return RES_OK;
     } else if constexpr (S == CC_TO || S == CC_MVCC) {
         u64 ts = 0;
-        if (li == 0) ts = atomicAdd(&p.ctl->ts.v, 1ull) + 1;
-        ts = tile.shfl(ts, 0);
+        {
+            StageClock c(th, STAGE_TS);
+            if (li == 0) ts = atomicAdd(&p.ctl->ts.v, 1ull) + 1;
+            ts = tile.shfl(ts, 0);
+        }
         if (draw_ts_overflow(ts, p)) return RES_FATAL;
         bool done = !act, pend = false;
         u64 saved = 0;
@@ -665,13 +800,13 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         for (;;) {
             int st = ST_DONE;
             if (!done) {
-                st = (S == CC_TO) ? to_step<WL>(p, y, L, gid, li, ts, pend, saved)
-                                  : mvcc_step<WL>(p, y, L, gid, li, ts, pend, saved);
+                st = (S == CC_TO) ? to_step<WL>(th, p, y, L, gid, li, ts, pend, saved)
+                                  : mvcc_step<WL>(th, p, y, L, gid, li, ts, pend, saved);
                 done = st == ST_DONE;
             }
             if (tile.any(st == ST_ABORT)) {
                 if (pend) {
-                    if (S == CC_TO) st_release(&p.meta[L.rec], saved);
+                    if (S == CC_TO) w_store(p, &p.meta[L.rec], saved);
                     else mvcc_restore<WL>(p, L, saved);
                 }
                 return RES_ABORT;
@@ -680,15 +815,15 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (tile.any(st == ST_RETRY)) continue;   // lost a CAS race: go again at once
             if (tile.any(!sp.wait(th))) {
                 if (pend) {
-                    if (S == CC_TO) st_release(&p.meta[L.rec], saved);
+                    if (S == CC_TO) w_store(p, &p.meta[L.rec], saved);
                     else mvcc_restore<WL>(p, L, saved);
                 }
                 return RES_FATAL;
             }
         }
         if (pend) {
-            if (S == CC_TO) to_commit<WL>(p, y, L, ts);
-            else mvcc_commit<WL>(p, y, L, gid, li, ts);
+            if (S == CC_TO) to_commit<WL>(th, p, y, L, ts);
+            else mvcc_commit<WL>(th, p, y, L, gid, li, ts);
         }
         key_hi = 0;
         key_lo = ts;
@@ -700,7 +835,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         for (;;) {   // read phase
             int st = ST_DONE;
             if (!done) {
-                st = occ_snap_step<WL>(p, y, L, gid, li, obs);
+                st = occ_snap_step<WL>(th, p, y, L, gid, li, obs);
                 done = st == ST_DONE;
             }
             if (tile.all(done)) break;
@@ -710,7 +845,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         bool locked = false, bad = false;
         u64 seen = 0;
         if (act && L.w) {
-            locked = occ_lock(&p.meta[L.rec], pre, seen);
+            locked = occ_lock(p, &p.meta[L.rec], pre, seen);
             bad = !locked;
         }
         {
@@ -732,7 +867,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 u64 c = 0;
                 if (act) c = max(L.w ? tt_rts(pre) + 1 : 0ull, tt_wts(obs));
                 cts = cg::reduce(tile, c, cg::greater<u64>());
-                if (act) bad = L.w ? (tt_wts(pre) != tt_wts(obs)) : !tictoc_validate(&p.meta[L.rec], obs, cts);
+                if (act) bad = L.w ? (tt_wts(pre) != tt_wts(obs)) : !tictoc_validate(p, &p.meta[L.rec], obs, cts);
                 if (!tile.any(bad)) {
                     if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // after validation
                     ticket = tile.shfl(ticket, 0);
@@ -740,7 +875,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
         }
         if (tile.any(bad)) {
-            if (locked) st_release(&p.meta[L.rec], pre);
+            if (locked) w_store(p, &p.meta[L.rec], pre);
             return RES_ABORT;
         }
         u64 nw;
@@ -753,9 +888,9 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             key_hi = cts;
         }
         key_lo = ticket;
-        if (act && L.w) WL::install(y, L, WL::row(y, L));
+        if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         fence_acqrel();
-        if (act && L.w) st_relaxed(&p.meta[L.rec], nw);
+        if (act && L.w) w_store_relaxed(p, &p.meta[L.rec], nw);
         return RES_OK;
     } else if constexpr (S == CC_GACCO) {
         int st = ST_DONE;
@@ -768,8 +903,8 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 if (!sp.wait(th)) { st = ST_ABORT; break; }
             if (st == ST_DONE) {
                 u64 *row = WL::row(y, L);
-                WL::read(y, L, gid, li, row);
-                if (L.w) WL::install(y, L, row);
+                rd<WL>(th, y, L, gid, li, row);
+                if (L.w) inst<WL>(th, y, L, row);
                 st_release32(cur, pos + 1);
             }
         }
@@ -788,8 +923,8 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         if (tile.any(st != ST_DONE)) return RES_FATAL;
         if (act) {
             u64 *row = WL::row(y, L);
-            WL::read(y, L, gid, li, row);
-            if (L.w) WL::install(y, L, row);
+            rd<WL>(th, y, L, gid, li, row);
+            if (L.w) inst<WL>(th, y, L, row);
         }
         tile.sync();   // every lane's install precedes the K-set release
         if (li == 0) atom_add_release32(&p.rank_done[k], 1u);
@@ -809,6 +944,7 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
     th.polls = 0;
     th.cw = nullptr;
     th.cv = 0;
+    stages_init(th, p, li == 0);   // stages are timed by each tile's leader
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L;
     Claim cl;
@@ -816,38 +952,52 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
         u32 gid = NO_TXN;
         if (li == 0) gid = claim_work<S>(th, cl);
         gid = tile.shfl(gid, 0);
-        if (gid == NO_TXN) return;
+        if (gid == NO_TXN) break;
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
             if (S == CC_GPUTX && li == 0) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);
             continue;
         }
-        const bool ok = WL::load_lane(p, y, gid, li, L);
+        bool ok;
+        {
+            StageClock c(th, STAGE_INDEX);
+            ok = WL::load_lane(p, y, gid, li, L);
+        }
         if (!tile.all(ok)) {
             if (li == 0) set_err(p.ctl, CC_ERR_KEY_NOT_FOUND);
-            return;
+            break;
         }
-        for (;;) {
+        bool stop = false, next = false;
+        while (!stop && !next) {
             u64 kh = 0, kl = 0;
+            AttemptClock ac(th);
             const int r = run_tile<S, WL>(tile, th, gid, L, y, kh, kl);
+            ac.done(r == RES_OK);
             if (r == RES_OK) {
-                WL::emit_tile(tile, p, y, gid, L, li);   // outputs + private reserved-slot writes
+                {
+                    StageClock c(th, STAGE_USEFUL);
+                    WL::emit_tile(tile, p, y, gid, L, li);   // outputs + private reserved-slot writes
+                }
                 if (li == 0) {
                     p.order_hi[gid] = kh;
                     p.order_lo[gid] = kl;
                     p.committed[gid] = 1;
                 }
-                break;
+                next = true;
+            } else if (r == RES_FATAL || DET) {
+                stop = true;
+            } else {
+                int push = 0;
+                if (li == 0) {
+                    const u32 nr = p.restarts[gid] + 1;
+                    p.restarts[gid] = nr;
+                    StageClock c(th, STAGE_ABORT);
+                    retry_pace<S>(th, gid, nr);
+                    push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
+                }
+                next = tile.shfl(push, 0) != 0;
             }
-            if (r == RES_FATAL || DET) return;
-            int push = 0;
-            if (li == 0) {
-                const u32 nr = p.restarts[gid] + 1;
-                p.restarts[gid] = nr;
-                retry_pace<S>(th, gid, nr);
-                push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
-            }
-            if (tile.shfl(push, 0)) break;
         }
+        if (stop) break;
     }
 }
 

@@ -60,7 +60,12 @@ struct ExecParams {
     uint32_t *rank_done;         // GPUTx: completed count per rank
     const uint32_t *rank_count;  // GPUTx: size of each rank (K-set)
     const uint8_t *skip;         // partitioned TPC-C: 1 = distributed txn, left to phase B
+    uint32_t *latch;             // CC_FLAG_LATCHED: one 32-bit latch per control word
+    unsigned long long *stages;  // CC_FLAG_STAGES: accumulated cycles per stage (STAGE_*)
 };
+// stage-time breakdown (Exp-6): cycles summed over workers
+enum { STAGE_INDEX = 0, STAGE_TS = 1, STAGE_WAIT = 2, STAGE_CC = 3, STAGE_ABORT = 4,
+       STAGE_USEFUL = 5, STAGE_ATTEMPTS = 6, STAGE_WORDS = 8 };
 
 // Cache-line search tree over a sorted key array (same lower-bound result as the
 // binary search of PAPER.md:344): the sorted array, padded with ~0 to a multiple of 16,
@@ -112,6 +117,7 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
+cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads, cudaStream_t s);
 
 struct TpccParams;
 cudaError_t launch_tpcc_exec(const ExecParams &p, const TpccParams &y, int grid, int block,

@@ -288,7 +288,26 @@ __global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t 
     }
 }
 
-__global__ void stats_kernel(const Ctl *c, uint64_t *stats) {
+// sum the per-thread stage slots (stages[8 + t*8 + k]) into stages[0..7]
+__global__ void stages_reduce_kernel(unsigned long long *stages, uint64_t n_threads) {
+    __shared__ unsigned long long acc[STAGE_WORDS];
+    if (threadIdx.x < STAGE_WORDS) acc[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_threads;
+         t += (uint64_t)gridDim.x * blockDim.x)
+        for (int k = 0; k < STAGE_WORDS; k++) {
+            const unsigned long long v = stages[STAGE_WORDS + t * STAGE_WORDS + k];
+            if (v) atomicAdd(&acc[k], v);
+        }
+    __syncthreads();
+    if (threadIdx.x < STAGE_WORDS && acc[threadIdx.x]) atomicAdd(&stages[threadIdx.x], acc[threadIdx.x]);
+}
+cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads, cudaStream_t s) {
+    stages_reduce_kernel<<<148, 256, 0, s>>>(stages, n_threads);
+    return cudaGetLastError();
+}
+
+__global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long long *stages) {
     stats[0] = c->done.v;
     stats[1] = c->aborts.v;
     stats[2] = c->done.v + c->aborts.v;
@@ -296,6 +315,8 @@ __global__ void stats_kernel(const Ctl *c, uint64_t *stats) {
     stats[4] = c->max_rank.v;
     stats[5] = c->ts.v;
     for (int k = 6; k < CC_STATS_WORDS; k++) stats[k] = 0;
+    if (stages)
+        for (int k = 0; k < 7; k++) stats[8 + k] = stages[k];
 }
 
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
@@ -327,7 +348,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         }
     }
     copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);
-    stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats);
+    stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats, p.stages);
     return cudaGetLastError();
 }
 

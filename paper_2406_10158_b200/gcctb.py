@@ -25,6 +25,9 @@ CC_FLAG_TIMING = 0x2
 CC_FLAG_PARTITIONED = 0x4
 CC_FLAG_PART_ALL = 0x8
 CC_FLAG_INDEX_BINARY = 0x10
+CC_FLAG_LATCHED = 0x20
+CC_FLAG_STAGES = 0x40
+STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16
 
@@ -72,7 +75,8 @@ class cc_stats(ctypes.Structure):
     _fields_ = [("commits", ctypes.c_uint64), ("aborts", ctypes.c_uint64),
                 ("attempts", ctypes.c_uint64), ("error", ctypes.c_uint64),
                 ("max_rank", ctypes.c_uint64), ("ts_last", ctypes.c_uint64),
-                ("reserved", ctypes.c_uint64 * 10)]
+                ("reserved", ctypes.c_uint64 * 2), ("stage_cycles", ctypes.c_uint64 * 7),
+                ("sm_clock_khz", ctypes.c_uint64)]
 
 
 _lib = None

@@ -243,3 +243,45 @@ def test_c1_parity_binary_index(c1, orc, scheme):
         db.sync()
         orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
     b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 4])
+@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc"])
+def test_c1_parity_latched(c1, orc, scheme, lanes):
+    """Exp-7 latched variants: same serializable results."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_LATCHED
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 51, T, A)
+    keys, ops = orc.ycsb_gen(51, 1024, 1024, 4, 0.5, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, flags=CC_FLAG_LATCHED)
+    assert db.sync().commits == 1024
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 4])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_stage_breakdown(c1, orc, scheme, lanes):
+    """Exp-6 stage accounting: every attempt is counted, stages are
+    non-negative and results are unchanged with the timers on."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_STAGES
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 52, T, A)
+    keys, ops = orc.ycsb_gen(52, 1024, 1024, 4, 0.5, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, flags=CC_FLAG_STAGES)
+    st = db.sync()
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    sc = list(st.stage_cycles)
+    assert sc[6] == st.commits + st.aborts               # attempts
+    assert sc[0] > 0 and sc[5] > 0                        # index lookups and row work happened
+    if st.aborts == 0:
+        assert sc[4] == 0                                 # no abort time without aborts
+    if scheme in ("to", "mvcc"):
+        assert sc[1] > 0                                  # timestamp allocation
+    b.free()
