@@ -4,6 +4,9 @@
           scheme, in the paper's launch (thread mode wd=0 bs=32) and the
           B200 tile mode (16 lanes per transaction).
   presets RO / MC / HC, both modes.
+  stages  Exp-6: per-stage time per transaction on RO/MC/HC, every
+          scheme, the paper's launch (wd=0, bs=32) and tile mode.
+  latch   Exp-7: latch-free vs latched, six CPU-oriented schemes, presets.
   wdbs    Exp-3/4/5-style heatmap on TPC-C configs[3] (64 warehouses, 45:43 mix):
           wd in 0..5 x bs in {1,2,4,8,16,32} per scheme, thread mode.
 
@@ -101,6 +104,82 @@ def sweep_presets(a, out):
     db.close()
 
 
+PRESETS = {"RO": (0.0, 0.0), "MC": (0.1, 0.6), "HC": (0.5, 0.8)}
+
+
+def sweep_stages(a, out):
+    from paper_2406_10158_b200.gcctb import CC_FLAG_STAGES, STAGES
+    db = ycsb_db(a.rows)
+    A = inputs.scramble_mult(a.rows)
+    for name, (W, th) in PRESETS.items():
+        T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
+        b = db.gen_ycsb(a.batch, 16, W, 13, T, A)
+        for mode, kw in MODES.items():
+            for s in SCHEMES:
+                try:
+                    db.timing(reset=True)
+                    db.submit(b, s, flags=CC_FLAG_STAGES | CC_FLAG_TIMING, watchdog_s=a.watchdog, **kw)
+                    st = db.sync()
+                    ms, _ = db.timing(reset=True)
+                    ns_per_cycle = 1e6 / max(st.sm_clock_khz, 1)
+                    per_txn = {STAGES[k]: st.stage_cycles[k] * ns_per_cycle / max(st.commits, 1) for k in range(6)}
+                    r = dict(stage_ns_per_txn=per_txn, attempts=st.stage_cycles[6], prep_ms=ms[1],
+                             exec_ms=ms[2], abort_rate=st.aborts / max(st.commits, 1))
+                except Exception as e:
+                    r = dict(error=str(e)[:120])
+                    db.close()
+                    db = ycsb_db(a.rows)
+                    b = db.gen_ycsb(a.batch, 16, W, 13, T, A)
+                r.update(exp="stages", preset=name, mode=mode, scheme=s)
+                out.write(json.dumps(r) + "\n")
+                out.flush()
+        b.free()
+    db.close()
+
+
+def sweep_latch(a, out):
+    from paper_2406_10158_b200.gcctb import CC_FLAG_LATCHED
+    db = ycsb_db(a.rows)
+    A = inputs.scramble_mult(a.rows)
+    for name, (W, th) in PRESETS.items():
+        T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
+        b = db.gen_ycsb(a.batch, 16, W, 14, T, A)
+        for mode, kw in MODES.items():
+            for s in SCHEMES[:6]:
+                for latched in (False, True):
+                    try:
+                        k2 = dict(kw)
+                        r = cell(db, b, s, a.reps, a.watchdog, **k2) if not latched else \
+                            cell_flags(db, b, s, a.reps, a.watchdog, CC_FLAG_LATCHED, **k2)
+                    except Exception as e:
+                        r = dict(error=str(e)[:120])
+                        db.close()
+                        db = ycsb_db(a.rows)
+                        b = db.gen_ycsb(a.batch, 16, W, 14, T, A)
+                    r.update(exp="latch", preset=name, mode=mode, scheme=s, latched=latched)
+                    out.write(json.dumps(r) + "\n")
+                    out.flush()
+        b.free()
+    db.close()
+
+
+def cell_flags(db, b, scheme, reps, watchdog, flags, **kw):
+    db.submit(b, scheme, watchdog_s=watchdog, flags=flags, **kw)
+    db.sync()
+    tots, ab, cm = [], 0, 0
+    for _ in range(reps):
+        db.timing(reset=True)
+        db.submit(b, scheme, flags=CC_FLAG_TIMING | flags, watchdog_s=watchdog, **kw)
+        st = db.sync()
+        ms, _ = db.timing(reset=True)
+        tots.append(ms[4])
+        ab += st.aborts
+        cm += st.commits
+    med = statistics.median(tots)
+    return dict(ms_median=med, ms_min=min(tots), ms_max=max(tots), txn_s=b.n_txn / (med / 1e3),
+                abort_rate=ab / max(cm, 1))
+
+
 def sweep_wdbs(a, out):
     db = DB(0)
     db.load_tpcc(64, 1, 65536)
@@ -122,7 +201,7 @@ def sweep_wdbs(a, out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("exp", choices=["theta", "presets", "wdbs"])
+    ap.add_argument("exp", choices=["theta", "presets", "wdbs", "stages", "latch"])
     ap.add_argument("--rows", type=int, default=10 * (1 << 20))
     ap.add_argument("--batch", type=int, default=1 << 16)
     ap.add_argument("--reps", type=int, default=3)
@@ -132,7 +211,8 @@ def main():
     a = ap.parse_args()
     out = sys.stdout if a.out == "-" else open(a.out, "a")
     t0 = time.time()
-    {"theta": sweep_theta, "presets": sweep_presets, "wdbs": sweep_wdbs}[a.exp](a, out)
+    {"theta": sweep_theta, "presets": sweep_presets, "wdbs": sweep_wdbs, "stages": sweep_stages,
+     "latch": sweep_latch}[a.exp](a, out)
     sys.stderr.write(f"{a.exp} done in {time.time() - t0:.1f}s\n")
 
 
