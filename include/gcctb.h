@@ -212,6 +212,9 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         under a 32-bit per-word latch instead of one 64-bit CAS */
 #define CC_FLAG_STAGES 0x40u         /* Exp-6: per-stage cycle
                                         accounting into cc_stats.stage_cycles */
+#define CC_FLAG_EVENTS 0x80u         /* debug event log: every row read / install
+                                        and every commit / abort gets a global sequence number;
+                                        read it with cc_events_read (capacity: cc_events_capacity) */
 #define CC_FLAG_INDEX_BINARY 0x10u   /* index lookups by plain binary search over the sorted
                                         array (the paper's index) instead of the
                                         default cache-line search tree over the same array
@@ -294,6 +297,14 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
 cc_status cc_part_send(cc_db db, const void **send, uint64_t *counts);
 cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp);
 cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent);
+
+/* Debug event log (CC_FLAG_EVENTS).  Each event is 24 bytes: u64 seq, u32 gid,
+ * u32 record (global id; 0xFFFFFFFF for commit/abort), u32 attempt, u32 kind (0 read,
+ * 1 write/install, 2 commit, 3 abort).  cc_events_capacity allocates room for `cap`
+ * events; cc_events_read waits, copies min(n, cap) events of the last submit to host
+ * memory and returns the number recorded (larger than cap means overflow). */
+cc_status cc_events_capacity(cc_db db, uint64_t cap);
+cc_status cc_events_read(cc_db db, void *dst, uint64_t cap, uint64_t *n_events);
 
 /* Wait for the db stream; surface asynchronous errors; if st != NULL copy the stats of
  * the last submit into it. */

@@ -273,6 +273,22 @@ class DB:
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self._chk(G.lib().cc_part_finish(self.h, resp.data_ptr() if n else None, n))
 
+    # ----------------------------------------------------------- debug event log (f-4)
+    EVENT_DTYPE = np.dtype([("seq", "<u8"), ("gid", "<u4"), ("rec", "<u4"), ("attempt", "<u4"), ("kind", "<u4")])
+
+    def events_capacity(self, cap: int):
+        self._chk(G.lib().cc_events_capacity(self.h, cap))
+        self._events_cap = cap
+
+    def events(self) -> np.ndarray:
+        cap = getattr(self, "_events_cap", 0)
+        buf = np.zeros(cap, dtype=self.EVENT_DTYPE)
+        n = ctypes.c_uint64()
+        self._chk(G.lib().cc_events_read(self.h, buf.ctypes.data, cap, ctypes.byref(n)))
+        if n.value > cap:
+            raise RuntimeError(f"event log overflow: {n.value} events > capacity {cap}")
+        return buf[:n.value]
+
     def sync(self) -> G.cc_stats:
         s = G.cc_stats()
         self._chk(G.lib().cc_sync(self.h, ctypes.byref(s)))

@@ -110,6 +110,8 @@ struct cc_db_s {
     uint32_t *latch = nullptr;          // CC_FLAG_LATCHED
     uint64_t latch_records = 0;
     u64 *stages = nullptr;              // CC_FLAG_STAGES accumulators
+    Event *events = nullptr;            // CC_FLAG_EVENTS log
+    uint64_t events_cap = 0;
     int clock_khz = 0;
     u64 *meta = nullptr;
     uint64_t meta_records = 0;
@@ -266,6 +268,7 @@ cc_status cc_db_destroy(cc_db db) {
     cudaFree(db->arena);
     cudaFree(db->latch);
     cudaFree(db->stages);
+    cudaFree(db->events);
     cudaFree(db->meta);
     cudaFree(db->ctl);
     cudaFree(db->stats_scratch);
@@ -831,6 +834,11 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         CUDA_TRY(db, launch_fill_u64(db->stages, 0ull, words, db->stream));
         p.stages = db->stages;
     }
+    if (desc->flags & CC_FLAG_EVENTS) {
+        if (!db->events) return fail(db, CC_ERR_CONFIG, "CC_FLAG_EVENTS needs cc_events_capacity first");
+        p.events = db->events;
+        p.events_cap = db->events_cap;
+    }
     const bool timing = desc->flags & CC_FLAG_TIMING;
     const bool partitioned = (desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) != 0;
     if (partitioned) {
@@ -971,6 +979,32 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent) {
         db->pending.push_back(P.ev);
     }
     P.pending = false;
+    return CC_OK;
+}
+
+cc_status cc_events_capacity(cc_db db, uint64_t cap) {
+    CHECK_DB(db);
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    cudaFree(db->events);
+    db->events = nullptr;
+    db->events_cap = 0;
+    if (cap) {
+        CUDA_TRY(db, dalloc(&db->events, cap * sizeof(Event)));
+        db->events_cap = cap;
+    }
+    return CC_OK;
+}
+
+cc_status cc_events_read(cc_db db, void *dst, uint64_t cap, uint64_t *n_events) {
+    CHECK_DB(db);
+    if (!n_events) return fail(db, CC_ERR_INVALID_ARG, "null n_events");
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    Ctl c;
+    CUDA_TRY(db, cudaMemcpy(&c, db->ctl, sizeof c, cudaMemcpyDeviceToHost));
+    *n_events = c.events.v;
+    uint64_t n = c.events.v < cap ? c.events.v : cap;
+    if (n > db->events_cap) n = db->events_cap;
+    if (n && dst) CUDA_TRY(db, cudaMemcpy(dst, db->events, n * sizeof(Event), cudaMemcpyDeviceToHost));
     return CC_OK;
 }
 

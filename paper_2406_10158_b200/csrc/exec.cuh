@@ -32,6 +32,7 @@ constexpr u32 NO_TXN = 0xFFFFFFFFu;
 struct Th {
     u64 deadline;
     const ExecParams *p;
+    u32 gid, attempt;     // current attempt (event log)
     u32 polls;
     bool timing;          // CC_FLAG_STAGES
     u64 *st;              // this worker's STAGE_WORDS accumulators (global memory), or null
@@ -73,16 +74,43 @@ struct StageClock {
     }
 };
 
+// debug event log (CC_FLAG_EVENTS): each event takes a global sequence
+// number right after the access it describes
+GC_DEV void log_event(const Th &th, u32 rec, u32 kind) {
+    const ExecParams &p = *th.p;
+    if (!p.events) return;
+    const u64 k = atomicAdd(&p.ctl->events.v, 1ull);
+    if (k >= p.events_cap) return;   // overflow: the count tells the host
+    Event &ev = p.events[k];
+    ev.seq = k;
+    ev.gid = th.gid;
+    ev.rec = rec;
+    ev.attempt = th.attempt;
+    ev.kind = kind;
+}
+
 // row work (the "useful" stage) done through these wrappers
 template <class WL>
 GC_DEV void rd(Th &th, const typename WL::Params &y, typename WL::Lane &L, u32 gid, u32 i, const u64 *src) {
-    StageClock c(th, STAGE_USEFUL);
-    WL::read(y, L, gid, i, src);
+    {
+        StageClock c(th, STAGE_USEFUL);
+        WL::read(y, L, gid, i, src);
+    }
+    if (th.p->events) {
+        fence_acqrel();
+        log_event(th, L.rec, 0);
+    }
 }
 template <class WL>
 GC_DEV void inst(Th &th, const typename WL::Params &y, const typename WL::Lane &L, u64 *dst) {
-    StageClock c(th, STAGE_USEFUL);
-    WL::install(y, L, dst);
+    {
+        StageClock c(th, STAGE_USEFUL);
+        WL::install(y, L, dst);
+    }
+    if (th.p->events) {
+        fence_acqrel();
+        log_event(th, L.rec, 1);
+    }
 }
 
 // per-attempt attribution: a committed attempt's time not spent in row
@@ -716,9 +744,12 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
         bool stop = false, next = false;
         while (!stop && !next) {
             u64 kh, kl;
+            th.gid = gid;
+            th.attempt = p.restarts[gid];
             AttemptClock ac(th);
             const int r = run_thread<S, WL>(th, gid, L, n, y, kh, kl);
             ac.done(r == RES_OK);
+            if (p.events && r != RES_FATAL) log_event(th, 0xFFFFFFFFu, r == RES_OK ? 2u : 3u);
             if (r == RES_OK) {
                 {
                     StageClock c(th, STAGE_USEFUL);
@@ -969,9 +1000,15 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
         bool stop = false, next = false;
         while (!stop && !next) {
             u64 kh = 0, kl = 0;
+            th.gid = gid;
+            th.attempt = tile.shfl(li == 0 ? p.restarts[gid] : 0u, 0);   // the leader owns restarts
             AttemptClock ac(th);
             const int r = run_tile<S, WL>(tile, th, gid, L, y, kh, kl);
             ac.done(r == RES_OK);
+            if (p.events && r != RES_FATAL) {
+                tile.sync();   // every lane's access events precede the commit / abort event
+                if (li == 0) log_event(th, 0xFFFFFFFFu, r == RES_OK ? 2u : 3u);
+            }
             if (r == RES_OK) {
                 {
                     StageClock c(th, STAGE_USEFUL);

@@ -26,6 +26,14 @@ struct Ctl {
     Counter max_rank;   // GPUTx: number of K-sets - 1
     Counter rank_head;  // GPUTx rank-pass claim counter
     Counter inflight;   // retry-batch appends in flight (sealing protocol)
+    Counter events;     // CC_FLAG_EVENTS: event sequence counter
+};
+// one event of the debug log: 24 bytes
+struct Event {
+    unsigned long long seq;   // global order (atomic counter)
+    uint32_t gid, rec;        // transaction, record (global record id)
+    uint32_t attempt;         // restart ordinal of the attempt
+    uint32_t kind;            // 0 read, 1 write (install), 2 commit, 3 abort
 };
 
 enum { KIND_YCSB = 1, KIND_TPCC = 2 };
@@ -62,6 +70,8 @@ struct ExecParams {
     const uint8_t *skip;         // partitioned TPC-C: 1 = distributed txn, left to phase B
     uint32_t *latch;             // CC_FLAG_LATCHED: one 32-bit latch per control word
     unsigned long long *stages;  // CC_FLAG_STAGES: accumulated cycles per stage (STAGE_*)
+    Event *events;               // CC_FLAG_EVENTS: event log (capacity events_cap)
+    unsigned long long events_cap;
 };
 // stage-time breakdown (Exp-6): cycles summed over workers
 enum { STAGE_INDEX = 0, STAGE_TS = 1, STAGE_WAIT = 2, STAGE_CC = 3, STAGE_ABORT = 4,

@@ -27,6 +27,7 @@ CC_FLAG_PART_ALL = 0x8
 CC_FLAG_INDEX_BINARY = 0x10
 CC_FLAG_LATCHED = 0x20
 CC_FLAG_STAGES = 0x40
+CC_FLAG_EVENTS = 0x80
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16
@@ -118,6 +119,8 @@ _SIGS = {
     "cc_batch_import_tpcc": (ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(_P)]),
     "cc_batch_export_tpcc": (ctypes.c_int, [_P, _P, _P]),
     "cc_part_send": (ctypes.c_int, [_P, ctypes.POINTER(_P), _P]),
+    "cc_events_capacity": (ctypes.c_int, [_P, ctypes.c_uint64]),
+    "cc_events_read": (ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]),
     "cc_part_apply": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P]),
     "cc_part_finish": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),
 }

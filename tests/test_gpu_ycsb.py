@@ -285,3 +285,28 @@ def test_stage_breakdown(c1, orc, scheme, lanes):
     if scheme in ("to", "mvcc"):
         assert sc[1] > 0                                  # timestamp allocation
     b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 4])
+@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd", "to", "silo", "tictoc", "gputx", "gacco"])
+def test_event_log_conflict_graph(c1, orc, scheme, lanes):
+    """f-4 debug mode: the device event log of a high-contention batch yields an acyclic
+    conflict graph, with one commit event per transaction."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_EVENTS
+    from paper_2406_10158_b200.verify import check_serializable
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 53, T, A)
+    keys, ops = orc.ycsb_gen(53, 1024, 1024, 4, 0.5, T, A)
+    db.events_capacity(1 << 22)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, flags=CC_FLAG_EVENTS)
+    st = db.sync()
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    ev = db.events()
+    assert int((ev["kind"] == 2).sum()) == 1024
+    assert int((ev["kind"] == 3).sum()) == st.aborts
+    ok, info = check_serializable(ev)
+    assert ok, f"cycle {info}"
+    b.free()
