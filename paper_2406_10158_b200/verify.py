@@ -68,13 +68,21 @@ def check_serializable(ev: np.ndarray):
                 q.append(m)
     if len(order) == len(indeg):
         return True, order
-    # report one cycle among the remaining nodes
+    # report one cycle: every node left after Kahn's peel has a remaining predecessor,
+    # so walking predecessors inside the remainder must repeat a node
     rest = {n for n, d in indeg.items() if d > 0}
+    preds = defaultdict(list)
+    for a, bs in edges.items():
+        if a in rest:
+            for b in bs:
+                if b in rest:
+                    preds[b].append(a)
     start = min(rest)
     path, seen = [start], {start: 0}
     while True:
-        nxt = min(m for m in edges[path[-1]] if m in rest)
+        nxt = min(preds[path[-1]])
         if nxt in seen:
-            return False, path[seen[nxt]:] + [nxt]
+            cyc = path[seen[nxt]:] + [nxt]
+            return False, cyc[::-1]
         seen[nxt] = len(path)
         path.append(nxt)
