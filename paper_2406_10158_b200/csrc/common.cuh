@@ -101,6 +101,10 @@ GC_DEV u64 globaltimer_ns() {
     return t;
 }
 
+// L2 prefetch: no memory-ordering effect, so it can run ahead of the acquire loads and
+// CASes that must precede the real accesses
+GC_DEV void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 GC_DEV u64 clk64() {
     u64 t;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));

@@ -365,7 +365,15 @@ struct TpccWL {
             L.price = (u32)ir[0];
             L.brand_i = has_original(reinterpret_cast<const uint8_t *>(ir + 4));
         }
+        if (!p.skip || !p.skip[gid]) prefetch_access(p, y, L);
         return true;
+    }
+
+    static GC_DEV void prefetch_access(const ExecParams &p, const TpccParams &y, const Lane &L) {
+        const u64 *rw = row(y, L);
+        const int n = row_words(L);
+        for (int k = 0; k < n && k < 40; k += 16) prefetch_l2(rw + k);   // the fields read
+        prefetch_l2(p.scheme == CC_MVCC ? p.meta + 2ull * L.rec : p.meta + L.rec);
     }
 
     static GC_DEV u32 load_all(const ExecParams &p, const TpccParams &y, u32 gid, Lane *L) {

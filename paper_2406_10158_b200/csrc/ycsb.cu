@@ -115,6 +115,8 @@ struct YcsbWL {
                     if (node[i] >= y.idx_n || __ldg(y.idx_keys + node[i]) != key[i]) ok = false;
                     else L[i].rec = (u32)__ldg(y.idx_rows + node[i]);
                 }
+            if (ok)
+                for (int i = 0; i < (int)p.K; i++) prefetch_access(p, y, L[i]);
             return ok ? p.K : 0xFFFFFFFFu;
         }
         u64 n = y.idx_n;
@@ -151,11 +153,22 @@ struct YcsbWL {
         L.w = op >> 7;
         if (p.acc_rec) {
             L.rec = p.acc_rec[a];
+            prefetch_access(p, y, L);
             return true;
         }
         const u64 r = lookup(y, y.keys[a]);
         L.rec = (u32)r;
+        if (r != ~0ull) prefetch_access(p, y, L);
         return r != ~0ull;
+    }
+
+    // bring the row (both 64 B halves) and the CC word into L2 while the scheme's ordered
+    // accesses to the word are still pending
+    static GC_DEV void prefetch_access(const ExecParams &p, const YcsbParams &y, const Lane &L) {
+        const u64 *rw = y.rows + (u64)L.rec * 16u;
+        prefetch_l2(rw);
+        prefetch_l2(rw + 8);
+        prefetch_l2(p.scheme == CC_MVCC ? p.meta + 2ull * L.rec : p.meta + L.rec);
     }
 
     static GC_DEV u64 *row(const YcsbParams &y, const Lane &L) { return y.rows + (u64)L.rec * 16u; }
