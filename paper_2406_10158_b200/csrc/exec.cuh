@@ -53,10 +53,13 @@ GC_DEV bool dead(Th &th) {
 
 struct Spin {
     unsigned ns = 16;
+    unsigned cap = 256;   // max sleep between polls (ns)
+    GC_DEV Spin() {}
+    GC_DEV explicit Spin(unsigned max_ns) : ns(max_ns < 16 ? max_ns : 16), cap(max_ns) {}
     GC_DEV bool wait(Th &th) {   // false -> give up (error / watchdog)
         const u64 t0 = th.timing ? clk64() : 0;
         __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
+        ns = ns < cap ? ns * 2 : cap;
         const bool alive = !dead(th);
         if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
         return alive;
@@ -681,7 +684,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 i = 0; i < n; i++) {
             const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
             u32 *cur = &p.cursor[seg];
-            Spin sp;
+            Spin sp(32);   // the hand-off chain on a hot item is GaccO's critical path
             while (ld_acquire32(cur) != pos)
                 if (!sp.wait(th)) return RES_FATAL;
             u64 *row = WL::row(y, L[i]);
@@ -929,7 +932,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             const u64 a = (u64)gid * p.K + li;
             const u32 seg = p.acc_seg[a], pos = p.acc_pos[a];
             u32 *cur = &p.cursor[seg];
-            Spin sp;
+            Spin sp(32);   // the hand-off chain on a hot item is GaccO's critical path
             while (ld_acquire32(cur) != pos)
                 if (!sp.wait(th)) { st = ST_ABORT; break; }
             if (st == ST_DONE) {
