@@ -28,14 +28,15 @@ def main():
     ap.add_argument("--lanes", type=int, default=1)
     ap.add_argument("--binary", action="store_true")
     ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--seeds", default="3")
     a = ap.parse_args()
     db = DB(0)
     db.load_ycsb(a.rows, 1)
     A = inputs.scramble_mult(a.rows)
     out = []
-    for th in [float(x) for x in a.thetas.split(",")]:
+    for th, seed in [(float(x), int(sd)) for x in a.thetas.split(",") for sd in a.seeds.split(",")]:
         T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
-        b = db.gen_ycsb(a.batch, a.K, a.W, 3, T, A)
+        b = db.gen_ycsb(a.batch, a.K, a.W, seed, T, A)
         for s in a.schemes.split(","):
             db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=0x10 if a.binary else 0, grid=a.grid)
             db.sync()
@@ -53,7 +54,7 @@ def main():
                 commits += st.commits
             import statistics
             med = statistics.median(tots)
-            row = dict(theta=th, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid,
+            row = dict(theta=th, seed=seed, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid,
                        index='binary' if a.binary else 'tree', txn_s=a.batch / (med / 1e3),
                        abort_rate=aborts / commits, ms_total_median=med, ms_total_min=min(tots),
                        ms_total_max=max(tots), ms_exec_median=statistics.median(execs), reps=a.reps)
