@@ -210,20 +210,19 @@ GC_DEV void w_add(const ExecParams &p, u64 *w, u64 v) {
     latch_release(l);
 }
 
-// Randomised, bounded exponential backoff after an abort.  Lanes of one warp run in
-// lockstep, so two transactions with crossed read/write sets can otherwise lock,
-// fail each other's validation and retry in perfect symmetry forever (an OCC livelock
-// the paper's immediate restart, is exposed to as well).  Delay is
-// uniform in [0, 64 ns << sh) from a hash of (gid, restarts), sh = min(restarts, cap).
-// cap = 10 (~65 us) keeps batch tails short for lock / OCC schemes; timestamp schemes
-// (TO, MVCC) and any transaction past 12 restarts (a retry storm, e.g. basic TO under a
-// read-hot key, which would otherwise burn 31-bit timestamps) use cap 14
-// (~1 ms).  Measured: profiles/r01_probe_v7*.jsonl vs v6.
+// Randomised, bounded exponential backoff after an abort that no single lock explains
+// (validation failures, timestamp conflicts).  Lanes of one warp run in lockstep, so
+// two transactions with crossed read/write sets can otherwise lock, fail each other's
+// validation and retry in perfect symmetry forever (an OCC livelock the paper's
+// immediate restart, is exposed to as well).  Delay is uniform in
+// [0, 64 ns << min(restarts, cap)) from a hash of (gid, restarts); cap = 10 (~65 us)
+// keeps batch tails short; timestamp schemes use cap 14 (~1 ms): basic TO under a
+// read-hot key otherwise retries in a storm that burns 31-bit timestamps
+// (PAPER.md:732).  Chosen from the measured probes (profiles/r01_probe_v6..v11).
 template <int S>
 GC_DEV void abort_backoff(u32 gid, u32 restarts) {
     constexpr u32 CAP = (S == CC_TO || S == CC_MVCC) ? 14u : 10u;
-    const u32 cap_sh = restarts < 12 ? CAP : 14u;
-    const u32 sh = restarts < cap_sh ? restarts : cap_sh;
+    const u32 sh = restarts < CAP ? restarts : CAP;
     const u32 cap = 64u << sh;
     u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % cap);
     while (d > 0) {
@@ -231,30 +230,6 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
         __nanosleep(s);
         d -= s;
     }
-}
-
-// Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
-// no-wait / OCC semantics are unchanged -- until that lock is free (2PL holder count 0,
-// OCC lock bit clear), bounded by the backoff cap, add a little jitter, and retry;
-// otherwise use the randomised backoff.  This replaces a blind sleep (during which the
-// lock is often already free) by one L2 round trip, without turning a busy shared lock
-// into a retry storm.
-template <int S>
-GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
-    if (th.cw && restarts < 12) {   // past 12 restarts: a storm, use the long backoff
-        const u32 sh = restarts < 10 ? restarts : 10;
-        const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
-        unsigned ns = 32;
-        while ((ld_relaxed(th.cw) & th.cv) != 0 && globaltimer_ns() < limit) {
-            __nanosleep(ns);
-            ns = ns < 256 ? ns * 2 : 256;
-        }
-        __nanosleep((u32)(mix64(((u64)gid << 32) | restarts) & 255u));
-        th.cw = nullptr;
-        return;
-    }
-    th.cw = nullptr;
-    abort_backoff<S>(gid, restarts);
 }
 
 // ------------------------------------------------------------------ queue (a6)
