@@ -232,6 +232,28 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
     }
 }
 
+// Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
+// no-wait / OCC semantics are unchanged -- until that lock is free (2PL holder count 0,
+// OCC lock bit clear), bounded, add a little jitter, and retry; otherwise use the
+// randomised backoff.  This replaces a blind sleep (during which the lock is often
+// already free) by one L2 round trip, without turning a busy shared lock into a storm.
+template <int S>
+GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
+    if (th.cw) {
+        const u32 sh = restarts < 10 ? restarts : 10;
+        const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
+        unsigned ns = 32;
+        while ((ld_relaxed(th.cw) & th.cv) != 0 && globaltimer_ns() < limit) {
+            __nanosleep(ns);
+            ns = ns < 256 ? ns * 2 : 256;
+        }
+        __nanosleep((u32)(mix64(((u64)gid << 32) | restarts) & 255u));
+        th.cw = nullptr;
+        return;
+    }
+    abort_backoff<S>(gid, restarts);
+}
+
 // ------------------------------------------------------------------ queue (a6)
 // Round 1 is the fresh batch, claimed in increasing id.  While fresh ids remain, an
 // aborted transaction is compacted into the retry batch (`ring`, appended with one
