@@ -274,6 +274,8 @@ __global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t 
     if (i < p.n_txn) {
         c = p.committed[i];
         a = p.restarts[i];
+        if (c && p.order_lo[i] >= 0xFFFFFFFFull)   // the 32-bit commit-position sort would be wrong
+            atomicCAS(&p.ctl->err.v, 0ull, (u64)CC_ERR_TS_OVERFLOW);
         r.committed[i] = (uint8_t)c;
         if (r.restarts) r.restarts[i] = a;
         if (r.order_hi) r.order_hi[i] = p.order_hi[i];
@@ -333,8 +335,10 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         iota_kernel<<<g, blk, 0, s>>>(b.gid_in, n);
         size_t bytes = b.cub_bytes;
         u64 *k1 = b.keys_in, *k2 = b.keys_out;   // n_acc >= n scratch
+        // key_lo is a ticket, a 31-bit timestamp or a gid: 32 bits suffice (copy_out flags
+        // a value >= 2^32 - 1 as an overflow), 4 radix passes instead of 8
         cudaError_t e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, p.order_lo, k1, b.gid_in,
-                                                        b.rank_order, (int)n, 0, 64, s);
+                                                        b.rank_order, (int)n, 0, 32, s);
         if (e) return e;
         if (two_pass) {
             gather_hi_kernel<<<g, blk, 0, s>>>(p.order_hi, b.rank_order, k1, n);
