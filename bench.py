@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--warehouses", type=int, default=512)
     ap.add_argument("--tpcc-batch", type=int, default=65536, help="transactions per rank per step")
     ap.add_argument("--tpcc-mix", type=int, default=5114, help="NewOrder share in 1/10,000 (45:43, PAPER.md:468)")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="tpcc: run G warehouse partitions as G dbs on this one GPU (a8 with a device-side exchange)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -396,6 +398,75 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xfla
             "note": "host wall clock around import(H2D) + submit x schemes + D2H of results"}
 
 
+def run_tpcc_loopback(args, local):
+    """configs[4] with G partitions held by G dbs on one GPU: the same phase A / pack /
+    apply / finish kernels as the multi-GPU path, the all-to-alls being device copies."""
+    import numpy as np
+    import torch
+
+    from paper_2406_10158_b200.api import DB, Result
+    from paper_2406_10158_b200.partition import loopback_round
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    G = args.loopback
+    schemes = args.schemes.split(",")
+    W, n = args.warehouses, args.tpcc_batch
+    wpr = W // G
+    dbs = []
+    for r in range(G):
+        db = DB(local, rank=r, world=G)
+        db.load_tpcc(W, 1, n, w_first=r * wpr, w_count=wpr)
+        dbs.append(db)
+    res = {s: [Result.alloc(n, 18, dev, stream=db.stream, out_words=48) for db in dbs] for s in schemes}
+
+    def step(i):
+        bs = [db.gen_tpcc(n, 7919 * (r + 1) + i, args.tpcc_mix, w_lo=r * wpr, w_hi=(r + 1) * wpr)
+              for r, db in enumerate(dbs)]
+        for s in schemes:
+            loopback_round(dbs, bs, s, results=res[s], bs=8, lanes=32, watchdog_s=60)
+        return bs
+
+    for i in range(args.warmup):
+        for b in step(i):
+            b.free()
+    for db in dbs:
+        db.sync()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    keep = [step(args.warmup + i) for i in range(args.steps)]
+    for db in dbs:
+        db.sync()
+    torch.cuda.synchronize(dev)
+    ms = (time.perf_counter() - t0) * 1e3   # G streams + host-driven exchange: host clock after full sync
+    clk = clocks.stop()
+    per = {}
+    for s in schemes:
+        c = a = 0
+        for r in res[s]:
+            h = r.stats.cpu().numpy().view(np.uint64)
+            c += int(h[0])
+            a += int(h[1])
+        per[s] = {"commits": c, "aborts": a, "abort_rate": a / max(1, c)}
+    for bs in keep:
+        for b in bs:
+            b.free()
+    value = args.steps * n * G * len(schemes) / (ms / 1e3)
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "txn/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "tpcc_configs4_partitioned_loopback", "warehouses": W, "partitions": G,
+                   "batch_per_partition": n, "neworder_permyriad": args.tpcc_mix, "schemes": schemes,
+                   "lanes_per_txn": 32, "parallelism": f"{G} warehouse partitions on 1 GPU, device-side exchange",
+                   "timing": "host clock around fully synchronised steps (G streams + host-orchestrated exchange)"},
+        "per_scheme": per, "clocks": clk}), flush=True)
+    for db in dbs:
+        db.close()
+
+
 def run_tpcc(args, rank, world, local):
     """configs[4]: TPC-C with W warehouses partitioned by contiguous ranges over the
     ranks; each rank runs its own batch of home transactions; cross-partition
@@ -485,7 +556,10 @@ def main():
         run_reference(args, rank, world)
         return
     if args.workload == "tpcc":
-        run_tpcc(args, rank, world, local)
+        if args.loopback:
+            run_tpcc_loopback(args, local)
+        else:
+            run_tpcc(args, rank, world, local)
         return
     run_ours(args, rank, world, local)
 
