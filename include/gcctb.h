@@ -306,8 +306,9 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent);
 cc_status cc_events_capacity(cc_db db, uint64_t cap);
 cc_status cc_events_read(cc_db db, void *dst, uint64_t cap, uint64_t *n_events);
 
-/* Wait for the db stream; surface asynchronous errors; if st != NULL copy the stats of
- * the last submit into it. */
+/* Wait for the db stream; surface asynchronous errors -- the first device error of any
+ * submit since the previous cc_sync (sticky across submits); if st != NULL copy the stats
+ * of the last submit into it. */
 cc_status cc_sync(cc_db db, cc_stats *st);
 
 /* Phase timing (CC_FLAG_TIMING): accumulated milliseconds per phase over the submits

@@ -769,6 +769,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.lanes = desc->lanes_per_txn <= 1 ? 1 : (is_tpcc ? 32 : desc->lanes_per_txn);
     p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
     p.ctl = db->ctl;
+    p.sticky = db->sticky_dev;
     p.meta = db->meta;
     p.arena = db->arena;
     p.ring = db->ring;
@@ -1042,7 +1043,10 @@ cc_status cc_sync(cc_db db, cc_stats *out) {
     if (out) *out = s;
     Ctl c;
     CUDA_TRY(db, cudaMemcpy(&c, db->ctl, sizeof c, cudaMemcpyDeviceToHost));
-    const u64 e = c.err.v ? c.err.v : w[3];
+    u64 sticky = 0;
+    CUDA_TRY(db, cudaMemcpy(&sticky, db->sticky_dev, 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(db, cudaMemset(db->sticky_dev, 0, 8));
+    const u64 e = sticky ? sticky : (c.err.v ? c.err.v : w[3]);
     if (e) {
         static const char *names[] = {"ok", "invalid arg", "config", "oom", "cuda", "nccl",
                                       "key not found", "timestamp overflow", "version exhausted",

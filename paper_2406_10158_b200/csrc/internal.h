@@ -70,6 +70,7 @@ struct ExecParams {
     const uint8_t *skip;         // partitioned TPC-C: 1 = distributed txn, left to phase B
     uint32_t *latch;             // CC_FLAG_LATCHED: one 32-bit latch per control word
     unsigned long long *stages;  // CC_FLAG_STAGES: accumulated cycles per stage (STAGE_*)
+    unsigned long long *sticky;  // first device error of any submit since the last cc_sync
     Event *events;               // CC_FLAG_EVENTS: event log (capacity events_cap)
     unsigned long long events_cap;
 };

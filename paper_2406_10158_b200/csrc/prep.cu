@@ -309,7 +309,9 @@ cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads,
     return cudaGetLastError();
 }
 
-__global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long long *stages) {
+__global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
+                             unsigned long long *sticky) {
+    if (c->err && sticky) atomicCAS(sticky, 0ull, c->err.v);   // survives the next submit's reset
     stats[0] = c->done.v;
     stats[1] = c->aborts.v;
     stats[2] = c->done.v + c->aborts.v;
@@ -352,7 +354,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         }
     }
     copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);
-    stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats, p.stages);
+    stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats, p.stages, p.sticky);
     return cudaGetLastError();
 }
 

@@ -310,3 +310,20 @@ def test_event_log_conflict_graph(c1, orc, scheme, lanes):
     ok, info = check_serializable(ev)
     assert ok, f"cycle {info}"
     b.free()
+
+
+def test_device_error_is_sticky_across_submits(c1):
+    """A device error of an earlier submit is reported by the next cc_sync even when
+    later submits (which reset the per-submit control block) succeeded."""
+    from paper_2406_10158_b200.gcctb import CCError
+    db, _ = c1
+    bad = db.import_ycsb(np.array([1, 5000], np.uint32), np.array([0, 0], np.uint8), 2)
+    good = db.import_ycsb(np.array([1, 2], np.uint32), np.array([0, 0], np.uint8), 2)
+    db.submit(bad, "tictoc")
+    db.submit(good, "tictoc")
+    with pytest.raises(CCError, match="KEY_NOT_FOUND"):
+        db.sync()
+    db.submit(good, "tictoc")
+    assert db.sync().commits == 1     # cleared after being reported
+    bad.free()
+    good.free()
