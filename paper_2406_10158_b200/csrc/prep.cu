@@ -311,7 +311,7 @@ cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads,
 
 __global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
                              unsigned long long *sticky) {
-    if (c->err && sticky) atomicCAS(sticky, 0ull, c->err.v);   // survives the next submit's reset
+    if (c->err.v && sticky) atomicCAS(sticky, 0ull, c->err.v);   // survives the next submit's reset
     stats[0] = c->done.v;
     stats[1] = c->aborts.v;
     stats[2] = c->done.v + c->aborts.v;
