@@ -104,3 +104,28 @@ def test_c3_full_size_parity(c3, orc, scheme, lanes):
     b = db.gen_tpcc(16384, 31, 5000)
     _run(db, S0, 1, b, scheme, lanes, orc)
     b.free()
+
+
+@pytest.fixture(scope="module")
+def c4(torch_cuda, orc):
+    """BASELINE.json configs[3]: 64 warehouses, 45:43 NewOrder/Payment, batch 64K."""
+    db = _db(64, 9, 65536)
+    S0 = IT.population(9, 64)
+    got = db.read_tpcc(["warehouse", "district"])
+    assert np.array_equal(got["warehouse"], S0["warehouse"]) and np.array_equal(got["district"], S0["district"])
+    for k in ("customer", "stock"):   # sampled rows of the big tables (the full compare is below)
+        t = db.read_table(db.tpcc_ids[k])
+        idx = np.random.default_rng(1).integers(0, t.shape[0], 4096)
+        assert np.array_equal(t[idx], S0[k][idx])
+    db.snapshot(True)
+    yield db, S0
+    db.close()
+
+
+@pytest.mark.parametrize("lanes", [1, 32])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c4_full_size_parity(c4, orc, scheme, lanes):
+    db, S0 = c4
+    b = db.gen_tpcc(65536, 41, 5114)
+    _run(db, S0, 64, b, scheme, lanes, orc)
+    b.free()
