@@ -232,6 +232,7 @@ typedef struct {
                                transaction; wd is ignored).  TPC-C batches use 32-lane
                                tiles for any value > 1 */
     double watchdog_s;      /* device watchdog in seconds (0 = 30 s) */
+    uint32_t claim_chunk;   /* fresh transaction ids a worker claims per atomic (0 = 1) */
 } cc_exec_desc;
 
 /* Per-transaction results, all DEVICE pointers owned by the caller.  Any may be NULL

@@ -239,12 +239,12 @@ class DB:
     # ----------------------------------------------------------- execution
     def submit(self, batch: Batch, scheme, wd: int = 0, bs: int = 32, flags: int = 0,
                grid: int = 0, watchdog_s: float = 30.0, result: Result | None = None,
-               read_out=True, lanes: int = 1) -> Result:
+               read_out=True, lanes: int = 1, claim_chunk: int = 1) -> Result:
         sid = G.SCHEME_ID[scheme] if isinstance(scheme, str) else int(scheme)
         if result is None:
             result = Result.alloc(batch.n_txn, batch.K, torch.device("cuda", self.device), read_out,
                                   stream=self.stream, out_words=batch.out_words)
-        d = G.cc_exec_desc(sid, wd, bs, flags, grid, lanes, watchdog_s)
+        d = G.cc_exec_desc(sid, wd, bs, flags, grid, lanes, watchdog_s, claim_chunk)
         r = result.c()
         self._chk(G.lib().cc_submit(self.h, batch.h, ctypes.byref(d), ctypes.byref(r)))
         return result

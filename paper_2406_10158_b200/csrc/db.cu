@@ -767,6 +767,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.wd = desc->wd;
     p.flags = desc->flags;
     p.lanes = desc->lanes_per_txn <= 1 ? 1 : (is_tpcc ? 32 : desc->lanes_per_txn);
+    p.claim_chunk = desc->claim_chunk ? desc->claim_chunk : 1;
     p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
     p.ctl = db->ctl;
     p.sticky = db->sticky_dev;

@@ -284,6 +284,7 @@ struct Claim {
     bool exhausted = false;
     bool sealed = false;
     u64 tail = 0;
+    u64 next = 0, end = 0;   // fresh ids claimed ahead (chunked claims), processed in order
 };
 
 // Claim work for one worker: a fresh id, else a retry-batch entry, else NO_TXN.
@@ -293,7 +294,13 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
     Ctl *c = p.ctl;
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
     if (!cl.exhausted) {
-        const u64 s = atomicAdd(&c->head.v, 1ull);
+        // chunked claims: one atomic per `claim_chunk` ids; ids stay increasing per worker
+        // and across workers' chunks, so every waited-on transaction is already claimed
+        if (cl.next >= cl.end) {
+            cl.next = atomicAdd(&c->head.v, (u64)p.claim_chunk);
+            cl.end = cl.next + p.claim_chunk;
+        }
+        const u64 s = cl.next++;
         if (s < p.n_txn) return (S == CC_GPUTX) ? p.rank_order[s] : (u32)s;
         cl.exhausted = true;
     }

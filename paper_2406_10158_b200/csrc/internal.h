@@ -46,6 +46,7 @@ struct ExecParams {
     uint32_t wd;
     uint32_t flags;
     uint32_t lanes;              // lanes per transaction (1 = thread per txn)
+    uint32_t claim_chunk;        // fresh ids claimed per atomic (>= 1)
     unsigned long long watchdog_ns;
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)

@@ -62,7 +62,8 @@ class cc_tpcc_gen_desc(ctypes.Structure):
 class cc_exec_desc(ctypes.Structure):
     _fields_ = [("scheme", ctypes.c_int), ("wd", ctypes.c_uint32), ("bs", ctypes.c_uint32),
                 ("flags", ctypes.c_uint32), ("grid", ctypes.c_uint32),
-                ("lanes_per_txn", ctypes.c_uint32), ("watchdog_s", ctypes.c_double)]
+                ("lanes_per_txn", ctypes.c_uint32), ("watchdog_s", ctypes.c_double),
+                ("claim_chunk", ctypes.c_uint32)]
 
 
 class cc_result(ctypes.Structure):
