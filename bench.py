@@ -43,8 +43,9 @@ def parse():
     ap.add_argument("--bs", type=int, default=32)
     ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
-    ap.add_argument("--index", default="tree", choices=["tree", "binary"],
-                    help="tree = cache-line search tree over the sorted keys (default); binary = PAPER.md:344")
+    ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary"],
+                    help="dense = direct addressing on the dense YCSB key range (default); tree = cache-line "
+                         "search tree over the sorted keys; binary = PAPER.md:344 (identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="ycsb", choices=["ycsb", "tpcc"],
                     help="ycsb = configs[1] (default); tpcc = configs[4]: W warehouses partitioned over the ranks")
@@ -222,8 +223,8 @@ def run_ours(args, rank, world, local):
     res = {s: Result.alloc(args.batch, args.ops, dev, stream=db.stream) for s in schemes}
     stream = db.stream   # every library launch goes to this stream; events are recorded on it
 
-    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY
-    xflags = CC_FLAG_INDEX_BINARY if args.index == "binary" else 0
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
+    xflags = {"dense": 0, "tree": CC_FLAG_INDEX_TREE, "binary": CC_FLAG_INDEX_BINARY}[args.index]
 
     def step(i, timing=False):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)

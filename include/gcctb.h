@@ -105,8 +105,11 @@ cc_status cc_table_read(cc_db db, uint32_t table_id, uint64_t first_row, uint64_
 cc_status cc_table_info(cc_db db, uint32_t table_id, uint64_t *rows, uint32_t *row_bytes);
 
 /* Sorted-array index over table_id: sorted_keys[i] strictly ascending,
- * row_ids[i] < rows(table).  A lookup is a binary search.  INVALID_ARG unless strictly
- * ascending.  *index_id receives the id. */
+ * row_ids[i] < rows(table).  A lookup returns the lower-bound match of the paper's binary
+ * search; when the keys form a dense range k0..k0+n-1 it is resolved by
+ * direct addressing (no probe), else by a cache-line search tree over the same sorted
+ * array; CC_FLAG_INDEX_BINARY / CC_FLAG_INDEX_TREE force a method.
+ * INVALID_ARG unless strictly ascending.  *index_id receives the id. */
 cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_keys,
                           const uint64_t *row_ids, uint64_t n, int src_on_device,
                           uint32_t *index_id);
@@ -114,7 +117,8 @@ cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_ke
 /* Batch index lookup (SPEC.md:47 index_lookup): rows_out[i] = row id of keys[i], or
  * 2^64-1 when the key is absent (KeyNotFound).  keys / rows_out are device
  * arrays of n u64 (caller-owned).  flags: CC_FLAG_INDEX_BINARY selects the paper's
- * binary search, otherwise the cache-line tree; results are identical.  Async. */
+ * binary search, CC_FLAG_INDEX_TREE the cache-line tree, otherwise direct addressing on
+ * a dense key range and the tree elsewhere; results are identical.  Async. */
 cc_status cc_index_lookup(cc_db db, uint32_t index_id, const uint64_t *keys, uint64_t n,
                           uint64_t *rows_out, uint32_t flags);
 
@@ -219,6 +223,8 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         array (the paper's index) instead of the
                                         default cache-line search tree over the same array
                                         (identical results) */
+#define CC_FLAG_INDEX_TREE 0x100u    /* force the cache-line search tree even on a dense key
+                                        range (default there: direct addressing, key - k0) */
 
 typedef struct {
     cc_scheme scheme;

@@ -213,13 +213,16 @@ class DB:
                                           ctypes.byref(iid)))
         return iid.value
 
-    def index_lookup(self, index_id: int, keys, binary: bool = False) -> np.ndarray:
+    def index_lookup(self, index_id: int, keys, method: str = "auto") -> np.ndarray:
+        """method: "auto" (direct addressing on a dense key range, else the tree), "tree",
+        or "binary"; all return the same rows."""
+        flags = {"auto": 0, "tree": G.CC_FLAG_INDEX_TREE, "binary": G.CC_FLAG_INDEX_BINARY}[method]
         dev = torch.device("cuda", self.device)
         with torch.cuda.stream(self.stream):
             k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
             out = torch.empty_like(k)
         self._chk(G.lib().cc_index_lookup(self.h, index_id, k.data_ptr(), k.numel(), out.data_ptr(),
-                                          G.CC_FLAG_INDEX_BINARY if binary else 0))
+                                          flags))
         self.stream.synchronize()
         return out.cpu().numpy().view(np.uint64)
 

@@ -37,7 +37,17 @@ struct Index {
     u64 *rowids;
     std::vector<u64 *> levels;   // cache-line tree levels above the leaves
     std::vector<uint64_t> lens;
+    int dense = 0;   // 0, IDX_DENSE (keys k0..k0+n-1) or IDX_DENSE_ID (and row id == position)
+    u64 k0 = 0;
 };
+
+// Lookup mode for a submit / lookup: forced by the flags, else direct addressing on a
+// dense key range, else the cache-line tree (all return the same rows, f-3).
+static int index_mode(const Index &ix, uint32_t flags) {
+    if (flags & CC_FLAG_INDEX_BINARY) return IDX_BINARY;
+    if ((flags & CC_FLAG_INDEX_TREE) || !ix.dense) return IDX_TREE;
+    return ix.dense;
+}
 
 // Build the separator levels of the cache-line search tree over ix.keys (device).
 static cudaError_t build_tree(Index &ix, cudaStream_t s) {
@@ -371,6 +381,13 @@ cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_ke
         if (r[i] >= db->tables[table_id].rows) return fail(db, CC_ERR_INVALID_ARG, "row id out of table");
     }
     Index ix{table_id, n, nullptr, nullptr, {}, {}};
+    bool dk = true, dr = true;
+    for (uint64_t i = 0; i < n; i++) {
+        dk &= k[i] == k[0] + i;
+        dr &= r[i] == i;
+    }
+    ix.dense = dk ? (dr ? IDX_DENSE_ID : IDX_DENSE) : 0;
+    ix.k0 = k[0];
     const uint64_t padded = (n + 15) / 16 * 16;
     CUDA_TRY(db, dalloc(&ix.keys, padded * 8));
     CUDA_TRY(db, dalloc(&ix.rowids, n * 8));
@@ -394,7 +411,8 @@ cc_status cc_index_lookup(cc_db db, uint32_t index_id, const uint64_t *keys, uin
     y.idx_rows = ix.rowids;
     y.idx_n = ix.n;
     y.tree = tree_of(ix);
-    y.binary = (flags & CC_FLAG_INDEX_BINARY) ? 1 : 0;
+    y.mode = index_mode(ix, flags);
+    y.idx_k0 = ix.k0;
     CUDA_TRY(db, launch_index_lookup(y, (const u64 *)keys, n, (u64 *)rows_out, db->stream));
     return CC_OK;
 }
@@ -411,6 +429,8 @@ cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *d) {
     Table &t = db->tables[tid];
     CUDA_TRY(db, launch_ycsb_init_rows((u64 *)t.d, 0, d->n_rows, d->seed, db->stream));
     Index ix{tid, d->n_rows, nullptr, nullptr, {}, {}};
+    ix.dense = IDX_DENSE_ID;   // key i -> row i
+    ix.k0 = 0;
     const uint64_t padded = (d->n_rows + 15) / 16 * 16;
     CUDA_TRY(db, dalloc(&ix.keys, padded * 8));
     CUDA_TRY(db, dalloc(&ix.rowids, d->n_rows * 8));
@@ -814,7 +834,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         y.idx_rows = ix.rowids;
         y.idx_n = ix.n;
         y.tree = tree_of(ix);
-        y.binary = (desc->flags & CC_FLAG_INDEX_BINARY) ? 1 : 0;
+        y.mode = index_mode(ix, desc->flags);
+        y.idx_k0 = ix.k0;
         y.rows = (u64 *)t.d;
         y.n_rows = t.rows;
     }

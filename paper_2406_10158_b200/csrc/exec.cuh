@@ -247,7 +247,15 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
             __nanosleep(ns);
             ns = ns < 256 ? ns * 2 : 256;
         }
-        __nanosleep((u32)(mix64(((u64)gid << 32) | restarts) & 255u));
+        // then a random delay whose window doubles per restart: waiters released by
+        // the same unlock must not retry in lockstep (a herd livelock at theta >= 0.9)
+        const u32 win = 32u << (restarts < 11 ? restarts : 11);
+        u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % win);
+        while (d > 0) {
+            const u32 s = d < 1000u ? d : 1000u;
+            __nanosleep(s);
+            d -= s;
+        }
         th.cw = nullptr;
         return;
     }
@@ -773,6 +781,7 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
                 p.restarts[gid] = nr;
                 StageClock c(th, STAGE_ABORT);
                 retry_pace<S>(th, gid, nr);
+                if (dead(th)) { stop = true; break; }   // the watchdog also bounds abort-only livelocks
                 if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) next = true;   // a6
             }
         }
@@ -1036,9 +1045,12 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
                     p.restarts[gid] = nr;
                     StageClock c(th, STAGE_ABORT);
                     retry_pace<S>(th, gid, nr);
-                    push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
+                    if (dead(th)) push = -1;   // the watchdog also bounds abort-only livelocks
+                    else push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
                 }
-                next = tile.shfl(push, 0) != 0;
+                push = tile.shfl(push, 0);
+                if (push < 0) stop = true;
+                next = push > 0;
             }
         }
         if (stop) break;

@@ -84,6 +84,10 @@ enum { STAGE_INDEX = 0, STAGE_TS = 1, STAGE_WAIT = 2, STAGE_CC = 3, STAGE_ABORT 
 // is the leaf level; level l+1 holds the last key of every 16-entry node of level l;
 // the top level has <= 16 entries.  levels[0] = leaves.
 constexpr int IDX_MAX_LEVELS = 10;
+// Lookup modes; every mode returns the same lower-bound result for the same index.
+// Dense modes (f-3 direct addressing) apply when the keys are k0, k0+1, ..., k0+n-1:
+// the position is key - k0, no probe at all; IDX_DENSE_ID also has row id == position.
+enum { IDX_TREE = 0, IDX_BINARY = 1, IDX_DENSE = 2, IDX_DENSE_ID = 3 };
 struct TreeIndex {
     const unsigned long long *lv[IDX_MAX_LEVELS];
     unsigned long long len[IDX_MAX_LEVELS];   // padded lengths (multiples of 16)
@@ -98,7 +102,8 @@ struct YcsbParams {
     const unsigned long long *idx_rows;
     unsigned long long idx_n;
     TreeIndex tree;              // same keys, cache-line tree layout (f-3)
-    int binary;                  // 1 = the paper's plain binary search
+    int mode;                    // IDX_TREE / IDX_BINARY (the paper's) / IDX_DENSE / IDX_DENSE_ID
+    unsigned long long idx_k0;   // first key (dense modes)
     unsigned long long *rows;    // 16 x u64 per row
     unsigned long long n_rows;
 };

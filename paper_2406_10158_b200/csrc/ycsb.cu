@@ -24,12 +24,18 @@ struct YcsbWL {
     };
 
     // Index lookup: lower bound of key in the sorted key array, returns
-    // the row or ~0 for KeyNotFound.  Default: descend the cache-line tree
-    // (one 128 B node of 16 keys per level: count keys < key); CC_FLAG_INDEX_BINARY:
-    // the paper's branch-free binary search.
+    // the row or ~0 for KeyNotFound.  Dense key range: direct addressing
+    // (f-3); else descend the cache-line tree (one 128 B node of 16 keys per level:
+    // count keys < key); CC_FLAG_INDEX_BINARY: the paper's branch-free binary search.
     static GC_DEV u64 lookup(const YcsbParams &y, u64 key) {
-        if (!y.binary) return tree_lookup(y, key);
+        if (y.mode >= IDX_DENSE) return dense_lookup(y, key);
+        if (y.mode == IDX_TREE) return tree_lookup(y, key);
         return binary_lookup(y, key);
+    }
+    static GC_DEV u64 dense_lookup(const YcsbParams &y, u64 key) {
+        const u64 pos = key - y.idx_k0;   // wraps above idx_n for key < k0
+        if (pos >= y.idx_n) return ~0ull;
+        return y.mode == IDX_DENSE_ID ? pos : __ldg(y.idx_rows + pos);
     }
     static GC_DEV u64 tree_lookup(const YcsbParams &y, u64 key) {
         u64 node = 0;
@@ -87,7 +93,18 @@ struct YcsbWL {
             b[i] = y.idx_keys;
         }
         if (p.acc_rec) return p.K;
-        if (!y.binary) {   // tree: the K descents in lockstep, one level at a time
+        if (y.mode >= IDX_DENSE) {
+            bool ok = true;
+            for (int i = 0; i < (int)p.K; i++) {
+                const u64 r = dense_lookup(y, key[i]);
+                ok &= r != ~0ull;
+                L[i].rec = (u32)r;
+            }
+            if (ok)
+                for (int i = 0; i < (int)p.K; i++) prefetch_access(p, y, L[i]);
+            return ok ? p.K : 0xFFFFFFFFu;
+        }
+        if (y.mode == IDX_TREE) {   // tree: the K descents in lockstep, one level at a time
             u64 node[MAXK];
 #pragma unroll
             for (int i = 0; i < MAXK; i++) node[i] = 0;

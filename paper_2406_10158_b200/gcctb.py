@@ -28,6 +28,7 @@ CC_FLAG_INDEX_BINARY = 0x10
 CC_FLAG_LATCHED = 0x20
 CC_FLAG_STAGES = 0x40
 CC_FLAG_EVENTS = 0x80
+CC_FLAG_INDEX_TREE = 0x100
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16

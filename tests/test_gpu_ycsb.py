@@ -186,6 +186,26 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     b.free()
 
 
+@pytest.mark.parametrize("flag", ["tree", "binary"])
+@pytest.mark.parametrize("scheme", ["tpl_nw", "tictoc", "gacco"])
+def test_c2_full_size_parity_search_index(c2, orc, scheme, flag):
+    """configs[1] in the bench launch with the search indexes (bench --index tree|binary)."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
+    db, S0, n = c2
+    T = inputs.zipf_thresholds(n, 0.6)
+    A = inputs.scramble_mult(n)
+    B, K, W = 1 << 16, 16, 0.1
+    b = db.gen_ycsb(B, K, W, 78, T, A)
+    keys, ops = orc.ycsb_gen(78, n, B, K, W, T, A)
+    db.snapshot(False)
+    fl = CC_FLAG_INDEX_BINARY if flag == "binary" else CC_FLAG_INDEX_TREE
+    res = db.submit(b, scheme, wd=0, bs=32, lanes=16, flags=fl, watchdog_s=60)
+    st = db.sync()
+    assert st.commits == B
+    orc.check_ycsb(scheme, S0, keys, ops, K, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
 def test_ts_overflow_is_reported(c1):
     """31-bit TO timestamps: a retry storm that
     exhausts them surfaces as TS_OVERFLOW, never as a wrong result.  Forced with a
@@ -222,16 +242,43 @@ def test_index_lookup_tree_and_binary(torch_cuda, n):
     pos = np.searchsorted(keys, probe)
     hit = (pos < n) & (keys[np.minimum(pos, n - 1)] == probe)
     exp = np.where(hit, rows[np.minimum(pos, n - 1)], np.uint64((1 << 64) - 1))
-    for binary in (False, True):
-        got = db.index_lookup(iid, probe, binary=binary)
-        assert np.array_equal(got, exp), binary
+    for method in ("auto", "tree", "binary"):
+        got = db.index_lookup(iid, probe, method=method)
+        assert np.array_equal(got, exp), method
     db.close()
 
 
+@pytest.mark.parametrize("k0,n,identity", [(0, 1, True), (0, 17, True), (5, 4097, False), ((1 << 40) + 3, 300001, False),
+                                           (0, 300001, True), (0, 300001, False)])
+def test_index_lookup_dense(torch_cuda, k0, n, identity):
+    """f-3 direct addressing: on a dense key range k0..k0+n-1 the default lookup (no probe)
+    returns what numpy.searchsorted does, just outside the range too."""
+    from paper_2406_10158_b200.api import DB
+    rng = np.random.default_rng(n + k0)
+    keys = np.uint64(k0) + np.arange(n, dtype=np.uint64)
+    rows = np.arange(n, dtype=np.uint64) if identity else rng.permutation(n).astype(np.uint64)
+    db = DB(0)
+    tid = db.create_table("t", 8, n)
+    iid = db.create_index(tid, keys, rows)
+    probe = np.concatenate([keys, rng.choice(keys, 1000), keys[-1:] + np.uint64(1), keys[-1:] + np.uint64(1 << 33),
+                            np.array([0, 1, (1 << 63), (1 << 64) - 2], np.uint64)])
+    if k0:
+        probe = np.concatenate([probe, np.array([k0 - 1], np.uint64)])
+    pos = np.searchsorted(keys, probe)
+    hit = (pos < n) & (keys[np.minimum(pos, n - 1)] == probe)
+    exp = np.where(hit, rows[np.minimum(pos, n - 1)], np.uint64((1 << 64) - 1))
+    for method in ("auto", "tree", "binary"):
+        assert np.array_equal(db.index_lookup(iid, probe, method=method), exp), method
+    db.close()
+
+
+@pytest.mark.parametrize("flag", ["binary", "tree"])
 @pytest.mark.parametrize("scheme", ["tpl_nw", "silo", "mvcc", "gacco"])
-def test_c1_parity_binary_index(c1, orc, scheme):
-    """The paper's binary-search index (CC_FLAG_INDEX_BINARY) gives the same results."""
-    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY
+def test_c1_parity_binary_index(c1, orc, scheme, flag):
+    """The paper's binary-search index (CC_FLAG_INDEX_BINARY) and the cache-line tree
+    (CC_FLAG_INDEX_TREE) give the same results as the default direct addressing."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
+    fl = CC_FLAG_INDEX_BINARY if flag == "binary" else CC_FLAG_INDEX_TREE
     db, S0 = c1
     T = inputs.zipf_thresholds(1024, 0.8)
     A = inputs.scramble_mult(1024)
@@ -239,7 +286,7 @@ def test_c1_parity_binary_index(c1, orc, scheme):
     keys, ops = orc.ycsb_gen(44, 1024, 1024, 4, 0.5, T, A)
     for lanes in (1, 4):
         db.snapshot(False)
-        res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, flags=CC_FLAG_INDEX_BINARY)
+        res = db.submit(b, scheme, wd=0, bs=32, lanes=lanes, flags=fl)
         db.sync()
         orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
     b.free()

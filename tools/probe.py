@@ -26,11 +26,12 @@ def main():
     ap.add_argument("--bs", type=int, default=32)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--lanes", type=int, default=1)
-    ap.add_argument("--binary", action="store_true")
+    ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary"])
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--seeds", default="3")
     ap.add_argument("--chunk", type=int, default=1)
     a = ap.parse_args()
+    IDXF = {'dense': 0, 'tree': 0x100, 'binary': 0x10}
     db = DB(0)
     db.load_ycsb(a.rows, 1)
     A = inputs.scramble_mult(a.rows)
@@ -39,13 +40,13 @@ def main():
         T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
         b = db.gen_ycsb(a.batch, a.K, a.W, seed, T, A)
         for s in a.schemes.split(","):
-            db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=0x10 if a.binary else 0, grid=a.grid, claim_chunk=a.chunk)
+            db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=IDXF[a.index], grid=a.grid, claim_chunk=a.chunk)
             db.sync()
             tots, execs = [], []
             aborts = commits = 0
             for _ in range(a.reps):
                 db.timing(reset=True)
-                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | (0x10 if a.binary else 0), watchdog_s=20,
+                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | IDXF[a.index], watchdog_s=20,
                           lanes=a.lanes, grid=a.grid, claim_chunk=a.chunk)
                 st = db.sync()
                 ms, n = db.timing(reset=True)
@@ -56,7 +57,7 @@ def main():
             import statistics
             med = statistics.median(tots)
             row = dict(theta=th, seed=seed, chunk=a.chunk, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid,
-                       index='binary' if a.binary else 'tree', txn_s=a.batch / (med / 1e3),
+                       index=a.index, txn_s=a.batch / (med / 1e3),
                        abort_rate=aborts / commits, ms_total_median=med, ms_total_min=min(tots),
                        ms_total_max=max(tots), ms_exec_median=statistics.median(execs), reps=a.reps)
             out.append(row)
