@@ -74,13 +74,14 @@ def wdbs_table(rows):
 
 def stages_table(rows):
     st = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful"]
-    out = ["| preset | mode | scheme | " + " | ".join(st) + " | (ns per committed txn) |",
-           "|---|---|---|" + "---|" * len(st) + "---|"]
+    out = ["| preset | mode | index | scheme | " + " | ".join(st) + " | (ns per committed txn) |",
+           "|---|---|---|---|" + "---|" * len(st) + "---|"]
     for r in rows:
         if "stage_ns_per_txn" not in r:
             continue
         d = r["stage_ns_per_txn"]
-        out.append(f"| {r['preset']} | {r['mode']} | {r['scheme']} | " + " | ".join(f"{d[k]:.0f}" for k in st) + " | |")
+        out.append(f"| {r['preset']} | {r['mode']} | {r.get('index', 'tree')} | {r['scheme']} | "
+                   + " | ".join(f"{d[k]:.0f}" for k in st) + " | |")
     return "\n".join(out)
 
 

@@ -47,6 +47,9 @@ def cell(db, b, scheme, reps, watchdog, **kw):
                 abort_rate=ab / max(cm, 1))
 
 
+IDXF = {"dense": 0, "tree": 0x100, "binary": 0x10}   # CC_FLAG_INDEX_TREE / CC_FLAG_INDEX_BINARY
+
+
 def ycsb_db(rows):
     db = DB(0)
     db.load_ycsb(rows, 1)
@@ -118,7 +121,7 @@ def sweep_stages(a, out):
             for s in SCHEMES:
                 try:
                     db.timing(reset=True)
-                    db.submit(b, s, flags=CC_FLAG_STAGES | CC_FLAG_TIMING, watchdog_s=a.watchdog, **kw)
+                    db.submit(b, s, flags=CC_FLAG_STAGES | CC_FLAG_TIMING | IDXF[a.index], watchdog_s=a.watchdog, **kw)
                     st = db.sync()
                     ms, _ = db.timing(reset=True)
                     ns_per_cycle = 1e6 / max(st.sm_clock_khz, 1)
@@ -130,7 +133,7 @@ def sweep_stages(a, out):
                     db.close()
                     db = ycsb_db(a.rows)
                     b = db.gen_ycsb(a.batch, 16, W, 13, T, A)
-                r.update(exp="stages", preset=name, mode=mode, scheme=s)
+                r.update(exp="stages", preset=name, mode=mode, scheme=s, index=a.index)
                 out.write(json.dumps(r) + "\n")
                 out.flush()
         b.free()
@@ -208,6 +211,8 @@ def main():
     ap.add_argument("--watchdog", type=float, default=20.0)
     ap.add_argument("--budget-ms", type=float, default=3000.0)
     ap.add_argument("--out", default="-")
+    ap.add_argument("--index", default="dense", choices=list(IDXF),
+                    help="stages: YCSB index (binary = the paper's, PAPER.md:344)")
     a = ap.parse_args()
     out = sys.stdout if a.out == "-" else open(a.out, "a")
     t0 = time.time()
