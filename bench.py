@@ -303,10 +303,10 @@ def run_ours(args, rank, world, local):
         peaks = load_peaks()
         peak = peaks["hbm_gbs"] if peaks else 6650.0
         achieved = alg_bytes_total / (exec_ms_total / 1e3) / 1e9
-        tr = load_traffic()
         traffic = None
-        if tr and tr.get("config") == config_key(args):
-            traffic = tr.get("dram_bytes_per_launch")
+        for tr in load_traffic() or []:   # ncu --set full DRAM bytes per launch, this exact config
+            if tr.get("config") == config_key(args):
+                traffic = tr.get("dram_bytes_per_launch")
         exec_share = phase_ms[2] / phase_ms[4] if phase_ms[4] else None
         line = {
             "metric": METRIC, "value": value, "unit": "txn/s", "n_gpus": world, "steps": args.steps,
