@@ -47,6 +47,8 @@ def parse():
                     help="dense = direct addressing on the dense YCSB key range (default); tree = cache-line "
                          "search tree over the sorted keys; binary = PAPER.md:344 (identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="run GPUTx / GaccO preprocessing inline instead of on the prep stream (f-4 ablation)")
     ap.add_argument("--workload", default="ycsb", choices=["ycsb", "tpcc"],
                     help="ycsb = configs[1] (default); tpcc = configs[4]: W warehouses partitioned over the ranks")
     ap.add_argument("--warehouses", type=int, default=512)
@@ -198,6 +200,7 @@ def config_of(args, world):
     return {"workload": "ycsb_configs1_10Mrows_64Kx16", "rows": args.rows, "batch": args.batch,
             "ops_per_txn": args.ops, "theta": args.theta, "write_frac": args.write_frac,
             "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs, "lanes_per_txn": args.lanes, "index": args.index,
+            "prep": "inline" if args.no_pipeline else "pipelined (cc_prepare on a second stream)",
             "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (1.34 GB table, 168 MB CC words)"}
 
 
@@ -226,8 +229,15 @@ def run_ours(args, rank, world, local):
     from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
     xflags = {"dense": 0, "tree": CC_FLAG_INDEX_TREE, "binary": CC_FLAG_INDEX_BINARY}[args.index]
 
+    def prepare(b):
+        """f-4: GPUTx / GaccO a3 on the prep stream, overlapping the other schemes' execution."""
+        if not args.no_pipeline:
+            for s in schemes:
+                db.prepare(b, s, xflags)
+
     def step(i, timing=False):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
+        prepare(b)
         for s in schemes:
             db.submit(b, s, wd=args.wd, bs=args.bs, flags=xflags | (CC_FLAG_TIMING if timing else 0),
                       result=res[s], watchdog_s=60, lanes=args.lanes)
@@ -317,7 +327,7 @@ def run_ours(args, rank, world, local):
             "per_scheme": per,
             "clocks": clk,
             "e2e": e2e,
-            "gpu_launches": launches_per_step(schemes) * args.steps,
+            "gpu_launches": launches_per_step(schemes, not args.no_pipeline) * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "exec_kernel (a4-a6), all schemes",
@@ -339,16 +349,17 @@ def config_key(args):
             f"wd={args.wd} bs={args.bs} lanes={args.lanes} index={args.index}")
 
 
-def launches_per_step(schemes):
+def launches_per_step(schemes, pipelined=False):
     """Kernel launches issued by libgcctb per step: 1 generator + per scheme: reset 2,
     exec 1, finalize (non-deterministic: iota + CUB radix sort (counted 1) + commit_pos
     + copy_out = 4, TicToc +2; deterministic: iota + commit_pos + copy_out = 3), plus
-    GaccO prep 6 (gather, sort, flags, scan, starts, positions) and GPUTx prep 13."""
+    GaccO prep 6 (gather, sort, flags, scan, starts, positions) and GPUTx prep 13
+    (pipelined: on the prep stream, + 1 error merge at submit)."""
     n = 1
     for s in schemes:
         n += 3
         if s in ("gputx", "gacco"):
-            n += 3 + (6 if s == "gacco" else 13)
+            n += 3 + (6 if s == "gacco" else 13) + (1 if pipelined else 0)
         else:
             n += 4 + (2 if s == "tictoc" else 0)
     return n
@@ -369,6 +380,9 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xfla
 
     def one():
         b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
+        if not args.no_pipeline:
+            for s in schemes:
+                db.prepare(b, s, xflags)
         with torch.cuda.stream(stream):
             for s in schemes:
                 db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes,

@@ -161,6 +161,10 @@ cc_status cc_batch_export_ycsb(cc_db db, cc_batch b, uint32_t *keys, uint8_t *op
 /* Batch geometry. */
 cc_status cc_batch_info(cc_db db, cc_batch b, uint32_t *n_txn, uint32_t *ops_per_txn,
                         uint32_t *kind);
+/* Release a batch.  Its device buffers go to a per-db pool (up to 16 batches) and are
+ * reused, in db-stream order, by the next batch of the same kind and shape, so that a
+ * steady stream of batches makes no cudaMalloc / cudaFree calls; the handle is invalid
+ * afterwards (it may come back from a later gen / import).  cc_db_destroy frees the pool. */
 cc_status cc_batch_free(cc_db db, cc_batch b);
 
 /* ----------------------------------------------------------------- TPC-C
@@ -223,6 +227,9 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         array (the paper's index) instead of the
                                         default cache-line search tree over the same array
                                         (identical results) */
+#define CC_FLAG_FLAT_JITTER 0x200u   /* ablation: after waiting out a conflicting lock, retry
+                                        with a flat 0..255 ns jitter instead of a window that
+                                        doubles per restart (retry pacing) */
 #define CC_FLAG_INDEX_TREE 0x100u    /* force the cache-line search tree even on a dense key
                                         range (default there: direct addressing, key - k0) */
 
@@ -285,6 +292,19 @@ typedef struct {
  * (GPUTx/GaccO, a3), execute with compaction of aborts into a retry queue until every
  * transaction commits (a4-a6), then emit results (a7).  Asynchronous on the db stream. */
 cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res);
+
+/* Pipelined preprocessing (GaccO's preprocessing
+ * can be pipelined with execution).  Runs a3 of `scheme` -- GPUTx K-set ranks or GaccO
+ * queue positions -- for batch b on the db's second (preprocessing) stream into buffers
+ * owned by b, waiting only for b's own generation / import, so it overlaps whatever the
+ * main stream is executing (e.g. the previous batch).  The next cc_submit of b with the
+ * same scheme consumes it and skips a3 (results identical to an inline a3); one
+ * cc_prepare feeds one submit.  flags: the CC_FLAG_INDEX_* bits.  Other schemes: no-op.
+ * Partitioned submits ignore it (their access sets depend on the per-submit phase split)
+ * and prepare inline.  Errors raised during the preparation (e.g. KEY_NOT_FOUND) surface
+ * at the consuming submit's cc_sync.  Asynchronous.  INVALID_ARG for an unknown batch,
+ * STATE while a partitioned submit is pending. */
+cc_status cc_prepare(cc_db db, cc_batch b, cc_scheme scheme, uint32_t flags);
 /* ------------------------------------------- partitioned TPC-C (a8)
  * Rank r of `world` (cc_db_desc) holds warehouses [r*W/world, (r+1)*W/world).  After a
  * cc_submit with CC_FLAG_PARTITIONED:

@@ -252,6 +252,12 @@ class DB:
         self._chk(G.lib().cc_submit(self.h, batch.h, ctypes.byref(d), ctypes.byref(r)))
         return result
 
+    def prepare(self, batch: Batch, scheme, flags: int = 0):
+        """f-4: run a3 of GPUTx / GaccO for `batch` on the preprocessing stream (overlaps the
+        main stream); the next submit of `batch` with `scheme` consumes it."""
+        sid = G.SCHEME_ID[scheme] if isinstance(scheme, str) else int(scheme)
+        self._chk(G.lib().cc_prepare(self.h, batch.h, sid, flags))
+
     # ----------------------------------------------------------- partitioned TPC-C (a8)
     def part_send(self):
         """(device uint8 tensor of the phase-B requests grouped by destination, counts list)."""

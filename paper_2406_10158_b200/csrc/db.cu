@@ -91,6 +91,17 @@ struct cc_batch_s {
     uint32_t *keys;   // YCSB
     uint8_t *ops;     // YCSB
     uint32_t *tx;     // TPC-C descriptors
+    cudaEvent_t ready = nullptr;   // recorded on the db stream after generation / import
+    // f-4: a3 results prepared ahead on the prep stream, slot 0 = GPUTx, 1 = GaccO
+    struct Prepared {
+        PrepBufs b{};
+        std::vector<void *> allocs;
+        Ctl *ctl = nullptr;            // errors raised during the prepare (merged at submit)
+        cudaEvent_t done = nullptr;    // prep finished (prep stream)
+        cudaEvent_t consumed = nullptr;   // the consuming submit's finalize finished (db stream)
+        bool has_consumer = false;
+        bool valid = false;
+    } prep[2];
 };
 
 struct TpccState {
@@ -110,6 +121,7 @@ struct cc_db_s {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t prep_stream = nullptr;   // f-4: a3 of the next batch (cc_prepare)
     int rank = 0, world = 1;
     int num_sms = 148;
     std::string err;
@@ -170,6 +182,10 @@ struct cc_db_s {
     uint64_t n_timed = 0;
     cc_stats last{};
     std::vector<cc_batch_s *> batches;
+    // freed batches kept with their device buffers for reuse by a batch of the same shape:
+    // no cudaMalloc / cudaFree (a device-wide sync) between steps.  Reuse is ordered after
+    // the old batch's work by the db stream (and, if it was prepared, by prep_idle).
+    std::vector<cc_batch_s *> pool;
 };
 
 static cc_status fail(cc_db db, cc_status st, const char *fmt, ...) {
@@ -234,6 +250,10 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
         }
         db->own_stream = true;
     }
+    if (cudaStreamCreateWithFlags(&db->prep_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete db;
+        return CC_ERR_CUDA;
+    }
     if (dalloc(&db->ctl, sizeof(Ctl)) || dalloc(&db->stats_scratch, 8 * CC_STATS_WORDS) ||
         dalloc(&db->sticky_dev, 8)) {
         delete db;
@@ -255,6 +275,20 @@ static void free_scratch(cc_db db) {
     db->cap_acc = 0;
 }
 
+static void free_batch_mem(cc_batch b) {
+    cudaFree(b->keys);
+    cudaFree(b->ops);
+    cudaFree(b->tx);
+    if (b->ready) cudaEventDestroy(b->ready);
+    for (auto &q : b->prep) {
+        for (void *a : q.allocs) cudaFree(a);
+        cudaFree(q.ctl);
+        if (q.done) cudaEventDestroy(q.done);
+        if (q.consumed) cudaEventDestroy(q.consumed);
+    }
+    delete b;
+}
+
 cc_status cc_db_destroy(cc_db db) {
     if (!db) return CC_ERR_INVALID_ARG;
     cudaSetDevice(db->device);
@@ -266,7 +300,9 @@ cc_status cc_db_destroy(cc_db db) {
         for (u64 *l : i.levels) cudaFree(l);
     }
     for (void *p : db->snap) cudaFree(p);
-    for (auto *b : db->batches) { cudaFree(b->keys); cudaFree(b->ops); cudaFree(b->tx); delete b; }
+    cudaStreamSynchronize(db->prep_stream);
+    for (auto *b : db->batches) free_batch_mem(b);
+    for (auto *b : db->pool) free_batch_mem(b);
     cudaFree(db->tpcc.nidx_start); cudaFree(db->tpcc.nidx_count); cudaFree(db->tpcc.nidx_rows);
     for (auto &pe : db->pending) for (auto &e : pe.ev) cudaEventDestroy(e);
     for (auto &pe : db->free_events) for (auto &e : pe.ev) cudaEventDestroy(e);
@@ -284,6 +320,7 @@ cc_status cc_db_destroy(cc_db db) {
     cudaFree(db->stats_scratch);
     cudaFree(db->sticky_dev);
     if (db->own_stream) cudaStreamDestroy(db->stream);
+    cudaStreamDestroy(db->prep_stream);
     delete db;
     return CC_OK;
 }
@@ -443,7 +480,26 @@ cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *d) {
     return CC_OK;
 }
 
+static cudaError_t batch_ready(cc_db db, cc_batch b) {
+    if (!b->ready) {
+        cudaError_t e = cudaEventCreateWithFlags(&b->ready, cudaEventDisableTiming);
+        if (e) return e;
+    }
+    return cudaEventRecord(b->ready, db->stream);
+}
+
+constexpr size_t BATCH_POOL_MAX = 16;
+
 static cc_status new_batch(cc_db db, uint32_t n_txn, uint32_t K, cc_batch *out, uint32_t kind = KIND_YCSB) {
+    for (size_t i = 0; i < db->pool.size(); i++) {
+        cc_batch b = db->pool[i];
+        if (b->kind != kind || b->n_txn != n_txn || b->K != K) continue;
+        db->pool.erase(db->pool.begin() + i);
+        for (auto &q : b->prep) q.valid = false;
+        db->batches.push_back(b);
+        *out = b;
+        return CC_OK;
+    }
     cc_batch b = new cc_batch_s();
     b->kind = kind;
     b->n_txn = n_txn;
@@ -491,6 +547,7 @@ cc_status cc_batch_gen_ycsb(cc_db db, const cc_ycsb_gen_desc *g, cc_batch *out) 
         CUDA_TRY(db, cudaStreamSynchronize(db->stream));
         cudaFree(tmp);
     }
+    CUDA_TRY(db, batch_ready(db, b));
     *out = b;
     return CC_OK;
 }
@@ -508,6 +565,7 @@ cc_status cc_batch_import_ycsb(cc_db db, const uint32_t *keys, const uint8_t *op
     CUDA_TRY(db, cudaMemcpyAsync(b->keys, keys, (size_t)n_txn * K * 4, kind, db->stream));
     CUDA_TRY(db, cudaMemcpyAsync(b->ops, ops, (size_t)n_txn * K, kind, db->stream));
     if (!src_on_device) CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, batch_ready(db, b));
     *out = b;
     return CC_OK;
 }
@@ -533,11 +591,16 @@ cc_status cc_batch_free(cc_db db, cc_batch b) {
     if (!db || !b) return CC_ERR_INVALID_ARG;
     for (size_t i = 0; i < db->batches.size(); i++)
         if (db->batches[i] == b) {
-            cudaStreamSynchronize(db->stream);
-            cudaFree(b->keys);
-            cudaFree(b->ops);
-            cudaFree(b->tx);
-            delete b;
+            bool prepared = false;
+            for (auto &q : b->prep) prepared |= !q.allocs.empty();
+            // a prepare may still read the batch: the next writer (db stream) must wait for it
+            if (prepared) cudaStreamSynchronize(db->prep_stream);
+            if (db->pool.size() < BATCH_POOL_MAX) {
+                db->pool.push_back(b);
+            } else {
+                cudaStreamSynchronize(db->stream);
+                free_batch_mem(b);
+            }
             db->batches.erase(db->batches.begin() + i);
             return CC_OK;
         }
@@ -628,6 +691,7 @@ cc_status cc_batch_gen_tpcc(cc_db db, const cc_tpcc_gen_desc *g, cc_batch *out) 
     CUDA_TRY(db, cudaMemsetAsync(db->ctl, 0, sizeof(Ctl), db->stream));
     CUDA_TRY(db, launch_tpcc_gen(b->tx, g->n_txn, g->seed, T.W, g->w_lo, g->w_hi, g->neworder_permyriad,
                                  T.c_run, T.c_id, T.c_item, db->ctl, db->stream));
+    CUDA_TRY(db, batch_ready(db, b));
     *out = b;
     return CC_OK;
 }
@@ -659,6 +723,7 @@ cc_status cc_batch_import_tpcc(cc_db db, const uint32_t *tx, uint32_t n_txn, int
     CUDA_TRY(db, cudaMemcpyAsync(b->tx, tx, (size_t)n_txn * TPCC_TX_WORDS * 4,
                                  src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, db->stream));
     if (!src_on_device) CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, batch_ready(db, b));
     *out = b;
     return CC_OK;
 }
@@ -672,6 +737,8 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx) {
 }
 
 // ---------------------------------------------------------------- execution
+static cudaError_t alloc_prep(PrepBufs &b, std::vector<void *> &allocs, uint64_t na, uint32_t nt);
+
 static cc_status ensure_scratch(cc_db db, uint32_t n_txn, uint64_t n_acc) {
     if (n_txn <= db->cap_txn && n_acc <= db->cap_acc) return CC_OK;
     cudaStreamSynchronize(db->stream);
@@ -685,35 +752,42 @@ static cc_status ensure_scratch(cc_db db, uint32_t n_txn, uint64_t n_acc) {
     const uint32_t cap = nt;   // each id is appended to the retry batch at most once
     CUDA_TRY(db, dalloc(&db->ring, (size_t)cap * 8));
     db->ring_cap = cap;
-    PrepBufs &b = db->prep;
-    auto A = [&](auto **p, size_t bytes) -> cudaError_t {
-        cudaError_t e = dalloc(p, bytes);
-        if (e == cudaSuccess) db->prep_allocs.push_back((void *)*p);
-        return e;
-    };
-    CUDA_TRY(db, A(&b.keys_in, na * 8));
-    CUDA_TRY(db, A(&b.keys_out, na * 8));
-    CUDA_TRY(db, A(&b.acc_rec, na * 4));
-    CUDA_TRY(db, A(&b.acc_seg, na * 4));
-    CUDA_TRY(db, A(&b.acc_pos, na * 4));
-    CUDA_TRY(db, A(&b.sorted_pos, na * 4));
-    CUDA_TRY(db, A(&b.head_flag, na * 4));
-    CUDA_TRY(db, A(&b.seg_id, na * 4));
-    CUDA_TRY(db, A(&b.seg_start, na * 4));
-    CUDA_TRY(db, A(&b.lw, na * 4));
-    CUDA_TRY(db, A(&b.cursor, na * 4));
-    CUDA_TRY(db, A(&b.rank, (size_t)nt * 4));
-    CUDA_TRY(db, A(&b.rank_sorted, (size_t)nt * 4));
-    CUDA_TRY(db, A(&b.gid_in, (size_t)nt * 4));
-    CUDA_TRY(db, A(&b.rank_order, (size_t)nt * 4));
-    CUDA_TRY(db, A(&b.rank_count, (size_t)nt * 4));
-    CUDA_TRY(db, A(&b.rank_done, (size_t)nt * 4));
-    CUDA_TRY(db, A(&b.rank_start, (size_t)nt * 4));
-    b.cub_bytes = prep_cub_bytes(na, nt);
-    CUDA_TRY(db, A((char **)&b.cub_tmp, b.cub_bytes));
+    CUDA_TRY(db, alloc_prep(db->prep, db->prep_allocs, na, nt));
     db->cap_txn = nt;
     db->cap_acc = na;
     return CC_OK;
+}
+
+// a3 buffers for n_acc accesses / n_txn transactions (allocations recorded in `allocs`)
+static cudaError_t alloc_prep(PrepBufs &b, std::vector<void *> &allocs, uint64_t na, uint32_t nt) {
+    auto A = [&](auto **p, size_t bytes) -> cudaError_t {
+        cudaError_t e = dalloc(p, bytes);
+        if (e == cudaSuccess) allocs.push_back((void *)*p);
+        return e;
+    };
+#define PTRY(x) do { cudaError_t e_ = (x); if (e_) return e_; } while (0)
+    PTRY(A(&b.keys_in, na * 8));
+    PTRY(A(&b.keys_out, na * 8));
+    PTRY(A(&b.acc_rec, na * 4));
+    PTRY(A(&b.acc_seg, na * 4));
+    PTRY(A(&b.acc_pos, na * 4));
+    PTRY(A(&b.sorted_pos, na * 4));
+    PTRY(A(&b.head_flag, na * 4));
+    PTRY(A(&b.seg_id, na * 4));
+    PTRY(A(&b.seg_start, na * 4));
+    PTRY(A(&b.lw, na * 4));
+    PTRY(A(&b.cursor, na * 4));
+    PTRY(A(&b.rank, (size_t)nt * 4));
+    PTRY(A(&b.rank_sorted, (size_t)nt * 4));
+    PTRY(A(&b.gid_in, (size_t)nt * 4));
+    PTRY(A(&b.rank_order, (size_t)nt * 4));
+    PTRY(A(&b.rank_count, (size_t)nt * 4));
+    PTRY(A(&b.rank_done, (size_t)nt * 4));
+    PTRY(A(&b.rank_start, (size_t)nt * 4));
+    b.cub_bytes = prep_cub_bytes(na, nt);
+    PTRY(A((char **)&b.cub_tmp, b.cub_bytes));
+#undef PTRY
+    return cudaSuccess;
 }
 
 static cc_status ensure_arena(cc_db db, uint64_t nodes, uint32_t row_words) {
@@ -753,6 +827,48 @@ static cc_status ensure_part(cc_db db, uint32_t n_txn) {
     CUDA_TRY(db, dalloc(&P.send, (size_t)n_txn * TPCC_K * sizeof(PartReq)));
     CUDA_TRY(db, dalloc(&P.stage, (size_t)n_txn * TPCC_K * sizeof(PartResp)));
     P.cap_txn = n_txn;
+    return CC_OK;
+}
+
+// kernel-side workload parameters of batch b (YCSB or TPC-C)
+static cc_status wl_params(cc_db db, cc_batch b, uint32_t flags, YcsbParams &y, TpccParams &tp) {
+    if (b->kind == KIND_TPCC) {
+        const TpccState &T = db->tpcc;
+        tp.tx = b->tx;
+        tp.wh = (u64 *)db->tables[T.ids[0]].d;
+        tp.di = (u64 *)db->tables[T.ids[1]].d;
+        tp.cu = (u64 *)db->tables[T.ids[2]].d;
+        tp.st = (u64 *)db->tables[T.ids[3]].d;
+        tp.it = (const u64 *)db->tables[T.ids[4]].d;
+        tp.o = (u64 *)db->tables[T.ids[5]].d;
+        tp.no = (u64 *)db->tables[T.ids[6]].d;
+        tp.ol = (u64 *)db->tables[T.ids[7]].d;
+        tp.h = (u64 *)db->tables[T.ids[8]].d;
+        tp.bW = db->tables[T.ids[0]].base;
+        tp.bD = db->tables[T.ids[1]].base;
+        tp.bC = db->tables[T.ids[2]].base;
+        tp.bS = db->tables[T.ids[3]].base;
+        tp.W = T.W;
+        tp.w_first = T.w_first;
+        tp.nidx_start = T.nidx_start;
+        tp.nidx_count = T.nidx_count;
+        tp.nidx_rows = T.nidx_rows;
+        tp.entry_date = 20240601;   // per-submit constant date (no wall clock)
+    } else {
+        if (db->ycsb_table < 0) return fail(db, CC_ERR_CONFIG, "no YCSB table loaded");
+        const Table &t = db->tables[db->ycsb_table];
+        const Index &ix = db->indexes[db->ycsb_index];
+        y.keys = b->keys;
+        y.ops = b->ops;
+        y.idx_keys = ix.keys;
+        y.idx_rows = ix.rowids;
+        y.idx_n = ix.n;
+        y.tree = tree_of(ix);
+        y.mode = index_mode(ix, flags);
+        y.idx_k0 = ix.k0;
+        y.rows = (u64 *)t.d;
+        y.n_rows = t.rows;
+    }
     return CC_OK;
 }
 
@@ -802,43 +918,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.read_out = (u64 *)res->read_out;
     YcsbParams y{};
     TpccParams tp{};
-    if (is_tpcc) {
-        const TpccState &T = db->tpcc;
-        tp.tx = b->tx;
-        tp.wh = (u64 *)db->tables[T.ids[0]].d;
-        tp.di = (u64 *)db->tables[T.ids[1]].d;
-        tp.cu = (u64 *)db->tables[T.ids[2]].d;
-        tp.st = (u64 *)db->tables[T.ids[3]].d;
-        tp.it = (const u64 *)db->tables[T.ids[4]].d;
-        tp.o = (u64 *)db->tables[T.ids[5]].d;
-        tp.no = (u64 *)db->tables[T.ids[6]].d;
-        tp.ol = (u64 *)db->tables[T.ids[7]].d;
-        tp.h = (u64 *)db->tables[T.ids[8]].d;
-        tp.bW = db->tables[T.ids[0]].base;
-        tp.bD = db->tables[T.ids[1]].base;
-        tp.bC = db->tables[T.ids[2]].base;
-        tp.bS = db->tables[T.ids[3]].base;
-        tp.W = T.W;
-        tp.w_first = T.w_first;
-        tp.nidx_start = T.nidx_start;
-        tp.nidx_count = T.nidx_count;
-        tp.nidx_rows = T.nidx_rows;
-        tp.entry_date = 20240601;   // per-submit constant date (no wall clock)
-    } else {
-        if (db->ycsb_table < 0) return fail(db, CC_ERR_CONFIG, "no YCSB table loaded");
-        const Table &t = db->tables[db->ycsb_table];
-        const Index &ix = db->indexes[db->ycsb_index];
-        y.keys = b->keys;
-        y.ops = b->ops;
-        y.idx_keys = ix.keys;
-        y.idx_rows = ix.rowids;
-        y.idx_n = ix.n;
-        y.tree = tree_of(ix);
-        y.mode = index_mode(ix, desc->flags);
-        y.idx_k0 = ix.k0;
-        y.rows = (u64 *)t.d;
-        y.n_rows = t.rows;
-    }
+    st = wl_params(db, b, desc->flags, y, tp);
+    if (st) return st;
 
     if (desc->flags & CC_FLAG_LATCHED) {   // one 32-bit latch per control word (Exp-7)
         if (db->latch_records < db->n_records) {
@@ -896,19 +977,30 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[1], db->stream));
     // a3: preprocessing for the conflict-graph schemes
+    cc_batch_s::Prepared *used = nullptr;   // f-4: a3 done ahead by cc_prepare
     if (det) {
-        if (is_tpcc) CUDA_TRY(db, launch_tpcc_gather(p, tp, db->prep, db->n_records, db->stream));
-        else CUDA_TRY(db, launch_ycsb_gather(p, y, db->prep, db->stream));
-        CUDA_TRY(db, launch_prep_common(p, db->prep, db->n_records, scheme == CC_GPUTX,
-                                        rank_kernel_grid(), db->stream));
-        p.acc_rec = db->prep.acc_rec;
-        p.acc_seg = db->prep.acc_seg;
-        p.acc_pos = db->prep.acc_pos;
-        p.cursor = db->prep.cursor;
-        p.rank_order = db->prep.rank_order;
-        p.rank_of = db->prep.rank;
-        p.rank_done = db->prep.rank_done;
-        p.rank_count = db->prep.rank_count;
+        PrepBufs *pb = &db->prep;
+        auto &q = b->prep[scheme == CC_GPUTX ? 0 : 1];
+        if (!partitioned && q.valid) {
+            CUDA_TRY(db, cudaStreamWaitEvent(db->stream, q.done, 0));
+            CUDA_TRY(db, launch_merge_err(q.ctl, db->ctl, db->stream));
+            pb = &q.b;
+            q.valid = false;
+            used = &q;
+        } else {
+            if (is_tpcc) CUDA_TRY(db, launch_tpcc_gather(p, tp, db->prep, db->n_records, db->stream));
+            else CUDA_TRY(db, launch_ycsb_gather(p, y, db->prep, db->stream));
+            CUDA_TRY(db, launch_prep_common(p, db->prep, db->n_records, scheme == CC_GPUTX,
+                                            rank_kernel_grid(), db->stream));
+        }
+        p.acc_rec = pb->acc_rec;
+        p.acc_seg = pb->acc_seg;
+        p.acc_pos = pb->acc_pos;
+        p.cursor = pb->cursor;
+        p.rank_order = pb->rank_order;
+        p.rank_of = pb->rank;
+        p.rank_done = pb->rank_done;
+        p.rank_count = pb->rank_count;
     }
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[2], db->stream));
     // a4-a6: persistent executor
@@ -939,6 +1031,10 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     cc_result r = *res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
     CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream));
+    if (used) {   // a later cc_prepare of this batch may overwrite the buffers after this point
+        CUDA_TRY(db, cudaEventRecord(used->consumed, db->stream));
+        used->has_consumer = true;
+    }
     if ((void *)r.stats != (void *)db->stats_scratch)
         CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS,
                                      cudaMemcpyDeviceToDevice, db->stream));
@@ -949,6 +1045,46 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     return CC_OK;
 }
 
+
+cc_status cc_prepare(cc_db db, cc_batch b, cc_scheme scheme, uint32_t flags) {
+    CHECK_DB(db);
+    if (!b) return fail(db, CC_ERR_INVALID_ARG, "cc_prepare: null batch");
+    if ((unsigned)scheme >= CC_NUM_SCHEMES) return fail(db, CC_ERR_INVALID_ARG, "bad scheme");
+    if (scheme != CC_GPUTX && scheme != CC_GACCO) return CC_OK;   // nothing to prepare
+    bool known = false;
+    for (auto *x : db->batches) known |= x == b;
+    if (!known || !b->ready) return fail(db, CC_ERR_INVALID_ARG, "cc_prepare: unknown batch");
+    if (db->part.pending) return fail(db, CC_ERR_STATE, "partitioned submit pending");
+    auto &q = b->prep[scheme == CC_GPUTX ? 0 : 1];
+    const uint64_t n_acc = (uint64_t)b->n_txn * b->K;
+    if (q.allocs.empty()) {
+        CUDA_TRY(db, alloc_prep(q.b, q.allocs, n_acc < b->n_txn ? b->n_txn : n_acc, b->n_txn));
+        CUDA_TRY(db, dalloc(&q.ctl, sizeof(Ctl)));
+        CUDA_TRY(db, cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming));
+        CUDA_TRY(db, cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
+    }
+    YcsbParams y{};
+    TpccParams tp{};
+    cc_status st = wl_params(db, b, flags, y, tp);
+    if (st) return st;
+    ExecParams p{};
+    p.scheme = (int)scheme;
+    p.n_txn = b->n_txn;
+    p.K = b->K;
+    p.flags = flags;
+    p.ctl = q.ctl;
+    p.watchdog_ns = 30000000000ull;
+    cudaStream_t ps = db->prep_stream;
+    CUDA_TRY(db, cudaStreamWaitEvent(ps, b->ready, 0));   // only the batch's own generation
+    if (q.has_consumer) CUDA_TRY(db, cudaStreamWaitEvent(ps, q.consumed, 0));
+    CUDA_TRY(db, cudaMemsetAsync(q.ctl, 0, sizeof(Ctl), ps));
+    if (b->kind == KIND_TPCC) CUDA_TRY(db, launch_tpcc_gather(p, tp, q.b, db->n_records, ps));
+    else CUDA_TRY(db, launch_ycsb_gather(p, y, q.b, ps));
+    CUDA_TRY(db, launch_prep_common(p, q.b, db->n_records, scheme == CC_GPUTX, rank_kernel_grid(), ps));
+    CUDA_TRY(db, cudaEventRecord(q.done, ps));
+    q.valid = true;
+    return CC_OK;
+}
 
 cc_status cc_part_send(cc_db db, const void **send, uint64_t *counts) {
     CHECK_DB(db);

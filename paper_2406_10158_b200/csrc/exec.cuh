@@ -79,30 +79,38 @@ struct StageClock {
 
 // debug event log (CC_FLAG_EVENTS): each event takes a global sequence
 // number right after the access it describes
-GC_DEV void log_event(const Th &th, u32 rec, u32 kind) {
+GC_DEV u64 log_event(const Th &th, u32 rec, u32 kind) {
     const ExecParams &p = *th.p;
-    if (!p.events) return;
+    if (!p.events) return ~0ull;
     const u64 k = atomicAdd(&p.ctl->events.v, 1ull);
-    if (k >= p.events_cap) return;   // overflow: the count tells the host
+    if (k >= p.events_cap) return ~0ull;   // overflow: the count tells the host
     Event &ev = p.events[k];
     ev.seq = k;
     ev.gid = th.gid;
     ev.rec = rec;
     ev.attempt = th.attempt;
     ev.kind = kind;
+    return k;
+}
+
+// A read whose re-check failed (seqlock / RTS CAS lost) is repeated in the same attempt:
+// its logged event did not happen logically, so it becomes kind 4 (retracted).
+GC_DEV void retract_read(const Th &th, u64 k) {
+    if (k != ~0ull) th.p->events[k].kind = 4u;
 }
 
 // row work (the "useful" stage) done through these wrappers
 template <class WL>
-GC_DEV void rd(Th &th, const typename WL::Params &y, typename WL::Lane &L, u32 gid, u32 i, const u64 *src) {
+GC_DEV u64 rd(Th &th, const typename WL::Params &y, typename WL::Lane &L, u32 gid, u32 i, const u64 *src) {
     {
         StageClock c(th, STAGE_USEFUL);
         WL::read(y, L, gid, i, src);
     }
     if (th.p->events) {
         fence_acqrel();
-        log_event(th, L.rec, 0);
+        return log_event(th, L.rec, 0);   // before the caller's re-check of the word
     }
+    return ~0ull;
 }
 template <class WL>
 GC_DEV void inst(Th &th, const typename WL::Params &y, const typename WL::Lane &L, u64 *dst) {
@@ -232,6 +240,10 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
     }
 }
 
+// Tile mode (2PL locks, OCC write-set locks): restarts after which a transaction takes its
+// locks one lane at a time in access order instead of all at once (run_tile)
+constexpr u32 TPL_ORDERED_AFTER = 4;
+
 // Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
 // no-wait / OCC semantics are unchanged -- until that lock is free (2PL holder count 0,
 // OCC lock bit clear), bounded, add a little jitter, and retry; otherwise use the
@@ -249,7 +261,7 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         }
         // then a random delay whose window doubles per restart: waiters released by
         // the same unlock must not retry in lockstep (a herd livelock at theta >= 0.9)
-        const u32 win = 32u << (restarts < 11 ? restarts : 11);
+        const u32 win = (th.p->flags & CC_FLAG_FLAT_JITTER) ? 256u : 32u << (restarts < 11 ? restarts : 11);
         u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % win);
         while (d > 0) {
             const u32 s = d < 1000u ? d : 1000u;
@@ -421,10 +433,12 @@ GC_DEV int to_step(Th &th, const ExecParams &p, const typename WL::Params &y, ty
     }
     if (ts < to_wts(v)) return ST_ABORT;
     if (v & TO_P) return ST_WAIT;
-    rd<WL>(th, y, L, gid, i, row);
+    const u64 ev = rd<WL>(th, y, L, gid, i, row);
     fence_acqrel();
-    if (to_rts(v) >= ts) return ld_relaxed(w) == v ? ST_DONE : ST_RETRY;
-    return w_cas(p, w, v, to_make(false, ts, to_wts(v))) == v ? ST_DONE : ST_RETRY;
+    const bool ok = (to_rts(v) >= ts) ? ld_relaxed(w) == v : w_cas(p, w, v, to_make(false, ts, to_wts(v))) == v;
+    if (ok) return ST_DONE;
+    retract_read(th, ev);
+    return ST_RETRY;
 }
 
 template <class WL>
@@ -454,12 +468,16 @@ GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, 
     if ((v & TO_P) && to_wts(v) < ts) return ST_WAIT;   // older pending writer: its version is ours
     const u64 h = ld_acquire(hi);
     if ((h >> 32) <= ts) {   // head visible: read in place, validate, raise RTS
-        rd<WL>(th, y, L, gid, i, row);
+        const u64 ev = rd<WL>(th, y, L, gid, i, row);
         fence_acqrel();
-        if (ld_relaxed(hi) != h) return ST_RETRY;
-        if (to_rts(v) >= ts) return ld_relaxed(lo) == v ? ST_DONE : ST_RETRY;
-        const u64 nv = (v & ~(M31 << 31)) | ((ts & M31) << 31);
-        return w_cas(p, lo, v, nv) == v ? ST_DONE : ST_RETRY;
+        bool ok = ld_relaxed(hi) == h;
+        if (ok) {
+            if (to_rts(v) >= ts) ok = ld_relaxed(lo) == v;
+            else ok = w_cas(p, lo, v, (v & ~(M31 << 31)) | ((ts & M31) << 31)) == v;
+        }
+        if (ok) return ST_DONE;
+        retract_read(th, ev);
+        return ST_RETRY;
     }
     // walk the history chain for the newest version with begin <= ts
     u64 idx = h & VNONE;
@@ -512,9 +530,12 @@ GC_DEV int occ_snap_step(Th &th, const ExecParams &p, const typename WL::Params 
     u64 *w = &p.meta[L.rec];
     const u64 v1 = ld_acquire(w);
     if (v1 & LOCKB) return ST_WAIT;
-    rd<WL>(th, y, L, gid, i, WL::row(y, L));
+    const u64 ev = rd<WL>(th, y, L, gid, i, WL::row(y, L));
     fence_acqrel();
-    if (ld_relaxed(w) != v1) return ST_RETRY;
+    if (ld_relaxed(w) != v1) {
+        retract_read(th, ev);
+        return ST_RETRY;
+    }
     obs = v1;
     return ST_DONE;
 }
@@ -730,6 +751,7 @@ template <int S, class WL>
 __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, typename WL::Params y) {
     const u32 lane = threadIdx.x & 31u;
     if (lane >= (1u << p.wd)) return;   // idle lanes exit at once
+    if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
     Th th;
     th.p = &p;
@@ -802,11 +824,23 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         constexpr bool WD = S == CC_TPL_WD;
         const u32 age = gid + 1;
         bool held = false;
+        // Parallel acquisition (every lane CASes its lock at once) is the fast path.  Under
+        // extreme contention every dying attempt still holds some locks for a moment, and
+        // those transient holds can keep a hot lock busy forever (TPC-C at 1 warehouse: W
+        // is never free when a Payment's lanes look).  After TPL_ORDERED_AFTER restarts the
+        // tile acquires in access (= key) order, one lane at a time, so an attempt that
+        // meets a held lock dies holding only locks that precede it (thread-mode behaviour).
+        const bool ordered = th.attempt >= TPL_ORDERED_AFTER;
         Spin sp;
         for (;;) {
             int st = ST_DONE;
             u64 seen = 0;
-            if (act && !held) {
+            bool mine = act && !held;
+            if (ordered) {
+                const unsigned want = tile.ballot(mine);
+                mine = mine && li == (u32)(__ffs(want) - 1);
+            }
+            if (mine) {
                 st = tpl_try<WD>(p, &p.meta[L.rec], L.w, age, seen);
                 held = st == ST_DONE;
             }
@@ -819,6 +853,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 return RES_ABORT;
             }
             if (tile.all(!act || held)) break;
+            if (!tile.any(st == ST_WAIT)) continue;   // ordered: the next lane's turn
             if (tile.any(!sp.wait(th))) {
                 if (held) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
                 return RES_FATAL;
@@ -891,9 +926,19 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         }
         bool locked = false, bad = false;
         u64 seen = 0;
-        if (act && L.w) {
-            locked = occ_lock(p, &p.meta[L.rec], pre, seen);
-            bad = !locked;
+        if (th.attempt < TPL_ORDERED_AFTER) {   // write set locked by all lanes at once
+            if (act && L.w) {
+                locked = occ_lock(p, &p.meta[L.rec], pre, seen);
+                bad = !locked;
+            }
+        } else {   // after repeated aborts: in access order, stop at the first busy lock (see 2PL)
+            for (unsigned todo = tile.ballot(act && L.w); todo; todo &= todo - 1) {
+                if (li == (u32)(__ffs(todo) - 1)) {
+                    locked = occ_lock(p, &p.meta[L.rec], pre, seen);
+                    bad = !locked;
+                }
+                if (tile.any(bad)) break;
+            }
         }
         {
             const unsigned busy = tile.ballot(bad && (seen & LOCKB));
@@ -985,6 +1030,7 @@ template <int S, class WL, int G>
 __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typename WL::Params y) {
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const u32 li = tile.thread_rank();
+    if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
     Th th;
     th.p = &p;

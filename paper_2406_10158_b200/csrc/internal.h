@@ -131,6 +131,7 @@ cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBuf
                                cudaStream_t s);
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,
                                bool gputx, int grid, cudaStream_t s);
+cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);

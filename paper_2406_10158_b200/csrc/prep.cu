@@ -358,4 +358,15 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
     return cudaGetLastError();
 }
 
+// f-4: fold an error raised while a batch was prepared ahead into the submit's control block
+__global__ void merge_err_kernel(const Ctl *src, Ctl *dst) {
+    const u64 e = src->err.v;
+    if (e) atomicCAS(&dst->err.v, 0ull, e);
+}
+
+cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s) {
+    merge_err_kernel<<<1, 1, 0, s>>>(src, dst);
+    return cudaGetLastError();
+}
+
 }  // namespace gcctb

@@ -664,9 +664,11 @@ __global__ void tpcc_gather_kernel(ExecParams p, TpccParams y, uint32_t *acc_rec
     for (u32 i = 0; i < (u32)p.K; i++) {
         if (i < n) {
             TpccWL::Lane L;
-            if (!TpccWL::load_lane(q, y, gid, i, L)) {
+            if (!TpccWL::load_lane(q, y, gid, i, L)) {   // reported; sentinel keeps a3 / exec in bounds
                 atomicCAS(&p.ctl->err.v, 0ull, (u64)CC_ERR_KEY_NOT_FOUND);
-                return;
+                acc_rec[base + i] = 0xFFFFFFFFu;
+                keys[base + i] = (sentinel << 27) | ((u64)gid << 6) | ((u64)i << 1);
+                continue;
             }
             acc_rec[base + i] = L.rec;
             keys[base + i] = ((u64)L.rec << 27) | ((u64)gid << 6) | ((u64)i << 1) | (u64)L.w;

@@ -300,10 +300,10 @@ __global__ void ycsb_gather_kernel(ExecParams p, YcsbParams y, uint32_t *acc_rec
     const u64 a = (u64)blockIdx.x * blockDim.x + threadIdx.x;   // one thread per access
     if (a >= (u64)p.n_txn * p.K) return;
     const u32 gid = (u32)(a / p.K), i = (u32)(a % p.K);
-    const u64 r = YcsbWL::lookup(y, y.keys[a]);
-    if (r == ~0ull) {
+    u64 r = YcsbWL::lookup(y, y.keys[a]);
+    if (r == ~0ull) {   // reported; record 0 keeps every later a3 / exec access in bounds
         atomicCAS(&p.ctl->err.v, 0ull, (u64)CC_ERR_KEY_NOT_FOUND);
-        return;
+        r = 0;
     }
     acc_rec[a] = (uint32_t)r;
     keys_out[a] = (r << 27) | ((u64)gid << 6) | ((u64)i << 1) | (u64)(y.ops[a] >> 7);

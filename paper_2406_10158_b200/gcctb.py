@@ -29,6 +29,7 @@ CC_FLAG_LATCHED = 0x20
 CC_FLAG_STAGES = 0x40
 CC_FLAG_EVENTS = 0x80
 CC_FLAG_INDEX_TREE = 0x100
+CC_FLAG_FLAT_JITTER = 0x200
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16
@@ -111,6 +112,7 @@ _SIGS = {
                                      ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "cc_batch_free": (ctypes.c_int, [_P, _P]),
     "cc_submit": (ctypes.c_int, [_P, _P, ctypes.POINTER(cc_exec_desc), ctypes.POINTER(cc_result)]),
+    "cc_prepare": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_uint32]),
     "cc_sync": (ctypes.c_int, [_P, ctypes.POINTER(cc_stats)]),
     "cc_timing_read": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double * 5),
                                       ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]),

@@ -134,13 +134,21 @@ def test_brute_force_tiny(c1, orc, scheme):
         b.free()
 
 
-def test_key_not_found(c1):
+@pytest.mark.parametrize("scheme,lanes", [("silo", 1), ("silo", 4), ("gacco", 1), ("gacco", 4), ("gputx", 4)])
+def test_key_not_found(c1, scheme, lanes):
+    """KeyNotFound is reported, also when a3 resolves the keys (GaccO / GPUTx:
+    no out-of-range record reaches the executor), and the db stays usable."""
     from paper_2406_10158_b200.gcctb import CCError
     db, _ = c1
-    b = db.import_ycsb(np.array([1, 5000], np.uint32), np.array([0, 0], np.uint8), 2)
-    db.submit(b, "silo")
+    b = db.import_ycsb(np.array([1, 5000, 7, 9], np.uint32), np.array([0, 0, 0x80, 0], np.uint8), 2)
+    db.submit(b, scheme, lanes=lanes)
     with pytest.raises(CCError, match="KEY_NOT_FOUND"):
         db.sync()
+    b.free()
+    b = db.import_ycsb(np.array([1, 2, 7, 9], np.uint32), np.array([0, 0, 0x80, 0], np.uint8), 2)
+    db.snapshot(False)
+    db.submit(b, scheme, lanes=lanes)
+    assert db.sync().commits == 2
     b.free()
 
 

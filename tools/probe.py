@@ -1,6 +1,7 @@
 """Quick perf probe (not the bench): C2-shaped YCSB, every scheme, a few thetas."""
 import argparse
 import json
+import statistics
 import os
 import sys
 import time
@@ -12,6 +13,29 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 from paper_2406_10158_b200.api import DB  # noqa: E402
 from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING, SCHEMES  # noqa: E402
+
+
+def cell(db, b, s, a):
+    kw = dict(wd=a.wd, bs=a.bs, watchdog_s=a.watchdog, lanes=a.lanes, grid=a.grid, claim_chunk=a.chunk)
+    db.submit(b, s, flags=IDXF[a.index] | a.flags, **kw)
+    db.sync()
+    tots, execs = [], []
+    aborts = commits = 0
+    for _ in range(a.reps):
+        db.timing(reset=True)
+        db.submit(b, s, flags=CC_FLAG_TIMING | IDXF[a.index] | a.flags, **kw)
+        st = db.sync()
+        ms, n = db.timing(reset=True)
+        tots.append(ms[4])
+        execs.append(ms[2])
+        aborts += st.aborts
+        commits += st.commits
+    med = statistics.median(tots)
+    return dict(txn_s=a.batch / (med / 1e3), abort_rate=aborts / commits, ms_total_median=med,
+                ms_total_min=min(tots), ms_total_max=max(tots), ms_exec_median=statistics.median(execs))
+
+
+IDXF = {"dense": 0, "tree": 0x100, "binary": 0x10}
 
 
 def main():
@@ -30,8 +54,9 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--seeds", default="3")
     ap.add_argument("--chunk", type=int, default=1)
+    ap.add_argument("--flags", type=lambda x: int(x, 0), default=0)
+    ap.add_argument("--watchdog", type=float, default=20)
     a = ap.parse_args()
-    IDXF = {'dense': 0, 'tree': 0x100, 'binary': 0x10}
     db = DB(0)
     db.load_ycsb(a.rows, 1)
     A = inputs.scramble_mult(a.rows)
@@ -40,26 +65,16 @@ def main():
         T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).cuda()
         b = db.gen_ycsb(a.batch, a.K, a.W, seed, T, A)
         for s in a.schemes.split(","):
-            db.submit(b, s, wd=a.wd, bs=a.bs, watchdog_s=20, lanes=a.lanes, flags=IDXF[a.index], grid=a.grid, claim_chunk=a.chunk)
-            db.sync()
-            tots, execs = [], []
-            aborts = commits = 0
-            for _ in range(a.reps):
-                db.timing(reset=True)
-                db.submit(b, s, wd=a.wd, bs=a.bs, flags=CC_FLAG_TIMING | IDXF[a.index], watchdog_s=20,
-                          lanes=a.lanes, grid=a.grid, claim_chunk=a.chunk)
-                st = db.sync()
-                ms, n = db.timing(reset=True)
-                tots.append(ms[4])
-                execs.append(ms[2])
-                aborts += st.aborts
-                commits += st.commits
-            import statistics
-            med = statistics.median(tots)
-            row = dict(theta=th, seed=seed, chunk=a.chunk, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid,
-                       index=a.index, txn_s=a.batch / (med / 1e3),
-                       abort_rate=aborts / commits, ms_total_median=med, ms_total_min=min(tots),
-                       ms_total_max=max(tots), ms_exec_median=statistics.median(execs), reps=a.reps)
+            base = dict(theta=th, seed=seed, chunk=a.chunk, scheme=s, wd=a.wd, bs=a.bs, lanes=a.lanes, grid=a.grid,
+                        index=a.index, flags=a.flags, reps=a.reps)
+            try:
+                row = dict(base, **cell(db, b, s, a))
+            except Exception as e:   # watchdog etc.: recorded; the db is rebuilt
+                row = dict(base, error=str(e)[:200])
+                db.close()
+                db = DB(0)
+                db.load_ycsb(a.rows, 1)
+                b = db.gen_ycsb(a.batch, a.K, a.W, seed, T, A)
             out.append(row)
             print(json.dumps(row), flush=True)
         b.free()
