@@ -113,7 +113,9 @@ class DB:
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1):
         L = G.lib()
         if stream is None or stream.cuda_stream == 0:
-            stream = torch.cuda.Stream(device)
+            # highest priority: pending blocks of the executor are scheduled before those of
+            # the library's low-priority preprocessing stream (cc_prepare)
+            stream = torch.cuda.Stream(device, priority=-8)
         self.stream = stream
         self.device = device
         d = G.cc_db_desc(device, ctypes.c_void_p(stream.cuda_stream), rank, world)

@@ -250,7 +250,9 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
         }
         db->own_stream = true;
     }
-    if (cudaStreamCreateWithFlags(&db->prep_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    int lo_prio = 0, hi_prio = 0;   // the prep stream yields to everything else
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (cudaStreamCreateWithPriority(&db->prep_stream, cudaStreamNonBlocking, lo_prio) != cudaSuccess) {
         delete db;
         return CC_ERR_CUDA;
     }
@@ -1080,7 +1082,9 @@ cc_status cc_prepare(cc_db db, cc_batch b, cc_scheme scheme, uint32_t flags) {
     CUDA_TRY(db, cudaMemsetAsync(q.ctl, 0, sizeof(Ctl), ps));
     if (b->kind == KIND_TPCC) CUDA_TRY(db, launch_tpcc_gather(p, tp, q.b, db->n_records, ps));
     else CUDA_TRY(db, launch_ycsb_gather(p, y, q.b, ps));
-    CUDA_TRY(db, launch_prep_common(p, q.b, db->n_records, scheme == CC_GPUTX, rank_kernel_grid(), ps));
+    // a quarter of the rank kernel's resident grid: it shares the GPU with the executor
+    const int rg = rank_kernel_grid() / 4;
+    CUDA_TRY(db, launch_prep_common(p, q.b, db->n_records, scheme == CC_GPUTX, rg > 0 ? rg : 1, ps));
     CUDA_TRY(db, cudaEventRecord(q.done, ps));
     q.valid = true;
     return CC_OK;

@@ -38,6 +38,7 @@ struct Th {
     u64 *st;              // this worker's STAGE_WORDS accumulators (global memory), or null
     u64 *cw;   // lock word whose holder caused the last abort (nullptr: none)
     u64 cv;    // wait until (*cw & cv) == 0: the conflicting lock is free
+    u32 hot;   // tile mode: 1 + lane of the lock that caused this transaction's last abort
 };
 
 GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err.v, 0ull, code); }
@@ -240,10 +241,6 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
     }
 }
 
-// Tile mode (2PL locks, OCC write-set locks): restarts after which a transaction takes its
-// locks one lane at a time in access order instead of all at once (run_tile)
-constexpr u32 TPL_ORDERED_AFTER = 4;
-
 // Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
 // no-wait / OCC semantics are unchanged -- until that lock is free (2PL holder count 0,
 // OCC lock bit clear), bounded, add a little jitter, and retry; otherwise use the
@@ -292,7 +289,7 @@ GC_DEV bool try_append_retry(Th &th, u32 gid) {
     bool ok = false;
     if (ld_relaxed(&c->head.v) < p.n_txn) {
         const u64 r = atomicAdd(&c->tail.v, 1ull);
-        st_relaxed(p.ring + r, (u64)gid);
+        st_relaxed(p.ring + r, (u64)gid | ((u64)th.hot << 32));   // the hot lane travels along
         ok = true;
     }
     fence_acqrel();
@@ -321,6 +318,7 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
             cl.end = cl.next + p.claim_chunk;
         }
         const u64 s = cl.next++;
+        th.hot = 0;
         if (s < p.n_txn) return (S == CC_GPUTX) ? p.rank_order[s] : (u32)s;
         cl.exhausted = true;
     }
@@ -336,7 +334,9 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
     if (cl.tail == 0 || ld_relaxed(&c->rhead.v) >= cl.tail) return NO_TXN;
     const u64 r = atomicAdd(&c->rhead.v, 1ull);
     if (r >= cl.tail) return NO_TXN;
-    return (u32)ld_relaxed(p.ring + r);
+    const u64 e = ld_relaxed(p.ring + r);
+    th.hot = (u32)(e >> 32);
+    return (u32)e;
 }
 
 // ------------------------------------------------------------------ 2PL (Table II)
@@ -718,8 +718,9 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
             u32 *cur = &p.cursor[seg];
             Spin sp(32);   // the hand-off chain on a hot item is GaccO's critical path
-            while (ld_acquire32(cur) != pos)
+            while (ld_relaxed32(cur) != pos)   // relaxed polls: no L1 invalidation per poll
                 if (!sp.wait(th)) return RES_FATAL;
+            fence_acqrel();                    // acquire once the turn is ours
             u64 *row = WL::row(y, L[i]);
             rd<WL>(th, y, L[i], gid, i, row);
             if (L[i].w) inst<WL>(th, y, L[i], row);
@@ -732,8 +733,9 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         const u32 k = p.rank_of[gid];
         if (k > 0) {
             Spin sp;
-            while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
+            while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
                 if (!sp.wait(th)) return RES_FATAL;
+            fence_acqrel();
         }
         for (u32 i = 0; i < n; i++) {
             u64 *row = WL::row(y, L[i]);
@@ -758,6 +760,7 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
     th.polls = 0;
     th.cw = nullptr;
     th.cv = 0;
+    th.hot = 0;
     stages_init(th, p, true);
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L[WL::MAXK];
@@ -825,21 +828,18 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         const u32 age = gid + 1;
         bool held = false;
         // Parallel acquisition (every lane CASes its lock at once) is the fast path.  Under
-        // extreme contention every dying attempt still holds some locks for a moment, and
-        // those transient holds can keep a hot lock busy forever (TPC-C at 1 warehouse: W
-        // is never free when a Payment's lanes look).  After TPL_ORDERED_AFTER restarts the
-        // tile acquires in access (= key) order, one lane at a time, so an attempt that
-        // meets a held lock dies holding only locks that precede it (thread-mode behaviour).
-        const bool ordered = th.attempt >= TPL_ORDERED_AFTER;
+        // extreme contention every dying attempt still holds its other locks for a moment,
+        // and those transient holds can keep a hot lock busy forever (TPC-C at 1 warehouse:
+        // W is never free when a Payment's lanes look).  So a retry under no-wait takes the
+        // lock that killed its previous attempt first, alone, and the rest in parallel once
+        // it holds it: a retry that meets the hot lock busy dies holding nothing.
+        const u32 first = WD ? 0u : th.hot;   // 1 + that lock's lane, 0: none
         Spin sp;
         for (;;) {
             int st = ST_DONE;
             u64 seen = 0;
             bool mine = act && !held;
-            if (ordered) {
-                const unsigned want = tile.ballot(mine);
-                mine = mine && li == (u32)(__ffs(want) - 1);
-            }
+            if (first && !tile.shfl(held || !act, first - 1)) mine = mine && li == first - 1;
             if (mine) {
                 st = tpl_try<WD>(p, &p.meta[L.rec], L.w, age, seen);
                 held = st == ST_DONE;
@@ -850,6 +850,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 const int src = __ffs(dying) - 1;   // remember one conflicting lock for the retry
                 th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
                 th.cv = M31 << 31;                   // wait until its holder count is 0
+                th.hot = (u32)src + 1;               // and take it first next time
                 return RES_ABORT;
             }
             if (tile.all(!act || held)) break;
@@ -926,26 +927,25 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         }
         bool locked = false, bad = false;
         u64 seen = 0;
-        if (th.attempt < TPL_ORDERED_AFTER) {   // write set locked by all lanes at once
-            if (act && L.w) {
-                locked = occ_lock(p, &p.meta[L.rec], pre, seen);
-                bad = !locked;
-            }
-        } else {   // after repeated aborts: in access order, stop at the first busy lock (see 2PL)
-            for (unsigned todo = tile.ballot(act && L.w); todo; todo &= todo - 1) {
-                if (li == (u32)(__ffs(todo) - 1)) {
-                    locked = occ_lock(p, &p.meta[L.rec], pre, seen);
-                    bad = !locked;
-                }
-                if (tile.any(bad)) break;
-            }
+        // write-set locks: all at once; a retry takes the lock that was busy last time
+        // first, alone (see 2PL)
+        const u32 first = th.hot;
+        if (first && li == first - 1 && act && L.w) {
+            locked = occ_lock(p, &p.meta[L.rec], pre, seen);
+            bad = !locked;
+        }
+        if (!tile.any(bad) && act && L.w && !locked) {
+            locked = occ_lock(p, &p.meta[L.rec], pre, seen);
+            bad = !locked;
         }
         {
             const unsigned busy = tile.ballot(bad && (seen & LOCKB));
+            th.hot = 0;
             if (busy) {
                 const int src = __ffs(busy) - 1;
                 th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
                 th.cv = LOCKB;                       // wait until unlocked
+                th.hot = (u32)src + 1;
             }
         }
         u64 ticket = 0, cts = 0;
@@ -991,9 +991,10 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             const u32 seg = p.acc_seg[a], pos = p.acc_pos[a];
             u32 *cur = &p.cursor[seg];
             Spin sp(32);   // the hand-off chain on a hot item is GaccO's critical path
-            while (ld_acquire32(cur) != pos)
+            while (ld_relaxed32(cur) != pos)   // relaxed polls: no L1 invalidation per poll
                 if (!sp.wait(th)) { st = ST_ABORT; break; }
             if (st == ST_DONE) {
+                fence_acqrel();                // acquire once the turn is ours
                 u64 *row = WL::row(y, L);
                 rd<WL>(th, y, L, gid, li, row);
                 if (L.w) inst<WL>(th, y, L, row);
@@ -1009,9 +1010,11 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         int st = ST_DONE;
         if (li == 0 && k > 0) {
             Spin sp;
-            while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
+            while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
                 if (!sp.wait(th)) { st = ST_ABORT; break; }
+            fence_acqrel();   // acquire: K-set k-1's installs happen-before ...
         }
+        tile.sync();          // ... every lane's accesses (memory-ordering warp barrier)
         if (tile.any(st != ST_DONE)) return RES_FATAL;
         if (act) {
             u64 *row = WL::row(y, L);
@@ -1037,6 +1040,7 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
     th.polls = 0;
     th.cw = nullptr;
     th.cv = 0;
+    th.hot = 0;
     stages_init(th, p, li == 0);   // stages are timed by each tile's leader
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     typename WL::Lane L;
@@ -1045,6 +1049,7 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
         u32 gid = NO_TXN;
         if (li == 0) gid = claim_work<S>(th, cl);
         gid = tile.shfl(gid, 0);
+        th.hot = tile.shfl(th.hot, 0);   // from the retry-batch entry (0 for a fresh id)
         if (gid == NO_TXN) break;
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
             if (S == CC_GPUTX && li == 0) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);

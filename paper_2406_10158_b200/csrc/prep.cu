@@ -127,20 +127,34 @@ __global__ void __launch_bounds__(256) gputx_rank_kernel(
             const bool has_q = q > s0;                        // inside this segment
             const uint32_t lo = has_q ? q - 1 : s0;           // first predecessor to visit
             const uint32_t hi = w ? p : (has_q ? q : s0);     // reads: only that write
-            for (uint32_t x = lo; x < hi && !fail; x++) {
-                const uint32_t u = (uint32_t)((keys[x] >> 6) & GID_MASK);
-                uint32_t ru;
-                unsigned ns = 8;
-                while ((ru = ld_acquire32(&rank[u])) == RANK_UNSET) {
-                    if (globaltimer_ns() > deadline || ld_relaxed(&ctl->err.v)) {
-                        atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_WATCHDOG);
-                        fail = true;
-                        break;
+            // A rank is written once (release), so a relaxed load that sees a value sees the
+            // final one and nothing else is read through it: the predecessors' ranks are
+            // loaded 8 at a time (independent loads), and only the unset ones are polled.
+            // (A write after a long run of reads -- a hot item -- otherwise paid one
+            // dependent L2 round trip per read.)
+            constexpr int B = 8;
+            for (uint32_t x = lo; x < hi && !fail; x += B) {
+                uint32_t u[B], ru[B];
+#pragma unroll
+                for (int j = 0; j < B; j++)
+                    u[j] = (x + j < hi) ? (uint32_t)((__ldg(keys + x + j) >> 6) & GID_MASK) : 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < B; j++) ru[j] = (u[j] != 0xFFFFFFFFu) ? ld_relaxed32(&rank[u[j]]) : 0u;
+#pragma unroll
+                for (int j = 0; j < B; j++) {
+                    unsigned ns = 8;
+                    while (ru[j] == RANK_UNSET && !fail) {
+                        if (globaltimer_ns() > deadline || ld_relaxed(&ctl->err.v)) {
+                            atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_WATCHDOG);
+                            fail = true;
+                            break;
+                        }
+                        __nanosleep(ns);
+                        ns = ns < 128 ? ns * 2 : 128;
+                        ru[j] = ld_relaxed32(&rank[u[j]]);
                     }
-                    __nanosleep(ns);
-                    ns = ns < 128 ? ns * 2 : 128;
+                    if (u[j] != 0xFFFFFFFFu) r = max(r, ru[j] + 1);
                 }
-                r = max(r, ru + 1);
             }
         }
         if (tile.any(fail)) return;
