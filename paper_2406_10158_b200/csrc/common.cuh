@@ -78,6 +78,16 @@ GC_DEV void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
 GC_DEV void ld_cg_v2(const u64 *p, u64 &a, u64 &b) {
     asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+// 32 B vectors (sm_100: one LDG.E.ENL2.256 request instead of two 128-bit ones); p must
+// be 32 B aligned
+GC_DEV void ld_cg_v4(const u64 *p, u64 &a, u64 &b, u64 &c, u64 &d) {
+    asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p) : "memory");
+}
+GC_DEV void st_cg_v4(u64 *p, u64 a, u64 b, u64 c, u64 d) {
+    asm volatile("st.global.cg.v4.u64 [%0], {%1, %2, %3, %4};" :: "l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
+                 : "memory");
+}
 GC_DEV u64 ld_cg(const u64 *p) {
     u64 a;
     asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(a) : "l"(p) : "memory");

@@ -798,7 +798,7 @@ static cc_status ensure_arena(cc_db db, uint64_t nodes, uint32_t row_words) {
     cudaFree(db->arena);
     db->arena = nullptr;
     db->arena_nodes = 0;
-    CUDA_TRY(db, dalloc(&db->arena, nodes * (2 + row_words) * 8));
+    CUDA_TRY(db, dalloc(&db->arena, nodes * (ARENA_HDR + row_words) * 8));
     db->arena_nodes = nodes;
     db->arena_row_words = row_words;
     return CC_OK;
@@ -1082,9 +1082,9 @@ cc_status cc_prepare(cc_db db, cc_batch b, cc_scheme scheme, uint32_t flags) {
     CUDA_TRY(db, cudaMemsetAsync(q.ctl, 0, sizeof(Ctl), ps));
     if (b->kind == KIND_TPCC) CUDA_TRY(db, launch_tpcc_gather(p, tp, q.b, db->n_records, ps));
     else CUDA_TRY(db, launch_ycsb_gather(p, y, q.b, ps));
-    // a quarter of the rank kernel's resident grid: it shares the GPU with the executor
-    const int rg = rank_kernel_grid() / 4;
-    CUDA_TRY(db, launch_prep_common(p, q.b, db->n_records, scheme == CC_GPUTX, rg > 0 ? rg : 1, ps));
+    // the rank kernel shares the GPU with the executor: 1024-thread blocks on 1/8 of the SMs
+    const int rg = db->num_sms / 8;
+    CUDA_TRY(db, launch_prep_common(p, q.b, db->n_records, scheme == CC_GPUTX, rg > 0 ? rg : 1, ps, 1024));
     CUDA_TRY(db, cudaEventRecord(q.done, ps));
     q.valid = true;
     return CC_OK;

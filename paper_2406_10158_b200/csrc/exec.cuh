@@ -284,6 +284,10 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
 GC_DEV bool try_append_retry(Th &th, u32 gid) {
     const ExecParams &p = *th.p;
     Ctl *c = p.ctl;
+    // Exhaustion is monotone: once seen, no append can happen, and this worker need not
+    // join the in-flight count -- which the sealers wait to see at 0 (aborts after the
+    // fresh ids ran out would otherwise keep it busy and stall every sealer).
+    if (ld_relaxed(&c->head.v) >= p.n_txn) return false;
     atomicAdd(&c->inflight.v, 1ull);
     fence_sc();   // Dekker pair with the sealer: one of us sees the other
     bool ok = false;
@@ -326,8 +330,9 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
     if (!cl.sealed) {
         fence_sc();
         Spin sp;
-        while (ld_acquire(&c->inflight.v) != 0)
+        while (ld_relaxed(&c->inflight.v) != 0)   // relaxed polls, then one acquire
             if (!sp.wait(th)) return NO_TXN;
+        fence_acqrel();
         cl.tail = ld_acquire(&c->tail.v);
         cl.sealed = true;
     }
@@ -340,9 +345,15 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
 }
 
 // ------------------------------------------------------------------ 2PL (Table II)
-// word = [62] shared | [61:31] holder count | [30:0] holder (wait-die: min age of the
-// holders, Z7; age = gid + 1).  Free <=> count == 0 (shared releases are a single
-// atomic subtract and may leave stale shared/holder bits behind).
+// word = [63] writer waiting (wait-die) | [62] shared | [61:31] holder count | [30:0]
+// holder (wait-die: min age of the holders, Z7; age = gid + 1).  Free <=> count == 0
+// (shared releases are a single atomic subtract and may leave stale bits behind; any
+// acquisition of a free word rewrites all of them).
+// Writer waiting: an older exclusive requester that waits on a shared-held lock sets it,
+// and while it is set a new shared requester counts as conflicting (wait-die decides).
+// Without it, the younger transactions the waiter kills keep re-joining the shared lock
+// on every retry, the count never drains and the writer starves (tile mode, theta=0.9).
+constexpr u64 TPL_WW = 1ull << 63;
 constexpr u64 TPL_S = 1ull << 62;
 constexpr u64 M31 = 0x7FFFFFFFull;
 constexpr u64 TPL_ONE = 1ull << 31;
@@ -365,14 +376,19 @@ GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen) {
             conflict = cnt != 0;
             nv = tpl_make(false, 1, age);
         } else {
-            conflict = cnt != 0 && !(v & TPL_S);
+            conflict = cnt != 0 && (!(v & TPL_S) || (WD && (v & TPL_WW)));
             nv = cnt == 0 ? tpl_make(true, 1, age) : tpl_make(true, cnt + 1, min(age, tpl_holder(v)));
         }
         if (conflict) {
             // no-wait: abort at once.  wait-die: an older requester
             // (smaller age) waits, a younger one dies.
             seen = v;
-            return (WD && age < tpl_holder(v)) ? 1 : 2;
+            if (!(WD && age < tpl_holder(v))) return 2;
+            if (ex && (v & TPL_S) && !(v & TPL_WW)) {   // announce the waiting writer
+                const u64 old = w_cas(p, w, v, v | TPL_WW);
+                if (old != v) { v = old; continue; }
+            }
+            return 1;
         }
         const u64 old = w_cas(p, w, v, nv);
         if (old == v) return 0;
@@ -482,10 +498,10 @@ GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, 
     // walk the history chain for the newest version with begin <= ts
     u64 idx = h & VNONE;
     while (idx != VNONE) {
-        const u64 *node = p.arena + idx * (2 + WL::ROW_WORDS);
+        const u64 *node = p.arena + idx * (ARENA_HDR + WL::ROW_WORDS);
         const u64 h0 = ld_cg(node);
         if ((h0 >> 32) <= ts) {
-            rd<WL>(th, y, L, gid, i, node + 2);
+            rd<WL>(th, y, L, gid, i, node + ARENA_HDR);
             return ST_DONE;
         }
         idx = h0 & VNONE;
@@ -512,9 +528,9 @@ GC_DEV void mvcc_commit(Th &th, const ExecParams &p, const typename WL::Params &
     u64 *hi = lo + 1;
     u64 *row = WL::row(y, L);
     const u64 nidx = (u64)gid * p.K + i;
-    u64 *node = p.arena + nidx * (2 + WL::ROW_WORDS);
+    u64 *node = p.arena + nidx * (ARENA_HDR + WL::ROW_WORDS);
     st_cg(node, ld_relaxed(hi));   // old head -> history node (begin, prev)
-    WL::copy_row(L, row, node + 2);
+    WL::copy_row(L, row, node + ARENA_HDR);
     fence_acqrel();
     w_store(p, hi, (ts << 32) | nidx);   // publish the history, then install in place
     fence_acqrel();
@@ -833,7 +849,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         // W is never free when a Payment's lanes look).  So a retry under no-wait takes the
         // lock that killed its previous attempt first, alone, and the rest in parallel once
         // it holds it: a retry that meets the hot lock busy dies holding nothing.
-        const u32 first = WD ? 0u : th.hot;   // 1 + that lock's lane, 0: none
+        const u32 first = (WD || th.attempt < 2) ? 0u : th.hot;   // 1 + that lock's lane, 0: none
         Spin sp;
         for (;;) {
             int st = ST_DONE;
@@ -929,7 +945,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         u64 seen = 0;
         // write-set locks: all at once; a retry takes the lock that was busy last time
         // first, alone (see 2PL)
-        const u32 first = th.hot;
+        const u32 first = th.attempt < 2 ? 0u : th.hot;
         if (first && li == first - 1 && act && L.w) {
             locked = occ_lock(p, &p.meta[L.rec], pre, seen);
             bad = !locked;

@@ -50,7 +50,7 @@ struct ExecParams {
     unsigned long long watchdog_ns;
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
-    unsigned long long *arena;   // MVCC version nodes
+    unsigned long long *arena;   // MVCC version nodes: ARENA_HDR header words + the row
     unsigned long long *ring;    // retry batch (compacted aborted ids), n_txn slots
     uint32_t ring_cap;
     // per-transaction internal results
@@ -83,6 +83,9 @@ enum { STAGE_INDEX = 0, STAGE_TS = 1, STAGE_WAIT = 2, STAGE_CC = 3, STAGE_ABORT 
 // binary search of PAPER.md:344): the sorted array, padded with ~0 to a multiple of 16,
 // is the leaf level; level l+1 holds the last key of every 16-entry node of level l;
 // the top level has <= 16 entries.  levels[0] = leaves.
+// MVCC history node = header word (begin ts << 32 | previous node) padded to 32 B, then
+// the row, so node rows stay 32 B aligned for 256-bit loads
+constexpr unsigned ARENA_HDR = 4;
 constexpr int IDX_MAX_LEVELS = 10;
 // Lookup modes; every mode returns the same lower-bound result for the same index.
 // Dense modes (f-3 direct addressing) apply when the keys are k0, k0+1, ..., k0+n-1:
@@ -129,8 +132,10 @@ cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid,
 int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block);
 cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBufs &b,
                                cudaStream_t s);
+// rank_block: threads per block of the GPUTx rank kernel (256 inline; 1024 on the prep
+// stream, so that its few blocks occupy few SMs beside the executor)
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,
-                               bool gputx, int grid, cudaStream_t s);
+                               bool gputx, int grid, cudaStream_t s, int rank_block = 256);
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s);

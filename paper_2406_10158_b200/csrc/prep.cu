@@ -103,7 +103,7 @@ __global__ void positions_kernel(const u64 *keys, const uint32_t *seg_id, const 
 constexpr uint32_t RANK_UNSET = 0xFFFFFFFFu;
 
 template <int G>
-__global__ void __launch_bounds__(256) gputx_rank_kernel(
+__global__ void __launch_bounds__(1024) gputx_rank_kernel(
     const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_id, const uint32_t *seg_start,
     const uint32_t *lw, uint32_t *rank, uint32_t n_txn, uint32_t K, Ctl *ctl,
     u64 watchdog_ns) {
@@ -224,7 +224,7 @@ size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn) {
 }
 
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records, bool gputx,
-                               int grid, cudaStream_t s) {
+                               int grid, cudaStream_t s, int rank_block) {
     const uint64_t n = (uint64_t)p.n_txn * p.K;
     const int blk = 256;
     const unsigned g = (unsigned)((n + blk - 1) / blk);
@@ -251,10 +251,10 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     if (e) return e;
     fill_u32_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank, RANK_UNSET, p.n_txn);
     if (p.K <= 16)
-        gputx_rank_kernel<16><<<grid, 256, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
+        gputx_rank_kernel<16><<<grid, rank_block, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
                                                    b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
     else
-        gputx_rank_kernel<32><<<grid, 256, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
+        gputx_rank_kernel<32><<<grid, rank_block, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
                                                    b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
     iota_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.gid_in, p.n_txn);
     bytes = b.cub_bytes;

@@ -195,7 +195,7 @@ struct YcsbWL {
     static GC_DEV void read(const YcsbParams &, Lane &L, u32 gid, u32 i, const u64 *src) {
         u64 r[16];
 #pragma unroll
-        for (int j = 0; j < 8; j++) ld_cg_v2(src + 2 * j, r[2 * j], r[2 * j + 1]);
+        for (int j = 0; j < 4; j++) ld_cg_v4(src + 4 * j, r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
         u64 fp = 0, rf = 0;
 #pragma unroll
         for (int j = 0; j < 16; j++) {
@@ -216,10 +216,10 @@ struct YcsbWL {
 
     static GC_DEV void copy_row(const Lane &, const u64 *src, u64 *dst) {
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            u64 a, b;
-            ld_cg_v2(src + 2 * j, a, b);
-            st_cg_v2(dst + 2 * j, a, b);
+        for (int j = 0; j < 4; j++) {
+            u64 a, b, c, d;
+            ld_cg_v4(src + 4 * j, a, b, c, d);
+            st_cg_v4(dst + 4 * j, a, b, c, d);
         }
     }
 
