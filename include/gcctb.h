@@ -230,6 +230,11 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
 #define CC_FLAG_FLAT_JITTER 0x200u   /* ablation: after waiting out a conflicting lock, retry
                                         with a flat 0..255 ns jitter instead of a window that
                                         doubles per restart (retry pacing) */
+#define CC_FLAG_MVCC_SPLIT 0x400u    /* MVCC metadata layout ablation (PAPER.md:636
+                                        attributes MVCC's gap to TO to its timestamps and version
+                                        pointers being interleaved): the timestamp words in one
+                                        dense array and the version-pointer words in another,
+                                        instead of Table II's interleaved 16 B per record */
 #define CC_FLAG_INDEX_TREE 0x100u    /* force the cache-line search tree even on a dense key
                                         range (default there: direct addressing, key - k0) */
 

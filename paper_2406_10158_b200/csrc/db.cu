@@ -964,8 +964,9 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         CUDA_TRY(db, cudaEventRecord(ev.ev[0], db->stream));
     }
     // a2: reset CC state (every record of every table)
+    p.mvcc_split = (scheme == CC_MVCC && (desc->flags & CC_FLAG_MVCC_SPLIT)) ? db->n_records : 0;
     CUDA_TRY(db, launch_reset_meta(scheme, db->meta, db->n_records, db->ring, db->ring_cap, db->ctl,
-                                   db->stream));
+                                   db->stream, p.mvcc_split != 0));
     CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
     if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
         const uint32_t wpr = db->tpcc.W / db->world;

@@ -465,11 +465,18 @@ GC_DEV void to_commit(Th &th, const ExecParams &p, const typename WL::Params &y,
 }
 
 // MVCC access step (Z6): writes append at the head only; reads never abort.
+// MVCC word pair of a record: interleaved (lo, hi), Table II's 16 B, or split arrays
+// (CC_FLAG_MVCC_SPLIT: lo words as dense as TO's; the PAPER.md:636 ablation)
+GC_DEV u64 *mvcc_lo(const ExecParams &p, u32 rec) { return p.mvcc_split ? p.meta + rec : p.meta + 2ull * rec; }
+GC_DEV u64 *mvcc_hi(const ExecParams &p, u32 rec) {
+    return p.mvcc_split ? p.meta + p.mvcc_split + rec : p.meta + 2ull * rec + 1;
+}
+
 template <class WL>
 GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                      u32 gid, u32 i, u64 ts, bool &pend, u64 &saved_wts) {
-    u64 *lo = &p.meta[2ull * L.rec];
-    u64 *hi = lo + 1;
+    u64 *lo = mvcc_lo(p, L.rec);
+    u64 *hi = mvcc_hi(p, L.rec);
     const u64 *row = WL::row(y, L);
     const u64 v = ld_acquire(lo);
     if (L.w) {
@@ -512,7 +519,7 @@ GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, 
 
 template <class WL>
 GC_DEV void mvcc_restore(const ExecParams &p, typename WL::Lane &L, u64 saved_wts) {
-    u64 *lo = &p.meta[2ull * L.rec];
+    u64 *lo = mvcc_lo(p, L.rec);
     u64 v = ld_relaxed(lo);
     for (;;) {   // keep RTS raised by readers while we were pending
         const u64 old = w_cas(p, lo, v, to_make(false, to_rts(v), saved_wts));
@@ -524,8 +531,8 @@ GC_DEV void mvcc_restore(const ExecParams &p, typename WL::Lane &L, u64 saved_wt
 template <class WL>
 GC_DEV void mvcc_commit(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                         u32 gid, u32 i, u64 ts) {
-    u64 *lo = &p.meta[2ull * L.rec];
-    u64 *hi = lo + 1;
+    u64 *lo = mvcc_lo(p, L.rec);
+    u64 *hi = mvcc_hi(p, L.rec);
     u64 *row = WL::row(y, L);
     const u64 nidx = (u64)gid * p.K + i;
     u64 *node = p.arena + nidx * (ARENA_HDR + WL::ROW_WORDS);

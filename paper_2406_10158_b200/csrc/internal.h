@@ -51,6 +51,8 @@ struct ExecParams {
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
     unsigned long long *arena;   // MVCC version nodes: ARENA_HDR header words + the row
+    unsigned long long mvcc_split;   // MVCC words: 0 = interleaved (lo, hi) pairs; else lo at
+                                     // meta[r], hi at meta[mvcc_split + r] (CC_FLAG_MVCC_SPLIT)
     unsigned long long *ring;    // retry batch (compacted aborted ids), n_txn slots
     uint32_t ring_cap;
     // per-transaction internal results
@@ -126,7 +128,7 @@ struct PrepBufs {
 // launchers (defined in the .cu files)
 cudaError_t launch_reset_meta(int scheme, unsigned long long *meta, uint64_t n_records,
                               unsigned long long *ring, uint32_t ring_cap, Ctl *ctl,
-                              cudaStream_t s);
+                              cudaStream_t s, bool mvcc_split = false);
 cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
                              cudaStream_t s);
 int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block);

@@ -19,10 +19,15 @@ constexpr u64 GID_MASK = (1ull << 21) - 1;
 // Reset the scheme's CC words (the throughput window starts "from the initialization
 // of the CC method", Z19), the retry ring and the control block.
 __global__ void reset_kernel(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
-                             uint32_t ring_cap, Ctl *ctl) {
+                             uint32_t ring_cap, Ctl *ctl, bool mvcc_split) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    if (scheme == CC_MVCC) {
+    if (scheme == CC_MVCC && mvcc_split) {   // lo words dense, hi words after them
+        for (uint64_t r = tid; r < n_records; r += stride) {
+            meta[r] = 0ull;
+            meta[n_records + r] = VNONE;
+        }
+    } else if (scheme == CC_MVCC) {
         for (uint64_t r = tid; r < n_records; r += stride) {
             // lo = 0 (RTS = WTS = 0, not pending); hi = head begins at ts 0, no history
             reinterpret_cast<ulonglong2 *>(meta)[r] = make_ulonglong2(0ull, VNONE);
@@ -46,11 +51,11 @@ __global__ void zero_txn_kernel(uint8_t *committed, uint32_t *restarts, u64 *ohi
 }
 
 cudaError_t launch_reset_meta(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
-                              uint32_t ring_cap, Ctl *ctl, cudaStream_t s) {
+                              uint32_t ring_cap, Ctl *ctl, cudaStream_t s, bool mvcc_split) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    reset_kernel<<<sms * 4, 512, 0, s>>>(scheme, meta, n_records, ring, ring_cap, ctl);
+    reset_kernel<<<sms * 4, 512, 0, s>>>(scheme, meta, n_records, ring, ring_cap, ctl, mvcc_split);
     return cudaGetLastError();
 }
 

@@ -185,7 +185,7 @@ struct YcsbWL {
         const u64 *rw = y.rows + (u64)L.rec * 16u;
         prefetch_l2(rw);
         prefetch_l2(rw + 8);
-        prefetch_l2(p.scheme == CC_MVCC ? p.meta + 2ull * L.rec : p.meta + L.rec);
+        prefetch_l2(p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : p.meta + L.rec);
     }
 
     static GC_DEV u64 *row(const YcsbParams &y, const Lane &L) { return y.rows + (u64)L.rec * 16u; }

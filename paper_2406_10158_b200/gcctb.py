@@ -30,6 +30,7 @@ CC_FLAG_STAGES = 0x40
 CC_FLAG_EVENTS = 0x80
 CC_FLAG_INDEX_TREE = 0x100
 CC_FLAG_FLAT_JITTER = 0x200
+CC_FLAG_MVCC_SPLIT = 0x400
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16

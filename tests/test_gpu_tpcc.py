@@ -40,11 +40,11 @@ def w4(torch_cuda, orc):
     db.close()
 
 
-def _run(db, S0, W, tx_batch, scheme, lanes, orc):
+def _run(db, S0, W, tx_batch, scheme, lanes, orc, flags=0):
     from oracle import tpcc as OT
     tx = tx_batch.export_tpcc()
     db.snapshot(False)
-    res = db.submit(tx_batch, scheme, wd=0, bs=32 if lanes == 1 else 8, lanes=lanes, watchdog_s=60)
+    res = db.submit(tx_batch, scheme, wd=0, bs=32 if lanes == 1 else 8, lanes=lanes, watchdog_s=60, flags=flags)
     st = db.sync()
     assert st.commits == tx_batch.n_txn
     h = res.host(db.stream)
@@ -128,4 +128,14 @@ def test_c4_full_size_parity(c4, orc, scheme, lanes):
     db, S0 = c4
     b = db.gen_tpcc(65536, 41, 5114)
     _run(db, S0, 64, b, scheme, lanes, orc)
+    b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 32])
+def test_mvcc_split_layout(w4, orc, lanes):
+    """f-3 metadata ablation (CC_FLAG_MVCC_SPLIT) on TPC-C: same results as interleaved."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_MVCC_SPLIT
+    db, S0 = w4
+    b = db.gen_tpcc(8192, 41, 5000)
+    _run(db, S0, 4, b, "mvcc", lanes, orc, flags=CC_FLAG_MVCC_SPLIT)
     b.free()

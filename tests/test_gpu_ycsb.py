@@ -194,6 +194,37 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     b.free()
 
 
+@pytest.mark.parametrize("lanes", [1, 4])
+def test_c1_parity_mvcc_split_layout(c1, orc, lanes):
+    """f-3 metadata ablation: MVCC with split timestamp / version-pointer arrays gives the
+    same results as Table II's interleaved layout."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_MVCC_SPLIT
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 45, T, A)
+    keys, ops = orc.ycsb_gen(45, 1024, 1024, 4, 0.5, T, A)
+    db.snapshot(False)
+    res = db.submit(b, "mvcc", wd=0, bs=32, lanes=lanes, flags=CC_FLAG_MVCC_SPLIT)
+    db.sync()
+    orc.check_ycsb("mvcc", S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
+def test_c2_mvcc_split_layout(c2, orc):
+    from paper_2406_10158_b200.gcctb import CC_FLAG_MVCC_SPLIT
+    db, S0, n = c2
+    T = inputs.zipf_thresholds(n, 0.9)
+    A = inputs.scramble_mult(n)
+    b = db.gen_ycsb(1 << 16, 16, 0.1, 79, T, A)
+    keys, ops = orc.ycsb_gen(79, n, 1 << 16, 16, 0.1, T, A)
+    db.snapshot(False)
+    res = db.submit(b, "mvcc", wd=0, bs=32, lanes=16, flags=CC_FLAG_MVCC_SPLIT, watchdog_s=60)
+    assert db.sync().commits == 1 << 16
+    orc.check_ycsb("mvcc", S0, keys, ops, 16, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
 @pytest.mark.parametrize("flag", ["tree", "binary"])
 @pytest.mark.parametrize("scheme", ["tpl_nw", "tictoc", "gacco"])
 def test_c2_full_size_parity_search_index(c2, orc, scheme, flag):
