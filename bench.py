@@ -47,8 +47,10 @@ def parse():
                     help="dense = direct addressing on the dense YCSB key range (default); tree = cache-line "
                          "search tree over the sorted keys; binary = PAPER.md:344 (identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-pipeline", action="store_true",
-                    help="run GPUTx / GaccO preprocessing inline instead of on the prep stream (f-4 ablation)")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="f-4: prepare GPUTx / GaccO for each step's batch on the low-priority prep stream "
+                         "(cc_prepare) while the other schemes execute.  Off by default: measured slower on "
+                         "B200, the persistent executors occupy every SM (profiles/r01_bench_v5_*)")
     ap.add_argument("--workload", default="ycsb", choices=["ycsb", "tpcc"],
                     help="ycsb = configs[1] (default); tpcc = configs[4]: W warehouses partitioned over the ranks")
     ap.add_argument("--warehouses", type=int, default=512)
@@ -200,7 +202,7 @@ def config_of(args, world):
     return {"workload": "ycsb_configs1_10Mrows_64Kx16", "rows": args.rows, "batch": args.batch,
             "ops_per_txn": args.ops, "theta": args.theta, "write_frac": args.write_frac,
             "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs, "lanes_per_txn": args.lanes, "index": args.index,
-            "prep": "inline" if args.no_pipeline else "pipelined (cc_prepare on a second stream)",
+            "prep": "pipelined (cc_prepare on a second stream)" if args.pipeline else "inline",
             "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (1.34 GB table, 168 MB CC words)"}
 
 
@@ -231,7 +233,7 @@ def run_ours(args, rank, world, local):
 
     def prepare(b):
         """f-4: GPUTx / GaccO a3 on the prep stream, overlapping the other schemes' execution."""
-        if not args.no_pipeline:
+        if args.pipeline:
             for s in schemes:
                 db.prepare(b, s, xflags)
 
@@ -327,7 +329,7 @@ def run_ours(args, rank, world, local):
             "per_scheme": per,
             "clocks": clk,
             "e2e": e2e,
-            "gpu_launches": launches_per_step(schemes, not args.no_pipeline) * args.steps,
+            "gpu_launches": launches_per_step(schemes, args.pipeline) * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "exec_kernel (a4-a6), all schemes",
@@ -380,7 +382,7 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xfla
 
     def one():
         b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
-        if not args.no_pipeline:
+        if args.pipeline:
             for s in schemes:
                 db.prepare(b, s, xflags)
         with torch.cuda.stream(stream):

@@ -345,14 +345,16 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
 }
 
 // ------------------------------------------------------------------ 2PL (Table II)
-// word = [63] writer waiting (wait-die) | [62] shared | [61:31] holder count | [30:0]
+// word = [63] writer intent (wait-die) | [62] shared | [61:31] holder count | [30:0]
 // holder (wait-die: min age of the holders, Z7; age = gid + 1).  Free <=> count == 0
 // (shared releases are a single atomic subtract and may leave stale bits behind; any
 // acquisition of a free word rewrites all of them).
-// Writer waiting: an older exclusive requester that waits on a shared-held lock sets it,
-// and while it is set a new shared requester counts as conflicting (wait-die decides).
-// Without it, the younger transactions the waiter kills keep re-joining the shared lock
-// on every retry, the count never drains and the writer starves (tile mode, theta=0.9).
+// Writer intent: an exclusive requester that waits on a shared-held lock sets it, and so
+// does a starving one that dies there (TPL_INTENT_AFTER restarts); while it is set a new shared requester counts as conflicting
+// (wait-die decides), so the lock drains.  Without it a hot read-mostly lock never drains:
+// its recorded min holder age can belong to a long-gone older reader (shared releases do
+// not rewrite it), so even the oldest writer compares itself against that stale age, dies
+// instead of waiting, and starves (tile mode, YCSB theta=0.9: watchdog).
 constexpr u64 TPL_WW = 1ull << 63;
 constexpr u64 TPL_S = 1ull << 62;
 constexpr u64 M31 = 0x7FFFFFFFull;
@@ -365,8 +367,14 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 
 // One acquisition step.  Returns 0 granted, 1 wait (wait-die older requester, or the
 // CAS lost a race), 2 die (conflict under no-wait, or younger requester).
+// A waiting writer always announces intent (TPL_WW); a dying one only once it has restarted
+// this often -- the stale-age starvation needs it, and announcing earlier makes readers die
+// needlessly (measured, YCSB tile 16: every writer at once: theta 0.6 96M -> 53M txn/s;
+// dying writers after 8 restarts: theta 0.8 6.1M -> 1.9M).
+constexpr u32 TPL_INTENT_AFTER = 32;
+
 template <bool WD>
-GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen) {
+GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, bool intent) {
     u64 v = ld_relaxed(w);
     for (;;) {   // latch-free read-transform-CAS loop
         const u32 cnt = tpl_cnt(v);
@@ -383,12 +391,12 @@ GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen) {
             // no-wait: abort at once.  wait-die: an older requester
             // (smaller age) waits, a younger one dies.
             seen = v;
-            if (!(WD && age < tpl_holder(v))) return 2;
-            if (ex && (v & TPL_S) && !(v & TPL_WW)) {   // announce the waiting writer
+            const bool wait = WD && age < tpl_holder(v);
+            if (WD && (wait || intent) && ex && (v & TPL_S) && !(v & TPL_WW)) {   // writer intent (TPL_WW)
                 const u64 old = w_cas(p, w, v, v | TPL_WW);
                 if (old != v) { v = old; continue; }
             }
-            return 1;
+            return wait ? 1 : 2;
         }
         const u64 old = w_cas(p, w, v, nv);
         if (old == v) return 0;
@@ -617,7 +625,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             Spin sp;
             int st;
             u64 seen = 0;
-            while ((st = tpl_try<WD>(p, &p.meta[L[i].rec], L[i].w, age, seen)) == ST_WAIT)
+            while ((st = tpl_try<WD>(p, &p.meta[L[i].rec], L[i].w, age, seen, th.attempt >= TPL_INTENT_AFTER)) == ST_WAIT)
                 if (!sp.wait(th)) { st = -1; break; }
             if (st == ST_ABORT) { th.cw = &p.meta[L[i].rec]; th.cv = M31 << 31; }   // until free
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
@@ -864,7 +872,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             bool mine = act && !held;
             if (first && !tile.shfl(held || !act, first - 1)) mine = mine && li == first - 1;
             if (mine) {
-                st = tpl_try<WD>(p, &p.meta[L.rec], L.w, age, seen);
+                st = tpl_try<WD>(p, &p.meta[L.rec], L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
                 held = st == ST_DONE;
             }
             const unsigned dying = tile.ballot(st == ST_ABORT);

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 300 python tools/probe.py --reps 2 --watchdog 60 --schemes tpl_wd,tpl_nw --thetas 0.6,0.8,0.9,0.99 --lanes 16 > gpurun_out/wd_v7.log 2>&1
+timeout 300 python tools/probe_tpcc.py --W 1 --lanes 32 --watchdog 30 --reps 2 --schemes tpl_wd > gpurun_out/wd_tpcc_v7.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -rf --timeout 600 -k "tpl_wd" > gpurun_out/wd_tests7.log 2>&1; tail -3 gpurun_out/wd_tests7.log
+echo done
