@@ -560,10 +560,50 @@ def run_tpcc(args, rank, world, local):
             "config": {"workload": "tpcc_configs4_partitioned", "warehouses": W, "batch_per_rank": n,
                        "neworder_permyriad": args.tpcc_mix, "schemes": schemes, "lanes_per_txn": 32,
                        "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else "")},
-            "per_scheme": per, "clocks": clk}), flush=True)
+            "per_scheme": per, "clocks": clk,
+            "gpu_launches": launches_per_step(schemes) * args.steps + (0 if world == 1 else
+                                                                       6 * len(schemes) * args.steps),
+            **({} if args.no_cpu_baseline else {"cpu_baseline": tpcc_cpu_baseline(args)})}), flush=True)
     db.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def tpcc_cpu_baseline(args, warehouses=8):
+    """The TPC-C oracle as it stands (oracle/: plain C serial NewOrder / Payment), one host
+    core, replaying configs[4]-shaped batches (same mix, NURand, remote rates) over an
+    8-warehouse population (per-transaction work does not depend on W; 512 warehouses of
+    population do not fit a bounded CPU sample)."""
+    import numpy as np
+    import inputs.tpcc as IT
+    from oracle import tpcc as OT
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    S0 = IT.population(1, warehouses)
+    n_txn = args.tpcc_batch
+    tx = np.ascontiguousarray(OT.gen(5, warehouses, n_txn, args.tpcc_mix, IT.nurand_consts(1)), np.uint32)
+    S = {k: np.array(S0[k], np.uint64, copy=True, order="C") for k in OT.TABLES}
+    S["item"] = np.ascontiguousarray(S0["item"], np.uint64)
+    S.update(OT.empty_slots(n_txn))
+    order = np.arange(n_txn, dtype=np.uint32)
+    out = np.zeros(n_txn * OT.OUT_WORDS, np.uint64)
+    L, P = OT._lib(), OT._ptr
+    args_ = [warehouses] + [P(S[k]) for k in ("warehouse", "district", "customer", "stock", "item", "order",
+                                               "new_order", "order_line", "history")]
+    done, n, t0 = 0, 0, time.perf_counter()
+    while True:   # the same batch again on the evolving state: every transaction still executes
+        st = L.orc_tpcc_replay(*args_, 20240601, n_txn, P(tx), P(order), n_txn, P(out))
+        assert st == 0, st
+        done += n_txn
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= min(args.cpu_seconds, 30.0):
+            break
+    return {"value": done / el, "unit": "txn/s", "cores": 1, "kind": "oracle",
+            "sample": f"serial replay of {n} x {n_txn}-txn TPC-C batches (NewOrder {args.tpcc_mix}/10^4, "
+                      f"Payment otherwise) over an {warehouses}-warehouse population, 1 core"}
 
 
 def main():
