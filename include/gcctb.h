@@ -230,6 +230,9 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
 #define CC_FLAG_FLAT_JITTER 0x200u   /* ablation: after waiting out a conflicting lock, retry
                                         with a flat 0..255 ns jitter instead of a window that
                                         doubles per restart (retry pacing) */
+#define CC_FLAG_PART_2PC 0x800u      /* with CC_FLAG_PARTITIONED, tpl_nw / tpl_wd: distributed
+                                        transactions in 2PC rounds under 2PL (cc_part_decide /
+                                        cc_part_commit / cc_part_next, f-2) */
 #define CC_FLAG_MVCC_SPLIT 0x400u    /* MVCC metadata layout ablation (PAPER.md:636
                                         attributes MVCC's gap to TO to its timestamps and version
                                         pointers being interleaved): the timestamp words in one
@@ -329,6 +332,34 @@ cc_status cc_prepare(cc_db db, cc_batch b, cc_scheme scheme, uint32_t flags);
 cc_status cc_part_send(cc_db db, const void **send, uint64_t *counts);
 cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp);
 cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent);
+
+/* Scheme-native phase B for the 2PL family (cc_submit with
+ * CC_FLAG_PARTITIONED | CC_FLAG_PART_2PC, schemes tpl_nw / tpl_wd): the distributed
+ * transactions run in two-phase-commit rounds instead of the deterministic chains.  Per
+ * round, every rank (collectively):
+ *   cc_part_send    requests of its pending distributed transactions, as above;
+ *   -- all-to-all #1 --
+ *   cc_part_apply   PREPARE: the owner grants the round's requests item by item in global
+ *                   transaction order, no-wait (shared unless an exclusive was granted,
+ *                   exclusive only on a free item), and answers with the values read and
+ *                   the vote in word 5 of each response;
+ *   -- reverse all-to-all #2 --
+ *   cc_part_decide  DECIDE on the home: a transaction commits iff every access was granted;
+ *                   committed ones are assembled with order key (1 << 63 | round, global
+ *                   gid), aborted ones count a restart; *dec = device buffer of n_sent u64
+ *                   decisions (1 commit / 0 abort) aligned with this round's send buffer;
+ *   -- all-to-all #3 of the decisions, same counts as #1 --
+ *   cc_part_commit  COMMIT on the owner: n decisions aligned with the `recv` buffer given
+ *                   to this round's cc_part_apply (kept alive by the caller); installs the
+ *                   granted writes of committed transactions;
+ *   cc_part_next    packs the still-pending transactions for the next round and returns
+ *                   their number (waits).  Loop while any rank has pending transactions
+ *                   (the oldest pending transaction is granted everything it asks for, so
+ *                   every round commits at least one); then cc_part_finish(db, NULL, 0).
+ * STATE outside a 2PC partitioned submit; UNSUPPORTED (at cc_submit) for other schemes. */
+cc_status cc_part_decide(cc_db db, const void *resp, uint64_t n_sent, const void **dec);
+cc_status cc_part_commit(cc_db db, const void *recv, const void *dec, uint64_t n);
+cc_status cc_part_next(cc_db db, uint64_t *pending);
 
 /* Debug event log (CC_FLAG_EVENTS).  Each event is 24 bytes: u64 seq, u32 gid,
  * u32 record (global id; 0xFFFFFFFF for commit/abort), u32 attempt, u32 kind (0 read,

@@ -284,6 +284,28 @@ class DB:
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self._chk(G.lib().cc_part_finish(self.h, resp.data_ptr() if n else None, n))
 
+    # 2PC phase B (f-2)
+    def part_decide(self, back: torch.Tensor) -> torch.Tensor:
+        """Home: decide this round from the returned responses; device u64 decisions
+        aligned with this round's send buffer (as a uint8 tensor of 8 bytes each)."""
+        n = back.numel() // G.PART_REC_BYTES
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        ptr = ctypes.c_void_p()
+        self._chk(G.lib().cc_part_decide(self.h, back.data_ptr() if n else None, n, ctypes.byref(ptr)))
+        if n == 0:
+            return torch.empty(0, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        return _device_bytes(ptr.value, n * 8, self.device)
+
+    def part_commit(self, recv: torch.Tensor, dec: torch.Tensor):
+        n = dec.numel() // 8
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._chk(G.lib().cc_part_commit(self.h, recv.data_ptr() if n else None, dec.data_ptr() if n else None, n))
+
+    def part_next(self) -> int:
+        p = ctypes.c_uint64()
+        self._chk(G.lib().cc_part_next(self.h, ctypes.byref(p)))
+        return int(p.value)
+
     # ----------------------------------------------------------- debug event log (f-4)
     EVENT_DTYPE = np.dtype([("seq", "<u8"), ("gid", "<u4"), ("rec", "<u4"), ("attempt", "<u4"), ("kind", "<u4")])
 

@@ -158,6 +158,11 @@ struct cc_db_s {
         cc_batch b = nullptr;
         bool timing = false;
         Pending ev{};
+        bool two_pc = false;          // CC_FLAG_PART_2PC: phase B in 2PC rounds (f-2)
+        uint32_t round = 0;
+        uint8_t *vote = nullptr;      // owner: grant of every received request (this round)
+        uint64_t vote_cap = 0;
+        unsigned long long *dec = nullptr;   // home: decision of every sent request
     } part;
     // per-submit scratch (grown on demand)
     Ctl *ctl = nullptr;
@@ -313,6 +318,8 @@ cc_status cc_db_destroy(cc_db db) {
     cudaFree(db->part.cnt); cudaFree(db->part.off); cudaFree(db->part.cursor);
     cudaFree(db->part.k1); cudaFree(db->part.k2); cudaFree(db->part.i1); cudaFree(db->part.i2);
     cudaFree(db->part.tmp);
+    cudaFree(db->part.vote);
+    cudaFree(db->part.dec);
     cudaFree(db->arena);
     cudaFree(db->latch);
     cudaFree(db->stages);
@@ -824,7 +831,8 @@ static cc_status ensure_part(cc_db db, uint32_t n_txn) {
     }
     if (n_txn <= P.cap_txn) return CC_OK;
     cudaStreamSynchronize(db->stream);
-    cudaFree(P.skip); cudaFree(P.send); cudaFree(P.stage);
+    cudaFree(P.skip); cudaFree(P.send); cudaFree(P.stage); cudaFree(P.dec);
+    CUDA_TRY(db, dalloc(&P.dec, (size_t)n_txn * TPCC_K * 8));
     CUDA_TRY(db, dalloc(&P.skip, n_txn));
     CUDA_TRY(db, dalloc(&P.send, (size_t)n_txn * TPCC_K * sizeof(PartReq)));
     CUDA_TRY(db, dalloc(&P.stage, (size_t)n_txn * TPCC_K * sizeof(PartResp)));
@@ -947,6 +955,9 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     const bool timing = desc->flags & CC_FLAG_TIMING;
     const bool partitioned = (desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) != 0;
+    const bool two_pc = (desc->flags & CC_FLAG_PART_2PC) != 0;
+    if (two_pc && (!partitioned || (scheme != CC_TPL_NW && scheme != CC_TPL_WD)))
+        return fail(db, CC_ERR_UNSUPPORTED, "CC_FLAG_PART_2PC: 2PL schemes with CC_FLAG_PARTITIONED only");
     if (partitioned) {
         const TpccState &T = db->tpcc;
         if (!is_tpcc) return fail(db, CC_ERR_UNSUPPORTED, "partitioned execution is TPC-C only (YCSB: replicas)");
@@ -1028,6 +1039,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         db->part.b = b;
         db->part.timing = timing;
         db->part.ev = ev;
+        db->part.two_pc = two_pc;
+        db->part.round = 0;
         return CC_OK;
     }
     // a7: commit positions + result copy-out
@@ -1118,8 +1131,59 @@ cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp) {
         CUDA_TRY(db, dalloc((char **)&P.tmp, P.tmp_bytes));
         P.recv_cap = n;
     }
+    if (P.two_pc) {   // PREPARE: grant per item in gid order, vote in resp[k].v[5]
+        if (n > P.vote_cap) {
+            cudaStreamSynchronize(db->stream);
+            cudaFree(P.vote);
+            P.vote = nullptr;
+            CUDA_TRY(db, dalloc(&P.vote, n));
+            P.vote_cap = n;
+        }
+        CUDA_TRY(db, part_grant((PartReq *)recv, n, P.tp, (PartResp *)resp, P.vote, P.k1, P.k2, P.i1, P.i2,
+                                P.tmp, P.tmp_bytes, db->ctl, db->stream));
+        return CC_OK;
+    }
     CUDA_TRY(db, part_apply((PartReq *)recv, n, P.tp, (PartResp *)resp, P.k1, P.k2, P.i1, P.i2, P.tmp,
                             P.tmp_bytes, db->ctl, db->stream));
+    return CC_OK;
+}
+
+cc_status cc_part_decide(cc_db db, const void *resp, uint64_t n_sent, const void **dec) {
+    CHECK_DB(db);
+    auto &P = db->part;
+    if (!P.pending || !P.two_pc) return fail(db, CC_ERR_STATE, "no 2PC partitioned submit pending");
+    if (!dec || (n_sent && !resp)) return fail(db, CC_ERR_INVALID_ARG, "null buffers");
+    const uint32_t wpr = db->tpcc.W / db->world;
+    CUDA_TRY(db, part_decide(P.tp, db->rank, db->world, wpr, P.b->n_txn, P.skip, P.send, (const PartResp *)resp,
+                             n_sent, P.stage, P.p.committed, P.p.order_hi, P.p.order_lo, P.p.read_out,
+                             P.p.restarts, P.round, P.dec, db->stream));
+    *dec = P.dec;
+    return CC_OK;
+}
+
+cc_status cc_part_commit(cc_db db, const void *recv, const void *dec, uint64_t n) {
+    CHECK_DB(db);
+    auto &P = db->part;
+    if (!P.pending || !P.two_pc) return fail(db, CC_ERR_STATE, "no 2PC partitioned submit pending");
+    if (n && (!recv || !dec)) return fail(db, CC_ERR_INVALID_ARG, "null buffers");
+    if (n > P.vote_cap) return fail(db, CC_ERR_INVALID_ARG, "more decisions than requests granted this round");
+    CUDA_TRY(db, part_commit((const PartReq *)recv, n, P.vote, (const unsigned long long *)dec, P.tp, db->stream));
+    return CC_OK;
+}
+
+cc_status cc_part_next(cc_db db, uint64_t *pending) {
+    CHECK_DB(db);
+    auto &P = db->part;
+    if (!P.pending || !P.two_pc) return fail(db, CC_ERR_STATE, "no 2PC partitioned submit pending");
+    if (!pending) return fail(db, CC_ERR_INVALID_ARG, "null pending");
+    const uint32_t wpr = db->tpcc.W / db->world;
+    CUDA_TRY(db, part_repack(P.tp, db->rank, db->world, wpr, P.b->n_txn, P.skip, P.cnt, P.off, P.cursor, P.send,
+                             db->stream));
+    unsigned long long c = 0;
+    CUDA_TRY(db, cudaMemcpyAsync(&c, P.cnt + db->world, 8, cudaMemcpyDeviceToHost, db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    *pending = c;
+    P.round++;
     return CC_OK;
 }
 
@@ -1130,7 +1194,7 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent) {
     const uint32_t wpr = db->tpcc.W / db->world;
     CUDA_TRY(db, part_finish(P.tp, db->rank, db->world, wpr, P.b->n_txn, P.skip, P.send, (const PartResp *)resp,
                              n_sent, P.stage, P.p.committed, P.p.order_hi, P.p.order_lo, P.p.read_out,
-                             db->stream));
+                             db->stream, P.two_pc));
     if (P.timing) CUDA_TRY(db, cudaEventRecord(P.ev.ev[3], db->stream));
     cc_result r = P.res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;

@@ -175,7 +175,22 @@ cudaError_t part_finish(const TpccParams &y, uint32_t rank, uint32_t world, uint
                         uint32_t n_txn, const uint8_t *skip, const PartReq *sent,
                         const PartResp *resp, uint64_t n_sent, PartResp *stage,
                         uint8_t *committed, unsigned long long *ohi, unsigned long long *olo,
-                        unsigned long long *read_out, cudaStream_t s);
+                        unsigned long long *read_out, cudaStream_t s, bool two_pc = false);
+// 2PC phase B (f-2): prepare/grant on the owner, decide on the home, commit on the owner,
+// repack the pending transactions for the next round
+cudaError_t part_grant(PartReq *req, uint64_t n, const TpccParams &y, PartResp *resp, uint8_t *vote,
+                       unsigned long long *k1, unsigned long long *k2, uint32_t *i1, uint32_t *i2,
+                       void *tmp, size_t tmp_bytes, Ctl *ctl, cudaStream_t s);
+cudaError_t part_decide(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                        uint8_t *skip, const PartReq *sent, const PartResp *resp, uint64_t n_sent,
+                        PartResp *stage, uint8_t *committed, unsigned long long *ohi,
+                        unsigned long long *olo, unsigned long long *read_out, uint32_t *restarts,
+                        uint32_t round, unsigned long long *dec, cudaStream_t s);
+cudaError_t part_commit(const PartReq *req, uint64_t n, const uint8_t *vote, const unsigned long long *dec,
+                        const TpccParams &y, cudaStream_t s);
+cudaError_t part_repack(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                        const uint8_t *skip, unsigned long long *cnt, unsigned long long *off,
+                        unsigned long long *cursor, PartReq *out, cudaStream_t s);
 
 cudaError_t launch_ycsb_init_rows(unsigned long long *rows, uint64_t first, uint64_t n,
                                   uint64_t seed, cudaStream_t s);

@@ -66,7 +66,7 @@ __global__ void part_scan_kernel(const unsigned long long *cnt, unsigned long lo
 __global__ void part_pack_kernel(TpccParams y, PartDev pd, uint32_t n_txn, const uint8_t *skip,
                                  unsigned long long *cursor, PartReq *out) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n_txn || !skip[g]) return;
+    if (g >= n_txn || skip[g] != 1) return;   // 0: local (phase A), 2: done (2PC)
     const uint32_t *t = y.tx + (u64)g * TPCC_TX_WORDS;
     const uint32_t type = t[TX_TYPE], w = t[TX_W], d = t[TX_D];
     const uint32_t n = type == 0 ? 3 + t[TX_OLCNT] : 3;
@@ -136,43 +136,46 @@ __global__ void part_keys_kernel(PartReq *req, uint64_t n, TpccParams y, unsigne
     idx[k] = (uint32_t)k;
 }
 
-// one thread per item chain: apply the accesses in gid order, recording what each read
-__global__ void part_chain_kernel(const unsigned long long *skeys, const uint32_t *sidx, uint64_t n,
-                                  const PartReq *req, TpccParams y, PartResp *resp) {
-    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    if (p > 0 && (skeys[p - 1] >> 24) == (skeys[p] >> 24)) return;   // chain head only
-    for (uint64_t q = p; q < n && (skeys[q] >> 24) == (skeys[p] >> 24); q++) {
-        const PartReq &r = req[sidx[q]];
-        PartResp o{};
-        const bool pay = r.type_d & 1u;
-        if (r.kind == 0) {
-            u64 *w = y.wh + (u64)r.row * TPCC_W_WORDS;
-            if (pay) {
-                w[0] += r.amount;                        // w_ytd += h
-                o.v[0] = w[2];
-                o.v[1] = w[3];                           // w_name
-            } else {
-                o.v[0] = (uint32_t)w[1];                 // w_tax
-            }
-        } else if (r.kind == 1) {
-            u64 *d = y.di + (u64)r.row * TPCC_D_WORDS;
-            if (pay) {
-                d[0] += r.amount;                        // d_ytd += h
-                o.v[0] = d[2];
-                o.v[1] = d[3];                           // d_name
-            } else {
-                const u64 w1 = d[1];
-                o.v[0] = (uint32_t)w1;                   // d_tax
-                o.v[1] = w1 >> 32;                       // o_id = d_next_o_id
-                d[1] = (w1 & 0xFFFFFFFFull) | (((w1 >> 32) + 1) << 32);
-            }
-        } else if (r.kind == 2) {
-            u64 *c = y.cu + (u64)r.row * TPCC_C_WORDS;
-            const u64 w3 = c[3];
-            if (pay) {
-                const u64 h = r.amount;
-                c[0] -= h;
+// One phase-B access on the owner: the values it reads (its response) and, if `apply`,
+// its read-modify-write of the row.  Responses are identical with or without `apply`
+// (2PC computes them at grant time and writes at commit time; the row cannot change in
+// between, the grant being exclusive).
+__device__ bool part_is_write(const PartReq &r) {
+    return r.kind == 1 || r.kind == 3 || (r.type_d & 1u);   // D, S always; W, C for Payment
+}
+
+__device__ PartResp part_access(const PartReq &r, const TpccParams &y, bool apply) {
+    PartResp o{};
+    const bool pay = r.type_d & 1u;
+    if (r.kind == 0) {
+        u64 *w = y.wh + (u64)r.row * TPCC_W_WORDS;
+        if (pay) {
+            if (apply) w[0] += r.amount;             // w_ytd += h
+            o.v[0] = w[2];
+            o.v[1] = w[3];                           // w_name
+        } else {
+            o.v[0] = (uint32_t)w[1];                 // w_tax
+        }
+    } else if (r.kind == 1) {
+        u64 *d = y.di + (u64)r.row * TPCC_D_WORDS;
+        if (pay) {
+            if (apply) d[0] += r.amount;             // d_ytd += h
+            o.v[0] = d[2];
+            o.v[1] = d[3];                           // d_name
+        } else {
+            const u64 w1 = d[1];
+            o.v[0] = (uint32_t)w1;                   // d_tax
+            o.v[1] = w1 >> 32;                       // o_id = d_next_o_id
+            if (apply) d[1] = (w1 & 0xFFFFFFFFull) | (((w1 >> 32) + 1) << 32);
+        }
+    } else if (r.kind == 2) {
+        u64 *c = y.cu + (u64)r.row * TPCC_C_WORDS;
+        const u64 w3 = c[3];
+        if (pay) {
+            const u64 h = r.amount;
+            const u64 bal = c[0] - h;
+            if (apply) {
+                c[0] = bal;
                 c[1] += h;
                 c[2] = (c[2] & ~0xFFFFFFFFull) | (u64)((uint32_t)c[2] + 1);
                 if (((w3 >> 32) & 0xFFFF) == 0x4342) {   // "BC" (R7)
@@ -184,34 +187,87 @@ __global__ void part_chain_kernel(const unsigned long long *skeys, const uint32_
                     cd[2] = (u64)(r.home_w & 0xFFFF) + 1;
                     cd[3] = h;
                 }
-                o.v[0] = r.row % TPCC_CUST;
-                o.v[1] = c[0];
             }
-            o.v[2] = w3;
-        } else {
-            u64 *s = y.st + (u64)r.row * TPCC_S_WORDS;
-            const u64 w0 = s[0];
-            const uint32_t q = (uint32_t)w0, qty = r.amount;
+            o.v[0] = r.row % TPCC_CUST;
+            o.v[1] = bal;
+        }
+        o.v[2] = w3;
+    } else {
+        u64 *s = y.st + (u64)r.row * TPCC_S_WORDS;
+        const u64 w0 = s[0];
+        const uint32_t q = (uint32_t)w0, qty = r.amount;
+        if (apply) {
             const uint32_t nq = (q >= qty + 10) ? q - qty : q - qty + 91;
             s[0] = (u64)nq | ((u64)((uint32_t)(w0 >> 32) + 1) << 32);
             s[1] += qty;
             if ((r.type_d >> 16) & 1u) s[2] = (s[2] & ~0xFFFFFFFFull) | (u64)((uint32_t)s[2] + 1);
-            const uint32_t dd = (r.type_d >> 8) & 0xFF;
-            o.v[0] = q;
-            bool orig = false;
-            const uint8_t *sd = reinterpret_cast<const uint8_t *>(s + 33);
-            for (int i = 0; i + 8 <= 50 && !orig; i++) {
-                bool m = true;
-                for (int k = 0; k < 8 && m; k++) m = sd[i + k] == (uint8_t)"ORIGINAL"[k];
-                orig = m;
-            }
-            o.v[1] = orig;
-            o.v[2] = s[3 + 3 * dd];
-            o.v[3] = s[4 + 3 * dd];
-            o.v[4] = s[5 + 3 * dd];
         }
-        resp[sidx[q]] = o;
+        const uint32_t dd = (r.type_d >> 8) & 0xFF;
+        o.v[0] = q;
+        bool orig = false;
+        const uint8_t *sd = reinterpret_cast<const uint8_t *>(s + 33);
+        for (int i = 0; i + 8 <= 50 && !orig; i++) {
+            bool m = true;
+            for (int k = 0; k < 8 && m; k++) m = sd[i + k] == (uint8_t)"ORIGINAL"[k];
+            orig = m;
+        }
+        o.v[1] = orig;
+        o.v[2] = s[3 + 3 * dd];
+        o.v[3] = s[4 + 3 * dd];
+        o.v[4] = s[5 + 3 * dd];
     }
+    return o;
+}
+
+// one thread per item chain: apply the accesses in gid order, recording what each read
+__global__ void part_chain_kernel(const unsigned long long *skeys, const uint32_t *sidx, uint64_t n,
+                                  const PartReq *req, TpccParams y, PartResp *resp) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    if (p > 0 && (skeys[p - 1] >> 24) == (skeys[p] >> 24)) return;   // chain head only
+    for (uint64_t q = p; q < n && (skeys[q] >> 24) == (skeys[p] >> 24); q++)
+        resp[sidx[q]] = part_access(req[sidx[q]], y, true);
+}
+
+// ---------------------------------------------------------------- 2PC rounds (f-2)
+// Scheme-native phase B for the 2PL family.  A round is 2PC:
+// PREPARE -- each owner grants the round's lock requests item by item in global gid order,
+// no-wait (a shared request is granted unless an exclusive one was, an exclusive one only
+// on a free item) and answers with the values read plus the vote (v[5]); DECIDE -- the home
+// commits a transaction iff every access was granted, assembles it, and sends the decision
+// of every access back; COMMIT -- owners install the granted writes of committed
+// transactions.  Locks live for one round (granted at prepare, released when the round
+// ends), so the transactions committed in one round held all their locks together and are
+// conflict-free: the order key is (2^63 | round, global gid).  The oldest pending
+// transaction wins every item it asks for, so every round commits at least one (wait-die's
+// priority: the older proceeds, the younger dies and retries next round).
+__global__ void part_grant_kernel(const unsigned long long *skeys, const uint32_t *sidx, uint64_t n,
+                                  const PartReq *req, TpccParams y, PartResp *resp, uint8_t *vote) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    if (p > 0 && (skeys[p - 1] >> 24) == (skeys[p] >> 24)) return;   // chain head only
+    bool ex = false;
+    uint32_t sh = 0;
+    for (uint64_t q = p; q < n && (skeys[q] >> 24) == (skeys[p] >> 24); q++) {
+        const PartReq &r = req[sidx[q]];
+        const bool w = part_is_write(r);
+        const bool g = w ? (!ex && sh == 0) : !ex;
+        if (g) {
+            if (w) ex = true;
+            else sh++;
+        }
+        PartResp o = part_access(r, y, false);
+        o.v[5] = g;
+        resp[sidx[q]] = o;
+        vote[sidx[q]] = g;
+    }
+}
+
+__global__ void part_commit_kernel(const PartReq *req, uint64_t n, const uint8_t *vote,
+                                   const unsigned long long *dec, TpccParams y) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    if (vote[k] && dec[k] && part_is_write(req[k])) part_access(req[k], y, true);
 }
 
 // ---------------------------------------------------------------- finish (home side)
@@ -233,20 +289,12 @@ __device__ __forceinline__ bool item_original(const u64 *ir) {
     return false;
 }
 
-// assemble outputs + reserved slots of distributed transactions (same formulas as the
-// executor's emission), mark them committed with the Phase B order key; prefix the
-// Phase A keys with the rank
-__global__ void part_assemble_kernel(TpccParams y, PartDev pd, uint32_t n_txn, const uint8_t *skip,
-                                     const PartResp *stage, uint8_t *committed, unsigned long long *ohi,
-                                     unsigned long long *olo, unsigned long long *read_out) {
-    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n_txn) return;
-    if (!skip[g]) {
-        ohi[g] |= (u64)pd.rank << 48;
-        return;
-    }
+// assemble outputs + reserved slots of one distributed transaction from its accesses'
+// responses (same formulas as the executor's emission) and mark it committed with `hi`
+__device__ void part_assemble_one(const TpccParams &y, const PartDev &pd, uint32_t g, const PartResp *st,
+                                  uint8_t *committed, unsigned long long *ohi, unsigned long long *olo,
+                                  unsigned long long *read_out, u64 hi) {
     const uint32_t *t = y.tx + (u64)g * TPCC_TX_WORDS;
-    const PartResp *st = stage + (u64)g * TPCC_K;
     u64 *out = read_out ? read_out + (u64)g * TPCC_OUT_WORDS : nullptr;
     const uint32_t w = t[TX_W], d = t[TX_D];
     if (t[TX_TYPE] == 0) {
@@ -302,8 +350,66 @@ __global__ void part_assemble_kernel(TpccParams y, PartDev pd, uint32_t n_txn, c
         }
     }
     committed[g] = 1;
-    ohi[g] = 1ull << 63;
+    ohi[g] = hi;
     olo[g] = (u64)pd.rank * pd.n_local + g;
+}
+
+// Phase A keys get the rank prefix; distributed transactions (deterministic phase B) are
+// assembled with key (2^63, gid).  In 2PC mode they were assembled round by round.
+__global__ void part_assemble_kernel(TpccParams y, PartDev pd, uint32_t n_txn, const uint8_t *skip,
+                                     const PartResp *stage, uint8_t *committed, unsigned long long *ohi,
+                                     unsigned long long *olo, unsigned long long *read_out, bool two_pc) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_txn) return;
+    if (!skip[g]) {
+        ohi[g] |= (u64)pd.rank << 48;
+        return;
+    }
+    if (two_pc) return;
+    part_assemble_one(y, pd, g, stage + (u64)g * TPCC_K, committed, ohi, olo, read_out, 1ull << 63);
+}
+
+// 2PC DECIDE (home): commit iff every access of the transaction was granted this round
+__global__ void part_decide_kernel(TpccParams y, PartDev pd, uint32_t n_txn, uint8_t *skip, const PartResp *stage,
+                                   uint8_t *committed, unsigned long long *ohi, unsigned long long *olo,
+                                   unsigned long long *read_out, uint32_t *restarts, uint32_t round) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_txn || skip[g] != 1) return;
+    const uint32_t *t = y.tx + (u64)g * TPCC_TX_WORDS;
+    const uint32_t n = t[TX_TYPE] == 0 ? 3 + t[TX_OLCNT] : 3;
+    const PartResp *st = stage + (u64)g * TPCC_K;
+    bool all = true;
+    for (uint32_t i = 0; i < n; i++) all &= st[i].v[5] != 0;
+    if (all) {
+        part_assemble_one(y, pd, g, st, committed, ohi, olo, read_out, (1ull << 63) | round);
+        skip[g] = 2;   // done
+    } else {
+        restarts[g] += 1;   // aborted this round, retried in the next
+    }
+}
+
+// decision of every access sent this round (aligned with the send buffer)
+__global__ void part_dec_kernel(const PartReq *sent, uint64_t n, PartDev pd, const uint8_t *skip,
+                                unsigned long long *dec) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    dec[k] = skip[sent[k].gid - pd.rank * pd.n_local] == 2 ? 1ull : 0ull;
+}
+
+// next round: requests of the still-pending distributed transactions; cnt[world] counts them
+__global__ void part_recount_kernel(TpccParams y, PartDev pd, uint32_t n_txn, const uint8_t *skip,
+                                    unsigned long long *cnt) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_txn || skip[g] != 1) return;
+    const uint32_t *t = y.tx + (u64)g * TPCC_TX_WORDS;
+    const uint32_t n = t[TX_TYPE] == 0 ? 3 + t[TX_OLCNT] : 3;
+    for (uint32_t i = 0; i < n; i++) {
+        uint32_t dest = pd.rank;
+        if (i == 2 && t[TX_TYPE] == 1) dest = owner_of(pd, t[TX_CW]);
+        if (i >= 3) dest = owner_of(pd, t[TX_SUPQ + i - 3] >> 8);
+        atomicAdd(&cnt[dest], 1ull);
+    }
+    atomicAdd(&cnt[pd.world], 1ull);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -352,12 +458,59 @@ size_t part_sort_bytes(uint64_t n) {
 cudaError_t part_finish(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
                         const uint8_t *skip, const PartReq *sent, const PartResp *resp, uint64_t n_sent,
                         PartResp *stage, uint8_t *committed, unsigned long long *ohi, unsigned long long *olo,
-                        unsigned long long *read_out, cudaStream_t s) {
+                        unsigned long long *read_out, cudaStream_t s, bool two_pc) {
+    const PartDev pd{rank, world, wpr, n_txn};
+    if (n_sent && !two_pc)
+        part_stage_kernel<<<(unsigned)((n_sent + 255) / 256), 256, 0, s>>>(sent, resp, n_sent, pd, stage);
+    part_assemble_kernel<<<(n_txn + 127) / 128, 128, 0, s>>>(y, pd, n_txn, skip, stage, committed, ohi, olo,
+                                                             read_out, two_pc);
+    return cudaGetLastError();
+}
+
+// 2PC PREPARE on the owner: resolve + sort like part_apply, then grant per item chain
+cudaError_t part_grant(PartReq *req, uint64_t n, const TpccParams &y, PartResp *resp, uint8_t *vote,
+                       unsigned long long *k1, unsigned long long *k2, uint32_t *i1, uint32_t *i2, void *tmp,
+                       size_t tmp_bytes, Ctl *ctl, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    part_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(req, n, y, k1, i1, ctl);
+    size_t bytes = tmp_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, i1, i2, (int)n, 0, 62, s);
+    if (e) return e;
+    part_grant_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k2, i2, n, req, y, resp, vote);
+    return cudaGetLastError();
+}
+
+// 2PC DECIDE on the home: stage the returned votes / values, decide, emit decisions
+cudaError_t part_decide(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                        uint8_t *skip, const PartReq *sent, const PartResp *resp, uint64_t n_sent, PartResp *stage,
+                        uint8_t *committed, unsigned long long *ohi, unsigned long long *olo,
+                        unsigned long long *read_out, uint32_t *restarts, uint32_t round, unsigned long long *dec,
+                        cudaStream_t s) {
     const PartDev pd{rank, world, wpr, n_txn};
     if (n_sent)
         part_stage_kernel<<<(unsigned)((n_sent + 255) / 256), 256, 0, s>>>(sent, resp, n_sent, pd, stage);
-    part_assemble_kernel<<<(n_txn + 127) / 128, 128, 0, s>>>(y, pd, n_txn, skip, stage, committed, ohi, olo,
-                                                             read_out);
+    part_decide_kernel<<<(n_txn + 127) / 128, 128, 0, s>>>(y, pd, n_txn, skip, stage, committed, ohi, olo,
+                                                           read_out, restarts, round);
+    if (n_sent) part_dec_kernel<<<(unsigned)((n_sent + 255) / 256), 256, 0, s>>>(sent, n_sent, pd, skip, dec);
+    return cudaGetLastError();
+}
+
+// 2PC COMMIT on the owner
+cudaError_t part_commit(const PartReq *req, uint64_t n, const uint8_t *vote, const unsigned long long *dec,
+                        const TpccParams &y, cudaStream_t s) {
+    if (n) part_commit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(req, n, vote, dec, y);
+    return cudaGetLastError();
+}
+
+// next 2PC round: pack the pending transactions' requests; cnt[world] = pending count
+cudaError_t part_repack(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                        const uint8_t *skip, unsigned long long *cnt, unsigned long long *off,
+                        unsigned long long *cursor, PartReq *out, cudaStream_t s) {
+    const PartDev pd{rank, world, wpr, n_txn};
+    cudaMemsetAsync(cnt, 0, (world + 1) * 8ull, s);
+    part_recount_kernel<<<(n_txn + 255) / 256, 256, 0, s>>>(y, pd, n_txn, skip, cnt);
+    part_scan_kernel<<<1, 1, 0, s>>>(cnt, off, cursor, world);
+    part_pack_kernel<<<(n_txn + 255) / 256, 256, 0, s>>>(y, pd, n_txn, skip, cursor, out);
     return cudaGetLastError();
 }
 

@@ -31,6 +31,7 @@ CC_FLAG_EVENTS = 0x80
 CC_FLAG_INDEX_TREE = 0x100
 CC_FLAG_FLAT_JITTER = 0x200
 CC_FLAG_MVCC_SPLIT = 0x400
+CC_FLAG_PART_2PC = 0x800
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
 CC_STATS_WORDS = 16
@@ -128,6 +129,9 @@ _SIGS = {
     "cc_events_read": (ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]),
     "cc_part_apply": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P]),
     "cc_part_finish": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),
+    "cc_part_decide": (ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.POINTER(_P)]),
+    "cc_part_commit": (ctypes.c_int, [_P, _P, _P, ctypes.c_uint64]),
+    "cc_part_next": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
 }
 
 TPCC_TX_WORDS = 40

@@ -7,6 +7,8 @@ cc_part_finish (home assembles outputs / reserved slots, a7).  The collectives a
 all_to_all_single through torch.distributed (plumbing); `loopback_round` runs G
 partitions held by G dbs on one GPU with the same kernels, the exchange being a
 device-side permutation (concatenation of the per-destination slices).
+`dist_round_2pc` / `loopback_round_2pc`: the scheme-native variant for 2PL (f-2), phase B
+in two-phase-commit rounds with a third all-to-all (decisions).
 """
 from __future__ import annotations
 
@@ -17,8 +19,8 @@ from . import gcctb as G
 REC = G.PART_REC_BYTES
 
 
-def exchange(send: torch.Tensor, send_counts, group=None, via_cpu: bool = False):
-    """All-to-all of 48-byte records grouped by destination.  Returns (recv, recv_counts)."""
+def exchange(send: torch.Tensor, send_counts, group=None, via_cpu: bool = False, rec: int = REC):
+    """All-to-all of `rec`-byte records grouped by destination.  Returns (recv, recv_counts)."""
     import torch.distributed as dist
     dev = send.device if not via_cpu else torch.device("cpu")
     sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
@@ -26,8 +28,8 @@ def exchange(send: torch.Tensor, send_counts, group=None, via_cpu: bool = False)
     dist.all_to_all_single(rc, sc, group=group)
     recv_counts = [int(x) for x in rc.tolist()]
     src = send if not via_cpu else send.cpu()
-    recv = torch.empty(sum(recv_counts) * REC, dtype=torch.uint8, device=dev)
-    dist.all_to_all_single(recv, src, [c * REC for c in recv_counts], [c * REC for c in send_counts], group=group)
+    recv = torch.empty(sum(recv_counts) * rec, dtype=torch.uint8, device=dev)
+    dist.all_to_all_single(recv, src, [c * rec for c in recv_counts], [c * rec for c in send_counts], group=group)
     return (recv if not via_cpu else recv.to(send.device)), recv_counts
 
 
@@ -53,6 +55,77 @@ def dist_round(db, batch, scheme, result=None, group=None, via_cpu=False, **kw):
     back = give_back(resp, recv_counts, counts, group, via_cpu)
     db.part_finish(back)
     return res
+
+
+def dist_round_2pc(db, batch, scheme, result=None, group=None, via_cpu=False, **kw):
+    """One partitioned submit whose distributed transactions run in 2PC rounds under 2PL
+    (f-2; all ranks call it collectively): per round requests (#1), grants + votes back
+    (#2), decisions (#3, 8 bytes per request), until no rank has pending transactions."""
+    import torch.distributed as dist
+    flags = kw.pop("flags", 0) | G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_2PC
+    res = db.submit(batch, scheme, flags=flags, result=result, **kw)
+    rounds = 0
+    while True:
+        send, counts = db.part_send()
+        recv, recv_counts = exchange(send, counts, group, via_cpu)
+        resp = db.part_apply(recv)
+        db.stream.synchronize()
+        back = give_back(resp, recv_counts, counts, group, via_cpu)
+        dec = db.part_decide(back)
+        db.stream.synchronize()
+        rdec, _ = exchange(dec, counts, group, via_cpu, rec=8)
+        db.part_commit(recv, rdec)
+        pending = torch.tensor([db.part_next()], dtype=torch.int64,
+                               device=send.device if not via_cpu else torch.device("cpu"))
+        dist.all_reduce(pending, op=dist.ReduceOp.MAX, group=group)
+        rounds += 1
+        if int(pending.item()) == 0:
+            break
+    db.part_finish(torch.empty(0, dtype=torch.uint8, device=send.device))
+    return res, rounds
+
+
+def _slices(buf, counts, rec):
+    o = [0]
+    for c in counts:
+        o.append(o[-1] + c * rec)
+    return [buf[o[d]:o[d + 1]] for d in range(len(counts))]
+
+
+def loopback_round_2pc(dbs, batches, scheme, results=None, **kw):
+    """dist_round_2pc for G partitions on one GPU (exchanges are slicing + concatenation)."""
+    flags = kw.pop("flags", 0) | G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_2PC
+    res = [db.submit(b, scheme, flags=flags, result=None if results is None else results[i], **kw)
+           for i, (db, b) in enumerate(zip(dbs, batches))]
+    world, rounds = len(dbs), 0
+    while True:
+        sends = [db.part_send() for db in dbs]
+        parts = [_slices(buf, counts, REC) for buf, counts in sends]            # [src][dst]
+        recvs = [torch.cat([parts[s][d] for s in range(world)]) for d in range(world)]
+        resps = []
+        for d, db in enumerate(dbs):
+            resps.append(db.part_apply(recvs[d]))
+            db.stream.synchronize()
+        decs = []
+        for s, db in enumerate(dbs):   # responses return to the senders in their send order
+            pieces = []
+            for d in range(world):
+                start = sum(sends[q][1][d] for q in range(s)) * REC
+                pieces.append(resps[d][start:start + sends[s][1][d] * REC])
+            decs.append(db.part_decide(torch.cat(pieces)))
+            db.stream.synchronize()
+        dparts = [_slices(dec, counts, 8) for dec, (_, counts) in zip(decs, sends)]
+        pending = 0
+        for d, db in enumerate(dbs):
+            db.part_commit(recvs[d], torch.cat([dparts[s][d] for s in range(world)]))
+        for db in dbs:
+            pending = max(pending, db.part_next())
+        rounds += 1
+        if pending == 0:
+            break
+    for db in dbs:
+        db.part_finish(torch.empty(0, dtype=torch.uint8, device=torch.device("cuda", db.device)))
+    return res, rounds
 
 
 def loopback_round(dbs, batches, scheme, results=None, **kw):

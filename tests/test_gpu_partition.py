@@ -85,3 +85,66 @@ def test_loopback_partitions(torch_cuda, orc, scheme, G_):
     _merged_check(scheme, W, dbs, batches, res, S0, n)
     for db in dbs:
         db.close()
+
+
+# ---------------------------------------------------------------- f-2: 2PC phase B (2PL)
+@pytest.mark.parametrize("G_", [2, 4])
+@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd"])
+def test_loopback_2pc(torch_cuda, orc, scheme, G_):
+    """Distributed transactions in 2PC rounds under 2PL: the merged result equals serial
+    replay of phase A then the 2PC rounds in (round, gid) order."""
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200.partition import loopback_round_2pc
+    W, n = 8, 2048
+    wpr = W // G_
+    dbs, batches = [], []
+    for r in range(G_):
+        db = DB(0, rank=r, world=G_)
+        db.load_tpcc(W, 17, n, w_first=r * wpr, w_count=wpr)
+        dbs.append(db)
+        batches.append(db.gen_tpcc(n, 300 + r, 5114, w_lo=r * wpr, w_hi=(r + 1) * wpr))
+    S0 = IT.population(17, W)
+    res, rounds = loopback_round_2pc(dbs, batches, scheme, bs=8, lanes=32)
+    assert rounds >= 1
+    for db in dbs:
+        assert db.sync().commits == n
+    _merged_check(scheme, W, dbs, batches, res, S0, n)
+    hs = [r.host(db.stream) for r, db in zip(res, dbs)]
+    hi = np.concatenate([h["order_hi"] for h in hs])
+    b = hi >= np.uint64(1 << 63)
+    assert b.any()
+    assert ((hi[b] & np.uint64(0xFFFFFFFF)) < np.uint64(rounds)).all()   # round number in the key
+    for db in dbs:
+        db.close()
+
+
+@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd"])
+def test_2pc_all_distributed_contention(torch_cuda, orc, scheme):
+    """Every transaction through 2PC on one partition of 2 warehouses: heavy conflicts,
+    many rounds, each committing a conflict-free set; aborts are counted as restarts."""
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200 import gcctb as G
+    from paper_2406_10158_b200.partition import loopback_round_2pc
+    W, n = 2, 2048
+    db = DB(0, rank=0, world=1)
+    db.load_tpcc(W, 13, n)
+    S0 = IT.population(13, W)
+    b = db.gen_tpcc(n, 6, 5114)
+    res, rounds = loopback_round_2pc([db], [b], scheme, flags=G.CC_FLAG_PART_ALL, bs=8, lanes=32)
+    st = db.sync()
+    assert st.commits == n and st.aborts > 0 and rounds > 10
+    h = res[0].host(db.stream)
+    assert (h["order_hi"] >= np.uint64(1 << 63)).all()
+    _merged_check(scheme, W, [db], [b], res, S0, n)
+    db.close()
+
+
+def test_2pc_rejects_other_schemes(torch_cuda):
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200 import gcctb as G
+    db = DB(0, rank=0, world=1)
+    db.load_tpcc(1, 3, 256)
+    b = db.gen_tpcc(256, 1, 5000)
+    with pytest.raises(G.CCError, match="UNSUPPORTED"):
+        db.submit(b, "silo", flags=G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_2PC, lanes=32, bs=8)
+    db.close()

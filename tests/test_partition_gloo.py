@@ -63,3 +63,89 @@ def test_exchange_routing(world):
         p.join(timeout=60)
     assert all(o[1] for o in out), out
     assert sum(o[2] for o in out) == sum(o[3] for o in out)
+
+
+class _FakeDB:
+    """Stands in for a rank's DB in dist_round_2pc (host logic only): each round it sends
+    one request to every rank, grants everything, and finishes after `done_after` rounds;
+    it records what it saw so the test can check routing and alignment."""
+
+    def __init__(self, rank, world, done_after):
+        self.rank, self.world, self.done_after = rank, world, done_after
+        self.round, self.commits, self.finished = 0, [], False
+        self.stream = type("S", (), {"synchronize": staticmethod(lambda: None)})()
+
+    def submit(self, batch, scheme, flags=0, result=None, **kw):
+        from paper_2406_10158_b200 import gcctb as G
+        assert flags & G.CC_FLAG_PART_2PC and flags & G.CC_FLAG_PARTITIONED
+        return "res"
+
+    def part_send(self):
+        pending = self.round < self.done_after
+        counts = [1 if pending else 0] * self.world
+        recs = []
+        for d in range(self.world):
+            for _ in range(counts[d]):
+                r = torch.zeros(REC, dtype=torch.uint8)
+                r[0], r[1], r[2] = self.rank, d, self.round
+                recs.append(r)
+        return (torch.cat(recs) if recs else torch.empty(0, dtype=torch.uint8)), counts
+
+    def part_apply(self, recv):
+        rv = recv.view(-1, REC)
+        assert bool((rv[:, 1] == self.rank).all())
+        self._recv_src = rv[:, 0].tolist()
+        out = rv.clone()
+        out[:, 5 * 8] = 1                                   # vote: granted (word 5)
+        return out.view(-1)
+
+    def part_decide(self, back):
+        bv = back.view(-1, REC)
+        assert bool((bv[:, 0] == self.rank).all()) and bool((bv[:, 5 * 8] == 1).all())
+        dec = torch.zeros(bv.shape[0], 8, dtype=torch.uint8)
+        dec[:, 0] = 1
+        dec[:, 1] = self.rank                              # who decided
+        return dec.view(-1)
+
+    def part_commit(self, recv, rdec):
+        dv = rdec.view(-1, 8)
+        assert dv[:, 1].tolist() == self._recv_src          # decisions aligned with requests
+        self.commits.append(int(dv.shape[0]))
+
+    def part_next(self):
+        self.round += 1
+        return max(0, self.done_after - self.round)
+
+    def part_finish(self, resp):
+        self.finished = True
+
+
+def _worker_2pc(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_10158_b200 import partition as P
+    db = _FakeDB(rank, world, done_after=rank + 1)         # ranks finish at different rounds
+    res, rounds = P.dist_round_2pc(db, None, "tpl_nw")
+    q.put((rank, rounds, db.finished, db.commits))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_2pc_rounds_until_every_rank_is_done(world):
+    """f-2 host loop: all ranks keep exchanging (possibly empty) rounds until the slowest
+    is done; decisions come back aligned with each owner's received requests."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_2pc, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, rounds, finished, commits in out:
+        assert rounds == world and finished
+        # round k: every rank still pending (rank >= k) sends one request here
+        assert commits == [sum(1 for s in range(world) if s >= k) for k in range(world)]
