@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--warehouses", type=int, default=512)
     ap.add_argument("--tpcc-batch", type=int, default=65536, help="transactions per rank per step")
     ap.add_argument("--tpcc-mix", type=int, default=5114, help="NewOrder share in 1/10,000 (45:43, PAPER.md:468)")
+    ap.add_argument("--two-pc", action="store_true",
+                    help="TPC-C: distributed transactions of tpl_nw / tpl_wd in 2PC rounds (f-2); the other "
+                         "schemes keep the deterministic phase B")
     ap.add_argument("--loopback", type=int, default=0,
                     help="tpcc: run G warehouse partitions as G dbs on this one GPU (a8 with a device-side exchange)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -422,7 +425,7 @@ def run_tpcc_loopback(args, local):
     import torch
 
     from paper_2406_10158_b200.api import DB, Result
-    from paper_2406_10158_b200.partition import loopback_round
+    from paper_2406_10158_b200.partition import loopback_round, loopback_round_2pc
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -441,7 +444,10 @@ def run_tpcc_loopback(args, local):
         bs = [db.gen_tpcc(n, 7919 * (r + 1) + i, args.tpcc_mix, w_lo=r * wpr, w_hi=(r + 1) * wpr)
               for r, db in enumerate(dbs)]
         for s in schemes:
-            loopback_round(dbs, bs, s, results=res[s], bs=8, lanes=32, watchdog_s=60)
+            if args.two_pc and s in ("tpl_nw", "tpl_wd"):
+                loopback_round_2pc(dbs, bs, s, results=res[s], bs=8, lanes=32, watchdog_s=60)
+            else:
+                loopback_round(dbs, bs, s, results=res[s], bs=8, lanes=32, watchdog_s=60)
         return bs
 
     for i in range(args.warmup):
@@ -478,6 +484,7 @@ def run_tpcc_loopback(args, local):
         "config": {"workload": "tpcc_configs4_partitioned_loopback", "warehouses": W, "partitions": G,
                    "batch_per_partition": n, "neworder_permyriad": args.tpcc_mix, "schemes": schemes,
                    "lanes_per_txn": 32, "parallelism": f"{G} warehouse partitions on 1 GPU, device-side exchange",
+                   "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic",
                    "timing": "host clock around fully synchronised steps (G streams + host-orchestrated exchange)"},
         "per_scheme": per, "clocks": clk}), flush=True)
     for db in dbs:
@@ -494,7 +501,7 @@ def run_tpcc(args, rank, world, local):
 
     from paper_2406_10158_b200.api import DB, Result
     from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
-    from paper_2406_10158_b200.partition import dist_round
+    from paper_2406_10158_b200.partition import dist_round, dist_round_2pc
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -511,7 +518,9 @@ def run_tpcc(args, rank, world, local):
     def step(i):
         b = db.gen_tpcc(n, 7919 * (rank + 1) + i, args.tpcc_mix, w_lo=rank * wpr, w_hi=(rank + 1) * wpr)
         for s in schemes:
-            if world > 1:
+            if world > 1 and args.two_pc and s in ("tpl_nw", "tpl_wd"):
+                dist_round_2pc(db, b, s, result=res[s], bs=8, lanes=32, watchdog_s=60)
+            elif world > 1:
                 dist_round(db, b, s, result=res[s], bs=8, lanes=32, watchdog_s=60)
             else:
                 db.submit(b, s, bs=8, lanes=32, result=res[s], watchdog_s=60)
@@ -559,7 +568,8 @@ def run_tpcc(args, rank, world, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "tpcc_configs4_partitioned", "warehouses": W, "batch_per_rank": n,
                        "neworder_permyriad": args.tpcc_mix, "schemes": schemes, "lanes_per_txn": 32,
-                       "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else "")},
+                       "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else ""),
+                       "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic"},
             "per_scheme": per, "clocks": clk,
             "gpu_launches": launches_per_step(schemes) * args.steps + (0 if world == 1 else
                                                                        6 * len(schemes) * args.steps),
