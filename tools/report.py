@@ -74,7 +74,7 @@ def wdbs_table(rows):
 
 def stages_table(rows):
     st = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful"]
-    out = ["| preset | mode | index | scheme | " + " | ".join(st) + " | (ns per committed txn) |",
+    out = ["| preset | mode | lookup | scheme | " + " | ".join(st) + " | (ns per committed txn) |",
            "|---|---|---|---|" + "---|" * len(st) + "---|"]
     for r in rows:
         if "stage_ns_per_txn" not in r:
