@@ -367,6 +367,11 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 
 // One acquisition step.  Returns 0 granted, 1 wait (wait-die older requester, or the
 // CAS lost a race), 2 die (conflict under no-wait, or younger requester).
+// Tile-mode TO: restarts after which a transaction's accesses are stepped one lane at a
+// time (measured, profiles/r01_probe_v16_*: 8 halves TO at theta=0.6, 32 keeps it; the
+// same for wait-die cost 4.7x at theta=0.8 and was dropped)
+constexpr u32 TO_SEQ_AFTER = 32;
+
 // A waiting writer always announces intent (TPL_WW); a dying one only once it has restarted
 // this often -- the stale-age starvation needs it, and announcing earlier makes readers die
 // needlessly (measured, YCSB tile 16: every writer at once: theta 0.6 96M -> 53M txn/s;
@@ -910,10 +915,21 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         if (draw_ts_overflow(ts, p)) return RES_FATAL;
         bool done = !act, pend = false;
         u64 saved = 0;
+        // Basic TO under heavy contention: an attempt doomed by one conflict would still
+        // raise the read timestamps of all its other items at once and abort their writers
+        // (tile mode at theta=0.99: 5 K txn/s).  After TO_SEQ_AFTER restarts a transaction
+        // steps one lane at a time in access order and stops at the first conflict, as the
+        // paper's one-thread-per-transaction launch does.
+        const bool seq = S == CC_TO && th.attempt >= TO_SEQ_AFTER;
         Spin sp;
         for (;;) {
             int st = ST_DONE;
-            if (!done) {
+            bool mine = !done;
+            if (seq) {
+                const unsigned want = tile.ballot(mine);
+                mine = mine && li == (u32)(__ffs(want) - 1);
+            }
+            if (mine) {
                 st = (S == CC_TO) ? to_step<WL>(th, p, y, L, gid, li, ts, pend, saved)
                                   : mvcc_step<WL>(th, p, y, L, gid, li, ts, pend, saved);
                 done = st == ST_DONE;
@@ -927,6 +943,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
             if (tile.all(done)) break;
             if (tile.any(st == ST_RETRY)) continue;   // lost a CAS race: go again at once
+            if (seq && !tile.any(st == ST_WAIT)) continue;   // sequential: the next lane's turn
             if (tile.any(!sp.wait(th))) {
                 if (pend) {
                     if (S == CC_TO) w_store(p, &p.meta[L.rec], saved);
