@@ -47,3 +47,15 @@ def test_no_oracle_import_in_product_path():
                 s = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in s and "from oracle" not in s, f
                 assert "oracle_ycsb" not in s and "liboracle" not in s, f
+
+
+def test_binding_flag_values_match_header():
+    """Every CC_FLAG_* the header defines has the same value in the Python binding."""
+    from paper_2406_10158_b200 import gcctb
+    src = open(os.path.join(ROOT, "include", "gcctb.h")).read()
+    flags = dict(re.findall(r"#define (CC_FLAG_[A-Z0-9_]+) (0x[0-9a-fA-F]+)u", src))
+    assert len(flags) >= 12
+    for name, val in flags.items():
+        assert hasattr(gcctb, name), name
+        assert getattr(gcctb, name) == int(val, 16), name
+    assert len(set(int(v, 16) for v in flags.values())) == len(flags)   # distinct bits
