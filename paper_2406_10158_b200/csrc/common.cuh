@@ -53,6 +53,14 @@ GC_DEV u64 cas_acqrel(u64 *p, u64 expect, u64 desired) {
                  : "=l"(old) : "l"(p), "l"(expect), "l"(desired) : "memory");
     return old;
 }
+// Lock acquisition: acquire ordering only (nothing before it is published by it), so
+// ptxas emits no MEMBAR in front of the CAS as it does for acq_rel.
+GC_DEV u64 cas_acquire(u64 *p, u64 expect, u64 desired) {
+    u64 old;
+    asm volatile("atom.acquire.gpu.global.cas.b64 %0, [%1], %2, %3;"
+                 : "=l"(old) : "l"(p), "l"(expect), "l"(desired) : "memory");
+    return old;
+}
 GC_DEV u64 atom_add_acqrel(u64 *p, u64 v) {
     u64 old;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;"

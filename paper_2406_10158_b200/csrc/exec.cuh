@@ -200,6 +200,16 @@ GC_DEV u64 w_cas(const ExecParams &p, u64 *w, u64 expect, u64 desired) {
     latch_release(l);
     return old;
 }
+// CAS that acquires a lock / pending bit: acquire ordering suffices (see cas_acquire)
+GC_DEV u64 w_cas_acq(const ExecParams &p, u64 *w, u64 expect, u64 desired) {
+    if (!p.latch) return cas_acquire(w, expect, desired);
+    uint32_t *l = latch_of(p, w);
+    latch_acquire(l);
+    const u64 old = ld_relaxed(w);
+    if (old == expect) st_relaxed(w, desired);
+    latch_release(l);
+    return old;
+}
 GC_DEV void w_store(const ExecParams &p, u64 *w, u64 v) {   // release store
     if (!p.latch) { st_release(w, v); return; }
     uint32_t *l = latch_of(p, w);
@@ -398,12 +408,12 @@ GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, boo
             seen = v;
             const bool wait = WD && age < tpl_holder(v);
             if (WD && (wait || intent) && ex && (v & TPL_S) && !(v & TPL_WW)) {   // writer intent (TPL_WW)
-                const u64 old = w_cas(p, w, v, v | TPL_WW);
+                const u64 old = w_cas_acq(p, w, v, v | TPL_WW);
                 if (old != v) { v = old; continue; }
             }
             return wait ? 1 : 2;
         }
-        const u64 old = w_cas(p, w, v, nv);
+        const u64 old = w_cas_acq(p, w, v, nv);
         if (old == v) return 0;
         v = old;
     }
@@ -454,7 +464,7 @@ GC_DEV int to_step(Th &th, const ExecParams &p, const typename WL::Params &y, ty
     if (L.w) {
         if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;   // older pending: wait (Z4)
         if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
-        if (w_cas(p, w, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
+        if (w_cas_acq(p, w, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
         pend = true;
         saved = v;
         rd<WL>(th, y, L, gid, i, row);   // stable: we own the pending bit
@@ -464,7 +474,7 @@ GC_DEV int to_step(Th &th, const ExecParams &p, const typename WL::Params &y, ty
     if (v & TO_P) return ST_WAIT;
     const u64 ev = rd<WL>(th, y, L, gid, i, row);
     fence_acqrel();
-    const bool ok = (to_rts(v) >= ts) ? ld_relaxed(w) == v : w_cas(p, w, v, to_make(false, ts, to_wts(v))) == v;
+    const bool ok = (to_rts(v) >= ts) ? ld_relaxed(w) == v : w_cas_acq(p, w, v, to_make(false, ts, to_wts(v))) == v;   // after the fence above
     if (ok) return ST_DONE;
     retract_read(th, ev);
     return ST_RETRY;
@@ -495,7 +505,7 @@ GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, 
     if (L.w) {
         if (v & TO_P) return to_wts(v) < ts ? ST_WAIT : ST_ABORT;
         if (ts < to_rts(v) || ts < to_wts(v)) return ST_ABORT;
-        if (w_cas(p, lo, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
+        if (w_cas_acq(p, lo, v, to_make(true, to_rts(v), ts)) != v) return ST_RETRY;
         pend = true;
         saved_wts = to_wts(v);
         rd<WL>(th, y, L, gid, i, row);
@@ -509,7 +519,7 @@ GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, 
         bool ok = ld_relaxed(hi) == h;
         if (ok) {
             if (to_rts(v) >= ts) ok = ld_relaxed(lo) == v;
-            else ok = w_cas(p, lo, v, (v & ~(M31 << 31)) | ((ts & M31) << 31)) == v;
+            else ok = w_cas_acq(p, lo, v, (v & ~(M31 << 31)) | ((ts & M31) << 31)) == v;   // after the fence
         }
         if (ok) return ST_DONE;
         retract_read(th, ev);
@@ -582,7 +592,7 @@ GC_DEV bool occ_lock(const ExecParams &p, u64 *w, u64 &pre, u64 &seen) {
     for (int k = 0; k < 8; k++) {
         seen = v;
         if (v & LOCKB) return false;
-        const u64 old = w_cas(p, w, v, v | LOCKB);
+        const u64 old = w_cas_acq(p, w, v, v | LOCKB);
         if (old == v) {
             pre = v;
             return true;
