@@ -264,16 +264,19 @@ def run_ours(args, rank, world, local):
     clocks.start()
     db.timing(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     batches = []
     barrier()
     e0.record(stream)
     for i in range(args.steps):
         batches.append(step(args.warmup + i, timing=True))
+        ev[i].record(stream)
     e1.record(stream)
     barrier()
     clk = clocks.stop()
     st = db.sync()
     ms = e0.elapsed_time(e1)
+    step_ms = [e0.elapsed_time(ev[0])] + [ev[i - 1].elapsed_time(ev[i]) for i in range(1, args.steps)]
     phase_ms, n_sub = db.timing(reset=True)
     # per-scheme stats from the last step (committed + aborts), checked complete
     per = {}
@@ -330,6 +333,7 @@ def run_ours(args, rank, world, local):
             "config": config_of(args, world),
             "abort_rate": sum(p["aborts"] for p in per.values()) / max(1, sum(p["commits"] for p in per.values())),
             "per_scheme": per,
+            "step_ms": step_ms,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches_per_step(schemes, args.pipeline) * args.steps,

@@ -2,6 +2,7 @@
 // allocation, enqueues the a1..a7 kernels on the db stream, and turns device errors
 // into cc_status.  No torch types anywhere: plain pointers and sizes.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -914,6 +915,10 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.flags = desc->flags;
     p.lanes = desc->lanes_per_txn <= 1 ? 1 : (is_tpcc ? 32 : desc->lanes_per_txn);
     p.claim_chunk = desc->claim_chunk ? desc->claim_chunk : 1;
+    {   // experiment knob (not part of the ABI): TO/MVCC retry backoff cap exponent
+        static const int to_cap = getenv("GCCTB_TO_BACKOFF_CAP") ? atoi(getenv("GCCTB_TO_BACKOFF_CAP")) : 0;
+        p.to_backoff_cap = (uint32_t)(to_cap > 0 && to_cap < 20 ? to_cap : 0);
+    }
     p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
     p.ctl = db->ctl;
     p.sticky = db->sticky_dev;

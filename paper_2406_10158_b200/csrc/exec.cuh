@@ -235,12 +235,22 @@ GC_DEV void w_add(const ExecParams &p, u64 *w, u64 v) {
 // validation and retry in perfect symmetry forever (an OCC livelock the paper's
 // immediate restart, is exposed to as well).  Delay is uniform in
 // [0, 64 ns << min(restarts, cap)) from a hash of (gid, restarts); cap = 10 (~65 us)
-// keeps batch tails short; timestamp schemes use cap 14 (~1 ms): basic TO under a
-// read-hot key otherwise retries in a storm that burns 31-bit timestamps
-// (PAPER.md:732).  Chosen from the measured probes (profiles/r01_probe_v6..v11).
+// keeps batch tails short.  Timestamp schemes adapt the cap to the number of
+// transactions backing off at that moment: 10 while few do (a moderately contended
+// batch: a fixed 1 ms cap made single stragglers sleep the batch long, TO at theta=0.6
+// 46-72 M vs 103-109 M txn/s), 12 from LO, 14 (~1 ms) from 4*LO (LO = 1,024 for TO, 256
+// for MVCC, which aborts less) -- basic TO under a read-hot key otherwise retries in a
+// storm that burns 31-bit timestamps (cap 10 at theta=0.8: 1.4 M vs 4.9 M).
+// profiles/r01_probe_v6..v11, v18.
 template <int S>
-GC_DEV void abort_backoff(u32 gid, u32 restarts) {
-    constexpr u32 CAP = (S == CC_TO || S == CC_MVCC) ? 14u : 10u;
+GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
+    constexpr bool TS = S == CC_TO || S == CC_MVCC;
+    u32 CAP = 10u;
+    if (TS) {
+        const u64 n = atomicAdd(&p.ctl->pacing.v, 1ull);   // transactions backing off now
+        constexpr u64 LO = S == CC_TO ? 1024 : 256;   // MVCC aborts less: fewer back off at once
+        CAP = p.to_backoff_cap ? p.to_backoff_cap : (n < LO ? 10u : (n < 4 * LO ? 12u : 14u));
+    }
     const u32 sh = restarts < CAP ? restarts : CAP;
     const u32 cap = 64u << sh;
     u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % cap);
@@ -249,6 +259,7 @@ GC_DEV void abort_backoff(u32 gid, u32 restarts) {
         __nanosleep(s);
         d -= s;
     }
+    if (TS) atomicAdd(&p.ctl->pacing.v, (u64)-1ll);
 }
 
 // Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
@@ -278,7 +289,7 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         th.cw = nullptr;
         return;
     }
-    abort_backoff<S>(gid, restarts);
+    abort_backoff<S>(*th.p, gid, restarts);
 }
 
 // ------------------------------------------------------------------ queue (a6)

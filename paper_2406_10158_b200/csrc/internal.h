@@ -27,6 +27,7 @@ struct Ctl {
     Counter rank_head;  // GPUTx rank-pass claim counter
     Counter inflight;   // retry-batch appends in flight (sealing protocol)
     Counter events;     // CC_FLAG_EVENTS: event sequence counter
+    Counter pacing;     // TO/MVCC: transactions in retry backoff right now (adaptive cap)
 };
 // one event of the debug log: 24 bytes
 struct Event {
@@ -51,6 +52,8 @@ struct ExecParams {
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
     unsigned long long *arena;   // MVCC version nodes: ARENA_HDR header words + the row
+    uint32_t to_backoff_cap;     // TO/MVCC backoff cap exponent (0: adaptive); experiment
+                                 // knob, environment GCCTB_TO_BACKOFF_CAP
     unsigned long long mvcc_split;   // MVCC words: 0 = interleaved (lo, hi) pairs; else lo at
                                      // meta[r], hi at meta[mvcc_split + r] (CC_FLAG_MVCC_SPLIT)
     unsigned long long *ring;    // retry batch (compacted aborted ids), n_txn slots
