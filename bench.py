@@ -375,39 +375,48 @@ def launches_per_step(schemes, pipelined=False):
 
 
 def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xflags=0):
-    """Same metric through the public C-ABI with HOST buffers: every step imports the
-    batch from pinned host memory (cc_batch_import_ycsb, src_on_device=0), runs all
-    schemes, and reads each scheme's commit flags, commit positions and read outputs
-    back to pinned host memory."""
+    """Same metric through the public C-ABI with HOST buffers, pipelined as a serving loop
+    would be: every step's batch is imported from pinned host memory with
+    cc_batch_import_ycsb(CC_SRC_HOST_ASYNC) -- the copy of step i+1 overlaps step i's
+    execution -- and each scheme's commit flags, commit positions and read outputs are read
+    back to pinned host memory on a side stream as soon as that scheme's submit is done,
+    overlapping the next scheme.  The timed region covers every copy of every step."""
     import torch
-    pk = torch.from_numpy(keys).pin_memory()
-    po = torch.from_numpy(ops).pin_memory()
+    pk = [torch.from_numpy(keys).pin_memory() for _ in range(2)]   # double-buffered inputs
+    po = [torch.from_numpy(ops).pin_memory() for _ in range(2)]
     outs = {s: (torch.empty(args.batch, dtype=torch.uint8).pin_memory(),
                 torch.empty(args.batch, dtype=torch.int32).pin_memory(),
                 torch.empty(args.batch * args.ops, dtype=torch.int64).pin_memory()) for s in schemes}
+    d2h = torch.cuda.Stream(dev)
     n_steps = max(2, min(args.steps, 5))
 
-    def one():
-        b = db.import_ycsb(pk.numpy(), po.numpy(), args.ops)
-        if args.pipeline:
-            for s in schemes:
-                db.prepare(b, s, xflags)
-        with torch.cuda.stream(stream):
+    def run(n):
+        b = db.import_ycsb(pk[0], po[0], args.ops, async_host=True)
+        for i in range(n):
+            nxt = db.import_ycsb(pk[(i + 1) % 2], po[(i + 1) % 2], args.ops, async_host=True) if i + 1 < n else None
+            if args.pipeline:
+                for s in schemes:
+                    db.prepare(b, s, xflags)
             for s in schemes:
                 db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes,
                           flags=xflags)
-                c, p_, r = outs[s]
-                c.copy_(res[s].committed, non_blocking=True)
-                p_.copy_(res[s].commit_pos, non_blocking=True)
-                r.copy_(res[s].read_out, non_blocking=True)
-        db.sync()
-        b.free()
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                d2h.wait_event(ev)
+                with torch.cuda.stream(d2h):
+                    c, p_, r = outs[s]
+                    c.copy_(res[s].committed, non_blocking=True)
+                    p_.copy_(res[s].commit_pos, non_blocking=True)
+                    r.copy_(res[s].read_out, non_blocking=True)
+            db.sync()
+            d2h.synchronize()
+            b.free()
+            b = nxt
 
-    one()
+    run(1)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(n_steps):
-        one()
+    run(n_steps)
     barrier()
     el = time.perf_counter() - t0
     if world > 1:
@@ -416,10 +425,11 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xfla
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     h2d = keys.nbytes + ops.nbytes
-    d2h = len(schemes) * (args.batch * (1 + 4) + args.batch * args.ops * 8)
+    d2h_bytes = len(schemes) * (args.batch * (1 + 4) + args.batch * args.ops * 8)
     return {"value": n_steps * args.batch * len(schemes) * world / el, "unit": "txn/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n_steps,
-            "note": "host wall clock around import(H2D) + submit x schemes + D2H of results"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_bytes, "steps": n_steps,
+            "note": "host wall clock around n steps of async pinned H2D import + submit x schemes + D2H of "
+                    "results on a side stream (copies overlap execution)"}
 
 
 def run_tpcc_loopback(args, local):

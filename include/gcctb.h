@@ -152,7 +152,13 @@ cc_status cc_batch_gen_ycsb(cc_db db, const cc_ycsb_gen_desc *g, cc_batch *out);
 
 /* Import a YCSB-form batch: keys u32[n_txn*K] (primary keys of "usertable", sorted
  * ascending and distinct within each transaction), ops u8[n_txn*K] (bit7 = write,
- * bits 0..3 = field < 15).  KEY_NOT_FOUND surfaces at submit for unknown keys. */
+ * bits 0..3 = field < 15).  KEY_NOT_FOUND surfaces at submit for unknown keys.
+ * src_on_device: 0 host buffers, copied before return; 1 device buffers;
+ * CC_SRC_HOST_ASYNC (2) host buffers (pinned for a true overlap) copied on the db's copy
+ * stream without waiting, so the transfer overlaps work already queued on the db stream;
+ * the caller keeps them unchanged until the first cc_submit of the batch has completed
+ * (cc_sync).  Submits of the batch wait for its copy on the device. */
+#define CC_SRC_HOST_ASYNC 2
 cc_status cc_batch_import_ycsb(cc_db db, const uint32_t *keys, const uint8_t *ops,
                                uint32_t n_txn, uint32_t ops_per_txn, int src_on_device,
                                cc_batch *out);

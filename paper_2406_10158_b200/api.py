@@ -161,19 +161,31 @@ class DB:
         del keep
         return Batch(self, h)
 
-    def import_ycsb(self, keys, ops, K: int) -> Batch:
+    def import_ycsb(self, keys, ops, K: int, async_host: bool = False) -> Batch:
+        """keys/ops: device tensors, or host arrays / CPU tensors.  async_host: copy host
+        buffers on the copy stream without waiting (CC_SRC_HOST_ASYNC; pass pinned CPU
+        tensors and keep them unchanged until the batch's first submit has completed)."""
         h = ctypes.c_void_p()
-        if isinstance(keys, torch.Tensor):
+        keep = None
+        if isinstance(keys, torch.Tensor) and keys.is_cuda:
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
             st = G.lib().cc_batch_import_ycsb(self.h, keys.data_ptr(), ops.data_ptr(),
                                               keys.numel() // K, K, 1, ctypes.byref(h))
         else:
-            k = np.ascontiguousarray(keys, dtype=np.uint32)
-            o = np.ascontiguousarray(ops, dtype=np.uint8)
-            st = G.lib().cc_batch_import_ycsb(self.h, k.ctypes.data, o.ctypes.data, k.size // K, K,
-                                              0, ctypes.byref(h))
+            if isinstance(keys, torch.Tensor):
+                k, o = keys.contiguous(), ops.contiguous()
+                kp, op, n = k.data_ptr(), o.data_ptr(), k.numel()
+            else:
+                k = np.ascontiguousarray(keys, dtype=np.uint32)
+                o = np.ascontiguousarray(ops, dtype=np.uint8)
+                kp, op, n = k.ctypes.data, o.ctypes.data, k.size
+            keep = (k, o)
+            st = G.lib().cc_batch_import_ycsb(self.h, kp, op, n // K, K, G.CC_SRC_HOST_ASYNC if async_host else 0,
+                                              ctypes.byref(h))
         self._chk(st)
-        return Batch(self, h)
+        b = Batch(self, h)
+        b._keep = keep if async_host else None   # host buffers stay alive with the batch
+        return b
 
     # ----------------------------------------------------------- TPC-C
     def load_tpcc(self, warehouses: int, seed: int, max_txn: int, w_first: int = 0, w_count: int | None = None):

@@ -123,6 +123,8 @@ struct cc_db_s {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t prep_stream = nullptr;   // f-4: a3 of the next batch (cc_prepare)
+    cudaStream_t copy_stream = nullptr;   // asynchronous host imports (src_on_device == 2)
+    cudaEvent_t copy_after = nullptr;     // orders an async import after the db stream's work
     int rank = 0, world = 1;
     int num_sms = 148;
     std::string err;
@@ -262,6 +264,11 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
         delete db;
         return CC_ERR_CUDA;
     }
+    if (cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&db->copy_after, cudaEventDisableTiming) != cudaSuccess) {
+        delete db;
+        return CC_ERR_CUDA;
+    }
     if (dalloc(&db->ctl, sizeof(Ctl)) || dalloc(&db->stats_scratch, 8 * CC_STATS_WORDS) ||
         dalloc(&db->sticky_dev, 8)) {
         delete db;
@@ -331,6 +338,9 @@ cc_status cc_db_destroy(cc_db db) {
     cudaFree(db->sticky_dev);
     if (db->own_stream) cudaStreamDestroy(db->stream);
     cudaStreamDestroy(db->prep_stream);
+    cudaStreamSynchronize(db->copy_stream);
+    cudaStreamDestroy(db->copy_stream);
+    cudaEventDestroy(db->copy_after);
     delete db;
     return CC_OK;
 }
@@ -490,12 +500,12 @@ cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *d) {
     return CC_OK;
 }
 
-static cudaError_t batch_ready(cc_db db, cc_batch b) {
+static cudaError_t batch_ready(cc_db db, cc_batch b, cudaStream_t s = nullptr) {
     if (!b->ready) {
         cudaError_t e = cudaEventCreateWithFlags(&b->ready, cudaEventDisableTiming);
         if (e) return e;
     }
-    return cudaEventRecord(b->ready, db->stream);
+    return cudaEventRecord(b->ready, s ? s : db->stream);
 }
 
 constexpr size_t BATCH_POOL_MAX = 16;
@@ -571,6 +581,15 @@ cc_status cc_batch_import_ycsb(cc_db db, const uint32_t *keys, const uint8_t *op
     cc_batch b;
     cc_status st = new_batch(db, n_txn, K, &b);
     if (st) return st;
+    if (src_on_device == CC_SRC_HOST_ASYNC) {   // copy stream; overlaps the db stream's work
+        CUDA_TRY(db, cudaEventRecord(db->copy_after, db->stream));   // a pooled buffer's old readers
+        CUDA_TRY(db, cudaStreamWaitEvent(db->copy_stream, db->copy_after, 0));
+        CUDA_TRY(db, cudaMemcpyAsync(b->keys, keys, (size_t)n_txn * K * 4, cudaMemcpyHostToDevice, db->copy_stream));
+        CUDA_TRY(db, cudaMemcpyAsync(b->ops, ops, (size_t)n_txn * K, cudaMemcpyHostToDevice, db->copy_stream));
+        CUDA_TRY(db, batch_ready(db, b, db->copy_stream));
+        *out = b;
+        return CC_OK;
+    }
     const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CUDA_TRY(db, cudaMemcpyAsync(b->keys, keys, (size_t)n_txn * K * 4, kind, db->stream));
     CUDA_TRY(db, cudaMemcpyAsync(b->ops, ops, (size_t)n_txn * K, kind, db->stream));
@@ -891,6 +910,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (desc->wd > 5 || desc->bs < 1 || desc->bs > 32)
         return fail(db, CC_ERR_INVALID_ARG, "wd must be 0..5 and bs 1..32 (PAPER.md:480-484)");
     const bool is_tpcc = b->kind == KIND_TPCC;
+    if (b->ready) CUDA_TRY(db, cudaStreamWaitEvent(db->stream, b->ready, 0));   // async imports
     {
         const uint32_t L = desc->lanes_per_txn;
         if (is_tpcc ? !(L <= 1 || L == 4 || L == 8 || L == 16 || L == 32)

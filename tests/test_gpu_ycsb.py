@@ -413,3 +413,21 @@ def test_device_error_is_sticky_across_submits(c1):
     assert db.sync().commits == 1     # cleared after being reported
     bad.free()
     good.free()
+
+
+def test_import_async_host(c1, orc):
+    """CC_SRC_HOST_ASYNC: pinned host batches copied on the copy stream (overlapping queued
+    work; a pooled buffer's previous readers finish first) give the oracle's results."""
+    import torch
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    for seed in (61, 62, 63):
+        keys, ops = orc.ycsb_gen(seed, 1024, 1024, 4, 0.5, T, A)
+        pk, po = torch.from_numpy(keys).pin_memory(), torch.from_numpy(ops).pin_memory()
+        db.snapshot(False)
+        b = db.import_ycsb(pk, po, 4, async_host=True)
+        res = db.submit(b, "tictoc", wd=0, bs=32, lanes=4)
+        db.sync()
+        orc.check_ycsb("tictoc", S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+        b.free()
