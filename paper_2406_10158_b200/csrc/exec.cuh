@@ -262,6 +262,28 @@ GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
     if (TS) atomicAdd(&p.ctl->pacing.v, (u64)-1ll);
 }
 
+// GPUTx K-set gate: wait until K-set k-1 has completed.  K-sets complete
+// in order and ctl->kdone counts them (set by each set's last finisher), so a waiter knows
+// how far the frontier is: the next set polls tightly, sets further ahead sleep in
+// proportion to their distance instead of hammering the same few counters.
+GC_DEV bool kset_wait(Th &th, const ExecParams &p, u32 k) {
+    const u64 t0 = th.timing ? clk64() : 0;
+    bool ok = true;
+    while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1]) {
+        const u64 done = ld_relaxed(&p.ctl->kdone.v);
+        const u64 dist = k > done ? k - done : 1;
+        __nanosleep(dist <= 1 ? 32u : (dist >= 32 ? 8192u : 256u * (unsigned)dist));
+        if (dead(th)) { ok = false; break; }
+    }
+    if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
+    fence_acqrel();   // acquire: K-set k-1's installs happen-before our accesses
+    return ok;
+}
+GC_DEV void kset_done(const ExecParams &p, u32 k) {
+    const u32 old = atom_add_release32(&p.rank_done[k], 1u);
+    if (old + 1 == p.rank_count[k]) atomicMax(&p.ctl->kdone.v, (u64)k + 1);
+}
+
 // Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
 // no-wait / OCC semantics are unchanged -- until that lock is free (2PL holder count 0,
 // OCC lock bit clear), bounded, add a little jitter, and retry; otherwise use the
@@ -788,18 +810,13 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         return RES_OK;
     } else {   // GPUTx: K-set k runs after K-set k-1 completes; no CC inside
         const u32 k = p.rank_of[gid];
-        if (k > 0) {
-            Spin sp;
-            while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
-                if (!sp.wait(th)) return RES_FATAL;
-            fence_acqrel();
-        }
+        if (k > 0 && !kset_wait(th, p, k)) return RES_FATAL;
         for (u32 i = 0; i < n; i++) {
             u64 *row = WL::row(y, L[i]);
             rd<WL>(th, y, L[i], gid, i, row);
             if (L[i].w) inst<WL>(th, y, L[i], row);
         }
-        atom_add_release32(&p.rank_done[k], 1u);
+        kset_done(p, k);
         key_hi = 0;
         key_lo = gid;
         return RES_OK;
@@ -826,7 +843,7 @@ __global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, type
         const u32 gid = claim_work<S>(th, cl);
         if (gid == NO_TXN) break;
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
-            if (S == CC_GPUTX) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);
+            if (S == CC_GPUTX) kset_done(p, p.rank_of[gid]);
             continue;
         }
         u32 n;
@@ -1077,13 +1094,8 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
     } else {   // GPUTx
         const u32 k = p.rank_of[gid];
         int st = ST_DONE;
-        if (li == 0 && k > 0) {
-            Spin sp;
-            while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1])
-                if (!sp.wait(th)) { st = ST_ABORT; break; }
-            fence_acqrel();   // acquire: K-set k-1's installs happen-before ...
-        }
-        tile.sync();          // ... every lane's accesses (memory-ordering warp barrier)
+        if (li == 0 && k > 0 && !kset_wait(th, p, k)) st = ST_ABORT;
+        tile.sync();          // the leader's acquire orders every lane's accesses (warp barrier)
         if (tile.any(st != ST_DONE)) return RES_FATAL;
         if (act) {
             u64 *row = WL::row(y, L);
@@ -1091,7 +1103,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (L.w) inst<WL>(th, y, L, row);
         }
         tile.sync();   // every lane's install precedes the K-set release
-        if (li == 0) atom_add_release32(&p.rank_done[k], 1u);
+        if (li == 0) kset_done(p, k);
         key_hi = 0;
         key_lo = gid;
         return RES_OK;
@@ -1121,7 +1133,7 @@ __global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typena
         th.hot = tile.shfl(th.hot, 0);   // from the retry-batch entry (0 for a fresh id)
         if (gid == NO_TXN) break;
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
-            if (S == CC_GPUTX && li == 0) atom_add_release32(&p.rank_done[p.rank_of[gid]], 1u);
+            if (S == CC_GPUTX && li == 0) kset_done(p, p.rank_of[gid]);
             continue;
         }
         bool ok;

@@ -28,6 +28,7 @@ struct Ctl {
     Counter inflight;   // retry-batch appends in flight (sealing protocol)
     Counter events;     // CC_FLAG_EVENTS: event sequence counter
     Counter pacing;     // TO/MVCC: transactions in retry backoff right now (adaptive cap)
+    Counter kdone;      // GPUTx: K-sets completed so far (they complete in order)
 };
 // one event of the debug log: 24 bytes
 struct Event {

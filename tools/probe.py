@@ -32,6 +32,7 @@ def cell(db, b, s, a):
         commits += st.commits
     med = statistics.median(tots)
     return dict(txn_s=a.batch / (med / 1e3), abort_rate=aborts / commits, ms_total_median=med,
+                max_rank=int(st.max_rank),
                 ms_total_min=min(tots), ms_total_max=max(tots), ms_exec_median=statistics.median(execs))
 
 
