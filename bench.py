@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--write-frac", type=float, default=0.1)
     ap.add_argument("--wd", type=int, default=0)          # paper launch wd=0, bs=32
     ap.add_argument("--bs", type=int, default=32)
+    ap.add_argument("--launch", choices=["tuned", "fixed"], default="tuned",
+                    help="tuned: per-scheme warps per SM measured best at configs[1] theta=0.6 "
+                         "(profiles/r01_tune_bs.jsonl; one block per SM); fixed: --wd/--bs for "
+                         "every scheme with a full-occupancy grid")
     ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
     ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary"],
@@ -131,6 +135,53 @@ def algorithmic_bytes(n_txn, K, n_writes, scheme):
     return b
 
 
+def atomics_per_batch(n_txn, K, n_writes, scheme):
+    """SURVEY.md §8(d) 'Atomics per transaction' (committed attempts, one claim each):
+    2PL acquire + release per op and a lock-point ticket; TO one CAS per op + one per
+    write (pending bit) + ts; MVCC one per op + two per write + ts; Silo write lock +
+    release + serialization ticket; TicToc the same (rts extensions only when needed:
+    not counted); GPUTx the K-set completion counter; GaccO none (release stores and
+    polls only: no L2-atomic ceiling)."""
+    n, w = n_txn * K, n_writes
+    a = {"tpl_nw": 2 * n + n_txn, "tpl_wd": 2 * n + n_txn, "to": n + w + n_txn,
+         "mvcc": n + 2 * w + n_txn, "silo": 2 * w + n_txn, "tictoc": 2 * w + n_txn,
+         "gputx": n_txn, "gacco": 0}[scheme]
+    return a + (n_txn if a else 0)
+
+
+def hot_record_counts(keys, ops, n_rows):
+    """Accesses and writes to the most-accessed / most-written record of a batch (keys map
+    to records one-to-one)."""
+    import numpy as np
+    k = keys.astype(np.int64).ravel()
+    w = (ops.ravel() & 0x80) != 0
+    acc = np.bincount(k, minlength=1)
+    wr = np.bincount(k[w], minlength=1) if w.any() else np.zeros(1, np.int64)
+    return int(acc.max()), int(wr.max())
+
+
+def scheme_bounds(scheme, exec_ms, alg_bytes, atomics, acc_max, w_max, max_rank, ceil):
+    """The three memory-system fractions of SURVEY.md §8(d) for one exec launch, and the
+    one that binds (closest to its ceiling):
+      gather        algorithmic bytes / time vs the measured random-128 B-line gather rate;
+      l2_atomic     atomics / time vs measured distinct-address CAS/s (L2-resident);
+      serialization (conflicting accesses on the hottest record) x measured hand-off /
+                    time: GaccO serialises every access of an item,
+                    GPUTx every K-set (max_rank + 1 of them), the other
+                    schemes at least every write of the hot record."""
+    t = exec_ms / 1e3
+    out = {"gather_frac": alg_bytes / t / 1e9 / ceil["gather_gbs"] if ceil["gather_gbs"] > 0 else None,
+           "atomic_frac": atomics / t / ceil["cas_l2_per_s"] if atomics and ceil["cas_l2_per_s"] > 0 else None}
+    chain = acc_max if scheme == "gacco" else (max_rank + 1 if scheme == "gputx" else w_max)
+    h = ceil["handoff_row_ns"]
+    out["serial_chain"] = chain
+    out["serial_bound_ms"] = chain * h / 1e6 if h > 0 else None
+    out["serial_frac"] = chain * h / 1e9 / t if h > 0 else None
+    fr = {k[:-5]: v for k, v in out.items() if k.endswith("_frac") and v is not None}
+    out["binding"] = max(fr, key=fr.get) if fr else None
+    return out
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -201,10 +252,25 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# YCSB tile mode: warps per SM with the lowest exec time at the bench workload
+# (configs[1], theta 0.6, 2 seeds; profiles/r01_tune_bs.jsonl).  Fewer resident transactions
+# collide less (TO: 0.54 -> 0.44 ms) and GPUTx's K-set chain runs faster with fewer
+# waiting tiles (0.97 -> 0.73 ms).
+TUNED_BS = {"tpl_nw": 16, "tpl_wd": 16, "to": 16, "mvcc": 16, "silo": 16, "tictoc": 12, "gputx": 8, "gacco": 24}
+
+
+def launch_of(args, scheme, n_sms):
+    if args.launch == "tuned" and args.lanes > 1 and args.wd == 0:
+        return {"wd": 0, "bs": TUNED_BS[scheme], "grid": n_sms}
+    return {"wd": args.wd, "bs": args.bs, "grid": 0}
+
+
 def config_of(args, world):
     return {"workload": "ycsb_configs1_10Mrows_64Kx16", "rows": args.rows, "batch": args.batch,
             "ops_per_txn": args.ops, "theta": args.theta, "write_frac": args.write_frac,
             "schemes": args.schemes.split(","), "wd": args.wd, "bs": args.bs, "lanes_per_txn": args.lanes, "index": args.index,
+            "launch": ({s: launch_of(args, s, 148)["bs"] for s in args.schemes.split(",")} | {"grid": "1 block/SM"})
+            if args.launch == "tuned" and args.lanes > 1 and args.wd == 0 else "fixed (wd, bs), full-occupancy grid",
             "prep": "pipelined (cc_prepare on a second stream)" if args.pipeline else "inline",
             "parallelism": f"replicas{world}", "l2": "inputs larger than L2 (1.34 GB table, 168 MB CC words)"}
 
@@ -230,6 +296,7 @@ def run_ours(args, rank, world, local):
     A = inputs.scramble_mult(args.rows)
     res = {s: Result.alloc(args.batch, args.ops, dev, stream=db.stream) for s in schemes}
     stream = db.stream   # every library launch goes to this stream; events are recorded on it
+    LA = {s: launch_of(args, s, db.num_sms) for s in schemes}
 
     from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
     xflags = {"dense": 0, "tree": CC_FLAG_INDEX_TREE, "binary": CC_FLAG_INDEX_BINARY}[args.index]
@@ -244,7 +311,7 @@ def run_ours(args, rank, world, local):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
         prepare(b)
         for s in schemes:
-            db.submit(b, s, wd=args.wd, bs=args.bs, flags=xflags | (CC_FLAG_TIMING if timing else 0),
+            db.submit(b, s, **LA[s], flags=xflags | (CC_FLAG_TIMING if timing else 0),
                       result=res[s], watchdog_s=60, lanes=args.lanes)
         return b
 
@@ -293,10 +360,12 @@ def run_ours(args, rank, world, local):
     b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 999_999 + rank, T, A)
     bk, bo = b.export_ycsb()
     nw2 = int(((bo & 0x80) != 0).sum())
+    acc_max, w_max = hot_record_counts(bk, bo, args.rows)
+    ceil = db.roofline_probe() if rank == 0 else None   # untimed: memory-system ceilings
     exec_ms_total, alg_bytes_total = 0.0, 0
     for s in schemes:
         db.timing(reset=True)
-        db.submit(b, s, wd=args.wd, bs=args.bs, flags=xflags | CC_FLAG_TIMING, result=res[s], watchdog_s=60,
+        db.submit(b, s, **LA[s], flags=xflags | CC_FLAG_TIMING, result=res[s], watchdog_s=60,
                   lanes=args.lanes)
         db.sync()
         pm, _ = db.timing(reset=True)
@@ -305,6 +374,10 @@ def run_ours(args, rank, world, local):
         per[s]["txn_s"] = args.batch / (pm[4] / 1e3)
         ab = algorithmic_bytes(args.batch, args.ops, nw2, s)
         per[s]["exec_GBps"] = ab / (pm[2] / 1e3) / 1e9
+        if ceil is not None:
+            max_rank = int(res[s].stats.cpu().numpy().view(np.uint64)[4])
+            per[s]["bounds"] = scheme_bounds(s, pm[2], ab, atomics_per_batch(args.batch, args.ops, nw2, s),
+                                             acc_max, w_max, max_rank, ceil)
         exec_ms_total += pm[2]
         alg_bytes_total += ab
     # ---- e2e through the public API with host buffers
@@ -341,7 +414,14 @@ def run_ours(args, rank, world, local):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "exec_kernel (a4-a6), all schemes",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
-                         "exec_share_of_step": exec_share},
+                         "exec_share_of_step": exec_share,
+                         # the ceilings a random-access, atomic, hand-off
+                         # bound path actually meets (cc_roofline_probe), per scheme in
+                         # per_scheme[s]["bounds"]
+                         "ceilings": ceil,
+                         "frac_gather": achieved / ceil["gather_gbs"] if ceil and ceil["gather_gbs"] > 0 else None,
+                         "hot_record": {"accesses": acc_max, "writes": w_max},
+                         "binding": {s: per[s].get("bounds", {}).get("binding") for s in schemes}},
         }
         if not args.no_cpu_baseline and world >= 1:
             tps, done, el, sample = oracle_replay_timed(args, args.cpu_seconds)
@@ -398,7 +478,7 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xfla
                 for s in schemes:
                     db.prepare(b, s, xflags)
             for s in schemes:
-                db.submit(b, s, wd=args.wd, bs=args.bs, result=res[s], watchdog_s=60, lanes=args.lanes,
+                db.submit(b, s, **launch_of(args, s, db.num_sms), result=res[s], watchdog_s=60, lanes=args.lanes,
                           flags=xflags)
                 ev = torch.cuda.Event()
                 ev.record(stream)

@@ -390,6 +390,29 @@ cc_status cc_timing_read(cc_db db, double ms[5], uint64_t *n_submits, int reset)
  * save=0 restores.  Used to reset the db between measurement repetitions. */
 cc_status cc_snapshot(cc_db db, int save);
 
+/* Memory-system ceilings for the roofline fractions (SURVEY.md §8(d) "Which roofline
+ * bounds the path"; the north star's "achieved fraction of the HBM/L2-atomic roofline").
+ * Runs three microbenchmarks on the db stream and waits for them:
+ *   gather_gbs      random 128 B line reads (the row read of every access) over 1 GiB;
+ *   cas_l2_per_s    64-bit CAS on distinct random words of an L2-resident 16 MiB array;
+ *   cas_hbm_per_s   the same over 256 MiB (larger than L2, like the CC words at configs[1]);
+ *   handoff_row_ns  one hop of a token passed around one warp per SM: relaxed poll,
+ *                   acquire, 128 B row read, 2-word install, release -- the per-record
+ *                   hand-off that serialises conflicting accesses (GaccO queue, lock
+ *                   release -> next acquire);
+ *   handoff_ns      the bare token hop (poll + release) without the row.
+ * Allocates ~1.3 GiB of scratch for the call and frees it.  A hand-off figure of -1
+ * means the ring timed out (blocks not co-resident).  Errors: INVALID_ARG (null),
+ * OOM, CUDA. */
+typedef struct {
+    double gather_gbs;
+    double cas_l2_per_s;
+    double cas_hbm_per_s;
+    double handoff_row_ns;
+    double handoff_ns;
+} cc_roofline;
+cc_status cc_roofline_probe(cc_db db, cc_roofline *out);
+
 #ifdef __cplusplus
 }
 #endif

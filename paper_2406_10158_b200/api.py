@@ -124,6 +124,7 @@ class DB:
         G.check(None, L.cc_db_create(ctypes.byref(d), ctypes.byref(h)))
         self.h = h
         self.ycsb_rows = 0
+        self.num_sms = torch.cuda.get_device_properties(device).multi_processor_count
 
     def close(self):
         if self.h:
@@ -344,6 +345,13 @@ class DB:
         n = ctypes.c_uint64()
         self._chk(G.lib().cc_timing_read(self.h, ctypes.byref(ms), ctypes.byref(n), int(reset)))
         return list(ms), n.value
+
+    def roofline_probe(self) -> dict:
+        """Memory-system ceilings (cc_roofline_probe): random-line gather GB/s, distinct-
+        address CAS/s (L2-resident and > L2), per-record hand-off ns (with / without row)."""
+        r = G.cc_roofline()
+        self._chk(G.lib().cc_roofline_probe(self.h, ctypes.byref(r)))
+        return {k: getattr(r, k) for k, _ in r._fields_}
 
     def snapshot(self, save: bool):
         self._chk(G.lib().cc_snapshot(self.h, 1 if save else 0))

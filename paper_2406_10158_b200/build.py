@@ -8,11 +8,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgcctb.so")
-SOURCES = ["db.cu", "ycsb.cu", "prep.cu", "tpcc.cu", "part.cu"]
+SOURCES = ["db.cu", "ycsb.cu", "prep.cu", "tpcc.cu", "part.cu", "roof.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-diag-suppress", "177,550"]
+# experiments only (e.g. "-DGC_EXEC_MAXT=512 -DGC_EXEC_MINB=3"); the shipped build sets none
+FLAGS += os.environ.get("GCCTB_NVCC_EXTRA", "").split()
 
 
 def _deps():

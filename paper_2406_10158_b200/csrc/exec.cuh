@@ -22,6 +22,16 @@
 #include "common.cuh"
 #include "internal.h"
 
+// Executor launch bounds: one 1024-thread block per SM by default (64 registers, no
+// spills); the build can trade registers for resident transactions with
+// -DGC_EXEC_MAXT=512 -DGC_EXEC_MINB=3 (40 registers, 1536 threads per SM).
+#ifndef GC_EXEC_MAXT
+#define GC_EXEC_MAXT 1024
+#endif
+#ifndef GC_EXEC_MINB
+#define GC_EXEC_MINB 1
+#endif
+
 namespace gcctb {
 namespace cg = cooperative_groups;
 
@@ -264,15 +274,32 @@ GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
 
 // GPUTx K-set gate: wait until K-set k-1 has completed.  K-sets complete
 // in order and ctl->kdone counts them (set by each set's last finisher), so a waiter knows
-// how far the frontier is: the next set polls tightly, sets further ahead sleep in
-// proportion to their distance instead of hammering the same few counters.
+// how far the frontier is: the next set polls tightly, sets further ahead sleep about as
+// long as the K-sets in between take (~1.5 us each at least, the measured hand-off).
+// Thousands of waiters polling the one kdone word at sub-microsecond periods saturated
+// its L2 slice, which also serves the rank_done counters of the frontier.
+GC_DEV unsigned kset_sleep_ns(u64 dist) {
+    return dist <= 1 ? 32u : (dist >= 34 ? 50000u : 1500u * (unsigned)(dist - 1));
+}
+// wait until K-set k-1 is the frontier (every earlier K-set complete)
+GC_DEV bool kset_near(Th &th, const ExecParams &p, u32 k) {
+    const u64 t0 = th.timing ? clk64() : 0;
+    bool ok = true;
+    for (;;) {
+        const u64 done = ld_relaxed(&p.ctl->kdone.v);
+        if (done + 1 >= k) break;
+        __nanosleep(kset_sleep_ns(k - done));
+        if (dead(th)) { ok = false; break; }
+    }
+    if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
+    return ok;
+}
 GC_DEV bool kset_wait(Th &th, const ExecParams &p, u32 k) {
     const u64 t0 = th.timing ? clk64() : 0;
     bool ok = true;
     while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1]) {
         const u64 done = ld_relaxed(&p.ctl->kdone.v);
-        const u64 dist = k > done ? k - done : 1;
-        __nanosleep(dist <= 1 ? 32u : (dist >= 32 ? 8192u : 256u * (unsigned)dist));
+        __nanosleep(kset_sleep_ns(k > done ? k - done : 1));
         if (dead(th)) { ok = false; break; }
     }
     if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
@@ -824,7 +851,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
 }
 
 template <int S, class WL>
-__global__ void __launch_bounds__(1024, 1) exec_thread_kernel(ExecParams p, typename WL::Params y) {
+__global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel(ExecParams p, typename WL::Params y) {
     const u32 lane = threadIdx.x & 31u;
     if (lane >= (1u << p.wd)) return;   // idle lanes exit at once
     if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs
@@ -1094,7 +1121,14 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
     } else {   // GPUTx
         const u32 k = p.rank_of[gid];
         int st = ST_DONE;
-        if (li == 0 && k > 0 && !kset_wait(th, p, k)) st = ST_ABORT;
+        if (k > 0) {
+            // The rows were prefetched at claim time, often long before the gate opens, and
+            // the L2 has turned over since: fetch them again once K-set k-1 is the frontier,
+            // so the reads after the gate -- on the K-set chain's critical path -- hit L2.
+            if (li == 0 && !kset_near(th, p, k)) st = ST_ABORT;
+            if (tile.shfl(st, 0) == ST_DONE && act) WL::prefetch_access(p, y, L);
+            if (li == 0 && st == ST_DONE && !kset_wait(th, p, k)) st = ST_ABORT;
+        }
         tile.sync();          // the leader's acquire orders every lane's accesses (warp barrier)
         if (tile.any(st != ST_DONE)) return RES_FATAL;
         if (act) {
@@ -1111,7 +1145,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
 }
 
 template <int S, class WL, int G>
-__global__ void __launch_bounds__(1024, 1) exec_tile_kernel(ExecParams p, typename WL::Params y) {
+__global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(ExecParams p, typename WL::Params y) {
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const u32 li = tile.thread_rank();
     if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs

@@ -6,6 +6,7 @@
 // so one radix sort groups accesses per item with transaction ids ascending; segment
 // boundaries come from a head-flag prefix sum (the paper uses thrust sort + scan; we
 // use CUB from the toolkit).
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "exec.cuh"
@@ -111,7 +112,7 @@ template <int G>
 __global__ void __launch_bounds__(1024) gputx_rank_kernel(
     const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_id, const uint32_t *seg_start,
     const uint32_t *lw, uint32_t *rank, uint32_t n_txn, uint32_t K, Ctl *ctl,
-    u64 watchdog_ns) {
+    u64 watchdog_ns, uint32_t poll_cap_ns) {
     // a tile of G lanes per transaction, lane i resolves the predecessors of access i
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const uint32_t li = tile.thread_rank();
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
                             break;
                         }
                         __nanosleep(ns);
-                        ns = ns < 128 ? ns * 2 : 128;
+                        ns = ns < poll_cap_ns ? ns * 2 : poll_cap_ns;
                         ru[j] = ld_relaxed32(&rank[u[j]]);
                     }
                     if (u[j] != 0xFFFFFFFFu) r = max(r, ru[j] + 1);
@@ -201,7 +202,11 @@ int rank_kernel_grid() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gputx_rank_kernel<32>, 256, 0);
-    return (nb > 0 ? nb : 1) * sms;
+    // a quarter of the resident capacity: fewer transactions waiting on predecessors poll
+    // less, and the long chains resolve faster (configs[1] theta 0.6: rank pass 0.81 ->
+    // 0.73 ms; theta 0.8: 13.5 -> 6.6 ms; profiles/r01_gputx_rank_sweep.txt)
+    const int g = (nb > 0 ? nb : 1) * sms / 4;
+    return g > 0 ? g : 1;
 }
 
 static int bits_for(uint64_t x) {
@@ -255,12 +260,16 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     e = cub::DeviceScan::InclusiveScan(b.cub_tmp, bytes, b.lw, b.head_flag, cub::Max(), (int)n, s);
     if (e) return e;
     fill_u32_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank, RANK_UNSET, p.n_txn);
+    // experiment knobs (environment): poll cap and a grid divisor for the rank pass
+    static const uint32_t poll_cap = getenv("GCCTB_RANK_POLL_NS") ? (uint32_t)atoi(getenv("GCCTB_RANK_POLL_NS")) : 512u;
+    static const int grid_div = getenv("GCCTB_RANK_GRID_DIV") ? atoi(getenv("GCCTB_RANK_GRID_DIV")) : 1;
+    if (grid_div > 1) grid = grid / grid_div > 0 ? grid / grid_div : 1;
     if (p.K <= 16)
         gputx_rank_kernel<16><<<grid, rank_block, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
-                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
+                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns, poll_cap);
     else
         gputx_rank_kernel<32><<<grid, rank_block, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
-                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns);
+                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns, poll_cap);
     iota_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.gid_in, p.n_txn);
     bytes = b.cub_bytes;
     e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.rank, b.rank_sorted, b.gid_in,

@@ -86,6 +86,12 @@ class cc_stats(ctypes.Structure):
                 ("sm_clock_khz", ctypes.c_uint64)]
 
 
+class cc_roofline(ctypes.Structure):
+    _fields_ = [("gather_gbs", ctypes.c_double), ("cas_l2_per_s", ctypes.c_double),
+                ("cas_hbm_per_s", ctypes.c_double), ("handoff_row_ns", ctypes.c_double),
+                ("handoff_ns", ctypes.c_double)]
+
+
 _lib = None
 
 # name -> (restype, argtypes)
@@ -133,6 +139,7 @@ _SIGS = {
     "cc_part_decide": (ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "cc_part_commit": (ctypes.c_int, [_P, _P, _P, ctypes.c_uint64]),
     "cc_part_next": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+    "cc_roofline_probe": (ctypes.c_int, [_P, ctypes.POINTER(cc_roofline)]),
 }
 
 TPCC_TX_WORDS = 40
