@@ -400,7 +400,9 @@ cc_status cc_snapshot(cc_db db, int save);
  *                   acquire, 128 B row read, 2-word install, release -- the per-record
  *                   hand-off that serialises conflicting accesses (GaccO queue, lock
  *                   release -> next acquire);
- *   handoff_ns      the bare token hop (poll + release) without the row.
+ *   handoff_ns      the bare token hop (poll + release) without the row;
+ *   handoff_acq_row_ns  handoff_row_ns with ld.acquire polls instead of relaxed polls
+ *                   followed by one fence.acq_rel (the executor's wait idiom).
  * Allocates ~1.3 GiB of scratch for the call and frees it.  A hand-off figure of -1
  * means the ring timed out (blocks not co-resident).  Errors: INVALID_ARG (null),
  * OOM, CUDA. */
@@ -410,6 +412,7 @@ typedef struct {
     double cas_hbm_per_s;
     double handoff_row_ns;
     double handoff_ns;
+    double handoff_acq_row_ns;
 } cc_roofline;
 cc_status cc_roofline_probe(cc_db db, cc_roofline *out);
 

@@ -1349,13 +1349,14 @@ cc_status cc_roofline_probe(cc_db db, cc_roofline *out) {
     CHECK_DB(db);
     if (!out) return fail(db, CC_ERR_INVALID_ARG, "null output");
     CUDA_TRY(db, cudaStreamSynchronize(db->stream));
-    double v[5] = {0, 0, 0, 0, 0};
+    double v[6] = {0, 0, 0, 0, 0, 0};
     CUDA_TRY(db, roofline_probe(db->stream, db->num_sms, v));
     out->gather_gbs = v[0];
     out->cas_l2_per_s = v[1];
     out->cas_hbm_per_s = v[2];
     out->handoff_row_ns = v[3];
     out->handoff_ns = v[4];
+    out->handoff_acq_row_ns = v[5];
     return CC_OK;
 }
 

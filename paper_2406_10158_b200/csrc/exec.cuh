@@ -272,6 +272,15 @@ GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
     if (TS) atomicAdd(&p.ctl->pacing.v, (u64)-1ll);
 }
 
+// Waits on a hand-off chain (GaccO turn, GPUTx K-set gate) poll with ld.acquire and need
+// no fence after the wait: the fence.acq_rel that used to follow relaxed polls cost ~0.3 us
+// per hop (ring microbenchmark 1.48 -> 1.17 us; GaccO configs[1] theta 0.6 1.28 ->
+// 1.04 ms, theta 0.8 19.1 -> 15.3 ms; profiles/r01_gacco_poll.txt).  GC_GACCO_SPIN caps
+// the sleep between polls.
+#ifndef GC_GACCO_SPIN
+#define GC_GACCO_SPIN 32
+#endif
+
 // GPUTx K-set gate: wait until K-set k-1 has completed.  K-sets complete
 // in order and ctl->kdone counts them (set by each set's last finisher), so a waiter knows
 // how far the frontier is: the next set polls tightly, sets further ahead sleep about as
@@ -297,13 +306,14 @@ GC_DEV bool kset_near(Th &th, const ExecParams &p, u32 k) {
 GC_DEV bool kset_wait(Th &th, const ExecParams &p, u32 k) {
     const u64 t0 = th.timing ? clk64() : 0;
     bool ok = true;
-    while (ld_relaxed32(&p.rank_done[k - 1]) < p.rank_count[k - 1]) {
+    // acquire polls: the one that sees K-set k-1 complete orders its installs before our
+    // accesses (no fence after the wait)
+    while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1]) {
         const u64 done = ld_relaxed(&p.ctl->kdone.v);
         __nanosleep(kset_sleep_ns(k > done ? k - done : 1));
         if (dead(th)) { ok = false; break; }
     }
     if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
-    fence_acqrel();   // acquire: K-set k-1's installs happen-before our accesses
     return ok;
 }
 GC_DEV void kset_done(const ExecParams &p, u32 k) {
@@ -823,10 +833,9 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 i = 0; i < n; i++) {
             const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
             u32 *cur = &p.cursor[seg];
-            Spin sp(32);   // the hand-off chain on a hot item is GaccO's critical path
-            while (ld_relaxed32(cur) != pos)   // relaxed polls: no L1 invalidation per poll
+            Spin sp(GC_GACCO_SPIN);   // the hand-off chain on a hot item is GaccO's critical path
+            while (ld_acquire32(cur) != pos)   // the poll that sees our turn is the acquire
                 if (!sp.wait(th)) return RES_FATAL;
-            fence_acqrel();                    // acquire once the turn is ours
             u64 *row = WL::row(y, L[i]);
             rd<WL>(th, y, L[i], gid, i, row);
             if (L[i].w) inst<WL>(th, y, L[i], row);
@@ -1103,11 +1112,10 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             const u64 a = (u64)gid * p.K + li;
             const u32 seg = p.acc_seg[a], pos = p.acc_pos[a];
             u32 *cur = &p.cursor[seg];
-            Spin sp(32);   // the hand-off chain on a hot item is GaccO's critical path
-            while (ld_relaxed32(cur) != pos)   // relaxed polls: no L1 invalidation per poll
+            Spin sp(GC_GACCO_SPIN);   // the hand-off chain on a hot item is GaccO's critical path
+            while (ld_acquire32(cur) != pos)   // the poll that sees our turn is the acquire
                 if (!sp.wait(th)) { st = ST_ABORT; break; }
             if (st == ST_DONE) {
-                fence_acqrel();                // acquire once the turn is ours
                 u64 *row = WL::row(y, L);
                 rd<WL>(th, y, L, gid, li, row);
                 if (L.w) inst<WL>(th, y, L, row);

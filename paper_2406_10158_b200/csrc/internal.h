@@ -210,7 +210,8 @@ cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32
                             const unsigned long long *T, uint64_t mult, Ctl *ctl,
                             cudaStream_t s);
 
-// roof.cu: out = {gather GB/s, CAS/s L2-resident, CAS/s > L2, hand-off ns (row), hop ns}
-cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[5]);
+// roof.cu: out = {gather GB/s, CAS/s L2-resident, CAS/s > L2, hand-off ns (row), hop ns,
+//                 hand-off ns (row, acquire polls)}
+cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[6]);
 
 }  // namespace gcctb

@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
         if (tile.any(fail)) return;
         r = cg::reduce(tile, r, cg::greater<uint32_t>());
         if (li == 0) {
-            st_release32(&rank[gid], r);
+            // relaxed: readers use only the value itself (nothing is published through it),
+            // so the MEMBAR of a release store would only lengthen the chain
+            st_relaxed32(&rank[gid], r);
             atomicMax(&ctl->max_rank.v, (u64)r);
         }
     }

@@ -72,21 +72,22 @@ __global__ void roof_cas_kernel(u64 *words, u64 word_mask, u32 iters, u64 *sink)
 
 // one warp per block, one block per SM; lane 0 of block j moves at token values
 // j, j + G, j + 2G, ...
-__global__ void roof_handoff_kernel(u32 *token, u64 *row, u32 rounds, int with_row, u64 timeout_ns,
-                                    u64 *sink) {
+// acq_poll: poll with ld.acquire (no separate fence) instead of relaxed polls + fence
+__global__ void roof_handoff_kernel(u32 *token, u64 *row, u32 rounds, int with_row, int acq_poll,
+                                    u64 timeout_ns, u64 *sink) {
     if (threadIdx.x != 0) return;
     const u64 deadline_ns = globaltimer_ns() + timeout_ns;
     const u32 G = gridDim.x, j = blockIdx.x;
     u64 acc = 0;
     for (u32 r = 0; r < rounds; r++) {
         const u32 turn = r * G + j;
-        while (ld_relaxed32(token) != turn) {
+        while ((acq_poll ? ld_acquire32(token) : ld_relaxed32(token)) != turn) {
             if (globaltimer_ns() > deadline_ns) {
                 sink[1] = 1;   // timed out (blocks not co-resident)
                 return;
             }
         }
-        fence_acqrel();
+        if (!acq_poll) fence_acqrel();
         if (with_row) {
             u64 v[16];
 #pragma unroll
@@ -111,8 +112,8 @@ static float time_ms(cudaStream_t s, cudaEvent_t a, cudaEvent_t b) {
 }
 
 // out[0] gather GB/s, out[1] CAS/s (L2-resident), out[2] CAS/s (> L2), out[3] hand-off
-// ns per hop with the row, out[4] bare token hop ns.  Scratch: 1 GiB + 256 MiB.
-cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[5]) {
+// ns per hop with the row, out[4] bare token hop ns, out[5] row hop with acquire polls.  Scratch: 1 GiB + 256 MiB.
+cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[6]) {
     const u64 gather_bytes = 1ull << 30, l2_words = 2ull << 20, hbm_words = 32ull << 20;
     u64 *buf = nullptr, *words = nullptr, *sink = nullptr, *row = nullptr;
     u32 *token = nullptr;
@@ -148,14 +149,15 @@ cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[5]) {
             cudaEventRecord(b, s);
             out[1 + v] = (double)threads * iters * CAS_ILP / (time_ms(s, a, b) * 1e-3);
         }
-        for (int v = 0; v < 2; v++) {
+        const int idx[3] = {3, 4, 5};
+        for (int v = 0; v < 3; v++) {   // row + fence, bare hop, row + acquire polls
             const u32 rounds = 40;
             cudaMemsetAsync(token, 0, 4, s);
             cudaEventRecord(a, s);
             // 2 s bound: the ring needs its blocks co-resident (one warp per SM is)
-            roof_handoff_kernel<<<num_sms, 32, 0, s>>>(token, row, rounds, v == 0, 2000000000ull, sink);
+            roof_handoff_kernel<<<num_sms, 32, 0, s>>>(token, row, rounds, v != 1, v == 2, 2000000000ull, sink);
             cudaEventRecord(b, s);
-            out[3 + v] = time_ms(s, a, b) * 1e6 / ((double)rounds * num_sms);
+            out[idx[v]] = time_ms(s, a, b) * 1e6 / ((double)rounds * num_sms);
         }
     }
     e = cudaGetLastError();
@@ -163,7 +165,7 @@ cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[5]) {
         u64 h[2] = {0, 0};
         cudaMemcpyAsync(h, sink, 16, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        if (h[1]) out[3] = out[4] = -1.0;   // ring timed out: no hand-off figure
+        if (h[1]) out[3] = out[4] = out[5] = -1.0;   // ring timed out: no hand-off figure
     }
 done:
     cudaStreamSynchronize(s);

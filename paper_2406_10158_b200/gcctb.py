@@ -89,7 +89,7 @@ class cc_stats(ctypes.Structure):
 class cc_roofline(ctypes.Structure):
     _fields_ = [("gather_gbs", ctypes.c_double), ("cas_l2_per_s", ctypes.c_double),
                 ("cas_hbm_per_s", ctypes.c_double), ("handoff_row_ns", ctypes.c_double),
-                ("handoff_ns", ctypes.c_double)]
+                ("handoff_ns", ctypes.c_double), ("handoff_acq_row_ns", ctypes.c_double)]
 
 
 _lib = None
