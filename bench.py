@@ -47,7 +47,7 @@ def parse():
                          "every scheme with a full-occupancy grid")
     ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
-    ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary"],
+    ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary", "eytz"],
                     help="dense = direct addressing on the dense YCSB key range (default); tree = cache-line "
                          "search tree over the sorted keys; binary = PAPER.md:344 (identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -173,7 +173,9 @@ def scheme_bounds(scheme, exec_ms, alg_bytes, atomics, acc_max, w_max, max_rank,
     out = {"gather_frac": alg_bytes / t / 1e9 / ceil["gather_gbs"] if ceil["gather_gbs"] > 0 else None,
            "atomic_frac": atomics / t / ceil["cas_l2_per_s"] if atomics and ceil["cas_l2_per_s"] > 0 else None}
     chain = acc_max if scheme == "gacco" else (max_rank + 1 if scheme == "gputx" else w_max)
-    h = ceil["handoff_row_ns"]
+    # the executor's waits poll with ld.acquire: the faster of the two measured idioms
+    h = min(x for x in (ceil["handoff_row_ns"], ceil.get("handoff_acq_row_ns", -1), float("inf")) if x > 0)
+    h = h if h != float("inf") else -1
     out["serial_chain"] = chain
     out["serial_bound_ms"] = chain * h / 1e6 if h > 0 else None
     out["serial_frac"] = chain * h / 1e9 / t if h > 0 else None
@@ -299,7 +301,8 @@ def run_ours(args, rank, world, local):
     LA = {s: launch_of(args, s, db.num_sms) for s in schemes}
 
     from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
-    xflags = {"dense": 0, "tree": CC_FLAG_INDEX_TREE, "binary": CC_FLAG_INDEX_BINARY}[args.index]
+    xflags = {"dense": 0, "tree": CC_FLAG_INDEX_TREE, "binary": CC_FLAG_INDEX_BINARY,
+              "eytz": 0x1000}[args.index]   # CC_FLAG_INDEX_EYTZ
 
     def prepare(b):
         """f-4: GPUTx / GaccO a3 on the prep stream, overlapping the other schemes' execution."""
@@ -435,7 +438,8 @@ def run_ours(args, rank, world, local):
 
 def config_key(args):
     return (f"ycsb rows={args.rows} batch={args.batch} K={args.ops} theta={args.theta} W={args.write_frac} "
-            f"wd={args.wd} bs={args.bs} lanes={args.lanes} index={args.index}")
+            f"wd={args.wd} bs={args.bs} lanes={args.lanes} index={args.index}"
+            + (" launch=tuned" if args.launch == "tuned" and args.lanes > 1 and args.wd == 0 else ""))
 
 
 def launches_per_step(schemes, pipelined=False):

@@ -108,7 +108,9 @@ cc_status cc_table_info(cc_db db, uint32_t table_id, uint64_t *rows, uint32_t *r
  * row_ids[i] < rows(table).  A lookup returns the lower-bound match of the paper's binary
  * search; when the keys form a dense range k0..k0+n-1 it is resolved by
  * direct addressing (no probe), else by a cache-line search tree over the same sorted
- * array; CC_FLAG_INDEX_BINARY / CC_FLAG_INDEX_TREE force a method.
+ * array; CC_FLAG_INDEX_BINARY / CC_FLAG_INDEX_TREE /
+ * CC_FLAG_INDEX_EYTZ force a method (the Eytzinger copy of the keys and row ids is built
+ * with the index: 2 x 2^ceil(log2(n+1)) u64).
  * INVALID_ARG unless strictly ascending.  *index_id receives the id. */
 cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_keys,
                           const uint64_t *row_ids, uint64_t n, int src_on_device,
@@ -117,7 +119,8 @@ cc_status cc_index_create(cc_db db, uint32_t table_id, const uint64_t *sorted_ke
 /* Batch index lookup (SPEC.md:47 index_lookup): rows_out[i] = row id of keys[i], or
  * 2^64-1 when the key is absent (KeyNotFound).  keys / rows_out are device
  * arrays of n u64 (caller-owned).  flags: CC_FLAG_INDEX_BINARY selects the paper's
- * binary search, CC_FLAG_INDEX_TREE the cache-line tree, otherwise direct addressing on
+ * binary search, CC_FLAG_INDEX_TREE the cache-line tree, CC_FLAG_INDEX_EYTZ the
+ * Eytzinger layout, otherwise direct addressing on
  * a dense key range and the tree elsewhere; results are identical.  Async. */
 cc_status cc_index_lookup(cc_db db, uint32_t index_id, const uint64_t *keys, uint64_t n,
                           uint64_t *rows_out, uint32_t flags);
@@ -246,6 +249,10 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         instead of Table II's interleaved 16 B per record */
 #define CC_FLAG_INDEX_TREE 0x100u    /* force the cache-line search tree even on a dense key
                                         range (default there: direct addressing, key - k0) */
+#define CC_FLAG_INDEX_EYTZ 0x1000u   /* index lookups in the Eytzinger (BFS) layout of the same
+                                        sorted keys: a branch-free
+                                        descent over a complete binary tree padded to 2^h - 1
+                                        keys; same lower-bound result as the binary search */
 
 typedef struct {
     cc_scheme scheme;

@@ -230,8 +230,9 @@ class DB:
 
     def index_lookup(self, index_id: int, keys, method: str = "auto") -> np.ndarray:
         """method: "auto" (direct addressing on a dense key range, else the tree), "tree",
-        or "binary"; all return the same rows."""
-        flags = {"auto": 0, "tree": G.CC_FLAG_INDEX_TREE, "binary": G.CC_FLAG_INDEX_BINARY}[method]
+        "eytz" (Eytzinger layout) or "binary"; all return the same rows."""
+        flags = {"auto": 0, "tree": G.CC_FLAG_INDEX_TREE, "binary": G.CC_FLAG_INDEX_BINARY,
+                 "eytz": G.CC_FLAG_INDEX_EYTZ}[method]
         dev = torch.device("cuda", self.device)
         with torch.cuda.stream(self.stream):
             k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)).to(dev)

@@ -40,12 +40,15 @@ struct Index {
     std::vector<uint64_t> lens;
     int dense = 0;   // 0, IDX_DENSE (keys k0..k0+n-1) or IDX_DENSE_ID (and row id == position)
     u64 k0 = 0;
+    u64 *eytz_keys = nullptr, *eytz_rows = nullptr;   // Eytzinger copy, 1-based (f-3)
+    uint64_t eytz_n = 0;                              // 2^h - 1
 };
 
 // Lookup mode for a submit / lookup: forced by the flags, else direct addressing on a
 // dense key range, else the cache-line tree (all return the same rows, f-3).
 static int index_mode(const Index &ix, uint32_t flags) {
     if (flags & CC_FLAG_INDEX_BINARY) return IDX_BINARY;
+    if (flags & CC_FLAG_INDEX_EYTZ) return IDX_EYTZ;
     if ((flags & CC_FLAG_INDEX_TREE) || !ix.dense) return IDX_TREE;
     return ix.dense;
 }
@@ -70,8 +73,17 @@ static cudaError_t build_tree(Index &ix, cudaStream_t s) {
         n_in = nodes;
         padded = out_padded;
     }
+    // Eytzinger layout of the same keys: a complete tree of 2^h - 1 slots (1-based)
+    int h = 1;
+    while (((1ull << h) - 1) < ix.n) h++;
+    ix.eytz_n = (1ull << h) - 1;
+    cudaError_t e = cudaMalloc((void **)&ix.eytz_keys, (ix.eytz_n + 1) * 8);
+    if (!e) e = cudaMalloc((void **)&ix.eytz_rows, (ix.eytz_n + 1) * 8);
+    if (!e) e = launch_eytz_build(ix.keys, ix.rowids, ix.n, h, ix.eytz_keys, ix.eytz_rows, s);
+    if (e) return e;
     return cudaStreamSynchronize(s);
 }
+
 
 static TreeIndex tree_of(const Index &ix) {
     TreeIndex t{};
@@ -83,6 +95,18 @@ static TreeIndex tree_of(const Index &ix) {
         t.len[k + 1] = ix.lens[k + 1];
     }
     return t;
+}
+
+static void index_params(const Index &ix, uint32_t flags, YcsbParams &y) {
+    y.idx_keys = ix.keys;
+    y.idx_rows = ix.rowids;
+    y.idx_n = ix.n;
+    y.tree = tree_of(ix);
+    y.mode = index_mode(ix, flags);
+    y.idx_k0 = ix.k0;
+    y.eytz_keys = ix.eytz_keys;
+    y.eytz_rows = ix.eytz_rows;
+    y.eytz_n = ix.eytz_n;
 }
 
 struct cc_batch_s {
@@ -313,6 +337,8 @@ cc_status cc_db_destroy(cc_db db) {
         cudaFree(i.keys);
         cudaFree(i.rowids);
         for (u64 *l : i.levels) cudaFree(l);
+        cudaFree(i.eytz_keys);
+        cudaFree(i.eytz_rows);
     }
     for (void *p : db->snap) cudaFree(p);
     cudaStreamSynchronize(db->prep_stream);
@@ -464,12 +490,7 @@ cc_status cc_index_lookup(cc_db db, uint32_t index_id, const uint64_t *keys, uin
         return fail(db, CC_ERR_INVALID_ARG, "cc_index_lookup: bad args");
     const Index &ix = db->indexes[index_id];
     YcsbParams y{};
-    y.idx_keys = ix.keys;
-    y.idx_rows = ix.rowids;
-    y.idx_n = ix.n;
-    y.tree = tree_of(ix);
-    y.mode = index_mode(ix, flags);
-    y.idx_k0 = ix.k0;
+    index_params(ix, flags, y);
     CUDA_TRY(db, launch_index_lookup(y, (const u64 *)keys, n, (u64 *)rows_out, db->stream));
     return CC_OK;
 }
@@ -890,12 +911,7 @@ static cc_status wl_params(cc_db db, cc_batch b, uint32_t flags, YcsbParams &y, 
         const Index &ix = db->indexes[db->ycsb_index];
         y.keys = b->keys;
         y.ops = b->ops;
-        y.idx_keys = ix.keys;
-        y.idx_rows = ix.rowids;
-        y.idx_n = ix.n;
-        y.tree = tree_of(ix);
-        y.mode = index_mode(ix, flags);
-        y.idx_k0 = ix.k0;
+        index_params(ix, flags, y);
         y.rows = (u64 *)t.d;
         y.n_rows = t.rows;
     }

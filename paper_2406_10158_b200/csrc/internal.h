@@ -96,7 +96,7 @@ constexpr int IDX_MAX_LEVELS = 10;
 // Lookup modes; every mode returns the same lower-bound result for the same index.
 // Dense modes (f-3 direct addressing) apply when the keys are k0, k0+1, ..., k0+n-1:
 // the position is key - k0, no probe at all; IDX_DENSE_ID also has row id == position.
-enum { IDX_TREE = 0, IDX_BINARY = 1, IDX_DENSE = 2, IDX_DENSE_ID = 3 };
+enum { IDX_TREE = 0, IDX_BINARY = 1, IDX_DENSE = 2, IDX_DENSE_ID = 3, IDX_EYTZ = 4 };
 struct TreeIndex {
     const unsigned long long *lv[IDX_MAX_LEVELS];
     unsigned long long len[IDX_MAX_LEVELS];   // padded lengths (multiples of 16)
@@ -111,6 +111,9 @@ struct YcsbParams {
     const unsigned long long *idx_rows;
     unsigned long long idx_n;
     TreeIndex tree;              // same keys, cache-line tree layout (f-3)
+    const unsigned long long *eytz_keys;   // same keys in Eytzinger (BFS) order, 1-based,
+    const unsigned long long *eytz_rows;   // padded with ~0 to 2^h - 1 entries (f-3)
+    unsigned long long eytz_n;             // 2^h - 1
     int mode;                    // IDX_TREE / IDX_BINARY (the paper's) / IDX_DENSE / IDX_DENSE_ID
     unsigned long long idx_k0;   // first key (dense modes)
     unsigned long long *rows;    // 16 x u64 per row
@@ -200,6 +203,8 @@ cudaError_t launch_ycsb_init_rows(unsigned long long *rows, uint64_t first, uint
                                   uint64_t seed, cudaStream_t s);
 cudaError_t launch_identity_index(unsigned long long *keys, unsigned long long *rows,
                                   uint64_t n, cudaStream_t s);
+cudaError_t launch_eytz_build(const unsigned long long *keys, const unsigned long long *rows, uint64_t n,
+                              int h, unsigned long long *ekeys, unsigned long long *erows, cudaStream_t s);
 cudaError_t launch_tree_level(const unsigned long long *in, uint64_t n_in, unsigned long long *out,
                               uint64_t n_out_padded, cudaStream_t s);
 cudaError_t launch_index_lookup(const YcsbParams &y, const unsigned long long *keys, uint64_t n,

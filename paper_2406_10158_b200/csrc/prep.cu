@@ -168,8 +168,7 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
         if (li == 0) {
             // relaxed: readers use only the value itself (nothing is published through it),
             // so the MEMBAR of a release store would only lengthen the chain
-            st_relaxed32(&rank[gid], r);
-            atomicMax(&ctl->max_rank.v, (u64)r);
+            st_relaxed32(&rank[gid], r);   // (max_rank: from the rank sort, not an atomic per txn)
         }
     }
 }
@@ -192,11 +191,12 @@ __global__ void rank_bounds_kernel(const uint32_t *rs, uint32_t *start, uint32_t
     if (p == 0 || rs[p - 1] != r) { start[r] = p; done[r] = 0; }
 }
 __global__ void rank_count_kernel(const uint32_t *rs, const uint32_t *start, uint32_t *count,
-                                  uint32_t n) {
+                                  uint32_t n, Ctl *ctl) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const uint32_t r = rs[p];
     if (p == n - 1 || rs[p + 1] != r) count[r] = p + 1 - start[r];
+    if (p == n - 1) ctl->max_rank.v = r;   // ranks sorted ascending: the last is the max
 }
 
 int rank_kernel_grid() {
@@ -280,7 +280,7 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     rank_bounds_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank_sorted, b.rank_start,
                                                                  b.rank_count, b.rank_done, p.n_txn);
     rank_count_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank_sorted, b.rank_start,
-                                                                b.rank_count, p.n_txn);
+                                                                b.rank_count, p.n_txn, p.ctl);
     return cudaGetLastError();
 }
 

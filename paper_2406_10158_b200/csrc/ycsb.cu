@@ -27,10 +27,23 @@ struct YcsbWL {
     // the row or ~0 for KeyNotFound.  Dense key range: direct addressing
     // (f-3); else descend the cache-line tree (one 128 B node of 16 keys per level:
     // count keys < key); CC_FLAG_INDEX_BINARY: the paper's branch-free binary search.
+    static GC_DEV bool is_dense(int mode) { return mode == IDX_DENSE || mode == IDX_DENSE_ID; }
     static GC_DEV u64 lookup(const YcsbParams &y, u64 key) {
-        if (y.mode >= IDX_DENSE) return dense_lookup(y, key);
+        if (is_dense(y.mode)) return dense_lookup(y, key);
         if (y.mode == IDX_TREE) return tree_lookup(y, key);
+        if (y.mode == IDX_EYTZ) return eytz_lookup(y, key);
         return binary_lookup(y, key);
+    }
+    // Eytzinger layout (f-3): node i (1-based) has children 2i, 2i+1; descend branch-free
+    // (i = 2i + [key > node]) to below the leaves, then strip the trailing right turns:
+    // the remaining node is the lower bound (0: every key is smaller).  The top levels are
+    // shared by every lookup and stay cached; one dependent load per level below them.
+    static GC_DEV u64 eytz_lookup(const YcsbParams &y, u64 key) {
+        u64 i = 1;
+        while (i <= y.eytz_n) i = 2 * i + (__ldg(y.eytz_keys + i) < key);
+        i >>= __ffsll((long long)~i);
+        if (i == 0 || __ldg(y.eytz_keys + i) != key) return ~0ull;
+        return __ldg(y.eytz_rows + i);
     }
     static GC_DEV u64 dense_lookup(const YcsbParams &y, u64 key) {
         const u64 pos = key - y.idx_k0;   // wraps above idx_n for key < k0
@@ -93,10 +106,10 @@ struct YcsbWL {
             b[i] = y.idx_keys;
         }
         if (p.acc_rec) return p.K;
-        if (y.mode >= IDX_DENSE) {
+        if (is_dense(y.mode) || y.mode == IDX_EYTZ) {
             bool ok = true;
             for (int i = 0; i < (int)p.K; i++) {
-                const u64 r = dense_lookup(y, key[i]);
+                const u64 r = is_dense(y.mode) ? dense_lookup(y, key[i]) : eytz_lookup(y, key[i]);
                 ok &= r != ~0ull;
                 L[i].rec = (u32)r;
             }
@@ -412,6 +425,26 @@ __global__ void index_lookup_kernel(YcsbParams y, const u64 *keys, uint64_t n, u
 }
 cudaError_t launch_index_lookup(const YcsbParams &y, const u64 *keys, uint64_t n, u64 *out, cudaStream_t s) {
     if (n) index_lookup_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(y, keys, n, out);
+    return cudaGetLastError();
+}
+// Eytzinger copy: sorted position j (in-order number m = j + 1 of a complete tree of height
+// h) sits at depth h-1-ctz(m), index m >> (ctz(m)+1) within its level, i.e. BFS slot
+// 2^(h-1-ctz(m)) + (m >> (ctz(m)+1)); positions >= n hold the ~0 padding.
+__global__ void eytz_build_kernel(const u64 *keys, const u64 *rows, uint64_t n, int h, u64 *ek, u64 *er) {
+    const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t slots = (1ull << h) - 1;
+    if (j >= slots) return;
+    const uint64_t m = j + 1;
+    const int t = __ffsll((long long)m) - 1;
+    const uint64_t i = (1ull << (h - 1 - t)) + (m >> (t + 1));
+    ek[i] = j < n ? keys[j] : ~0ull;
+    er[i] = j < n ? rows[j] : ~0ull;
+    if (j == 0) { ek[0] = ~0ull; er[0] = ~0ull; }   // slot 0 unused
+}
+cudaError_t launch_eytz_build(const u64 *keys, const u64 *rows, uint64_t n, int h, u64 *ek, u64 *er,
+                              cudaStream_t s) {
+    const uint64_t slots = (1ull << h) - 1;
+    eytz_build_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, s>>>(keys, rows, n, h, ek, er);
     return cudaGetLastError();
 }
 // one tree level: out[c] = in[min(16c + 15, n_in - 1)] (the last key of node c), ~0 padding

@@ -225,11 +225,11 @@ def test_c2_mvcc_split_layout(c2, orc):
     b.free()
 
 
-@pytest.mark.parametrize("flag", ["tree", "binary"])
+@pytest.mark.parametrize("flag", ["tree", "binary", "eytz"])
 @pytest.mark.parametrize("scheme", ["tpl_nw", "tictoc", "gacco"])
 def test_c2_full_size_parity_search_index(c2, orc, scheme, flag):
-    """configs[1] in the bench launch with the search indexes (bench --index tree|binary)."""
-    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
+    """configs[1] in the bench launch with the search indexes (bench --index tree|binary|eytz)."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_EYTZ, CC_FLAG_INDEX_TREE
     db, S0, n = c2
     T = inputs.zipf_thresholds(n, 0.6)
     A = inputs.scramble_mult(n)
@@ -237,7 +237,7 @@ def test_c2_full_size_parity_search_index(c2, orc, scheme, flag):
     b = db.gen_ycsb(B, K, W, 78, T, A)
     keys, ops = orc.ycsb_gen(78, n, B, K, W, T, A)
     db.snapshot(False)
-    fl = CC_FLAG_INDEX_BINARY if flag == "binary" else CC_FLAG_INDEX_TREE
+    fl = {"binary": CC_FLAG_INDEX_BINARY, "tree": CC_FLAG_INDEX_TREE, "eytz": CC_FLAG_INDEX_EYTZ}[flag]
     res = db.submit(b, scheme, wd=0, bs=32, lanes=16, flags=fl, watchdog_s=60)
     st = db.sync()
     assert st.commits == B
@@ -281,7 +281,7 @@ def test_index_lookup_tree_and_binary(torch_cuda, n):
     pos = np.searchsorted(keys, probe)
     hit = (pos < n) & (keys[np.minimum(pos, n - 1)] == probe)
     exp = np.where(hit, rows[np.minimum(pos, n - 1)], np.uint64((1 << 64) - 1))
-    for method in ("auto", "tree", "binary"):
+    for method in ("auto", "tree", "binary", "eytz"):
         got = db.index_lookup(iid, probe, method=method)
         assert np.array_equal(got, exp), method
     db.close()
@@ -306,18 +306,19 @@ def test_index_lookup_dense(torch_cuda, k0, n, identity):
     pos = np.searchsorted(keys, probe)
     hit = (pos < n) & (keys[np.minimum(pos, n - 1)] == probe)
     exp = np.where(hit, rows[np.minimum(pos, n - 1)], np.uint64((1 << 64) - 1))
-    for method in ("auto", "tree", "binary"):
+    for method in ("auto", "tree", "binary", "eytz"):
         assert np.array_equal(db.index_lookup(iid, probe, method=method), exp), method
     db.close()
 
 
-@pytest.mark.parametrize("flag", ["binary", "tree"])
+@pytest.mark.parametrize("flag", ["binary", "tree", "eytz"])
 @pytest.mark.parametrize("scheme", ["tpl_nw", "silo", "mvcc", "gacco"])
 def test_c1_parity_binary_index(c1, orc, scheme, flag):
-    """The paper's binary-search index (CC_FLAG_INDEX_BINARY) and the cache-line tree
-    (CC_FLAG_INDEX_TREE) give the same results as the default direct addressing."""
-    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_TREE
-    fl = CC_FLAG_INDEX_BINARY if flag == "binary" else CC_FLAG_INDEX_TREE
+    """The paper's binary-search index (CC_FLAG_INDEX_BINARY), the cache-line tree
+    (CC_FLAG_INDEX_TREE) and the Eytzinger layout (CC_FLAG_INDEX_EYTZ) give the same
+    results as the default direct addressing."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_INDEX_BINARY, CC_FLAG_INDEX_EYTZ, CC_FLAG_INDEX_TREE
+    fl = {"binary": CC_FLAG_INDEX_BINARY, "tree": CC_FLAG_INDEX_TREE, "eytz": CC_FLAG_INDEX_EYTZ}[flag]
     db, S0 = c1
     T = inputs.zipf_thresholds(1024, 0.8)
     A = inputs.scramble_mult(1024)

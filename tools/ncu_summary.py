@@ -18,7 +18,9 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "smsp__warps_eligible.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
            "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-           "lts__t_requests_srcunit_tex.sum"]
+           "lts__t_requests_srcunit_tex.sum", "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum",
+           "l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum",
+           "smsp__thread_inst_executed_per_inst_executed.ratio"]
 STALLS = "smsp__pcsamp_warps_issue_stalled_"
 
 
@@ -51,8 +53,8 @@ def main():
              f"Report `{os.path.basename(a.report)}`; bench config `{a.config}`.",
              "Serialised, cold-cache replay (ncu flushes caches between passes): absolute times are not bench "
              "times; shares and traffic are what to read.", "",
-             "| scheme | ms | DRAM MB | DRAM B/op | L2 hit % | warps active % | eligible/cycle | issue % | L1 % | L2 % | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+             "| scheme | ms | DRAM MB | DRAM B/op | L2 hit % | L2 atom+red sectors (M/s) | threads/inst | warps active % | eligible/cycle | issue % | L1 % | L2 % | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     per = []
     for s, r in zip(SCHEMES, rows):
         g = lambda m: num(r[col[m]]) if m in col else 0.0  # noqa: E731
@@ -62,8 +64,15 @@ def main():
               if h.startswith(STALLS) and not h.endswith("not_issued")}
         tot = sum(st.values()) or 1.0
         top = ", ".join(f"{k} {v / tot * 100:.0f}%" for k, v in sorted(st.items(), key=lambda t: -t[1])[:3])
-        lines.append(f"| {s} | {g('gpu__time_duration.sum'):.3f} | {dram / 1e6:.0f} | {dram / (65536 * 16):.0f} | "
-                     f"{g('lts__t_sector_hit_rate.pct'):.1f} | {g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
+        t_ms = g('gpu__time_duration.sum')
+        tu = units[col["gpu__time_duration.sum"]]
+        t_s = t_ms * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(tu, 1e-3)
+        atom = (g("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum")
+                + g("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum"))   # sectors sent to L2
+        lines.append(f"| {s} | {t_ms:.3f} | {dram / 1e6:.0f} | {dram / (65536 * 16):.0f} | "
+                     f"{g('lts__t_sector_hit_rate.pct'):.1f} | {atom / t_s / 1e6 if t_s else 0:.0f} | "
+                     f"{g('smsp__thread_inst_executed_per_inst_executed.ratio'):.1f} | "
+                     f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{g('smsp__warps_eligible.avg.per_cycle_active'):.3f} | "
                      f"{g('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{g('l1tex__throughput.avg.pct_of_peak_sustained_active'):.1f} | "

@@ -36,7 +36,7 @@ def cell(db, b, s, a):
                 ms_total_min=min(tots), ms_total_max=max(tots), ms_exec_median=statistics.median(execs))
 
 
-IDXF = {"dense": 0, "tree": 0x100, "binary": 0x10}
+IDXF = {"dense": 0, "tree": 0x100, "binary": 0x10, "eytz": 0x1000}
 
 
 def main():
@@ -51,7 +51,7 @@ def main():
     ap.add_argument("--bs", type=int, default=32)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--lanes", type=int, default=1)
-    ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary"])
+    ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary", "eytz"])
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--seeds", default="3")
     ap.add_argument("--chunk", type=int, default=1)

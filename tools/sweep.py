@@ -47,7 +47,7 @@ def cell(db, b, scheme, reps, watchdog, **kw):
                 abort_rate=ab / max(cm, 1))
 
 
-IDXF = {"dense": 0, "tree": 0x100, "binary": 0x10}   # CC_FLAG_INDEX_TREE / CC_FLAG_INDEX_BINARY
+IDXF = {"dense": 0, "tree": 0x100, "binary": 0x10, "eytz": 0x1000}   # CC_FLAG_INDEX_TREE / CC_FLAG_INDEX_BINARY
 
 
 def ycsb_db(rows):
