@@ -261,6 +261,18 @@ def run_reference(args, rank, world):
 TUNED_BS = {"tpl_nw": 16, "tpl_wd": 16, "to": 16, "mvcc": 16, "silo": 16, "tictoc": 12, "gputx": 8, "gacco": 24}
 
 
+# TPC-C tile mode (32 lanes), configs[4] shape on one GPU (512 warehouses, 64K batch;
+# profiles/r01_tpcc_launch.txt): the full-occupancy grid is best for every scheme but
+# GaccO, whose hand-off chains prefer 16 warps on one block per SM (49 -> 55 M txn/s).
+# (At 64 warehouses one block of 4-8 warps per SM wins instead: contention decides.)
+TUNED_TPCC = {"gacco": (16, True)}
+
+
+def tpcc_launch(args, scheme, n_sms):
+    bs, one_block = TUNED_TPCC.get(scheme, (8, False)) if args.launch == "tuned" else (8, False)
+    return {"bs": bs, "grid": n_sms if one_block else 0}
+
+
 def launch_of(args, scheme, n_sms):
     if args.launch == "tuned" and args.lanes > 1 and args.wd == 0:
         return {"wd": 0, "bs": TUNED_BS[scheme], "grid": n_sms}
@@ -543,9 +555,9 @@ def run_tpcc_loopback(args, local):
               for r, db in enumerate(dbs)]
         for s in schemes:
             if args.two_pc and s in ("tpl_nw", "tpl_wd"):
-                loopback_round_2pc(dbs, bs, s, results=res[s], bs=8, lanes=32, watchdog_s=60)
+                loopback_round_2pc(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms), lanes=32, watchdog_s=60)
             else:
-                loopback_round(dbs, bs, s, results=res[s], bs=8, lanes=32, watchdog_s=60)
+                loopback_round(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms), lanes=32, watchdog_s=60)
         return bs
 
     for i in range(args.warmup):
@@ -582,6 +594,8 @@ def run_tpcc_loopback(args, local):
         "config": {"workload": "tpcc_configs4_partitioned_loopback", "warehouses": W, "partitions": G,
                    "batch_per_partition": n, "neworder_permyriad": args.tpcc_mix, "schemes": schemes,
                    "lanes_per_txn": 32, "parallelism": f"{G} warehouse partitions on 1 GPU, device-side exchange",
+                   "launch": {s: tpcc_launch(args, s, 148) for s in schemes} if args.launch == "tuned"
+                   else "bs 8, full-occupancy grid",
                    "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic",
                    "timing": "host clock around fully synchronised steps (G streams + host-orchestrated exchange)"},
         "per_scheme": per, "clocks": clk}), flush=True)
@@ -617,11 +631,11 @@ def run_tpcc(args, rank, world, local):
         b = db.gen_tpcc(n, 7919 * (rank + 1) + i, args.tpcc_mix, w_lo=rank * wpr, w_hi=(rank + 1) * wpr)
         for s in schemes:
             if world > 1 and args.two_pc and s in ("tpl_nw", "tpl_wd"):
-                dist_round_2pc(db, b, s, result=res[s], bs=8, lanes=32, watchdog_s=60)
+                dist_round_2pc(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
             elif world > 1:
-                dist_round(db, b, s, result=res[s], bs=8, lanes=32, watchdog_s=60)
+                dist_round(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
             else:
-                db.submit(b, s, bs=8, lanes=32, result=res[s], watchdog_s=60)
+                db.submit(b, s, **tpcc_launch(args, s, db.num_sms), lanes=32, result=res[s], watchdog_s=60)
         return b
 
     def barrier():
@@ -666,6 +680,8 @@ def run_tpcc(args, rank, world, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "tpcc_configs4_partitioned", "warehouses": W, "batch_per_rank": n,
                        "neworder_permyriad": args.tpcc_mix, "schemes": schemes, "lanes_per_txn": 32,
+                       "launch": {s: tpcc_launch(args, s, 148) for s in schemes} if args.launch == "tuned"
+                       else "bs 8, full-occupancy grid",
                        "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else ""),
                        "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic"},
             "per_scheme": per, "clocks": clk,

@@ -280,6 +280,32 @@ GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
 #ifndef GC_GACCO_SPIN
 #define GC_GACCO_SPIN 32
 #endif
+// A GaccO access knows its queue position and reads the item's cursor, so it knows how
+// many hand-offs (>= ~1.2 us each, measured) are still ahead of it: far waiters sleep in
+// proportion to that distance with relaxed polls, and only the next in line polls with
+// acquire loads.  Hundreds of waiters polling one hot cursor at full rate otherwise
+// saturate its L2 slice and slow the very hand-offs they wait for.
+#ifndef GC_GACCO_HOP_NS
+#define GC_GACCO_HOP_NS 600
+#endif
+GC_DEV bool gacco_turn(Th &th, u32 *cur, u32 pos) {
+    u32 c = ld_acquire32(cur);
+    if (c == pos) return true;
+    const u64 t0 = th.timing ? clk64() : 0;
+    bool ok = true;
+    while (pos - c > 1) {   // the cursor never passes pos before we release it
+        const u32 d = pos - c - 1;
+        __nanosleep(d >= 80 ? 50000u : d * GC_GACCO_HOP_NS);
+        if (dead(th)) { ok = false; break; }
+        c = ld_relaxed32(cur);
+    }
+    if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
+    if (!ok) return false;
+    Spin sp(GC_GACCO_SPIN);
+    while (ld_acquire32(cur) != pos)   // the poll that sees our turn is the acquire
+        if (!sp.wait(th)) return false;
+    return true;
+}
 
 // GPUTx K-set gate: wait until K-set k-1 has completed.  K-sets complete
 // in order and ctl->kdone counts them (set by each set's last finisher), so a waiter knows
@@ -838,9 +864,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 i = 0; i < n; i++) {
             const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
             u32 *cur = &p.cursor[seg];
-            Spin sp(GC_GACCO_SPIN);   // the hand-off chain on a hot item is GaccO's critical path
-            while (ld_acquire32(cur) != pos)   // the poll that sees our turn is the acquire
-                if (!sp.wait(th)) return RES_FATAL;
+            if (!gacco_turn(th, cur, pos)) return RES_FATAL;
             u64 *row = WL::row(y, L[i]);
             rd<WL>(th, y, L[i], gid, i, row);
             if (L[i].w) inst<WL>(th, y, L[i], row);
@@ -1117,9 +1141,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             const u64 a = (u64)gid * p.K + li;
             const u32 seg = p.acc_seg[a], pos = p.acc_pos[a];
             u32 *cur = &p.cursor[seg];
-            Spin sp(GC_GACCO_SPIN);   // the hand-off chain on a hot item is GaccO's critical path
-            while (ld_acquire32(cur) != pos)   // the poll that sees our turn is the acquire
-                if (!sp.wait(th)) { st = ST_ABORT; break; }
+            if (!gacco_turn(th, cur, pos)) st = ST_ABORT;
             if (st == ST_DONE) {
                 u64 *row = WL::row(y, L);
                 rd<WL>(th, y, L, gid, li, row);

@@ -17,7 +17,7 @@ def fresh(a):
 
 
 def cell(db, b, s, a):
-    kw = dict(wd=a.wd, bs=a.bs, lanes=a.lanes, watchdog_s=a.watchdog)
+    kw = dict(wd=a.wd, bs=a.bs, lanes=a.lanes, watchdog_s=a.watchdog, grid=a.grid)
     db.snapshot(False)
     db.submit(b, s, flags=a.flags, **kw)
     db.sync()
@@ -42,12 +42,14 @@ def main():
     ap.add_argument("--wd", type=int, default=0)
     ap.add_argument("--bs", type=int, default=8)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--grid", type=int, default=0, help="blocks (0: resident capacity)")
     ap.add_argument("--flags", type=lambda x: int(x, 0), default=0)
     ap.add_argument("--watchdog", type=float, default=30)
     a = ap.parse_args()
     db, b = fresh(a)
     for s in a.schemes.split(","):
-        row = dict(W=a.W, batch=a.batch, mix=a.mix, scheme=s, lanes=a.lanes, wd=a.wd, bs=a.bs, flags=a.flags)
+        row = dict(W=a.W, batch=a.batch, mix=a.mix, scheme=s, lanes=a.lanes, wd=a.wd, bs=a.bs, grid=a.grid,
+                   flags=a.flags)
         try:
             row.update(cell(db, b, s, a))
         except Exception as e:   # watchdog etc.: recorded, the db is rebuilt
