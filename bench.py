@@ -268,7 +268,15 @@ TUNED_BS = {"tpl_nw": 16, "tpl_wd": 16, "to": 16, "mvcc": 16, "silo": 16, "ticto
 TUNED_TPCC = {"gacco": (16, True)}
 
 
-def tpcc_launch(args, scheme, n_sms):
+# Loopback partitions share one GPU: each partition's executor takes one block per SM so
+# the G partitions run side by side (warps per SM as at 64 warehouses; 4 partitions x
+# 128 warehouses: 9.0 -> 45 M txn/s against full-occupancy grids that serialise them).
+LOOPBACK_TPCC_BS = {"tpl_nw": 8, "tpl_wd": 8, "to": 8, "mvcc": 8, "silo": 4, "tictoc": 8, "gputx": 8, "gacco": 4}
+
+
+def tpcc_launch(args, scheme, n_sms, loopback=False):
+    if loopback and args.launch == "tuned":
+        return {"bs": LOOPBACK_TPCC_BS[scheme], "grid": n_sms}
     bs, one_block = TUNED_TPCC.get(scheme, (8, False)) if args.launch == "tuned" else (8, False)
     return {"bs": bs, "grid": n_sms if one_block else 0}
 
@@ -555,9 +563,9 @@ def run_tpcc_loopback(args, local):
               for r, db in enumerate(dbs)]
         for s in schemes:
             if args.two_pc and s in ("tpl_nw", "tpl_wd"):
-                loopback_round_2pc(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms), lanes=32, watchdog_s=60)
+                loopback_round_2pc(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms, True), lanes=32, watchdog_s=60)
             else:
-                loopback_round(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms), lanes=32, watchdog_s=60)
+                loopback_round(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms, True), lanes=32, watchdog_s=60)
         return bs
 
     for i in range(args.warmup):
@@ -594,7 +602,7 @@ def run_tpcc_loopback(args, local):
         "config": {"workload": "tpcc_configs4_partitioned_loopback", "warehouses": W, "partitions": G,
                    "batch_per_partition": n, "neworder_permyriad": args.tpcc_mix, "schemes": schemes,
                    "lanes_per_txn": 32, "parallelism": f"{G} warehouse partitions on 1 GPU, device-side exchange",
-                   "launch": {s: tpcc_launch(args, s, 148) for s in schemes} if args.launch == "tuned"
+                   "launch": {s: tpcc_launch(args, s, 148, True) for s in schemes} if args.launch == "tuned"
                    else "bs 8, full-occupancy grid",
                    "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic",
                    "timing": "host clock around fully synchronised steps (G streams + host-orchestrated exchange)"},

@@ -261,9 +261,10 @@ typedef struct {
     uint32_t flags;         /* CC_FLAG_* */
     uint32_t grid;          /* blocks; 0 = resident capacity (persistent grid) */
     uint32_t lanes_per_txn; /* 0/1: one lane per transaction (the paper's model, wd and bs
-                               apply); 4/8/16: a tile of that many lanes runs one
+                               apply); 4/8/16/32: a tile of that many lanes runs one
                                transaction, lane i owning access i (must be >= ops per
-                               transaction; wd is ignored).  TPC-C batches use 32-lane
+                               transaction; wd is ignored; 32 gives every transaction a
+                               warp of its own).  TPC-C batches use 32-lane
                                tiles for any value > 1 */
     double watchdog_s;      /* device watchdog in seconds (0 = 30 s) */
     uint32_t claim_chunk;   /* fresh transaction ids a worker claims per atomic (0 = 1) */

@@ -387,10 +387,11 @@ static cc_status create_table(cc_db db, const char *name, uint32_t row_bytes, ui
     CUDA_TRY(db, dalloc(&t.d, (size_t)row_bytes * rows));
     CUDA_TRY(db, cudaMemsetAsync(t.d, 0, (size_t)row_bytes * rows, db->stream));
     if (cc) {
-        // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B)
+        // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B),
+        // GC_META_STRIDE words in the padded ablation build
         const uint64_t need = db->n_records + rows;
         u64 *meta = nullptr;
-        CUDA_TRY(db, dalloc(&meta, need * 16));
+        CUDA_TRY(db, dalloc(&meta, need * 8 * (GC_META_STRIDE > 2 ? GC_META_STRIDE : 2)));
         CUDA_TRY(db, cudaStreamSynchronize(db->stream));
         if (db->meta) cudaFree(db->meta);
         db->meta = meta;
@@ -929,9 +930,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (b->ready) CUDA_TRY(db, cudaStreamWaitEvent(db->stream, b->ready, 0));   // async imports
     {
         const uint32_t L = desc->lanes_per_txn;
-        if (is_tpcc ? !(L <= 1 || L == 4 || L == 8 || L == 16 || L == 32)
-                    : (!(L <= 1 || L == 4 || L == 8 || L == 16) || (L > 1 && L < b->K)))
-            return fail(db, CC_ERR_INVALID_ARG, "lanes_per_txn must be 0/1 or 4/8/16 (>= ops per txn); TPC-C uses 32-lane tiles");
+        if (!(L <= 1 || L == 4 || L == 8 || L == 16 || L == 32) || (!is_tpcc && L > 1 && L < b->K))
+            return fail(db, CC_ERR_INVALID_ARG, "lanes_per_txn must be 0/1 or 4/8/16/32 (YCSB: >= ops per txn)");
     }
     const int scheme = (int)desc->scheme;
     const bool det = scheme == CC_GPUTX || scheme == CC_GACCO;
@@ -1017,8 +1017,9 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     // a2: reset CC state (every record of every table)
     p.mvcc_split = (scheme == CC_MVCC && (desc->flags & CC_FLAG_MVCC_SPLIT)) ? db->n_records : 0;
+    p.meta_stride = scheme != CC_MVCC ? GC_META_STRIDE : 1u;
     CUDA_TRY(db, launch_reset_meta(scheme, db->meta, db->n_records, db->ring, db->ring_cap, db->ctl,
-                                   db->stream, p.mvcc_split != 0));
+                                   db->stream, p.mvcc_split != 0, p.meta_stride));
     CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
     if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
         const uint32_t wpr = db->tpcc.W / db->world;

@@ -53,6 +53,11 @@ struct Th {
 
 GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err.v, 0ull, code); }
 
+// control word of a record (single-word schemes): packed 8 B SoA words, or -- in the
+// ablation build -DGC_META_STRIDE=4 -- one word per 32 B sector (f-3; a compile-time
+// stride: a runtime one cost the tile kernels 12-100 B of spills).  MVCC: mvcc_lo / _hi.
+GC_DEV u64 *cw(const ExecParams &p, u32 rec) { return p.meta + (u64)rec * GC_META_STRIDE; }
+
 GC_DEV bool dead(Th &th) {
     if (globaltimer_ns() > th.deadline) {
         set_err(th.p->ctl, CC_ERR_WATCHDOG);
@@ -199,7 +204,9 @@ GC_DEV void latch_acquire(uint32_t *l) {
     }
 }
 GC_DEV void latch_release(uint32_t *l) { st_release32(l, 0u); }
-GC_DEV uint32_t *latch_of(const ExecParams &p, const u64 *w) { return p.latch + (w - p.meta); }
+GC_DEV uint32_t *latch_of(const ExecParams &p, const u64 *w) {
+    return p.latch + (p.scheme == CC_MVCC ? (w - p.meta) : (w - p.meta) / GC_META_STRIDE);
+}
 
 GC_DEV u64 w_cas(const ExecParams &p, u64 *w, u64 expect, u64 desired) {
     if (!p.latch) return cas_acqrel(w, expect, desired);
@@ -554,7 +561,7 @@ enum { ST_DONE = 0, ST_WAIT = 1, ST_ABORT = 2, ST_RETRY = 3 };   // RETRY: lost 
 template <class WL>
 GC_DEV int to_step(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                    u32 gid, u32 i, u64 ts, bool &pend, u64 &saved) {
-    u64 *w = &p.meta[L.rec];
+    u64 *w = cw(p, L.rec);
     const u64 *row = WL::row(y, L);
     const u64 v = ld_acquire(w);
     if (L.w) {
@@ -580,7 +587,7 @@ template <class WL>
 GC_DEV void to_commit(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L, u64 ts) {
     inst<WL>(th, y, L, WL::row(y, L));
     fence_acqrel();
-    w_store_relaxed(p, &p.meta[L.rec], to_make(false, ts, ts));
+    w_store_relaxed(p, cw(p, L.rec), to_make(false, ts, ts));
 }
 
 // MVCC access step (Z6): writes append at the head only; reads never abort.
@@ -669,7 +676,7 @@ GC_DEV void mvcc_commit(Th &th, const ExecParams &p, const typename WL::Params &
 template <class WL>
 GC_DEV int occ_snap_step(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L,
                          u32 gid, u32 i, u64 &obs) {
-    u64 *w = &p.meta[L.rec];
+    u64 *w = cw(p, L.rec);
     const u64 v1 = ld_acquire(w);
     if (v1 & LOCKB) return ST_WAIT;
     const u64 ev = rd<WL>(th, y, L, gid, i, WL::row(y, L));
@@ -736,15 +743,15 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             Spin sp;
             int st;
             u64 seen = 0;
-            while ((st = tpl_try<WD>(p, &p.meta[L[i].rec], L[i].w, age, seen, th.attempt >= TPL_INTENT_AFTER)) == ST_WAIT)
+            while ((st = tpl_try<WD>(p, cw(p, L[i].rec), L[i].w, age, seen, th.attempt >= TPL_INTENT_AFTER)) == ST_WAIT)
                 if (!sp.wait(th)) { st = -1; break; }
-            if (st == ST_ABORT) { th.cw = &p.meta[L[i].rec]; th.cv = M31 << 31; }   // until free
+            if (st == ST_ABORT) { th.cw = cw(p, L[i].rec); th.cv = M31 << 31; }   // until free
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
             rd<WL>(th, y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
         }
         if (r != RES_OK) {
             fence_acqrel();
-            for (u32 j = 0; j < i; j++) tpl_release_relaxed(p, &p.meta[L[j].rec], L[j].w);
+            for (u32 j = 0; j < i; j++) tpl_release_relaxed(p, cw(p, L[j].rec), L[j].w);
             return r;
         }
         // lock point: every lock held, none released -> a valid serial order (strict 2PL)
@@ -753,7 +760,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 j = 0; j < n; j++)
             if (L[j].w) inst<WL>(th, y, L[j], WL::row(y, L[j]));
         fence_acqrel();
-        for (u32 j = 0; j < n; j++) tpl_release_relaxed(p, &p.meta[L[j].rec], L[j].w);
+        for (u32 j = 0; j < n; j++) tpl_release_relaxed(p, cw(p, L[j].rec), L[j].w);
         return RES_OK;
     } else if constexpr (S == CC_TO || S == CC_MVCC) {
         u64 ts;
@@ -781,7 +788,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         if (r != RES_OK) {
             for (u32 j = 0; j < n; j++)
                 if ((pendm >> j) & 1) {
-                    if (S == CC_TO) w_store(p, &p.meta[L[j].rec], saved[j]);
+                    if (S == CC_TO) w_store(p, cw(p, L[j].rec), saved[j]);
                     else mvcc_restore<WL>(p, L[j], saved[j]);
                 }
             return r;
@@ -807,10 +814,10 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         for (u32 i = 0; i < n && ok; i++)
             if (L[i].w) {
                 u64 seen = 0;
-                if (occ_lock(p, &p.meta[L[i].rec], pre[i], seen)) locked |= 1u << i;
+                if (occ_lock(p, cw(p, L[i].rec), pre[i], seen)) locked |= 1u << i;
                 else {
                     ok = false;
-                    if (seen & LOCKB) { th.cw = &p.meta[L[i].rec]; th.cv = LOCKB; }   // until unlocked
+                    if (seen & LOCKB) { th.cw = cw(p, L[i].rec); th.cv = LOCKB; }   // until unlocked
                 }
             }
         u64 ticket = 0, cts = 0;
@@ -823,7 +830,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             // the paper's launch ran 2.5 ms with the dense index, 425 ms with the binary
             // search.)
             for (u32 i = 0; i < n && ok; i++)
-                ok = L[i].w ? (pre[i] == obs[i]) : (ld_relaxed(&p.meta[L[i].rec]) == obs[i]);
+                ok = L[i].w ? (pre[i] == obs[i]) : (ld_relaxed(cw(p, L[i].rec)) == obs[i]);
         }
         if (ok && S == CC_TICTOC) {
             for (u32 i = 0; i < n; i++) {   // commit_ts
@@ -832,13 +839,13 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             }
             for (u32 i = 0; i < n && ok; i++)
                 ok = L[i].w ? (tt_wts(pre[i]) == tt_wts(obs[i]))
-                            : tictoc_validate(p, &p.meta[L[i].rec], obs[i], cts);
+                            : tictoc_validate(p, cw(p, L[i].rec), obs[i], cts);
             if (ok) ticket = agg_fetch_add(&p.ctl->ticket.v);   // after validation
         }
         if (!ok) {
             fence_acqrel();
             for (u32 j = 0; j < n; j++)
-                if ((locked >> j) & 1) w_store_relaxed(p, &p.meta[L[j].rec], pre[j]);
+                if ((locked >> j) & 1) w_store_relaxed(p, cw(p, L[j].rec), pre[j]);
             return RES_ABORT;
         }
         u64 nw;
@@ -856,7 +863,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             if (L[j].w) inst<WL>(th, y, L[j], WL::row(y, L[j]));
         fence_acqrel();
         for (u32 j = 0; j < n; j++)
-            if (L[j].w) w_store_relaxed(p, &p.meta[L[j].rec], nw);
+            if (L[j].w) w_store_relaxed(p, cw(p, L[j].rec), nw);
         return RES_OK;
     } else if constexpr (S == CC_GACCO) {
         // wait for the turn, access, advance the cursor (release after the op, Z3)
@@ -980,14 +987,14 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             bool mine = act && !held;
             if (first && !tile.shfl(held || !act, first - 1)) mine = mine && li == first - 1;
             if (mine) {
-                st = tpl_try<WD>(p, &p.meta[L.rec], L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
+                st = tpl_try<WD>(p, cw(p, L.rec), L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
                 held = st == ST_DONE;
             }
             const unsigned dying = tile.ballot(st == ST_ABORT);
             if (dying) {
-                if (held) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
+                if (held) tpl_release_relaxed(p, cw(p, L.rec), L.w);
                 const int src = __ffs(dying) - 1;   // remember one conflicting lock for the retry
-                th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
+                th.cw = (u64 *)tile.shfl((u64)cw(p, L.rec), src);
                 th.cv = M31 << 31;                   // wait until its holder count is 0
                 th.hot = (u32)src + 1;               // and take it first next time
                 return RES_ABORT;
@@ -995,7 +1002,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (tile.all(!act || held)) break;
             if (!tile.any(st == ST_WAIT)) continue;   // ordered: the next lane's turn
             if (tile.any(!sp.wait(th))) {
-                if (held) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
+                if (held) tpl_release_relaxed(p, cw(p, L.rec), L.w);
                 return RES_FATAL;
             }
         }
@@ -1006,7 +1013,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         key_hi = 0;
         if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         fence_acqrel();
-        if (act) tpl_release_relaxed(p, &p.meta[L.rec], L.w);
+        if (act) tpl_release_relaxed(p, cw(p, L.rec), L.w);
         return RES_OK;
     } else if constexpr (S == CC_TO || S == CC_MVCC) {
         u64 ts = 0;
@@ -1039,7 +1046,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
             if (tile.any(st == ST_ABORT)) {
                 if (pend) {
-                    if (S == CC_TO) w_store(p, &p.meta[L.rec], saved);
+                    if (S == CC_TO) w_store(p, cw(p, L.rec), saved);
                     else mvcc_restore<WL>(p, L, saved);
                 }
                 return RES_ABORT;
@@ -1049,7 +1056,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (seq && !tile.any(st == ST_WAIT)) continue;   // sequential: the next lane's turn
             if (tile.any(!sp.wait(th))) {
                 if (pend) {
-                    if (S == CC_TO) w_store(p, &p.meta[L.rec], saved);
+                    if (S == CC_TO) w_store(p, cw(p, L.rec), saved);
                     else mvcc_restore<WL>(p, L, saved);
                 }
                 return RES_FATAL;
@@ -1082,11 +1089,11 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         // first, alone (see 2PL)
         const u32 first = th.attempt < 2 ? 0u : th.hot;
         if (first && li == first - 1 && act && L.w) {
-            locked = occ_lock(p, &p.meta[L.rec], pre, seen);
+            locked = occ_lock(p, cw(p, L.rec), pre, seen);
             bad = !locked;
         }
         if (!tile.any(bad) && act && L.w && !locked) {
-            locked = occ_lock(p, &p.meta[L.rec], pre, seen);
+            locked = occ_lock(p, cw(p, L.rec), pre, seen);
             bad = !locked;
         }
         {
@@ -1094,7 +1101,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             th.hot = 0;
             if (busy) {
                 const int src = __ffs(busy) - 1;
-                th.cw = (u64 *)tile.shfl((u64)&p.meta[L.rec], src);
+                th.cw = (u64 *)tile.shfl((u64)cw(p, L.rec), src);
                 th.cv = LOCKB;                       // wait until unlocked
                 th.hot = (u32)src + 1;
             }
@@ -1105,12 +1112,12 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // serialization point
                 ticket = tile.shfl(ticket, 0);
                 fence_acqrel();
-                if (act) bad = L.w ? (pre != obs) : (ld_relaxed(&p.meta[L.rec]) != obs);   // see run_thread
+                if (act) bad = L.w ? (pre != obs) : (ld_relaxed(cw(p, L.rec)) != obs);   // see run_thread
             } else {
                 u64 c = 0;
                 if (act) c = max(L.w ? tt_rts(pre) + 1 : 0ull, tt_wts(obs));
                 cts = cg::reduce(tile, c, cg::greater<u64>());
-                if (act) bad = L.w ? (tt_wts(pre) != tt_wts(obs)) : !tictoc_validate(p, &p.meta[L.rec], obs, cts);
+                if (act) bad = L.w ? (tt_wts(pre) != tt_wts(obs)) : !tictoc_validate(p, cw(p, L.rec), obs, cts);
                 if (!tile.any(bad)) {
                     if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // after validation
                     ticket = tile.shfl(ticket, 0);
@@ -1118,7 +1125,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
         }
         if (tile.any(bad)) {
-            if (locked) w_store(p, &p.meta[L.rec], pre);
+            if (locked) w_store(p, cw(p, L.rec), pre);
             return RES_ABORT;
         }
         u64 nw;
@@ -1133,7 +1140,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         key_lo = ticket;
         if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         fence_acqrel();
-        if (act && L.w) w_store_relaxed(p, &p.meta[L.rec], nw);
+        if (act && L.w) w_store_relaxed(p, cw(p, L.rec), nw);
         return RES_OK;
     } else if constexpr (S == CC_GACCO) {
         int st = ST_DONE;

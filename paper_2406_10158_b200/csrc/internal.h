@@ -5,6 +5,13 @@
 
 #include "../../include/gcctb.h"
 
+// Words per record of the single-word schemes' control-word array: 1 (packed 8 B SoA,
+// the shipped build) or 4 (one word per 32 B sector: the false-sharing ablation build,
+// GCCTB_NVCC_EXTRA=-DGC_META_STRIDE=4).
+#ifndef GC_META_STRIDE
+#define GC_META_STRIDE 1
+#endif
+
 namespace gcctb {
 
 // Device control block of one submit (reset by the a2 reset kernel).  Every hot
@@ -52,6 +59,7 @@ struct ExecParams {
     unsigned long long watchdog_ns;
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
+    uint32_t meta_stride = 1;    // words per record for the single-word schemes (GC_META_STRIDE)
     unsigned long long *arena;   // MVCC version nodes: ARENA_HDR header words + the row
     uint32_t to_backoff_cap;     // TO/MVCC backoff cap exponent (0: adaptive); experiment
                                  // knob, environment GCCTB_TO_BACKOFF_CAP
@@ -135,7 +143,7 @@ struct PrepBufs {
 // launchers (defined in the .cu files)
 cudaError_t launch_reset_meta(int scheme, unsigned long long *meta, uint64_t n_records,
                               unsigned long long *ring, uint32_t ring_cap, Ctl *ctl,
-                              cudaStream_t s, bool mvcc_split = false);
+                              cudaStream_t s, bool mvcc_split = false, uint32_t meta_stride = 1);
 cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
                              cudaStream_t s);
 int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block);

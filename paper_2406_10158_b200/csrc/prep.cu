@@ -20,7 +20,7 @@ constexpr u64 GID_MASK = (1ull << 21) - 1;
 // Reset the scheme's CC words (the throughput window starts "from the initialization
 // of the CC method", Z19), the retry ring and the control block.
 __global__ void reset_kernel(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
-                             uint32_t ring_cap, Ctl *ctl, bool mvcc_split) {
+                             uint32_t ring_cap, Ctl *ctl, bool mvcc_split, uint32_t meta_stride) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     if (scheme == CC_MVCC && mvcc_split) {   // lo words dense, hi words after them
@@ -34,7 +34,7 @@ __global__ void reset_kernel(int scheme, u64 *meta, uint64_t n_records, u64 *rin
             reinterpret_cast<ulonglong2 *>(meta)[r] = make_ulonglong2(0ull, VNONE);
         }
     } else {
-        for (uint64_t r = tid; r < n_records; r += stride) meta[r] = 0ull;
+        for (uint64_t r = tid; r < n_records * meta_stride; r += stride) meta[r] = 0ull;
     }
     for (uint64_t r = tid; r < ring_cap; r += stride) ring[r] = 0ull;
     for (uint64_t r = tid; r < sizeof(Ctl) / 8; r += stride) reinterpret_cast<u64 *>(ctl)[r] = 0ull;
@@ -52,11 +52,13 @@ __global__ void zero_txn_kernel(uint8_t *committed, uint32_t *restarts, u64 *ohi
 }
 
 cudaError_t launch_reset_meta(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
-                              uint32_t ring_cap, Ctl *ctl, cudaStream_t s, bool mvcc_split) {
+                              uint32_t ring_cap, Ctl *ctl, cudaStream_t s, bool mvcc_split,
+                              uint32_t meta_stride) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    reset_kernel<<<sms * 4, 512, 0, s>>>(scheme, meta, n_records, ring, ring_cap, ctl, mvcc_split);
+    reset_kernel<<<sms * 4, 512, 0, s>>>(scheme, meta, n_records, ring, ring_cap, ctl, mvcc_split,
+                                         meta_stride);
     return cudaGetLastError();
 }
 

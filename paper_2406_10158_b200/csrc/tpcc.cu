@@ -373,7 +373,7 @@ struct TpccWL {
         const u64 *rw = row(y, L);
         const int n = row_words(L);
         for (int k = 0; k < n && k < 40; k += 16) prefetch_l2(rw + k);   // the fields read
-        prefetch_l2(p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : p.meta + L.rec);
+        prefetch_l2(p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : cw(p, L.rec));
     }
 
     static GC_DEV u32 load_all(const ExecParams &p, const TpccParams &y, u32 gid, Lane *L) {

@@ -198,7 +198,7 @@ struct YcsbWL {
         const u64 *rw = y.rows + (u64)L.rec * 16u;
         prefetch_l2(rw);
         prefetch_l2(rw + 8);
-        prefetch_l2(p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : p.meta + L.rec);
+        prefetch_l2(p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : cw(p, L.rec));
     }
 
     static GC_DEV u64 *row(const YcsbParams &y, const Lane &L) { return y.rows + (u64)L.rec * 16u; }
@@ -254,6 +254,7 @@ static cudaError_t launch_s(const ExecParams &p, const YcsbParams &y, int grid, 
         case 4: exec_tile_kernel<S, YcsbWL, 4><<<grid, block, 0, s>>>(p, y); break;
         case 8: exec_tile_kernel<S, YcsbWL, 8><<<grid, block, 0, s>>>(p, y); break;
         case 16: exec_tile_kernel<S, YcsbWL, 16><<<grid, block, 0, s>>>(p, y); break;
+        case 32: exec_tile_kernel<S, YcsbWL, 32><<<grid, block, 0, s>>>(p, y); break;
         default: exec_thread_kernel<S, YcsbWL><<<grid, block, 0, s>>>(p, y); break;
     }
     return cudaGetLastError();
@@ -287,6 +288,7 @@ static int occ_s(int lanes, int block) {
         case 4: return occ_of(exec_tile_kernel<S, YcsbWL, 4>, block);
         case 8: return occ_of(exec_tile_kernel<S, YcsbWL, 8>, block);
         case 16: return occ_of(exec_tile_kernel<S, YcsbWL, 16>, block);
+        case 32: return occ_of(exec_tile_kernel<S, YcsbWL, 32>, block);
         default: return occ_of(exec_thread_kernel<S, YcsbWL>, block);
     }
 }
