@@ -51,6 +51,8 @@ def parse():
                     help="dense = direct addressing on the dense YCSB key range (default); tree = cache-line "
                          "search tree over the sorted keys; binary = PAPER.md:344 (identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ceilings", action="store_true",
+                    help="skip cc_roofline_probe (for ncu launch lists: its ring kernel is long)")
     ap.add_argument("--pipeline", action="store_true",
                     help="f-4: prepare GPUTx / GaccO for each step's batch on the low-priority prep stream "
                          "(cc_prepare) while the other schemes execute.  Off by default: measured slower on "
@@ -384,7 +386,7 @@ def run_ours(args, rank, world, local):
     bk, bo = b.export_ycsb()
     nw2 = int(((bo & 0x80) != 0).sum())
     acc_max, w_max = hot_record_counts(bk, bo, args.rows)
-    ceil = db.roofline_probe() if rank == 0 else None   # untimed: memory-system ceilings
+    ceil = db.roofline_probe() if rank == 0 and not args.no_ceilings else None   # untimed ceilings
     exec_ms_total, alg_bytes_total = 0.0, 0
     for s in schemes:
         db.timing(reset=True)
