@@ -40,11 +40,12 @@ def w4(torch_cuda, orc):
     db.close()
 
 
-def _run(db, S0, W, tx_batch, scheme, lanes, orc, flags=0):
+def _run(db, S0, W, tx_batch, scheme, lanes, orc, flags=0, launch=None):
     from oracle import tpcc as OT
     tx = tx_batch.export_tpcc()
     db.snapshot(False)
-    res = db.submit(tx_batch, scheme, wd=0, bs=32 if lanes == 1 else 8, lanes=lanes, watchdog_s=60, flags=flags)
+    la = launch or {"bs": 32 if lanes == 1 else 8}
+    res = db.submit(tx_batch, scheme, wd=0, lanes=lanes, watchdog_s=60, flags=flags, **la)
     st = db.sync()
     assert st.commits == tx_batch.n_txn
     h = res.host(db.stream)
@@ -128,6 +129,20 @@ def test_c4_full_size_parity(c4, orc, scheme, lanes):
     db, S0 = c4
     b = db.gen_tpcc(65536, 41, 5114)
     _run(db, S0, 64, b, scheme, lanes, orc)
+    b.free()
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c4_full_size_parity_bench_launch(c4, orc, scheme, loopback):
+    """configs[3] in the launches bench.py times for TPC-C (bench.tpcc_launch: per-scheme
+    warps per SM, one block per SM where tuned; the loopback partitions' launch)."""
+    import types
+    import bench
+    db, S0 = c4
+    la = bench.tpcc_launch(types.SimpleNamespace(launch="tuned"), scheme, db.num_sms, loopback)
+    b = db.gen_tpcc(65536, 43, 5114)
+    _run(db, S0, 64, b, scheme, 32, orc, launch=la)
     b.free()
 
 

@@ -194,6 +194,46 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     b.free()
 
 
+@pytest.mark.parametrize("theta", [0.6, 0.9])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta):
+    """configs[1] at full size in exactly the launch bench.py times (bench.launch_of: tile
+    16, per-scheme warps per SM, one block per SM), at the bench's theta and above."""
+    import types
+    import bench
+    db, S0, n = c2
+    a = types.SimpleNamespace(launch="tuned", lanes=16, wd=0, bs=32)
+    la = bench.launch_of(a, scheme, db.num_sms)
+    assert la["grid"] == db.num_sms
+    T = inputs.zipf_thresholds(n, theta)
+    A = inputs.scramble_mult(n)
+    B, K, W = 1 << 16, 16, 0.1
+    b = db.gen_ycsb(B, K, W, 79, T, A)
+    keys, ops = orc.ycsb_gen(79, n, B, K, W, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, lanes=16, watchdog_s=60, **la)
+    st = db.sync()
+    assert st.commits == B
+    orc.check_ycsb(scheme, S0, keys, ops, K, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c1_parity_warp_per_txn(c1, orc, scheme):
+    """32-lane tiles (one warp per transaction, lanes >= K idle) give the oracle's results."""
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 46, T, A)
+    keys, ops = orc.ycsb_gen(46, 1024, 1024, 4, 0.5, T, A)
+    for bs, grid in ((32, 0), (4, 148)):
+        db.snapshot(False)
+        res = db.submit(b, scheme, bs=bs, grid=grid, lanes=32)
+        db.sync()
+        orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
 @pytest.mark.parametrize("lanes", [1, 4])
 def test_c1_parity_mvcc_split_layout(c1, orc, lanes):
     """f-3 metadata ablation: MVCC with split timestamp / version-pointer arrays gives the
