@@ -332,12 +332,22 @@ def run_ours(args, rank, world, local):
             for s in schemes:
                 db.prepare(b, s, xflags)
 
+    scheme_ev = []   # timed steps: an event after each scheme's submit (per-step attribution)
+
     def step(i, timing=False):
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
         prepare(b)
+        evs = []
         for s in schemes:
+            if timing:
+                evs.append(torch.cuda.Event(enable_timing=True))
+                evs[-1].record(stream)
             db.submit(b, s, **LA[s], flags=xflags | (CC_FLAG_TIMING if timing else 0),
                       result=res[s], watchdog_s=60, lanes=args.lanes)
+        if timing:
+            evs.append(torch.cuda.Event(enable_timing=True))
+            evs[-1].record(stream)
+            scheme_ev.append(evs)
         return b
 
     def barrier():
@@ -369,6 +379,8 @@ def run_ours(args, rank, world, local):
     st = db.sync()
     ms = e0.elapsed_time(e1)
     step_ms = [e0.elapsed_time(ev[0])] + [ev[i - 1].elapsed_time(ev[i]) for i in range(1, args.steps)]
+    step_scheme_ms = {s: [round(evs[k].elapsed_time(evs[k + 1]), 4) for evs in scheme_ev]
+                      for k, s in enumerate(schemes)}
     phase_ms, n_sub = db.timing(reset=True)
     # per-scheme stats from the last step (committed + aborts), checked complete
     per = {}
@@ -432,6 +444,7 @@ def run_ours(args, rank, world, local):
             "abort_rate": sum(p["aborts"] for p in per.values()) / max(1, sum(p["commits"] for p in per.values())),
             "per_scheme": per,
             "step_ms": step_ms,
+            "step_scheme_ms": step_scheme_ms,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches_per_step(schemes, args.pipeline) * args.steps,

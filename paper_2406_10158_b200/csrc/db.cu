@@ -1018,8 +1018,10 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     // a2: reset CC state (every record of every table)
     p.mvcc_split = (scheme == CC_MVCC && (desc->flags & CC_FLAG_MVCC_SPLIT)) ? db->n_records : 0;
     p.meta_stride = scheme != CC_MVCC ? GC_META_STRIDE : 1u;
-    CUDA_TRY(db, launch_reset_meta(scheme, db->meta, db->n_records, db->ring, db->ring_cap, db->ctl,
-                                   db->stream, p.mvcc_split != 0, p.meta_stride));
+    // (GaccO / GPUTx keep no per-record control word: their cursors and K-set counters are
+    // reset by a3, so only the ring and the control block are cleared for them)
+    CUDA_TRY(db, launch_reset_meta(scheme, db->meta, det ? 0 : db->n_records, db->ring, db->ring_cap,
+                                   db->ctl, db->stream, p.mvcc_split != 0, p.meta_stride));
     CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
     if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
         const uint32_t wpr = db->tpcc.W / db->world;
@@ -1088,7 +1090,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     // a7: commit positions + result copy-out
     cc_result r = *res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
-    CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream));
+    CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream,
+                                 scheme == CC_TPL_NW || scheme == CC_TPL_WD));
     if (used) {   // a later cc_prepare of this batch may overwrite the buffers after this point
         CUDA_TRY(db, cudaEventRecord(used->consumed, db->stream));
         used->has_consumer = true;

@@ -155,7 +155,7 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
                                bool gputx, int grid, cudaStream_t s, int rank_block = 256);
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, bool two_pass, cudaStream_t s);
+                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket = false);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
 cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads, cudaStream_t s);
 

@@ -355,14 +355,24 @@ __global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long 
         for (int k = 0; k < 7; k++) stats[8 + k] = stages[k];
 }
 
+// 2PL: the lock-point ticket is drawn only by attempts that commit, so the committed
+// set's tickets are exactly 0 .. n_committed-1 and the ticket is the commit position
+__global__ void dense_ticket_pos_kernel(const u64 *lo, const uint8_t *committed, uint32_t *pos_out,
+                                        uint32_t n) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) pos_out[g] = committed[g] ? (uint32_t)lo[g] : 0xFFFFFFFFu;
+}
+
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, bool two_pass, cudaStream_t s) {
+                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket) {
     const uint32_t n = p.n_txn;
     const int blk = 256;
     const unsigned g = (n + blk - 1) / blk;
     // commit positions: a stable radix sort of the order keys (lo, then hi when used)
     uint32_t *pos = b.acc_pos;   // reuse as n-sized scratch after execution
-    if (deterministic) {
+    if (dense_ticket) {
+        dense_ticket_pos_kernel<<<g, blk, 0, s>>>(p.order_lo, p.committed, pos, n);
+    } else if (deterministic) {
         iota_kernel<<<g, blk, 0, s>>>(b.rank_order, n);
         commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
     } else {
