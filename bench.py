@@ -53,10 +53,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ceilings", action="store_true",
                     help="skip cc_roofline_probe (for ncu launch lists: its ring kernel is long)")
-    ap.add_argument("--pipeline", action="store_true",
-                    help="f-4: prepare GPUTx / GaccO for each step's batch on the low-priority prep stream "
-                         "(cc_prepare) while the other schemes execute.  Off by default: measured slower on "
-                         "B200, the persistent executors occupy every SM (profiles/r01_bench_v5_*)")
+    ap.add_argument("--pipeline", action=argparse.BooleanOptionalAction, default=True,
+                    help="f-4 (default on): prepare GPUTx / GaccO for each step's batch on the low-priority "
+                         "prep stream (cc_prepare) while the other schemes execute.  With the tuned launch "
+                         "(one block of 8-24 warps per SM) the rank pass runs beside the executors: 78 -> 85 M "
+                         "txn/s (profiles/r01_bench_v24_pipeline.jsonl); with full-occupancy grids it was "
+                         "slower (profiles/r01_bench_v5_*).  --no-pipeline: inline a3")
     ap.add_argument("--workload", default="ycsb", choices=["ycsb", "tpcc"],
                     help="ycsb = configs[1] (default); tpcc = configs[4]: W warehouses partitioned over the ranks")
     ap.add_argument("--warehouses", type=int, default=512)
@@ -364,8 +366,14 @@ def run_ours(args, rank, world, local):
         b = step(i)
         db.sync()
         b.free()
-    # fill the batch pool with one buffer set per timed step: no cudaMalloc while timing
-    for b in [db.gen_ycsb(args.batch, args.ops, args.write_frac, 0, T, A) for _ in range(args.steps)]:
+    # fill the batch pool with one buffer set per timed step (with --pipeline, prepared
+    # once, so each batch also owns its a3 buffers): no cudaMalloc while timing
+    pre = [db.gen_ycsb(args.batch, args.ops, args.write_frac, 0, T, A) for _ in range(args.steps)]
+    for b in pre:
+        prepare(b)
+    db.sync()
+    torch.cuda.synchronize(dev)
+    for b in pre:
         b.free()
     barrier()
     # ---- timed region
