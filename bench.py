@@ -590,7 +590,7 @@ def run_tpcc_loopback(args, local):
         bs = [db.gen_tpcc(n, 7919 * (r + 1) + i, args.tpcc_mix, w_lo=r * wpr, w_hi=(r + 1) * wpr)
               for r, db in enumerate(dbs)]
         for s in schemes:
-            if args.two_pc and s in ("tpl_nw", "tpl_wd"):
+            if args.two_pc and s not in ("gputx", "gacco"):
                 loopback_round_2pc(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms, True), lanes=32, watchdog_s=60)
             else:
                 loopback_round(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms, True), lanes=32, watchdog_s=60)
@@ -633,7 +633,7 @@ def run_tpcc_loopback(args, local):
                    "lanes_per_txn": 32, "parallelism": f"{G} warehouse partitions on 1 GPU, device-side exchange",
                    "launch": {s: tpcc_launch(args, s, 148, True) for s in schemes} if args.launch == "tuned"
                    else "bs 8, full-occupancy grid",
-                   "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic",
+                   "phase_b": "2PC rounds for the six non-deterministic schemes (f-2), deterministic for GPUTx/GaccO" if args.two_pc else "deterministic",
                    "timing": "host clock around fully synchronised steps (G streams + host-orchestrated exchange)"},
         "per_scheme": per, "clocks": clk}), flush=True)
     for db in dbs:
@@ -667,7 +667,7 @@ def run_tpcc(args, rank, world, local):
     def step(i):
         b = db.gen_tpcc(n, 7919 * (rank + 1) + i, args.tpcc_mix, w_lo=rank * wpr, w_hi=(rank + 1) * wpr)
         for s in schemes:
-            if world > 1 and args.two_pc and s in ("tpl_nw", "tpl_wd"):
+            if world > 1 and args.two_pc and s not in ("gputx", "gacco"):
                 dist_round_2pc(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
             elif world > 1:
                 dist_round(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
@@ -721,7 +721,7 @@ def run_tpcc(args, rank, world, local):
                        "launch": {s: tpcc_launch(args, s, 148) for s in schemes} if args.launch == "tuned"
                        else "bs 8, full-occupancy grid",
                        "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else ""),
-                       "phase_b": "2PC rounds for tpl_nw/tpl_wd (f-2), deterministic otherwise" if args.two_pc else "deterministic"},
+                       "phase_b": "2PC rounds for the six non-deterministic schemes (f-2), deterministic for GPUTx/GaccO" if args.two_pc else "deterministic"},
             "per_scheme": per, "clocks": clk,
             "gpu_launches": launches_per_step(schemes) * args.steps + (0 if world == 1 else
                                                                        6 * len(schemes) * args.steps),

@@ -239,8 +239,9 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
 #define CC_FLAG_FLAT_JITTER 0x200u   /* ablation: after waiting out a conflicting lock, retry
                                         with a flat 0..255 ns jitter instead of a window that
                                         doubles per restart (retry pacing) */
-#define CC_FLAG_PART_2PC 0x800u      /* with CC_FLAG_PARTITIONED, tpl_nw / tpl_wd: distributed
-                                        transactions in 2PC rounds under 2PL (cc_part_decide /
+#define CC_FLAG_PART_2PC 0x800u      /* with CC_FLAG_PARTITIONED, the six non-deterministic
+                                        schemes: distributed transactions in 2PC rounds under
+                                        the scheme's round rule (cc_part_decide /
                                         cc_part_commit / cc_part_next, f-2) */
 #define CC_FLAG_MVCC_SPLIT 0x400u    /* MVCC metadata layout ablation (PAPER.md:636
                                         attributes MVCC's gap to TO to its timestamps and version
@@ -347,16 +348,22 @@ cc_status cc_part_send(cc_db db, const void **send, uint64_t *counts);
 cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp);
 cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent);
 
-/* Scheme-native phase B for the 2PL family (cc_submit with
- * CC_FLAG_PARTITIONED | CC_FLAG_PART_2PC, schemes tpl_nw / tpl_wd): the distributed
- * transactions run in two-phase-commit rounds instead of the deterministic chains.  Per
- * round, every rank (collectively):
+/* Scheme-native phase B (cc_submit with CC_FLAG_PARTITIONED |
+ * CC_FLAG_PART_2PC, the six non-deterministic schemes; GPUTx / GaccO are deterministic and
+ * keep the gid-ordered chains): the distributed transactions run in two-phase-commit rounds
+ * instead of the deterministic chains.  Per round, every rank (collectively):
  *   cc_part_send    requests of its pending distributed transactions, as above;
  *   -- all-to-all #1 --
  *   cc_part_apply   PREPARE: the owner grants the round's requests item by item in global
- *                   transaction order, no-wait (shared unless an exclusive was granted,
- *                   exclusive only on a free item), and answers with the values read and
- *                   the vote in word 5 of each response;
+ *                   transaction order, no-wait, and answers with the values read and the
+ *                   vote in word 5 of each response.  2PL: shared unless an exclusive was
+ *                   granted, exclusive only on a free item.  TO / MVCC / Silo / TicToc,
+ *                   with the round's timestamps ts = (round, global gid): an access is
+ *                   granted unless an earlier write to the item was granted this round
+ *                   (TO: a read or write behind a pending older write waits -- here:
+ *                   retries next round; a write behind granted older reads is in
+ *                   timestamp order; OCC: the first writer takes the write lock, a read
+ *                   behind it would fail validation);
  *   -- reverse all-to-all #2 --
  *   cc_part_decide  DECIDE on the home: a transaction commits iff every access was granted;
  *                   committed ones are assembled with order key (1 << 63 | round, global

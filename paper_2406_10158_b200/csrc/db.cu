@@ -997,8 +997,9 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     const bool timing = desc->flags & CC_FLAG_TIMING;
     const bool partitioned = (desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) != 0;
     const bool two_pc = (desc->flags & CC_FLAG_PART_2PC) != 0;
-    if (two_pc && (!partitioned || (scheme != CC_TPL_NW && scheme != CC_TPL_WD)))
-        return fail(db, CC_ERR_UNSUPPORTED, "CC_FLAG_PART_2PC: 2PL schemes with CC_FLAG_PARTITIONED only");
+    if (two_pc && (!partitioned || scheme == CC_GPUTX || scheme == CC_GACCO))
+        return fail(db, CC_ERR_UNSUPPORTED,
+                    "CC_FLAG_PART_2PC: non-deterministic schemes with CC_FLAG_PARTITIONED only");
     if (partitioned) {
         const TpccState &T = db->tpcc;
         if (!is_tpcc) return fail(db, CC_ERR_UNSUPPORTED, "partitioned execution is TPC-C only (YCSB: replicas)");
@@ -1184,8 +1185,9 @@ cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp) {
             CUDA_TRY(db, dalloc(&P.vote, n));
             P.vote_cap = n;
         }
+        const bool ts_rule = P.p.scheme != CC_TPL_NW && P.p.scheme != CC_TPL_WD;
         CUDA_TRY(db, part_grant((PartReq *)recv, n, P.tp, (PartResp *)resp, P.vote, P.k1, P.k2, P.i1, P.i2,
-                                P.tmp, P.tmp_bytes, db->ctl, db->stream));
+                                P.tmp, P.tmp_bytes, db->ctl, db->stream, ts_rule));
         return CC_OK;
     }
     CUDA_TRY(db, part_apply((PartReq *)recv, n, P.tp, (PartResp *)resp, P.k1, P.k2, P.i1, P.i2, P.tmp,

@@ -195,7 +195,7 @@ cudaError_t part_finish(const TpccParams &y, uint32_t rank, uint32_t world, uint
 // repack the pending transactions for the next round
 cudaError_t part_grant(PartReq *req, uint64_t n, const TpccParams &y, PartResp *resp, uint8_t *vote,
                        unsigned long long *k1, unsigned long long *k2, uint32_t *i1, uint32_t *i2,
-                       void *tmp, size_t tmp_bytes, Ctl *ctl, cudaStream_t s);
+                       void *tmp, size_t tmp_bytes, Ctl *ctl, cudaStream_t s, bool ts_rule = false);
 cudaError_t part_decide(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
                         uint8_t *skip, const PartReq *sent, const PartResp *resp, uint64_t n_sent,
                         PartResp *stage, uint8_t *committed, unsigned long long *ohi,

@@ -241,8 +241,17 @@ __global__ void part_chain_kernel(const unsigned long long *skeys, const uint32_
 // conflict-free: the order key is (2^63 | round, global gid).  The oldest pending
 // transaction wins every item it asks for, so every round commits at least one (wait-die's
 // priority: the older proceeds, the younger dies and retries next round).
+// ts_rule (TO / MVCC / Silo / TicToc): with the round's timestamps (round, gid) every
+// item's chain is in timestamp order, so the only conflict left inside a round is an access
+// behind an older granted (pending) write -- TO makes it wait, MVCC's reader of an older
+// pending version waits for it, OCC's writer holds the write lock and a reader behind it
+// fails validation: it is denied and retries next round.  A write behind granted older
+// reads is in timestamp order and is granted (2PL refuses it: the shared holders).  The
+// committed set of a round is serializable in (round, gid) order, and the oldest pending
+// transaction is granted everything, so every round commits at least one.
 __global__ void part_grant_kernel(const unsigned long long *skeys, const uint32_t *sidx, uint64_t n,
-                                  const PartReq *req, TpccParams y, PartResp *resp, uint8_t *vote) {
+                                  const PartReq *req, TpccParams y, PartResp *resp, uint8_t *vote,
+                                  bool ts_rule) {
     const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     if (p > 0 && (skeys[p - 1] >> 24) == (skeys[p] >> 24)) return;   // chain head only
@@ -251,7 +260,7 @@ __global__ void part_grant_kernel(const unsigned long long *skeys, const uint32_
     for (uint64_t q = p; q < n && (skeys[q] >> 24) == (skeys[p] >> 24); q++) {
         const PartReq &r = req[sidx[q]];
         const bool w = part_is_write(r);
-        const bool g = w ? (!ex && sh == 0) : !ex;
+        const bool g = (w && !ts_rule) ? (!ex && sh == 0) : !ex;
         if (g) {
             if (w) ex = true;
             else sh++;
@@ -470,13 +479,13 @@ cudaError_t part_finish(const TpccParams &y, uint32_t rank, uint32_t world, uint
 // 2PC PREPARE on the owner: resolve + sort like part_apply, then grant per item chain
 cudaError_t part_grant(PartReq *req, uint64_t n, const TpccParams &y, PartResp *resp, uint8_t *vote,
                        unsigned long long *k1, unsigned long long *k2, uint32_t *i1, uint32_t *i2, void *tmp,
-                       size_t tmp_bytes, Ctl *ctl, cudaStream_t s) {
+                       size_t tmp_bytes, Ctl *ctl, cudaStream_t s, bool ts_rule) {
     if (n == 0) return cudaSuccess;
     part_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(req, n, y, k1, i1, ctl);
     size_t bytes = tmp_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, i1, i2, (int)n, 0, 62, s);
     if (e) return e;
-    part_grant_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k2, i2, n, req, y, resp, vote);
+    part_grant_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k2, i2, n, req, y, resp, vote, ts_rule);
     return cudaGetLastError();
 }
 

@@ -7,8 +7,10 @@ cc_part_finish (home assembles outputs / reserved slots, a7).  The collectives a
 all_to_all_single through torch.distributed (plumbing); `loopback_round` runs G
 partitions held by G dbs on one GPU with the same kernels, the exchange being a
 device-side permutation (concatenation of the per-destination slices).
-`dist_round_2pc` / `loopback_round_2pc`: the scheme-native variant for 2PL (f-2), phase B
-in two-phase-commit rounds with a third all-to-all (decisions).
+`dist_round_2pc` / `loopback_round_2pc`: the scheme-native variant (f-2) for the six
+non-deterministic schemes, phase B in two-phase-commit rounds with a third all-to-all
+(decisions); owners grant under 2PL locks or, for TO / MVCC / Silo / TicToc, in the
+round's timestamp order.
 """
 from __future__ import annotations
 
@@ -58,8 +60,8 @@ def dist_round(db, batch, scheme, result=None, group=None, via_cpu=False, **kw):
 
 
 def dist_round_2pc(db, batch, scheme, result=None, group=None, via_cpu=False, **kw):
-    """One partitioned submit whose distributed transactions run in 2PC rounds under 2PL
-    (f-2; all ranks call it collectively): per round requests (#1), grants + votes back
+    """One partitioned submit whose distributed transactions run in 2PC rounds under the
+    scheme's round rule (f-2; all ranks call it collectively): per round requests (#1), grants + votes back
     (#2), decisions (#3, 8 bytes per request), until no rank has pending transactions."""
     import torch.distributed as dist
     flags = kw.pop("flags", 0) | G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_2PC

@@ -87,11 +87,15 @@ def test_loopback_partitions(torch_cuda, orc, scheme, G_):
         db.close()
 
 
-# ---------------------------------------------------------------- f-2: 2PC phase B (2PL)
+# ---------------------------------------------------------------- f-2: 2PC phase B
+TWO_PC = ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc"]
+
+
 @pytest.mark.parametrize("G_", [2, 4])
-@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd"])
+@pytest.mark.parametrize("scheme", TWO_PC)
 def test_loopback_2pc(torch_cuda, orc, scheme, G_):
-    """Distributed transactions in 2PC rounds under 2PL: the merged result equals serial
+    """Distributed transactions in 2PC rounds under the scheme's round rule (2PL locks,
+    or timestamp order for TO / MVCC / Silo / TicToc): the merged result equals serial
     replay of phase A then the 2PC rounds in (round, gid) order."""
     from paper_2406_10158_b200.api import DB
     from paper_2406_10158_b200.partition import loopback_round_2pc
@@ -118,7 +122,7 @@ def test_loopback_2pc(torch_cuda, orc, scheme, G_):
         db.close()
 
 
-@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd"])
+@pytest.mark.parametrize("scheme", TWO_PC)
 def test_2pc_all_distributed_contention(torch_cuda, orc, scheme):
     """Every transaction through 2PC on one partition of 2 warehouses: heavy conflicts,
     many rounds, each committing a conflict-free set; aborts are counted as restarts."""
@@ -146,5 +150,5 @@ def test_2pc_rejects_other_schemes(torch_cuda):
     db.load_tpcc(1, 3, 256)
     b = db.gen_tpcc(256, 1, 5000)
     with pytest.raises(G.CCError, match="UNSUPPORTED"):
-        db.submit(b, "silo", flags=G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_2PC, lanes=32, bs=8)
+        db.submit(b, "gacco", flags=G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_2PC, lanes=32, bs=8)
     db.close()
