@@ -492,8 +492,9 @@ def config_key(args):
 
 def launches_per_step(schemes, pipelined=False):
     """Kernel launches issued by libgcctb per step: 1 generator + per scheme: reset 2,
-    exec 1, finalize (non-deterministic: iota + CUB radix sort (counted 1) + commit_pos
-    + copy_out = 4, TicToc +2; deterministic: iota + commit_pos + copy_out = 3), plus
+    exec 1, finalize (2PL: ticket positions + copy_out = 2; other non-deterministic: iota +
+    CUB radix sort (counted 1) + commit_pos + copy_out = 4, TicToc +2; deterministic: iota
+    + commit_pos + copy_out = 3), plus
     GaccO prep 6 (gather, sort, flags, scan, starts, positions) and GPUTx prep 13
     (pipelined: on the prep stream, + 1 error merge at submit)."""
     n = 1
@@ -501,6 +502,8 @@ def launches_per_step(schemes, pipelined=False):
         n += 3
         if s in ("gputx", "gacco"):
             n += 3 + (6 if s == "gacco" else 13) + (1 if pipelined else 0)
+        elif s in ("tpl_nw", "tpl_wd"):
+            n += 2
         else:
             n += 4 + (2 if s == "tictoc" else 0)
     return n
