@@ -154,3 +154,15 @@ def test_mvcc_split_layout(w4, orc, lanes):
     b = db.gen_tpcc(8192, 41, 5000)
     _run(db, S0, 4, b, "mvcc", lanes, orc, flags=CC_FLAG_MVCC_SPLIT)
     b.free()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("n,mix", [(1, 10000), (1, 0), (37, 10000), (1029, 5114)])
+def test_ragged_batches_and_pure_mixes(w4, orc, scheme, n, mix):
+    """A single transaction, batches that leave a partial last warp / block, and a
+    NewOrder-only mix (every line a stock RMW; Payment-only is covered above)."""
+    db, S0 = w4
+    b = db.gen_tpcc(n, 500 + n + mix, mix)
+    for lanes in (1, 32):
+        _run(db, S0, 4, b, scheme, lanes, orc, launch={"bs": 32 if n > 64 else 1})
+    b.free()

@@ -472,3 +472,51 @@ def test_import_async_host(c1, orc):
         db.sync()
         orc.check_ycsb("tictoc", S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
         b.free()
+
+
+# Ragged shapes: a single transaction, batch sizes that leave a partial last tile / warp /
+# block, K that leaves idle lanes in a 4/8/16-lane tile, K=1.
+RAGGED = [(1, 16), (4099, 5), (2053, 16), (777, 1), (33, 3)]
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("n,K", RAGGED)
+def test_ragged_shapes(c1, orc, scheme, n, K):
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(n, K, 0.5, 100 + n + K, T, A)
+    keys, ops = orc.ycsb_gen(100 + n + K, 1024, n, K, 0.5, T, A)
+    for lanes in [1] + [L for L in (4, 8, 16) if L >= K]:
+        db.snapshot(False)
+        res = db.submit(b, scheme, wd=0, bs=32 if n > 64 else 1, lanes=lanes)
+        st = db.sync()
+        assert st.commits == n, (lanes, st.commits)
+        h = res.host(db.stream)
+        assert int(h["restarts"].astype(np.int64).sum()) == st.aborts
+        orc.check_ycsb(scheme, S0, keys, ops, K, h, db.read_table(0))
+    b.free()
+
+
+def test_bad_geometry_is_rejected_before_enqueue(c1):
+    """include/gcctb.h: argument / config errors return before anything is enqueued and
+    leave the db usable."""
+    from paper_2406_10158_b200.gcctb import CCError, STATUS_NAMES
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    for n, K in [(0, 4), (16, 0), (16, 17), ((1 << 21) + 1, 4)]:
+        with pytest.raises(CCError) as e:
+            db.gen_ycsb(n, K, 0.5, 1, T, A)
+        assert STATUS_NAMES[e.value.status] in ("CONFIG", "INVALID_ARG")
+    with pytest.raises(CCError) as e:
+        db.import_ycsb(np.zeros(0, np.uint32), np.zeros(0, np.uint8), 4)
+    assert STATUS_NAMES[e.value.status] == "INVALID_ARG"
+    b = db.gen_ycsb(64, 8, 0.5, 1, T, A)
+    with pytest.raises(CCError) as e:      # an 8-op transaction does not fit a 4-lane tile
+        db.submit(b, "silo", lanes=4)
+    assert STATUS_NAMES[e.value.status] == "INVALID_ARG"
+    db.snapshot(False)
+    db.submit(b, "silo", lanes=8)          # the db is still usable
+    assert db.sync().commits == 64
+    b.free()
