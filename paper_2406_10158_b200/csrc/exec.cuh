@@ -295,6 +295,9 @@ GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
 #ifndef GC_GACCO_HOP_NS
 #define GC_GACCO_HOP_NS 600
 #endif
+#ifndef GC_GACCO_MAX_SLEEP_NS
+#define GC_GACCO_MAX_SLEEP_NS 50000u
+#endif
 GC_DEV bool gacco_turn(Th &th, u32 *cur, u32 pos) {
     u32 c = ld_acquire32(cur);
     if (c == pos) return true;
@@ -302,7 +305,8 @@ GC_DEV bool gacco_turn(Th &th, u32 *cur, u32 pos) {
     bool ok = true;
     while (pos - c > 1) {   // the cursor never passes pos before we release it
         const u32 d = pos - c - 1;
-        __nanosleep(d >= 80 ? 50000u : d * GC_GACCO_HOP_NS);
+        const u32 ns = d * GC_GACCO_HOP_NS;
+        __nanosleep(ns < GC_GACCO_MAX_SLEEP_NS ? ns : GC_GACCO_MAX_SLEEP_NS);
         if (dead(th)) { ok = false; break; }
         c = ld_relaxed32(cur);
     }
@@ -320,8 +324,13 @@ GC_DEV bool gacco_turn(Th &th, u32 *cur, u32 pos) {
 // long as the K-sets in between take (~1.5 us each at least, the measured hand-off).
 // Thousands of waiters polling the one kdone word at sub-microsecond periods saturated
 // its L2 slice, which also serves the rank_done counters of the frontier.
+#ifndef GC_KSET_MAX_SLEEP_NS
+#define GC_KSET_MAX_SLEEP_NS 50000u
+#endif
 GC_DEV unsigned kset_sleep_ns(u64 dist) {
-    return dist <= 1 ? 32u : (dist >= 34 ? 50000u : 1500u * (unsigned)(dist - 1));
+    if (dist <= 1) return 32u;
+    const u64 ns = 1500ull * (dist - 1);
+    return ns < GC_KSET_MAX_SLEEP_NS ? (unsigned)ns : GC_KSET_MAX_SLEEP_NS;
 }
 // wait until K-set k-1 is the frontier (every earlier K-set complete)
 GC_DEV bool kset_near(Th &th, const ExecParams &p, u32 k) {
