@@ -250,6 +250,12 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         instead of Table II's interleaved 16 B per record */
 #define CC_FLAG_INDEX_TREE 0x100u    /* force the cache-line search tree even on a dense key
                                         range (default there: direct addressing, key - k0) */
+#define CC_FLAG_WARM 0x2000u        /* tile mode, YCSB, the six non-deterministic schemes:
+                                        before a transaction's first attempt every lane waits
+                                        until its prefetched row and control word have
+                                        reached L2 (one load per 32 B sector), so a lock /
+                                        pending write is held across L2 latencies only, not
+                                        across its cold rows' HBM misses.  Same results. */
 #define CC_FLAG_INDEX_EYTZ 0x1000u   /* index lookups in the Eytzinger (BFS) layout of the same
                                         sorted keys: a branch-free
                                         descent over a complete binary tree padded to 2^h - 1

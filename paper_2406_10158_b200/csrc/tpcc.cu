@@ -376,6 +376,8 @@ struct TpccWL {
         prefetch_l2(p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : cw(p, L.rec));
     }
 
+    static GC_DEV u64 warm(const ExecParams &, const TpccParams &, const Lane &) { return 0; }
+
     static GC_DEV u32 load_all(const ExecParams &p, const TpccParams &y, u32 gid, Lane *L) {
         const uint32_t *t = y.tx + (u64)gid * TPCC_TX_WORDS;
         const u32 n = t[TX_TYPE] == 0 ? 3 + t[TX_OLCNT] : 3;

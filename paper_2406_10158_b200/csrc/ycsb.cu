@@ -203,6 +203,14 @@ struct YcsbWL {
 
     static GC_DEV u64 *row(const YcsbParams &y, const Lane &L) { return y.rows + (u64)L.rec * 16u; }
 
+    // CC_FLAG_WARM: wait until the prefetched row and control word are in L2 -- one load
+    // per 32 B sector, folded into a value the caller consumes before its first CC step
+    static GC_DEV u64 warm(const ExecParams &p, const YcsbParams &y, const Lane &L) {
+        const u64 *rw = y.rows + (u64)L.rec * 16u;
+        const u64 *w = p.scheme == CC_MVCC ? mvcc_lo(p, L.rec) : cw(p, L.rec);
+        return ld_cg(rw) ^ ld_cg(rw + 4) ^ ld_cg(rw + 8) ^ ld_cg(rw + 12) ^ ld_relaxed(w);
+    }
+
     // op semantics (Z11): out = fp(row); a write buffers r[f]*G + ((gid<<4)|i) + 1 and
     // r[15] + 1 (installed at commit by the scheme).
     static GC_DEV void read(const YcsbParams &, Lane &L, u32 gid, u32 i, const u64 *src) {

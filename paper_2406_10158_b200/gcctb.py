@@ -33,6 +33,7 @@ CC_FLAG_FLAT_JITTER = 0x200
 CC_FLAG_MVCC_SPLIT = 0x400
 CC_FLAG_PART_2PC = 0x800
 CC_FLAG_INDEX_EYTZ = 0x1000
+CC_FLAG_WARM = 0x2000
 CC_SRC_HOST_ASYNC = 2
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48

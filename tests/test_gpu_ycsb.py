@@ -194,9 +194,10 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     b.free()
 
 
+@pytest.mark.parametrize("warm", [False, True])
 @pytest.mark.parametrize("theta", [0.6, 0.9])
 @pytest.mark.parametrize("scheme", SCHEMES)
-def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta):
+def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta, warm):
     """configs[1] at full size in exactly the launch bench.py times (bench.launch_of: tile
     16, per-scheme warps per SM, one block per SM), at the bench's theta and above."""
     import types
@@ -211,10 +212,30 @@ def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta):
     b = db.gen_ycsb(B, K, W, 79, T, A)
     keys, ops = orc.ycsb_gen(79, n, B, K, W, T, A)
     db.snapshot(False)
-    res = db.submit(b, scheme, lanes=16, watchdog_s=60, **la)
+    from paper_2406_10158_b200.gcctb import CC_FLAG_WARM
+    res = db.submit(b, scheme, lanes=16, watchdog_s=60, flags=CC_FLAG_WARM if warm else 0, **la)
     st = db.sync()
     assert st.commits == B
     orc.check_ycsb(scheme, S0, keys, ops, K, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
+@pytest.mark.parametrize("lanes", [4, 8, 16])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c1_parity_warm(c1, orc, scheme, lanes):
+    """CC_FLAG_WARM (wait for the lines to reach L2 before the first CC step) changes
+    timing only: same serial-replay parity at configs[0]."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_WARM
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 17, T, A)
+    keys, ops = orc.ycsb_gen(17, 1024, 1024, 4, 0.5, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=8, lanes=lanes, flags=CC_FLAG_WARM)
+    st = db.sync()
+    assert st.commits == 1024
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
     b.free()
 
 
