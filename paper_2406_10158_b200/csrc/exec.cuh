@@ -259,10 +259,13 @@ GC_DEV void w_add(const ExecParams &p, u64 *w, u64 v) {
 // for MVCC, which aborts less) -- basic TO under a read-hot key otherwise retries in a
 // storm that burns 31-bit timestamps (cap 10 at theta=0.8: 1.4 M vs 4.9 M).
 // profiles/r01_probe_v6..v11, v18.
+#ifndef GC_BACKOFF_CAP
+#define GC_BACKOFF_CAP 10u   // lock / OCC schemes: 64 ns << 10 = 65 us
+#endif
 template <int S>
 GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
     constexpr bool TS = S == CC_TO || S == CC_MVCC;
-    u32 CAP = 10u;
+    u32 CAP = GC_BACKOFF_CAP;
     if (TS) {
         const u64 n = atomicAdd(&p.ctl->pacing.v, 1ull);   // transactions backing off now
         constexpr u64 LO = S == CC_TO ? 1024 : 256;   // MVCC aborts less: fewer back off at once
@@ -368,9 +371,30 @@ GC_DEV void kset_done(const ExecParams &p, u32 k) {
 // OCC lock bit clear), bounded, add a little jitter, and retry; otherwise use the
 // randomised backoff.  This replaces a blind sleep (during which the lock is often
 // already free) by one L2 round trip, without turning a busy shared lock into a storm.
+#ifndef GC_JITTER_MAX_SHIFT
+#define GC_JITTER_MAX_SHIFT 11   // post-wait jitter window cap: 32 ns << 11 = 65 us
+#endif
+// Adaptive cap: while fewer than GC_JITTER_LO transactions are pacing after a lock wait,
+// the window stops growing at 32 ns << GC_JITTER_LO_SHIFT (~8 us; 0: static cap only).
+// A moderately contended batch ends in a tail of a few hot-record retriers whose 65 us
+// windows left the lock idle; a herd (theta >= 0.8, one TPC-C warehouse) keeps the wide
+// windows.  YCSB configs[1] theta=0.6, tuned launch: tpl_nw 107 -> 123, tpl_wd 126 ->
+// 142 M txn/s; theta=0.8 and TPC-C at 1 / 64 warehouses unchanged; a static 8 us cap
+// instead cost wait-die 40 % at theta=0.8 (profiles/r01_pacing_v39_v40/).
+#ifndef GC_JITTER_LO
+#define GC_JITTER_LO 32
+#endif
+#ifndef GC_JITTER_LO_SHIFT
+#define GC_JITTER_LO_SHIFT 8
+#endif
 template <int S>
 GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
     if (th.cw) {
+        u32 jcap = GC_JITTER_MAX_SHIFT;
+        if (GC_JITTER_LO > 0) {
+            const u64 n = atomicAdd(&th.p->ctl->pacing_lk.v, 1ull);   // pacing after a lock wait now
+            if (n < (u64)GC_JITTER_LO) jcap = GC_JITTER_LO_SHIFT;
+        }
         const u32 sh = restarts < 10 ? restarts : 10;
         const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
         unsigned ns = 32;
@@ -380,13 +404,15 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         }
         // then a random delay whose window doubles per restart: waiters released by
         // the same unlock must not retry in lockstep (a herd livelock at theta >= 0.9)
-        const u32 win = (th.p->flags & CC_FLAG_FLAT_JITTER) ? 256u : 32u << (restarts < 11 ? restarts : 11);
+        const u32 win = (th.p->flags & CC_FLAG_FLAT_JITTER) ? 256u
+                                                               : 32u << (restarts < jcap ? restarts : jcap);
         u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % win);
         while (d > 0) {
             const u32 s = d < 1000u ? d : 1000u;
             __nanosleep(s);
             d -= s;
         }
+        if (GC_JITTER_LO > 0) atomicAdd(&th.p->ctl->pacing_lk.v, (u64)-1ll);
         th.cw = nullptr;
         return;
     }

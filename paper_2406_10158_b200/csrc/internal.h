@@ -36,6 +36,7 @@ struct Ctl {
     Counter events;     // CC_FLAG_EVENTS: event sequence counter
     Counter pacing;     // TO/MVCC: transactions in retry backoff right now (adaptive cap)
     Counter kdone;      // GPUTx: K-sets completed so far (they complete in order)
+    Counter pacing_lk;  // transactions in post-lock-wait jitter right now (adaptive cap)
     Counter warm_hits;  // CC_FLAG_WARM: sink for the warm loads (practically never incremented)
 };
 // one event of the debug log: 24 bytes
