@@ -182,3 +182,26 @@ def test_w4_parity_flags(w4, orc, scheme, mode):
     for lanes in (1, 32):
         _run(db, S0, 4, b, scheme, lanes, orc, flags=flags)
     b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 32])
+@pytest.mark.parametrize("scheme", ["tpl_nw", "tpl_wd", "to", "silo", "tictoc", "gputx", "gacco"])
+def test_w4_event_log_conflict_graph(w4, orc, scheme, lanes):
+    """f-4 debug mode on TPC-C: the device event log of the CC-managed accesses (W, D, C,
+    stock rows) yields an acyclic conflict graph with one commit event per
+    transaction.  (MVCC reads of older versions are not physical-order conflicts: MVCC is
+    covered by the replay.)"""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_EVENTS
+    from paper_2406_10158_b200.verify import check_serializable
+    db, S0 = w4
+    b = db.gen_tpcc(2048, 71, 5000)
+    db.events_capacity(1 << 22)
+    st = _run(db, S0, 4, b, scheme, lanes, orc, flags=CC_FLAG_EVENTS)
+    ev = db.events()
+    assert int((ev["kind"] == 2).sum()) == 2048
+    assert int((ev["kind"] == 3).sum()) == st.aborts
+    assert int((ev["kind"] == 0).sum()) > 0 and int((ev["kind"] == 1).sum()) > 0   # reads and installs logged
+    ok, info = check_serializable(ev)
+    assert ok, f"cycle {info}"
+    db.events_capacity(0)
+    b.free()
