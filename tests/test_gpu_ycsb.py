@@ -541,3 +541,24 @@ def test_bad_geometry_is_rejected_before_enqueue(c1):
     db.submit(b, "silo", lanes=8)          # the db is still usable
     assert db.sync().commits == 64
     b.free()
+
+
+@pytest.mark.parametrize("lanes", [1, 8])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c1_all_writes_extreme_contention(c1, orc, scheme, lanes):
+    """W=1, theta=0.99 on the 1,024-row table: every access a write, ~40 % of them on one
+    row -- the abort, retry-pacing, hot-first, wait-die intent and TO sequential paths all
+    fire; parity must hold and every transaction commits."""
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.99)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(512, 8, 1.0, 29, T, A)
+    keys, ops = orc.ycsb_gen(29, 1024, 512, 8, 1.0, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=0, bs=8, lanes=lanes, watchdog_s=60)
+    st = db.sync()
+    assert st.commits == 512
+    h = res.host(db.stream)
+    assert int(h["restarts"].astype(np.int64).sum()) == st.aborts
+    orc.check_ycsb(scheme, S0, keys, ops, 8, h, db.read_table(0))
+    b.free()
