@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--loopback", type=int, default=0,
                     help="tpcc: run G warehouse partitions as G dbs on this one GPU (a8 with a device-side exchange)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-tpcc", action="store_true", help="skip the TPC-C block of the YCSB line")
+    ap.add_argument("--no-index-binary", action="store_true", help="skip the binary-index pass")
     return ap.parse_args()
 
 
@@ -337,7 +339,10 @@ def run_ours(args, rank, world, local):
     scheme_ev = []   # timed steps: an event after each scheme's submit (per-step attribution)
     ev_pool = [[torch.cuda.Event(enable_timing=True) for _ in range(len(schemes) + 1)] for _ in range(args.steps)]
 
-    def step(i, timing=False):
+    def step(i, timing=False, keep=False):
+        """One step: a1 generation, f-4 preparation, then a2-a7 under every scheme.  The
+        batch is released after its last submit (its buffers return to the pool and the next
+        step's generation reuses them in stream order; cc_batch_free never blocks)."""
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
         prepare(b)
         evs = ev_pool[len(scheme_ev)] if timing else None   # created before the timed region
@@ -349,7 +354,10 @@ def run_ours(args, rank, world, local):
         if timing:
             evs[-1].record(stream)
             scheme_ev.append(evs)
-        return b
+        if keep:
+            return b
+        b.free()
+        return None
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -363,12 +371,11 @@ def run_ours(args, rank, world, local):
     clocks.start()
     time.sleep(0.5)
     for i in range(args.warmup):
-        b = step(i)
+        step(i)
         db.sync()
-        b.free()
-    # fill the batch pool with one buffer set per timed step (with --pipeline, prepared
-    # once, so each batch also owns its a3 buffers): no cudaMalloc while timing
-    pre = [db.gen_ycsb(args.batch, args.ops, args.write_frac, 0, T, A) for _ in range(args.steps)]
+    # the pool holds two prepared buffer sets (the steady loop recycles one; the last
+    # step keeps its batch): no cudaMalloc / cudaFree while timing -- asserted below
+    pre = [db.gen_ycsb(args.batch, args.ops, args.write_frac, 0, T, A) for _ in range(2)]
     for b in pre:
         prepare(b)
     db.sync()
@@ -382,14 +389,20 @@ def run_ours(args, rank, world, local):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     batches = []
     barrier()
+    mem0 = db.mem_stats()
     e0.record(stream)
     for i in range(args.steps):
-        batches.append(step(args.warmup + i, timing=True))
+        b = step(args.warmup + i, timing=True, keep=i == args.steps - 1)
+        if b is not None:
+            batches.append(b)
         ev[i].record(stream)
     e1.record(stream)
+    mem1 = db.mem_stats()
     barrier()
     clk = clocks.stop()
     st = db.sync()
+    allocs_timed = (mem1[0] - mem0[0], mem1[1] - mem0[1])
+    assert allocs_timed == (0, 0), f"device allocations inside the timed region: {allocs_timed}"
     ms = e0.elapsed_time(e1)
     step_ms = [e0.elapsed_time(ev[0])] + [ev[i - 1].elapsed_time(ev[i]) for i in range(1, args.steps)]
     step_scheme_ms = {s: [round(evs[k].elapsed_time(evs[k + 1]), 4) for evs in scheme_ev]
@@ -431,6 +444,11 @@ def run_ours(args, rank, world, local):
         exec_ms_total += pm[2]
         alg_bytes_total += ab
     # ---- e2e through the public API with host buffers
+    # the paper's index (binary search over the sorted keys) beside the
+    # direct-addressed headline: same batch, same launches, identical results
+    idx_bin = None
+    if args.index == "dense" and not args.no_index_binary:
+        idx_bin = index_pass(args, db, b, schemes, LA, res, CC_FLAG_INDEX_BINARY)
     e2e = run_e2e(args, db, bk, bo, schemes, res, dev, stream, barrier, world, xflags)
     b.free()
 
@@ -461,6 +479,8 @@ def run_ours(args, rank, world, local):
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches_per_step(schemes, args.pipeline) * args.steps,
+            "device_allocs_in_timed_region": {"cudaMalloc": allocs_timed[0], "cudaFree": allocs_timed[1]},
+            "step_ms_max_over_median": max(step_ms) / sorted(step_ms)[len(step_ms) // 2],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "exec_kernel (a4-a6), all schemes",
@@ -478,10 +498,120 @@ def run_ours(args, rank, world, local):
             tps, done, el, sample = oracle_replay_timed(args, args.cpu_seconds)
             line["cpu_baseline"] = {"value": tps, "unit": "txn/s", "cores": 1, "kind": "oracle",
                                     "sample": sample}
-        print(json.dumps(line), flush=True)
+        if idx_bin is not None:
+            line["index_binary"] = idx_bin
     db.close()
+    if rank == 0 and not args.no_tpcc:
+        line["tpcc"] = tpcc_block(args, local, schemes)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def index_pass(args, db, b, schemes, LA, res, flag):
+    """One timed submit per scheme of batch b with an index flag (untimed overall): the
+    per-scheme submit / exec times and the aggregate committed txn/s over the 8 submits."""
+    from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
+    out = {"index": "binary (PAPER.md:344)", "per_scheme": {}}
+    tot = 0.0
+    for s in schemes:
+        db.submit(b, s, **LA[s], flags=flag, result=res[s], watchdog_s=60, lanes=args.lanes)   # warm
+        db.sync()
+        db.timing(reset=True)
+        db.submit(b, s, **LA[s], flags=flag | CC_FLAG_TIMING, result=res[s], watchdog_s=60, lanes=args.lanes)
+        db.sync()
+        pm, _ = db.timing(reset=True)
+        out["per_scheme"][s] = {"submit_ms": pm[4], "exec_ms": pm[2], "txn_s": args.batch / (pm[4] / 1e3)}
+        tot += pm[4]
+    out["value"] = len(schemes) * args.batch / (tot / 1e3)
+    out["unit"] = "txn/s"
+    return out
+
+
+# TPC-C launches per configuration (tile mode, a warp per transaction; profiles/r01_tpcc_launch.txt):
+# (warps per block, blocks: 0 = full-occupancy grid, else blocks = SMs).  One warehouse: one
+# warp per SM (the hot W row's hand-off chain decides, fewer resident transactions collide
+# less); 64 warehouses: 8 warps per SM; 512 warehouses: the full grid, GaccO 16 warps per SM.
+TPCC_CONFIGS = [
+    {"name": "configs2_1wh_16K_50:50", "W": 1, "n": 16384, "mix": 5000, "launch": {"*": (1, True)}},
+    {"name": "configs3_64wh_64K_45:43", "W": 64, "n": 65536, "mix": 5114, "launch": {"*": (8, True)}},
+    {"name": "configs4_shape_512wh_64K_45:43_1gpu", "W": 512, "n": 65536, "mix": 5114,
+     "launch": {"*": (8, False), "gacco": (16, True)}},
+]
+
+
+def tpcc_alg_bytes(tx):
+    """SURVEY.md §8(d) algorithmic bytes of a TPC-C batch: NewOrder 320 B of header rows
+    (W, D, C reads, D update, O / NO slots) + 258 B per line (I 82 + S 112 RMW + OL 64);
+    Payment 600 B + 1,000 B for a BC customer's c_data rewrite (10 % of customers, counted
+    at that expectation: +100 B); 16 B per CC-managed access (word acquire + release);
+    160 B of descriptor per transaction."""
+    import numpy as np
+    t = tx.reshape(-1, 40)
+    no = t[:, 0] == 0
+    lines = int(t[no, 8].sum())
+    n_no, n_pay = int(no.sum()), int((~no).sum())
+    b = n_no * 320 + lines * 258 + n_pay * 700
+    b += 16 * (3 * n_no + lines + 3 * n_pay) + 160 * len(t)
+    return b
+
+
+def tpcc_block(args, local, schemes):
+    """configs[2], configs[3] and the configs[4] shape on one GPU: per scheme, median of 3
+    timed submits (a2-a7, CUDA events on the db stream) of fresh seeded batches after one
+    warm-up submit; committed txn/s, abort rate, exec ms and the exec kernel's algorithmic
+    GB/s against the HBM peak."""
+    import numpy as np
+    import torch
+
+    from paper_2406_10158_b200.api import DB, Result
+    from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    peak = peaks["hbm_gbs"] if peaks else 6650.0
+    out = {}
+    for cfg in TPCC_CONFIGS:
+        db = DB(local)
+        db.load_tpcc(cfg["W"], 1, cfg["n"])
+        res = Result.alloc(cfg["n"], 18, dev, stream=db.stream, out_words=48)
+        per = {}
+        tot_ms, tot_commits = 0.0, 0
+        for s in schemes:
+            bs, per_sm = cfg["launch"].get(s, cfg["launch"]["*"])
+            la = {"bs": bs, "grid": db.num_sms if per_sm else 0}
+            sub, exe, ab, cm = [], [], 0, 0
+            alg = 0
+            for r in range(4):
+                b = db.gen_tpcc(cfg["n"], 101 + r, cfg["mix"])
+                if r == 3:
+                    alg = tpcc_alg_bytes(b.export_tpcc())
+                db.timing(reset=True)
+                db.submit(b, s, **la, lanes=32, flags=CC_FLAG_TIMING, result=res, watchdog_s=120)
+                st = db.sync()
+                pm, _ = db.timing(reset=True)
+                b.free()
+                if r == 0:
+                    continue   # warm-up
+                assert st.commits == cfg["n"], (cfg["name"], s, st.commits)
+                sub.append(pm[4])
+                exe.append(pm[2])
+                ab += st.aborts
+                cm += st.commits
+            sub.sort()
+            exe.sort()
+            gbs = alg / (exe[1] / 1e3) / 1e9
+            per[s] = {"txn_s": cfg["n"] / (sub[1] / 1e3), "abort_rate": ab / max(1, cm), "submit_ms": sub[1],
+                      "exec_ms": exe[1], "launch": la, "exec_alg_GBps": gbs, "exec_hbm_frac": gbs / peak}
+            tot_ms += sub[1]
+            tot_commits += cfg["n"]
+        out[cfg["name"]] = {"value": tot_commits / (tot_ms / 1e3), "unit": "txn/s", "warehouses": cfg["W"],
+                            "batch": cfg["n"], "neworder_permyriad": cfg["mix"], "lanes_per_txn": 32,
+                            "per_scheme": per}
+        db.close()
+        del res
+        torch.cuda.empty_cache()
+    return out
 
 
 def config_key(args):
@@ -523,7 +653,7 @@ def run_e2e(args, db, keys, ops, schemes, res, dev, stream, barrier, world, xfla
                 torch.empty(args.batch, dtype=torch.int32).pin_memory(),
                 torch.empty(args.batch * args.ops, dtype=torch.int64).pin_memory()) for s in schemes}
     d2h = torch.cuda.Stream(dev)
-    n_steps = max(2, min(args.steps, 5))
+    n_steps = max(2, args.steps)
 
     def run(n):
         b = db.import_ycsb(pk[0], po[0], args.ops, async_host=True)

@@ -137,6 +137,9 @@ typedef struct {
 cc_status cc_load_ycsb(cc_db db, const cc_ycsb_db_desc *desc);
 
 /* On-device YCSB batch generator.
+ * A device-side generator failure (a transaction whose distinct keys could not be drawn:
+ * CONFIG) is recorded in the batch itself; every cc_submit of the batch then executes
+ * nothing and cc_sync returns CONFIG.  STATE while a partitioned submit is pending.
  * thresholds: u64[n_rows] Zipf inverse-CDF table (see inputs/ycsb.py), host or device
  * per thresholds_on_device; it is read during the call (device) or copied (host).
  * Key = ((rank-1) * scramble_mult) mod n_rows; duplicates within a transaction are
@@ -170,11 +173,21 @@ cc_status cc_batch_export_ycsb(cc_db db, cc_batch b, uint32_t *keys, uint8_t *op
 /* Batch geometry. */
 cc_status cc_batch_info(cc_db db, cc_batch b, uint32_t *n_txn, uint32_t *ops_per_txn,
                         uint32_t *kind);
-/* Release a batch.  Its device buffers go to a per-db pool (up to 16 batches) and are
- * reused, in db-stream order, by the next batch of the same kind and shape, so that a
- * steady stream of batches makes no cudaMalloc / cudaFree calls; the handle is invalid
- * afterwards (it may come back from a later gen / import).  cc_db_destroy frees the pool. */
+/* Release a batch.  Its device buffers (and any buffers cc_prepare attached to it) go to
+ * a per-db pool and are reused, in stream order, by the next batch of the same kind and
+ * shape, so that a steady stream of batches makes no cudaMalloc / cudaFree calls (each is
+ * an implicit device synchronisation).  Never blocks the host: the reuse waits on the
+ * device for the old batch's readers (db stream, and the prep stream via an event).  The
+ * handle is invalid afterwards (it may come back from a later gen / import).  STATE for
+ * the batch of a pending partitioned submit.  cc_pool_trim / cc_db_destroy free the pool. */
 cc_status cc_batch_free(cc_db db, cc_batch b);
+/* Free the pooled buffers of released batches (waits for the db's streams). */
+cc_status cc_pool_trim(cc_db db);
+/* Process-wide counters of the driver's device allocations: number of cudaMalloc and
+ * cudaFree calls and bytes allocated since the library was loaded (any pointer may be
+ * NULL).  A steady batch loop (gen / prepare / submit / free) leaves the first two
+ * unchanged once the pool holds its batches (bench.py asserts it over the timed region). */
+cc_status cc_mem_stats(cc_db db, uint64_t *n_allocs, uint64_t *n_frees, uint64_t *bytes_allocated);
 
 /* ----------------------------------------------------------------- TPC-C
  * TPC-C NewOrder + Payment.  Creates, in this order, the CC-managed

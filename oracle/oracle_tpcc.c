@@ -17,7 +17,10 @@
  *
  * Pins (tests/test_oracle_tpcc.py): TPC-C §3.3.2 consistency conditions 1-4, 8-9 in
  * delta form, per-customer and per-stock conservation, a hand-worked NewOrder total,
- * NURand range / non-uniformity, remote rates, and serial-order sensitivity.
+ * NURand range / non-uniformity, remote rates, and serial-order sensitivity;
+ * tests/test_oracle_pins.py: a hand-worked BC Payment (c_data rewrite, h_data, history,
+ * tests/golden/tpcc_payment_bc.json) and orc_tpcc_accesses against the rows a replay
+ * writes / the rows whose perturbation changes the output.
  */
 #include <stdint.h>
 #include <stdlib.h>

@@ -22,8 +22,9 @@
  * shared keys, Zipf hottest-key frequency vs the Hurwitz-zeta closed form, binomial
  * bounds on W, SPEC.md worked examples for ranks / access tables (tests/golden/),
  * and same-rank non-conflict + minimality for ranks.  The fingerprint fp() and the
- * affine write are readings (Z11) with no paper value: "parity unpinned" for their
- * exact constants, pinned only through the invariants above.
+ * affine write are readings (Z11) with no paper value; tests/test_oracle_pins.py pins
+ * them with closed forms on rows of special structure (single words, top bits, all-ones,
+ * zero / one fields), so a wrong rotation, word, field, "+1" or counter fails.
  */
 #include <stdint.h>
 #include <stdlib.h>

@@ -354,5 +354,14 @@ class DB:
         self._chk(G.lib().cc_roofline_probe(self.h, ctypes.byref(r)))
         return {k: getattr(r, k) for k, _ in r._fields_}
 
+    def mem_stats(self) -> tuple[int, int, int]:
+        """(cudaMalloc calls, cudaFree calls, bytes allocated) of the driver so far."""
+        a, f, b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self._chk(G.lib().cc_mem_stats(self.h, ctypes.byref(a), ctypes.byref(f), ctypes.byref(b)))
+        return a.value, f.value, b.value
+
+    def pool_trim(self):
+        self._chk(G.lib().cc_pool_trim(self.h))
+
     def snapshot(self, save: bool):
         self._chk(G.lib().cc_snapshot(self.h, 1 if save else 0))

@@ -17,6 +17,16 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 FLAGS += os.environ.get("GCCTB_NVCC_EXTRA", "").split()
 
 
+STAMP = os.path.join(HERE, ".libgcctb.flags")
+
+
+def _flags_id() -> str:
+    """The compile command (flags + GCCTB_NVCC_EXTRA): an ablation build is never mistaken
+    for the shipped one."""
+    import hashlib
+    return hashlib.sha256(" ".join([NVCC] + FLAGS).encode()).hexdigest()[:16]
+
+
 def _deps():
     files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     files.append(os.path.join(os.path.dirname(HERE), "include", "gcctb.h"))
@@ -24,7 +34,8 @@ def _deps():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
+    same_flags = os.path.exists(STAMP) and open(STAMP).read().strip() == _flags_id()
+    if not force and os.path.exists(LIB) and same_flags:
         mt = os.path.getmtime(LIB)
         if all(os.path.getmtime(f) <= mt for f in _deps()):
             return LIB
@@ -43,12 +54,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError(f"nvcc failed on {s}")
+    # register / spill report of the build (compile times dropped: the file only changes
+    # when the code or the flags do)
+    text = "\n".join(l for l in "\n".join(log).splitlines() if "Compile time" not in l) + "\n"
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
-        f.write("\n".join(log))
+        f.write(text)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs
     subprocess.check_call(cmd)
     for o in objs:
         os.remove(o)
+    with open(STAMP, "w") as f:
+        f.write(_flags_id() + "\n")
     if verbose:
         print("\n".join(log))
     return LIB

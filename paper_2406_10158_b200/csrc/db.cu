@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
+#include <atomic>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -22,6 +23,22 @@ int rank_kernel_grid();
 
 using namespace gcctb;
 typedef unsigned long long u64;
+
+// Every device allocation / free the driver makes goes through dalloc / dfree, which count
+// them (cc_mem_stats): the bench asserts that a timed loop of steps makes none (a
+// cudaMalloc / cudaFree is an implicit device synchronisation).
+static std::atomic<uint64_t> g_allocs{0}, g_frees{0}, g_alloc_bytes{0};
+template <class T>
+static cudaError_t dalloc(T **p, size_t bytes) {
+    g_allocs++;
+    g_alloc_bytes += bytes ? bytes : 16;
+    return cudaMalloc((void **)p, bytes ? bytes : 16);
+}
+static void dfree(void *p) {
+    if (!p) return;
+    g_frees++;
+    cudaFree(p);
+}
 
 struct Table {
     std::string name;
@@ -63,7 +80,7 @@ static cudaError_t build_tree(Index &ix, cudaStream_t s) {
         const uint64_t nodes = padded / 16;
         const uint64_t out_padded = (nodes + 15) / 16 * 16;
         u64 *out = nullptr;
-        cudaError_t e = cudaMalloc((void **)&out, out_padded * 8);
+        cudaError_t e = dalloc(&out, out_padded * 8);
         if (e) return e;
         e = launch_tree_level(in, n_in, out, out_padded, s);
         if (e) return e;
@@ -77,8 +94,8 @@ static cudaError_t build_tree(Index &ix, cudaStream_t s) {
     int h = 1;
     while (((1ull << h) - 1) < ix.n) h++;
     ix.eytz_n = (1ull << h) - 1;
-    cudaError_t e = cudaMalloc((void **)&ix.eytz_keys, (ix.eytz_n + 1) * 8);
-    if (!e) e = cudaMalloc((void **)&ix.eytz_rows, (ix.eytz_n + 1) * 8);
+    cudaError_t e = dalloc(&ix.eytz_keys, (ix.eytz_n + 1) * 8);
+    if (!e) e = dalloc(&ix.eytz_rows, (ix.eytz_n + 1) * 8);
     if (!e) e = launch_eytz_build(ix.keys, ix.rowids, ix.n, h, ix.eytz_keys, ix.eytz_rows, s);
     if (e) return e;
     return cudaStreamSynchronize(s);
@@ -116,7 +133,10 @@ struct cc_batch_s {
     uint32_t *keys;   // YCSB
     uint8_t *ops;     // YCSB
     uint32_t *tx;     // TPC-C descriptors
+    u64 *err = nullptr;            // a1 error word of this batch (generator failure), merged at submit
     cudaEvent_t ready = nullptr;   // recorded on the db stream after generation / import
+    cudaEvent_t idle = nullptr;    // pooled: the prep stream's last read of the batch (cc_batch_free)
+    bool idle_rec = false;
     // f-4: a3 results prepared ahead on the prep stream, slot 0 = GPUTx, 1 = GaccO
     struct Prepared {
         PrepBufs b{};
@@ -249,10 +269,6 @@ static cc_status fail(cc_db db, cc_status st, const char *fmt, ...) {
             return fail(db, CC_ERR_CUDA, "cudaSetDevice(%d) failed", (db)->device); \
     } while (0)
 
-template <class T>
-static cudaError_t dalloc(T **p, size_t bytes) {
-    return cudaMalloc((void **)p, bytes ? bytes : 16);
-}
 
 extern "C" {
 
@@ -305,9 +321,9 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
 }
 
 static void free_scratch(cc_db db) {
-    cudaFree(db->committed); cudaFree(db->restarts); cudaFree(db->ohi); cudaFree(db->olo);
-    cudaFree(db->ring);
-    for (void *p : db->prep_allocs) cudaFree(p);
+    dfree(db->committed); dfree(db->restarts); dfree(db->ohi); dfree(db->olo);
+    dfree(db->ring);
+    for (void *p : db->prep_allocs) dfree(p);
     db->prep_allocs.clear();
     db->committed = nullptr; db->restarts = nullptr; db->ohi = db->olo = nullptr; db->ring = nullptr;
     db->cap_txn = 0;
@@ -315,13 +331,15 @@ static void free_scratch(cc_db db) {
 }
 
 static void free_batch_mem(cc_batch b) {
-    cudaFree(b->keys);
-    cudaFree(b->ops);
-    cudaFree(b->tx);
+    dfree(b->keys);
+    dfree(b->ops);
+    dfree(b->tx);
+    dfree(b->err);
     if (b->ready) cudaEventDestroy(b->ready);
+    if (b->idle) cudaEventDestroy(b->idle);
     for (auto &q : b->prep) {
-        for (void *a : q.allocs) cudaFree(a);
-        cudaFree(q.ctl);
+        for (void *a : q.allocs) dfree(a);
+        dfree(q.ctl);
         if (q.done) cudaEventDestroy(q.done);
         if (q.consumed) cudaEventDestroy(q.consumed);
     }
@@ -332,36 +350,36 @@ cc_status cc_db_destroy(cc_db db) {
     if (!db) return CC_ERR_INVALID_ARG;
     cudaSetDevice(db->device);
     cudaStreamSynchronize(db->stream);
-    for (auto &t : db->tables) cudaFree(t.d);
+    for (auto &t : db->tables) dfree(t.d);
     for (auto &i : db->indexes) {
-        cudaFree(i.keys);
-        cudaFree(i.rowids);
-        for (u64 *l : i.levels) cudaFree(l);
-        cudaFree(i.eytz_keys);
-        cudaFree(i.eytz_rows);
+        dfree(i.keys);
+        dfree(i.rowids);
+        for (u64 *l : i.levels) dfree(l);
+        dfree(i.eytz_keys);
+        dfree(i.eytz_rows);
     }
-    for (void *p : db->snap) cudaFree(p);
+    for (void *p : db->snap) dfree(p);
     cudaStreamSynchronize(db->prep_stream);
     for (auto *b : db->batches) free_batch_mem(b);
     for (auto *b : db->pool) free_batch_mem(b);
-    cudaFree(db->tpcc.nidx_start); cudaFree(db->tpcc.nidx_count); cudaFree(db->tpcc.nidx_rows);
+    dfree(db->tpcc.nidx_start); dfree(db->tpcc.nidx_count); dfree(db->tpcc.nidx_rows);
     for (auto &pe : db->pending) for (auto &e : pe.ev) cudaEventDestroy(e);
     for (auto &pe : db->free_events) for (auto &e : pe.ev) cudaEventDestroy(e);
     free_scratch(db);
-    cudaFree(db->part.skip); cudaFree(db->part.send); cudaFree(db->part.stage);
-    cudaFree(db->part.cnt); cudaFree(db->part.off); cudaFree(db->part.cursor);
-    cudaFree(db->part.k1); cudaFree(db->part.k2); cudaFree(db->part.i1); cudaFree(db->part.i2);
-    cudaFree(db->part.tmp);
-    cudaFree(db->part.vote);
-    cudaFree(db->part.dec);
-    cudaFree(db->arena);
-    cudaFree(db->latch);
-    cudaFree(db->stages);
-    cudaFree(db->events);
-    cudaFree(db->meta);
-    cudaFree(db->ctl);
-    cudaFree(db->stats_scratch);
-    cudaFree(db->sticky_dev);
+    dfree(db->part.skip); dfree(db->part.send); dfree(db->part.stage);
+    dfree(db->part.cnt); dfree(db->part.off); dfree(db->part.cursor);
+    dfree(db->part.k1); dfree(db->part.k2); dfree(db->part.i1); dfree(db->part.i2);
+    dfree(db->part.tmp);
+    dfree(db->part.vote);
+    dfree(db->part.dec);
+    dfree(db->arena);
+    dfree(db->latch);
+    dfree(db->stages);
+    dfree(db->events);
+    dfree(db->meta);
+    dfree(db->ctl);
+    dfree(db->stats_scratch);
+    dfree(db->sticky_dev);
     if (db->own_stream) cudaStreamDestroy(db->stream);
     cudaStreamDestroy(db->prep_stream);
     cudaStreamSynchronize(db->copy_stream);
@@ -393,7 +411,7 @@ static cc_status create_table(cc_db db, const char *name, uint32_t row_bytes, ui
         u64 *meta = nullptr;
         CUDA_TRY(db, dalloc(&meta, need * 8 * (GC_META_STRIDE > 2 ? GC_META_STRIDE : 2)));
         CUDA_TRY(db, cudaStreamSynchronize(db->stream));
-        if (db->meta) cudaFree(db->meta);
+        if (db->meta) dfree(db->meta);
         db->meta = meta;
         db->meta_records = need;
         db->n_records = need;
@@ -530,14 +548,17 @@ static cudaError_t batch_ready(cc_db db, cc_batch b, cudaStream_t s = nullptr) {
     return cudaEventRecord(b->ready, s ? s : db->stream);
 }
 
-constexpr size_t BATCH_POOL_MAX = 16;
-
 static cc_status new_batch(cc_db db, uint32_t n_txn, uint32_t K, cc_batch *out, uint32_t kind = KIND_YCSB) {
+    if (db->part.pending) return fail(db, CC_ERR_STATE, "a partitioned submit is pending (cc_part_finish first)");
     for (size_t i = 0; i < db->pool.size(); i++) {
         cc_batch b = db->pool[i];
         if (b->kind != kind || b->n_txn != n_txn || b->K != K) continue;
         db->pool.erase(db->pool.begin() + i);
         for (auto &q : b->prep) q.valid = false;
+        // the new contents are written on the db stream: after the prep stream's last read
+        if (b->idle_rec) CUDA_TRY(db, cudaStreamWaitEvent(db->stream, b->idle, 0));
+        b->idle_rec = false;
+        CUDA_TRY(db, cudaMemsetAsync(b->err, 0, 8, db->stream));
         db->batches.push_back(b);
         *out = b;
         return CC_OK;
@@ -552,10 +573,13 @@ static cc_status new_batch(cc_db db, uint32_t n_txn, uint32_t K, cc_batch *out, 
     cudaError_t e = kind == KIND_YCSB
                         ? (dalloc(&b->keys, (size_t)n_txn * K * 4) ?: dalloc(&b->ops, (size_t)n_txn * K))
                         : dalloc(&b->tx, (size_t)n_txn * TPCC_TX_WORDS * 4);
+    if (!e) e = dalloc(&b->err, 8);
+    if (!e) e = cudaMemsetAsync(b->err, 0, 8, db->stream);
     if (e) {
-        cudaFree(b->keys);
-        cudaFree(b->ops);
-        cudaFree(b->tx);
+        dfree(b->keys);
+        dfree(b->ops);
+        dfree(b->tx);
+        dfree(b->err);
         delete b;
         return fail(db, CC_ERR_OOM, "batch allocation failed");
     }
@@ -582,12 +606,11 @@ cc_status cc_batch_gen_ycsb(cc_db db, const cc_ycsb_gen_desc *g, cc_batch *out) 
         CUDA_TRY(db, cudaMemcpyAsync(tmp, g->thresholds, n * 8, cudaMemcpyHostToDevice, db->stream));
         T = tmp;
     }
-    CUDA_TRY(db, cudaMemsetAsync(db->ctl, 0, sizeof(Ctl), db->stream));
     CUDA_TRY(db, launch_ycsb_gen(b->keys, b->ops, g->n_txn, g->ops_per_txn, n, g->write_frac,
-                                 g->seed, T, g->scramble_mult % n, db->ctl, db->stream));
+                                 g->seed, T, g->scramble_mult % n, b->err, db->stream));
     if (tmp) {
         CUDA_TRY(db, cudaStreamSynchronize(db->stream));
-        cudaFree(tmp);
+        dfree(tmp);
     }
     CUDA_TRY(db, batch_ready(db, b));
     *out = b;
@@ -642,20 +665,40 @@ cc_status cc_batch_free(cc_db db, cc_batch b) {
     if (!db || !b) return CC_ERR_INVALID_ARG;
     for (size_t i = 0; i < db->batches.size(); i++)
         if (db->batches[i] == b) {
+            if (db->part.pending && db->part.b == b)
+                return fail(db, CC_ERR_STATE, "the batch of a pending partitioned submit");
             bool prepared = false;
             for (auto &q : b->prep) prepared |= !q.allocs.empty();
-            // a prepare may still read the batch: the next writer (db stream) must wait for it
-            if (prepared) cudaStreamSynchronize(db->prep_stream);
-            if (db->pool.size() < BATCH_POOL_MAX) {
-                db->pool.push_back(b);
-            } else {
-                cudaStreamSynchronize(db->stream);
-                free_batch_mem(b);
+            // a prepare may still read the batch: the next writer (db stream) waits for this
+            // event when the buffers are reused -- no host synchronisation here
+            if (prepared) {
+                if (!b->idle) CUDA_TRY(db, cudaEventCreateWithFlags(&b->idle, cudaEventDisableTiming));
+                CUDA_TRY(db, cudaEventRecord(b->idle, db->prep_stream));
+                b->idle_rec = true;
             }
+            db->pool.push_back(b);
             db->batches.erase(db->batches.begin() + i);
             return CC_OK;
         }
     return fail(db, CC_ERR_INVALID_ARG, "unknown batch");
+}
+
+cc_status cc_pool_trim(cc_db db) {
+    CHECK_DB(db);
+    CUDA_TRY(db, cudaStreamSynchronize(db->prep_stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->copy_stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    for (auto *b : db->pool) free_batch_mem(b);
+    db->pool.clear();
+    return CC_OK;
+}
+
+cc_status cc_mem_stats(cc_db db, uint64_t *n_allocs, uint64_t *n_frees, uint64_t *bytes_allocated) {
+    if (!db) return CC_ERR_INVALID_ARG;
+    if (n_allocs) *n_allocs = g_allocs.load();
+    if (n_frees) *n_frees = g_frees.load();
+    if (bytes_allocated) *bytes_allocated = g_alloc_bytes.load();
+    return CC_OK;
 }
 
 
@@ -739,9 +782,8 @@ cc_status cc_batch_gen_tpcc(cc_db db, const cc_tpcc_gen_desc *g, cc_batch *out) 
     cc_batch b;
     cc_status st = new_batch(db, g->n_txn, TPCC_K, &b, KIND_TPCC);
     if (st) return st;
-    CUDA_TRY(db, cudaMemsetAsync(db->ctl, 0, sizeof(Ctl), db->stream));
     CUDA_TRY(db, launch_tpcc_gen(b->tx, g->n_txn, g->seed, T.W, g->w_lo, g->w_hi, g->neworder_permyriad,
-                                 T.c_run, T.c_id, T.c_item, db->ctl, db->stream));
+                                 T.c_run, T.c_id, T.c_item, b->err, db->stream));
     CUDA_TRY(db, batch_ready(db, b));
     *out = b;
     return CC_OK;
@@ -844,7 +886,7 @@ static cudaError_t alloc_prep(PrepBufs &b, std::vector<void *> &allocs, uint64_t
 static cc_status ensure_arena(cc_db db, uint64_t nodes, uint32_t row_words) {
     if (nodes <= db->arena_nodes && row_words == db->arena_row_words) return CC_OK;
     cudaStreamSynchronize(db->stream);
-    cudaFree(db->arena);
+    dfree(db->arena);
     db->arena = nullptr;
     db->arena_nodes = 0;
     CUDA_TRY(db, dalloc(&db->arena, nodes * (ARENA_HDR + row_words) * 8));
@@ -873,7 +915,7 @@ static cc_status ensure_part(cc_db db, uint32_t n_txn) {
     }
     if (n_txn <= P.cap_txn) return CC_OK;
     cudaStreamSynchronize(db->stream);
-    cudaFree(P.skip); cudaFree(P.send); cudaFree(P.stage); cudaFree(P.dec);
+    dfree(P.skip); dfree(P.send); dfree(P.stage); dfree(P.dec);
     CUDA_TRY(db, dalloc(&P.dec, (size_t)n_txn * TPCC_K * 8));
     CUDA_TRY(db, dalloc(&P.skip, n_txn));
     CUDA_TRY(db, dalloc(&P.send, (size_t)n_txn * TPCC_K * sizeof(PartReq)));
@@ -975,7 +1017,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (desc->flags & CC_FLAG_LATCHED) {   // one 32-bit latch per control word (Exp-7)
         if (db->latch_records < db->n_records) {
             cudaStreamSynchronize(db->stream);
-            cudaFree(db->latch);
+            dfree(db->latch);
             db->latch = nullptr;
             CUDA_TRY(db, dalloc(&db->latch, db->n_records * 8));
             db->latch_records = db->n_records;
@@ -1024,6 +1066,13 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     CUDA_TRY(db, launch_reset_meta(scheme, db->meta, det ? 0 : db->n_records, db->ring, db->ring_cap,
                                    db->ctl, db->stream, p.mvcc_split != 0, p.meta_stride));
     CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
+    CUDA_TRY(db, launch_merge_word(b->err, db->ctl, db->stream));   // a1 failure: nothing executes
+    {   // test hook (not part of the ABI): the TO / MVCC timestamp counter starts at
+        // GCCTB_TS_BASE instead of 0, so the 31-bit overflow path is reachable
+        const char *tb = getenv("GCCTB_TS_BASE");
+        const unsigned long long base = tb ? strtoull(tb, nullptr, 0) : 0ull;
+        if (base) CUDA_TRY(db, launch_fill_u64(&db->ctl->ts.v, base, 1, db->stream));
+    }
     if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
         const uint32_t wpr = db->tpcc.W / db->world;
         CUDA_TRY(db, part_classify_pack(tp, db->rank, db->world, wpr, b->n_txn, db->part.skip, db->part.cnt,
@@ -1168,7 +1217,7 @@ cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp) {
     if (n && (!recv || !resp)) return fail(db, CC_ERR_INVALID_ARG, "null buffers");
     if (n > P.recv_cap) {
         cudaStreamSynchronize(db->stream);
-        cudaFree(P.k1); cudaFree(P.k2); cudaFree(P.i1); cudaFree(P.i2); cudaFree(P.tmp);
+        dfree(P.k1); dfree(P.k2); dfree(P.i1); dfree(P.i2); dfree(P.tmp);
         CUDA_TRY(db, dalloc(&P.k1, n * 8));
         CUDA_TRY(db, dalloc(&P.k2, n * 8));
         CUDA_TRY(db, dalloc(&P.i1, n * 4));
@@ -1180,7 +1229,7 @@ cc_status cc_part_apply(cc_db db, void *recv, uint64_t n, void *resp) {
     if (P.two_pc) {   // PREPARE: grant per item in gid order, vote in resp[k].v[5]
         if (n > P.vote_cap) {
             cudaStreamSynchronize(db->stream);
-            cudaFree(P.vote);
+            dfree(P.vote);
             P.vote = nullptr;
             CUDA_TRY(db, dalloc(&P.vote, n));
             P.vote_cap = n;
@@ -1260,7 +1309,7 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent) {
 cc_status cc_events_capacity(cc_db db, uint64_t cap) {
     CHECK_DB(db);
     CUDA_TRY(db, cudaStreamSynchronize(db->stream));
-    cudaFree(db->events);
+    dfree(db->events);
     db->events = nullptr;
     db->events_cap = 0;
     if (cap) {
@@ -1347,7 +1396,7 @@ cc_status cc_timing_read(cc_db db, double ms[5], uint64_t *n_submits, int reset)
 cc_status cc_snapshot(cc_db db, int save) {
     CHECK_DB(db);
     if (save) {
-        for (void *p : db->snap) cudaFree(p);
+        for (void *p : db->snap) dfree(p);
         db->snap.clear();
         for (auto &t : db->tables) {
             void *p = nullptr;

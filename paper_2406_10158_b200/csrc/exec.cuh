@@ -633,6 +633,9 @@ GC_DEV int to_step(Th &th, const ExecParams &p, const typename WL::Params &y, ty
 
 template <class WL>
 GC_DEV void to_commit(Th &th, const ExecParams &p, const typename WL::Params &y, typename WL::Lane &L, u64 ts) {
+    // the pending bit was taken with an acquire-only CAS: a release fence orders it before
+    // the installs, so an optimistic reader that sees new row bytes also sees the bit
+    fence_acqrel();
     inst<WL>(th, y, L, WL::row(y, L));
     fence_acqrel();
     w_store_relaxed(p, cw(p, L.rec), to_make(false, ts, ts));
@@ -907,6 +910,7 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             key_hi = cts;
         }
         key_lo = ticket;
+        if (S == CC_TICTOC) fence_acqrel();   // locks (acquire-only CAS) before the installs (Silo: fenced above)
         for (u32 j = 0; j < n; j++)
             if (L[j].w) inst<WL>(th, y, L[j], WL::row(y, L[j]));
         fence_acqrel();
@@ -1186,6 +1190,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             key_hi = cts;
         }
         key_lo = ticket;
+        if (S == CC_TICTOC && act && L.w) fence_acqrel();   // locks (acquire-only CAS) before the installs
         if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         fence_acqrel();
         if (act && L.w) w_store_relaxed(p, cw(p, L.rec), nw);

@@ -156,6 +156,8 @@ cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBuf
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,
                                bool gputx, int grid, cudaStream_t s, int rank_block = 256);
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
+// a1: fold the batch's generator error word into the submit's control block (after a2)
+cudaError_t launch_merge_word(const unsigned long long *err, Ctl *dst, cudaStream_t s);
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket = false);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
@@ -176,7 +178,7 @@ cudaError_t build_name_index(const unsigned long long *cu, uint32_t n_cust,
                              uint32_t *idx_rows, uint32_t n_groups, cudaStream_t s);
 cudaError_t launch_tpcc_gen(uint32_t *tx, uint32_t n_txn, unsigned long long seed, uint32_t W,
                             uint32_t w_lo, uint32_t w_hi, uint32_t no_pm, uint32_t c_last_run,
-                            uint32_t c_id_c, uint32_t c_item_c, Ctl *ctl, cudaStream_t s);
+                            uint32_t c_id_c, uint32_t c_item_c, unsigned long long *err, cudaStream_t s);
 
 struct PartReq;
 struct PartResp;
@@ -222,7 +224,7 @@ cudaError_t launch_index_lookup(const YcsbParams &y, const unsigned long long *k
 cudaError_t launch_fill_u64(unsigned long long *p, unsigned long long v, uint64_t n, cudaStream_t s);
 cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                             uint64_t n_rows, double W, uint64_t seed,
-                            const unsigned long long *T, uint64_t mult, Ctl *ctl,
+                            const unsigned long long *T, uint64_t mult, unsigned long long *err,
                             cudaStream_t s);
 
 // roof.cu: out = {gather GB/s, CAS/s L2-resident, CAS/s > L2, hand-off ns (row), hop ns,

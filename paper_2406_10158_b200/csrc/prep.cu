@@ -404,6 +404,15 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
 __global__ void merge_err_kernel(const Ctl *src, Ctl *dst) {
     const u64 e = src->err.v;
     if (e) atomicCAS(&dst->err.v, 0ull, e);
+    dst->max_rank.v = src->max_rank.v;   // GPUTx: the prepared rank pass counted the K-sets
+}
+__global__ void merge_word_kernel(const u64 *err, Ctl *dst) {
+    const u64 e = *err;
+    if (e) atomicCAS(&dst->err.v, 0ull, e);
+}
+cudaError_t launch_merge_word(const u64 *err, Ctl *dst, cudaStream_t s) {
+    merge_word_kernel<<<1, 1, 0, s>>>(err, dst);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s) {

@@ -201,7 +201,7 @@ __device__ __forceinline__ u64 nurand(u64 ua, u64 ub, u64 A, u64 x, u64 y, u64 C
 
 __global__ void tpcc_gen_kernel(uint32_t *txo, uint32_t n_txn, u64 seed, uint32_t W, uint32_t w_lo,
                                 uint32_t w_hi, uint32_t no_pm, uint32_t c_last_run, uint32_t c_id_c,
-                                uint32_t c_item_c, Ctl *ctl) {
+                                uint32_t c_item_c, u64 *err) {
     const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_txn) return;
     uint32_t t[TPCC_TX_WORDS];
@@ -223,7 +223,7 @@ __global__ void tpcc_gen_kernel(uint32_t *txo, uint32_t n_txn, u64 seed, uint32_
         for (uint32_t j = 0; j < n; j++) {
             for (u64 k = 0;; k++) {
                 if (k > 4096) {
-                    atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_CONFIG);
+                    atomicCAS(err, 0ull, (u64)CC_ERR_CONFIG);   // the batch's error word
                     return;
                 }
                 const uint32_t i = (uint32_t)nurand(draw(seed, g, S_ITEMA, j, k), draw(seed, g, S_ITEMB, j, k), 8191, 1,
@@ -280,10 +280,10 @@ __global__ void tpcc_gen_kernel(uint32_t *txo, uint32_t n_txn, u64 seed, uint32_
 }
 
 cudaError_t launch_tpcc_gen(uint32_t *tx, uint32_t n_txn, u64 seed, uint32_t W, uint32_t w_lo, uint32_t w_hi,
-                            uint32_t no_pm, uint32_t c_last_run, uint32_t c_id_c, uint32_t c_item_c, Ctl *ctl,
+                            uint32_t no_pm, uint32_t c_last_run, uint32_t c_id_c, uint32_t c_item_c, u64 *err,
                             cudaStream_t s) {
     tpcc_gen_kernel<<<(n_txn + 127) / 128, 128, 0, s>>>(tx, n_txn, seed, W, w_lo, w_hi, no_pm, c_last_run, c_id_c,
-                                                        c_item_c, ctl);
+                                                        c_item_c, err);
     return cudaGetLastError();
 }
 

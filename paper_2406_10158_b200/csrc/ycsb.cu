@@ -375,14 +375,14 @@ cudaError_t launch_identity_index(u64 *keys, u64 *rowids, uint64_t n, cudaStream
 //   field = rng(seed,gid,3<<56|i) mod 15.
 __global__ void ycsb_gen_kernel(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                                 uint64_t n, u64 wthr, uint64_t seed, const u64 *T,
-                                uint64_t A, Ctl *ctl) {
+                                uint64_t A, u64 *err) {
     const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n_txn) return;
     u32 kk[16];
     for (u32 i = 0; i < K; i++) {
         for (u64 k = 0;; k++) {
             if (k >= (1u << 24)) {
-                atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_CONFIG);
+                atomicCAS(err, 0ull, (u64)CC_ERR_CONFIG);   // the batch's error word
                 return;
             }
             const u64 u = rng3(seed, gid, (1ull << 56) | ((u64)i << 24) | k);
@@ -418,11 +418,11 @@ __global__ void ycsb_gen_kernel(uint32_t *keys, uint8_t *ops, uint32_t n_txn, ui
 
 cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                             uint64_t n_rows, double W, uint64_t seed, const u64 *T,
-                            uint64_t mult, Ctl *ctl, cudaStream_t s) {
+                            uint64_t mult, u64 *err, cudaStream_t s) {
     const u64 wthr = (u64)(W * 9007199254740992.0);
     const int blk = 128;
     ycsb_gen_kernel<<<(n_txn + blk - 1) / blk, blk, 0, s>>>(keys, ops, n_txn, K, n_rows, wthr,
-                                                            seed, T, mult, ctl);
+                                                            seed, T, mult, err);
     return cudaGetLastError();
 }
 

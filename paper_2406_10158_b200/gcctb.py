@@ -122,6 +122,9 @@ _SIGS = {
     "cc_batch_info": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "cc_batch_free": (ctypes.c_int, [_P, _P]),
+    "cc_pool_trim": (ctypes.c_int, [_P]),
+    "cc_mem_stats": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                                    ctypes.POINTER(ctypes.c_uint64)]),
     "cc_submit": (ctypes.c_int, [_P, _P, ctypes.POINTER(cc_exec_desc), ctypes.POINTER(cc_result)]),
     "cc_prepare": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_uint32]),
     "cc_sync": (ctypes.c_int, [_P, ctypes.POINTER(cc_stats)]),

@@ -168,10 +168,9 @@ def c2(torch_cuda, orc):
 
 
 # full size: the paper's launch (thread mode, wd=0, bs=32) across the theta range, and
-# the tile mode the bench uses (16 lanes) up to theta=0.9.  (At theta=0.99 basic TO in
-# tile mode is a retry storm that may end in the paper's own timestamp overflow,
-# covered by test_ts_overflow_is_reported.)
-C2_CASES = [(0.0, 1), (0.6, 1), (0.99, 1), (0.6, 16), (0.9, 16)]
+# tile mode (16 lanes) in the full-occupancy grid; the bench's own per-scheme launch is
+# covered up to theta=0.99 by test_c2_full_size_parity_bench_launch.
+C2_CASES = [(0.0, 1), (0.6, 1), (0.99, 1), (0.6, 16), (0.9, 16), (0.99, 16)]
 
 
 @pytest.mark.parametrize("theta,lanes", C2_CASES)
@@ -194,8 +193,8 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
     b.free()
 
 
-@pytest.mark.parametrize("warm", [False, True])
-@pytest.mark.parametrize("theta", [0.6, 0.9])
+@pytest.mark.parametrize("theta,warm", [(0.6, False), (0.6, True), (0.9, False), (0.9, True),
+                                        (0.95, False), (0.99, False)])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta, warm):
     """configs[1] at full size in exactly the launch bench.py times (bench.launch_of: tile
@@ -306,22 +305,32 @@ def test_c2_full_size_parity_search_index(c2, orc, scheme, flag):
     b.free()
 
 
-def test_ts_overflow_is_reported(c1):
-    """31-bit TO timestamps: a retry storm that
-    exhausts them surfaces as TS_OVERFLOW, never as a wrong result.  Forced with a
-    tiny hot table, all writes, and the paper's immediate retry."""
+@pytest.mark.parametrize("lanes", [1, 16])
+@pytest.mark.parametrize("scheme", ["to", "mvcc"])
+def test_ts_overflow_is_reported(c1, monkeypatch, scheme, lanes):
+    """31-bit TO / MVCC timestamps: exhausting them
+    surfaces as TS_OVERFLOW, never as a wrong result or a hang.  The counter starts 2,000
+    below 2^31 (test hook GCCTB_TS_BASE) and 1,024 all-write transactions on 4 hot rows
+    need far more than 2,000 attempts, so the overflow must be reported -- a watchdog
+    expiry fails the test."""
     from paper_2406_10158_b200.gcctb import CCError
-    db, _ = c1
+    db, S0 = c1
     keys = np.tile(np.arange(4, dtype=np.uint32), 1024)
     ops = np.full(keys.size, 0x81, np.uint8)
     b = db.import_ycsb(keys, ops, 4)
     db.snapshot(False)
-    res = db.submit(b, "to", wd=5, bs=32, watchdog_s=5)
-    try:
-        st = db.sync()
-        assert st.commits == 1024    # finished before overflow: must then be correct
-    except CCError as e:
-        assert "TS_OVERFLOW" in str(e) or "WATCHDOG" in str(e)
+    monkeypatch.setenv("GCCTB_TS_BASE", str((1 << 31) - 2000))
+    db.submit(b, scheme, wd=5, bs=32, lanes=lanes, watchdog_s=20)
+    with pytest.raises(CCError) as ei:
+        db.sync()
+    assert "TS_OVERFLOW" in str(ei.value)
+    # the same batch from timestamp 1 commits every transaction correctly
+    monkeypatch.delenv("GCCTB_TS_BASE")
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=5, bs=32, lanes=lanes, watchdog_s=60)
+    assert db.sync().commits == 1024
+    import oracle
+    oracle.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
     b.free()
 
 
