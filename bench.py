@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--two-pc", action="store_true",
                     help="TPC-C: distributed transactions of tpl_nw / tpl_wd in 2PC rounds (f-2); the other "
                          "schemes keep the deterministic phase B")
+    ap.add_argument("--exchange", choices=["p2p", "host"], default="p2p",
+                    help="tpcc partitions: p2p = the exchange inside the library over peer memory "
+                         "(CC_FLAG_PART_P2P, no host step per round); host = cc_part_send/apply/finish "
+                         "with torch.distributed all-to-alls (or device copies in --loopback)")
     ap.add_argument("--loopback", type=int, default=0,
                     help="tpcc: run G warehouse partitions as G dbs on this one GPU (a8 with a device-side exchange)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -704,7 +708,7 @@ def run_tpcc_loopback(args, local):
     import torch
 
     from paper_2406_10158_b200.api import DB, Result
-    from paper_2406_10158_b200.partition import loopback_round, loopback_round_2pc
+    from paper_2406_10158_b200.partition import loopback_p2p, loopback_round, loopback_round_2pc
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -718,15 +722,20 @@ def run_tpcc_loopback(args, local):
         db.load_tpcc(W, 1, n, w_first=r * wpr, w_count=wpr)
         dbs.append(db)
     res = {s: [Result.alloc(n, 18, dev, stream=db.stream, out_words=48) for db in dbs] for s in schemes}
+    if args.exchange == "p2p":
+        DB.part_connect_local(dbs)
 
     def step(i):
         bs = [db.gen_tpcc(n, 7919 * (r + 1) + i, args.tpcc_mix, w_lo=r * wpr, w_hi=(r + 1) * wpr)
               for r, db in enumerate(dbs)]
         for s in schemes:
+            la = tpcc_launch(args, s, dbs[0].num_sms, True)
             if args.two_pc and s not in ("gputx", "gacco"):
-                loopback_round_2pc(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms, True), lanes=32, watchdog_s=60)
+                loopback_round_2pc(dbs, bs, s, results=res[s], **la, lanes=32, watchdog_s=60)
+            elif args.exchange == "p2p":
+                loopback_p2p(dbs, bs, s, results=res[s], **la, lanes=32, watchdog_s=60)
             else:
-                loopback_round(dbs, bs, s, results=res[s], **tpcc_launch(args, s, dbs[0].num_sms, True), lanes=32, watchdog_s=60)
+                loopback_round(dbs, bs, s, results=res[s], **la, lanes=32, watchdog_s=60)
         return bs
 
     clocks = Clocks(local)   # before the warm-up: NVML start-up stays out of the timed region
@@ -767,7 +776,9 @@ def run_tpcc_loopback(args, local):
                    "launch": {s: tpcc_launch(args, s, 148, True) for s in schemes} if args.launch == "tuned"
                    else "bs 8, full-occupancy grid",
                    "phase_b": "2PC rounds for the six non-deterministic schemes (f-2), deterministic for GPUTx/GaccO" if args.two_pc else "deterministic",
-                   "timing": "host clock around fully synchronised steps (G streams + host-orchestrated exchange)"},
+                   "exchange": "in-library over device memory (CC_FLAG_PART_P2P)" if args.exchange == "p2p" and not args.two_pc
+                   else "host-orchestrated device copies",
+                   "timing": "host clock around fully synchronised steps (G streams)"},
         "per_scheme": per, "clocks": clk}), flush=True)
     for db in dbs:
         db.close()
@@ -783,7 +794,7 @@ def run_tpcc(args, rank, world, local):
 
     from paper_2406_10158_b200.api import DB, Result
     from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
-    from paper_2406_10158_b200.partition import dist_round, dist_round_2pc
+    from paper_2406_10158_b200.partition import dist_round, dist_round_2pc, p2p_round, p2p_setup
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -796,11 +807,16 @@ def run_tpcc(args, rank, world, local):
     db = DB(local, rank=rank, world=world)
     db.load_tpcc(W, 1, n, w_first=rank * wpr, w_count=wpr)
     res = {s: Result.alloc(n, 18, dev, stream=db.stream, out_words=48) for s in schemes}
+    p2p = world > 1 and args.exchange == "p2p"
+    if p2p:
+        p2p_setup(db)   # windows mapped across the GPUs (CUDA IPC over NVLink), handles gathered once
 
     def step(i):
         b = db.gen_tpcc(n, 7919 * (rank + 1) + i, args.tpcc_mix, w_lo=rank * wpr, w_hi=(rank + 1) * wpr)
         for s in schemes:
-            if world > 1 and args.two_pc and s not in ("gputx", "gacco"):
+            if p2p and not (args.two_pc and s not in ("gputx", "gacco")):
+                p2p_round(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
+            elif world > 1 and args.two_pc and s not in ("gputx", "gacco"):
                 dist_round_2pc(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
             elif world > 1:
                 dist_round(db, b, s, result=res[s], **tpcc_launch(args, s, db.num_sms), lanes=32, watchdog_s=60)
@@ -853,7 +869,9 @@ def run_tpcc(args, rank, world, local):
                        "neworder_permyriad": args.tpcc_mix, "schemes": schemes, "lanes_per_txn": 32,
                        "launch": {s: tpcc_launch(args, s, 148) for s in schemes} if args.launch == "tuned"
                        else "bs 8, full-occupancy grid",
-                       "parallelism": f"warehouse-partitioned x{world}" + (" (NCCL all-to-all)" if world > 1 else ""),
+                       "parallelism": f"warehouse-partitioned x{world}" + (
+                           (" (in-library exchange over NVLink peer memory)" if p2p else " (NCCL all-to-all)")
+                           if world > 1 else ""),
                        "phase_b": "2PC rounds for the six non-deterministic schemes (f-2), deterministic for GPUTx/GaccO" if args.two_pc else "deterministic"},
             "per_scheme": per, "clocks": clk,
             "gpu_launches": launches_per_step(schemes) * args.steps + (0 if world == 1 else

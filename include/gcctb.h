@@ -269,6 +269,18 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         reached L2 (one load per 32 B sector), so a lock /
                                         pending write is held across L2 latencies only, not
                                         across its cold rows' HBM misses.  Same results. */
+#define CC_FLAG_NO_LOOKAHEAD 0x8000u /* ablation: tile mode without the claim / key / line look-ahead
+                                        (DESIGN.md §2); same results */
+#define CC_FLAG_META_PAD 0x10000u    /* single-word schemes: one control word per 32 B sector instead of
+                                        packed 8 B words (the north star's metadata padded against
+                                        false sharing in L2).  Same results;
+                                        measured per workload */
+#define CC_FLAG_PART_P2P 0x4000u     /* with CC_FLAG_PARTITIONED (deterministic phase B): the exchange
+                                        runs inside the library over peer memory -- requests and
+                                        responses are stored straight into the peers' exchange
+                                        windows, published by system-scope release flags -- so the
+                                        submit enqueues phase A, phase B and a7 on the db stream and
+                                        completes without the host (cc_part_window / connect) */
 #define CC_FLAG_INDEX_EYTZ 0x1000u   /* index lookups in the Eytzinger (BFS) layout of the same
                                         sorted keys: a branch-free
                                         descent over a complete binary tree padded to 2^h - 1
@@ -400,6 +412,38 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent);
 cc_status cc_part_decide(cc_db db, const void *resp, uint64_t n_sent, const void **dec);
 cc_status cc_part_commit(cc_db db, const void *recv, const void *dec, uint64_t n);
 cc_status cc_part_next(cc_db db, uint64_t *pending);
+
+/* In-library exchange over peer memory (CC_FLAG_PART_P2P; the north
+ * star's "all-to-all exchange of remote accesses over NVLink each round", fused with the
+ * kernels that produce and consume it).  Each rank's db owns an exchange window in device
+ * memory: system-scope flags, an inbox of cap request slots per source rank (cap =
+ * max_txn x 18 accesses: a source can never overflow it) and the staging array of its own
+ * transactions' phase-B responses.  A partitioned submit with CC_FLAG_PART_P2P then runs on
+ * the db stream, with no host synchronisation and no collective call:
+ *   pack + send    requests are stored by the pack kernel straight into the owners'
+ *                  inboxes (NVLink stores to a peer GPU), then one release flag per owner
+ *                  carries (epoch, count);
+ *   phase A        the local transactions under the scheme (as without P2P);
+ *   receive        wait for every source's flag of this epoch, compact, sort by (item, gid);
+ *   apply + reply  each item's chain in global gid order, every response stored straight
+ *                  into its home's staging array, then one release flag per home;
+ *   finish         wait for every owner's flag, assemble, a7.
+ * Results are those of cc_part_send / apply / finish (the same phase-B kernels decide what
+ * is applied and returned).  All ranks must issue the same sequence of P2P submits.
+ *   cc_part_window   allocates this db's window (TPC-C must be loaded; world from
+ *                    cc_db_desc) and returns its handle: a CUDA IPC handle plus the shape;
+ *   cc_part_connect  maps the windows of all ranks, handles[world] indexed by rank (as
+ *                    gathered by the caller, e.g. all_gather over torch.distributed);
+ *   cc_part_connect_local  the same for `n` dbs of this process (ranks 0..n-1, one GPU or
+ *                    several with peer access), by plain device pointers.
+ * Errors: CONFIG (shapes differ, > 64 ranks), STATE (already connected), CUDA (IPC). */
+typedef struct {
+    unsigned char ipc[64];   /* cudaIpcMemHandle_t of the window */
+    uint32_t rank, world, cap, max_txn;
+} cc_ipc_handle;
+cc_status cc_part_window(cc_db db, cc_ipc_handle *out);
+cc_status cc_part_connect(cc_db db, const cc_ipc_handle *handles);
+cc_status cc_part_connect_local(cc_db *dbs, int n);
 
 /* Debug event log (CC_FLAG_EVENTS).  Each event is 24 bytes: u64 seq, u32 gid,
  * u32 record (global id; 0xFFFFFFFF for commit/abort), u32 attempt, u32 kind (0 read,

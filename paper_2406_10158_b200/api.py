@@ -298,6 +298,24 @@ class DB:
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self._chk(G.lib().cc_part_finish(self.h, resp.data_ptr() if n else None, n))
 
+    # in-library exchange over peer memory (CC_FLAG_PART_P2P)
+    def part_window(self) -> bytes:
+        """This db's exchange window handle (bytes of cc_ipc_handle), to be gathered by all ranks."""
+        h = G.cc_ipc_handle()
+        self._chk(G.lib().cc_part_window(self.h, ctypes.byref(h)))
+        return bytes(h)
+
+    def part_connect(self, handles: list[bytes]):
+        arr = (G.cc_ipc_handle * len(handles))()
+        for i, hb in enumerate(handles):
+            ctypes.memmove(ctypes.byref(arr[i]), hb, ctypes.sizeof(G.cc_ipc_handle))
+        self._chk(G.lib().cc_part_connect(self.h, arr))
+
+    @staticmethod
+    def part_connect_local(dbs: list["DB"]):
+        arr = (ctypes.c_void_p * len(dbs))(*[db.h.value for db in dbs])
+        G.check(dbs[0].h, G.lib().cc_part_connect_local(arr, len(dbs)))
+
     # 2PC phase B (f-2)
     def part_decide(self, back: torch.Tensor) -> torch.Tensor:
         """Home: decide this round from the returned responses; device u64 decisions

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgcctb.so")
-SOURCES = ["db.cu", "ycsb.cu", "prep.cu", "tpcc.cu", "part.cu", "roof.cu"]
+SOURCES = ["db.cu", "ycsb.cu", "prep.cu", "tpcc.cu", "part.cu", "roof.cu", "sort.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr",

@@ -24,6 +24,13 @@ int rank_kernel_grid();
 using namespace gcctb;
 typedef unsigned long long u64;
 
+// largest per-block shared-memory footprint of an executor (contexts + thread-mode staged
+// accesses): above it the staged accesses move to a global workspace, and the rest of
+// the 228 KB per SM stays free for the L1 share the executor's loads use
+#ifndef GC_STAGE_SMEM_MAX
+#define GC_STAGE_SMEM_MAX (180u * 1024u)
+#endif
+
 // Every device allocation / free the driver makes goes through dalloc / dfree, which count
 // them (cc_mem_stats): the bench asserts that a timed loop of steps makes none (a
 // cudaMalloc / cudaFree is an implicit device synchronisation).
@@ -210,6 +217,15 @@ struct cc_db_s {
         uint8_t *vote = nullptr;      // owner: grant of every received request (this round)
         uint64_t vote_cap = 0;
         unsigned long long *dec = nullptr;   // home: decision of every sent request
+        // CC_FLAG_PART_P2P: in-library exchange over peer memory
+        void *win = nullptr;                 // this rank's window [flags | inbox | staging]
+        uint32_t win_cap = 0, win_txn = 0;   // request slots per source, transactions
+        PeerTab pt{};                        // every rank's window, as pointers of this process
+        bool connected = false;
+        std::vector<void *> ipc_open;        // peers' windows opened through CUDA IPC
+        unsigned long long epoch = 0;        // partitioned P2P submits so far (all ranks in step)
+        unsigned long long *rc = nullptr;    // [2 world + 1]: counts, offsets, total received
+        PartReq *recv = nullptr;             // compacted inboxes (world x cap)
     } part;
     // per-submit scratch (grown on demand)
     Ctl *ctl = nullptr;
@@ -222,6 +238,8 @@ struct cc_db_s {
     u64 *ohi = nullptr, *olo = nullptr;
     u64 *ring = nullptr;
     uint32_t ring_cap = 0;
+    void *ws = nullptr;                 // thread-mode staging workspace (global fallback)
+    uint64_t ws_bytes = 0;
     u64 *arena = nullptr;
     uint64_t arena_nodes = 0;
     uint32_t arena_row_words = 0;
@@ -372,7 +390,12 @@ cc_status cc_db_destroy(cc_db db) {
     dfree(db->part.tmp);
     dfree(db->part.vote);
     dfree(db->part.dec);
+    for (void *p : db->part.ipc_open) cudaIpcCloseMemHandle(p);
+    dfree(db->part.win);
+    dfree(db->part.rc);
+    dfree(db->part.recv);
     dfree(db->arena);
+    dfree(db->ws);
     dfree(db->latch);
     dfree(db->stages);
     dfree(db->events);
@@ -406,10 +429,10 @@ static cc_status create_table(cc_db db, const char *name, uint32_t row_bytes, ui
     CUDA_TRY(db, cudaMemsetAsync(t.d, 0, (size_t)row_bytes * rows, db->stream));
     if (cc) {
         // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B),
-        // GC_META_STRIDE words in the padded ablation build
+        // GC_META_PAD_WORDS words per record for the padded layout (CC_FLAG_META_PAD)
         const uint64_t need = db->n_records + rows;
         u64 *meta = nullptr;
-        CUDA_TRY(db, dalloc(&meta, need * 8 * (GC_META_STRIDE > 2 ? GC_META_STRIDE : 2)));
+        CUDA_TRY(db, dalloc(&meta, need * 8 * GC_META_PAD_WORDS));   // room for the padded layout
         CUDA_TRY(db, cudaStreamSynchronize(db->stream));
         if (db->meta) dfree(db->meta);
         db->meta = meta;
@@ -1042,6 +1065,12 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (two_pc && (!partitioned || scheme == CC_GPUTX || scheme == CC_GACCO))
         return fail(db, CC_ERR_UNSUPPORTED,
                     "CC_FLAG_PART_2PC: non-deterministic schemes with CC_FLAG_PARTITIONED only");
+    const bool p2p = (desc->flags & CC_FLAG_PART_P2P) != 0;
+    if (p2p && (!partitioned || two_pc))
+        return fail(db, CC_ERR_UNSUPPORTED, "CC_FLAG_PART_P2P: with CC_FLAG_PARTITIONED, deterministic phase B only");
+    if (p2p && (!db->part.connected || b->n_txn > db->part.win_txn))
+        return fail(db, CC_ERR_STATE, "CC_FLAG_PART_P2P: cc_part_connect first (window for %u transactions)",
+                    db->part.win_txn);
     if (partitioned) {
         const TpccState &T = db->tpcc;
         if (!is_tpcc) return fail(db, CC_ERR_UNSUPPORTED, "partitioned execution is TPC-C only (YCSB: replicas)");
@@ -1060,7 +1089,9 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     // a2: reset CC state (every record of every table)
     p.mvcc_split = (scheme == CC_MVCC && (desc->flags & CC_FLAG_MVCC_SPLIT)) ? db->n_records : 0;
-    p.meta_stride = scheme != CC_MVCC ? GC_META_STRIDE : 1u;
+    p.meta_stride = (scheme != CC_MVCC && (desc->flags & CC_FLAG_META_PAD)) ? GC_META_PAD_WORDS : 1u;
+    p.meta_shift = p.meta_stride == 1 ? 0u : 2u;
+    static_assert(GC_META_PAD_WORDS == 4, "meta_shift assumes 4 words per padded record");
     // (GaccO / GPUTx keep no per-record control word: their cursors and K-set counters are
     // reset by a3, so only the ring and the control block are cleared for them)
     CUDA_TRY(db, launch_reset_meta(scheme, db->meta, det ? 0 : db->n_records, db->ring, db->ring_cap,
@@ -1073,7 +1104,14 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         const unsigned long long base = tb ? strtoull(tb, nullptr, 0) : 0ull;
         if (base) CUDA_TRY(db, launch_fill_u64(&db->ctl->ts.v, base, 1, db->stream));
     }
-    if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
+    if (partitioned && p2p) {   // a8 over peer memory: requests go straight into the owners' windows
+        const uint32_t wpr = db->tpcc.W / db->world;
+        db->part.epoch++;
+        CUDA_TRY(db, p2p_send(tp, db->rank, db->world, wpr, b->n_txn, db->part.skip, db->part.cnt, db->part.cursor,
+                              db->part.pt, db->part.win_cap, db->part.epoch, db->ctl,
+                              (desc->flags & CC_FLAG_PART_ALL) != 0, db->stream));
+        p.skip = db->part.skip;
+    } else if (partitioned) {   // a8: classify local / distributed, pack phase-B requests per owner
         const uint32_t wpr = db->tpcc.W / db->world;
         CUDA_TRY(db, part_classify_pack(tp, db->rank, db->world, wpr, b->n_txn, db->part.skip, db->part.cnt,
                                         db->part.off, db->part.cursor, db->part.send, db->stream));
@@ -1113,18 +1151,64 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[2], db->stream));
     // a4-a6: persistent executor
     const int block = 32 * (int)desc->bs;
+    // thread mode: each working lane's staged read/write set (K lanes of the workload's
+    // access record) in dynamic shared memory, or -- when a block's working lanes need more
+    // than GC_STAGE_SMEM_MAX -- in a global workspace with the same strided layout
+    // (plus, in every mode, each working lane's context -- exec_th_bytes() -- in shared memory)
+    size_t smem = 0;
+    uint64_t ws_per_block = 0;
+    if (p.lanes == 1) {
+        const uint64_t working = (uint64_t)desc->bs << desc->wd;
+        const uint64_t bytes = working * (is_tpcc ? TPCC_K : b->K) * (is_tpcc ? tpcc_lane_bytes() : ycsb_lane_bytes());
+        smem = (size_t)(working * exec_th_bytes());
+        if (smem + bytes <= GC_STAGE_SMEM_MAX) smem += (size_t)bytes;
+        else ws_per_block = bytes;
+    } else {   // TPC-C tile lanes keep their access entry in shared memory too
+        smem = (size_t)block * (exec_th_bytes() + (is_tpcc ? tpcc_lane_bytes() : 0));
+    }
     int grid = (int)desc->grid;
     if (grid <= 0) {
-        const int per_sm = is_tpcc ? tpcc_exec_max_blocks_per_sm(scheme, (int)p.lanes, block)
-                                   : ycsb_exec_max_blocks_per_sm(scheme, (int)p.lanes, block);
+        const int per_sm = is_tpcc ? tpcc_exec_max_blocks_per_sm(scheme, (int)p.lanes, block, smem)
+                                   : ycsb_exec_max_blocks_per_sm(scheme, (int)p.lanes, block, smem);
         if (per_sm <= 0) return fail(db, CC_ERR_CONFIG, "executor cannot launch %d threads/block", block);
         grid = per_sm * db->num_sms;
     }
     if ((uint64_t)grid * block > (1ull << 21)) return fail(db, CC_ERR_CONFIG, "grid x block > 2^21 threads");
-    if (is_tpcc) CUDA_TRY(db, launch_tpcc_exec(p, tp, grid, block, db->stream));
-    else CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, db->stream));
+    if (ws_per_block) {
+        const uint64_t need = ws_per_block * (uint64_t)grid;
+        if (need > db->ws_bytes) {
+            CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+            dfree(db->ws);
+            db->ws = nullptr;
+            db->ws_bytes = 0;
+            CUDA_TRY(db, dalloc(&db->ws, need));
+            db->ws_bytes = need;
+        }
+        p.ws = db->ws;
+    }
+    if (is_tpcc) CUDA_TRY(db, launch_tpcc_exec(p, tp, grid, block, smem, db->stream));
+    else CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, smem, db->stream));
     if (p.stages) CUDA_TRY(db, launch_stages_reduce(p.stages, (uint64_t)grid * block, db->stream));
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
+    if (partitioned && p2p) {   // phase B through the windows, then a7: the submit is complete
+        auto &P = db->part;
+        const uint32_t wpr = db->tpcc.W / db->world;
+        CUDA_TRY(db, p2p_phase_b(tp, db->rank, db->world, wpr, b->n_txn, P.skip, P.pt, P.win_cap, P.epoch, P.rc, P.recv,
+                                 P.k1, P.k2, P.i1, P.i2, P.tmp, P.tmp_bytes, p.committed, p.order_hi, p.order_lo,
+                                 p.read_out, db->ctl, p.watchdog_ns, db->stream));
+        if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
+        cc_result r = *res;
+        if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
+        CUDA_TRY(db, launch_finalize(p, r, db->prep, false, true, db->stream));
+        if ((void *)r.stats != (void *)db->stats_scratch)
+            CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS, cudaMemcpyDeviceToDevice,
+                                         db->stream));
+        if (timing) {
+            CUDA_TRY(db, cudaEventRecord(ev.ev[4], db->stream));
+            db->pending.push_back(ev);
+        }
+        return CC_OK;
+    }
     if (partitioned) {   // phase B happens in cc_part_apply / cc_part_finish
         db->part.pending = true;
         db->part.p = p;
@@ -1141,7 +1225,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     cc_result r = *res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
     CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream,
-                                 scheme == CC_TPL_NW || scheme == CC_TPL_WD));
+                                 scheme == CC_TPL_NW || scheme == CC_TPL_WD, scheme == CC_TICTOC));
     if (used) {   // a later cc_prepare of this batch may overwrite the buffers after this point
         CUDA_TRY(db, cudaEventRecord(used->consumed, db->stream));
         used->has_consumer = true;
@@ -1303,6 +1387,133 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent) {
         db->pending.push_back(P.ev);
     }
     P.pending = false;
+    return CC_OK;
+}
+
+// ---------------------------------------------------------------- P2P exchange windows
+static cc_status ensure_window(cc_db db) {
+    auto &P = db->part;
+    if (P.win) return CC_OK;
+    if (!db->tpcc.loaded) return fail(db, CC_ERR_CONFIG, "cc_part_window: TPC-C not loaded");
+    if (db->world > P2P_MAXW) return fail(db, CC_ERR_CONFIG, "cc_part_window: at most %d ranks", P2P_MAXW);
+    P.win_txn = db->tpcc.max_txn;
+    P.win_cap = P.win_txn * TPCC_K;   // a source can send at most every access of its batch
+    const size_t bytes = p2p_window_bytes(db->world, P.win_cap, P.win_txn);
+    CUDA_TRY(db, dalloc(&P.win, bytes));
+    CUDA_TRY(db, cudaMemsetAsync(P.win, 0, P2P_FLAG_BYTES, db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    return CC_OK;
+}
+
+static void window_ptrs(void *base, uint32_t world, uint32_t cap, PartReq **inbox, PartResp **stage,
+                        unsigned long long **flags) {
+    char *b = (char *)base;
+    *flags = (unsigned long long *)b;
+    *inbox = (PartReq *)(b + P2P_FLAG_BYTES);
+    *stage = (PartResp *)(b + P2P_FLAG_BYTES + (size_t)world * cap * sizeof(PartReq));
+}
+
+static void preload_all_kernels() {
+    static bool done = false;   // once per process (modules are shared by the dbs)
+    if (done) return;
+    preload_prep_kernels();
+    preload_sort_kernels();
+    preload_part_kernels();
+    preload_tpcc_kernels();
+    preload_ycsb_kernels();
+    done = true;
+}
+
+static cc_status p2p_buffers(cc_db db) {
+    preload_all_kernels();
+    auto &P = db->part;
+    const uint64_t capn = (uint64_t)db->world * P.win_cap;
+    if (!P.rc) CUDA_TRY(db, dalloc(&P.rc, (2ull * db->world + 1) * 8));
+    if (!P.recv) CUDA_TRY(db, dalloc(&P.recv, capn * sizeof(PartReq)));
+    if (capn > P.recv_cap) {   // sort buffers of phase B (shared with the host-driven exchange)
+        CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+        dfree(P.k1); dfree(P.k2); dfree(P.i1); dfree(P.i2); dfree(P.tmp);
+        CUDA_TRY(db, dalloc(&P.k1, capn * 8));
+        CUDA_TRY(db, dalloc(&P.k2, capn * 8));
+        CUDA_TRY(db, dalloc(&P.i1, capn * 4));
+        CUDA_TRY(db, dalloc(&P.i2, capn * 4));
+        P.tmp_bytes = part_sort_bytes(capn);
+        CUDA_TRY(db, dalloc((char **)&P.tmp, P.tmp_bytes));
+        P.recv_cap = capn;
+    }
+    cc_status st = ensure_part(db, P.win_txn);
+    if (st) return st;
+    // everything a P2P submit of up to win_txn transactions can need is allocated now: a
+    // cudaMalloc inside a submit may block the host until the device idles, while another
+    // rank's kernels of this process already wait on the device for this rank's requests
+    st = ensure_scratch(db, P.win_txn, (uint64_t)P.win_txn * TPCC_K);
+    if (st) return st;
+    st = ensure_arena(db, (uint64_t)P.win_txn * TPCC_K, TPCC_C_WORDS);
+    if (st) return st;
+    P.connected = true;
+    return CC_OK;
+}
+
+cc_status cc_part_window(cc_db db, cc_ipc_handle *out) {
+    CHECK_DB(db);
+    if (!out) return fail(db, CC_ERR_INVALID_ARG, "null handle");
+    cc_status st = ensure_window(db);
+    if (st) return st;
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(db, cudaIpcGetMemHandle(&h, db->part.win));
+    static_assert(sizeof(h) == sizeof(out->ipc), "IPC handle size");
+    memcpy(out->ipc, &h, sizeof h);
+    out->rank = (uint32_t)db->rank;
+    out->world = (uint32_t)db->world;
+    out->cap = db->part.win_cap;
+    out->max_txn = db->part.win_txn;
+    return CC_OK;
+}
+
+cc_status cc_part_connect(cc_db db, const cc_ipc_handle *handles) {
+    CHECK_DB(db);
+    auto &P = db->part;
+    if (!handles) return fail(db, CC_ERR_INVALID_ARG, "null handles");
+    cc_status st = ensure_window(db);
+    if (st) return st;
+    if (P.connected) return fail(db, CC_ERR_STATE, "cc_part_connect: already connected");
+    for (int r = 0; r < db->world; r++) {
+        const cc_ipc_handle &h = handles[r];
+        if (h.rank != (uint32_t)r || h.world != (uint32_t)db->world || h.cap != P.win_cap || h.max_txn != P.win_txn)
+            return fail(db, CC_ERR_CONFIG, "cc_part_connect: handle %d does not match this db's window", r);
+        void *base = P.win;
+        if (r != db->rank) {
+            cudaIpcMemHandle_t ih;
+            memcpy(&ih, h.ipc, sizeof ih);
+            CUDA_TRY(db, cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess));
+            P.ipc_open.push_back(base);
+        }
+        window_ptrs(base, db->world, P.win_cap, &P.pt.inbox[r], &P.pt.stage[r], &P.pt.flags[r]);
+    }
+    return p2p_buffers(db);
+}
+
+cc_status cc_part_connect_local(cc_db *dbs, int n) {
+    if (!dbs || n < 1 || n > P2P_MAXW) return CC_ERR_INVALID_ARG;
+    for (int r = 0; r < n; r++) {
+        cc_db db = dbs[r];
+        CHECK_DB(db);
+        if (db->rank != r || db->world != n) return fail(db, CC_ERR_CONFIG, "cc_part_connect_local: db %d is not rank %d of %d", r, r, n);
+        cc_status st = ensure_window(db);
+        if (st) return st;
+        if (db->part.connected) return fail(db, CC_ERR_STATE, "cc_part_connect_local: already connected");
+    }
+    for (int r = 0; r < n; r++) {
+        auto &P = dbs[r]->part;
+        for (int q = 0; q < n; q++) {
+            const auto &Q = dbs[q]->part;
+            if (Q.win_cap != P.win_cap || Q.win_txn != P.win_txn) return fail(dbs[r], CC_ERR_CONFIG, "window shapes differ");
+            window_ptrs(Q.win, n, Q.win_cap, &P.pt.inbox[q], &P.pt.stage[q], &P.pt.flags[q]);
+        }
+        cudaSetDevice(dbs[r]->device);
+        cc_status st = p2p_buffers(dbs[r]);
+        if (st) return st;
+    }
     return CC_OK;
 }
 

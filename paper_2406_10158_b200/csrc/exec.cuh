@@ -39,6 +39,15 @@ enum { RES_OK = 0, RES_ABORT = 1, RES_FATAL = 2 };
 constexpr u32 NO_TXN = 0xFFFFFFFFu;
 
 // ------------------------------------------------------------------ thread context
+// claim state of a worker (queue, a6); lives in its shared-memory context
+struct Claim {
+    bool exhausted = false;
+    bool sealed = false;
+    bool fresh = false;      // the last id returned was a fresh one (restarts = 0)
+    u64 tail = 0;
+    u64 next = 0, end = 0;   // fresh ids claimed ahead (chunked claims), processed in order
+};
+
 struct Th {
     u64 deadline;
     const ExecParams *p;
@@ -49,14 +58,21 @@ struct Th {
     u64 *cw;   // lock word whose holder caused the last abort (nullptr: none)
     u64 cv;    // wait until (*cw & cv) == 0: the conflicting lock is free
     u32 hot;   // tile mode: 1 + lane of the lock that caused this transaction's last abort
+    u64 a_t0, a_u0, a_w0, a_s0;   // CC_FLAG_STAGES: the current attempt's start snapshot
+    Claim cl;                     // the worker's claim state (leader lane in tile mode)
 };
 
 GC_DEV void set_err(Ctl *c, u64 code) { atomicCAS(&c->err.v, 0ull, code); }
 
-// control word of a record (single-word schemes): packed 8 B SoA words, or -- in the
-// ablation build -DGC_META_STRIDE=4 -- one word per 32 B sector (f-3; a compile-time
-// stride: a runtime one cost the tile kernels 12-100 B of spills).  MVCC: mvcc_lo / _hi.
-GC_DEV u64 *cw(const ExecParams &p, u32 rec) { return p.meta + (u64)rec * GC_META_STRIDE; }
+// control word of a record (single-word schemes): packed 8 B SoA words, or with
+// CC_FLAG_META_PAD one word per 32 B sector (f-3; the north star's metadata "padded to
+// avoid false sharing in L2"), a per-submit choice (ExecParams in shared memory keeps the
+// runtime stride off the register budget).  MVCC: mvcc_lo / _hi.
+GC_DEV u64 *cw(const ExecParams &p, u32 rec) {
+    // re-read at every use (volatile): a stride held in a register across the transaction
+    // loop made four tile kernels spill; the shared-memory load is ~30 cycles
+    return p.meta + ((u64)rec << *reinterpret_cast<const volatile uint32_t *>(&p.meta_shift));
+}
 
 GC_DEV bool dead(Th &th) {
     if (globaltimer_ns() > th.deadline) {
@@ -143,27 +159,28 @@ GC_DEV void inst(Th &th, const typename WL::Params &y, const typename WL::Lane &
 // per-attempt attribution: a committed attempt's time not spent in row
 // work, waits or timestamp allocation is CC-manager time; an aborted attempt's whole time
 // minus its timestamp allocation is abort time (its row work and waits included).
+// (the snapshot lives in the worker's shared-memory context, not in registers held across
+// the attempt)
 struct AttemptClock {
     Th &th;
-    u64 t0, u0, w0, s0;
-    GC_DEV explicit AttemptClock(Th &t) : th(t), t0(0), u0(0), w0(0), s0(0) {
+    GC_DEV explicit AttemptClock(Th &t) : th(t) {
         if (t.timing) {
-            t0 = clk64();
-            u0 = t.st[STAGE_USEFUL];
-            w0 = t.st[STAGE_WAIT];
-            s0 = t.st[STAGE_TS];
+            t.a_t0 = clk64();
+            t.a_u0 = t.st[STAGE_USEFUL];
+            t.a_w0 = t.st[STAGE_WAIT];
+            t.a_s0 = t.st[STAGE_TS];
         }
     }
     GC_DEV void done(bool committed) {
         if (!th.timing) return;
-        const u64 el = clk64() - t0;
-        const u64 du = th.st[STAGE_USEFUL] - u0, dw = th.st[STAGE_WAIT] - w0, ds = th.st[STAGE_TS] - s0;
+        const u64 el = clk64() - th.a_t0;
+        const u64 du = th.st[STAGE_USEFUL] - th.a_u0, dw = th.st[STAGE_WAIT] - th.a_w0, ds = th.st[STAGE_TS] - th.a_s0;
         th.st[STAGE_ATTEMPTS] += 1;
         if (committed) {
             th.st[STAGE_CC] += el > du + dw + ds ? el - du - dw - ds : 0;
         } else {
-            th.st[STAGE_USEFUL] = u0;
-            th.st[STAGE_WAIT] = w0;
+            th.st[STAGE_USEFUL] = th.a_u0;
+            th.st[STAGE_WAIT] = th.a_w0;
             th.st[STAGE_ABORT] += el > ds ? el - ds : 0;
         }
     }
@@ -205,7 +222,7 @@ GC_DEV void latch_acquire(uint32_t *l) {
 }
 GC_DEV void latch_release(uint32_t *l) { st_release32(l, 0u); }
 GC_DEV uint32_t *latch_of(const ExecParams &p, const u64 *w) {
-    return p.latch + (p.scheme == CC_MVCC ? (w - p.meta) : (w - p.meta) / GC_META_STRIDE);
+    return p.latch + (p.scheme == CC_MVCC ? (w - p.meta) : (w - p.meta) >> p.meta_shift);
 }
 
 GC_DEV u64 w_cas(const ExecParams &p, u64 *w, u64 expect, u64 desired) {
@@ -434,40 +451,37 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
 
 // ------------------------------------------------------------------ queue (a6)
 // Round 1 is the fresh batch, claimed in increasing id.  While fresh ids remain, an
-// aborted transaction is compacted into the retry batch (`ring`, appended with one
-// atomic per converged group); each id is appended at most once before the fresh ids
-// run out, so n_txn slots always suffice.  When a worker finds the fresh ids exhausted
-// it seals the retry batch -- it waits until no append is in flight, then every later
-// append attempt sees the exhaustion and retries in place -- and round 2 consumes the
-// sealed batch with one atomicAdd per claim.  Aborts after exhaustion retry in place
-// after their backoff.  Workers exit when both rounds are drained: no worker ever
-// polls for work that may not exist.
+// aborted transaction is compacted into the retry batch (`ring`): the converged workers
+// of a warp that append at the same moment take their slots with ONE atomicAdd on the
+// ring's tail word (ballot/popc through a coalesced group, the leader adds the group size
+// and shuffles the base back), then each writes its entry with a release store.  Each id
+// is appended at most once before the fresh ids run out, so n_txn slots always suffice.
+// The tail word carries a seal bit: the first worker that finds the fresh ids exhausted
+// sets it with one atomicOr, whose return value is the exact number of appends that won
+// a slot; it publishes that size (rtail = size + 1).  An append whose atomicAdd returns a
+// sealed word was refused and retries in place; round 2 consumes the sealed batch with
+// one atomicAdd per claim, waiting on an entry only in the rare case that its appender
+// has reserved the slot but not yet written it.  Aborts after exhaustion retry in place
+// after their backoff.  Workers exit when both rounds are drained.
+constexpr u64 RING_SEALED = 1ull << 63;    // tail word: seal bit | number of reserved slots
+constexpr u64 RING_VALID = 1ull << 63;     // ring entry: written | hot lane << 32 | gid
+
 GC_DEV bool try_append_retry(Th &th, u32 gid) {
     const ExecParams &p = *th.p;
     Ctl *c = p.ctl;
-    // Exhaustion is monotone: once seen, no append can happen, and this worker need not
-    // join the in-flight count -- which the sealers wait to see at 0 (aborts after the
-    // fresh ids ran out would otherwise keep it busy and stall every sealer).
+    // exhaustion is monotone: after it nothing is appended (and the seal follows)
     if (ld_relaxed(&c->head.v) >= p.n_txn) return false;
-    atomicAdd(&c->inflight.v, 1ull);
-    fence_sc();   // Dekker pair with the sealer: one of us sees the other
-    bool ok = false;
-    if (ld_relaxed(&c->head.v) < p.n_txn) {
-        const u64 r = atomicAdd(&c->tail.v, 1ull);
-        st_relaxed(p.ring + r, (u64)gid | ((u64)th.hot << 32));   // the hot lane travels along
-        ok = true;
-    }
-    fence_acqrel();
-    atomicAdd(&c->inflight.v, (u64)-1ll);
-    return ok;
+    cg::coalesced_group g = cg::coalesced_threads();
+    u64 old = 0;
+    if (g.thread_rank() == 0) old = atomicAdd(&c->tail.v, (u64)g.size());   // one atomic per group
+    old = g.shfl(old, 0);
+    if (old & RING_SEALED) return false;   // refused: the batch was sealed first
+    const u64 r = old + g.thread_rank();
+    // release: restarts[gid] (and everything this attempt released) precede the entry
+    st_release(p.ring + r, RING_VALID | ((u64)th.hot << 32) | gid);
+    return true;
 }
 
-struct Claim {
-    bool exhausted = false;
-    bool sealed = false;
-    u64 tail = 0;
-    u64 next = 0, end = 0;   // fresh ids claimed ahead (chunked claims), processed in order
-};
 
 // Claim work for one worker: a fresh id, else a retry-batch entry, else NO_TXN.
 template <int S>
@@ -484,24 +498,38 @@ GC_DEV u32 claim_work(Th &th, Claim &cl) {
         }
         const u64 s = cl.next++;
         th.hot = 0;
+        cl.fresh = true;
         if (s < p.n_txn) return (S == CC_GPUTX) ? p.rank_order[s] : (u32)s;
         cl.exhausted = true;
     }
+    cl.fresh = false;
     if (DET || (p.flags & CC_FLAG_IMMEDIATE_RETRY)) return NO_TXN;
     if (!cl.sealed) {
-        fence_sc();
-        Spin sp;
-        while (ld_relaxed(&c->inflight.v) != 0)   // relaxed polls, then one acquire
-            if (!sp.wait(th)) return NO_TXN;
-        fence_acqrel();
-        cl.tail = ld_acquire(&c->tail.v);
+        u64 t = ld_relaxed(&c->rtail.v);
+        if (t == 0) {
+            const u64 old = atomicOr(&c->tail.v, RING_SEALED);
+            if (!(old & RING_SEALED)) {   // this worker sealed: the size is exact
+                t = old + 1;
+                st_relaxed(&c->rtail.v, t);
+            } else {
+                Spin sp;
+                while ((t = ld_relaxed(&c->rtail.v)) == 0)
+                    if (!sp.wait(th)) return NO_TXN;
+            }
+        }
+        cl.tail = t - 1;
         cl.sealed = true;
     }
     if (cl.tail == 0 || ld_relaxed(&c->rhead.v) >= cl.tail) return NO_TXN;
     const u64 r = atomicAdd(&c->rhead.v, 1ull);
     if (r >= cl.tail) return NO_TXN;
-    const u64 e = ld_relaxed(p.ring + r);
-    th.hot = (u32)(e >> 32);
+    u64 e = ld_acquire(p.ring + r);   // pairs with the appender's release store
+    if (!(e & RING_VALID)) {          // reserved before the seal, not yet written
+        Spin sp(64);
+        while (!((e = ld_acquire(p.ring + r)) & RING_VALID))
+            if (!sp.wait(th)) return NO_TXN;
+    }
+    th.hot = (u32)(e >> 32) & 0x7FFFFFFFu;
     return (u32)e;
 }
 
@@ -771,6 +799,23 @@ GC_DEV bool tictoc_validate(const ExecParams &p, u64 *w, u64 obs, u64 cts) {
     }
 }
 
+// N1 intra-warp conflict detection.  Among the converged lanes of a warp that are about to
+// CAS a lock word, those naming the same record with at least one exclusive request are
+// arbitrated locally, by transaction age (gid + 1; smaller = older): the oldest goes on
+// to its CAS, the others take the scheme's conflict outcome at once without touching the
+// word -- no-wait / OCC write locks: abort; wait-die: the younger dies.  Equivalent to the
+// oldest winning the CAS race (a schedule the racing CASes could produce), but without the
+// losing CASes on a hot word, and lockstep lanes stop killing each other symmetrically
+// (the oldest always survives the local round).  Lanes alone on their record, or sharing
+// it only in shared mode, are unaffected.
+GC_DEV bool warp_lock_loser(u32 rec, bool ex, u32 age) {
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, rec);
+    const unsigned exm = __ballot_sync(act, ex) & peers;
+    if ((peers & (peers - 1)) == 0 || exm == 0) return false;   // alone, or all shared
+    return __reduce_min_sync(peers, age) != age;
+}
+
 GC_DEV bool draw_ts_overflow(u64 ts, const ExecParams &p) {
     if (ts > M31) {   // 31-bit field
         set_err(p.ctl, CC_ERR_TS_OVERFLOW);
@@ -780,10 +825,37 @@ GC_DEV bool draw_ts_overflow(u64 ts, const ExecParams &p) {
 }
 
 // ===================================================================== thread mode
-// One lane per transaction; accesses processed in ascending key order.
-template <int S, class WL>
-GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typename WL::Params &y,
-                      u64 &key_hi, u64 &key_lo) {
+// One lane per transaction; accesses processed in ascending key order.  The transaction's
+// read/write set -- one WL::Lane per access: record, mode, the value read, the buffered new
+// values and the control-word value it saw (OCC snapshot / lock-time word, TO / MVCC saved
+// word) -- is staged in shared memory (the OCC "private workspace"): a
+// strided array, element i of worker w at base[i * stride + w].  When the launch's working
+// lanes do not fit (dense wd, large bs) the same layout lives in a global workspace instead.
+// Either way no per-access state sits in registers or local memory (no spills).
+// Register budget: the executors run 1024-thread blocks, i.e. at most 64 registers, and a
+// row read alone needs 32 for its 16 words in flight.  So the per-worker context (Th) and
+// the block-uniform ExecParams live in shared memory: a kernel parameter whose address is
+// taken (th.p) would otherwise be copied to local memory, and Th's rarely used fields
+// (deadline, pacing state, stage pointers) would hold registers across the whole loop.
+extern __shared__ __align__(16) unsigned char gc_dyn_smem[];
+__shared__ __align__(16) unsigned char gc_exec_params[sizeof(ExecParams)];   // raw: no __shared__ constructor
+GC_DEV void exec_params_copy(const ExecParams &p) {
+    if (threadIdx.x == 0) *reinterpret_cast<ExecParams *>(gc_exec_params) = p;
+    __syncthreads();
+}
+GC_DEV const ExecParams *exec_params_smem(const ExecParams &) {
+    return reinterpret_cast<const ExecParams *>(gc_exec_params);
+}
+
+template <class Lane>
+struct Staged {
+    Lane *b;
+    u32 s;
+    GC_DEV Lane &operator[](u32 i) const { return b[(u64)i * s]; }
+};
+
+template <int S, class WL, class LA>
+GC_DEV int run_thread(Th &th, u32 gid, LA L, u32 n, const typename WL::Params &y, u64 &key_hi, u64 &key_lo) {
     const ExecParams &p = *th.p;
     if constexpr (S == CC_TPL_NW || S == CC_TPL_WD) {
         constexpr bool WD = S == CC_TPL_WD;
@@ -791,14 +863,17 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         u32 i = 0;
         int r = RES_OK;
         for (; i < n; i++) {
+            typename WL::Lane &Li = L[i];
             Spin sp;
             int st;
             u64 seen = 0;
-            while ((st = tpl_try<WD>(p, cw(p, L[i].rec), L[i].w, age, seen, th.attempt >= TPL_INTENT_AFTER)) == ST_WAIT)
-                if (!sp.wait(th)) { st = -1; break; }
-            if (st == ST_ABORT) { th.cw = cw(p, L[i].rec); th.cv = M31 << 31; }   // until free
+            if (warp_lock_loser(Li.rec, Li.w, age)) st = ST_ABORT;   // an older lane of this warp takes it
+            else
+                while ((st = tpl_try<WD>(p, cw(p, Li.rec), Li.w, age, seen, th.attempt >= TPL_INTENT_AFTER)) == ST_WAIT)
+                    if (!sp.wait(th)) { st = -1; break; }
+            if (st == ST_ABORT) { th.cw = cw(p, Li.rec); th.cv = M31 << 31; }   // until free
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
-            rd<WL>(th, y, L[i], gid, i, WL::row(y, L[i]));   // stable under the lock
+            rd<WL>(th, y, Li, gid, i, WL::row(y, Li));   // stable under the lock
         }
         if (r != RES_OK) {
             fence_acqrel();
@@ -821,14 +896,14 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         }
         if (draw_ts_overflow(ts, p)) return RES_FATAL;
         u32 pendm = 0;
-        u64 saved[WL::MAXK];
         int r = RES_OK;
         for (u32 i = 0; i < n && r == RES_OK; i++) {
+            typename WL::Lane &Li = L[i];
             Spin sp;
             for (;;) {
                 bool pend = false;
-                const int st = (S == CC_TO) ? to_step<WL>(th, p, y, L[i], gid, i, ts, pend, saved[i])
-                                            : mvcc_step<WL>(th, p, y, L[i], gid, i, ts, pend, saved[i]);
+                const int st = (S == CC_TO) ? to_step<WL>(th, p, y, Li, gid, i, ts, pend, Li.cv)
+                                            : mvcc_step<WL>(th, p, y, Li, gid, i, ts, pend, Li.cv);
                 if (pend) pendm |= 1u << i;
                 if (st == ST_DONE) break;
                 if (st == ST_ABORT) { r = RES_ABORT; break; }
@@ -839,8 +914,8 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         if (r != RES_OK) {
             for (u32 j = 0; j < n; j++)
                 if ((pendm >> j) & 1) {
-                    if (S == CC_TO) w_store(p, cw(p, L[j].rec), saved[j]);
-                    else mvcc_restore<WL>(p, L[j], saved[j]);
+                    if (S == CC_TO) w_store(p, cw(p, L[j].rec), L[j].cv);
+                    else mvcc_restore<WL>(p, L[j], L[j].cv);
                 }
             return r;
         }
@@ -853,24 +928,44 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
         key_lo = ts;
         return RES_OK;
     } else if constexpr (S == CC_SILO || S == CC_TICTOC) {
-        u64 obs[WL::MAXK], pre[WL::MAXK];
+        // read phase: L[i].cv = the word observed with the snapshot
         for (u32 i = 0; i < n; i++) {
             Spin sp;
             int st;
-            while ((st = occ_snap_step<WL>(th, p, y, L[i], gid, i, obs[i])) != ST_DONE)
+            while ((st = occ_snap_step<WL>(th, p, y, L[i], gid, i, L[i].cv)) != ST_DONE)
                 if (st == ST_WAIT && !sp.wait(th)) return RES_FATAL;
         }
+        // write-set locks (no-wait).  The lock-time word `pre` is checked against
+        // the snapshot at once -- Silo: pre == obs; TicToc: same WTS -- the check validation
+        // would make (the word cannot change while we hold its lock); for TicToc the write's
+        // slot then keeps `pre` (its RTS enters commit_ts, and an abort restores it).
         u32 locked = 0;
         bool ok = true;
-        for (u32 i = 0; i < n && ok; i++)
-            if (L[i].w) {
-                u64 seen = 0;
-                if (occ_lock(p, cw(p, L[i].rec), pre[i], seen)) locked |= 1u << i;
-                else {
-                    ok = false;
-                    if (seen & LOCKB) { th.cw = cw(p, L[i].rec); th.cv = LOCKB; }   // until unlocked
-                }
+        const u32 age = gid + 1;
+        for (u32 i = 0; i < n && ok; i++) {
+            typename WL::Lane &Li = L[i];
+            if (!Li.w) continue;
+            u64 seen = 0, pre = 0;
+            if (warp_lock_loser(Li.rec, true, age)) {   // an older lane of this warp locks it
+                ok = false;
+                th.cw = cw(p, Li.rec);
+                th.cv = LOCKB;
+                break;
             }
+            if (occ_lock(p, cw(p, Li.rec), pre, seen)) {
+                locked |= 1u << i;
+                if (S == CC_SILO ? pre != Li.cv : tt_wts(pre) != tt_wts(Li.cv)) {
+                    ok = false;
+                    w_store(p, cw(p, Li.rec), pre);   // changed since the read: unlock, abort
+                    locked &= ~(1u << i);
+                } else {
+                    Li.cv = pre;
+                }
+            } else {
+                ok = false;
+                if (seen & LOCKB) { th.cw = cw(p, Li.rec); th.cv = LOCKB; }   // until unlocked
+            }
+        }
         u64 ticket = 0, cts = 0;
         if (ok && S == CC_SILO) {
             ticket = agg_fetch_add(&p.ctl->ticket.v);   // serialization point
@@ -881,28 +976,28 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
             // the paper's launch ran 2.5 ms with the dense index, 425 ms with the binary
             // search.)
             for (u32 i = 0; i < n && ok; i++)
-                ok = L[i].w ? (pre[i] == obs[i]) : (ld_relaxed(cw(p, L[i].rec)) == obs[i]);
+                if (!L[i].w) ok = ld_relaxed(cw(p, L[i].rec)) == L[i].cv;
         }
         if (ok && S == CC_TICTOC) {
             for (u32 i = 0; i < n; i++) {   // commit_ts
-                if (L[i].w) cts = max(cts, tt_rts(pre[i]) + 1);
-                cts = max(cts, tt_wts(obs[i]));
+                const u64 v = L[i].cv;
+                if (L[i].w) cts = max(cts, tt_rts(v) + 1);
+                cts = max(cts, tt_wts(v));
             }
             for (u32 i = 0; i < n && ok; i++)
-                ok = L[i].w ? (tt_wts(pre[i]) == tt_wts(obs[i]))
-                            : tictoc_validate(p, cw(p, L[i].rec), obs[i], cts);
+                if (!L[i].w) ok = tictoc_validate(p, cw(p, L[i].rec), L[i].cv, cts);
             if (ok) ticket = agg_fetch_add(&p.ctl->ticket.v);   // after validation
         }
         if (!ok) {
             fence_acqrel();
             for (u32 j = 0; j < n; j++)
-                if ((locked >> j) & 1) w_store_relaxed(p, cw(p, L[j].rec), pre[j]);
+                if ((locked >> j) & 1) w_store_relaxed(p, cw(p, L[j].rec), L[j].cv);
             return RES_ABORT;
         }
         u64 nw;
         if (S == CC_SILO) {
             u64 tid = 0;
-            for (u32 i = 0; i < n; i++) tid = max(tid, obs[i]);
+            for (u32 i = 0; i < n; i++) tid = max(tid, L[i].cv);
             nw = (tid + 1) & ~LOCKB;   // TID = 1 + max observed (epoch dropped)
             key_hi = 0;
         } else {
@@ -950,19 +1045,33 @@ GC_DEV int run_thread(Th &th, u32 gid, typename WL::Lane *L, u32 n, const typena
 template <int S, class WL>
 __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel(ExecParams p, typename WL::Params y) {
     const u32 lane = threadIdx.x & 31u;
+    exec_params_copy(p);
     if (lane >= (1u << p.wd)) return;   // idle lanes exit at once
     if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
-    Th th;
-    th.p = &p;
+    // shared memory: [Th of every working lane][staged lanes (unless p.ws)]
+    const u32 per_warp = 1u << p.wd, per_block = (blockDim.x >> 5) * per_warp;
+    const u32 w_in_block = (threadIdx.x >> 5) * per_warp + lane;
+    Th &th = reinterpret_cast<Th *>(gc_dyn_smem)[w_in_block];
+    th.p = exec_params_smem(p);
     th.polls = 0;
     th.cw = nullptr;
     th.cv = 0;
     th.hot = 0;
     stages_init(th, p, true);
     th.deadline = globaltimer_ns() + p.watchdog_ns;
-    typename WL::Lane L[WL::MAXK];
-    Claim cl;
+    // the worker's staged read/write set: shared memory, or the global workspace
+    th.cl = Claim{};
+    Claim &cl = th.cl;
+    using Lane = typename WL::Lane;
+    Staged<Lane> L;
+    if (p.ws) {
+        L.b = reinterpret_cast<Lane *>(p.ws) + (u64)blockIdx.x * per_block + w_in_block;
+        L.s = gridDim.x * per_block;
+    } else {
+        L.b = reinterpret_cast<Lane *>(gc_dyn_smem + (size_t)per_block * sizeof(Th)) + w_in_block;
+        L.s = per_block;
+    }
     for (;;) {
         const u32 gid = claim_work<S>(th, cl);
         if (gid == NO_TXN) break;
@@ -1039,7 +1148,8 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             bool mine = act && !held;
             if (first && !tile.shfl(held || !act, first - 1)) mine = mine && li == first - 1;
             if (mine) {
-                st = tpl_try<WD>(p, cw(p, L.rec), L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
+                if (warp_lock_loser(L.rec, L.w, age)) st = ST_ABORT;   // an older tile of this warp takes it
+                else st = tpl_try<WD>(p, cw(p, L.rec), L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
                 held = st == ST_DONE;
             }
             const unsigned dying = tile.ballot(st == ST_ABORT);
@@ -1140,13 +1250,14 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         // write-set locks: all at once; a retry takes the lock that was busy last time
         // first, alone (see 2PL)
         const u32 first = th.attempt < 2 ? 0u : th.hot;
+        const u32 age = gid + 1;
         if (first && li == first - 1 && act && L.w) {
-            locked = occ_lock(p, cw(p, L.rec), pre, seen);
-            bad = !locked;
+            if (warp_lock_loser(L.rec, true, age)) { bad = true; seen = LOCKB; }   // an older tile locks it
+            else { locked = occ_lock(p, cw(p, L.rec), pre, seen); bad = !locked; }
         }
         if (!tile.any(bad) && act && L.w && !locked) {
-            locked = occ_lock(p, cw(p, L.rec), pre, seen);
-            bad = !locked;
+            if (warp_lock_loser(L.rec, true, age)) { bad = true; seen = LOCKB; }
+            else { locked = occ_lock(p, cw(p, L.rec), pre, seen); bad = !locked; }
         }
         {
             const unsigned busy = tile.ballot(bad && (seen & LOCKB));
@@ -1243,24 +1354,77 @@ template <int S, class WL, int G>
 __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(ExecParams p, typename WL::Params y) {
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const u32 li = tile.thread_rank();
+    exec_params_copy(p);
     if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
-    Th th;
-    th.p = &p;
+    Th &th = reinterpret_cast<Th *>(gc_dyn_smem)[threadIdx.x];   // per-lane context in shared memory
+    th.p = exec_params_smem(p);
     th.polls = 0;
     th.cw = nullptr;
     th.cv = 0;
     th.hot = 0;
     stages_init(th, p, li == 0);   // stages are timed by each tile's leader
     th.deadline = globaltimer_ns() + p.watchdog_ns;
-    typename WL::Lane L;
-    Claim cl;
+    // the lane's access (its read/write-set entry): registers, or -- for workloads whose
+    // entry is large (TPC-C: values read, buffered writes, strings) -- shared memory after
+    // the contexts, so the tile loop keeps its registers for the row reads
+    typename WL::Lane Lr;
+    typename WL::Lane &L = WL::STAGE_TILE_LANE
+                               ? reinterpret_cast<typename WL::Lane *>(gc_dyn_smem + (size_t)blockDim.x * sizeof(Th))[threadIdx.x]
+                               : Lr;
+    th.cl = Claim{};
+    Claim &cl = th.cl;
+    // Look-ahead (fresh ids; workloads whose accesses resolve without a memory probe --
+    // YCSB direct addressing, or a3's record table): a worker keeps two more fresh ids in a
+    // three-stage pipeline -- the claim's atomic is issued one transaction ahead, the next
+    // id's keys are loaded one transaction ahead and its rows and control words prefetched
+    // into L2 the transaction after that -- so a transaction starts with its claim, keys
+    // and lines already on chip instead of paying three dependent round trips first.  Ids
+    // are still executed in claim order per worker, so every transaction waited on is
+    // claimed by a running worker (the liveness argument of the queue is unchanged).
+    const bool LA = S != CC_GPUTX && p.claim_chunk <= 1 && WL::lookahead(p, y) && !(p.flags & CC_FLAG_NO_LOOKAHEAD);
+    u32 qX = NO_TXN, qP = NO_TXN;   // next to execute (lines prefetched) / keys loaded, lines prefetched now
+    u32 tokP = 0;                    // this lane's access token (key or record) of qP
+    u64 pend = ~0ull;                // leader: in-flight fresh claim (atomicAdd result)
+    u32 att = 0;                     // leader: restarts of the current transaction
     for (;;) {
         u32 gid = NO_TXN;
-        if (li == 0) gid = claim_work<S>(th, cl);
-        gid = tile.shfl(gid, 0);
-        th.hot = tile.shfl(th.hot, 0);   // from the retry-batch entry (0 for a fresh id)
+        bool fresh = false;
+        if (LA) {
+            u32 nid = NO_TXN;
+            if (li == 0 && pend != ~0ull) {   // the claim issued a transaction ago has arrived
+                if (pend < p.n_txn) {
+                    nid = (u32)pend;
+                    pend = atomicAdd(&p.ctl->head.v, 1ull);
+                } else {
+                    cl.exhausted = true;
+                    pend = ~0ull;
+                }
+            }
+            nid = tile.shfl(nid, 0);
+            gid = qX;   // the oldest claimed id runs: ids execute in claim order
+            if (gid == NO_TXN) { gid = qP; qP = NO_TXN; }   // (pipeline filling or draining)
+            if (gid == NO_TXN) { gid = nid; nid = NO_TXN; }
+            if (qP != NO_TXN) WL::prefetch_token(p, y, qP, li, tokP);   // its lines arrive during this transaction
+            const u32 tokN = nid != NO_TXN ? WL::token(p, y, nid, li) : 0u;   // consumed next round
+            qX = qP;
+            qP = nid;
+            tokP = tokN;
+            fresh = gid != NO_TXN;
+            th.hot = 0;
+        }
+        if (gid == NO_TXN) {   // synchronous claim: the first id, or the retry batch
+            if (li == 0) {
+                gid = claim_work<S>(th, cl);
+                fresh = cl.fresh;
+                if (LA && fresh && gid != NO_TXN && !cl.exhausted) pend = atomicAdd(&p.ctl->head.v, 1ull);
+            }
+            gid = tile.shfl(gid, 0);
+            fresh = tile.shfl(fresh, 0);
+            th.hot = tile.shfl(th.hot, 0);   // from the retry-batch entry (0 for a fresh id)
+        }
         if (gid == NO_TXN) break;
+        if (li == 0) att = fresh ? 0u : p.restarts[gid];   // fresh ids start at 0 restarts
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it
             if (S == CC_GPUTX && li == 0) kset_done(p, p.rank_of[gid]);
             continue;
@@ -1285,7 +1449,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
         while (!stop && !next) {
             u64 kh = 0, kl = 0;
             th.gid = gid;
-            th.attempt = tile.shfl(li == 0 ? p.restarts[gid] : 0u, 0);   // the leader owns restarts
+            th.attempt = tile.shfl(att, 0);   // the leader owns restarts
             AttemptClock ac(th);
             const int r = run_tile<S, WL>(tile, th, gid, L, y, kh, kl);
             ac.done(r == RES_OK);
@@ -1309,7 +1473,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
             } else {
                 int push = 0;
                 if (li == 0) {
-                    const u32 nr = p.restarts[gid] + 1;
+                    const u32 nr = ++att;
                     p.restarts[gid] = nr;
                     StageClock c(th, STAGE_ABORT);
                     retry_pace<S>(th, gid, nr);

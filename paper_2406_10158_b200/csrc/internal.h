@@ -5,12 +5,10 @@
 
 #include "../../include/gcctb.h"
 
-// Words per record of the single-word schemes' control-word array: 1 (packed 8 B SoA,
-// the shipped build) or 4 (one word per 32 B sector: the false-sharing ablation build,
-// GCCTB_NVCC_EXTRA=-DGC_META_STRIDE=4).
-#ifndef GC_META_STRIDE
-#define GC_META_STRIDE 1
-#endif
+// Words per record of the single-word schemes' control-word array: 1 (packed 8 B SoA) or,
+// with CC_FLAG_META_PAD, GC_META_PAD_WORDS (one word per 32 B sector);
+// the array is allocated for the padded layout.
+constexpr unsigned GC_META_PAD_WORDS = 4;
 
 namespace gcctb {
 
@@ -23,7 +21,7 @@ struct alignas(256) Counter {
 };
 struct Ctl {
     Counter head;       // claim counter over [0, n_txn)
-    Counter tail;       // retry-ring append counter (producers)
+    Counter tail;       // retry-ring append counter (producers): seal bit 63 | reserved slots
     Counter rhead;      // retry-ring claim counter (consumers)
     Counter done;       // committed transactions (counted at emission)
     Counter ts;         // TO/MVCC timestamp allocator (first ts = 1)
@@ -32,7 +30,7 @@ struct Ctl {
     Counter aborts;     // sum of restarts (counted at emission)
     Counter max_rank;   // GPUTx: number of K-sets - 1
     Counter rank_head;  // GPUTx rank-pass claim counter
-    Counter inflight;   // retry-batch appends in flight (sealing protocol)
+    Counter rtail;      // sealed retry-batch size + 1 (0: not sealed yet)
     Counter events;     // CC_FLAG_EVENTS: event sequence counter
     Counter pacing;     // TO/MVCC: transactions in retry backoff right now (adaptive cap)
     Counter kdone;      // GPUTx: K-sets completed so far (they complete in order)
@@ -61,13 +59,16 @@ struct ExecParams {
     unsigned long long watchdog_ns;
     Ctl *ctl;
     unsigned long long *meta;    // CC words: 1 x u64 per record, MVCC 2 x u64 (lo, hi)
-    uint32_t meta_stride = 1;    // words per record for the single-word schemes (GC_META_STRIDE)
+    uint32_t meta_stride = 1;    // words per record for the single-word schemes (1 or GC_META_PAD_WORDS)
+    uint32_t meta_shift = 0;     // log2(meta_stride)
     unsigned long long *arena;   // MVCC version nodes: ARENA_HDR header words + the row
     uint32_t to_backoff_cap;     // TO/MVCC backoff cap exponent (0: adaptive); experiment
                                  // knob, environment GCCTB_TO_BACKOFF_CAP
     unsigned long long mvcc_split;   // MVCC words: 0 = interleaved (lo, hi) pairs; else lo at
                                      // meta[r], hi at meta[mvcc_split + r] (CC_FLAG_MVCC_SPLIT)
     unsigned long long *ring;    // retry batch (compacted aborted ids), n_txn slots
+    void *ws;                    // thread mode: per-worker access workspace in global memory when
+                                 // it does not fit shared memory (else null: dynamic smem)
     uint32_t ring_cap;
     // per-transaction internal results
     uint8_t *committed;
@@ -134,8 +135,10 @@ struct YcsbParams {
 struct PrepBufs {
     unsigned long long *keys_in, *keys_out;   // (rec << 27) | (gid << 6) | (i << 1) | w
     uint32_t *acc_rec, *acc_seg, *acc_pos, *sorted_pos;
-    uint32_t *head_flag, *seg_id, *seg_start;
-    uint32_t *lw;          // last-write position (+1) at or before each sorted entry
+    uint32_t *head_flag;   // scan input: p at a segment head, else 0
+    uint32_t *lw;          // scan input: p + 1 at a write, else 0
+    uint32_t *seg_start;   // per sorted position: first position of its item's segment
+    uint32_t *seg_id;      // per sorted position: last write at or before it, + 1 (0: none)
     uint32_t *cursor;
     uint32_t *rank, *rank_sorted, *gid_in, *rank_order, *rank_count, *rank_done, *rank_start;
     void *cub_tmp;
@@ -146,9 +149,15 @@ struct PrepBufs {
 cudaError_t launch_reset_meta(int scheme, unsigned long long *meta, uint64_t n_records,
                               unsigned long long *ring, uint32_t ring_cap, Ctl *ctl,
                               cudaStream_t s, bool mvcc_split = false, uint32_t meta_stride = 1);
-cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
+// `smem` bytes of dynamic shared memory: the per-worker contexts (exec_th_bytes() per
+// working lane: every lane in tile mode, 2^wd per warp in thread mode), then in thread
+// mode the workers' staged accesses unless ExecParams::ws holds them in global memory
+cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block, size_t smem,
                              cudaStream_t s);
-int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block);
+int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block, size_t smem);
+size_t ycsb_lane_bytes();
+size_t exec_th_bytes();
+size_t tpcc_lane_bytes();
 cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBufs &b,
                                cudaStream_t s);
 // rank_block: threads per block of the GPUTx rank kernel (256 inline; 1024 on the prep
@@ -159,14 +168,27 @@ cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
 // a1: fold the batch's generator error word into the submit's control block (after a2)
 cudaError_t launch_merge_word(const unsigned long long *err, Ctl *dst, cudaStream_t s);
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket = false);
+                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket = false,
+                            bool lo_dense = false);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
+// sort.cu: stable LSD radix sort of u64 keys (+ optional u32 values) on bits [lo, hi),
+// keys_alt / vals_alt the ping-pong buffers, n = *n_dev if given (device-resident count,
+// cap the host-side capacity that sizes the grids) else cap; *keys_out / *vals_out
+// receive whichever buffer holds the result.  gc_scan_max2: inclusive max-scan of two u32
+// arrays (out may alias in).
+size_t gc_sort_temp_bytes(uint64_t cap);
+cudaError_t gc_sort(unsigned long long *keys, uint32_t *vals, unsigned long long *keys_alt, uint32_t *vals_alt,
+                    uint64_t cap, const unsigned long long *n_dev, int lo_bit, int hi_bit, void *temp,
+                    size_t temp_bytes, cudaStream_t s, unsigned long long **keys_out, uint32_t **vals_out);
+size_t gc_scan_temp_bytes(uint64_t n);
+cudaError_t gc_scan_max2(const uint32_t *a, const uint32_t *b, uint32_t *oa, uint32_t *ob, uint64_t n, void *temp,
+                         size_t temp_bytes, cudaStream_t s);
 cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads, cudaStream_t s);
 
 struct TpccParams;
-cudaError_t launch_tpcc_exec(const ExecParams &p, const TpccParams &y, int grid, int block,
+cudaError_t launch_tpcc_exec(const ExecParams &p, const TpccParams &y, int grid, int block, size_t smem,
                              cudaStream_t s);
-int tpcc_exec_max_blocks_per_sm(int scheme, int lanes, int block);
+int tpcc_exec_max_blocks_per_sm(int scheme, int lanes, int block, size_t smem);
 cudaError_t launch_tpcc_gather(const ExecParams &p, const TpccParams &y, PrepBufs &b,
                                uint64_t n_records, cudaStream_t s);
 cudaError_t launch_tpcc_pop(int table, unsigned long long *rows, unsigned long long first,
@@ -207,6 +229,18 @@ cudaError_t part_decide(const TpccParams &y, uint32_t rank, uint32_t world, uint
                         uint32_t round, unsigned long long *dec, cudaStream_t s);
 cudaError_t part_commit(const PartReq *req, uint64_t n, const uint8_t *vote, const unsigned long long *dec,
                         const TpccParams &y, cudaStream_t s);
+// CC_FLAG_PART_P2P (part.cu): window layout [flags | inbox world x cap | staging max_txn x K]
+struct PeerTab;
+size_t p2p_window_bytes(uint32_t world, uint32_t cap, uint32_t max_txn);
+cudaError_t p2p_send(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn, uint8_t *skip,
+                     unsigned long long *cnt, unsigned long long *cursor, const PeerTab &pt, uint32_t cap,
+                     unsigned long long epoch, Ctl *ctl, bool all, cudaStream_t s);
+cudaError_t p2p_phase_b(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                        const uint8_t *skip, const PeerTab &pt, uint32_t cap, unsigned long long epoch,
+                        unsigned long long *rc, PartReq *recv, unsigned long long *k1, unsigned long long *k2,
+                        uint32_t *i1, uint32_t *i2, void *tmp, size_t tmp_bytes, uint8_t *committed,
+                        unsigned long long *ohi, unsigned long long *olo, unsigned long long *read_out, Ctl *ctl,
+                        unsigned long long watchdog_ns, cudaStream_t s);
 cudaError_t part_repack(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
                         const uint8_t *skip, unsigned long long *cnt, unsigned long long *off,
                         unsigned long long *cursor, PartReq *out, cudaStream_t s);
@@ -230,5 +264,13 @@ cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32
 // roof.cu: out = {gather GB/s, CAS/s L2-resident, CAS/s > L2, hand-off ns (row), hop ns,
 //                 hand-off ns (row, acquire polls)}
 cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[6]);
+
+// load every kernel of the library now (lazy module loading may otherwise synchronise the
+// context at a first launch while kernels of this process wait on each other)
+void preload_prep_kernels();
+void preload_sort_kernels();
+void preload_part_kernels();
+void preload_tpcc_kernels();
+void preload_ycsb_kernels();
 
 }  // namespace gcctb

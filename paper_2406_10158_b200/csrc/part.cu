@@ -12,7 +12,6 @@
 // Result: Phase A (any interleaving across ranks: disjoint data) then Phase B in global
 // gid order, a serial order; the order key is (rank << 48 | scheme key) for Phase A
 // and (1 << 63, gid) for Phase B.
-#include <cub/cub.cuh>
 
 #include "exec.cuh"
 #include "tpcc.h"
@@ -118,9 +117,9 @@ __global__ void part_pack_kernel(TpccParams y, PartDev pd, uint32_t n_txn, const
 // resolve by-name customers on the owner's immutable index, then build sort keys
 // (kind << 60) | (row << 24) | (gid mod 2^24)
 __global__ void part_keys_kernel(PartReq *req, uint64_t n, TpccParams y, unsigned long long *keys,
-                                 uint32_t *idx, Ctl *ctl) {
+                                 uint32_t *idx, Ctl *ctl, const unsigned long long *n_dev = nullptr) {
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    if (k >= (n_dev ? *n_dev : n)) return;
     PartReq &r = req[k];
     if (r.kind == 2 && r.row == 0xFFFFFFFFu) {
         const uint32_t grp = r.cust * 1000u + r.last;
@@ -450,19 +449,15 @@ cudaError_t part_apply(PartReq *req, uint64_t n, const TpccParams &y, PartResp *
                        cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     part_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(req, n, y, k1, i1, ctl);
-    size_t bytes = tmp_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, i1, i2, (int)n, 0, 62, s);
+    u64 *sk = nullptr;
+    uint32_t *si = nullptr;
+    cudaError_t e = gc_sort(k1, i1, k2, i2, n, nullptr, 0, 62, tmp, tmp_bytes, s, &sk, &si);
     if (e) return e;
-    part_chain_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k2, i2, n, req, y, resp);
+    part_chain_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sk, si, n, req, y, resp);
     return cudaGetLastError();
 }
 
-size_t part_sort_bytes(uint64_t n) {
-    size_t b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n, 0, 62);
-    return b + 256;
-}
+size_t part_sort_bytes(uint64_t n) { return gc_sort_temp_bytes(n) + 256; }
 
 cudaError_t part_finish(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
                         const uint8_t *skip, const PartReq *sent, const PartResp *resp, uint64_t n_sent,
@@ -482,10 +477,11 @@ cudaError_t part_grant(PartReq *req, uint64_t n, const TpccParams &y, PartResp *
                        size_t tmp_bytes, Ctl *ctl, cudaStream_t s, bool ts_rule) {
     if (n == 0) return cudaSuccess;
     part_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(req, n, y, k1, i1, ctl);
-    size_t bytes = tmp_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, i1, i2, (int)n, 0, 62, s);
+    u64 *sk = nullptr;
+    uint32_t *si = nullptr;
+    cudaError_t e = gc_sort(k1, i1, k2, i2, n, nullptr, 0, 62, tmp, tmp_bytes, s, &sk, &si);
     if (e) return e;
-    part_grant_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(k2, i2, n, req, y, resp, vote, ts_rule);
+    part_grant_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sk, si, n, req, y, resp, vote, ts_rule);
     return cudaGetLastError();
 }
 
@@ -523,4 +519,232 @@ cudaError_t part_repack(const TpccParams &y, uint32_t rank, uint32_t world, uint
     return cudaGetLastError();
 }
 
+// ================================================================ exchange over peer memory
+// The deterministic phase B without the host in the loop (CC_FLAG_PART_P2P).  Every rank
+// owns an exchange window in its device memory -- flags, an inbox of `cap` request slots
+// per source rank, and the staging array of its own transactions' responses -- and maps
+// the windows of its peers (CUDA IPC across processes / GPUs over NVLink; plain pointers
+// between dbs of one process).  One partitioned cc_submit then runs, on the db stream:
+//   pack    the sender writes each request straight into the owner's inbox (a remote store
+//           over NVLink, a local one for itself) -- the pack and the transfer are one kernel;
+//   signal  one release store per owner (system scope): epoch << 32 | number of requests;
+//   [phase A executes meanwhile on this rank]
+//   wait    until every source's flag carries this epoch, then compact the inboxes;
+//   chain   sort by (item, global gid), apply each item's chain in gid order and store every
+//           response straight into the home's staging array (compute + transfer fused);
+//   signal  one release store per home: epoch;
+//   wait    for every owner, then assemble the distributed transactions and emit (a7).
+// The same kernels as the host-driven exchange decide what is applied and returned, so the
+// results are identical; only the transport differs.  A round's inbox is compacted before
+// its owner signals, and a sender packs its next round only after every owner's signal, so
+// windows are reused without further synchronisation.
+static __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+static __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+static __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__global__ void p2p_pack_kernel(TpccParams y, PartDev pd, uint32_t n_txn, const uint8_t *skip,
+                                unsigned long long *cursor, PeerTab pt, uint32_t cap, Ctl *ctl) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_txn || skip[g] != 1) return;
+    const uint32_t *t = y.tx + (u64)g * TPCC_TX_WORDS;
+    const uint32_t type = t[TX_TYPE], w = t[TX_W], d = t[TX_D];
+    const uint32_t n = type == 0 ? 3 + t[TX_OLCNT] : 3;
+    for (uint32_t i = 0; i < n; i++) {
+        PartReq r{};
+        r.gid = pd.rank * pd.n_local + g;
+        r.home = pd.rank | (i << 16);
+        r.type_d = type | (d << 8);
+        r.home_w = w | (d << 16);
+        r.last = 0xFFFFFFFFu;
+        uint32_t dest = pd.rank;
+        const uint32_t lw = w - pd.rank * pd.wpr;
+        if (i == 0) {
+            r.kind = 0;
+            r.row = lw;
+            r.amount = type == 1 ? t[TX_HAMT] : 0;
+        } else if (i == 1) {
+            r.kind = 1;
+            r.row = lw * TPCC_DIST + d;
+            r.amount = type == 1 ? t[TX_HAMT] : 0;
+        } else if (i == 2) {
+            r.kind = 2;
+            const uint32_t cw = type == 0 ? w : t[TX_CW], cd = type == 0 ? d : t[TX_CD];
+            dest = owner_of(pd, cw);
+            const uint32_t lcw = cw - dest * pd.wpr;
+            r.cust = lcw * TPCC_DIST + cd;
+            r.c_ids = cw | (cd << 16);
+            r.amount = type == 1 ? t[TX_HAMT] : 0;
+            if (t[TX_C] == 0xFFFFFFFFu) {
+                r.row = 0xFFFFFFFFu;
+                r.last = t[TX_CLAST];
+            } else {
+                r.row = r.cust * TPCC_CUST + t[TX_C];
+            }
+        } else {
+            r.kind = 3;
+            const uint32_t sw = t[TX_SUPQ + i - 3] >> 8;
+            dest = owner_of(pd, sw);
+            r.row = (sw - dest * pd.wpr) * TPCC_STOCK + t[TX_ITEM + i - 3];
+            r.amount = t[TX_SUPQ + i - 3] & 0xFF;
+            r.type_d |= (sw != w ? 1u : 0u) << 16;
+        }
+        const unsigned long long pos = atomicAdd(&cursor[dest], 1ull);
+        if (pos < cap) pt.inbox[dest][(u64)pd.rank * cap + pos] = r;   // into the owner's window
+        else atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_CONFIG);      // exchange capacity exceeded
+    }
+}
+
+// flags: req[s] at flags[s * P2P_FLAG_STRIDE], resp[d] at flags[(P2P_MAXW + d) * P2P_FLAG_STRIDE]
+__global__ void p2p_signal_req_kernel(PeerTab pt, PartDev pd, const unsigned long long *cursor, uint32_t cap,
+                                      unsigned long long epoch) {
+    const uint32_t d = threadIdx.x;
+    if (d >= pd.world) return;
+    const unsigned long long c = cursor[d] < cap ? cursor[d] : cap;
+    fence_sys();   // the pack kernel's stores (ordered before this kernel) precede the flag
+    st_release_sys(pt.flags[d] + (u64)pd.rank * P2P_FLAG_STRIDE, (epoch << 32) | c);
+}
+
+// wait for every source's requests of this epoch; rc[s] = count, rc[world + s] = offset,
+// rc[2 * world] = total
+__global__ void p2p_wait_req_kernel(const unsigned long long *flags, PartDev pd, unsigned long long epoch,
+                                    unsigned long long *rc, Ctl *ctl, u64 watchdog_ns) {
+    const uint32_t s = threadIdx.x;
+    const u64 deadline = globaltimer_ns() + watchdog_ns;
+    if (s < pd.world) {
+        unsigned long long v;
+        unsigned ns = 32;
+        while (((v = ld_acquire_sys(flags + (u64)s * P2P_FLAG_STRIDE)) >> 32) != epoch) {
+            if (globaltimer_ns() > deadline) {
+                atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_WATCHDOG);
+                v = epoch << 32;   // count 0: nothing from this source
+                break;
+            }
+            __nanosleep(ns);
+            ns = ns < 1024 ? ns * 2 : 1024;
+        }
+        rc[s] = v & 0xFFFFFFFFull;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long o = 0;
+        for (uint32_t k = 0; k < pd.world; k++) {
+            rc[pd.world + k] = o;
+            o += rc[k];
+        }
+        rc[2 * pd.world] = o;
+    }
+}
+
+__global__ void p2p_compact_kernel(const PartReq *inbox, const unsigned long long *rc, uint32_t world, uint32_t cap,
+                                   PartReq *recv) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= (uint64_t)world * cap) return;
+    const uint32_t s = (uint32_t)(k / cap), j = (uint32_t)(k % cap);
+    if (j < rc[s]) recv[rc[world + s] + j] = inbox[k];
+}
+
+// one thread per item chain, in gid order; each response goes straight to its home's
+// staging array (remote store): slot (local gid, access lane)
+__global__ void p2p_chain_kernel(const unsigned long long *skeys, const uint32_t *sidx, const unsigned long long *n_dev,
+                                 const PartReq *req, TpccParams y, PeerTab pt, uint32_t n_local) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t n = *n_dev;
+    if (p >= n) return;
+    if (p > 0 && (skeys[p - 1] >> 24) == (skeys[p] >> 24)) return;   // chain head only
+    for (uint64_t q = p; q < n && (skeys[q] >> 24) == (skeys[p] >> 24); q++) {
+        const PartReq &r = req[sidx[q]];
+        const uint32_t home = r.home & 0xFFFFu, lane = r.home >> 16;
+        pt.stage[home][(u64)(r.gid - home * n_local) * TPCC_K + lane] = part_access(r, y, true);
+    }
+}
+
+__global__ void p2p_signal_resp_kernel(PeerTab pt, PartDev pd, unsigned long long epoch) {
+    const uint32_t h = threadIdx.x;
+    if (h >= pd.world) return;
+    fence_sys();   // the chain kernel's remote stores precede the flag
+    st_release_sys(pt.flags[h] + (u64)(P2P_MAXW + pd.rank) * P2P_FLAG_STRIDE, epoch << 32);
+}
+
+__global__ void p2p_wait_resp_kernel(const unsigned long long *flags, PartDev pd, unsigned long long epoch, Ctl *ctl,
+                                     u64 watchdog_ns) {
+    const uint32_t d = threadIdx.x;
+    if (d >= pd.world) return;
+    const u64 deadline = globaltimer_ns() + watchdog_ns;
+    unsigned ns = 32;
+    while ((ld_acquire_sys(flags + (u64)(P2P_MAXW + d) * P2P_FLAG_STRIDE) >> 32) != epoch) {
+        if (globaltimer_ns() > deadline) {
+            atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_WATCHDOG);
+            return;
+        }
+        __nanosleep(ns);
+        ns = ns < 1024 ? ns * 2 : 1024;
+    }
+}
+
+size_t p2p_window_bytes(uint32_t world, uint32_t cap, uint32_t max_txn) {
+    return P2P_FLAG_BYTES + (size_t)world * cap * sizeof(PartReq) + (size_t)max_txn * TPCC_K * sizeof(PartResp);
+}
+
+// send side: classify, pack into the owners' windows, signal (before phase A)
+cudaError_t p2p_send(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn, uint8_t *skip,
+                     unsigned long long *cnt, unsigned long long *cursor, const PeerTab &pt, uint32_t cap,
+                     unsigned long long epoch, Ctl *ctl, bool all, cudaStream_t s) {
+    const PartDev pd{rank, world, wpr, n_txn};
+    cudaMemsetAsync(cnt, 0, world * 8ull, s);
+    cudaMemsetAsync(cursor, 0, world * 8ull, s);
+    part_classify_kernel<<<(n_txn + 255) / 256, 256, 0, s>>>(y, pd, n_txn, skip, cnt, all);
+    p2p_pack_kernel<<<(n_txn + 255) / 256, 256, 0, s>>>(y, pd, n_txn, skip, cursor, pt, cap, ctl);
+    p2p_signal_req_kernel<<<1, P2P_MAXW, 0, s>>>(pt, pd, cursor, cap, epoch);
+    return cudaGetLastError();
+}
+
+// owner side (after phase A) and home side: phase B through the windows, then assemble
+cudaError_t p2p_phase_b(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
+                        const uint8_t *skip, const PeerTab &pt, uint32_t cap, unsigned long long epoch,
+                        unsigned long long *rc, PartReq *recv, unsigned long long *k1, unsigned long long *k2,
+                        uint32_t *i1, uint32_t *i2, void *tmp, size_t tmp_bytes, uint8_t *committed,
+                        unsigned long long *ohi, unsigned long long *olo, unsigned long long *read_out, Ctl *ctl,
+                        u64 watchdog_ns, cudaStream_t s) {
+    const PartDev pd{rank, world, wpr, n_txn};
+    const unsigned long long *myflags = pt.flags[rank];
+    p2p_wait_req_kernel<<<1, P2P_MAXW, 0, s>>>(myflags, pd, epoch, rc, ctl, watchdog_ns);
+    const uint64_t capn = (uint64_t)world * cap;
+    const unsigned gb = (unsigned)((capn + 255) / 256);
+    p2p_compact_kernel<<<gb, 256, 0, s>>>(pt.inbox[rank], rc, world, cap, recv);
+    const unsigned long long *n_dev = rc + 2 * world;
+    part_keys_kernel<<<gb, 256, 0, s>>>(recv, capn, y, k1, i1, ctl, n_dev);
+    u64 *sk = nullptr;
+    uint32_t *si = nullptr;
+    cudaError_t e = gc_sort(k1, i1, k2, i2, capn, n_dev, 0, 62, tmp, tmp_bytes, s, &sk, &si);
+    if (e) return e;
+    p2p_chain_kernel<<<gb, 256, 0, s>>>(sk, si, n_dev, recv, y, pt, n_txn);
+    p2p_signal_resp_kernel<<<1, P2P_MAXW, 0, s>>>(pt, pd, epoch);
+    p2p_wait_resp_kernel<<<1, P2P_MAXW, 0, s>>>(myflags, pd, epoch, ctl, watchdog_ns);
+    part_assemble_kernel<<<(n_txn + 127) / 128, 128, 0, s>>>(y, pd, n_txn, skip, pt.stage[rank], committed, ohi, olo,
+                                                             read_out, false);
+    return cudaGetLastError();
+}
+
+// Lazy module loading (the CUDA 12 default) may synchronise the context the first time a
+// kernel is launched -- which deadlocks once kernels of one process wait on each other
+// across streams (CC_FLAG_PART_P2P between the dbs of one process).  cc_part_connect*
+// loads every kernel up front.
+template <class F>
+static void preload1(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, f);
+}
+void preload_part_kernels() {
+    preload1(part_classify_kernel); preload1(part_scan_kernel); preload1(part_pack_kernel); preload1(part_keys_kernel);
+    preload1(part_chain_kernel); preload1(part_grant_kernel); preload1(part_commit_kernel); preload1(part_stage_kernel);
+    preload1(part_assemble_kernel); preload1(part_decide_kernel); preload1(part_dec_kernel); preload1(part_recount_kernel);
+    preload1(p2p_pack_kernel); preload1(p2p_signal_req_kernel); preload1(p2p_wait_req_kernel); preload1(p2p_compact_kernel);
+    preload1(p2p_chain_kernel); preload1(p2p_signal_resp_kernel); preload1(p2p_wait_resp_kernel);
+}
 }  // namespace gcctb

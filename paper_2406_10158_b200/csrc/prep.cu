@@ -3,11 +3,12 @@
 //
 // Access table: every access becomes the 64-bit sort key
 //   (rec << 27) | (gid << 6) | (i << 1) | is_write
-// so one radix sort groups accesses per item with transaction ids ascending; segment
-// boundaries come from a head-flag prefix sum (the paper uses thrust sort + scan; we
-// use CUB from the toolkit).
+// so one radix sort groups accesses per item with transaction ids ascending (keys arrive
+// in (gid, i) order and the sort is stable, so only the record bits are sorted).  Each
+// sorted position then needs the start of its item's segment and the last write at or
+// before it: one fused max-scan of (head ? p : 0, write ? p + 1 : 0).  The paper uses
+// thrust sort + scan; here both are the library's own kernels (sort.cu).
 #include <cstdlib>
-#include <cub/cub.cuh>
 
 #include "exec.cuh"
 
@@ -69,38 +70,30 @@ cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, u64 *ohi, u6
 }
 
 // ------------------------------------------------------------------ a3 kernels
-__global__ void head_flag_kernel(const u64 *keys, uint32_t *head, uint32_t *wpos, uint64_t n) {
+// markers for the fused max-scan: segment heads (their own position) and writes (p + 1)
+__global__ void a3_marks_kernel(const u64 *keys, uint32_t *head_at, uint32_t *write_at, uint64_t n) {
     const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const u64 k = keys[p];
-    head[p] = (p == 0 || (keys[p - 1] >> KEY_SHIFT) != (k >> KEY_SHIFT)) ? 1u : 0u;
-    wpos[p] = (k & 1ull) ? (uint32_t)(p + 1) : 0u;   // write marker for the last-write scan
-}
-
-__global__ void seg_start_kernel(const uint32_t *head, const uint32_t *seg_id, uint32_t *seg_start,
-                                 uint32_t *cursor, uint64_t n) {
-    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    if (head[p]) {
-        seg_start[seg_id[p] - 1] = (uint32_t)p;
-        cursor[seg_id[p] - 1] = 0u;
-    }
+    head_at[p] = (p == 0 || (keys[p - 1] >> KEY_SHIFT) != (k >> KEY_SHIFT)) ? (uint32_t)p : 0u;
+    write_at[p] = (k & 1ull) ? (uint32_t)(p + 1) : 0u;   // write marker for the last-write scan
 }
 
 // GaccO lock table: queue position of each access inside its item's segment
-// ("recording which transaction currently owns each data item").
-__global__ void positions_kernel(const u64 *keys, const uint32_t *seg_id, const uint32_t *seg_start,
-                                 uint32_t K, uint32_t *acc_seg, uint32_t *acc_pos,
-                                 uint32_t *sorted_pos, uint64_t n) {
+// ("recording which transaction currently owns each data item").  An item's
+// segment is named by its first sorted position, which also indexes its cursor.
+__global__ void positions_kernel(const u64 *keys, const uint32_t *seg_of, uint32_t K, uint32_t *acc_seg,
+                                 uint32_t *acc_pos, uint32_t *sorted_pos, uint32_t *cursor, uint64_t n) {
     const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const u64 k = keys[p];
     const uint64_t gid = (k >> 6) & GID_MASK, i = (k >> 1) & 31u;
     const uint64_t a = gid * K + i;
-    const uint32_t seg = seg_id[p] - 1;
+    const uint32_t seg = seg_of[p];
     acc_seg[a] = seg;
-    acc_pos[a] = (uint32_t)p - seg_start[seg];
+    acc_pos[a] = (uint32_t)p - seg;
     sorted_pos[a] = (uint32_t)p;
+    if (seg == (uint32_t)p) cursor[p] = 0u;
 }
 
 // GPUTx ranks (PAPER.md:218 read per Z1): rank(T) = 1 + max rank over the conflicting
@@ -112,7 +105,7 @@ constexpr uint32_t RANK_UNSET = 0xFFFFFFFFu;
 
 template <int G>
 __global__ void __launch_bounds__(1024) gputx_rank_kernel(
-    const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_id, const uint32_t *seg_start,
+    const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_of,
     const uint32_t *lw, uint32_t *rank, uint32_t n_txn, uint32_t K, Ctl *ctl,
     u64 watchdog_ns, uint32_t poll_cap_ns) {
     // a tile of G lanes per transaction, lane i resolves the predecessors of access i
@@ -129,7 +122,7 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
         bool fail = false;
         if (li < K) {
             const uint32_t p = sorted_pos[(u64)gid * K + li];
-            const uint32_t s0 = seg_start[seg_id[p] - 1];
+            const uint32_t s0 = seg_of[p];   // first position of this item's segment
             const bool w = keys[p] & 1ull;
             const uint32_t q = (p > s0) ? lw[p - 1] : 0u;   // last write before p (+1)
             const bool has_q = q > s0;                        // inside this segment
@@ -184,21 +177,32 @@ __global__ void iota_kernel(uint32_t *a, uint32_t n) {
     if (i < n) a[i] = i;
 }
 
-// K-set boundaries over the rank-sorted transactions
-__global__ void rank_bounds_kernel(const uint32_t *rs, uint32_t *start, uint32_t *count,
+// K-set boundaries over the rank-sorted transactions (sorted ranks as u64 sort keys)
+__global__ void rank_bounds_kernel(const u64 *rs, uint32_t *start, uint32_t *count,
                                    uint32_t *done, uint32_t n) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const uint32_t r = rs[p];
-    if (p == 0 || rs[p - 1] != r) { start[r] = p; done[r] = 0; }
+    const uint32_t r = (uint32_t)rs[p];
+    if (p == 0 || (uint32_t)rs[p - 1] != r) { start[r] = p; done[r] = 0; }
 }
-__global__ void rank_count_kernel(const uint32_t *rs, const uint32_t *start, uint32_t *count,
+__global__ void rank_count_kernel(const u64 *rs, const uint32_t *start, uint32_t *count,
                                   uint32_t n, Ctl *ctl) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const uint32_t r = rs[p];
-    if (p == n - 1 || rs[p + 1] != r) count[r] = p + 1 - start[r];
+    const uint32_t r = (uint32_t)rs[p];
+    if (p == n - 1 || (uint32_t)rs[p + 1] != r) count[r] = p + 1 - start[r];
     if (p == n - 1) ctl->max_rank.v = r;   // ranks sorted ascending: the last is the max
+}
+// sort keys of a u32 (rank) or u64 (order key) array, with the identity permutation
+__global__ void keys_iota_kernel(const uint32_t *r32, const u64 *r64, u64 *keys, uint32_t *idx, uint32_t n) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    keys[g] = r32 ? (u64)r32[g] : r64[g];
+    idx[g] = g;
+}
+__global__ void copy_u32_kernel(const uint32_t *src, uint32_t *dst, uint32_t n) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) dst[g] = src[g];
 }
 
 int rank_kernel_grid() {
@@ -220,21 +224,8 @@ static int bits_for(uint64_t x) {
 }
 
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn) {
-    size_t a = 0, b = 0, c = 0, d = 0, e = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, a, (const u64 *)nullptr, (u64 *)nullptr, (int)n_acc);
-    cub::DeviceScan::InclusiveSum(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_acc);
-    cub::DeviceScan::InclusiveScan(nullptr, c, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                   cub::Max(), (int)n_acc);
-    cub::DeviceRadixSort::SortPairs(nullptr, d, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_txn);
-    cub::DeviceRadixSort::SortPairs(nullptr, e, (const u64 *)nullptr, (u64 *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_txn);
-    size_t m = a;
-    m = m > b ? m : b;
-    m = m > c ? m : c;
-    m = m > d ? m : d;
-    m = m > e ? m : e;
-    return m + 256;
+    const size_t a = gc_sort_temp_bytes(n_acc > n_txn ? n_acc : n_txn), b = gc_scan_temp_bytes(n_acc);
+    return (a > b ? a : b) + 256;
 }
 
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records, bool gputx,
@@ -242,47 +233,44 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     const uint64_t n = (uint64_t)p.n_txn * p.K;
     const int blk = 256;
     const unsigned g = (unsigned)((n + blk - 1) / blk);
-    size_t bytes = b.cub_bytes;
     cudaError_t e;
     const int end_bit = KEY_SHIFT + bits_for(n_records);
     // keys arrive in (gid, i) order; a stable LSD sort on the record bits alone keeps
     // transaction ids ascending within each item (3 passes for 2^24 records, not 7)
-    e = cub::DeviceRadixSort::SortKeys(b.cub_tmp, bytes, b.keys_in, b.keys_out, (int)n, KEY_SHIFT,
-                                       end_bit > 64 ? 64 : end_bit, s);
+    u64 *sk = nullptr;
+    e = gc_sort(b.keys_in, nullptr, b.keys_out, nullptr, n, nullptr, KEY_SHIFT, end_bit > 64 ? 64 : end_bit,
+                b.cub_tmp, b.cub_bytes, s, &sk, nullptr);
     if (e) return e;
-    head_flag_kernel<<<g, blk, 0, s>>>(b.keys_out, b.head_flag, b.lw, n);
-    bytes = b.cub_bytes;
-    e = cub::DeviceScan::InclusiveSum(b.cub_tmp, bytes, b.head_flag, b.seg_id, (int)n, s);
+    // per sorted position: its segment's first position (seg_start) and the last write at
+    // or before it, + 1 (seg_id's storage)
+    a3_marks_kernel<<<g, blk, 0, s>>>(sk, b.head_flag, b.lw, n);
+    e = gc_scan_max2(b.head_flag, b.lw, b.seg_start, b.seg_id, n, b.cub_tmp, b.cub_bytes, s);
     if (e) return e;
-    seg_start_kernel<<<g, blk, 0, s>>>(b.head_flag, b.seg_id, b.seg_start, b.cursor, n);
-    positions_kernel<<<g, blk, 0, s>>>(b.keys_out, b.seg_id, b.seg_start, p.K, b.acc_seg,
-                                       b.acc_pos, b.sorted_pos, n);
+    positions_kernel<<<g, blk, 0, s>>>(sk, b.seg_start, p.K, b.acc_seg, b.acc_pos, b.sorted_pos, b.cursor, n);
     if (!gputx) return cudaGetLastError();
-    // last write at or before each sorted position (+1): inclusive max-scan of markers
-    bytes = b.cub_bytes;
-    // (head_flag is dead after the positions pass; it receives the scan output)
-    e = cub::DeviceScan::InclusiveScan(b.cub_tmp, bytes, b.lw, b.head_flag, cub::Max(), (int)n, s);
-    if (e) return e;
     fill_u32_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank, RANK_UNSET, p.n_txn);
     // experiment knobs (environment): poll cap and a grid divisor for the rank pass
     static const uint32_t poll_cap = getenv("GCCTB_RANK_POLL_NS") ? (uint32_t)atoi(getenv("GCCTB_RANK_POLL_NS")) : 512u;
     static const int grid_div = getenv("GCCTB_RANK_GRID_DIV") ? atoi(getenv("GCCTB_RANK_GRID_DIV")) : 1;
     if (grid_div > 1) grid = grid / grid_div > 0 ? grid / grid_div : 1;
     if (p.K <= 16)
-        gputx_rank_kernel<16><<<grid, rank_block, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
-                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns, poll_cap);
+        gputx_rank_kernel<16><<<grid, rank_block, 0, s>>>(sk, b.sorted_pos, b.seg_start, b.seg_id, b.rank, p.n_txn,
+                                                          p.K, p.ctl, p.watchdog_ns, poll_cap);
     else
-        gputx_rank_kernel<32><<<grid, rank_block, 0, s>>>(b.keys_out, b.sorted_pos, b.seg_id, b.seg_start,
-                                                   b.head_flag, b.rank, p.n_txn, p.K, p.ctl, p.watchdog_ns, poll_cap);
-    iota_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.gid_in, p.n_txn);
-    bytes = b.cub_bytes;
-    e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, b.rank, b.rank_sorted, b.gid_in,
-                                        b.rank_order, (int)p.n_txn, 0, bits_for(p.n_txn), s);
+        gputx_rank_kernel<32><<<grid, rank_block, 0, s>>>(sk, b.sorted_pos, b.seg_start, b.seg_id, b.rank, p.n_txn,
+                                                          p.K, p.ctl, p.watchdog_ns, poll_cap);
+    // K-sets: transactions sorted by rank (stable: ids ascending inside a K-set)
+    const unsigned gt = (p.n_txn + blk - 1) / blk;
+    u64 *k1 = sk == b.keys_in ? b.keys_out : b.keys_in, *k2 = sk;   // the access keys are dead now
+    keys_iota_kernel<<<gt, blk, 0, s>>>(b.rank, nullptr, k1, b.gid_in, p.n_txn);
+    u64 *rk = nullptr;
+    uint32_t *ro = nullptr;
+    e = gc_sort(k1, b.gid_in, k2, b.rank_sorted, p.n_txn, nullptr, 0, bits_for(p.n_txn), b.cub_tmp, b.cub_bytes, s,
+                &rk, &ro);
     if (e) return e;
-    rank_bounds_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank_sorted, b.rank_start,
-                                                                 b.rank_count, b.rank_done, p.n_txn);
-    rank_count_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank_sorted, b.rank_start,
-                                                                b.rank_count, p.n_txn, p.ctl);
+    copy_u32_kernel<<<gt, blk, 0, s>>>(ro, b.rank_order, p.n_txn);
+    rank_bounds_kernel<<<gt, blk, 0, s>>>(rk, b.rank_start, b.rank_count, b.rank_done, p.n_txn);
+    rank_count_kernel<<<gt, blk, 0, s>>>(rk, b.rank_start, b.rank_count, p.n_txn, p.ctl);
     return cudaGetLastError();
 }
 
@@ -363,8 +351,15 @@ __global__ void dense_ticket_pos_kernel(const u64 *lo, const uint8_t *committed,
     if (g < n) pos_out[g] = committed[g] ? (uint32_t)lo[g] : 0xFFFFFFFFu;
 }
 
+// TicToc: every committed transaction drew one ticket 0..n-1 -- the order by key_lo is
+// the inverse permutation, no sort
+__global__ void ticket_perm_kernel(const u64 *lo, const uint8_t *committed, uint32_t *perm, uint32_t n) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n && committed[g] && lo[g] < n) perm[lo[g]] = g;
+}
+
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket) {
+                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket, bool lo_dense) {
     const uint32_t n = p.n_txn;
     const int blk = 256;
     const unsigned g = (n + blk - 1) / blk;
@@ -376,24 +371,28 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         iota_kernel<<<g, blk, 0, s>>>(b.rank_order, n);
         commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
     } else {
-        iota_kernel<<<g, blk, 0, s>>>(b.gid_in, n);
-        size_t bytes = b.cub_bytes;
         u64 *k1 = b.keys_in, *k2 = b.keys_out;   // n_acc >= n scratch
-        // key_lo is a ticket, a 31-bit timestamp or a gid: 32 bits suffice (copy_out flags
-        // a value >= 2^32 - 1 as an overflow), 4 radix passes instead of 8
-        cudaError_t e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, p.order_lo, k1, b.gid_in,
-                                                        b.rank_order, (int)n, 0, 32, s);
-        if (e) return e;
-        if (two_pass) {
-            gather_hi_kernel<<<g, blk, 0, s>>>(p.order_hi, b.rank_order, k1, n);
-            bytes = b.cub_bytes;
-            e = cub::DeviceRadixSort::SortPairs(b.cub_tmp, bytes, k1, k2, b.rank_order, b.gid_in,
-                                                (int)n, 0, 64, s);
-            if (e) return e;
-            commit_pos_kernel<<<g, blk, 0, s>>>(b.gid_in, p.committed, pos, n);
+        u64 *sk = k2;
+        uint32_t *perm = b.rank_order;
+        cudaError_t e;
+        if (lo_dense) {   // TicToc: tickets are drawn only by committing attempts -- 0..n-1
+            ticket_perm_kernel<<<g, blk, 0, s>>>(p.order_lo, p.committed, perm, n);
         } else {
-            commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
+            keys_iota_kernel<<<g, blk, 0, s>>>(nullptr, p.order_lo, k1, b.gid_in, n);
+            // key_lo is a ticket, a 31-bit timestamp or a gid: 32 bits suffice (copy_out flags
+            // a value >= 2^32 - 1 as an overflow), 4 radix passes instead of 8
+            e = gc_sort(k1, b.gid_in, k2, b.rank_order, n, nullptr, 0, 32, b.cub_tmp, b.cub_bytes, s, &sk, &perm);
+            if (e) return e;
         }
+        if (two_pass) {   // then by key_hi (stable): TicToc's (commit_ts, ticket), partitioned (phase, ...)
+            u64 *hk = sk == k1 ? k2 : k1;
+            uint32_t *hv = perm == b.gid_in ? b.rank_order : b.gid_in;
+            gather_hi_kernel<<<g, blk, 0, s>>>(p.order_hi, perm, hk, n);
+            // TicToc: key_hi = commit_ts (48 bits); partitioned: the phase bits (63, rank << 48)
+            e = gc_sort(hk, perm, sk, hv, n, nullptr, 0, lo_dense ? 48 : 64, b.cub_tmp, b.cub_bytes, s, &sk, &perm);
+            if (e) return e;
+        }
+        commit_pos_kernel<<<g, blk, 0, s>>>(perm, p.committed, pos, n);
     }
     copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);
     stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats, p.stages, p.sticky);
@@ -420,4 +419,22 @@ cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+
+// Lazy module loading (the CUDA 12 default) may synchronise the context the first time a
+// kernel is launched -- which deadlocks once kernels of one process wait on each other
+// across streams (CC_FLAG_PART_P2P between the dbs of one process).  cc_part_connect*
+// loads every kernel up front.
+template <class F>
+static void preload1(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, f);
+}
+void preload_prep_kernels() {
+    preload1(reset_kernel); preload1(zero_txn_kernel); preload1(a3_marks_kernel); preload1(positions_kernel);
+    preload1(gputx_rank_kernel<16>); preload1(gputx_rank_kernel<32>); preload1(fill_u32_kernel); preload1(iota_kernel);
+    preload1(rank_bounds_kernel); preload1(rank_count_kernel); preload1(keys_iota_kernel); preload1(copy_u32_kernel);
+    preload1(commit_pos_kernel); preload1(gather_hi_kernel); preload1(copy_out_kernel); preload1(stages_reduce_kernel);
+    preload1(stats_kernel); preload1(dense_ticket_pos_kernel); preload1(ticket_perm_kernel); preload1(merge_err_kernel);
+    preload1(merge_word_kernel);
+}
 }  // namespace gcctb

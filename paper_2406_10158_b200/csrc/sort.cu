@@ -1,0 +1,329 @@
+// sort.cu -- the library's own radix sort and max-scan (no CUB on the hot path).
+//
+// Where they are used: the a3 access table ("sort the access table by
+// item, then transaction id"; the paper uses thrust), the GPUTx K-set order (sort by
+// rank), a7 commit positions (sort by the scheme's order key) and phase B of
+// partitioned TPC-C (sort the received requests by item, then global transaction id).
+//
+// gc_sort: stable LSD radix sort of u64 keys (optionally carrying a u32 value) over a bit
+// range, 8-bit digits, three kernels per pass:
+//   count   -- one block per 4,096-key tile: per-digit counts of its tile (smem atomics),
+//              written digit-major so that one exclusive scan gives every (digit, tile) its
+//              output base;
+//   scan    -- one 1,024-thread block scans the 256 x tiles counts;
+//   scatter -- one block per tile, each warp a contiguous 512-key run in 32-key chunks:
+//              a key's rank among equal digits is __match_any_sync + popc in its chunk plus
+//              its warp's running count (smem), so the scatter is stable (warp multisplit).
+// The number of keys may live in device memory (n_dev): grids are sized for the host
+// capacity and tiles past n exit, so a caller whose n is known only on the device (the
+// phase-B exchange) sorts without a host synchronisation.
+//
+// gc_scan_max2: inclusive max-scan of two u32 arrays at once (segment starts and last
+// writes of the access table), reduce-then-scan in three kernels.
+#include <cstdint>
+
+#include "internal.h"
+
+namespace gcctb {
+
+typedef unsigned long long u64;
+typedef uint32_t u32;
+
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+constexpr int SORT_PER = 16;                              // keys per thread
+constexpr int SORT_TILE = SORT_THREADS * SORT_PER;        // 4,096 keys per tile
+constexpr int SORT_WTILE = 32 * SORT_PER;                 // 512 keys per warp, contiguous
+
+static __device__ __forceinline__ u64 n_of(const u64 *n_dev, u64 n_host) { return n_dev ? *n_dev : n_host; }
+
+// per-tile digit counts, digit-major (counts[d * tiles + t]); tiles past n write zeros
+__global__ void __launch_bounds__(SORT_THREADS) sort_count_kernel(const u64 *keys, const u64 *n_dev, u64 n_host,
+                                                                   int shift, u32 *counts, u32 tiles) {
+    __shared__ u32 h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const u64 n = n_of(n_dev, n_host);
+    const u64 base = (u64)blockIdx.x * SORT_TILE;
+    if (base < n) {
+#pragma unroll
+        for (int r = 0; r < SORT_PER; r++) {
+            const u64 i = base + (u64)r * SORT_THREADS + threadIdx.x;
+            if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFF], 1u);
+        }
+    }
+    __syncthreads();
+    counts[(u64)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan (digit-major) of the counts of the tiles that hold keys, in place: one
+// block, 4 threads per digit row -- row totals, a scan of the 256 totals, then each row's
+// scan from its carry.  Loads are independent (unrolled) so a row costs a few round trips.
+__global__ void __launch_bounds__(1024) sort_scan_kernel(u32 *counts, u32 tiles, const u64 *n_dev, u64 n_host) {
+    __shared__ u32 part[1024];
+    __shared__ u32 rowbase[257];
+    const u64 n = n_of(n_dev, n_host);
+    const u32 active = (u32)((n + SORT_TILE - 1) / SORT_TILE);
+    const u32 d = threadIdx.x >> 2, q = threadIdx.x & 3;
+    const u32 per = (active + 3) / 4, lo = q * per, hi = min(active, lo + per);
+    u32 *row = counts + (u64)d * tiles;
+    u32 s = 0;
+#pragma unroll 8
+    for (u32 t = lo; t < hi; t++) s += row[t];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {   // one warp scans the 256 row totals (8 rows per lane)
+        u32 tot[8], acc = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const u32 r = threadIdx.x * 8 + k;
+            tot[k] = part[4 * r] + part[4 * r + 1] + part[4 * r + 2] + part[4 * r + 3];
+            acc += tot[k];
+        }
+        u32 x = acc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (threadIdx.x >= (u32)o) x += y;
+        }
+        u32 run = x - acc;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            rowbase[threadIdx.x * 8 + k] = run;
+            run += tot[k];
+        }
+    }
+    __syncthreads();
+    u32 run = rowbase[d];
+    for (u32 k = 0; k < q; k++) run += part[4 * d + k];
+    for (u32 t = lo; t < hi; t++) {
+        const u32 c = row[t];
+        row[t] = run;
+        run += c;
+    }
+}
+
+// stable scatter of one tile: warp w owns keys [w * 512, (w + 1) * 512) of the tile, in
+// chunks of 32 processed in order.  Phase 1 counts each warp's digits (a chunk's equal
+// digits are one __match_any_sync group, its lowest lane adds the group size -- no
+// atomics); phase 2 turns them into each warp's first output position per digit (global
+// base of the tile + the warps before it); phase 3 writes every key at its warp's running
+// position + its rank in the chunk's group.  Two block barriers per tile.
+template <bool PAIRS>
+__global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *keys, const u32 *vals, u64 *keys_out,
+                                                                     u32 *vals_out, const u64 *n_dev, u64 n_host,
+                                                                     int shift, const u32 *offs, u32 tiles) {
+    __shared__ u32 wc[SORT_WARPS][256];
+    const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const u64 n = n_of(n_dev, n_host);
+    const u64 w0 = (u64)blockIdx.x * SORT_TILE + (u64)warp * SORT_WTILE;
+    if ((u64)blockIdx.x * SORT_TILE >= n) return;   // uniform
+#pragma unroll
+    for (int w = 0; w < SORT_WARPS; w++) wc[w][tid] = 0;
+    __syncthreads();
+    u64 k[SORT_PER];
+    u32 dg[SORT_PER];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int c = 0; c < SORT_PER; c++) {
+        const u64 i = w0 + (u64)c * 32 + lane;
+        const bool ok = i < n;
+        k[c] = ok ? keys[i] : 0ull;
+        dg[c] = ok ? (u32)((k[c] >> shift) & 0xFF) : 256u;
+    }
+#pragma unroll
+    for (int c = 0; c < SORT_PER; c++) {
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg[c]);
+        if (dg[c] < 256u && (peers & lt) == 0) wc[warp][dg[c]] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {   // thread `tid` owns digit `tid`: first position of each warp's keys of that digit
+        u32 run = offs[(u64)tid * tiles + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < SORT_WARPS; w++) {
+            const u32 c = wc[w][tid];
+            wc[w][tid] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < SORT_PER; c++) {
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg[c]);
+        if (dg[c] < 256u) {
+            const u32 pos = wc[warp][dg[c]] + __popc(peers & lt);
+            keys_out[pos] = k[c];
+            if (PAIRS) vals_out[pos] = vals[w0 + (u64)c * 32 + lane];
+        }
+        __syncwarp();
+        if (dg[c] < 256u && (peers & lt) == 0) wc[warp][dg[c]] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+size_t gc_sort_temp_bytes(uint64_t cap) {
+    const u64 tiles = (cap + SORT_TILE - 1) / SORT_TILE;
+    return (size_t)(256 * (tiles ? tiles : 1)) * sizeof(u32) + 256;
+}
+
+cudaError_t gc_sort(u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, uint64_t cap, const u64 *n_dev,
+                    int lo_bit, int hi_bit, void *temp, size_t temp_bytes, cudaStream_t s, u64 **keys_out,
+                    u32 **vals_out) {
+    u64 *ka = keys, *kb = keys_alt;
+    u32 *va = vals, *vb = vals_alt;
+    *keys_out = ka;
+    if (vals_out) *vals_out = va;
+    if (cap == 0 || hi_bit <= lo_bit) return cudaSuccess;
+    const u64 tiles = (cap + SORT_TILE - 1) / SORT_TILE;
+    if (gc_sort_temp_bytes(cap) > temp_bytes || tiles > 0xFFFFFFFFull) return cudaErrorInvalidValue;
+    u32 *counts = reinterpret_cast<u32 *>(temp);
+    for (int sh = lo_bit; sh < hi_bit; sh += 8) {
+        sort_count_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, n_dev, cap, sh, counts, (u32)tiles);
+        sort_scan_kernel<<<1, 1024, 0, s>>>(counts, (u32)tiles, n_dev, cap);
+        if (va)
+            sort_scatter_kernel<true><<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, va, kb, vb, n_dev, cap, sh, counts,
+                                                                             (u32)tiles);
+        else
+            sort_scatter_kernel<false><<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, nullptr, kb, nullptr, n_dev, cap, sh,
+                                                                              counts, (u32)tiles);
+        u64 *tk = ka; ka = kb; kb = tk;
+        u32 *tv = va; va = vb; vb = tv;
+    }
+    *keys_out = ka;
+    if (vals_out) *vals_out = va;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ max-scan of two arrays
+constexpr int SCAN_THREADS = 256, SCAN_PER = 8, SCAN_TILE = SCAN_THREADS * SCAN_PER;
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const u32 *a, const u32 *b, u64 n, u32 *bm) {
+    __shared__ u32 ra[SCAN_THREADS / 32], rb[SCAN_THREADS / 32];
+    const u64 t0 = (u64)blockIdx.x * SCAN_TILE;
+    u32 ma = 0, mb = 0;
+    for (int r = 0; r < SCAN_PER; r++) {
+        const u64 i = t0 + (u64)r * SCAN_THREADS + threadIdx.x;
+        if (i < n) {
+            ma = max(ma, a[i]);
+            mb = max(mb, b[i]);
+        }
+    }
+    ma = __reduce_max_sync(0xFFFFFFFFu, ma);
+    mb = __reduce_max_sync(0xFFFFFFFFu, mb);
+    if ((threadIdx.x & 31) == 0) {
+        ra[threadIdx.x >> 5] = ma;
+        rb[threadIdx.x >> 5] = mb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < SCAN_THREADS / 32; w++) {
+            ma = max(ma, ra[w]);
+            mb = max(mb, rb[w]);
+        }
+        bm[2 * blockIdx.x] = ra[0] > ma ? ra[0] : ma;
+        bm[2 * blockIdx.x + 1] = rb[0] > mb ? rb[0] : mb;
+    }
+}
+
+// exclusive max-scan of the block maxima (pairs), one block of 1,024 threads, each a
+// contiguous chunk (independent loads), then a scan of the chunk maxima
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(u32 *bm, u64 tiles) {
+    __shared__ u32 pa[1024], pb[1024];
+    const u64 per = (tiles + 1023) / 1024, lo = (u64)threadIdx.x * per, hi = lo + per < tiles ? lo + per : tiles;
+    u32 ma = 0, mb = 0;
+    for (u64 t = lo; t < hi; t++) {
+        ma = max(ma, bm[2 * t]);
+        mb = max(mb, bm[2 * t + 1]);
+    }
+    pa[threadIdx.x] = ma;
+    pb[threadIdx.x] = mb;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const u32 xa = threadIdx.x >= (unsigned)o ? pa[threadIdx.x - o] : 0u;
+        const u32 xb = threadIdx.x >= (unsigned)o ? pb[threadIdx.x - o] : 0u;
+        __syncthreads();
+        pa[threadIdx.x] = max(pa[threadIdx.x], xa);
+        pb[threadIdx.x] = max(pb[threadIdx.x], xb);
+        __syncthreads();
+    }
+    u32 ca = threadIdx.x ? pa[threadIdx.x - 1] : 0u, cb = threadIdx.x ? pb[threadIdx.x - 1] : 0u;
+    for (u64 t = lo; t < hi; t++) {
+        const u32 xa = bm[2 * t], xb = bm[2 * t + 1];
+        bm[2 * t] = ca;
+        bm[2 * t + 1] = cb;
+        ca = max(ca, xa);
+        cb = max(cb, xb);
+    }
+}
+
+// block-local inclusive max-scan with the carry of the tiles before; out may alias in
+__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const u32 *a, const u32 *b, u64 n, const u32 *bm,
+                                                                   u32 *oa, u32 *ob) {
+    __shared__ u32 wa[SCAN_THREADS / 32], wb[SCAN_THREADS / 32];
+    const u64 t0 = (u64)blockIdx.x * SCAN_TILE;
+    u32 ca = bm[2 * blockIdx.x], cb = bm[2 * blockIdx.x + 1];
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = 0; r < SCAN_PER; r++) {
+        const u64 i = t0 + (u64)r * SCAN_THREADS + threadIdx.x;
+        u32 xa = i < n ? a[i] : 0u, xb = i < n ? b[i] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {   // warp inclusive max-scan
+            const u32 ya = __shfl_up_sync(0xFFFFFFFFu, xa, o), yb = __shfl_up_sync(0xFFFFFFFFu, xb, o);
+            if (lane >= (u32)o) {
+                xa = max(xa, ya);
+                xb = max(xb, yb);
+            }
+        }
+        if (lane == 31) {
+            wa[warp] = xa;
+            wb[warp] = xb;
+        }
+        __syncthreads();
+        u32 pa = ca, pb = cb;
+        for (u32 w = 0; w < warp; w++) {
+            pa = max(pa, wa[w]);
+            pb = max(pb, wb[w]);
+        }
+        if (i < n) {
+            oa[i] = max(pa, xa);
+            ob[i] = max(pb, xb);
+        }
+        for (u32 w = 0; w < SCAN_THREADS / 32; w++) {   // carry into the next round
+            ca = max(ca, wa[w]);
+            cb = max(cb, wb[w]);
+        }
+        __syncthreads();
+    }
+}
+
+size_t gc_scan_temp_bytes(uint64_t n) { return (size_t)(2 * ((n + SCAN_TILE - 1) / SCAN_TILE + 1)) * sizeof(u32); }
+
+cudaError_t gc_scan_max2(const u32 *a, const u32 *b, u32 *oa, u32 *ob, uint64_t n, void *temp, size_t temp_bytes,
+                         cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (gc_scan_temp_bytes(n) > temp_bytes) return cudaErrorInvalidValue;
+    const u64 tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    u32 *bm = reinterpret_cast<u32 *>(temp);
+    scan_reduce_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(a, b, n, bm);
+    scan_blocks_kernel<<<1, 1024, 0, s>>>(bm, tiles);
+    scan_apply_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(a, b, n, bm, oa, ob);
+    return cudaGetLastError();
+}
+
+
+// Lazy module loading (the CUDA 12 default) may synchronise the context the first time a
+// kernel is launched -- which deadlocks once kernels of one process wait on each other
+// across streams (CC_FLAG_PART_P2P between the dbs of one process).  cc_part_connect*
+// loads every kernel up front.
+template <class F>
+static void preload1(F f) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, f);
+}
+void preload_sort_kernels() {
+    preload1(sort_count_kernel); preload1(sort_scan_kernel); preload1(sort_scatter_kernel<true>);
+    preload1(sort_scatter_kernel<false>); preload1(scan_reduce_kernel); preload1(scan_blocks_kernel);
+    preload1(scan_apply_kernel);
+}
+}  // namespace gcctb

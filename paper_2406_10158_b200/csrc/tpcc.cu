@@ -7,7 +7,6 @@
 // are writes to per-transaction reserved slots (Z15); Item and the name index are
 // immutable and outside CC (Z16); NewOrder's rollback omitted (Z17); totals rounded
 // half up (Z18); NewOrder increments d_next_o_id (Z14).
-#include <cub/cub.cuh>
 
 #include "exec.cuh"
 #include "tpcc.h"
@@ -123,7 +122,7 @@ cudaError_t launch_tpcc_pop(int table, u64 *rows, u64 first, u64 n, u64 seed, ui
 // ---------------------------------------------------------------- name index
 // Immutable (Z16): per (w, d, last) group the customers sorted by (c_first, c_id)
 // (TPC-C §2.5.2.2; ties by c_id, reading R5).  Built once at load.
-__global__ void name_key_kernel(const u64 *cu, uint32_t n, uint32_t *key, uint32_t *val, u64 seed,
+__global__ void name_key_kernel(const u64 *cu, uint32_t n, u64 *key, uint32_t *val, u64 seed,
                                 uint32_t c_load, u64 first_row) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -138,7 +137,7 @@ __device__ __forceinline__ u64 bswap64(u64 x) {
     return ((u64)lo << 32) | hi;
 }
 
-__global__ void name_group_kernel(const uint32_t *skey, uint32_t *vals, uint32_t n, uint32_t *start,
+__global__ void name_group_kernel(const u64 *skey, uint32_t *vals, uint32_t n, uint32_t *start,
                                   uint32_t *count, const u64 *cu) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -167,21 +166,23 @@ __global__ void name_group_kernel(const uint32_t *skey, uint32_t *vals, uint32_t
 cudaError_t build_name_index(const u64 *cu, uint32_t n_cust, u64 first_row, u64 seed, uint32_t c_load,
                              uint32_t *idx_start, uint32_t *idx_count, uint32_t *idx_rows,
                              uint32_t n_groups, cudaStream_t s) {
-    uint32_t *k1 = nullptr, *k2 = nullptr, *v1 = nullptr;
+    u64 *k1 = nullptr, *k2 = nullptr, *sk = nullptr;
+    uint32_t *v1 = nullptr, *v2 = nullptr, *sv = nullptr;
     void *tmp = nullptr;
-    size_t bytes = 0;
+    const size_t bytes = gc_sort_temp_bytes(n_cust);
     cudaError_t e;
-    if ((e = cudaMalloc(&k1, n_cust * 4ull)) || (e = cudaMalloc(&k2, n_cust * 4ull)) ||
-        (e = cudaMalloc(&v1, n_cust * 4ull)))
+    if ((e = cudaMalloc(&k1, n_cust * 8ull)) || (e = cudaMalloc(&k2, n_cust * 8ull)) ||
+        (e = cudaMalloc(&v1, n_cust * 4ull)) || (e = cudaMalloc(&v2, n_cust * 4ull)) || (e = cudaMalloc(&tmp, bytes)))
         return e;
     cudaMemsetAsync(idx_count, 0, n_groups * 4ull, s);
     name_key_kernel<<<(n_cust + 255) / 256, 256, 0, s>>>(cu, n_cust, k1, v1, seed, c_load, first_row);
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1, k2, v1, idx_rows, (int)n_cust, 0, 32, s);
-    if ((e = cudaMalloc(&tmp, bytes))) return e;
-    cub::DeviceRadixSort::SortPairs(tmp, bytes, k1, k2, v1, idx_rows, (int)n_cust, 0, 32, s);
-    name_group_kernel<<<(n_cust + 255) / 256, 256, 0, s>>>(k2, idx_rows, n_cust, idx_start, idx_count, cu);
-    e = cudaStreamSynchronize(s);
-    cudaFree(k1); cudaFree(k2); cudaFree(v1); cudaFree(tmp);
+    int hb = 1;   // group keys < n_groups
+    while (hb < 32 && (1ull << hb) < n_groups) hb++;
+    e = gc_sort(k1, v1, k2, v2, n_cust, nullptr, 0, hb, tmp, bytes, s, &sk, &sv);
+    if (!e) e = cudaMemcpyAsync(idx_rows, sv, n_cust * 4ull, cudaMemcpyDeviceToDevice, s);
+    if (!e) name_group_kernel<<<(n_cust + 255) / 256, 256, 0, s>>>(sk, idx_rows, n_cust, idx_start, idx_count, cu);
+    if (!e) e = cudaStreamSynchronize(s);
+    cudaFree(k1); cudaFree(k2); cudaFree(v1); cudaFree(v2); cudaFree(tmp);
     return e ? e : cudaGetLastError();
 }
 
@@ -291,6 +292,7 @@ cudaError_t launch_tpcc_gen(uint32_t *tx, uint32_t n_txn, u64 seed, uint32_t W, 
 struct TpccWL {
     static constexpr int MAXK = TPCC_K;          // W, D, C + up to 15 stock lines
     static constexpr int ROW_WORDS = TPCC_C_WORDS;   // largest CC row (MVCC node payload)
+    static constexpr bool STAGE_TILE_LANE = true;    // tile mode: the ~110 B entry lives in shared memory
     using Params = TpccParams;
     enum { KW = 0, KD = 1, KC = 2, KS = 3 };
     struct Lane {
@@ -301,6 +303,7 @@ struct TpccWL {
         u32 qty, sw, item, price, brand_i;
         u64 v0, v1, v2, v3;   // values read / buffered new values (per kind)
         u64 s0, s1, s2, s3;   // string payload (w_name / d_name / s_dist) or the BC record
+        u64 cv;               // thread mode: control word seen (OCC snapshot / lock-time word, TO / MVCC saved word)
     };
 
     static GC_DEV u64 *row(const TpccParams &y, const Lane &L) {
@@ -377,13 +380,43 @@ struct TpccWL {
     }
 
     static GC_DEV u64 warm(const ExecParams &, const TpccParams &, const Lane &) { return 0; }
+    // tile-mode look-ahead: off -- a TPC-C access needs its descriptor (and a by-name Payment
+    // the name index) before its row is known, so only the descriptor lines could be fetched
+    // ahead, and the pipeline's registers made the GaccO tile kernel spill
+    static GC_DEV bool lookahead(const ExecParams &, const TpccParams &) { return false; }
+    static GC_DEV u32 token(const ExecParams &, const TpccParams &, u32, u32) { return 0u; }
+    static GC_DEV void prefetch_token(const ExecParams &, const TpccParams &y, u32 gid, u32 i, u32) {
+        if (i < 2) prefetch_l2(y.tx + (u64)gid * TPCC_TX_WORDS + 32 * i);   // 160 B: two lines
+    }
 
-    static GC_DEV u32 load_all(const ExecParams &p, const TpccParams &y, u32 gid, Lane *L) {
+    template <class LA>
+    static GC_DEV u32 load_all(const ExecParams &p, const TpccParams &y, u32 gid, LA L) {
         const uint32_t *t = y.tx + (u64)gid * TPCC_TX_WORDS;
         const u32 n = t[TX_TYPE] == 0 ? 3 + t[TX_OLCNT] : 3;
         for (u32 i = 0; i < n; i++)
             if (!load_lane(p, y, gid, i, L[i])) return 0xFFFFFFFFu;
         return n;
+    }
+
+    // the same test on s_data read through L2 as words: the 8-byte window at byte offset
+    // i < 43 of the 50 letters, assembled from two adjacent little-endian words in registers
+    // (a byte array here lived in local memory)
+    static GC_DEV bool has_original_words(const u64 *src) {
+        constexpr u64 ORIG = 0x4C414E494749524Full;   // "ORIGINAL" as a little-endian u64
+        bool found = false;
+        u64 a = ld_cg(src);
+#pragma unroll
+        for (int j = 0; j < 6; j++) {
+            const u64 b = ld_cg(src + j + 1);
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+                if (8 * j + r > 42) break;
+                const u64 win = r ? ((a >> (8 * r)) | (b << (64 - 8 * r))) : a;
+                found |= win == ORIG;
+            }
+            a = b;
+        }
+        return found;
     }
 
     static GC_DEV bool has_original(const uint8_t *s) {
@@ -452,9 +485,7 @@ struct TpccWL {
                 L.s0 = ld_cg(src + 3 + 3 * d);                          // s_dist_{d}
                 L.s1 = ld_cg(src + 4 + 3 * d);
                 L.s2 = ld_cg(src + 5 + 3 * d);
-                u64 sd[7];
-                for (int k = 0; k < 7; k++) sd[k] = ld_cg(src + 33 + k);
-                const bool bs = has_original(reinterpret_cast<const uint8_t *>(sd));
+                const bool bs = has_original_words(src + 33);
                 L.v3 = (u64)q | ((u64)(bs && L.brand_i) << 32);         // q before, brand-generic
                 break;
             }
@@ -579,7 +610,8 @@ struct TpccWL {
         }
     }
 
-    static GC_DEV void emit_txn(const ExecParams &p, const TpccParams &y, u32 gid, const Lane *L, u32 n) {
+    template <class LA>
+    static GC_DEV void emit_txn(const ExecParams &p, const TpccParams &y, u32 gid, LA L, u32 n) {
         const uint32_t *t = y.tx + (u64)gid * TPCC_TX_WORDS;
         u64 sum = 0;
         for (u32 i = 3; i < n; i++) {
@@ -608,46 +640,56 @@ struct TpccWL {
 
 // ---------------------------------------------------------------- launchers
 template <int S>
-static cudaError_t launch_s(const ExecParams &p, const TpccParams &y, int grid, int block, cudaStream_t s) {
-    if (p.lanes > 1) exec_tile_kernel<S, TpccWL, 32><<<grid, block, 0, s>>>(p, y);
-    else exec_thread_kernel<S, TpccWL><<<grid, block, 0, s>>>(p, y);
-    return cudaGetLastError();
+static cudaError_t launch_s(const ExecParams &p, const TpccParams &y, int grid, int block, size_t smem,
+                            cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kern) {
+        if (smem > 32 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) kern<<<grid, block, smem, s>>>(p, y);
+    };
+    if (p.lanes > 1) go(exec_tile_kernel<S, TpccWL, 32>);
+    else go(exec_thread_kernel<S, TpccWL>);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_tpcc_exec(const ExecParams &p, const TpccParams &y, int grid, int block, cudaStream_t s) {
+cudaError_t launch_tpcc_exec(const ExecParams &p, const TpccParams &y, int grid, int block, size_t smem,
+                             cudaStream_t s) {
     switch (p.scheme) {
-        case CC_TPL_NW: return launch_s<CC_TPL_NW>(p, y, grid, block, s);
-        case CC_TPL_WD: return launch_s<CC_TPL_WD>(p, y, grid, block, s);
-        case CC_TO: return launch_s<CC_TO>(p, y, grid, block, s);
-        case CC_MVCC: return launch_s<CC_MVCC>(p, y, grid, block, s);
-        case CC_SILO: return launch_s<CC_SILO>(p, y, grid, block, s);
-        case CC_TICTOC: return launch_s<CC_TICTOC>(p, y, grid, block, s);
-        case CC_GPUTX: return launch_s<CC_GPUTX>(p, y, grid, block, s);
-        case CC_GACCO: return launch_s<CC_GACCO>(p, y, grid, block, s);
+        case CC_TPL_NW: return launch_s<CC_TPL_NW>(p, y, grid, block, smem, s);
+        case CC_TPL_WD: return launch_s<CC_TPL_WD>(p, y, grid, block, smem, s);
+        case CC_TO: return launch_s<CC_TO>(p, y, grid, block, smem, s);
+        case CC_MVCC: return launch_s<CC_MVCC>(p, y, grid, block, smem, s);
+        case CC_SILO: return launch_s<CC_SILO>(p, y, grid, block, smem, s);
+        case CC_TICTOC: return launch_s<CC_TICTOC>(p, y, grid, block, smem, s);
+        case CC_GPUTX: return launch_s<CC_GPUTX>(p, y, grid, block, smem, s);
+        case CC_GACCO: return launch_s<CC_GACCO>(p, y, grid, block, smem, s);
     }
     return cudaErrorInvalidValue;
 }
 
 template <class F>
-static int occ_of(F f, int block) {
+static int occ_of(F f, int block, size_t smem) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, block, 0);
+    if (smem > 32 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, block, smem);
     return nb;
 }
 template <int S>
-static int occ_s(int lanes, int block) {
-    return lanes > 1 ? occ_of(exec_tile_kernel<S, TpccWL, 32>, block) : occ_of(exec_thread_kernel<S, TpccWL>, block);
+static int occ_s(int lanes, int block, size_t smem) {
+    return lanes > 1 ? occ_of(exec_tile_kernel<S, TpccWL, 32>, block, smem)
+                     : occ_of(exec_thread_kernel<S, TpccWL>, block, smem);
 }
-int tpcc_exec_max_blocks_per_sm(int scheme, int lanes, int block) {
+size_t tpcc_lane_bytes() { return sizeof(TpccWL::Lane); }
+int tpcc_exec_max_blocks_per_sm(int scheme, int lanes, int block, size_t smem) {
     switch (scheme) {
-        case CC_TPL_NW: return occ_s<CC_TPL_NW>(lanes, block);
-        case CC_TPL_WD: return occ_s<CC_TPL_WD>(lanes, block);
-        case CC_TO: return occ_s<CC_TO>(lanes, block);
-        case CC_MVCC: return occ_s<CC_MVCC>(lanes, block);
-        case CC_SILO: return occ_s<CC_SILO>(lanes, block);
-        case CC_TICTOC: return occ_s<CC_TICTOC>(lanes, block);
-        case CC_GPUTX: return occ_s<CC_GPUTX>(lanes, block);
-        case CC_GACCO: return occ_s<CC_GACCO>(lanes, block);
+        case CC_TPL_NW: return occ_s<CC_TPL_NW>(lanes, block, smem);
+        case CC_TPL_WD: return occ_s<CC_TPL_WD>(lanes, block, smem);
+        case CC_TO: return occ_s<CC_TO>(lanes, block, smem);
+        case CC_MVCC: return occ_s<CC_MVCC>(lanes, block, smem);
+        case CC_SILO: return occ_s<CC_SILO>(lanes, block, smem);
+        case CC_TICTOC: return occ_s<CC_TICTOC>(lanes, block, smem);
+        case CC_GPUTX: return occ_s<CC_GPUTX>(lanes, block, smem);
+        case CC_GACCO: return occ_s<CC_GACCO>(lanes, block, smem);
     }
     return 0;
 }
@@ -689,4 +731,14 @@ cudaError_t launch_tpcc_gather(const ExecParams &p, const TpccParams &y, PrepBuf
     return cudaGetLastError();
 }
 
+
+void preload_tpcc_kernels() {   // (see preload_prep_kernels) every executor instantiation
+    for (int sc = 0; sc < CC_NUM_SCHEMES; sc++) {
+        tpcc_exec_max_blocks_per_sm(sc, 1, 256, 0);
+        tpcc_exec_max_blocks_per_sm(sc, 32, 256, 0);
+    }
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, tpcc_gen_kernel);
+    cudaFuncGetAttributes(&a, tpcc_gather_kernel);
+}
 }  // namespace gcctb

@@ -53,4 +53,14 @@ static_assert(sizeof(PartReq) == 48, "PartReq is 48 bytes");
 struct PartResp {
     unsigned long long v[6];
 };
+// CC_FLAG_PART_P2P: the peers' exchange windows (inbox, staging array, flags) as device
+// pointers of this process (IPC-mapped, or local), indexed by rank
+constexpr int P2P_MAXW = 64;
+constexpr int P2P_FLAG_STRIDE = 32;   // one flag per 256 B
+constexpr size_t P2P_FLAG_BYTES = (size_t)2 * P2P_MAXW * P2P_FLAG_STRIDE * 8;
+struct PeerTab {
+    PartReq *inbox[P2P_MAXW];
+    PartResp *stage[P2P_MAXW];
+    unsigned long long *flags[P2P_MAXW];
+};
 }  // namespace gcctb

@@ -6,6 +6,9 @@
 // Zipfian keys (theta), write fraction W.  Row = 16 x u64 (128 B, one L2 line pair
 // of sectors; reading Z11).  Op semantics (Z11): out = fp(row) = sum_j rotl(r[j], j);
 // a write also sets r[f] = r[f]*0x9E3779B97F4A7C15 + ((gid<<4)|i) + 1 and r[15] += 1.
+#include <cstdio>
+#include <cstdlib>
+
 #include "exec.cuh"
 
 namespace gcctb {
@@ -13,6 +16,7 @@ namespace gcctb {
 struct YcsbWL {
     static constexpr int MAXK = 16;
     static constexpr int ROW_WORDS = 16;
+    static constexpr bool STAGE_TILE_LANE = false;   // tile mode: the 40 B entry stays in registers
     using Params = YcsbParams;
     // One access of a transaction and its private workspace ("private
     // workspace"): the value read and the buffered new values of a write.
@@ -21,6 +25,7 @@ struct YcsbWL {
         bool act, w;
         uint8_t field;
         u64 out, nf, n15;
+        u64 cv;   // thread mode: control word seen (OCC snapshot / lock-time word, TO / MVCC saved word)
     };
 
     // Index lookup: lower bound of key in the sorted key array, returns
@@ -86,91 +91,97 @@ struct YcsbWL {
     }
 
     // Thread mode: resolve every access up front (read/write sets are predetermined,
-    // PAPER.md:446); the K binary searches run in lockstep for memory-level parallelism.
-    static GC_DEV u32 load_all(const ExecParams &p, const YcsbParams &y, u32 gid, Lane *L) {
+    // PAPER.md:446) into the staged lanes; the K searches of the tree / binary index run
+    // in lockstep for memory-level parallelism (u32 keys and positions: 2 x 16 registers).
+    template <class LA>
+    static GC_DEV u32 load_all(const ExecParams &p, const YcsbParams &y, u32 gid, LA L) {
         const u64 base = (u64)gid * p.K;
-        u64 key[MAXK];
-        const u64 *b[MAXK];
-#pragma unroll
-        for (int i = 0; i < MAXK; i++) {
-            L[i].act = i < (int)p.K;
-            if (L[i].act) {
-                const uint8_t op = y.ops[base + i];
-                L[i].field = op & 0x0F;
-                L[i].w = op >> 7;
-                key[i] = y.keys[base + i];
-                if (p.acc_rec) L[i].rec = p.acc_rec[base + i];   // resolved by a3
-            } else {
-                key[i] = 0;
-            }
-            b[i] = y.idx_keys;
+        const u32 K = p.K;
+        for (u32 i = 0; i < K; i++) {
+            Lane &Li = L[i];
+            const uint8_t op = y.ops[base + i];
+            Li.act = true;
+            Li.field = op & 0x0F;
+            Li.w = op >> 7;
+            if (p.acc_rec) Li.rec = p.acc_rec[base + i];   // resolved by a3
         }
-        if (p.acc_rec) return p.K;
+        if (p.acc_rec) return K;
+        bool ok = true;
         if (is_dense(y.mode) || y.mode == IDX_EYTZ) {
-            bool ok = true;
-            for (int i = 0; i < (int)p.K; i++) {
-                const u64 r = is_dense(y.mode) ? dense_lookup(y, key[i]) : eytz_lookup(y, key[i]);
+            for (u32 i = 0; i < K; i++) {
+                const u64 key = y.keys[base + i];
+                const u64 r = is_dense(y.mode) ? dense_lookup(y, key) : eytz_lookup(y, key);
                 ok &= r != ~0ull;
                 L[i].rec = (u32)r;
             }
-            if (ok)
-                for (int i = 0; i < (int)p.K; i++) prefetch_access(p, y, L[i]);
-            return ok ? p.K : 0xFFFFFFFFu;
-        }
-        if (y.mode == IDX_TREE) {   // tree: the K descents in lockstep, one level at a time
-            u64 node[MAXK];
+        } else if (y.mode == IDX_TREE) {
+            // descents in lockstep, TG keys at a time (TG x 8 independent 16 B loads per level
+            // in flight; all 16 at once spilled ~700 B per thread)
+            constexpr int TG = 2;
+            for (u32 i0 = 0; i0 < K; i0 += TG) {
+                u32 key[TG], node[TG];
 #pragma unroll
-            for (int i = 0; i < MAXK; i++) node[i] = 0;
-            bool ok = true;
-            for (int l = y.tree.n_levels - 1; l >= 0; l--) {
-                const u64 *lv = y.tree.lv[l];
+                for (int g = 0; g < TG; g++) {
+                    key[g] = i0 + g < K ? y.keys[base + i0 + g] : 0u;
+                    node[g] = 0;
+                }
+                for (int l = y.tree.n_levels - 1; l >= 0; l--) {
+                    const u64 *lv = y.tree.lv[l];
 #pragma unroll
-                for (int i = 0; i < MAXK; i++)
-                    if (i < (int)p.K) {
-                        const u64 *nd = lv + node[i] * 16;
+                    for (int g = 0; g < TG; g++) {
+                        const u64 *nd = lv + (u64)node[g] * 16;
                         u32 j = 0;
 #pragma unroll
                         for (int w = 0; w < 8; w++) {
                             u64 a, b;
                             asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(nd + 2 * w));
-                            j += (a < key[i]) + (b < key[i]);
+                            j += (a < key[g]) + (b < key[g]);
                         }
-                        ok &= j < 16;
-                        node[i] = node[i] * 16 + (j < 16 ? j : 0);
+                        if (i0 + g < K) ok &= j < 16;
+                        node[g] = node[g] * 16 + (j < 16 ? j : 0);
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < TG; g++)
+                    if (i0 + g < K) {
+                        if (node[g] >= y.idx_n || __ldg(y.idx_keys + node[g]) != key[g]) ok = false;
+                        else L[i0 + g].rec = (u32)__ldg(y.idx_rows + node[g]);
                     }
             }
+        } else {   // the paper's binary search, lower bound; BG searches in lockstep
+            constexpr int BG = 4;
+            for (u32 i0 = 0; i0 < K; i0 += BG) {
+                u32 key[BG], lo[BG];
 #pragma unroll
-            for (int i = 0; i < MAXK; i++)
-                if (i < (int)p.K) {
-                    if (node[i] >= y.idx_n || __ldg(y.idx_keys + node[i]) != key[i]) ok = false;
-                    else L[i].rec = (u32)__ldg(y.idx_rows + node[i]);
+                for (int g = 0; g < BG; g++) {
+                    key[g] = i0 + g < K ? y.keys[base + i0 + g] : 0u;
+                    lo[g] = 0;
                 }
-            if (ok)
-                for (int i = 0; i < (int)p.K; i++) prefetch_access(p, y, L[i]);
-            return ok ? p.K : 0xFFFFFFFFu;
-        }
-        u64 n = y.idx_n;
-        while (n > 1) {
-            const u64 half = n >> 1;
+                u64 n = y.idx_n;
+                while (n > 1) {
+                    const u64 half = n >> 1;
 #pragma unroll
-            for (int i = 0; i < MAXK; i++)
-                if (i < (int)p.K) b[i] = (__ldg(b[i] + half) < key[i]) ? b[i] + half : b[i];
-            n -= half;
-        }
-        bool ok = true;
-#pragma unroll
-        for (int i = 0; i < MAXK; i++)
-            if (i < (int)p.K) {
-                u64 pos = (u64)(b[i] - y.idx_keys);
-                u64 kv = __ldg(b[i]);
-                if (kv < key[i]) {
-                    pos++;
-                    kv = pos < y.idx_n ? __ldg(y.idx_keys + pos) : ~0ull;
+                    for (int g = 0; g < BG; g++)
+                        lo[g] = (__ldg(y.idx_keys + lo[g] + half) < key[g]) ? lo[g] + (u32)half : lo[g];
+                    n -= half;
                 }
-                if (pos >= y.idx_n || kv != key[i]) ok = false;
-                else L[i].rec = (u32)__ldg(y.idx_rows + pos);
+#pragma unroll
+                for (int g = 0; g < BG; g++)
+                    if (i0 + g < K) {
+                        u64 pos = lo[g];
+                        u64 kv = __ldg(y.idx_keys + pos);
+                        if (kv < key[g]) {
+                            pos++;
+                            kv = pos < y.idx_n ? __ldg(y.idx_keys + pos) : ~0ull;
+                        }
+                        if (pos >= y.idx_n || kv != key[g]) ok = false;
+                        else L[i0 + g].rec = (u32)__ldg(y.idx_rows + pos);
+                    }
             }
-        return ok ? p.K : 0xFFFFFFFFu;
+        }
+        if (!ok) return 0xFFFFFFFFu;
+        for (u32 i = 0; i < K; i++) prefetch_access(p, y, L[i]);
+        return K;
     }
 
     // Tile mode: lane i resolves access i.
@@ -190,6 +201,26 @@ struct YcsbWL {
         L.rec = (u32)r;
         if (r != ~0ull) prefetch_access(p, y, L);
         return r != ~0ull;
+    }
+
+    // tile-mode look-ahead (exec_tile_kernel): only when an access resolves without a memory
+    // probe -- direct addressing, or the record table a3 built -- so the prefetch of a
+    // later transaction's lines costs no dependent round trip
+    static GC_DEV bool lookahead(const ExecParams &p, const YcsbParams &y) {
+        return p.acc_rec != nullptr || is_dense(y.mode);
+    }
+    static GC_DEV u32 token(const ExecParams &p, const YcsbParams &y, u32 gid, u32 i) {
+        if (i >= p.K) return 0u;
+        const u64 a = (u64)gid * p.K + i;
+        return p.acc_rec ? p.acc_rec[a] : y.keys[a];
+    }
+    static GC_DEV void prefetch_token(const ExecParams &p, const YcsbParams &y, u32, u32 i, u32 tok) {
+        if (i >= p.K) return;
+        Lane L;
+        const u64 r = p.acc_rec ? (u64)tok : dense_lookup(y, tok);
+        if (r == ~0ull) return;   // unknown key: load_lane reports it when the transaction runs
+        L.rec = (u32)r;
+        prefetch_access(p, y, L);
     }
 
     // bring the row (both 64 B halves) and the CC word into L2 while the scheme's ordered
@@ -237,14 +268,17 @@ struct YcsbWL {
 
     static GC_DEV void copy_row(const Lane &, const u64 *src, u64 *dst) {
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            u64 a, b, c, d;
+        for (int j = 0; j < 4; j += 2) {   // two 32 B loads in flight (all four spilled)
+            u64 a, b, c, d, e, f, g, h;
             ld_cg_v4(src + 4 * j, a, b, c, d);
+            ld_cg_v4(src + 4 * j + 4, e, f, g, h);
             st_cg_v4(dst + 4 * j, a, b, c, d);
+            st_cg_v4(dst + 4 * j + 4, e, f, g, h);
         }
     }
 
-    static GC_DEV void emit_txn(const ExecParams &p, const YcsbParams &, u32 gid, const Lane *L, u32 n) {
+    template <class LA>
+    static GC_DEV void emit_txn(const ExecParams &p, const YcsbParams &, u32 gid, LA L, u32 n) {
         if (!p.read_out) return;
         for (u32 i = 0; i < n; i++) p.read_out[(u64)gid * p.K + i] = L[i].out;
     }
@@ -256,61 +290,76 @@ struct YcsbWL {
 
 // ---------------------------------------------------------------- executor launch
 template <int S>
-static cudaError_t launch_s(const ExecParams &p, const YcsbParams &y, int grid, int block,
+static cudaError_t launch_s(const ExecParams &p, const YcsbParams &y, int grid, int block, size_t smem,
                             cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kern) {
+        if (smem > 32 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (getenv("GCCTB_DEBUG_LAUNCH")) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kern);
+            fprintf(stderr, "launch lanes=%u grid=%d block=%d smem=%zu set=%d static=%zu maxdyn=%d regs=%d maxthr=%d\n",
+                    p.lanes, grid, block, smem, (int)e, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.numRegs,
+                    fa.maxThreadsPerBlock);
+        }
+        if (e == cudaSuccess) kern<<<grid, block, smem, s>>>(p, y);
+    };
     switch (p.lanes) {
-        case 4: exec_tile_kernel<S, YcsbWL, 4><<<grid, block, 0, s>>>(p, y); break;
-        case 8: exec_tile_kernel<S, YcsbWL, 8><<<grid, block, 0, s>>>(p, y); break;
-        case 16: exec_tile_kernel<S, YcsbWL, 16><<<grid, block, 0, s>>>(p, y); break;
-        case 32: exec_tile_kernel<S, YcsbWL, 32><<<grid, block, 0, s>>>(p, y); break;
-        default: exec_thread_kernel<S, YcsbWL><<<grid, block, 0, s>>>(p, y); break;
+        case 4: go(exec_tile_kernel<S, YcsbWL, 4>); break;
+        case 8: go(exec_tile_kernel<S, YcsbWL, 8>); break;
+        case 16: go(exec_tile_kernel<S, YcsbWL, 16>); break;
+        case 32: go(exec_tile_kernel<S, YcsbWL, 32>); break;
+        default: go(exec_thread_kernel<S, YcsbWL>); break;
     }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block,
+cudaError_t launch_ycsb_exec(const ExecParams &p, const YcsbParams &y, int grid, int block, size_t smem,
                              cudaStream_t s) {
     switch (p.scheme) {
-        case CC_TPL_NW: return launch_s<CC_TPL_NW>(p, y, grid, block, s);
-        case CC_TPL_WD: return launch_s<CC_TPL_WD>(p, y, grid, block, s);
-        case CC_TO: return launch_s<CC_TO>(p, y, grid, block, s);
-        case CC_MVCC: return launch_s<CC_MVCC>(p, y, grid, block, s);
-        case CC_SILO: return launch_s<CC_SILO>(p, y, grid, block, s);
-        case CC_TICTOC: return launch_s<CC_TICTOC>(p, y, grid, block, s);
-        case CC_GPUTX: return launch_s<CC_GPUTX>(p, y, grid, block, s);
-        case CC_GACCO: return launch_s<CC_GACCO>(p, y, grid, block, s);
+        case CC_TPL_NW: return launch_s<CC_TPL_NW>(p, y, grid, block, smem, s);
+        case CC_TPL_WD: return launch_s<CC_TPL_WD>(p, y, grid, block, smem, s);
+        case CC_TO: return launch_s<CC_TO>(p, y, grid, block, smem, s);
+        case CC_MVCC: return launch_s<CC_MVCC>(p, y, grid, block, smem, s);
+        case CC_SILO: return launch_s<CC_SILO>(p, y, grid, block, smem, s);
+        case CC_TICTOC: return launch_s<CC_TICTOC>(p, y, grid, block, smem, s);
+        case CC_GPUTX: return launch_s<CC_GPUTX>(p, y, grid, block, smem, s);
+        case CC_GACCO: return launch_s<CC_GACCO>(p, y, grid, block, smem, s);
     }
     return cudaErrorInvalidValue;
 }
 
 template <class F>
-static int occ_of(F f, int block) {
+static int occ_of(F f, int block, size_t smem = 0) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, block, 0);
+    if (smem > 32 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, block, smem);
     return nb;
 }
 
 template <int S>
-static int occ_s(int lanes, int block) {
+static int occ_s(int lanes, int block, size_t smem) {
     switch (lanes) {
-        case 4: return occ_of(exec_tile_kernel<S, YcsbWL, 4>, block);
-        case 8: return occ_of(exec_tile_kernel<S, YcsbWL, 8>, block);
-        case 16: return occ_of(exec_tile_kernel<S, YcsbWL, 16>, block);
-        case 32: return occ_of(exec_tile_kernel<S, YcsbWL, 32>, block);
-        default: return occ_of(exec_thread_kernel<S, YcsbWL>, block);
+        case 4: return occ_of(exec_tile_kernel<S, YcsbWL, 4>, block, smem);
+        case 8: return occ_of(exec_tile_kernel<S, YcsbWL, 8>, block, smem);
+        case 16: return occ_of(exec_tile_kernel<S, YcsbWL, 16>, block, smem);
+        case 32: return occ_of(exec_tile_kernel<S, YcsbWL, 32>, block, smem);
+        default: return occ_of(exec_thread_kernel<S, YcsbWL>, block, smem);
     }
 }
 
-int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block) {
+size_t ycsb_lane_bytes() { return sizeof(YcsbWL::Lane); }
+size_t exec_th_bytes() { return sizeof(Th); }
+int ycsb_exec_max_blocks_per_sm(int scheme, int lanes, int block, size_t smem) {
     switch (scheme) {
-        case CC_TPL_NW: return occ_s<CC_TPL_NW>(lanes, block);
-        case CC_TPL_WD: return occ_s<CC_TPL_WD>(lanes, block);
-        case CC_TO: return occ_s<CC_TO>(lanes, block);
-        case CC_MVCC: return occ_s<CC_MVCC>(lanes, block);
-        case CC_SILO: return occ_s<CC_SILO>(lanes, block);
-        case CC_TICTOC: return occ_s<CC_TICTOC>(lanes, block);
-        case CC_GPUTX: return occ_s<CC_GPUTX>(lanes, block);
-        case CC_GACCO: return occ_s<CC_GACCO>(lanes, block);
+        case CC_TPL_NW: return occ_s<CC_TPL_NW>(lanes, block, smem);
+        case CC_TPL_WD: return occ_s<CC_TPL_WD>(lanes, block, smem);
+        case CC_TO: return occ_s<CC_TO>(lanes, block, smem);
+        case CC_MVCC: return occ_s<CC_MVCC>(lanes, block, smem);
+        case CC_SILO: return occ_s<CC_SILO>(lanes, block, smem);
+        case CC_TICTOC: return occ_s<CC_TICTOC>(lanes, block, smem);
+        case CC_GPUTX: return occ_s<CC_GPUTX>(lanes, block, smem);
+        case CC_GACCO: return occ_s<CC_GACCO>(lanes, block, smem);
     }
     return 0;
 }
@@ -475,5 +524,16 @@ __global__ void fill_u64_kernel(u64 *p, u64 v, uint64_t n) {
 cudaError_t launch_fill_u64(u64 *p, u64 v, uint64_t n, cudaStream_t s) {
     if (n) fill_u64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, v, n);
     return cudaGetLastError();
+}
+
+void preload_ycsb_kernels() {   // (see preload_prep_kernels) every executor instantiation
+    const int lanes[5] = {1, 4, 8, 16, 32};
+    for (int sc = 0; sc < CC_NUM_SCHEMES; sc++)
+        for (int l : lanes) ycsb_exec_max_blocks_per_sm(sc, l, 256, 0);
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, ycsb_gen_kernel);
+    cudaFuncGetAttributes(&a, ycsb_gather_kernel);
+    cudaFuncGetAttributes(&a, fill_u64_kernel);
+    cudaFuncGetAttributes(&a, index_lookup_kernel);
 }
 }  // namespace gcctb

@@ -34,6 +34,9 @@ CC_FLAG_MVCC_SPLIT = 0x400
 CC_FLAG_PART_2PC = 0x800
 CC_FLAG_INDEX_EYTZ = 0x1000
 CC_FLAG_WARM = 0x2000
+CC_FLAG_PART_P2P = 0x4000
+CC_FLAG_NO_LOOKAHEAD = 0x8000
+CC_FLAG_META_PAD = 0x10000
 CC_SRC_HOST_ASYNC = 2
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
 PART_REC_BYTES = 48
@@ -94,6 +97,11 @@ class cc_roofline(ctypes.Structure):
                 ("handoff_ns", ctypes.c_double), ("handoff_acq_row_ns", ctypes.c_double)]
 
 
+class cc_ipc_handle(ctypes.Structure):
+    _fields_ = [("ipc", ctypes.c_ubyte * 64), ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32),
+                ("cap", ctypes.c_uint32), ("max_txn", ctypes.c_uint32)]
+
+
 _lib = None
 
 # name -> (restype, argtypes)
@@ -145,6 +153,9 @@ _SIGS = {
     "cc_part_commit": (ctypes.c_int, [_P, _P, _P, ctypes.c_uint64]),
     "cc_part_next": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "cc_roofline_probe": (ctypes.c_int, [_P, ctypes.POINTER(cc_roofline)]),
+    "cc_part_window": (ctypes.c_int, [_P, ctypes.POINTER(cc_ipc_handle)]),
+    "cc_part_connect": (ctypes.c_int, [_P, ctypes.POINTER(cc_ipc_handle)]),
+    "cc_part_connect_local": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int]),
 }
 
 TPCC_TX_WORDS = 40

@@ -11,6 +11,10 @@ device-side permutation (concatenation of the per-destination slices).
 non-deterministic schemes, phase B in two-phase-commit rounds with a third all-to-all
 (decisions); owners grant under 2PL locks or, for TO / MVCC / Silo / TicToc, in the
 round's timestamp order.
+`p2p_setup` / `p2p_round` / `loopback_p2p`: the deterministic phase B with the exchange
+inside the library (CC_FLAG_PART_P2P): requests and responses are stored straight into
+the peers' exchange windows over peer memory, so a round involves neither the host nor a
+collective call -- the only torch.distributed use is gathering the window handles once.
 """
 from __future__ import annotations
 
@@ -85,6 +89,32 @@ def dist_round_2pc(db, batch, scheme, result=None, group=None, via_cpu=False, **
             break
     db.part_finish(torch.empty(0, dtype=torch.uint8, device=send.device))
     return res, rounds
+
+
+def p2p_setup(db, group=None):
+    """Collective: create this rank's exchange window, all_gather the handles, map the peers'
+    windows (CC_FLAG_PART_P2P).  Afterwards `p2p_round` needs no host participation."""
+    import torch.distributed as dist
+    mine = db.part_window()
+    handles = [None] * db.world
+    dist.all_gather_object(handles, mine, group=group)
+    db.part_connect(handles)
+
+
+def p2p_round(db, batch, scheme, result=None, **kw):
+    """One partitioned submit with the exchange inside the library: phase A, the request /
+    response transfers over peer memory, phase B and a7 are all enqueued on the db stream
+    (every rank issues the same sequence of these submits)."""
+    flags = kw.pop("flags", 0) | G.CC_FLAG_PARTITIONED | G.CC_FLAG_PART_P2P
+    return db.submit(batch, scheme, flags=flags, result=result, **kw)
+
+
+def loopback_p2p(dbs, batches, scheme, results=None, **kw):
+    """G partitions held by G dbs of this process (connected with DB.part_connect_local):
+    the partitioned submits are enqueued back to back and the exchange runs between their
+    streams over device memory -- no host synchronisation anywhere in the round."""
+    return [p2p_round(db, b, scheme, result=None if results is None else results[i], **kw)
+            for i, (db, b) in enumerate(zip(dbs, batches))]
 
 
 def _slices(buf, counts, rec):

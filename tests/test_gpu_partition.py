@@ -87,6 +87,95 @@ def test_loopback_partitions(torch_cuda, orc, scheme, G_):
         db.close()
 
 
+# ------------------------------------------------- in-library exchange over peer memory
+def _partitions(G_, seed, n=2048, W=8):
+    from paper_2406_10158_b200.api import DB
+    wpr = W // G_
+    dbs, batches = [], []
+    for r in range(G_):
+        db = DB(0, rank=r, world=G_)
+        db.load_tpcc(W, 17, n, w_first=r * wpr, w_count=wpr)
+        dbs.append(db)
+        batches.append(db.gen_tpcc(n, seed + r, 5114, w_lo=r * wpr, w_hi=(r + 1) * wpr))
+    return dbs, batches
+
+
+@pytest.mark.parametrize("G_", [2, 4])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_loopback_p2p(torch_cuda, orc, scheme, G_):
+    """CC_FLAG_PART_P2P: phase A, the exchange over the dbs' windows, phase B and a7 all
+    enqueued by one cc_submit per partition (no host step in between); twice in a row, so
+    the windows and epochs are reused."""
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200.partition import loopback_p2p
+    W, n = 8, 2048
+    dbs, batches = _partitions(G_, 100)
+    DB.part_connect_local(dbs)
+    for db in dbs:
+        db.snapshot(True)
+    S0 = IT.population(17, W)
+    for rep in range(2):
+        for db in dbs:
+            db.snapshot(False)
+        res = loopback_p2p(dbs, batches, scheme, bs=8, lanes=32, watchdog_s=60)
+        for db in dbs:
+            assert db.sync().commits == n
+        _merged_check(scheme, W, dbs, batches, res, S0, n)
+    for db in dbs:
+        db.close()
+
+
+@pytest.mark.parametrize("scheme", ["gputx", "gacco"])
+def test_p2p_equals_host_exchange(torch_cuda, orc, scheme):
+    """The deterministic schemes' partitioned results are a function of the input alone:
+    the in-library exchange and the host-driven one give identical outputs and tables."""
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200.partition import loopback_p2p, loopback_round
+    G_ = 4
+    dbs, batches = _partitions(G_, 700)
+    DB.part_connect_local(dbs)
+    for db in dbs:
+        db.snapshot(True)
+    out = []
+    for run in (loopback_round, loopback_p2p):
+        for db in dbs:
+            db.snapshot(False)
+        res = run(dbs, batches, scheme, bs=8, lanes=32, watchdog_s=60)
+        hs = [r.host(db.stream) for r, db in zip(res, dbs)]
+        tabs = [db.read_tpcc(["warehouse", "district", "customer", "stock", "order", "new_order", "order_line",
+                              "history"]) for db in dbs]
+        out.append((hs, tabs))
+    (h1, t1), (h2, t2) = out
+    for a, b in zip(h1, h2):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+    for a, b in zip(t1, t2):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+    for db in dbs:
+        db.close()
+
+
+def test_p2p_phase_b_only(torch_cuda, orc):
+    """CC_FLAG_PART_ALL with the in-library exchange on one partition: every transaction
+    through phase B over the window, equal to serial replay in gid order."""
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200 import gcctb as G
+    from paper_2406_10158_b200.partition import loopback_p2p
+    W, n = 2, 2048
+    db = DB(0, rank=0, world=1)
+    db.load_tpcc(W, 13, n)
+    DB.part_connect_local([db])
+    S0 = IT.population(13, W)
+    b = db.gen_tpcc(n, 5, 5114)
+    res = loopback_p2p([db], [b], "tpl_nw", flags=G.CC_FLAG_PART_ALL, bs=8, lanes=32)
+    st = db.sync()
+    assert st.commits == n and st.aborts == 0
+    assert (res[0].host(db.stream)["order_hi"] == np.uint64(1 << 63)).all()
+    _merged_check("tpl_nw", W, [db], [b], res, S0, n)
+    db.close()
+
+
 # ---------------------------------------------------------------- f-2: 2PC phase B
 TWO_PC = ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc"]
 

@@ -219,6 +219,28 @@ def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta, warm):
     b.free()
 
 
+@pytest.mark.parametrize("mode", ["meta_pad", "no_lookahead", "meta_pad_latched"])
+@pytest.mark.parametrize("lanes", [1, 16])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c1_parity_layout_flags(c1, orc, scheme, lanes, mode):
+    """CC_FLAG_META_PAD (one control word per 32 B sector, f-3) -- also under latched
+    words, whose latch index follows the word -- and CC_FLAG_NO_LOOKAHEAD change the
+    memory layout / timing only: the same serial-replay parity at configs[0]."""
+    from paper_2406_10158_b200 import gcctb as G
+    flags = {"meta_pad": G.CC_FLAG_META_PAD, "no_lookahead": G.CC_FLAG_NO_LOOKAHEAD,
+             "meta_pad_latched": G.CC_FLAG_META_PAD | G.CC_FLAG_LATCHED}[mode]
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 23, T, A)
+    keys, ops = orc.ycsb_gen(23, 1024, 1024, 4, 0.5, T, A)
+    db.snapshot(False)
+    res = db.submit(b, scheme, wd=5 if lanes == 1 else 0, bs=8, lanes=lanes, flags=flags)
+    assert db.sync().commits == 1024
+    orc.check_ycsb(scheme, S0, keys, ops, 4, res.host(db.stream), db.read_table(0))
+    b.free()
+
+
 @pytest.mark.parametrize("lanes", [4, 8, 16])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_c1_parity_warm(c1, orc, scheme, lanes):

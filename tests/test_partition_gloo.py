@@ -149,3 +149,45 @@ def test_2pc_rounds_until_every_rank_is_done(world):
         assert rounds == world and finished
         # round k: every rank still pending (rank >= k) sends one request here
         assert commits == [sum(1 for s in range(world) if s >= k) for k in range(world)]
+
+
+class _WinDB:
+    """Stands in for a rank's DB in p2p_setup: its window handle names its rank."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world, self.got = rank, world, None
+
+    def part_window(self):
+        return bytes([self.rank]) * 80   # sizeof(cc_ipc_handle)
+
+    def part_connect(self, handles):
+        self.got = handles
+
+
+def _worker_p2p_setup(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_10158_b200 import partition as P
+    db = _WinDB(rank, world)
+    P.p2p_setup(db)
+    q.put((rank, [h[0] for h in db.got], [len(h) for h in db.got]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_setup_gathers_handles_in_rank_order(world):
+    """CC_FLAG_PART_P2P set-up: every rank receives all window handles, indexed by rank
+    (cc_part_connect checks handle r is rank r's)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_p2p_setup, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, firsts, lens in out:
+        assert firsts == list(range(world)) and lens == [80] * world
