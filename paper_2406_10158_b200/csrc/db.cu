@@ -238,6 +238,7 @@ struct cc_db_s {
     u64 *ohi = nullptr, *olo = nullptr;
     u64 *ring = nullptr;
     uint32_t ring_cap = 0;
+    RankBitmap rank_bm{};               // a7 commit positions of TO / MVCC / Silo
     void *ws = nullptr;                 // thread-mode staging workspace (global fallback)
     uint64_t ws_bytes = 0;
     u64 *arena = nullptr;
@@ -396,6 +397,9 @@ cc_status cc_db_destroy(cc_db db) {
     dfree(db->part.recv);
     dfree(db->arena);
     dfree(db->ws);
+    dfree(db->rank_bm.bits);
+    dfree(db->rank_bm.pre);
+    dfree(db->rank_bm.csum);
     dfree(db->latch);
     dfree(db->stages);
     dfree(db->events);
@@ -1163,8 +1167,11 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         smem = (size_t)(working * exec_th_bytes());
         if (smem + bytes <= GC_STAGE_SMEM_MAX) smem += (size_t)bytes;
         else ws_per_block = bytes;
-    } else {   // TPC-C tile lanes keep their access entry in shared memory too
-        smem = (size_t)block * (exec_th_bytes() + (is_tpcc ? tpcc_lane_bytes() : 0));
+    } else {   // TPC-C tile lanes keep their access entry in shared memory too (else global)
+        smem = (size_t)block * exec_th_bytes();
+        const uint64_t bytes = is_tpcc ? (uint64_t)block * tpcc_lane_bytes() : 0;
+        if (smem + bytes <= GC_STAGE_SMEM_MAX) smem += (size_t)bytes;
+        else ws_per_block = bytes;
     }
     int grid = (int)desc->grid;
     if (grid <= 0) {
@@ -1224,8 +1231,16 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     // a7: commit positions + result copy-out
     cc_result r = *res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
+    const bool bitmap_rank = scheme == CC_TO || scheme == CC_MVCC || scheme == CC_SILO;
+    if (bitmap_rank && !db->rank_bm.bits) {   // once per db: 512 MB for the 31-bit key range
+        CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+        CUDA_TRY(db, dalloc(&db->rank_bm.bits, RANK_BITMAP_BITS / 8));
+        CUDA_TRY(db, dalloc(&db->rank_bm.pre, RANK_BITMAP_BITS / 8));
+        CUDA_TRY(db, dalloc(&db->rank_bm.csum, RANK_BITMAP_BITS / 32 / 1024 * 4 + 64));
+    }
     CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream,
-                                 scheme == CC_TPL_NW || scheme == CC_TPL_WD, scheme == CC_TICTOC));
+                                 scheme == CC_TPL_NW || scheme == CC_TPL_WD, scheme == CC_TICTOC,
+                                 bitmap_rank ? &db->rank_bm : nullptr));
     if (used) {   // a later cc_prepare of this batch may overwrite the buffers after this point
         CUDA_TRY(db, cudaEventRecord(used->consumed, db->stream));
         used->has_consumer = true;

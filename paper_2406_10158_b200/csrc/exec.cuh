@@ -559,13 +559,19 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 // Tile-mode TO: restarts after which a transaction's accesses are stepped one lane at a
 // time (measured, profiles/r01_probe_v16_*: 8 halves TO at theta=0.6, 32 keeps it; the
 // same for wait-die cost 4.7x at theta=0.8 and was dropped)
-constexpr u32 TO_SEQ_AFTER = 32;
+#ifndef GC_TO_SEQ_AFTER
+#define GC_TO_SEQ_AFTER 32
+#endif
+constexpr u32 TO_SEQ_AFTER = GC_TO_SEQ_AFTER;
 
 // A waiting writer always announces intent (TPL_WW); a dying one only once it has restarted
 // this often -- the stale-age starvation needs it, and announcing earlier makes readers die
 // needlessly (measured, YCSB tile 16: every writer at once: theta 0.6 96M -> 53M txn/s;
 // dying writers after 8 restarts: theta 0.8 6.1M -> 1.9M).
 constexpr u32 TPL_INTENT_AFTER = 32;
+#ifndef GC_WD_SEQ_AFTER
+#define GC_WD_SEQ_AFTER 0
+#endif
 
 template <bool WD>
 GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, bool intent) {
@@ -1141,12 +1147,20 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         // lock that killed its previous attempt first, alone, and the rest in parallel once
         // it holds it: a retry that meets the hot lock busy dies holding nothing.
         const u32 first = (WD || th.attempt < 2) ? 0u : th.hot;   // 1 + that lock's lane, 0: none
+        // wait-die under extreme contention (experiment knob): from GC_WD_SEQ_AFTER restarts
+        // on, take the locks one lane at a time in access (key) order, as the paper's
+        // one-thread launch does
+        const bool seq = WD && GC_WD_SEQ_AFTER > 0 && th.attempt >= GC_WD_SEQ_AFTER;
         Spin sp;
         for (;;) {
             int st = ST_DONE;
             u64 seen = 0;
             bool mine = act && !held;
             if (first && !tile.shfl(held || !act, first - 1)) mine = mine && li == first - 1;
+            if (seq) {
+                const unsigned want = tile.ballot(mine);
+                mine = mine && li == (u32)(__ffs(want) - 1);
+            }
             if (mine) {
                 if (warp_lock_loser(L.rec, L.w, age)) st = ST_ABORT;   // an older tile of this warp takes it
                 else st = tpl_try<WD>(p, cw(p, L.rec), L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
@@ -1369,20 +1383,21 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
     // entry is large (TPC-C: values read, buffered writes, strings) -- shared memory after
     // the contexts, so the tile loop keeps its registers for the row reads
     typename WL::Lane Lr;
-    typename WL::Lane &L = WL::STAGE_TILE_LANE
-                               ? reinterpret_cast<typename WL::Lane *>(gc_dyn_smem + (size_t)blockDim.x * sizeof(Th))[threadIdx.x]
-                               : Lr;
+    typename WL::Lane *Ls = p.ws ? reinterpret_cast<typename WL::Lane *>(p.ws) + (u64)blockIdx.x * blockDim.x
+                                 : reinterpret_cast<typename WL::Lane *>(gc_dyn_smem + (size_t)blockDim.x * sizeof(Th));
+    typename WL::Lane &L = WL::STAGE_TILE_LANE ? Ls[threadIdx.x] : Lr;   // (global when it does not fit)
     th.cl = Claim{};
     Claim &cl = th.cl;
-    // Look-ahead (fresh ids; workloads whose accesses resolve without a memory probe --
-    // YCSB direct addressing, or a3's record table): a worker keeps two more fresh ids in a
+    // Look-ahead (fresh ids of the six non-deterministic schemes -- GaccO / GPUTx are bound
+    // by their hand-off chains, where it measured slower -- on workloads whose accesses
+    // resolve without a memory probe, i.e. YCSB direct addressing): a worker keeps two more fresh ids in a
     // three-stage pipeline -- the claim's atomic is issued one transaction ahead, the next
     // id's keys are loaded one transaction ahead and its rows and control words prefetched
     // into L2 the transaction after that -- so a transaction starts with its claim, keys
     // and lines already on chip instead of paying three dependent round trips first.  Ids
     // are still executed in claim order per worker, so every transaction waited on is
     // claimed by a running worker (the liveness argument of the queue is unchanged).
-    const bool LA = S != CC_GPUTX && p.claim_chunk <= 1 && WL::lookahead(p, y) && !(p.flags & CC_FLAG_NO_LOOKAHEAD);
+    const bool LA = !DET && p.claim_chunk <= 1 && WL::lookahead(p, y) && !(p.flags & CC_FLAG_NO_LOOKAHEAD);
     u32 qX = NO_TXN, qP = NO_TXN;   // next to execute (lines prefetched) / keys loaded, lines prefetched now
     u32 tokP = 0;                    // this lane's access token (key or record) of qP
     u64 pend = ~0ull;                // leader: in-flight fresh claim (atomicAdd result)

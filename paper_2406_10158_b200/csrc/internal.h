@@ -167,9 +167,15 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
 // a1: fold the batch's generator error word into the submit's control block (after a2)
 cudaError_t launch_merge_word(const unsigned long long *err, Ctl *dst, cudaStream_t s);
+// a7 commit positions of TO / MVCC / Silo by bitmap (bits: 2^31 / 32 words, pre: one u32
+// per word, csum: one per 1,024 words); null: radix sort
+struct RankBitmap {
+    uint32_t *bits, *pre, *csum;
+};
+constexpr unsigned long long RANK_BITMAP_BITS = 1ull << 31;   // 31-bit timestamps
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket = false,
-                            bool lo_dense = false);
+                            bool lo_dense = false, const RankBitmap *rb = nullptr);
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
 // sort.cu: stable LSD radix sort of u64 keys (+ optional u32 values) on bits [lo, hi),
 // keys_alt / vals_alt the ping-pong buffers, n = *n_dev if given (device-resident count,

@@ -351,6 +351,104 @@ __global__ void dense_ticket_pos_kernel(const u64 *lo, const uint8_t *committed,
     if (g < n) pos_out[g] = committed[g] ? (uint32_t)lo[g] : 0xFFFFFFFFu;
 }
 
+// TO / MVCC / Silo: the committed order keys are distinct integers below R (the last
+// timestamp + 1, or the number of tickets drawn), so a transaction's commit position is
+// the number of committed keys below its own -- a bitmap over [0, R) and a prefix count
+// of its set bits (five small kernels instead of four radix passes of four kernels each).
+// The kernels loop over [0, R) with R read on the device, so the grids do not depend on it.
+constexpr int BM_CHUNK = 1024;   // words per chunk: one block scans one chunk
+__device__ __forceinline__ u64 bm_range(const u64 *rptr, u64 radd) {
+    const u64 r = *rptr + radd;
+    return r < RANK_BITMAP_BITS ? r : RANK_BITMAP_BITS;   // beyond: reported by bm_set_kernel
+}
+
+__global__ void bm_zero_kernel(uint32_t *bm, const u64 *rptr, u64 radd) {
+    const u64 words = (bm_range(rptr, radd) + 31) / 32;
+    for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (u64)gridDim.x * blockDim.x) bm[w] = 0u;
+}
+__global__ void bm_set_kernel(const u64 *lo, const uint8_t *committed, uint32_t *bm, uint32_t n, Ctl *ctl) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n || !committed[g]) return;
+    if (lo[g] >= RANK_BITMAP_BITS) {   // a 32-bit ticket range is beyond the bitmap (never seen)
+        atomicCAS(&ctl->err.v, 0ull, (u64)CC_ERR_TS_OVERFLOW);
+        return;
+    }
+    atomicOr(&bm[lo[g] >> 5], 1u << (lo[g] & 31));
+}
+// per chunk of 1,024 words: exclusive prefix of the words' popcounts, and the chunk total
+__global__ void __launch_bounds__(BM_CHUNK) bm_chunk_kernel(const uint32_t *bm, uint32_t *pre, uint32_t *csum,
+                                                           const u64 *rptr, u64 radd) {
+    __shared__ uint32_t ws[BM_CHUNK / 32];
+    const u64 words = (bm_range(rptr, radd) + 31) / 32, chunks = (words + BM_CHUNK - 1) / BM_CHUNK;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (u64 c = blockIdx.x; c < chunks; c += gridDim.x) {
+        const u64 w = c * BM_CHUNK + threadIdx.x;
+        const uint32_t v = w < words ? __popc(bm[w]) : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) ws[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t t = ws[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+                if (lane >= (uint32_t)o) t += y;
+            }
+            ws[lane] = t;
+        }
+        __syncthreads();
+        if (w < words) pre[w] = (warp ? ws[warp - 1] : 0u) + x - v;
+        if (threadIdx.x == 0) csum[c] = ws[31];
+        __syncthreads();
+    }
+}
+// exclusive scan of the chunk totals, one block (loops with a carry)
+__global__ void __launch_bounds__(1024) bm_csum_kernel(uint32_t *csum, const u64 *rptr, u64 radd) {
+    __shared__ uint32_t ws[32];
+    const u64 words = (bm_range(rptr, radd) + 31) / 32, chunks = (words + BM_CHUNK - 1) / BM_CHUNK;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t carry = 0;
+    for (u64 c0 = 0; c0 < chunks; c0 += 1024) {
+        const u64 c = c0 + threadIdx.x;
+        const uint32_t v = c < chunks ? csum[c] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) ws[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t t = ws[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+                if (lane >= (uint32_t)o) t += y;
+            }
+            ws[lane] = t;
+        }
+        __syncthreads();
+        if (c < chunks) csum[c] = carry + (warp ? ws[warp - 1] : 0u) + x - v;
+        carry += ws[31];
+        __syncthreads();
+    }
+}
+__global__ void bm_pos_kernel(const u64 *lo, const uint8_t *committed, const uint32_t *bm, const uint32_t *pre,
+                              const uint32_t *csum, uint32_t *pos, uint32_t n) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    if (!committed[g]) { pos[g] = 0xFFFFFFFFu; return; }
+    const u64 k = lo[g], w = k >> 5;
+    if (k >= RANK_BITMAP_BITS) { pos[g] = 0xFFFFFFFFu; return; }
+    pos[g] = csum[w / BM_CHUNK] + pre[w] + __popc(bm[w] & ((1u << (k & 31)) - 1u));
+}
+
 // TicToc: every committed transaction drew one ticket 0..n-1 -- the order by key_lo is
 // the inverse permutation, no sort
 __global__ void ticket_perm_kernel(const u64 *lo, const uint8_t *committed, uint32_t *perm, uint32_t n) {
@@ -359,7 +457,8 @@ __global__ void ticket_perm_kernel(const u64 *lo, const uint8_t *committed, uint
 }
 
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
-                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket, bool lo_dense) {
+                            bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket, bool lo_dense,
+                            const RankBitmap *rb) {
     const uint32_t n = p.n_txn;
     const int blk = 256;
     const unsigned g = (n + blk - 1) / blk;
@@ -370,6 +469,16 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
     } else if (deterministic) {
         iota_kernel<<<g, blk, 0, s>>>(b.rank_order, n);
         commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
+    } else if (rb && !two_pass) {   // TO / MVCC / Silo: bitmap + prefix count
+        const bool ts = p.scheme == CC_TO || p.scheme == CC_MVCC;
+        const u64 *rptr = ts ? &p.ctl->ts.v : &p.ctl->ticket.v;
+        const u64 radd = ts ? 1 : 0;
+        const int gs = 148 * 4;
+        bm_zero_kernel<<<gs, 256, 0, s>>>(rb->bits, rptr, radd);
+        bm_set_kernel<<<g, blk, 0, s>>>(p.order_lo, p.committed, rb->bits, n, p.ctl);
+        bm_chunk_kernel<<<gs, BM_CHUNK, 0, s>>>(rb->bits, rb->pre, rb->csum, rptr, radd);
+        bm_csum_kernel<<<1, 1024, 0, s>>>(rb->csum, rptr, radd);
+        bm_pos_kernel<<<g, blk, 0, s>>>(p.order_lo, p.committed, rb->bits, rb->pre, rb->csum, pos, n);
     } else {
         u64 *k1 = b.keys_in, *k2 = b.keys_out;   // n_acc >= n scratch
         u64 *sk = k2;
@@ -435,6 +544,7 @@ void preload_prep_kernels() {
     preload1(rank_bounds_kernel); preload1(rank_count_kernel); preload1(keys_iota_kernel); preload1(copy_u32_kernel);
     preload1(commit_pos_kernel); preload1(gather_hi_kernel); preload1(copy_out_kernel); preload1(stages_reduce_kernel);
     preload1(stats_kernel); preload1(dense_ticket_pos_kernel); preload1(ticket_perm_kernel); preload1(merge_err_kernel);
-    preload1(merge_word_kernel);
+    preload1(merge_word_kernel); preload1(bm_zero_kernel); preload1(bm_set_kernel); preload1(bm_chunk_kernel);
+    preload1(bm_csum_kernel); preload1(bm_pos_kernel);
 }
 }  // namespace gcctb

@@ -10,10 +10,13 @@
 //   count   -- one block per 4,096-key tile: per-digit counts of its tile (smem atomics),
 //              written digit-major so that one exclusive scan gives every (digit, tile) its
 //              output base;
-//   scan    -- one 1,024-thread block scans the 256 x tiles counts;
+//   scan    -- one block per digit row scans it across the tiles, one warp the 256 row
+//              totals (two kernels);
 //   scatter -- one block per tile, each warp a contiguous 512-key run in 32-key chunks:
 //              a key's rank among equal digits is __match_any_sync + popc in its chunk plus
-//              its warp's running count (smem), so the scatter is stable (warp multisplit).
+//              its warp's running count (smem), so the scatter is stable (warp multisplit);
+//              the tile is reordered in shared memory first, so each digit's run goes out
+//              as consecutive addresses.
 // The number of keys may live in device memory (n_dev): grids are sized for the host
 // capacity and tiles past n exit, so a caller whose n is known only on the device (the
 // phase-B exchange) sorts without a host synchronisation.
@@ -56,70 +59,96 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_count_kernel(const u64 *key
     counts[(u64)threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan (digit-major) of the counts of the tiles that hold keys, in place: one
-// block, 4 threads per digit row -- row totals, a scan of the 256 totals, then each row's
-// scan from its carry.  Loads are independent (unrolled) so a row costs a few round trips.
-__global__ void __launch_bounds__(1024) sort_scan_kernel(u32 *counts, u32 tiles, const u64 *n_dev, u64 n_host) {
-    __shared__ u32 part[1024];
-    __shared__ u32 rowbase[257];
+// exclusive scan (digit-major) of the counts of the tiles that hold keys, in two kernels:
+// one block per digit row scans that row across the tiles (coalesced, in place) and
+// records the row total; then one warp turns the 256 totals into each row's base
+// (rowbase[d]).  A key's output position is rowbase[digit] + row offset of its tile + its
+// place inside the tile.
+__global__ void __launch_bounds__(1024) sort_rowscan_kernel(u32 *counts, u32 tiles, const u64 *n_dev, u64 n_host,
+                                                             u32 *rowsum) {
+    __shared__ u32 wsum[32];
     const u64 n = n_of(n_dev, n_host);
     const u32 active = (u32)((n + SORT_TILE - 1) / SORT_TILE);
-    const u32 d = threadIdx.x >> 2, q = threadIdx.x & 3;
-    const u32 per = (active + 3) / 4, lo = q * per, hi = min(active, lo + per);
-    u32 *row = counts + (u64)d * tiles;
-    u32 s = 0;
-#pragma unroll 8
-    for (u32 t = lo; t < hi; t++) s += row[t];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {   // one warp scans the 256 row totals (8 rows per lane)
-        u32 tot[8], acc = 0;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const u32 r = threadIdx.x * 8 + k;
-            tot[k] = part[4 * r] + part[4 * r + 1] + part[4 * r + 2] + part[4 * r + 3];
-            acc += tot[k];
-        }
-        u32 x = acc;
+    u32 *row = counts + (u64)blockIdx.x * tiles;
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u32 carry = 0;
+    for (u32 t0 = 0; t0 < active; t0 += 1024) {
+        const u32 t = t0 + threadIdx.x;
+        const u32 c = t < active ? row[t] : 0u;
+        u32 x = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-            if (threadIdx.x >= (u32)o) x += y;
+            if (lane >= (u32)o) x += y;
         }
-        u32 run = x - acc;
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            u32 v = wsum[lane];
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            rowbase[threadIdx.x * 8 + k] = run;
-            run += tot[k];
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                if (lane >= (u32)o) v += y;
+            }
+            wsum[lane] = v;   // inclusive over warps
         }
+        __syncthreads();
+        const u32 before = (warp ? wsum[warp - 1] : 0u) + carry;
+        if (t < active) row[t] = before + x - c;   // exclusive within the row
+        carry += wsum[31];
+        __syncthreads();
     }
-    __syncthreads();
-    u32 run = rowbase[d];
-    for (u32 k = 0; k < q; k++) run += part[4 * d + k];
-    for (u32 t = lo; t < hi; t++) {
-        const u32 c = row[t];
-        row[t] = run;
-        run += c;
+    if (threadIdx.x == 0) rowsum[blockIdx.x] = carry;
+}
+
+__global__ void sort_rowbase_kernel(u32 *rowsum) {   // one warp: exclusive scan of 256 totals, in place
+    const u32 lane = threadIdx.x;
+    u32 v[8], acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        v[k] = rowsum[lane * 8 + k];
+        acc += v[k];
+    }
+    u32 x = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= (u32)o) x += y;
+    }
+    u32 run = x - acc;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        rowsum[lane * 8 + k] = run;
+        run += v[k];
     }
 }
 
-// stable scatter of one tile: warp w owns keys [w * 512, (w + 1) * 512) of the tile, in
-// chunks of 32 processed in order.  Phase 1 counts each warp's digits (a chunk's equal
-// digits are one __match_any_sync group, its lowest lane adds the group size -- no
-// atomics); phase 2 turns them into each warp's first output position per digit (global
-// base of the tile + the warps before it); phase 3 writes every key at its warp's running
-// position + its rank in the chunk's group.  Two block barriers per tile.
+// stable scatter of one tile, staged through shared memory so the global writes are
+// coalesced runs per digit: warp w owns keys [w * 512, (w + 1) * 512) of the tile in
+// 32-key chunks processed in order.  Phase 1 counts each warp's digits (a chunk's equal
+// digits form one __match_any_sync group whose lowest lane adds the group size); phase 2
+// scans them into each warp's first slot of each digit inside the tile's digit-sorted
+// order; phase 3 places every key there (+ its rank in its group) in shared memory;
+// phase 4 writes the tile's keys out in that order, each digit's run at its global base.
 template <bool PAIRS>
 __global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *keys, const u32 *vals, u64 *keys_out,
                                                                      u32 *vals_out, const u64 *n_dev, u64 n_host,
-                                                                     int shift, const u32 *offs, u32 tiles) {
+                                                                     int shift, const u32 *offs, const u32 *rowbase,
+                                                                     u32 tiles) {
     __shared__ u32 wc[SORT_WARPS][256];
+    __shared__ u32 tstart[256], gbase[256];
+    extern __shared__ __align__(16) unsigned char sort_smem[];
+    u64 *sk = reinterpret_cast<u64 *>(sort_smem);
+    u32 *sv = reinterpret_cast<u32 *>(sort_smem + SORT_TILE * sizeof(u64));
     const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const u64 n = n_of(n_dev, n_host);
-    const u64 w0 = (u64)blockIdx.x * SORT_TILE + (u64)warp * SORT_WTILE;
-    if ((u64)blockIdx.x * SORT_TILE >= n) return;   // uniform
+    const u64 tb = (u64)blockIdx.x * SORT_TILE;
+    if (tb >= n) return;   // uniform
+    const u32 cnt = (u32)(n - tb < SORT_TILE ? n - tb : SORT_TILE);
+    const u64 w0 = tb + (u64)warp * SORT_WTILE;
 #pragma unroll
     for (int w = 0; w < SORT_WARPS; w++) wc[w][tid] = 0;
+    gbase[tid] = rowbase[tid] + offs[(u64)tid * tiles + blockIdx.x];
     __syncthreads();
     u64 k[SORT_PER];
     u32 dg[SORT_PER];
@@ -138,34 +167,58 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *k
         __syncwarp();
     }
     __syncthreads();
-    {   // thread `tid` owns digit `tid`: first position of each warp's keys of that digit
-        u32 run = offs[(u64)tid * tiles + blockIdx.x];
+    {   // thread `tid` owns digit `tid`: its count in the tile, and the warps' prefixes
+        u32 pre[SORT_WARPS], tot = 0;
 #pragma unroll
         for (int w = 0; w < SORT_WARPS; w++) {
-            const u32 c = wc[w][tid];
-            wc[w][tid] = run;
-            run += c;
+            pre[w] = tot;
+            tot += wc[w][tid];
         }
+        // exclusive scan of the 256 digit totals across the block (digit = thread)
+        u32 x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= (u32)o) x += y;
+        }
+        __shared__ u32 ws[SORT_WARPS];
+        if (lane == 31) ws[warp] = x;
+        __syncthreads();
+        u32 before = 0;
+        for (u32 w = 0; w < warp; w++) before += ws[w];
+        const u32 start = before + x - tot;   // first slot of digit `tid` in the tile's order
+        tstart[tid] = start;
+#pragma unroll
+        for (int w = 0; w < SORT_WARPS; w++) wc[w][tid] = start + pre[w];
     }
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < SORT_PER; c++) {
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg[c]);
         if (dg[c] < 256u) {
-            const u32 pos = wc[warp][dg[c]] + __popc(peers & lt);
-            keys_out[pos] = k[c];
-            if (PAIRS) vals_out[pos] = vals[w0 + (u64)c * 32 + lane];
+            const u32 slot = wc[warp][dg[c]] + __popc(peers & lt);
+            sk[slot] = k[c];
+            if (PAIRS) sv[slot] = vals[w0 + (u64)c * 32 + lane];
         }
         __syncwarp();
         if (dg[c] < 256u && (peers & lt) == 0) wc[warp][dg[c]] += __popc(peers);
         __syncwarp();
     }
+    __syncthreads();
+    for (u32 i = tid; i < cnt; i += SORT_THREADS) {   // consecutive slots of a digit: consecutive addresses
+        const u64 key = sk[i];
+        const u32 d = (u32)((key >> shift) & 0xFF);
+        const u32 pos = gbase[d] + (i - tstart[d]);
+        keys_out[pos] = key;
+        if (PAIRS) vals_out[pos] = sv[i];
+    }
 }
 
 size_t gc_sort_temp_bytes(uint64_t cap) {
     const u64 tiles = (cap + SORT_TILE - 1) / SORT_TILE;
-    return (size_t)(256 * (tiles ? tiles : 1)) * sizeof(u32) + 256;
+    return (size_t)(256 * (tiles ? tiles : 1) + 256) * sizeof(u32) + 256;
 }
+constexpr size_t SORT_SMEM = (size_t)SORT_TILE * (sizeof(u64) + sizeof(u32));   // 48 KB staging
 
 cudaError_t gc_sort(u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, uint64_t cap, const u64 *n_dev,
                     int lo_bit, int hi_bit, void *temp, size_t temp_bytes, cudaStream_t s, u64 **keys_out,
@@ -178,15 +231,23 @@ cudaError_t gc_sort(u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, uint64_t
     const u64 tiles = (cap + SORT_TILE - 1) / SORT_TILE;
     if (gc_sort_temp_bytes(cap) > temp_bytes || tiles > 0xFFFFFFFFull) return cudaErrorInvalidValue;
     u32 *counts = reinterpret_cast<u32 *>(temp);
+    u32 *rowsum = counts + 256 * tiles;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(sort_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
+        cudaFuncSetAttribute(sort_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
+        attr = true;
+    }
     for (int sh = lo_bit; sh < hi_bit; sh += 8) {
         sort_count_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, n_dev, cap, sh, counts, (u32)tiles);
-        sort_scan_kernel<<<1, 1024, 0, s>>>(counts, (u32)tiles, n_dev, cap);
+        sort_rowscan_kernel<<<256, 1024, 0, s>>>(counts, (u32)tiles, n_dev, cap, rowsum);
+        sort_rowbase_kernel<<<1, 32, 0, s>>>(rowsum);
         if (va)
-            sort_scatter_kernel<true><<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, va, kb, vb, n_dev, cap, sh, counts,
-                                                                             (u32)tiles);
+            sort_scatter_kernel<true><<<(unsigned)tiles, SORT_THREADS, SORT_SMEM, s>>>(ka, va, kb, vb, n_dev, cap, sh,
+                                                                                     counts, rowsum, (u32)tiles);
         else
-            sort_scatter_kernel<false><<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, nullptr, kb, nullptr, n_dev, cap, sh,
-                                                                              counts, (u32)tiles);
+            sort_scatter_kernel<false><<<(unsigned)tiles, SORT_THREADS, SORT_SMEM, s>>>(ka, nullptr, kb, nullptr, n_dev,
+                                                                                      cap, sh, counts, rowsum, (u32)tiles);
         u64 *tk = ka; ka = kb; kb = tk;
         u32 *tv = va; va = vb; vb = tv;
     }
@@ -322,7 +383,8 @@ static void preload1(F f) {
     cudaFuncGetAttributes(&a, f);
 }
 void preload_sort_kernels() {
-    preload1(sort_count_kernel); preload1(sort_scan_kernel); preload1(sort_scatter_kernel<true>);
+    preload1(sort_count_kernel); preload1(sort_rowscan_kernel); preload1(sort_rowbase_kernel);
+    preload1(sort_scatter_kernel<true>);
     preload1(sort_scatter_kernel<false>); preload1(scan_reduce_kernel); preload1(scan_blocks_kernel);
     preload1(scan_apply_kernel);
 }
