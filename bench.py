@@ -689,22 +689,27 @@ def config_key(args):
             + (" launch=tuned" if args.launch == "tuned" and args.lanes > 1 and args.wd == 0 else ""))
 
 
-def launches_per_step(schemes, pipelined=False):
-    """Kernel launches issued by libgcctb per step: 1 generator + per scheme: reset 2,
-    exec 1, finalize (2PL: ticket positions + copy_out = 2; other non-deterministic: iota +
-    CUB radix sort (counted 1) + commit_pos + copy_out = 4, TicToc +2; deterministic: iota
-    + commit_pos + copy_out = 3), plus
-    GaccO prep 6 (gather, sort, flags, scan, starts, positions) and GPUTx prep 13
-    (pipelined: on the prep stream, + 1 error merge at submit)."""
+def launches_per_step(schemes, pipelined=False, a3_passes=3, rank_passes=3):
+    """Kernel launches libgcctb issues per step (memsets excluded): 1 generator; per scheme
+    a2 = reset + zero + batch-error merge (3), the executor (1), a7 = commit positions +
+    copy_out + stats: 2PL dense tickets 1; TO / MVCC / Silo bitmap 5; TicToc ticket inverse
+    + gather + 6 radix passes x 4 kernels + commit_pos = 27; GPUTx / GaccO iota + commit_pos
+    2 (+ 1 error merge when prepared).  a3 (GaccO 18, GPUTx 36: gather, a3_passes radix
+    passes x 4, marks, 3-kernel max-scan, positions; GPUTx + fill, rank pass, keys, rank_passes
+    radix passes x 4, copy, bounds, count) on the prep stream when pipelined."""
+    a3 = 1 + 4 * a3_passes + 1 + 3 + 1
     n = 1
     for s in schemes:
-        n += 3
-        if s in ("gputx", "gacco"):
-            n += 3 + (6 if s == "gacco" else 13) + (1 if pipelined else 0)
-        elif s in ("tpl_nw", "tpl_wd"):
-            n += 2
+        n += 3 + 1 + 2
+        if s in ("tpl_nw", "tpl_wd"):
+            n += 1
+        elif s in ("to", "mvcc", "silo"):
+            n += 5
+        elif s == "tictoc":
+            n += 27
         else:
-            n += 4 + (2 if s == "tictoc" else 0)
+            n += 2 + (1 if pipelined else 0)
+            n += a3 + (0 if s == "gacco" else 1 + 1 + 1 + 4 * rank_passes + 3)
     return n
 
 

@@ -302,8 +302,12 @@ typedef struct {
     uint32_t claim_chunk;   /* fresh transaction ids a worker claims per atomic (0 = 1) */
 } cc_exec_desc;
 
-/* Per-transaction results, all DEVICE pointers owned by the caller.  Any may be NULL
- * except committed.  n = n_txn of the batch, K = ops_per_txn.
+/* Per-transaction results, owned by the caller: all DEVICE pointers, or all HOST pointers
+ * (a mix is INVALID_ARG).  Host buffers are filled by copies the submit enqueues at its end
+ * from library-owned device staging (pinned memory: asynchronous, complete at cc_sync;
+ * pageable memory: the copy waits for the submit); a host-driven partitioned submit
+ * (CC_FLAG_PARTITIONED without CC_FLAG_PART_P2P) takes device buffers only (UNSUPPORTED).
+ * Any may be NULL except committed.  n = n_txn of the batch, K = ops_per_txn.
  *   committed u8[n]   1 iff the transaction committed
  *   restarts  u32[n]  number of aborted attempts
  *   order_hi/lo u64[n] the scheme's serialization-order key;

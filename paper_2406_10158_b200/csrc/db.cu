@@ -239,6 +239,8 @@ struct cc_db_s {
     u64 *ring = nullptr;
     uint32_t ring_cap = 0;
     RankBitmap rank_bm{};               // a7 commit positions of TO / MVCC / Silo
+    cc_result hres{};                   // device staging of results requested in host memory
+    uint32_t hres_txn = 0, hres_words = 0;
     void *ws = nullptr;                 // thread-mode staging workspace (global fallback)
     uint64_t ws_bytes = 0;
     u64 *arena = nullptr;
@@ -397,6 +399,8 @@ cc_status cc_db_destroy(cc_db db) {
     dfree(db->part.recv);
     dfree(db->arena);
     dfree(db->ws);
+    dfree(db->hres.committed); dfree(db->hres.restarts); dfree(db->hres.order_hi); dfree(db->hres.order_lo);
+    dfree(db->hres.commit_pos); dfree(db->hres.read_out); dfree(db->hres.stats);
     dfree(db->rank_bm.bits);
     dfree(db->rank_bm.pre);
     dfree(db->rank_bm.csum);
@@ -988,10 +992,79 @@ static cc_status wl_params(cc_db db, cc_batch b, uint32_t flags, YcsbParams &y, 
     return CC_OK;
 }
 
-cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res) {
+// Results requested in host memory: 0 device, 1 host (pinned or pageable), -1 mixed
+static int result_kind(const cc_result *r) {
+    const void *ptrs[7] = {r->committed, r->restarts, r->order_hi, r->order_lo, r->commit_pos, r->read_out, r->stats};
+    int kind = -2;
+    for (const void *q : ptrs) {
+        if (!q) continue;
+        cudaPointerAttributes a{};
+        const bool host = cudaPointerGetAttributes(&a, q) != cudaSuccess || a.type == cudaMemoryTypeHost ||
+                          a.type == cudaMemoryTypeUnregistered;
+        cudaGetLastError();   // an unregistered pointer may leave an error behind on older runtimes
+        const int k = host ? 1 : 0;
+        if (kind == -2) kind = k;
+        else if (kind != k) return -1;
+    }
+    return kind < 0 ? 0 : kind;
+}
+
+// device staging for host-memory results (grown on demand, never inside a P2P round)
+static cc_status ensure_hres(cc_db db, uint32_t n_txn, uint32_t words) {
+    if (n_txn <= db->hres_txn && words <= db->hres_words) return CC_OK;
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    cc_result &h = db->hres;
+    dfree(h.committed); dfree(h.restarts); dfree(h.order_hi); dfree(h.order_lo); dfree(h.commit_pos);
+    dfree(h.read_out); dfree(h.stats);
+    h = cc_result{};
+    CUDA_TRY(db, dalloc(&h.committed, n_txn));
+    CUDA_TRY(db, dalloc(&h.restarts, n_txn * 4ull));
+    CUDA_TRY(db, dalloc(&h.order_hi, n_txn * 8ull));
+    CUDA_TRY(db, dalloc(&h.order_lo, n_txn * 8ull));
+    CUDA_TRY(db, dalloc(&h.commit_pos, n_txn * 4ull));
+    CUDA_TRY(db, dalloc(&h.read_out, (uint64_t)n_txn * words * 8));
+    CUDA_TRY(db, dalloc(&h.stats, 8 * CC_STATS_WORDS));
+    db->hres_txn = n_txn;
+    db->hres_words = words;
+    return CC_OK;
+}
+
+// copy the staged results of a submit to the caller's host buffers (db stream)
+static cc_status copy_results_out(cc_db db, const cc_result *user, uint32_t n_txn, uint32_t words) {
+    const cc_result &h = db->hres;
+    auto cp = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
+        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, db->stream) : cudaSuccess;
+    };
+    CUDA_TRY(db, cp(user->committed, h.committed, n_txn));
+    CUDA_TRY(db, cp(user->restarts, h.restarts, n_txn * 4ull));
+    CUDA_TRY(db, cp(user->order_hi, h.order_hi, n_txn * 8ull));
+    CUDA_TRY(db, cp(user->order_lo, h.order_lo, n_txn * 8ull));
+    CUDA_TRY(db, cp(user->commit_pos, h.commit_pos, n_txn * 4ull));
+    CUDA_TRY(db, cp(user->read_out, h.read_out, (uint64_t)n_txn * words * 8));
+    CUDA_TRY(db, cp(user->stats, h.stats, 8 * CC_STATS_WORDS));
+    return CC_OK;
+}
+
+cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res_in) {
     CHECK_DB(db);
-    if (!b || !desc || !res || !res->committed)
+    if (!b || !desc || !res_in || !res_in->committed)
         return fail(db, CC_ERR_INVALID_ARG, "cc_submit: null batch/desc/result");
+    // results in host memory are staged in library-owned device buffers and copied out at
+    // the end of the submit (pinned: asynchronously on the db stream)
+    const int rkind = result_kind(res_in);
+    if (rkind < 0) return fail(db, CC_ERR_INVALID_ARG, "cc_submit: result pointers mix host and device memory");
+    const uint32_t out_words = b->kind == KIND_TPCC ? TPCC_OUT_WORDS : b->K;
+    cc_result staged{};
+    const cc_result *res = res_in;
+    if (rkind == 1) {
+        if ((desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) && !(desc->flags & CC_FLAG_PART_P2P))
+            return fail(db, CC_ERR_UNSUPPORTED, "host result buffers: not with a host-driven partitioned submit");
+        cc_status st0 = ensure_hres(db, b->n_txn, out_words);
+        if (st0) return st0;
+        staged = db->hres;
+        if (!res_in->read_out) staged.read_out = nullptr;
+        res = &staged;
+    }
     if ((unsigned)desc->scheme >= CC_NUM_SCHEMES) return fail(db, CC_ERR_INVALID_ARG, "bad scheme");
     if (desc->wd > 5 || desc->bs < 1 || desc->bs > 32)
         return fail(db, CC_ERR_INVALID_ARG, "wd must be 0..5 and bs 1..32 (PAPER.md:480-484)");
@@ -1210,6 +1283,10 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         if ((void *)r.stats != (void *)db->stats_scratch)
             CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS, cudaMemcpyDeviceToDevice,
                                          db->stream));
+        if (rkind == 1) {
+            cc_status st1 = copy_results_out(db, res_in, b->n_txn, out_words);
+            if (st1) return st1;
+        }
         if (timing) {
             CUDA_TRY(db, cudaEventRecord(ev.ev[4], db->stream));
             db->pending.push_back(ev);
@@ -1248,6 +1325,10 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if ((void *)r.stats != (void *)db->stats_scratch)
         CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS,
                                      cudaMemcpyDeviceToDevice, db->stream));
+    if (rkind == 1) {
+        cc_status st1 = copy_results_out(db, res_in, b->n_txn, out_words);
+        if (st1) return st1;
+    }
     if (timing) {
         CUDA_TRY(db, cudaEventRecord(ev.ev[4], db->stream));
         db->pending.push_back(ev);
@@ -1464,6 +1545,8 @@ static cc_status p2p_buffers(cc_db db) {
     st = ensure_scratch(db, P.win_txn, (uint64_t)P.win_txn * TPCC_K);
     if (st) return st;
     st = ensure_arena(db, (uint64_t)P.win_txn * TPCC_K, TPCC_C_WORDS);
+    if (st) return st;
+    st = ensure_hres(db, P.win_txn, TPCC_OUT_WORDS);   // host-memory results of a P2P submit
     if (st) return st;
     P.connected = true;
     return CC_OK;

@@ -572,6 +572,9 @@ constexpr u32 TPL_INTENT_AFTER = 32;
 #ifndef GC_WD_SEQ_AFTER
 #define GC_WD_SEQ_AFTER 0
 #endif
+#ifndef GC_WD_RELEASE_ON_WAIT
+#define GC_WD_RELEASE_ON_WAIT 0
+#endif
 
 template <bool WD>
 GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, bool intent) {
@@ -1177,17 +1180,28 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
             if (tile.all(!act || held)) break;
             if (!tile.any(st == ST_WAIT)) continue;   // ordered: the next lane's turn
+            if (WD && GC_WD_RELEASE_ON_WAIT && held) {
+                // (experiment knob) an older transaction that must wait gives back the locks
+                // it holds so far -- no row has been read under them yet (rows are read once
+                // every lock is held), so this is not an abort -- and re-requests them all
+                tpl_release_relaxed(p, cw(p, L.rec), L.w);
+                held = false;
+            }
             if (tile.any(!sp.wait(th))) {
                 if (held) tpl_release_relaxed(p, cw(p, L.rec), L.w);
                 return RES_FATAL;
             }
         }
-        if (act) rd<WL>(th, y, L, gid, li, WL::row(y, L));   // stable under the lock
+        // lock point: the ticket's atomic is issued before the row reads, so its round trip
+        // overlaps them instead of lengthening the critical section; the shuffle before the
+        // releases makes every lane wait for it (a conflicting successor draws its ticket
+        // only after acquiring a lock released here)
         u64 ticket = 0;
-        if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);   // lock point
+        if (li == 0) ticket = atomicAdd(&p.ctl->ticket.v, 1ull);
+        if (act) rd<WL>(th, y, L, gid, li, WL::row(y, L));   // stable under the lock
+        if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         key_lo = tile.shfl(ticket, 0);
         key_hi = 0;
-        if (act && L.w) inst<WL>(th, y, L, WL::row(y, L));
         fence_acqrel();
         if (act) tpl_release_relaxed(p, cw(p, L.rec), L.w);
         return RES_OK;

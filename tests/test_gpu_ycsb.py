@@ -593,3 +593,27 @@ def test_c1_all_writes_extreme_contention(c1, orc, scheme, lanes):
     assert int(h["restarts"].astype(np.int64).sum()) == st.aborts
     orc.check_ycsb(scheme, S0, keys, ops, 8, h, db.read_table(0))
     b.free()
+
+
+def test_generator_failure_is_reported_at_submit(torch_cuda):
+    """an a1 failure (no distinct keys drawable: every threshold 0 puts all the
+    Zipf mass on one rank) stays with its batch -- the next submit's a2 reset does not
+    erase it -- so the submit executes nothing and cc_sync reports CONFIG; the db is not
+    sticky-failed, a valid batch afterwards commits normally."""
+    from paper_2406_10158_b200.api import DB
+    from paper_2406_10158_b200.gcctb import CCError
+    db = DB(0)
+    db.load_ycsb(64, 3)
+    T0 = np.zeros(64, np.uint64)
+    bad = db.gen_ycsb(1, 2, 0.0, 1, T0, 5)
+    res = db.submit(bad, "tpl_nw", lanes=1, wd=0, bs=1)
+    with pytest.raises(CCError, match="CONFIG"):
+        db.sync()
+    assert int(res.committed.cpu().sum()) == 0
+    bad.free()
+    T = inputs.zipf_thresholds(64, 0.5)
+    ok = db.gen_ycsb(32, 2, 0.5, 2, T, 5)
+    db.submit(ok, "tpl_nw", lanes=1, wd=0, bs=1)
+    assert db.sync().commits == 32
+    ok.free()
+    db.close()

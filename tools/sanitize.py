@@ -21,8 +21,10 @@ SCHEMES = ["tpl_nw", "tpl_wd", "to", "mvcc", "silo", "tictoc", "gputx", "gacco"]
 
 
 def main():
-    only = sys.argv[1].split(",") if len(sys.argv) > 1 else SCHEMES
-    n_rows, B, K, W, theta = 1024, 1024, 4, 0.5, 0.8
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    small = "--small" in sys.argv   # racecheck: a quarter of the batch (its instrumentation is slow)
+    only = args[0].split(",") if args else SCHEMES
+    n_rows, B, K, W, theta = 1024, 256 if small else 1024, 4, 0.5, 0.8
     db = DB(0)
     db.load_ycsb(n_rows, 11)
     S0 = db.read_table(0)
@@ -45,16 +47,17 @@ def main():
     from inputs import tpcc as IT
     from oracle import tpcc as OT
     db = DB(0)
-    db.load_tpcc(2, 5, 512)
+    NT = 128 if small else 512
+    db.load_tpcc(2, 5, NT)
     P0 = IT.population(5, 2)
     db.snapshot(True)
-    tb = db.gen_tpcc(512, 3, 5114)
+    tb = db.gen_tpcc(NT, 3, 5114)
     tx = tb.export_tpcc()
     for scheme in only:
         for lanes in (1, 32):
             db.snapshot(False)
             res = db.submit(tb, scheme, wd=0, bs=8, lanes=lanes, watchdog_s=600)
-            assert db.sync().commits == 512
+            assert db.sync().commits == NT
             OT.check(scheme, P0, tx, 2, res.host(db.stream), db.read_tpcc(list(OT.TABLES + OT.SLOTS)))
             print(f"tpcc {scheme} lanes={lanes}: ok", flush=True)
     db.close()
