@@ -269,8 +269,6 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         reached L2 (one load per 32 B sector), so a lock /
                                         pending write is held across L2 latencies only, not
                                         across its cold rows' HBM misses.  Same results. */
-#define CC_FLAG_NO_LOOKAHEAD 0x8000u /* ablation: tile mode without the claim / key / line look-ahead
-                                        (DESIGN.md §2); same results */
 #define CC_FLAG_META_PAD 0x10000u    /* single-word schemes: one control word per 32 B sector instead of
                                         packed 8 B words (the north star's metadata padded against
                                         false sharing in L2).  Same results;
@@ -497,6 +495,11 @@ typedef struct {
     double handoff_acq_row_ns;
 } cc_roofline;
 cc_status cc_roofline_probe(cc_db db, cc_roofline *out);
+/* Access-size sweep of the gather ceiling (check the 128 B figure against
+ * other sizes and ncu): GB/s of random, size-aligned reads of 32, 64, 128 and 256 B over
+ * 1 GiB, 8 or 16 in flight per thread (the better), on the db stream; waits.  Allocates
+ * 1 GiB of scratch for the call.  Errors: INVALID_ARG (null), OOM, CUDA. */
+cc_status cc_gather_sweep(cc_db db, double gbs[4]);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,21 @@ class Result:
             stats=torch.zeros(G.CC_STATS_WORDS, dtype=torch.int64, **z),
         )
 
+    @staticmethod
+    def alloc_host(n_txn: int, K: int, read_out=True, out_words=None) -> "Result":
+        """Pinned host buffers: the submit stages the results on the device and copies them
+        out asynchronously (complete at the next sync)."""
+        z = dict(device="cpu", pin_memory=True)
+        return Result(
+            committed=torch.zeros(n_txn, dtype=torch.uint8, **z),
+            restarts=torch.zeros(n_txn, dtype=torch.int32, **z),
+            order_hi=torch.zeros(n_txn, dtype=torch.int64, **z),
+            order_lo=torch.zeros(n_txn, dtype=torch.int64, **z),
+            commit_pos=torch.zeros(n_txn, dtype=torch.int32, **z),
+            read_out=torch.zeros(n_txn * (out_words or K), dtype=torch.int64, **z) if read_out else None,
+            stats=torch.zeros(G.CC_STATS_WORDS, dtype=torch.int64, **z),
+        )
+
     def c(self) -> G.cc_result:
         p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
         return G.cc_result(p(self.committed), p(self.restarts), p(self.order_hi), p(self.order_lo),
@@ -380,6 +395,12 @@ class DB:
 
     def pool_trim(self):
         self._chk(G.lib().cc_pool_trim(self.h))
+
+    def gather_sweep(self) -> dict:
+        """GB/s of random 32 / 64 / 128 / 256 B reads over 1 GiB (cc_gather_sweep)."""
+        out = (ctypes.c_double * 4)()
+        self._chk(G.lib().cc_gather_sweep(self.h, ctypes.byref(out)))
+        return {32: out[0], 64: out[1], 128: out[2], 256: out[3]}
 
     def snapshot(self, save: bool):
         self._chk(G.lib().cc_snapshot(self.h, 1 if save else 0))

@@ -239,7 +239,10 @@ struct cc_db_s {
     u64 *ring = nullptr;
     uint32_t ring_cap = 0;
     RankBitmap rank_bm{};               // a7 commit positions of TO / MVCC / Silo
-    cc_result hres{};                   // device staging of results requested in host memory
+    cc_result hres[2]{};                // device staging of results requested in host memory
+    cudaEvent_t hres_out[2]{};          // the copy-out of the submit that last used staging set k
+    bool hres_used[2] = {false, false};
+    int hres_next = 0;                  // alternating: a submit's copy-out overlaps the next one
     uint32_t hres_txn = 0, hres_words = 0;
     void *ws = nullptr;                 // thread-mode staging workspace (global fallback)
     uint64_t ws_bytes = 0;
@@ -399,8 +402,12 @@ cc_status cc_db_destroy(cc_db db) {
     dfree(db->part.recv);
     dfree(db->arena);
     dfree(db->ws);
-    dfree(db->hres.committed); dfree(db->hres.restarts); dfree(db->hres.order_hi); dfree(db->hres.order_lo);
-    dfree(db->hres.commit_pos); dfree(db->hres.read_out); dfree(db->hres.stats);
+    for (int k = 0; k < 2; k++) {
+        cc_result &h = db->hres[k];
+        dfree(h.committed); dfree(h.restarts); dfree(h.order_hi); dfree(h.order_lo);
+        dfree(h.commit_pos); dfree(h.read_out); dfree(h.stats);
+        if (db->hres_out[k]) cudaEventDestroy(db->hres_out[k]);
+    }
     dfree(db->rank_bm.bits);
     dfree(db->rank_bm.pre);
     dfree(db->rank_bm.csum);
@@ -1009,31 +1016,40 @@ static int result_kind(const cc_result *r) {
     return kind < 0 ? 0 : kind;
 }
 
-// device staging for host-memory results (grown on demand, never inside a P2P round)
+// device staging for host-memory results: two sets, so one submit's copy-out (on the
+// copy stream) overlaps the next submit (grown on demand, never inside a P2P round)
 static cc_status ensure_hres(cc_db db, uint32_t n_txn, uint32_t words) {
     if (n_txn <= db->hres_txn && words <= db->hres_words) return CC_OK;
     CUDA_TRY(db, cudaStreamSynchronize(db->stream));
-    cc_result &h = db->hres;
-    dfree(h.committed); dfree(h.restarts); dfree(h.order_hi); dfree(h.order_lo); dfree(h.commit_pos);
-    dfree(h.read_out); dfree(h.stats);
-    h = cc_result{};
-    CUDA_TRY(db, dalloc(&h.committed, n_txn));
-    CUDA_TRY(db, dalloc(&h.restarts, n_txn * 4ull));
-    CUDA_TRY(db, dalloc(&h.order_hi, n_txn * 8ull));
-    CUDA_TRY(db, dalloc(&h.order_lo, n_txn * 8ull));
-    CUDA_TRY(db, dalloc(&h.commit_pos, n_txn * 4ull));
-    CUDA_TRY(db, dalloc(&h.read_out, (uint64_t)n_txn * words * 8));
-    CUDA_TRY(db, dalloc(&h.stats, 8 * CC_STATS_WORDS));
+    CUDA_TRY(db, cudaStreamSynchronize(db->copy_stream));
+    for (int k = 0; k < 2; k++) {
+        cc_result &h = db->hres[k];
+        dfree(h.committed); dfree(h.restarts); dfree(h.order_hi); dfree(h.order_lo); dfree(h.commit_pos);
+        dfree(h.read_out); dfree(h.stats);
+        h = cc_result{};
+        CUDA_TRY(db, dalloc(&h.committed, n_txn));
+        CUDA_TRY(db, dalloc(&h.restarts, n_txn * 4ull));
+        CUDA_TRY(db, dalloc(&h.order_hi, n_txn * 8ull));
+        CUDA_TRY(db, dalloc(&h.order_lo, n_txn * 8ull));
+        CUDA_TRY(db, dalloc(&h.commit_pos, n_txn * 4ull));
+        CUDA_TRY(db, dalloc(&h.read_out, (uint64_t)n_txn * words * 8));
+        CUDA_TRY(db, dalloc(&h.stats, 8 * CC_STATS_WORDS));
+        if (!db->hres_out[k]) CUDA_TRY(db, cudaEventCreateWithFlags(&db->hres_out[k], cudaEventDisableTiming));
+        db->hres_used[k] = false;
+    }
     db->hres_txn = n_txn;
     db->hres_words = words;
     return CC_OK;
 }
 
-// copy the staged results of a submit to the caller's host buffers (db stream)
-static cc_status copy_results_out(cc_db db, const cc_result *user, uint32_t n_txn, uint32_t words) {
-    const cc_result &h = db->hres;
+// copy the staged results of a submit (set k) to the caller's host buffers on the copy
+// stream, after the submit's work on the db stream; cc_sync waits for it
+static cc_status copy_results_out(cc_db db, int k, const cc_result *user, uint32_t n_txn, uint32_t words) {
+    const cc_result &h = db->hres[k];
+    CUDA_TRY(db, cudaEventRecord(db->copy_after, db->stream));
+    CUDA_TRY(db, cudaStreamWaitEvent(db->copy_stream, db->copy_after, 0));
     auto cp = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
-        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, db->stream) : cudaSuccess;
+        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, db->copy_stream) : cudaSuccess;
     };
     CUDA_TRY(db, cp(user->committed, h.committed, n_txn));
     CUDA_TRY(db, cp(user->restarts, h.restarts, n_txn * 4ull));
@@ -1042,6 +1058,8 @@ static cc_status copy_results_out(cc_db db, const cc_result *user, uint32_t n_tx
     CUDA_TRY(db, cp(user->commit_pos, h.commit_pos, n_txn * 4ull));
     CUDA_TRY(db, cp(user->read_out, h.read_out, (uint64_t)n_txn * words * 8));
     CUDA_TRY(db, cp(user->stats, h.stats, 8 * CC_STATS_WORDS));
+    CUDA_TRY(db, cudaEventRecord(db->hres_out[k], db->copy_stream));
+    db->hres_used[k] = true;
     return CC_OK;
 }
 
@@ -1055,13 +1073,18 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (rkind < 0) return fail(db, CC_ERR_INVALID_ARG, "cc_submit: result pointers mix host and device memory");
     const uint32_t out_words = b->kind == KIND_TPCC ? TPCC_OUT_WORDS : b->K;
     cc_result staged{};
+    int hk = 0;
     const cc_result *res = res_in;
     if (rkind == 1) {
         if ((desc->flags & (CC_FLAG_PARTITIONED | CC_FLAG_PART_ALL)) && !(desc->flags & CC_FLAG_PART_P2P))
             return fail(db, CC_ERR_UNSUPPORTED, "host result buffers: not with a host-driven partitioned submit");
         cc_status st0 = ensure_hres(db, b->n_txn, out_words);
         if (st0) return st0;
-        staged = db->hres;
+        hk = db->hres_next;
+        db->hres_next ^= 1;
+        // the set's previous copy-out must have drained before this submit overwrites it
+        if (db->hres_used[hk]) CUDA_TRY(db, cudaStreamWaitEvent(db->stream, db->hres_out[hk], 0));
+        staged = db->hres[hk];
         if (!res_in->read_out) staged.read_out = nullptr;
         res = &staged;
     }
@@ -1284,7 +1307,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
             CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS, cudaMemcpyDeviceToDevice,
                                          db->stream));
         if (rkind == 1) {
-            cc_status st1 = copy_results_out(db, res_in, b->n_txn, out_words);
+            cc_status st1 = copy_results_out(db, hk, res_in, b->n_txn, out_words);
             if (st1) return st1;
         }
         if (timing) {
@@ -1326,7 +1349,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS,
                                      cudaMemcpyDeviceToDevice, db->stream));
     if (rkind == 1) {
-        cc_status st1 = copy_results_out(db, res_in, b->n_txn, out_words);
+        cc_status st1 = copy_results_out(db, hk, res_in, b->n_txn, out_words);
         if (st1) return st1;
     }
     if (timing) {
@@ -1510,14 +1533,17 @@ static void window_ptrs(void *base, uint32_t world, uint32_t cap, PartReq **inbo
 }
 
 static void preload_all_kernels() {
-    static bool done = false;   // once per process (modules are shared by the dbs)
-    if (done) return;
+    static std::atomic<uint64_t> done{0};   // once per device (modules load per context)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load() & bit) return;
     preload_prep_kernels();
     preload_sort_kernels();
     preload_part_kernels();
     preload_tpcc_kernels();
     preload_ycsb_kernels();
-    done = true;
+    done |= bit;
 }
 
 static cc_status p2p_buffers(cc_db db) {
@@ -1659,6 +1685,7 @@ static cc_status drain_timing(cc_db db) {
 cc_status cc_sync(cc_db db, cc_stats *out) {
     CHECK_DB(db);
     CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->copy_stream));   // host-memory results of the submits
     CUDA_TRY(db, cudaGetLastError());
     u64 w[CC_STATS_WORDS];
     CUDA_TRY(db, cudaMemcpy(w, db->stats_scratch, sizeof w, cudaMemcpyDeviceToHost));
@@ -1737,6 +1764,15 @@ cc_status cc_roofline_probe(cc_db db, cc_roofline *out) {
     out->handoff_row_ns = v[3];
     out->handoff_ns = v[4];
     out->handoff_acq_row_ns = v[5];
+    return CC_OK;
+}
+
+cc_status cc_gather_sweep(cc_db db, double gbs[4]) {
+    CHECK_DB(db);
+    if (!gbs) return fail(db, CC_ERR_INVALID_ARG, "null output");
+    CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    for (int k = 0; k < 4; k++) gbs[k] = 0;
+    CUDA_TRY(db, gather_sweep(db->stream, db->num_sms, gbs));
     return CC_OK;
 }
 

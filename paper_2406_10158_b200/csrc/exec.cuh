@@ -572,9 +572,6 @@ constexpr u32 TPL_INTENT_AFTER = 32;
 #ifndef GC_WD_SEQ_AFTER
 #define GC_WD_SEQ_AFTER 0
 #endif
-#ifndef GC_WD_RELEASE_ON_WAIT
-#define GC_WD_RELEASE_ON_WAIT 0
-#endif
 
 template <bool WD>
 GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, bool intent) {
@@ -1180,13 +1177,6 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
             if (tile.all(!act || held)) break;
             if (!tile.any(st == ST_WAIT)) continue;   // ordered: the next lane's turn
-            if (WD && GC_WD_RELEASE_ON_WAIT && held) {
-                // (experiment knob) an older transaction that must wait gives back the locks
-                // it holds so far -- no row has been read under them yet (rows are read once
-                // every lock is held), so this is not an abort -- and re-requests them all
-                tpl_release_relaxed(p, cw(p, L.rec), L.w);
-                held = false;
-            }
             if (tile.any(!sp.wait(th))) {
                 if (held) tpl_release_relaxed(p, cw(p, L.rec), L.w);
                 return RES_FATAL;
@@ -1402,56 +1392,17 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
     typename WL::Lane &L = WL::STAGE_TILE_LANE ? Ls[threadIdx.x] : Lr;   // (global when it does not fit)
     th.cl = Claim{};
     Claim &cl = th.cl;
-    // Look-ahead (fresh ids of the six non-deterministic schemes -- GaccO / GPUTx are bound
-    // by their hand-off chains, where it measured slower -- on workloads whose accesses
-    // resolve without a memory probe, i.e. YCSB direct addressing): a worker keeps two more fresh ids in a
-    // three-stage pipeline -- the claim's atomic is issued one transaction ahead, the next
-    // id's keys are loaded one transaction ahead and its rows and control words prefetched
-    // into L2 the transaction after that -- so a transaction starts with its claim, keys
-    // and lines already on chip instead of paying three dependent round trips first.  Ids
-    // are still executed in claim order per worker, so every transaction waited on is
-    // claimed by a running worker (the liveness argument of the queue is unchanged).
-    const bool LA = !DET && p.claim_chunk <= 1 && WL::lookahead(p, y) && !(p.flags & CC_FLAG_NO_LOOKAHEAD);
-    u32 qX = NO_TXN, qP = NO_TXN;   // next to execute (lines prefetched) / keys loaded, lines prefetched now
-    u32 tokP = 0;                    // this lane's access token (key or record) of qP
-    u64 pend = ~0ull;                // leader: in-flight fresh claim (atomicAdd result)
-    u32 att = 0;                     // leader: restarts of the current transaction
+    u32 att = 0;   // leader: restarts of the current transaction (fresh ids: 0, not loaded)
     for (;;) {
         u32 gid = NO_TXN;
         bool fresh = false;
-        if (LA) {
-            u32 nid = NO_TXN;
-            if (li == 0 && pend != ~0ull) {   // the claim issued a transaction ago has arrived
-                if (pend < p.n_txn) {
-                    nid = (u32)pend;
-                    pend = atomicAdd(&p.ctl->head.v, 1ull);
-                } else {
-                    cl.exhausted = true;
-                    pend = ~0ull;
-                }
-            }
-            nid = tile.shfl(nid, 0);
-            gid = qX;   // the oldest claimed id runs: ids execute in claim order
-            if (gid == NO_TXN) { gid = qP; qP = NO_TXN; }   // (pipeline filling or draining)
-            if (gid == NO_TXN) { gid = nid; nid = NO_TXN; }
-            if (qP != NO_TXN) WL::prefetch_token(p, y, qP, li, tokP);   // its lines arrive during this transaction
-            const u32 tokN = nid != NO_TXN ? WL::token(p, y, nid, li) : 0u;   // consumed next round
-            qX = qP;
-            qP = nid;
-            tokP = tokN;
-            fresh = gid != NO_TXN;
-            th.hot = 0;
+        if (li == 0) {
+            gid = claim_work<S>(th, cl);
+            fresh = cl.fresh;
         }
-        if (gid == NO_TXN) {   // synchronous claim: the first id, or the retry batch
-            if (li == 0) {
-                gid = claim_work<S>(th, cl);
-                fresh = cl.fresh;
-                if (LA && fresh && gid != NO_TXN && !cl.exhausted) pend = atomicAdd(&p.ctl->head.v, 1ull);
-            }
-            gid = tile.shfl(gid, 0);
-            fresh = tile.shfl(fresh, 0);
-            th.hot = tile.shfl(th.hot, 0);   // from the retry-batch entry (0 for a fresh id)
-        }
+        gid = tile.shfl(gid, 0);
+        fresh = tile.shfl(fresh, 0);
+        th.hot = tile.shfl(th.hot, 0);   // from the retry-batch entry (0 for a fresh id)
         if (gid == NO_TXN) break;
         if (li == 0) att = fresh ? 0u : p.restarts[gid];   // fresh ids start at 0 restarts
         if (p.skip && p.skip[gid]) {   // distributed (partitioned TPC-C): phase B handles it

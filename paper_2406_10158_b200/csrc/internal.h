@@ -270,6 +270,8 @@ cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32
 // roof.cu: out = {gather GB/s, CAS/s L2-resident, CAS/s > L2, hand-off ns (row), hop ns,
 //                 hand-off ns (row, acquire polls)}
 cudaError_t roofline_probe(cudaStream_t s, int num_sms, double out[6]);
+// roof.cu: GB/s of random 32 / 64 / 128 / 256 B reads over 1 GiB
+cudaError_t gather_sweep(cudaStream_t s, int num_sms, double out[4]);
 
 // load every kernel of the library now (lazy module loading may otherwise synchronise the
 // context at a first launch while kernels of this process wait on each other)

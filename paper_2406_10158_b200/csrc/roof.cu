@@ -54,6 +54,80 @@ __global__ void roof_gather_kernel(const u64 *buf, u64 line_mask, u32 iters, u64
     if (acc == 0x5A5A5A5A5A5A5A5Aull) sink[0] = acc;   // keeps the loads alive
 }
 
+// access-size sweep of the gather ceiling: random BYTES-sized, BYTES-aligned reads (32 B
+// .cg vectors), ILP of them in flight per thread
+template <int BYTES, int ILP>
+__global__ void roof_gather_sweep_kernel(const u64 *buf, u64 unit_mask, u32 iters, u64 *sink) {
+    constexpr int V = BYTES / 32;   // 32 B vectors per access
+    const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    u64 acc = 0;
+    for (u32 it = 0; it < iters; it++) {
+        u64 v[ILP];
+#pragma unroll
+        for (int k = 0; k < ILP; k++) {
+            const u64 u = roof_hash(t * 0x10001ull + it * ILP + k) & unit_mask;
+            const u64 *p = buf + u * (BYTES / 8);
+            u64 x = 0;
+#pragma unroll
+            for (int j = 0; j < V; j++) {
+                u64 a, b, c, d;
+                ld_cg_v4(p + 4 * j, a, b, c, d);
+                x ^= a ^ b ^ c ^ d;
+            }
+            v[k] = x;
+        }
+#pragma unroll
+        for (int k = 0; k < ILP; k++) acc += v[k];
+    }
+    if (acc == 0x5A5A5A5A5A5A5A5Aull) sink[0] = acc;
+}
+
+template <int BYTES>
+static double sweep_one(cudaStream_t s, int num_sms, const u64 *buf, u64 bytes, u64 *sink, cudaEvent_t a,
+                        cudaEvent_t b) {
+    const int blk = 256, grid = num_sms * 8;
+    const u64 threads = (u64)grid * blk, units = bytes / BYTES;
+    double best = 0;
+    roof_gather_sweep_kernel<BYTES, 8><<<grid, blk, 0, s>>>(buf, units - 1, 1, sink);   // warm-up
+    for (int v = 0; v < 2; v++) {   // 8 or 16 accesses in flight per thread
+        const u32 iters = 8;
+        cudaEventRecord(a, s);
+        if (v == 0) roof_gather_sweep_kernel<BYTES, 8><<<grid, blk, 0, s>>>(buf, units - 1, iters, sink);
+        else roof_gather_sweep_kernel<BYTES, 16><<<grid, blk, 0, s>>>(buf, units - 1, iters / 2, sink);
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double gbs = (double)threads * 8 * BYTES / (ms * 1e-3) / 1e9;
+        best = gbs > best ? gbs : best;
+    }
+    return best;
+}
+
+// GB/s of random reads of 32, 64, 128 and 256 B over 1 GiB (larger than L2)
+cudaError_t gather_sweep(cudaStream_t s, int num_sms, double out[4]) {
+    const u64 bytes = 1ull << 30;
+    u64 *buf = nullptr, *sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&buf, bytes)) || (e = cudaMalloc(&sink, 64)) || (e = cudaEventCreate(&a)) ||
+        (e = cudaEventCreate(&b)))
+        goto done;
+    cudaMemsetAsync(buf, 0x3C, bytes, s);
+    out[0] = sweep_one<32>(s, num_sms, buf, bytes, sink, a, b);
+    out[1] = sweep_one<64>(s, num_sms, buf, bytes, sink, a, b);
+    out[2] = sweep_one<128>(s, num_sms, buf, bytes, sink, a, b);
+    out[3] = sweep_one<256>(s, num_sms, buf, bytes, sink, a, b);
+    e = cudaGetLastError();
+done:
+    cudaStreamSynchronize(s);
+    if (buf) cudaFree(buf);
+    if (sink) cudaFree(sink);
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    return e;
+}
+
 __global__ void roof_cas_kernel(u64 *words, u64 word_mask, u32 iters, u64 *sink) {   // 2^k words
     const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     u64 acc = 0;

@@ -232,12 +232,10 @@ cudaError_t gc_sort(u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, uint64_t
     if (gc_sort_temp_bytes(cap) > temp_bytes || tiles > 0xFFFFFFFFull) return cudaErrorInvalidValue;
     u32 *counts = reinterpret_cast<u32 *>(temp);
     u32 *rowsum = counts + 256 * tiles;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(sort_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
-        cudaFuncSetAttribute(sort_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
-        attr = true;
-    }
+    // (per call: the attribute belongs to the current device's context)
+    cudaError_t ea = cudaFuncSetAttribute(va ? (const void *)sort_scatter_kernel<true> : (const void *)sort_scatter_kernel<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
+    if (ea) return ea;
     for (int sh = lo_bit; sh < hi_bit; sh += 8) {
         sort_count_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, n_dev, cap, sh, counts, (u32)tiles);
         sort_rowscan_kernel<<<256, 1024, 0, s>>>(counts, (u32)tiles, n_dev, cap, rowsum);

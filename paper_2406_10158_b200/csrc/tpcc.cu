@@ -380,14 +380,7 @@ struct TpccWL {
     }
 
     static GC_DEV u64 warm(const ExecParams &, const TpccParams &, const Lane &) { return 0; }
-    // tile-mode look-ahead: off -- a TPC-C access needs its descriptor (and a by-name Payment
-    // the name index) before its row is known, so only the descriptor lines could be fetched
-    // ahead, and the pipeline's registers made the GaccO tile kernel spill
-    static GC_DEV bool lookahead(const ExecParams &, const TpccParams &) { return false; }
-    static GC_DEV u32 token(const ExecParams &, const TpccParams &, u32, u32) { return 0u; }
-    static GC_DEV void prefetch_token(const ExecParams &, const TpccParams &y, u32 gid, u32 i, u32) {
-        if (i < 2) prefetch_l2(y.tx + (u64)gid * TPCC_TX_WORDS + 32 * i);   // 160 B: two lines
-    }
+
 
     template <class LA>
     static GC_DEV u32 load_all(const ExecParams &p, const TpccParams &y, u32 gid, LA L) {

@@ -203,26 +203,6 @@ struct YcsbWL {
         return r != ~0ull;
     }
 
-    // tile-mode look-ahead (exec_tile_kernel): only when an access resolves without a memory
-    // probe -- direct addressing, or the record table a3 built -- so the prefetch of a
-    // later transaction's lines costs no dependent round trip
-    static GC_DEV bool lookahead(const ExecParams &p, const YcsbParams &y) {
-        return p.acc_rec != nullptr || is_dense(y.mode);
-    }
-    static GC_DEV u32 token(const ExecParams &p, const YcsbParams &y, u32 gid, u32 i) {
-        if (i >= p.K) return 0u;
-        const u64 a = (u64)gid * p.K + i;
-        return p.acc_rec ? p.acc_rec[a] : y.keys[a];
-    }
-    static GC_DEV void prefetch_token(const ExecParams &p, const YcsbParams &y, u32, u32 i, u32 tok) {
-        if (i >= p.K) return;
-        Lane L;
-        const u64 r = p.acc_rec ? (u64)tok : dense_lookup(y, tok);
-        if (r == ~0ull) return;   // unknown key: load_lane reports it when the transaction runs
-        L.rec = (u32)r;
-        prefetch_access(p, y, L);
-    }
-
     // bring the row (both 64 B halves) and the CC word into L2 while the scheme's ordered
     // accesses to the word are still pending
     static GC_DEV void prefetch_access(const ExecParams &p, const YcsbParams &y, const Lane &L) {

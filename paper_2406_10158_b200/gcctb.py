@@ -35,7 +35,6 @@ CC_FLAG_PART_2PC = 0x800
 CC_FLAG_INDEX_EYTZ = 0x1000
 CC_FLAG_WARM = 0x2000
 CC_FLAG_PART_P2P = 0x4000
-CC_FLAG_NO_LOOKAHEAD = 0x8000
 CC_FLAG_META_PAD = 0x10000
 CC_SRC_HOST_ASYNC = 2
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
@@ -153,6 +152,7 @@ _SIGS = {
     "cc_part_commit": (ctypes.c_int, [_P, _P, _P, ctypes.c_uint64]),
     "cc_part_next": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "cc_roofline_probe": (ctypes.c_int, [_P, ctypes.POINTER(cc_roofline)]),
+    "cc_gather_sweep": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double * 4)]),
     "cc_part_window": (ctypes.c_int, [_P, ctypes.POINTER(cc_ipc_handle)]),
     "cc_part_connect": (ctypes.c_int, [_P, ctypes.POINTER(cc_ipc_handle)]),
     "cc_part_connect_local": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int]),

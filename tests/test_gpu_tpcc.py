@@ -168,17 +168,17 @@ def test_ragged_batches_and_pure_mixes(w4, orc, scheme, n, mix):
     b.free()
 
 
-@pytest.mark.parametrize("mode", ["latched", "immediate", "stages", "binary_index", "meta_pad", "no_lookahead"])
+@pytest.mark.parametrize("mode", ["latched", "immediate", "stages", "binary_index", "meta_pad"])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_w4_parity_flags(w4, orc, scheme, mode):
     """The execution flags change timing / instrumentation only: Exp-7 latched words
     (PAPER.md:836-852), the paper's immediate restart, Exp-6 stage clocks
-    (PAPER.md:473), the paper's binary-search index, the padded control-word layout (f-3)
-    and the executor without look-ahead keep TPC-C serial-replay parity."""
+    (PAPER.md:473), the paper's binary-search index and the padded control-word layout
+    (f-3) keep TPC-C serial-replay parity."""
     from paper_2406_10158_b200 import gcctb as G
     flags = {"latched": G.CC_FLAG_LATCHED, "immediate": G.CC_FLAG_IMMEDIATE_RETRY,
              "stages": G.CC_FLAG_STAGES, "binary_index": G.CC_FLAG_INDEX_BINARY,
-             "meta_pad": G.CC_FLAG_META_PAD, "no_lookahead": G.CC_FLAG_NO_LOOKAHEAD}[mode]
+             "meta_pad": G.CC_FLAG_META_PAD}[mode]
     db, S0 = w4
     b = db.gen_tpcc(2048, 61, 5114)
     for lanes in (1, 32):

@@ -219,16 +219,15 @@ def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta, warm):
     b.free()
 
 
-@pytest.mark.parametrize("mode", ["meta_pad", "no_lookahead", "meta_pad_latched"])
+@pytest.mark.parametrize("mode", ["meta_pad", "meta_pad_latched"])
 @pytest.mark.parametrize("lanes", [1, 16])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_c1_parity_layout_flags(c1, orc, scheme, lanes, mode):
     """CC_FLAG_META_PAD (one control word per 32 B sector, f-3) -- also under latched
-    words, whose latch index follows the word -- and CC_FLAG_NO_LOOKAHEAD change the
-    memory layout / timing only: the same serial-replay parity at configs[0]."""
+    words, whose latch index follows the word -- changes the memory layout only: the
+    same serial-replay parity at configs[0]."""
     from paper_2406_10158_b200 import gcctb as G
-    flags = {"meta_pad": G.CC_FLAG_META_PAD, "no_lookahead": G.CC_FLAG_NO_LOOKAHEAD,
-             "meta_pad_latched": G.CC_FLAG_META_PAD | G.CC_FLAG_LATCHED}[mode]
+    flags = {"meta_pad": G.CC_FLAG_META_PAD, "meta_pad_latched": G.CC_FLAG_META_PAD | G.CC_FLAG_LATCHED}[mode]
     db, S0 = c1
     T = inputs.zipf_thresholds(1024, 0.8)
     A = inputs.scramble_mult(1024)
@@ -617,3 +616,26 @@ def test_generator_failure_is_reported_at_submit(torch_cuda):
     assert db.sync().commits == 32
     ok.free()
     db.close()
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_host_result_buffers(c1, orc, scheme):
+    """cc_result in pinned host memory (results to host or device): the
+    submit stages them on the device and copies them out on the copy stream; after sync
+    they equal a device-buffer run's and pass the oracle check.  Several submits in a row
+    exercise the two alternating staging sets."""
+    from paper_2406_10158_b200.api import Result
+    db, S0 = c1
+    T = inputs.zipf_thresholds(1024, 0.8)
+    A = inputs.scramble_mult(1024)
+    b = db.gen_ycsb(1024, 4, 0.5, 31, T, A)
+    keys, ops = orc.ycsb_gen(31, 1024, 1024, 4, 0.5, T, A)
+    hs = [Result.alloc_host(1024, 4) for _ in range(3)]
+    for h in hs:
+        db.snapshot(False)
+        db.prepare(b, scheme)
+        db.submit(b, scheme, wd=0, bs=8, lanes=16, result=h)
+        assert db.sync().commits == 1024
+        orc.check_ycsb(scheme, S0, keys, ops, 4, h.host(), db.read_table(0))
+        assert int(h.stats[0]) == 1024
+    b.free()
