@@ -98,7 +98,7 @@ static double sweep_one(cudaStream_t s, int num_sms, const u64 *buf, u64 bytes, 
         cudaEventSynchronize(b);
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
-        const double gbs = (double)threads * 8 * BYTES / (ms * 1e-3) / 1e9;
+        const double gbs = (double)threads * 64 * BYTES / (ms * 1e-3) / 1e9;   // 8 x 8 or 16 x 4 accesses
         best = gbs > best ? gbs : best;
     }
     return best;
