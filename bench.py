@@ -604,9 +604,10 @@ def index_pass(args, db, b, schemes, LA, res, flag):
 # less); 64 warehouses: 8 warps per SM; 512 warehouses: the full grid, GaccO 16 warps per SM.
 TPCC_CONFIGS = [
     {"name": "configs2_1wh_16K_50:50", "W": 1, "n": 16384, "mix": 5000, "launch": {"*": (1, True)}},
-    {"name": "configs3_64wh_64K_45:43", "W": 64, "n": 65536, "mix": 5114, "launch": {"*": (8, True)}},
+    {"name": "configs3_64wh_64K_45:43", "W": 64, "n": 65536, "mix": 5114, "launch": {"*": (8, True)},
+     "meta_pad": True},
     {"name": "configs4_shape_512wh_64K_45:43_1gpu", "W": 512, "n": 65536, "mix": 5114,
-     "launch": {"*": (8, False), "gacco": (16, True)}},
+     "launch": {"*": (8, False), "gacco": (16, True)}, "meta_pad": True},
 ]
 
 
@@ -635,7 +636,7 @@ def tpcc_block(args, local, schemes):
     import torch
 
     from paper_2406_10158_b200.api import DB, Result
-    from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING
+    from paper_2406_10158_b200.gcctb import CC_FLAG_META_PAD, CC_FLAG_TIMING
     dev = torch.device("cuda", local)
     peaks = load_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
@@ -646,6 +647,8 @@ def tpcc_block(args, local, schemes):
         res = Result.alloc(cfg["n"], 18, dev, stream=db.stream, out_words=48)
         per = {}
         tot_ms, tot_commits = 0.0, 0
+        # one control word per 32 B sector where it measured faster (profiles/r02_probe_meta_pad.jsonl)
+        flags = CC_FLAG_TIMING | (CC_FLAG_META_PAD if cfg.get("meta_pad") else 0)
         for s in schemes:
             bs, per_sm = cfg["launch"].get(s, cfg["launch"]["*"])
             la = {"bs": bs, "grid": db.num_sms if per_sm else 0}
@@ -656,7 +659,7 @@ def tpcc_block(args, local, schemes):
                 if r == 3:
                     alg = tpcc_alg_bytes(b.export_tpcc())
                 db.timing(reset=True)
-                db.submit(b, s, **la, lanes=32, flags=CC_FLAG_TIMING, result=res, watchdog_s=120)
+                db.submit(b, s, **la, lanes=32, flags=flags, result=res, watchdog_s=120)
                 st = db.sync()
                 pm, _ = db.timing(reset=True)
                 b.free()
@@ -676,6 +679,7 @@ def tpcc_block(args, local, schemes):
             tot_commits += cfg["n"]
         out[cfg["name"]] = {"value": tot_commits / (tot_ms / 1e3), "unit": "txn/s", "warehouses": cfg["W"],
                             "batch": cfg["n"], "neworder_permyriad": cfg["mix"], "lanes_per_txn": 32,
+                            "meta_pad": bool(cfg.get("meta_pad")),
                             "per_scheme": per}
         db.close()
         del res

@@ -273,6 +273,10 @@ cc_status cc_batch_export_tpcc(cc_db db, cc_batch b, uint32_t *tx);
                                         packed 8 B words (the north star's metadata padded against
                                         false sharing in L2).  Same results;
                                         measured per workload */
+#define CC_FLAG_L2_PERSIST 0x8000u   /* ablation: an L2 access-policy window (persisting) over the
+                                        control words during the executor; reserves the device's
+                                        persisting L2 set-aside on first use (measured
+                                        slower on the bench).  Same results */
 #define CC_FLAG_PART_P2P 0x4000u     /* with CC_FLAG_PARTITIONED (deterministic phase B): the exchange
                                         runs inside the library over peer memory -- requests and
                                         responses are stored straight into the peers' exchange

@@ -178,6 +178,8 @@ struct cc_db_s {
     cudaEvent_t copy_after = nullptr;     // orders an async import after the db stream's work
     int rank = 0, world = 1;
     int num_sms = 148;
+    size_t persist_l2 = 0;     // L2 set aside for persisting accesses (the control words), bytes
+    size_t max_window = 0;     // largest access-policy window
     std::string err;
     cc_status sticky = CC_OK;
     std::vector<Table> tables;
@@ -1192,6 +1194,37 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.meta_stride = (scheme != CC_MVCC && (desc->flags & CC_FLAG_META_PAD)) ? GC_META_PAD_WORDS : 1u;
     p.meta_shift = p.meta_stride == 1 ? 0u : 2u;
     static_assert(GC_META_PAD_WORDS == 4, "meta_shift assumes 4 words per padded record");
+    // CC_FLAG_L2_PERSIST (ablation, off by default): an access-policy window marks the
+    // scheme's word array persisting and everything else streaming from the a2 reset until
+    // after the executor (a random 8 B word otherwise costs a ~128 B DRAM fetch, profiles/
+    // r02_gather_sweep.md).  Measured a loss on the bench (profiles/r02_l2_persist.md): the
+    // set-aside shrinks L2 for the other kernels, and persisting lines outlive the window
+    // (and an L2 flush), so a back-to-back gain is partly stale warm lines.
+    bool persist = false;
+    if ((desc->flags & CC_FLAG_L2_PERSIST) && !det) {
+        if (!db->persist_l2) {   // device-wide set-aside, reserved on first use
+            int pmax = 0, wmax = 0;
+            cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, db->device);
+            cudaDeviceGetAttribute(&wmax, cudaDevAttrMaxAccessPolicyWindowSize, db->device);
+            if (pmax > 0 && wmax > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)pmax) == cudaSuccess) {
+                db->persist_l2 = (size_t)pmax;
+                db->max_window = (size_t)wmax;
+            }
+            cudaGetLastError();
+        }
+        persist = db->persist_l2 > 0;
+    }
+    if (persist) {
+        const uint64_t words = scheme == CC_MVCC ? 2 * db->n_records : (uint64_t)db->n_records * p.meta_stride;
+        cudaStreamAttrValue a{};
+        a.accessPolicyWindow.base_ptr = db->meta;
+        a.accessPolicyWindow.num_bytes = (size_t)(words * 8 < db->max_window ? words * 8 : db->max_window);
+        const double ratio = (double)db->persist_l2 / (double)a.accessPolicyWindow.num_bytes;
+        a.accessPolicyWindow.hitRatio = (float)(ratio < 1.0 ? ratio : 1.0);
+        a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        CUDA_TRY(db, cudaStreamSetAttribute(db->stream, cudaStreamAttributeAccessPolicyWindow, &a));
+    }
     // (GaccO / GPUTx keep no per-record control word: their cursors and K-set counters are
     // reset by a3, so only the ring and the control block are cleared for them)
     CUDA_TRY(db, launch_reset_meta(scheme, db->meta, det ? 0 : db->n_records, db->ring, db->ring_cap,
@@ -1291,6 +1324,11 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     if (is_tpcc) CUDA_TRY(db, launch_tpcc_exec(p, tp, grid, block, smem, db->stream));
     else CUDA_TRY(db, launch_ycsb_exec(p, y, grid, block, smem, db->stream));
+    if (persist) {
+        cudaStreamAttrValue a{};
+        a.accessPolicyWindow.num_bytes = 0;   // later work on the stream: normal caching
+        CUDA_TRY(db, cudaStreamSetAttribute(db->stream, cudaStreamAttributeAccessPolicyWindow, &a));
+    }
     if (p.stages) CUDA_TRY(db, launch_stages_reduce(p.stages, (uint64_t)grid * block, db->stream));
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
     if (partitioned && p2p) {   // phase B through the windows, then a7: the submit is complete

@@ -35,6 +35,7 @@ CC_FLAG_PART_2PC = 0x800
 CC_FLAG_INDEX_EYTZ = 0x1000
 CC_FLAG_WARM = 0x2000
 CC_FLAG_PART_P2P = 0x4000
+CC_FLAG_L2_PERSIST = 0x8000
 CC_FLAG_META_PAD = 0x10000
 CC_SRC_HOST_ASYNC = 2
 STAGES = ["index", "ts_alloc", "wait", "cc_manager", "abort", "useful", "attempts"]
