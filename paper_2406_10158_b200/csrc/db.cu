@@ -904,6 +904,7 @@ static cudaError_t alloc_prep(PrepBufs &b, std::vector<void *> &allocs, uint64_t
     PTRY(A(&b.acc_rec, na * 4));
     PTRY(A(&b.acc_seg, na * 4));
     PTRY(A(&b.acc_pos, na * 4));
+    PTRY(A(&b.acc_rdy, na * 4));
     PTRY(A(&b.sorted_pos, na * 4));
     PTRY(A(&b.head_flag, na * 4));
     PTRY(A(&b.seg_id, na * 4));
@@ -1275,6 +1276,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         p.acc_rec = pb->acc_rec;
         p.acc_seg = pb->acc_seg;
         p.acc_pos = pb->acc_pos;
+        p.acc_rdy = pb->acc_rdy;
         p.cursor = pb->cursor;
         p.rank_order = pb->rank_order;
         p.rank_of = pb->rank;

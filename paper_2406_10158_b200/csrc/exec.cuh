@@ -331,13 +331,15 @@ GC_DEV void abort_backoff(const ExecParams &p, u32 gid, u32 restarts) {
 #ifndef GC_GACCO_MAX_SLEEP_NS
 #define GC_GACCO_MAX_SLEEP_NS 50000u
 #endif
-GC_DEV bool gacco_turn(Th &th, u32 *cur, u32 pos) {
+// Wait until the item's cursor has reached `target` (the cursor only grows, one hand-off at
+// a time; it never passes our own position before we release it).
+GC_DEV bool gacco_reach(Th &th, u32 *cur, u32 target) {
     u32 c = ld_acquire32(cur);
-    if (c == pos) return true;
+    if ((int)(target - c) <= 0) return true;
     const u64 t0 = th.timing ? clk64() : 0;
     bool ok = true;
-    while (pos - c > 1) {   // the cursor never passes pos before we release it
-        const u32 d = pos - c - 1;
+    while ((int)(target - c) > 1) {
+        const u32 d = target - c - 1;
         const u32 ns = d * GC_GACCO_HOP_NS;
         __nanosleep(ns < GC_GACCO_MAX_SLEEP_NS ? ns : GC_GACCO_MAX_SLEEP_NS);
         if (dead(th)) { ok = false; break; }
@@ -346,8 +348,35 @@ GC_DEV bool gacco_turn(Th &th, u32 *cur, u32 pos) {
     if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
     if (!ok) return false;
     Spin sp(GC_GACCO_SPIN);
-    while (ld_acquire32(cur) != pos)   // the poll that sees our turn is the acquire
+    while ((int)(target - ld_acquire32(cur)) > 0)   // the poll that sees it is the acquire
         if (!sp.wait(th)) return false;
+    return true;
+}
+
+// One GaccO access: it owns the item from its turn (cursor == pos) until it
+// advances the cursor.  Its row read is hoisted to the moment the item's last earlier write
+// has installed (cursor >= rdy, acc_rdy from a3): only reads sit between that write and
+// this access, so the row then already holds what the access reads at its turn.  The turn,
+// the install and the hand-off stay in queue order; what leaves the hand-off chain's
+// critical path is the row read (an L2 round trip per hop on a read-hot item).
+// GC_GACCO_HOIST=0 reads at the turn (ablation).
+#ifndef GC_GACCO_HOIST
+#define GC_GACCO_HOIST 1
+#endif
+template <class WL>
+GC_DEV bool gacco_access(Th &th, const typename WL::Params &y, typename WL::Lane &L, u32 gid, u32 i,
+                         u32 *cur, u32 pos, u32 rdy) {
+    u64 *row = WL::row(y, L);
+    if (GC_GACCO_HOIST) {
+        if (!gacco_reach(th, cur, rdy)) return false;
+        rd<WL>(th, y, L, gid, i, row);
+        if (!gacco_reach(th, cur, pos)) return false;
+    } else {
+        if (!gacco_reach(th, cur, pos)) return false;
+        rd<WL>(th, y, L, gid, i, row);
+    }
+    if (L.w) inst<WL>(th, y, L, row);
+    st_release32(cur, pos + 1);
     return true;
 }
 
@@ -1022,13 +1051,8 @@ GC_DEV int run_thread(Th &th, u32 gid, LA L, u32 n, const typename WL::Params &y
         // wait for the turn, access, advance the cursor (release after the op, Z3)
         const u64 base = (u64)gid * p.K;
         for (u32 i = 0; i < n; i++) {
-            const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i];
-            u32 *cur = &p.cursor[seg];
-            if (!gacco_turn(th, cur, pos)) return RES_FATAL;
-            u64 *row = WL::row(y, L[i]);
-            rd<WL>(th, y, L[i], gid, i, row);
-            if (L[i].w) inst<WL>(th, y, L[i], row);
-            st_release32(cur, pos + 1);
+            const u32 seg = p.acc_seg[base + i], pos = p.acc_pos[base + i], rdy = p.acc_rdy[base + i];
+            if (!gacco_access<WL>(th, y, L[i], gid, i, &p.cursor[seg], pos, rdy)) return RES_FATAL;
         }
         key_hi = 0;
         key_lo = gid;
@@ -1328,15 +1352,8 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         int st = ST_DONE;
         if (act) {   // each lane waits for its own item's turn: overlapped across items
             const u64 a = (u64)gid * p.K + li;
-            const u32 seg = p.acc_seg[a], pos = p.acc_pos[a];
-            u32 *cur = &p.cursor[seg];
-            if (!gacco_turn(th, cur, pos)) st = ST_ABORT;
-            if (st == ST_DONE) {
-                u64 *row = WL::row(y, L);
-                rd<WL>(th, y, L, gid, li, row);
-                if (L.w) inst<WL>(th, y, L, row);
-                st_release32(cur, pos + 1);
-            }
+            const u32 seg = p.acc_seg[a], pos = p.acc_pos[a], rdy = p.acc_rdy[a];
+            if (!gacco_access<WL>(th, y, L, gid, li, &p.cursor[seg], pos, rdy)) st = ST_ABORT;
         }
         if (tile.any(st != ST_DONE)) return RES_FATAL;
         key_hi = 0;

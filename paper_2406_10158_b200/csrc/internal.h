@@ -80,6 +80,8 @@ struct ExecParams {
     const uint32_t *acc_rec;     // resolved record of each access (n_txn*K) or null
     const uint32_t *acc_seg;     // GaccO: segment (item) id of each access
     const uint32_t *acc_pos;     // GaccO: queue position of each access
+    const uint32_t *acc_rdy;     // GaccO: cursor value at which the item's last earlier write
+                                 // has installed (0: none before it in the queue)
     uint32_t *cursor;            // GaccO: per-segment owner cursor
     const uint32_t *rank_order;  // GPUTx: transactions sorted by rank
     const uint32_t *rank_of;     // GPUTx: rank of each transaction
@@ -134,7 +136,7 @@ struct YcsbParams {
 // Deterministic-scheme preprocessing buffers (a3), sized n_acc = n_txn*K.
 struct PrepBufs {
     unsigned long long *keys_in, *keys_out;   // (rec << 27) | (gid << 6) | (i << 1) | w
-    uint32_t *acc_rec, *acc_seg, *acc_pos, *sorted_pos;
+    uint32_t *acc_rec, *acc_seg, *acc_pos, *acc_rdy, *sorted_pos;
     uint32_t *head_flag;   // scan input: p at a segment head, else 0
     uint32_t *lw;          // scan input: p + 1 at a write, else 0
     uint32_t *seg_start;   // per sorted position: first position of its item's segment

@@ -81,9 +81,13 @@ __global__ void a3_marks_kernel(const u64 *keys, uint32_t *head_at, uint32_t *wr
 
 // GaccO lock table: queue position of each access inside its item's segment
 // ("recording which transaction currently owns each data item").  An item's
-// segment is named by its first sorted position, which also indexes its cursor.
-__global__ void positions_kernel(const u64 *keys, const uint32_t *seg_of, uint32_t K, uint32_t *acc_seg,
-                                 uint32_t *acc_pos, uint32_t *sorted_pos, uint32_t *cursor, uint64_t n) {
+// segment is named by its first sorted position, which also indexes its cursor.  acc_rdy:
+// the cursor value at which the last earlier write of the item has installed (its queue
+// position + 1; 0 if no write precedes the access): from then on the row holds exactly what
+// the access would read at its turn, since only reads sit between that write and it.
+__global__ void positions_kernel(const u64 *keys, const uint32_t *seg_of, const uint32_t *lw_scan,
+                                 uint32_t K, uint32_t *acc_seg, uint32_t *acc_pos, uint32_t *acc_rdy,
+                                 uint32_t *sorted_pos, uint32_t *cursor, uint64_t n) {
     const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const u64 k = keys[p];
@@ -92,6 +96,8 @@ __global__ void positions_kernel(const u64 *keys, const uint32_t *seg_of, uint32
     const uint32_t seg = seg_of[p];
     acc_seg[a] = seg;
     acc_pos[a] = (uint32_t)p - seg;
+    const uint32_t q = p > seg ? lw_scan[p - 1] : 0u;   // last write before p, + 1
+    acc_rdy[a] = q > seg ? q - seg : 0u;
     sorted_pos[a] = (uint32_t)p;
     if (seg == (uint32_t)p) cursor[p] = 0u;
 }
@@ -246,7 +252,8 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     a3_marks_kernel<<<g, blk, 0, s>>>(sk, b.head_flag, b.lw, n);
     e = gc_scan_max2(b.head_flag, b.lw, b.seg_start, b.seg_id, n, b.cub_tmp, b.cub_bytes, s);
     if (e) return e;
-    positions_kernel<<<g, blk, 0, s>>>(sk, b.seg_start, p.K, b.acc_seg, b.acc_pos, b.sorted_pos, b.cursor, n);
+    positions_kernel<<<g, blk, 0, s>>>(sk, b.seg_start, b.seg_id, p.K, b.acc_seg, b.acc_pos, b.acc_rdy,
+                                       b.sorted_pos, b.cursor, n);
     if (!gputx) return cudaGetLastError();
     fill_u32_kernel<<<(p.n_txn + blk - 1) / blk, blk, 0, s>>>(b.rank, RANK_UNSET, p.n_txn);
     // experiment knobs (environment): poll cap and a grid divisor for the rank pass
