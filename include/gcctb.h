@@ -459,6 +459,14 @@ cc_status cc_part_connect_local(cc_db *dbs, int n);
 cc_status cc_events_capacity(cc_db db, uint64_t cap);
 cc_status cc_events_read(cc_db db, void *dst, uint64_t cap, uint64_t *n_events);
 
+/* Make the db stream wait (on the device; the host does not block) for the library's
+ * background work enqueued so far: the zeroing of the CC words a submit used, which runs
+ * on a reset stream beside the next submit (the a2 of PAPER.md:472, Z19, off the critical
+ * path).  A CUDA event recorded on the db stream after cc_join covers all of it -- what a
+ * caller timing a sequence of submits wants.  Submits order themselves; cc_sync waits for
+ * everything.  CUDA on a launch error. */
+cc_status cc_join(cc_db db);
+
 /* Wait for the db stream; surface asynchronous errors -- the first device error of any
  * submit since the previous cc_sync (sticky across submits); if st != NULL copy the stats
  * of the last submit into it. */

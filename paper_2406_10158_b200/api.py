@@ -369,6 +369,11 @@ class DB:
             raise RuntimeError(f"event log overflow: {n.value} events > capacity {cap}")
         return buf[:n.value]
 
+    def join(self) -> None:
+        """The db stream waits (on the device) for the library's background zeroing of CC
+        words, so an event recorded after it covers every submit so far (cc_join)."""
+        self._chk(G.lib().cc_join(self.h))
+
     def sync(self) -> G.cc_stats:
         s = G.cc_stats()
         self._chk(G.lib().cc_sync(self.h, ctypes.byref(s)))

@@ -33,7 +33,12 @@ def _deps():
     return files
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: str = "") -> str:
+    """Build the shipped library in-tree; with `out`, an experiment variant (extra nvcc
+    flags, e.g. "-DGC_GACCO_HOIST=0") at that path instead -- the in-tree library, its
+    stamp and ptxas.log are left alone.  Load a variant with GCCTB_LIB=<path>."""
+    if out:
+        return _build_variant(out, extra.split())
     same_flags = os.path.exists(STAMP) and open(STAMP).read().strip() == _flags_id()
     if not force and os.path.exists(LIB) and same_flags:
         mt = os.path.getmtime(LIB)
@@ -70,6 +75,34 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def _build_variant(out: str, extra: list) -> str:
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    tag = os.path.splitext(os.path.basename(out))[0]
+    objs, procs = [], []
+    for s in SOURCES:
+        obj = os.path.join(os.path.dirname(os.path.abspath(out)), f"{tag}_{s.replace('.cu', '.o')}")
+        cmd = [NVCC] + [f for f in FLAGS if f != "-shared"] + extra + ["-c", os.path.join(CSRC, s), "-o", obj]
+        procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+        objs.append(obj)
+    log = []
+    for s, p in procs:
+        o, _ = p.communicate()
+        log.append(o.decode())
+        if p.returncode != 0:
+            sys.stderr.write(o.decode())
+            raise RuntimeError(f"nvcc failed on {s}")
+    with open(out + ".ptxas.log", "w") as f:
+        f.write("\n".join(l for l in "\n".join(log).splitlines() if "Compile time" not in l) + "\n")
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out] + objs)
+    for o in objs:
+        os.remove(o)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="-f" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--out" in sys.argv:   # python build.py --out variants/x.so "-DFOO=1 -DBAR=0"
+        i = sys.argv.index("--out")
+        print(build(out=sys.argv[i + 1], extra=sys.argv[i + 2] if len(sys.argv) > i + 2 else ""))
+    else:
+        build(force="-f" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

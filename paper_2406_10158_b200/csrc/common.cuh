@@ -82,6 +82,12 @@ GC_DEV u32 atom_add_release32(u32 *p, u32 v) {
                  : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+GC_DEV u32 atom_add_acqrel32(u32 *p, u32 v) {
+    u32 old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 GC_DEV void fence_acqrel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 GC_DEV void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
 

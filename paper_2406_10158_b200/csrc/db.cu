@@ -16,8 +16,6 @@ namespace gcctb {
 cudaError_t launch_part_all(const TpccParams &y, uint32_t rank, uint32_t world, uint32_t wpr, uint32_t n_txn,
                             uint8_t *skip, unsigned long long *cnt, unsigned long long *off,
                             unsigned long long *cursor, PartReq *out, cudaStream_t s);
-cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, unsigned long long *ohi,
-                            unsigned long long *olo, uint32_t n, cudaStream_t s);
 int rank_kernel_grid();
 }  // namespace gcctb
 
@@ -191,8 +189,17 @@ struct cc_db_s {
     Event *events = nullptr;            // CC_FLAG_EVENTS log
     uint64_t events_cap = 0;
     int clock_khz = 0;
-    u64 *meta = nullptr;
+    u64 *meta = nullptr;                 // meta_buf[0]
     uint64_t meta_records = 0;
+    // a2 off the critical path: two sets of CC words.  A submit executes on one set while
+    // the set its predecessor used is zeroed on reset_stream (every scheme's initial words
+    // are zeros); a partitioned submit leaves its set dirty, zeroed in stream before reuse.
+    u64 *meta_buf[2] = {nullptr, nullptr};
+    int meta_cur = 0;
+    uint64_t meta_dirty[2] = {0, 0};          // words to zero in stream before the next use
+    bool meta_cleaning[2] = {false, false};   // a zeroing on reset_stream is in flight
+    cudaEvent_t meta_used[2] = {nullptr, nullptr}, meta_clean[2] = {nullptr, nullptr};
+    cudaStream_t reset_stream = nullptr;
     int ycsb_table = -1, ycsb_index = -1;
     TpccState tpcc;
     struct Part {
@@ -331,6 +338,11 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
         return CC_ERR_CUDA;
     }
     if (cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&db->reset_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&db->meta_used[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&db->meta_used[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&db->meta_clean[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&db->meta_clean[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&db->copy_after, cudaEventDisableTiming) != cudaSuccess) {
         delete db;
         return CC_ERR_CUDA;
@@ -416,7 +428,9 @@ cc_status cc_db_destroy(cc_db db) {
     dfree(db->latch);
     dfree(db->stages);
     dfree(db->events);
-    dfree(db->meta);
+    cudaStreamSynchronize(db->reset_stream);
+    dfree(db->meta_buf[0]);
+    dfree(db->meta_buf[1]);
     dfree(db->ctl);
     dfree(db->stats_scratch);
     dfree(db->sticky_dev);
@@ -425,6 +439,11 @@ cc_status cc_db_destroy(cc_db db) {
     cudaStreamSynchronize(db->copy_stream);
     cudaStreamDestroy(db->copy_stream);
     cudaEventDestroy(db->copy_after);
+    cudaStreamDestroy(db->reset_stream);
+    for (int k = 0; k < 2; k++) {
+        cudaEventDestroy(db->meta_used[k]);
+        cudaEventDestroy(db->meta_clean[k]);
+    }
     delete db;
     return CC_OK;
 }
@@ -447,12 +466,23 @@ static cc_status create_table(cc_db db, const char *name, uint32_t row_bytes, ui
     if (cc) {
         // CC metadata: 2 words per record so MVCC's (lo, hi) pair fits (Table II: 16 B),
         // GC_META_PAD_WORDS words per record for the padded layout (CC_FLAG_META_PAD)
+        // (two sets: see cc_db_s::meta_buf), zeroed: every scheme's initial state
         const uint64_t need = db->n_records + rows;
-        u64 *meta = nullptr;
-        CUDA_TRY(db, dalloc(&meta, need * 8 * GC_META_PAD_WORDS));   // room for the padded layout
+        u64 *mb[2] = {nullptr, nullptr};
+        for (int k = 0; k < 2; k++) {
+            CUDA_TRY(db, dalloc(&mb[k], need * 8 * GC_META_PAD_WORDS));   // room for the padded layout
+            CUDA_TRY(db, cudaMemsetAsync(mb[k], 0, need * 8 * GC_META_PAD_WORDS, db->stream));
+        }
         CUDA_TRY(db, cudaStreamSynchronize(db->stream));
-        if (db->meta) dfree(db->meta);
-        db->meta = meta;
+        CUDA_TRY(db, cudaStreamSynchronize(db->reset_stream));
+        for (int k = 0; k < 2; k++) {
+            dfree(db->meta_buf[k]);
+            db->meta_buf[k] = mb[k];
+            db->meta_dirty[k] = 0;
+            db->meta_cleaning[k] = false;
+        }
+        db->meta = mb[0];
+        db->meta_cur = 0;
         db->meta_records = need;
         db->n_records = need;
     }
@@ -883,7 +913,7 @@ static cc_status ensure_scratch(cc_db db, uint32_t n_txn, uint64_t n_acc) {
     CUDA_TRY(db, dalloc(&db->ohi, (size_t)nt * 8));
     CUDA_TRY(db, dalloc(&db->olo, (size_t)nt * 8));
     const uint32_t cap = nt;   // each id is appended to the retry batch at most once
-    CUDA_TRY(db, dalloc(&db->ring, (size_t)cap * 8));
+    CUDA_TRY(db, dalloc(&db->ring, ((size_t)cap + GC_RQ_N) * 8));   // + the retry queues
     db->ring_cap = cap;
     CUDA_TRY(db, alloc_prep(db->prep, db->prep_allocs, na, nt));
     db->cap_txn = nt;
@@ -1126,10 +1156,12 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.watchdog_ns = (u64)((desc->watchdog_s > 0 ? desc->watchdog_s : 30.0) * 1e9);
     p.ctl = db->ctl;
     p.sticky = db->sticky_dev;
-    p.meta = db->meta;
+    const int mk = db->meta_cur;   // the word set this submit executes on
+    p.meta = db->meta_buf[mk];
     p.arena = db->arena;
     p.ring = db->ring;
     p.ring_cap = db->ring_cap;
+    p.rq = db->ring + db->ring_cap;
     p.committed = db->committed;
     p.restarts = db->restarts;
     p.order_hi = db->ohi;
@@ -1190,6 +1222,12 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         ev = get_events(db);
         CUDA_TRY(db, cudaEventRecord(ev.ev[0], db->stream));
     }
+#if GC_TRACE_COMMIT
+    {   // experiment builds: histogram of commit / abort times (tools/trace_tail.py)
+        const char *tp_ = getenv("GCCTB_TRACE_PTR");
+        p.trace = tp_ ? (unsigned long long *)strtoull(tp_, nullptr, 0) : nullptr;
+    }
+#endif
     // a2: reset CC state (every record of every table)
     p.mvcc_split = (scheme == CC_MVCC && (desc->flags & CC_FLAG_MVCC_SPLIT)) ? db->n_records : 0;
     p.meta_stride = (scheme != CC_MVCC && (desc->flags & CC_FLAG_META_PAD)) ? GC_META_PAD_WORDS : 1u;
@@ -1218,7 +1256,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     if (persist) {
         const uint64_t words = scheme == CC_MVCC ? 2 * db->n_records : (uint64_t)db->n_records * p.meta_stride;
         cudaStreamAttrValue a{};
-        a.accessPolicyWindow.base_ptr = db->meta;
+        a.accessPolicyWindow.base_ptr = p.meta;
         a.accessPolicyWindow.num_bytes = (size_t)(words * 8 < db->max_window ? words * 8 : db->max_window);
         const double ratio = (double)db->persist_l2 / (double)a.accessPolicyWindow.num_bytes;
         a.accessPolicyWindow.hitRatio = (float)(ratio < 1.0 ? ratio : 1.0);
@@ -1228,10 +1266,19 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     // (GaccO / GPUTx keep no per-record control word: their cursors and K-set counters are
     // reset by a3, so only the ring and the control block are cleared for them)
-    CUDA_TRY(db, launch_reset_meta(scheme, db->meta, det ? 0 : db->n_records, db->ring, db->ring_cap,
-                                   db->ctl, db->stream, p.mvcc_split != 0, p.meta_stride));
-    CUDA_TRY(db, launch_zero_txn(db->committed, db->restarts, db->ohi, db->olo, b->n_txn, db->stream));
-    CUDA_TRY(db, launch_merge_word(b->err, db->ctl, db->stream));   // a1 failure: nothing executes
+    // (GaccO / GPUTx keep no per-record control word)
+    if (!det) {
+        if (db->meta_cleaning[mk]) {   // zeroed behind the previous submit on the reset stream
+            CUDA_TRY(db, cudaStreamWaitEvent(db->stream, db->meta_clean[mk], 0));
+            db->meta_cleaning[mk] = false;
+        }
+        if (db->meta_dirty[mk]) {
+            CUDA_TRY(db, cudaMemsetAsync(p.meta, 0, db->meta_dirty[mk] * 8, db->stream));
+            db->meta_dirty[mk] = 0;
+        }
+    }
+    CUDA_TRY(db, launch_a2(db->ring, db->ring_cap + GC_RQ_N, db->ctl, db->committed, db->restarts, db->ohi,
+                           db->olo, b->n_txn, b->err, db->stream));   // a1 failure: nothing executes
     {   // test hook (not part of the ABI): the TO / MVCC timestamp counter starts at
         // GCCTB_TS_BASE instead of 0, so the 31-bit overflow path is reachable
         const char *tb = getenv("GCCTB_TS_BASE");
@@ -1330,6 +1377,19 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         cudaStreamAttrValue a{};
         a.accessPolicyWindow.num_bytes = 0;   // later work on the stream: normal caching
         CUDA_TRY(db, cudaStreamSetAttribute(db->stream, cudaStreamAttributeAccessPolicyWindow, &a));
+    }
+    if (!det) {   // this word set is zeroed for its next user while the next submit runs on the other
+        const uint64_t words = scheme == CC_MVCC ? 2 * db->n_records : db->n_records * p.meta_stride;
+        if (partitioned) {
+            db->meta_dirty[mk] = words;   // phase B may still use it; zeroed in stream at reuse
+        } else {
+            CUDA_TRY(db, cudaEventRecord(db->meta_used[mk], db->stream));
+            CUDA_TRY(db, cudaStreamWaitEvent(db->reset_stream, db->meta_used[mk], 0));
+            CUDA_TRY(db, cudaMemsetAsync(p.meta, 0, words * 8, db->reset_stream));
+            CUDA_TRY(db, cudaEventRecord(db->meta_clean[mk], db->reset_stream));
+            db->meta_cleaning[mk] = true;
+            db->meta_cur = mk ^ 1;
+        }
     }
     if (p.stages) CUDA_TRY(db, launch_stages_reduce(p.stages, (uint64_t)grid * block, db->stream));
     if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
@@ -1722,9 +1782,17 @@ static cc_status drain_timing(cc_db db) {
     return CC_OK;
 }
 
+cc_status cc_join(cc_db db) {
+    CHECK_DB(db);
+    for (int k = 0; k < 2; k++)
+        if (db->meta_cleaning[k]) CUDA_TRY(db, cudaStreamWaitEvent(db->stream, db->meta_clean[k], 0));
+    return CC_OK;
+}
+
 cc_status cc_sync(cc_db db, cc_stats *out) {
     CHECK_DB(db);
     CUDA_TRY(db, cudaStreamSynchronize(db->stream));
+    CUDA_TRY(db, cudaStreamSynchronize(db->reset_stream));
     CUDA_TRY(db, cudaStreamSynchronize(db->copy_stream));   // host-memory results of the submits
     CUDA_TRY(db, cudaGetLastError());
     u64 w[CC_STATS_WORDS];

@@ -58,6 +58,8 @@ struct Th {
     u64 *cw;   // lock word whose holder caused the last abort (nullptr: none)
     u64 cv;    // wait until (*cw & cv) == 0: the conflicting lock is free
     u32 hot;   // tile mode: 1 + lane of the lock that caused this transaction's last abort
+    u64 *turn; // GC_RETRY_FIFO: the retry queue whose turn this worker holds (nullptr: none)
+    bool cw_ex;   // the access that died on *cw wanted it exclusively (a write)
     u64 a_t0, a_u0, a_w0, a_s0;   // CC_FLAG_STAGES: the current attempt's start snapshot
     Claim cl;                     // the worker's claim state (leader lane in tile mode)
 };
@@ -407,22 +409,45 @@ GC_DEV bool kset_near(Th &th, const ExecParams &p, u32 k) {
     if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
     return ok;
 }
+// GC_KSET_KDONE=1: the gate polls ctl->kdone, which only each K-set's last finisher
+// writes (one release store after its acq_rel count increment, which reads from every
+// earlier finisher's release increment), instead of the K-set's counter rank_done[k-1]:
+// with the counter polled, a K-set's few hundred waiters loaded the very word its
+// finishers were incrementing.  Measured slower (configs[1] bench launch, theta 0.6: 1.47 ->
+// 1.54 ms per submit, theta 0.8: 15.8 -> 16.6 ms; profiles/r02_probe_kset_kdone.log): the
+// finisher's extra store is on the chain.  0 (default): poll the counter.
+#ifndef GC_KSET_KDONE
+#define GC_KSET_KDONE 0
+#endif
 GC_DEV bool kset_wait(Th &th, const ExecParams &p, u32 k) {
     const u64 t0 = th.timing ? clk64() : 0;
     bool ok = true;
     // acquire polls: the one that sees K-set k-1 complete orders its installs before our
     // accesses (no fence after the wait)
-    while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1]) {
-        const u64 done = ld_relaxed(&p.ctl->kdone.v);
-        __nanosleep(kset_sleep_ns(k > done ? k - done : 1));
-        if (dead(th)) { ok = false; break; }
+    if (GC_KSET_KDONE) {
+        u64 done;
+        while ((done = ld_acquire(&p.ctl->kdone.v)) < k) {
+            __nanosleep(kset_sleep_ns(k - done));
+            if (dead(th)) { ok = false; break; }
+        }
+    } else {
+        while (ld_acquire32(&p.rank_done[k - 1]) < p.rank_count[k - 1]) {
+            const u64 done = ld_relaxed(&p.ctl->kdone.v);
+            __nanosleep(kset_sleep_ns(k > done ? k - done : 1));
+            if (dead(th)) { ok = false; break; }
+        }
     }
     if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
     return ok;
 }
 GC_DEV void kset_done(const ExecParams &p, u32 k) {
-    const u32 old = atom_add_release32(&p.rank_done[k], 1u);
-    if (old + 1 == p.rank_count[k]) atomicMax(&p.ctl->kdone.v, (u64)k + 1);
+    if (GC_KSET_KDONE) {
+        const u32 old = atom_add_acqrel32(&p.rank_done[k], 1u);
+        if (old + 1 == p.rank_count[k]) st_release(&p.ctl->kdone.v, (u64)k + 1);   // K-sets finish in order
+    } else {
+        const u32 old = atom_add_release32(&p.rank_done[k], 1u);
+        if (old + 1 == p.rank_count[k]) atomicMax(&p.ctl->kdone.v, (u64)k + 1);
+    }
 }
 
 // Retry pacing after an abort.  If a held lock caused it, wait -- holding nothing, so
@@ -446,32 +471,88 @@ GC_DEV void kset_done(const ExecParams &p, u32 k) {
 #ifndef GC_JITTER_LO_SHIFT
 #define GC_JITTER_LO_SHIFT 8
 #endif
+// Retry queues (GC_RETRY_FIFO): an exclusive request killed by a held lock (2PL writes, the
+// OCC lock phase) takes a ticket in the FIFO of that lock's control word (hashed, GC_RQ_N queues) and
+// waits -- holding nothing, so no-wait / wait-die / OCC semantics are unchanged -- for its
+// turn, then for the lock to be free, and retries at once, in place; the turn passes on
+// when that attempt ends, committed or not.  The random jitter that keeps a herd of
+// retriers from colliding in lockstep is replaced by an order, so a hot lock's retriers
+// hand it on one after another instead of leaving it idle for a jitter window.  (Readers
+// keep the jitter: queued one at a time they lost the sharing -- YCSB theta 0.6 wait-die
+// 141 -> 73 M txn/s, profiles/r02_probe_fifo_v1.log.)
+#ifndef GC_RETRY_FIFO
+#define GC_RETRY_FIFO 1
+#endif
+// Queue only while at least this many transactions pace after a lock wait (a herd); below
+// it the jitter stays (measured, configs[1] tile 16, profiles/r02_probe_fifo_v5_herd.log:
+// queueing from 64 pacers cost 2PL 10-25 % at theta 0.6-0.8, from 1024 it is neutral there
+// and 2-8x faster at theta 0.99; Silo / TicToc gain from 64 at theta >= 0.8 and are neutral
+// at 0.6).
+#ifndef GC_RQ_HERD_2PL
+#define GC_RQ_HERD_2PL 2048
+#endif
+#ifndef GC_RQ_HERD_OCC
+#define GC_RQ_HERD_OCC 64
+#endif
+#ifndef GC_RQ_TURN_NS
+#define GC_RQ_TURN_NS 1500u   // sleep per turn ahead (about one attempt on a hot lock)
+#endif
+GC_DEV u64 *rq_of(const ExecParams &p, const u64 *w) {
+    const u64 h = ((u64)(uintptr_t)w >> 3) * 0x9E3779B97F4A7C15ull;
+    return p.rq + (h >> 48);   // GC_RQ_N = 2^16
+}
+GC_DEV void rq_release(Th &th) {
+    if (th.turn) {
+        atomicAdd(th.turn, 1ull << 32);
+        th.turn = nullptr;
+    }
+}
+// wait (holding nothing) until the lock that killed the attempt is free, bounded
+GC_DEV void wait_lock_free(Th &th, u32 restarts) {
+    const u32 sh = restarts < 10 ? restarts : 10;
+    const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
+    unsigned ns = 32;
+    while ((ld_relaxed(th.cw) & th.cv) != 0 && globaltimer_ns() < limit) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+    }
+}
 template <int S>
 GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
     if (th.cw) {
-        u32 jcap = GC_JITTER_MAX_SHIFT;
-        if (GC_JITTER_LO > 0) {
-            const u64 n = atomicAdd(&th.p->ctl->pacing_lk.v, 1ull);   // pacing after a lock wait now
-            if (n < (u64)GC_JITTER_LO) jcap = GC_JITTER_LO_SHIFT;
+        // how many transactions pace after a lock wait right now (this one included)
+        const u64 n = (GC_JITTER_LO > 0 || GC_RETRY_FIFO) ? atomicAdd(&th.p->ctl->pacing_lk.v, 1ull) : 0ull;
+        const bool flat = (th.p->flags & CC_FLAG_FLAT_JITTER) != 0;
+        constexpr u64 HERD = (S == CC_TPL_NW || S == CC_TPL_WD) ? GC_RQ_HERD_2PL : GC_RQ_HERD_OCC;
+        if (GC_RETRY_FIFO && th.cw_ex && n >= HERD && !flat) {   // a herd: queue
+            u64 *q = rq_of(*th.p, th.cw);
+            const u64 old = atomicAdd(q, 1ull);
+            const u32 t = (u32)old;
+            u32 sv = (u32)(old >> 32);
+            while (sv != t) {   // far waiters sleep in proportion to the turns ahead,
+                const u32 d = t - sv;   // the next in line polls
+                const u32 ns = d > 30u ? 50000u : (d - 1) * GC_RQ_TURN_NS;
+                __nanosleep(ns < 64u ? 64u : ns);
+                if (dead(th)) break;
+                sv = (u32)(ld_relaxed(q) >> 32);
+            }
+            th.turn = q;   // held through the next attempt (in place), released after it
+            wait_lock_free(th, restarts);
+        } else {
+            const u32 jcap = (GC_JITTER_LO > 0 && n < (u64)GC_JITTER_LO) ? (u32)GC_JITTER_LO_SHIFT
+                                                                         : (u32)GC_JITTER_MAX_SHIFT;
+            wait_lock_free(th, restarts);
+            // then a random delay whose window doubles per restart: waiters released by
+            // the same unlock must not retry in lockstep (a herd livelock at theta >= 0.9)
+            const u32 win = flat ? 256u : 32u << (restarts < jcap ? restarts : jcap);
+            u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % win);
+            while (d > 0) {
+                const u32 s = d < 1000u ? d : 1000u;
+                __nanosleep(s);
+                d -= s;
+            }
         }
-        const u32 sh = restarts < 10 ? restarts : 10;
-        const u64 limit = globaltimer_ns() + (64ull << sh) + 1000ull;
-        unsigned ns = 32;
-        while ((ld_relaxed(th.cw) & th.cv) != 0 && globaltimer_ns() < limit) {
-            __nanosleep(ns);
-            ns = ns < 256 ? ns * 2 : 256;
-        }
-        // then a random delay whose window doubles per restart: waiters released by
-        // the same unlock must not retry in lockstep (a herd livelock at theta >= 0.9)
-        const u32 win = (th.p->flags & CC_FLAG_FLAT_JITTER) ? 256u
-                                                               : 32u << (restarts < jcap ? restarts : jcap);
-        u32 d = (u32)(mix64(((u64)gid << 32) | restarts) % win);
-        while (d > 0) {
-            const u32 s = d < 1000u ? d : 1000u;
-            __nanosleep(s);
-            d -= s;
-        }
-        if (GC_JITTER_LO > 0) atomicAdd(&th.p->ctl->pacing_lk.v, (u64)-1ll);
+        if (GC_JITTER_LO > 0 || GC_RETRY_FIFO) atomicAdd(&th.p->ctl->pacing_lk.v, (u64)-1ll);
         th.cw = nullptr;
         return;
     }
@@ -598,10 +679,20 @@ constexpr u32 TO_SEQ_AFTER = GC_TO_SEQ_AFTER;
 // needlessly (measured, YCSB tile 16: every writer at once: theta 0.6 96M -> 53M txn/s;
 // dying writers after 8 restarts: theta 0.8 6.1M -> 1.9M).
 constexpr u32 TPL_INTENT_AFTER = 32;
+// no-wait writer intent (experiment): a writer that has died this often on a shared-held
+// lock announces itself too, and new readers then die on the announced lock so it drains
+// (0: off -- readers never conflict with an announcement under no-wait)
+#ifndef GC_NW_INTENT_AFTER
+#define GC_NW_INTENT_AFTER 0
+#endif
 #ifndef GC_WD_SEQ_AFTER
 #define GC_WD_SEQ_AFTER 0
 #endif
 
+template <bool WD>
+GC_DEV bool tpl_intent(u32 attempt) {
+    return WD ? attempt >= TPL_INTENT_AFTER : (GC_NW_INTENT_AFTER > 0 && attempt >= (u32)GC_NW_INTENT_AFTER);
+}
 template <bool WD>
 GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, bool intent) {
     u64 v = ld_relaxed(w);
@@ -613,7 +704,7 @@ GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, boo
             conflict = cnt != 0;
             nv = tpl_make(false, 1, age);
         } else {
-            conflict = cnt != 0 && (!(v & TPL_S) || (WD && (v & TPL_WW)));
+            conflict = cnt != 0 && (!(v & TPL_S) || ((WD || GC_NW_INTENT_AFTER > 0) && (v & TPL_WW)));
             nv = cnt == 0 ? tpl_make(true, 1, age) : tpl_make(true, cnt + 1, min(age, tpl_holder(v)));
         }
         if (conflict) {
@@ -621,7 +712,7 @@ GC_DEV int tpl_try(const ExecParams &p, u64 *w, bool ex, u32 age, u64 &seen, boo
             // (smaller age) waits, a younger one dies.
             seen = v;
             const bool wait = WD && age < tpl_holder(v);
-            if (WD && (wait || intent) && ex && (v & TPL_S) && !(v & TPL_WW)) {   // writer intent (TPL_WW)
+            if ((WD ? (wait || intent) : intent) && ex && (v & TPL_S) && !(v & TPL_WW)) {   // writer intent (TPL_WW)
                 const u64 old = w_cas_acq(p, w, v, v | TPL_WW);
                 if (old != v) { v = old; continue; }
             }
@@ -652,10 +743,11 @@ GC_DEV u64 to_make(bool pend, u64 rts, u64 wts) {
 // ------------------------------------------------------------------ MVCC (Table II)
 // meta[2r]   lo = TO word (pending | RTS | WTS); while pending WTS = pending writer ts
 // meta[2r+1] hi = version pointer word: [63:32] begin ts of the in-place head version,
-//                 [31:0] arena index of the previous version (NONE = 0xFFFFFFFF).
+//                 [31:0] 1 + arena index of the previous version (0: none), so the
+//                 initial state of every scheme's words is all zeros.
 // History nodes (one per write op of the batch): word0 = the hi word
 // of the version they replaced ((begin << 32) | prev), word1 = 0, then the row content.
-constexpr u64 VNONE = 0xFFFFFFFFull;
+constexpr u64 VIDX = 0xFFFFFFFFull;   // hi / node word: 1 + previous node index, 0 = none
 
 // ------------------------------------------------------------------ OCC (Table II)
 constexpr u64 LOCKB = 1ull << 63;    // Silo: [63] lock | [62:0] TID
@@ -743,15 +835,15 @@ GC_DEV int mvcc_step(Th &th, const ExecParams &p, const typename WL::Params &y, 
         return ST_RETRY;
     }
     // walk the history chain for the newest version with begin <= ts
-    u64 idx = h & VNONE;
-    while (idx != VNONE) {
-        const u64 *node = p.arena + idx * (ARENA_HDR + WL::ROW_WORDS);
+    u64 idx = h & VIDX;
+    while (idx != 0) {
+        const u64 *node = p.arena + (idx - 1) * (ARENA_HDR + WL::ROW_WORDS);
         const u64 h0 = ld_cg(node);
         if ((h0 >> 32) <= ts) {
             rd<WL>(th, y, L, gid, i, node + ARENA_HDR);
             return ST_DONE;
         }
-        idx = h0 & VNONE;
+        idx = h0 & VIDX;
     }
     set_err(p.ctl, CC_ERR_VERSION_EXHAUSTED);
     return ST_ABORT;
@@ -779,7 +871,7 @@ GC_DEV void mvcc_commit(Th &th, const ExecParams &p, const typename WL::Params &
     st_cg(node, ld_relaxed(hi));   // old head -> history node (begin, prev)
     WL::copy_row(L, row, node + ARENA_HDR);
     fence_acqrel();
-    w_store(p, hi, (ts << 32) | nidx);   // publish the history, then install in place
+    w_store(p, hi, (ts << 32) | (nidx + 1));   // publish the history, then install in place
     fence_acqrel();
     inst<WL>(th, y, L, row);
     fence_acqrel();
@@ -904,9 +996,9 @@ GC_DEV int run_thread(Th &th, u32 gid, LA L, u32 n, const typename WL::Params &y
             u64 seen = 0;
             if (warp_lock_loser(Li.rec, Li.w, age)) st = ST_ABORT;   // an older lane of this warp takes it
             else
-                while ((st = tpl_try<WD>(p, cw(p, Li.rec), Li.w, age, seen, th.attempt >= TPL_INTENT_AFTER)) == ST_WAIT)
+                while ((st = tpl_try<WD>(p, cw(p, Li.rec), Li.w, age, seen, tpl_intent<WD>(th.attempt))) == ST_WAIT)
                     if (!sp.wait(th)) { st = -1; break; }
-            if (st == ST_ABORT) { th.cw = cw(p, Li.rec); th.cv = M31 << 31; }   // until free
+            if (st == ST_ABORT) { th.cw = cw(p, Li.rec); th.cv = M31 << 31; th.cw_ex = Li.w; }   // until free
             if (st != ST_DONE) { r = st < 0 ? RES_FATAL : RES_ABORT; break; }
             rd<WL>(th, y, Li, gid, i, WL::row(y, Li));   // stable under the lock
         }
@@ -985,6 +1077,7 @@ GC_DEV int run_thread(Th &th, u32 gid, LA L, u32 n, const typename WL::Params &y
                 ok = false;
                 th.cw = cw(p, Li.rec);
                 th.cv = LOCKB;
+                th.cw_ex = true;
                 break;
             }
             if (occ_lock(p, cw(p, Li.rec), pre, seen)) {
@@ -998,7 +1091,7 @@ GC_DEV int run_thread(Th &th, u32 gid, LA L, u32 n, const typename WL::Params &y
                 }
             } else {
                 ok = false;
-                if (seen & LOCKB) { th.cw = cw(p, Li.rec); th.cv = LOCKB; }   // until unlocked
+                if (seen & LOCKB) { th.cw = cw(p, Li.rec); th.cv = LOCKB; th.cw_ex = true; }   // until unlocked
             }
         }
         u64 ticket = 0, cts = 0;
@@ -1088,6 +1181,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel
     th.cw = nullptr;
     th.cv = 0;
     th.hot = 0;
+    th.turn = nullptr;
     stages_init(th, p, true);
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     // the worker's staged read/write set: shared memory, or the global workspace
@@ -1125,6 +1219,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel
             th.attempt = p.restarts[gid];
             AttemptClock ac(th);
             const int r = run_thread<S, WL>(th, gid, L, n, y, kh, kl);
+            rq_release(th);   // GC_RETRY_FIFO: this attempt used its turn
             ac.done(r == RES_OK);
             if (p.events && r != RES_FATAL) log_event(th, 0xFFFFFFFFu, r == RES_OK ? 2u : 3u);
             if (r == RES_OK) {
@@ -1144,7 +1239,8 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel
                 StageClock c(th, STAGE_ABORT);
                 retry_pace<S>(th, gid, nr);
                 if (dead(th)) { stop = true; break; }   // the watchdog also bounds abort-only livelocks
-                if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid)) next = true;   // a6
+                // (a worker that holds a retry-queue turn retries in place)
+                if (!(p.flags & CC_FLAG_IMMEDIATE_RETRY) && !th.turn && try_append_retry(th, gid)) next = true;   // a6
             }
         }
         if (stop) break;
@@ -1187,7 +1283,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             }
             if (mine) {
                 if (warp_lock_loser(L.rec, L.w, age)) st = ST_ABORT;   // an older tile of this warp takes it
-                else st = tpl_try<WD>(p, cw(p, L.rec), L.w, age, seen, th.attempt >= TPL_INTENT_AFTER);
+                else st = tpl_try<WD>(p, cw(p, L.rec), L.w, age, seen, tpl_intent<WD>(th.attempt));
                 held = st == ST_DONE;
             }
             const unsigned dying = tile.ballot(st == ST_ABORT);
@@ -1195,6 +1291,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                 if (held) tpl_release_relaxed(p, cw(p, L.rec), L.w);
                 const int src = __ffs(dying) - 1;   // remember one conflicting lock for the retry
                 th.cw = (u64 *)tile.shfl((u64)cw(p, L.rec), src);
+                th.cw_ex = tile.shfl((int)L.w, src) != 0;
                 th.cv = M31 << 31;                   // wait until its holder count is 0
                 th.hot = (u32)src + 1;               // and take it first next time
                 return RES_ABORT;
@@ -1307,6 +1404,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (busy) {
                 const int src = __ffs(busy) - 1;
                 th.cw = (u64 *)tile.shfl((u64)cw(p, L.rec), src);
+                th.cw_ex = true;
                 th.cv = LOCKB;                       // wait until unlocked
                 th.hot = (u32)src + 1;
             }
@@ -1385,10 +1483,32 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
     }
 }
 
+// Experiment builds (-DGC_TRACE_COMMIT=1, tools/trace_tail.py): trace[0] = kernel start
+// (ns), trace[1] = bucket width (ns), trace[2 + b] = commits, trace[1026 + b] = aborts in
+// time bucket b since the start.
+#ifndef GC_TRACE_COMMIT
+#define GC_TRACE_COMMIT 0
+#endif
+GC_DEV void trace_event(const ExecParams &p, bool commit) {
+#if GC_TRACE_COMMIT
+    if (!p.trace) return;
+    const u64 t = globaltimer_ns(), t0 = ld_relaxed(&p.trace[0]), w = p.trace[1];
+    u64 b = (t > t0 ? t - t0 : 0) / (w ? w : 1000);
+    if (b > 1023) b = 1023;
+    atomicAdd(&p.trace[(commit ? 2 : 1026) + b], 1ull);
+#endif
+}
+
 template <int S, class WL, int G>
 __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(ExecParams p, typename WL::Params y) {
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const u32 li = tile.thread_rank();
+#if GC_TRACE_COMMIT
+    if (p.trace) {
+        if (threadIdx.x == 0) atomicCAS(&p.trace[0], 0ull, globaltimer_ns());
+        __syncthreads();
+    }
+#endif
     exec_params_copy(p);
     if (ld_relaxed(&p.ctl->err.v) != 0) return;   // a3 failed (e.g. KEY_NOT_FOUND): nothing runs
     constexpr bool DET = (S == CC_GPUTX || S == CC_GACCO);
@@ -1398,6 +1518,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
     th.cw = nullptr;
     th.cv = 0;
     th.hot = 0;
+    th.turn = nullptr;
     stages_init(th, p, li == 0);   // stages are timed by each tile's leader
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     // the lane's access (its read/write-set entry): registers, or -- for workloads whose
@@ -1449,6 +1570,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
             th.attempt = tile.shfl(att, 0);   // the leader owns restarts
             AttemptClock ac(th);
             const int r = run_tile<S, WL>(tile, th, gid, L, y, kh, kl);
+            if (li == 0) rq_release(th);   // GC_RETRY_FIFO: this attempt used its turn
             ac.done(r == RES_OK);
             if (p.events && r != RES_FATAL) {
                 tile.sync();   // every lane's access events precede the commit / abort event
@@ -1463,6 +1585,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
                     p.order_hi[gid] = kh;
                     p.order_lo[gid] = kl;
                     p.committed[gid] = 1;
+                    trace_event(p, true);
                 }
                 next = true;
             } else if (r == RES_FATAL || DET) {
@@ -1470,12 +1593,13 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
             } else {
                 int push = 0;
                 if (li == 0) {
+                    trace_event(p, false);
                     const u32 nr = ++att;
                     p.restarts[gid] = nr;
                     StageClock c(th, STAGE_ABORT);
                     retry_pace<S>(th, gid, nr);
                     if (dead(th)) push = -1;   // the watchdog also bounds abort-only livelocks
-                    else push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && try_append_retry(th, gid);   // a6
+                    else push = !(p.flags & CC_FLAG_IMMEDIATE_RETRY) && !th.turn && try_append_retry(th, gid);   // a6
                 }
                 push = tile.shfl(push, 0);
                 if (push < 0) stop = true;

@@ -47,6 +47,8 @@ struct Event {
 
 enum { KIND_YCSB = 1, KIND_TPCC = 2 };
 
+// retry queues: one FIFO word per hashed control word (GC_RETRY_FIFO), after the ring
+constexpr uint32_t GC_RQ_N = 1u << 16;
 // Workload-independent execution parameters.
 struct ExecParams {
     int scheme;
@@ -70,6 +72,8 @@ struct ExecParams {
     void *ws;                    // thread mode: per-worker access workspace in global memory when
                                  // it does not fit shared memory (else null: dynamic smem)
     uint32_t ring_cap;
+    unsigned long long *rq;      // retry queues (GC_RETRY_FIFO): GC_RQ_N words after the ring,
+                                 // ticket (low 32) | serving (high 32), hashed by control word
     // per-transaction internal results
     uint8_t *committed;
     uint32_t *restarts;
@@ -93,6 +97,7 @@ struct ExecParams {
     unsigned long long *sticky;  // first device error of any submit since the last cc_sync
     Event *events;               // CC_FLAG_EVENTS: event log (capacity events_cap)
     unsigned long long events_cap;
+    unsigned long long *trace;   // GC_TRACE_COMMIT experiment builds only (else null)
 };
 // stage-time breakdown (Exp-6): cycles summed over workers
 enum { STAGE_INDEX = 0, STAGE_TS = 1, STAGE_WAIT = 2, STAGE_CC = 3, STAGE_ABORT = 4,
@@ -148,9 +153,11 @@ struct PrepBufs {
 };
 
 // launchers (defined in the .cu files)
-cudaError_t launch_reset_meta(int scheme, unsigned long long *meta, uint64_t n_records,
-                              unsigned long long *ring, uint32_t ring_cap, Ctl *ctl,
-                              cudaStream_t s, bool mvcc_split = false, uint32_t meta_stride = 1);
+// a2 prologue: ring + retry queues (ring_words), control block, per-transaction results,
+// then the batch's a1 error word (may be null) folded into the control block
+cudaError_t launch_a2(unsigned long long *ring, uint32_t ring_words, Ctl *ctl, uint8_t *committed,
+                      uint32_t *restarts, unsigned long long *ohi, unsigned long long *olo, uint32_t n_txn,
+                      const unsigned long long *batch_err, cudaStream_t s);
 // `smem` bytes of dynamic shared memory: the per-worker contexts (exec_th_bytes() per
 // working lane: every lane in tile mode, 2^wd per warp in thread mode), then in thread
 // mode the workers' staged accesses unless ExecParams::ws holds them in global memory
@@ -167,8 +174,6 @@ cudaError_t launch_ycsb_gather(const ExecParams &p, const YcsbParams &y, PrepBuf
 cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_records,
                                bool gputx, int grid, cudaStream_t s, int rank_block = 256);
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s);
-// a1: fold the batch's generator error word into the submit's control block (after a2)
-cudaError_t launch_merge_word(const unsigned long long *err, Ctl *dst, cudaStream_t s);
 // a7 commit positions of TO / MVCC / Silo by bitmap (bits: 2^31 / 32 words, pre: one u32
 // per word, csum: one per 1,024 words); null: radix sort
 struct RankBitmap {

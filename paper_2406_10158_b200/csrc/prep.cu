@@ -18,33 +18,27 @@ constexpr int KEY_SHIFT = 27;
 constexpr u64 GID_MASK = (1ull << 21) - 1;
 
 // ------------------------------------------------------------------ a2 reset
-// Reset the scheme's CC words (the throughput window starts "from the initialization
-// of the CC method", Z19), the retry ring and the control block.
-__global__ void reset_kernel(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
-                             uint32_t ring_cap, Ctl *ctl, bool mvcc_split, uint32_t meta_stride) {
+// a2 prologue of a submit, one launch: the retry ring and retry queues, the per-
+// transaction results and the control block; then the batch's own a1 error word is
+// folded into the fresh control block (block 0, after its reset), so a failed generation
+// stops the submit before anything executes.  The CC words themselves (the throughput
+// window starts "from the initialization of the CC method", Z19) are zeroed
+// by the submit that used them, on the reset stream, while the next submit runs on the
+// other word set (cc_submit); every scheme's initial words are zeros.
+__global__ void a2_kernel(u64 *ring, uint32_t ring_words, Ctl *ctl, uint8_t *committed, uint32_t *restarts,
+                          u64 *ohi, u64 *olo, uint32_t n_txn, const u64 *batch_err) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    if (scheme == CC_MVCC && mvcc_split) {   // lo words dense, hi words after them
-        for (uint64_t r = tid; r < n_records; r += stride) {
-            meta[r] = 0ull;
-            meta[n_records + r] = VNONE;
+    if (blockIdx.x == 0) {
+        for (uint32_t r = threadIdx.x; r < sizeof(Ctl) / 8; r += blockDim.x) reinterpret_cast<u64 *>(ctl)[r] = 0ull;
+        __syncthreads();
+        if (threadIdx.x == 0 && batch_err) {
+            const u64 e = *batch_err;
+            if (e) ctl->err.v = e;
         }
-    } else if (scheme == CC_MVCC) {
-        for (uint64_t r = tid; r < n_records; r += stride) {
-            // lo = 0 (RTS = WTS = 0, not pending); hi = head begins at ts 0, no history
-            reinterpret_cast<ulonglong2 *>(meta)[r] = make_ulonglong2(0ull, VNONE);
-        }
-    } else {
-        for (uint64_t r = tid; r < n_records * meta_stride; r += stride) meta[r] = 0ull;
     }
-    for (uint64_t r = tid; r < ring_cap; r += stride) ring[r] = 0ull;
-    for (uint64_t r = tid; r < sizeof(Ctl) / 8; r += stride) reinterpret_cast<u64 *>(ctl)[r] = 0ull;
-}
-
-__global__ void zero_txn_kernel(uint8_t *committed, uint32_t *restarts, u64 *ohi, u64 *olo,
-                                uint32_t n) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
+    for (uint64_t r = tid; r < ring_words; r += stride) ring[r] = 0ull;
+    for (uint64_t i = tid; i < n_txn; i += stride) {
         committed[i] = 0;
         restarts[i] = 0;
         ohi[i] = ~0ull;
@@ -52,20 +46,11 @@ __global__ void zero_txn_kernel(uint8_t *committed, uint32_t *restarts, u64 *ohi
     }
 }
 
-cudaError_t launch_reset_meta(int scheme, u64 *meta, uint64_t n_records, u64 *ring,
-                              uint32_t ring_cap, Ctl *ctl, cudaStream_t s, bool mvcc_split,
-                              uint32_t meta_stride) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    reset_kernel<<<sms * 4, 512, 0, s>>>(scheme, meta, n_records, ring, ring_cap, ctl, mvcc_split,
-                                         meta_stride);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_zero_txn(uint8_t *committed, uint32_t *restarts, u64 *ohi, u64 *olo,
-                            uint32_t n, cudaStream_t s) {
-    zero_txn_kernel<<<(n + 255) / 256, 256, 0, s>>>(committed, restarts, ohi, olo, n);
+cudaError_t launch_a2(u64 *ring, uint32_t ring_words, Ctl *ctl, uint8_t *committed, uint32_t *restarts, u64 *ohi,
+                      u64 *olo, uint32_t n_txn, const u64 *batch_err, cudaStream_t s) {
+    const uint64_t work = ring_words > n_txn ? ring_words : n_txn;
+    const unsigned g = (unsigned)((work + 1023) / 1024);
+    a2_kernel<<<g < 2 ? 2 : g, 256, 0, s>>>(ring, ring_words, ctl, committed, restarts, ohi, olo, n_txn, batch_err);
     return cudaGetLastError();
 }
 
@@ -521,15 +506,6 @@ __global__ void merge_err_kernel(const Ctl *src, Ctl *dst) {
     if (e) atomicCAS(&dst->err.v, 0ull, e);
     dst->max_rank.v = src->max_rank.v;   // GPUTx: the prepared rank pass counted the K-sets
 }
-__global__ void merge_word_kernel(const u64 *err, Ctl *dst) {
-    const u64 e = *err;
-    if (e) atomicCAS(&dst->err.v, 0ull, e);
-}
-cudaError_t launch_merge_word(const u64 *err, Ctl *dst, cudaStream_t s) {
-    merge_word_kernel<<<1, 1, 0, s>>>(err, dst);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_merge_err(const Ctl *src, Ctl *dst, cudaStream_t s) {
     merge_err_kernel<<<1, 1, 0, s>>>(src, dst);
     return cudaGetLastError();
@@ -546,12 +522,12 @@ static void preload1(F f) {
     cudaFuncGetAttributes(&a, f);
 }
 void preload_prep_kernels() {
-    preload1(reset_kernel); preload1(zero_txn_kernel); preload1(a3_marks_kernel); preload1(positions_kernel);
+    preload1(a2_kernel); preload1(a3_marks_kernel); preload1(positions_kernel);
     preload1(gputx_rank_kernel<16>); preload1(gputx_rank_kernel<32>); preload1(fill_u32_kernel); preload1(iota_kernel);
     preload1(rank_bounds_kernel); preload1(rank_count_kernel); preload1(keys_iota_kernel); preload1(copy_u32_kernel);
     preload1(commit_pos_kernel); preload1(gather_hi_kernel); preload1(copy_out_kernel); preload1(stages_reduce_kernel);
     preload1(stats_kernel); preload1(dense_ticket_pos_kernel); preload1(ticket_perm_kernel); preload1(merge_err_kernel);
-    preload1(merge_word_kernel); preload1(bm_zero_kernel); preload1(bm_set_kernel); preload1(bm_chunk_kernel);
+    preload1(bm_zero_kernel); preload1(bm_set_kernel); preload1(bm_chunk_kernel);
     preload1(bm_csum_kernel); preload1(bm_pos_kernel);
 }
 }  // namespace gcctb

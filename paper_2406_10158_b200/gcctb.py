@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgcctb.so")
+# GCCTB_LIB: an experiment variant built by build.py --out (never set by the tests or bench)
+LIB_PATH = os.environ.get("GCCTB_LIB") or os.path.join(HERE, "libgcctb.so")
 
 CC_OK = 0
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "OOM", 4: "CUDA", 5: "NCCL",
@@ -136,6 +137,7 @@ _SIGS = {
     "cc_submit": (ctypes.c_int, [_P, _P, ctypes.POINTER(cc_exec_desc), ctypes.POINTER(cc_result)]),
     "cc_prepare": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_uint32]),
     "cc_sync": (ctypes.c_int, [_P, ctypes.POINTER(cc_stats)]),
+    "cc_join": (ctypes.c_int, [_P]),
     "cc_timing_read": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double * 5),
                                       ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]),
     "cc_snapshot": (ctypes.c_int, [_P, ctypes.c_int]),

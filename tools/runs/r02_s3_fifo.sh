@@ -1,0 +1,23 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+GCCTB_LIB=$PWD/variants/fifo_trace.so timeout 600 python tools/trace_tail.py --schemes tpl_nw,tpl_wd,silo,tictoc --thetas 0.6 --bucket_ns 5000 > gpurun_out/s3_trace_fifo.jsonl 2>&1
+GCCTB_LIB=$PWD/variants/fifo_trace.so timeout 600 python tools/trace_tail.py --schemes tpl_nw,tpl_wd,silo,tictoc --thetas 0.8 --bucket_ns 20000 >> gpurun_out/s3_trace_fifo.jsonl 2>&1
+cut -c1-250 gpurun_out/s3_trace_fifo.jsonl
+for v in main fifo; do
+  if [ $v = main ]; then unset GCCTB_LIB; else export GCCTB_LIB=$PWD/variants/$v.so; fi
+  echo "# $v"
+  timeout 900 python tools/probe.py --reps 3 --schemes tpl_nw,tpl_wd,silo,tictoc --thetas 0,0.6,0.8,0.9,0.99 --lanes 16 --bs 16 --grid 148 --watchdog 60 2>&1 | cut -c1-330
+  timeout 900 python tools/probe.py --reps 2 --schemes tpl_nw,tpl_wd,silo,tictoc --thetas 0.6,0.9 --lanes 1 --wd 5 --bs 8 --watchdog 60 2>&1 | cut -c1-330
+done > gpurun_out/s3_probe_fifo.log
+unset GCCTB_LIB
+cat gpurun_out/s3_probe_fifo.log | python -c "
+import sys,json
+for l in sys.stdin:
+    if l.startswith('#'): print(l.strip()); continue
+    try: d=json.loads(l[:l.index(', \"ms_total_min')]+'}')
+    except Exception: print(l[:200]); continue
+    print(d['scheme'], d['theta'], d['lanes'], round(d['txn_s']/1e6,2), round(d['abort_rate'],2), round(d['ms_total_median'],3))
+"
+GCCTB_LIB=$PWD/variants/fifo.so timeout 1200 python -m pytest tests/test_gpu_ycsb.py tests/test_gpu_tpcc.py -m gpu -q -x -k "tpl or silo or tictoc" --timeout 600 > gpurun_out/s3f_tests.log 2>&1; tail -3 gpurun_out/s3f_tests.log
+echo done
