@@ -679,9 +679,11 @@ constexpr u32 TO_SEQ_AFTER = GC_TO_SEQ_AFTER;
 // needlessly (measured, YCSB tile 16: every writer at once: theta 0.6 96M -> 53M txn/s;
 // dying writers after 8 restarts: theta 0.8 6.1M -> 1.9M).
 constexpr u32 TPL_INTENT_AFTER = 32;
-// no-wait writer intent (experiment): a writer that has died this often on a shared-held
+// no-wait writer intent (ablation): a writer that has died this often on a shared-held
 // lock announces itself too, and new readers then die on the announced lock so it drains
-// (0: off -- readers never conflict with an announcement under no-wait)
+// (0: off -- readers never conflict with an announcement under no-wait).  Measured slower
+// (configs[1] tile 16, exec ms: theta 0.6 0.51 -> 0.54 / 0.64 from 8 / 2 restarts, theta 0.8
+// 5.9 -> 7.1 / 9.1; profiles/r02_probe_nw_intent.log).
 #ifndef GC_NW_INTENT_AFTER
 #define GC_NW_INTENT_AFTER 0
 #endif
@@ -1250,6 +1252,15 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel
 // ===================================================================== tile mode
 // G lanes per transaction; lane i owns access i.  Every loop below is tile-uniform:
 // the exit conditions are tile votes, so all lanes execute the same collectives.
+// Restarts from which a retry takes the lock that killed its last attempt first, alone
+// (round 1: from 2, against hot-lock livelocks at one TPC-C warehouse).  With the retry
+// queues it is no longer needed and only lengthens the critical section by one round
+// trip: off (configs[1] tile 16, exec ms: tpl_nw theta 0.6 0.51 -> 0.45, theta 0.8 5.9 ->
+// 5.2; TPC-C one warehouse tpl_nw 0.21 -> 0.23 M txn/s; Silo / TicToc within noise;
+// profiles/r02_probe_hot_first.log).
+#ifndef GC_HOT_FIRST_AFTER
+#define GC_HOT_FIRST_AFTER 0xFFFFFFFFu
+#endif
 template <int S, class WL, class Tile>
 GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                     const typename WL::Params &y, u64 &key_hi, u64 &key_lo) {
@@ -1266,7 +1277,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         // W is never free when a Payment's lanes look).  So a retry under no-wait takes the
         // lock that killed its previous attempt first, alone, and the rest in parallel once
         // it holds it: a retry that meets the hot lock busy dies holding nothing.
-        const u32 first = (WD || th.attempt < 2) ? 0u : th.hot;   // 1 + that lock's lane, 0: none
+        const u32 first = (WD || th.attempt < GC_HOT_FIRST_AFTER) ? 0u : th.hot;   // 1 + that lock's lane, 0: none
         // wait-die under extreme contention (experiment knob): from GC_WD_SEQ_AFTER restarts
         // on, take the locks one lane at a time in access (key) order, as the paper's
         // one-thread launch does
@@ -1388,7 +1399,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         u64 seen = 0;
         // write-set locks: all at once; a retry takes the lock that was busy last time
         // first, alone (see 2PL)
-        const u32 first = th.attempt < 2 ? 0u : th.hot;
+        const u32 first = th.attempt < GC_HOT_FIRST_AFTER ? 0u : th.hot;
         const u32 age = gid + 1;
         if (first && li == first - 1 && act && L.w) {
             if (warp_lock_loser(L.rec, true, age)) { bad = true; seen = LOCKB; }   // an older tile locks it

@@ -25,7 +25,11 @@
 // writes of the access table), reduce-then-scan in three kernels.
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace gcctb {
 
@@ -129,26 +133,22 @@ __global__ void sort_rowbase_kernel(u32 *rowsum) {   // one warp: exclusive scan
 // digits form one __match_any_sync group whose lowest lane adds the group size); phase 2
 // scans them into each warp's first slot of each digit inside the tile's digit-sorted
 // order; phase 3 places every key there (+ its rank in its group) in shared memory;
-// phase 4 writes the tile's keys out in that order, each digit's run at its global base.
+// phase 4 writes the tile's keys out in that order, each digit's run at its global base
+// (gbase[d], filled by the caller before the first __syncthreads here).
+struct ScatterSmem {
+    u32 wc[SORT_WARPS][256];
+    u32 tstart[256], gbase[256];
+    u32 ws[SORT_WARPS];
+};
 template <bool PAIRS>
-__global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *keys, const u32 *vals, u64 *keys_out,
-                                                                     u32 *vals_out, const u64 *n_dev, u64 n_host,
-                                                                     int shift, const u32 *offs, const u32 *rowbase,
-                                                                     u32 tiles) {
-    __shared__ u32 wc[SORT_WARPS][256];
-    __shared__ u32 tstart[256], gbase[256];
-    extern __shared__ __align__(16) unsigned char sort_smem[];
-    u64 *sk = reinterpret_cast<u64 *>(sort_smem);
-    u32 *sv = reinterpret_cast<u32 *>(sort_smem + SORT_TILE * sizeof(u64));
+__device__ __forceinline__ void scatter_tile(ScatterSmem &S, u64 *sk, u32 *sv, const u64 *keys, const u32 *vals,
+                                             u64 *keys_out, u32 *vals_out, u64 n, int shift, u32 tile) {
     const u32 tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const u64 n = n_of(n_dev, n_host);
-    const u64 tb = (u64)blockIdx.x * SORT_TILE;
-    if (tb >= n) return;   // uniform
+    const u64 tb = (u64)tile * SORT_TILE;
     const u32 cnt = (u32)(n - tb < SORT_TILE ? n - tb : SORT_TILE);
     const u64 w0 = tb + (u64)warp * SORT_WTILE;
 #pragma unroll
-    for (int w = 0; w < SORT_WARPS; w++) wc[w][tid] = 0;
-    gbase[tid] = rowbase[tid] + offs[(u64)tid * tiles + blockIdx.x];
+    for (int w = 0; w < SORT_WARPS; w++) S.wc[w][tid] = 0;
     __syncthreads();
     u64 k[SORT_PER];
     u32 dg[SORT_PER];
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *k
 #pragma unroll
     for (int c = 0; c < SORT_PER; c++) {
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg[c]);
-        if (dg[c] < 256u && (peers & lt) == 0) wc[warp][dg[c]] += __popc(peers);
+        if (dg[c] < 256u && (peers & lt) == 0) S.wc[warp][dg[c]] += __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *k
 #pragma unroll
         for (int w = 0; w < SORT_WARPS; w++) {
             pre[w] = tot;
-            tot += wc[w][tid];
+            tot += S.wc[w][tid];
         }
         // exclusive scan of the 256 digit totals across the block (digit = thread)
         u32 x = tot;
@@ -181,36 +181,140 @@ __global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *k
             const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
             if (lane >= (u32)o) x += y;
         }
-        __shared__ u32 ws[SORT_WARPS];
-        if (lane == 31) ws[warp] = x;
+        if (lane == 31) S.ws[warp] = x;
         __syncthreads();
         u32 before = 0;
-        for (u32 w = 0; w < warp; w++) before += ws[w];
+        for (u32 w = 0; w < warp; w++) before += S.ws[w];
         const u32 start = before + x - tot;   // first slot of digit `tid` in the tile's order
-        tstart[tid] = start;
+        S.tstart[tid] = start;
 #pragma unroll
-        for (int w = 0; w < SORT_WARPS; w++) wc[w][tid] = start + pre[w];
+        for (int w = 0; w < SORT_WARPS; w++) S.wc[w][tid] = start + pre[w];
     }
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < SORT_PER; c++) {
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg[c]);
         if (dg[c] < 256u) {
-            const u32 slot = wc[warp][dg[c]] + __popc(peers & lt);
+            const u32 slot = S.wc[warp][dg[c]] + __popc(peers & lt);
             sk[slot] = k[c];
             if (PAIRS) sv[slot] = vals[w0 + (u64)c * 32 + lane];
         }
         __syncwarp();
-        if (dg[c] < 256u && (peers & lt) == 0) wc[warp][dg[c]] += __popc(peers);
+        if (dg[c] < 256u && (peers & lt) == 0) S.wc[warp][dg[c]] += __popc(peers);
         __syncwarp();
     }
     __syncthreads();
     for (u32 i = tid; i < cnt; i += SORT_THREADS) {   // consecutive slots of a digit: consecutive addresses
         const u64 key = sk[i];
         const u32 d = (u32)((key >> shift) & 0xFF);
-        const u32 pos = gbase[d] + (i - tstart[d]);
+        const u32 pos = S.gbase[d] + (i - S.tstart[d]);
         keys_out[pos] = key;
         if (PAIRS) vals_out[pos] = sv[i];
+    }
+}
+
+template <bool PAIRS>
+__global__ void __launch_bounds__(SORT_THREADS) sort_scatter_kernel(const u64 *keys, const u32 *vals, u64 *keys_out,
+                                                                     u32 *vals_out, const u64 *n_dev, u64 n_host,
+                                                                     int shift, const u32 *offs, const u32 *rowbase,
+                                                                     u32 tiles) {
+    __shared__ ScatterSmem S;
+    extern __shared__ __align__(16) unsigned char sort_smem[];
+    u64 *sk = reinterpret_cast<u64 *>(sort_smem);
+    u32 *sv = reinterpret_cast<u32 *>(sort_smem + SORT_TILE * sizeof(u64));
+    const u64 n = n_of(n_dev, n_host);
+    if ((u64)blockIdx.x * SORT_TILE >= n) return;   // uniform
+    S.gbase[threadIdx.x] = rowbase[threadIdx.x] + offs[(u64)threadIdx.x * tiles + blockIdx.x];
+    scatter_tile<PAIRS>(S, sk, sv, keys, vals, keys_out, vals_out, n, shift, blockIdx.x);
+}
+
+// Small sorts (a7 commit positions, the GPUTx rank order: n <= GC_COOP_MAX_TILES tiles)
+// in ONE cooperative launch, one block per tile: per pass the tile counts, a grid barrier,
+// every block derives its tile's digit bases from all tiles' counts (a 256 x tiles scan
+// it repeats for itself), the stable scatter above, a grid barrier.  Passes above the
+// largest key's top byte are skipped on the device (the keys' range -- e.g. TicToc's
+// commit timestamps -- is known only there); if the skipped passes leave the keys in the
+// other buffer than the host-side ping-pong expects, a final copy puts them there.
+#ifndef GC_COOP_MAX_TILES
+#define GC_COOP_MAX_TILES 128u
+#endif
+template <bool PAIRS>
+__global__ void __launch_bounds__(SORT_THREADS) sort_coop_kernel(u64 *ka, u32 *va, u64 *kb, u32 *vb, u64 n, int lo_bit,
+                                                                  int hi_bit, u32 *counts, u64 *bmax) {
+    __shared__ ScatterSmem S;
+    __shared__ u64 smax[SORT_WARPS];
+    __shared__ u32 dtot[256];
+    extern __shared__ __align__(16) unsigned char sort_smem[];
+    u64 *sk = reinterpret_cast<u64 *>(sort_smem);
+    u32 *sv = reinterpret_cast<u32 *>(sort_smem + SORT_TILE * sizeof(u64));
+    cg::grid_group grid = cg::this_grid();
+    const u32 tiles = gridDim.x, t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u64 tb = (u64)t * SORT_TILE;
+    // largest key (grid-wide): each block publishes its tile's maximum
+    {
+        u64 m = 0;
+        for (u64 i = tb + tid; i < n && i < tb + SORT_TILE; i += SORT_THREADS) m = max(m, ka[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, (u64)__shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (lane == 0) smax[warp] = m;
+        __syncthreads();
+        if (tid == 0) {
+            u64 x = 0;
+            for (int w = 0; w < SORT_WARPS; w++) x = max(x, smax[w]);
+            bmax[t] = x;
+        }
+    }
+    grid.sync();
+    u64 kmax = 0;
+    for (u32 b = 0; b < tiles; b++) kmax = max(kmax, bmax[b]);   // (same value in every block)
+    u64 *src = ka, *dst = kb;
+    u32 *vs = va, *vd = vb;
+    int total = 0, done = 0;
+    for (int sh = lo_bit; sh < hi_bit; sh += 8) total++;
+    for (int sh = lo_bit; sh < hi_bit; sh += 8) {
+        if (sh >= 64 || (kmax >> sh) == 0) break;   // every remaining digit is 0: identity
+        // 1. tile digit counts
+        if (tid < 256) dtot[tid] = 0;
+        __syncthreads();
+        for (u64 i = tb + tid; i < n && i < tb + SORT_TILE; i += SORT_THREADS) atomicAdd(&dtot[(src[i] >> sh) & 0xFF], 1u);
+        __syncthreads();
+        counts[(u64)tid * tiles + t] = dtot[tid];
+        grid.sync();
+        // 2. this tile's base of each digit: all tiles' counts of smaller digits, plus the
+        // counts of this digit in the tiles before
+        {
+            u32 tot = 0, pre = 0;
+            const u32 *row = counts + (u64)tid * tiles;
+            for (u32 b = 0; b < tiles; b++) {
+                const u32 c = row[b];
+                tot += c;
+                if (b < t) pre += c;
+            }
+            u32 x = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= (u32)o) x += y;
+            }
+            __syncthreads();   // S.ws is reused by the scatter
+            if (lane == 31) S.ws[warp] = x;
+            __syncthreads();
+            u32 before = 0;
+            for (u32 w = 0; w < warp; w++) before += S.ws[w];
+            S.gbase[tid] = before + x - tot + pre;
+        }
+        // 3. stable scatter
+        if (tb < n) scatter_tile<PAIRS>(S, sk, sv, src, vs, dst, vd, n, sh, t);
+        grid.sync();
+        u64 *tk = src; src = dst; dst = tk;
+        u32 *tv = vs; vs = vd; vd = tv;
+        done++;
+    }
+    if ((total - done) & 1) {   // the host expects the result after `total` swaps
+        for (u64 i = (u64)t * SORT_THREADS + tid; i < n; i += (u64)tiles * SORT_THREADS) {
+            dst[i] = src[i];
+            if (PAIRS) vd[i] = vs[i];
+        }
     }
 }
 
@@ -236,6 +340,24 @@ cudaError_t gc_sort(u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, uint64_t
     cudaError_t ea = cudaFuncSetAttribute(va ? (const void *)sort_scatter_kernel<true> : (const void *)sort_scatter_kernel<false>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
     if (ea) return ea;
+    if (!n_dev && tiles <= GC_COOP_MAX_TILES) {   // one cooperative launch (see sort_coop_kernel)
+        const void *f = va ? (const void *)sort_coop_kernel<true> : (const void *)sort_coop_kernel<false>;
+        cudaError_t ec = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SORT_SMEM);
+        if (ec) return ec;
+        u64 n = cap;
+        int lo = lo_bit, hi = hi_bit;
+        u64 *bmax = reinterpret_cast<u64 *>(rowsum);
+        void *args[] = {&ka, &va, &kb, &vb, &n, &lo, &hi, &counts, &bmax};
+        ec = cudaLaunchCooperativeKernel(f, dim3((unsigned)tiles), dim3(SORT_THREADS), args, SORT_SMEM, s);
+        if (ec) return ec;
+        int passes = 0;
+        for (int sh = lo_bit; sh < hi_bit; sh += 8) passes++;
+        if (passes & 1) {
+            *keys_out = kb;
+            if (vals_out) *vals_out = vb;
+        }
+        return cudaSuccess;
+    }
     for (int sh = lo_bit; sh < hi_bit; sh += 8) {
         sort_count_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(ka, n_dev, cap, sh, counts, (u32)tiles);
         sort_rowscan_kernel<<<256, 1024, 0, s>>>(counts, (u32)tiles, n_dev, cap, rowsum);
@@ -383,7 +505,7 @@ static void preload1(F f) {
 void preload_sort_kernels() {
     preload1(sort_count_kernel); preload1(sort_rowscan_kernel); preload1(sort_rowbase_kernel);
     preload1(sort_scatter_kernel<true>);
-    preload1(sort_scatter_kernel<false>); preload1(scan_reduce_kernel); preload1(scan_blocks_kernel);
+    preload1(sort_scatter_kernel<false>); preload1(sort_coop_kernel<true>); preload1(sort_coop_kernel<false>); preload1(scan_reduce_kernel); preload1(scan_blocks_kernel);
     preload1(scan_apply_kernel);
 }
 }  // namespace gcctb
