@@ -397,61 +397,74 @@ cudaError_t launch_identity_index(u64 *keys, u64 *rowids, uint64_t n, cudaStream
 }
 
 // ---------------------------------------------------------------- a1 generator
-// One thread per transaction (readings Z12, Z13):
+// The definition (readings Z12, Z13), per transaction:
 //   op i: draw k = 0,1,..: u = rng(seed, gid, 1<<56 | i<<24 | k), rank = Zipf(u) by
 //   binary search in the threshold table, key = ((rank-1)*A) mod n, until distinct;
 //   sort keys ascending; write iff (rng(seed,gid,2<<56|i) >> 11) < floor(W*2^53);
 //   field = rng(seed,gid,3<<56|i) mod 15.
+// One warp per transaction: lane i draws op i's first candidate (k = 0) -- the binary
+// searches of a transaction's ops run in parallel, not one after another as in the
+// paper's one-thread loop -- then the warp resolves duplicates in op order (op i redraws
+// k = 1, 2, ... while it equals an earlier op's key: the same draw sequence as the serial
+// definition, so the keys are bit-identical), ranks the K distinct keys (ascending) and
+// writes them; lane i writes op byte i.
+__device__ __forceinline__ u32 ycsb_draw(uint64_t seed, u32 gid, u32 i, u64 k, uint64_t n, const u64 *T,
+                                         uint64_t A) {
+    const u64 u = rng3(seed, gid, (1ull << 56) | ((u64)i << 24) | k);
+    u64 lo = 0, hi = n;   // count = #{j : T[j] <= u}
+    while (lo < hi) {
+        const u64 mid = lo + (hi - lo) / 2;
+        if (__ldg(T + mid) <= u) lo = mid + 1; else hi = mid;
+    }
+    if (lo > n - 1) lo = n - 1;
+    return (u32)((lo * A) % n);   // (rank - 1) * A mod n
+}
+
 __global__ void ycsb_gen_kernel(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                                 uint64_t n, u64 wthr, uint64_t seed, const u64 *T,
                                 uint64_t A, u64 *err) {
-    const u32 gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= n_txn) return;
-    u32 kk[16];
-    for (u32 i = 0; i < K; i++) {
-        for (u64 k = 0;; k++) {
+    const u32 lane = threadIdx.x & 31u;
+    const u32 gid = (u32)(((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (gid >= n_txn) return;   // warp-uniform
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    u32 mine = lane < K ? ycsb_draw(seed, gid, lane, 0, n, T, A) : 0xFFFFFFFFu;
+    for (u32 i = 1; i < K; i++) {
+        u32 ki = __shfl_sync(FULL, mine, (int)i);
+        for (u64 k = 1;; k++) {
+            if (!__any_sync(FULL, lane < i && mine == ki)) break;   // distinct from ops 0..i-1
             if (k >= (1u << 24)) {
-                atomicCAS(err, 0ull, (u64)CC_ERR_CONFIG);   // the batch's error word
+                if (lane == 0) atomicCAS(err, 0ull, (u64)CC_ERR_CONFIG);   // the batch's error word
                 return;
             }
-            const u64 u = rng3(seed, gid, (1ull << 56) | ((u64)i << 24) | k);
-            // count = #{j : T[j] <= u}
-            u64 lo = 0, hi = n;
-            while (lo < hi) {
-                const u64 mid = lo + (hi - lo) / 2;
-                if (__ldg(T + mid) <= u) lo = mid + 1; else hi = mid;
-            }
-            if (lo > n - 1) lo = n - 1;
-            const u64 key = (lo * A) % n;   // (rank - 1) * A mod n
-            bool dup = false;
-            for (u32 j = 0; j < i; j++) dup |= (kk[j] == (u32)key);
-            if (!dup) { kk[i] = (u32)key; break; }
+            ki = ycsb_draw(seed, gid, i, k, n, T, A);   // (every lane: the same redraw)
         }
+        if (lane == i) mine = ki;
     }
-    for (u32 i = 1; i < K; i++) {
-        const u32 v = kk[i];
-        int j = (int)i - 1;
-        while (j >= 0 && kk[j] > v) { kk[j + 1] = kk[j]; j--; }
-        kk[j + 1] = v;
+    u32 rank = 0;   // keys are distinct: position = number of smaller keys
+    for (u32 j = 0; j < K; j++) {
+        const u32 kj = __shfl_sync(FULL, mine, (int)j);
+        rank += (lane < K && kj < mine) ? 1u : 0u;
     }
-    const u64 base = (u64)gid * K;
-    for (u32 i = 0; i < K; i++) {
-        const u64 um = rng3(seed, gid, (2ull << 56) | i);
-        const u64 uf = rng3(seed, gid, (3ull << 56) | i);
+    if (lane < K) {
+        const u64 base = (u64)gid * K;
+        keys[base + rank] = mine;
+        const u64 um = rng3(seed, gid, (2ull << 56) | lane);
+        const u64 uf = rng3(seed, gid, (3ull << 56) | lane);
         uint8_t op = (uint8_t)(uf % 15u);
         if ((um >> 11) < wthr) op |= 0x80u;
-        keys[base + i] = kk[i];
-        ops[base + i] = op;
+        ops[base + lane] = op;
     }
 }
 
 cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                             uint64_t n_rows, double W, uint64_t seed, const u64 *T,
                             uint64_t mult, u64 *err, cudaStream_t s) {
+    if (K > 32) return cudaErrorInvalidValue;
     const u64 wthr = (u64)(W * 9007199254740992.0);
-    const int blk = 128;
-    ycsb_gen_kernel<<<(n_txn + blk - 1) / blk, blk, 0, s>>>(keys, ops, n_txn, K, n_rows, wthr,
-                                                            seed, T, mult, err);
+    const int blk = 128;   // 4 transactions per block
+    const u64 threads = (u64)n_txn * 32;
+    ycsb_gen_kernel<<<(unsigned)((threads + blk - 1) / blk), blk, 0, s>>>(keys, ops, n_txn, K, n_rows, wthr,
+                                                                          seed, T, mult, err);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+for v in main same; do
+echo "# $v"
+if [ $v = main ]; then unset GCCTB_LIB; else export GCCTB_LIB=$PWD/variants/$v.so; fi
+for i in 1 2 3 4 5 6 7 8; do timeout 900 python -m pytest tests/test_gpu_partition.py -m gpu -q --timeout 600 -k "test_loopback_2pc and (to or mvcc or silo or tictoc)" 2>&1 | grep -E "passed|FAILED"; done
+done
