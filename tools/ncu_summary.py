@@ -66,10 +66,10 @@ def main():
         top = ", ".join(f"{k} {v / tot * 100:.0f}%" for k, v in sorted(st.items(), key=lambda t: -t[1])[:3])
         t_ms = g('gpu__time_duration.sum')
         tu = units[col["gpu__time_duration.sum"]]
-        t_s = t_ms * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(tu, 1e-3)
+        t_s = t_ms * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0, "s": 1.0}.get(tu, 1e-3)
         atom = (g("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum")
                 + g("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum"))   # sectors sent to L2
-        lines.append(f"| {s} | {t_ms:.3f} | {dram / 1e6:.0f} | {dram / (65536 * 16):.0f} | "
+        lines.append(f"| {s} | {t_s * 1e3:.3f} | {dram / 1e6:.0f} | {dram / (65536 * 16):.0f} | "
                      f"{g('lts__t_sector_hit_rate.pct'):.1f} | {atom / t_s / 1e6 if t_s else 0:.0f} | "
                      f"{g('smsp__thread_inst_executed_per_inst_executed.ratio'):.1f} | "
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
