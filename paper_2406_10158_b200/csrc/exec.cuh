@@ -60,6 +60,7 @@ struct Th {
     u32 hot;   // tile mode: 1 + lane of the lock that caused this transaction's last abort
     u64 *turn; // GC_RETRY_FIFO: the retry queue whose turn this worker holds (nullptr: none)
     bool cw_ex;   // the access that died on *cw wanted it exclusively (a write)
+    u64 *tq;      // TO / MVCC: control word of the write whose timestamp check killed the attempt
     u64 a_t0, a_u0, a_w0, a_s0;   // CC_FLAG_STAGES: the current attempt's start snapshot
     Claim cl;                     // the worker's claim state (leader lane in tile mode)
 };
@@ -507,6 +508,33 @@ GC_DEV void rq_release(Th &th) {
         th.turn = nullptr;
     }
 }
+// take a ticket in the queue of control word w and wait for the turn (holding nothing)
+GC_DEV void rq_wait(Th &th, const u64 *w) {
+    u64 *q = rq_of(*th.p, w);
+    const u64 old = atomicAdd(q, 1ull);
+    const u32 t = (u32)old;
+    u32 sv = (u32)(old >> 32);
+    while (sv != t) {   // far waiters sleep in proportion to the turns ahead,
+        const u32 d = t - sv;   // the next in line polls
+        const u32 ns = d > 30u ? 50000u : (d - 1) * GC_RQ_TURN_NS;
+        __nanosleep(ns < 64u ? 64u : ns);
+        if (dead(th)) break;
+        sv = (u32)(ld_relaxed(q) >> 32);
+    }
+    th.turn = q;
+}
+// TO / MVCC (ablation, GC_TS_FIFO): a write killed by its timestamp check queues the same
+// way once at least GC_RQ_HERD_TS transactions back off (instead of the randomised
+// exponential backoff, whose window reaches ~1 ms in a herd).  Measured (tile 16,
+// profiles/r02_probe_ts_fifo.log): TO unchanged (theta 0.99 0.27 M txn/s either way: its
+// aborts are read-timestamp conflicts, not a queue); MVCC theta 0.99 0.91 -> 1.24 but theta
+// 0.8 13.0 -> 9.0.  Off.
+#ifndef GC_TS_FIFO
+#define GC_TS_FIFO 0
+#endif
+#ifndef GC_RQ_HERD_TS
+#define GC_RQ_HERD_TS 1024
+#endif
 // wait (holding nothing) until the lock that killed the attempt is free, bounded
 GC_DEV void wait_lock_free(Th &th, u32 restarts) {
     const u32 sh = restarts < 10 ? restarts : 10;
@@ -525,18 +553,7 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         const bool flat = (th.p->flags & CC_FLAG_FLAT_JITTER) != 0;
         constexpr u64 HERD = (S == CC_TPL_NW || S == CC_TPL_WD) ? GC_RQ_HERD_2PL : GC_RQ_HERD_OCC;
         if (GC_RETRY_FIFO && th.cw_ex && n >= HERD && !flat) {   // a herd: queue
-            u64 *q = rq_of(*th.p, th.cw);
-            const u64 old = atomicAdd(q, 1ull);
-            const u32 t = (u32)old;
-            u32 sv = (u32)(old >> 32);
-            while (sv != t) {   // far waiters sleep in proportion to the turns ahead,
-                const u32 d = t - sv;   // the next in line polls
-                const u32 ns = d > 30u ? 50000u : (d - 1) * GC_RQ_TURN_NS;
-                __nanosleep(ns < 64u ? 64u : ns);
-                if (dead(th)) break;
-                sv = (u32)(ld_relaxed(q) >> 32);
-            }
-            th.turn = q;   // held through the next attempt (in place), released after it
+            rq_wait(th, th.cw);   // held through the next attempt (in place), released after it
             wait_lock_free(th, restarts);
         } else {
             const u32 jcap = (GC_JITTER_LO > 0 && n < (u64)GC_JITTER_LO) ? (u32)GC_JITTER_LO_SHIFT
@@ -555,6 +572,16 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         if (GC_JITTER_LO > 0 || GC_RETRY_FIFO) atomicAdd(&th.p->ctl->pacing_lk.v, (u64)-1ll);
         th.cw = nullptr;
         return;
+    }
+    if ((S == CC_TO || S == CC_MVCC) && GC_TS_FIFO && th.tq) {
+        const u64 *w = th.tq;
+        th.tq = nullptr;
+        if (ld_relaxed(&th.p->ctl->pacing.v) >= (u64)GC_RQ_HERD_TS) {   // a herd: queue
+            atomicAdd(&th.p->ctl->pacing.v, 1ull);
+            rq_wait(th, w);
+            atomicAdd(&th.p->ctl->pacing.v, (u64)-1ll);
+            return;
+        }
     }
     abort_backoff<S>(*th.p, gid, restarts);
 }
@@ -1035,7 +1062,11 @@ GC_DEV int run_thread(Th &th, u32 gid, LA L, u32 n, const typename WL::Params &y
                                             : mvcc_step<WL>(th, p, y, Li, gid, i, ts, pend, Li.cv);
                 if (pend) pendm |= 1u << i;
                 if (st == ST_DONE) break;
-                if (st == ST_ABORT) { r = RES_ABORT; break; }
+                if (st == ST_ABORT) {
+                    if (GC_TS_FIFO && Li.w) th.tq = (S == CC_TO) ? cw(p, Li.rec) : mvcc_lo(p, Li.rec);
+                    r = RES_ABORT;
+                    break;
+                }
                 if (st == ST_RETRY) continue;
                 if (!sp.wait(th)) { r = RES_FATAL; break; }
             }
@@ -1184,6 +1215,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel
     th.cv = 0;
     th.hot = 0;
     th.turn = nullptr;
+    th.tq = nullptr;
     stages_init(th, p, true);
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     // the worker's staged read/write set: shared memory, or the global workspace
@@ -1361,6 +1393,14 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
                     if (S == CC_TO) w_store(p, cw(p, L.rec), saved);
                     else mvcc_restore<WL>(p, L, saved);
                 }
+                if (GC_TS_FIFO) {   // a write whose timestamp check failed: its word names the queue
+                    const unsigned wab = tile.ballot(st == ST_ABORT && L.w);
+                    th.tq = nullptr;
+                    if (wab) {
+                        const int src = __ffs(wab) - 1;
+                        th.tq = (u64 *)tile.shfl((u64)((S == CC_TO) ? cw(p, L.rec) : mvcc_lo(p, L.rec)), src);
+                    }
+                }
                 return RES_ABORT;
             }
             if (tile.all(done)) break;
@@ -1530,6 +1570,7 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_tile_kernel(E
     th.cv = 0;
     th.hot = 0;
     th.turn = nullptr;
+    th.tq = nullptr;
     stages_init(th, p, li == 0);   // stages are timed by each tile's leader
     th.deadline = globaltimer_ns() + p.watchdog_ns;
     // the lane's access (its read/write-set entry): registers, or -- for workloads whose
