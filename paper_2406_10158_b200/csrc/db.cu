@@ -338,7 +338,7 @@ cc_status cc_db_create(const cc_db_desc *desc, cc_db *out) {
         return CC_ERR_CUDA;
     }
     if (cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&db->reset_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&db->reset_stream, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
         cudaEventCreateWithFlags(&db->meta_used[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&db->meta_used[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&db->meta_clean[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -1162,6 +1162,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     p.ring = db->ring;
     p.ring_cap = db->ring_cap;
     p.rq = db->ring + db->ring_cap;
+    p.rq_herd_2pl = is_tpcc ? 256u : 2048u;   // retry-queue threshold for 2PL (see exec.cuh)
     p.committed = db->committed;
     p.restarts = db->restarts;
     p.order_hi = db->ohi;
@@ -1385,7 +1386,7 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         } else {
             CUDA_TRY(db, cudaEventRecord(db->meta_used[mk], db->stream));
             CUDA_TRY(db, cudaStreamWaitEvent(db->reset_stream, db->meta_used[mk], 0));
-            CUDA_TRY(db, cudaMemsetAsync(p.meta, 0, words * 8, db->reset_stream));
+            CUDA_TRY(db, launch_zero_words(p.meta, words, db->reset_stream));
             CUDA_TRY(db, cudaEventRecord(db->meta_clean[mk], db->reset_stream));
             db->meta_cleaning[mk] = true;
             db->meta_cur = mk ^ 1;

@@ -488,7 +488,10 @@ GC_DEV void kset_done(const ExecParams &p, u32 k) {
 // it the jitter stays (measured, configs[1] tile 16, profiles/r02_probe_fifo_v5_herd.log:
 // queueing from 64 pacers cost 2PL 10-25 % at theta 0.6-0.8, from 1024 it is neutral there
 // and 2-8x faster at theta 0.99; Silo / TicToc gain from 64 at theta >= 0.8 and are neutral
-// at 0.6).
+// at 0.6).  The 2PL threshold is per workload (ExecParams::rq_herd_2pl, set by the host):
+// TPC-C, whose warehouse / district rows are hot for every transaction, gains from 256
+// (one warehouse +10 %, 64 warehouses +7-11 %, profiles/r02_probe_tpcc_herd2pl.log) where
+// YCSB at theta 0.6 loses 21 %.
 #ifndef GC_RQ_HERD_2PL
 #define GC_RQ_HERD_2PL 2048
 #endif
@@ -551,7 +554,10 @@ GC_DEV void retry_pace(Th &th, u32 gid, u32 restarts) {
         // how many transactions pace after a lock wait right now (this one included)
         const u64 n = (GC_JITTER_LO > 0 || GC_RETRY_FIFO) ? atomicAdd(&th.p->ctl->pacing_lk.v, 1ull) : 0ull;
         const bool flat = (th.p->flags & CC_FLAG_FLAT_JITTER) != 0;
-        constexpr u64 HERD = (S == CC_TPL_NW || S == CC_TPL_WD) ? GC_RQ_HERD_2PL : GC_RQ_HERD_OCC;
+        u64 HERD = (S == CC_TPL_NW || S == CC_TPL_WD)
+                       ? (th.p->rq_herd_2pl ? (u64)th.p->rq_herd_2pl : (u64)GC_RQ_HERD_2PL)
+                       : (u64)GC_RQ_HERD_OCC;
+        if (HERD > (u64)(th.p->n_txn >> 3)) HERD = th.p->n_txn >> 3;   // small batches: an eighth pacing is a herd
         if (GC_RETRY_FIFO && th.cw_ex && n >= HERD && !flat) {   // a herd: queue
             rq_wait(th, th.cw);   // held through the next attempt (in place), released after it
             wait_lock_free(th, restarts);
@@ -700,6 +706,13 @@ GC_DEV u64 tpl_make(bool s, u64 cnt, u64 holder) {
 #define GC_TO_SEQ_AFTER 32
 #endif
 constexpr u32 TO_SEQ_AFTER = GC_TO_SEQ_AFTER;
+// Restarts from which tile-mode TO steps one lane at a time while at least 1,024
+// transactions back off (a herd; 0: off).  configs[1], M txn/s (profiles/
+// r02_probe_to_seq_herd.log): theta 0.99 0.27 -> 0.33 (the paper's thread launch: 0.30),
+// theta 0.9 0.93 -> 0.90, theta 0.6 unchanged; from 2 restarts: 0.35 / 0.79.
+#ifndef GC_TO_SEQ_HERD
+#define GC_TO_SEQ_HERD 6
+#endif
 
 // A waiting writer always announces intent (TPL_WW); a dying one only once it has restarted
 // this often -- the stale-age starvation needs it, and announcing earlier makes readers die
@@ -1285,13 +1298,16 @@ __global__ void __launch_bounds__(GC_EXEC_MAXT, GC_EXEC_MINB) exec_thread_kernel
 // G lanes per transaction; lane i owns access i.  Every loop below is tile-uniform:
 // the exit conditions are tile votes, so all lanes execute the same collectives.
 // Restarts from which a retry takes the lock that killed its last attempt first, alone
-// (round 1: from 2, against hot-lock livelocks at one TPC-C warehouse).  With the retry
-// queues it is no longer needed and only lengthens the critical section by one round
-// trip: off (configs[1] tile 16, exec ms: tpl_nw theta 0.6 0.51 -> 0.45, theta 0.8 5.9 ->
-// 5.2; TPC-C one warehouse tpl_nw 0.21 -> 0.23 M txn/s; Silo / TicToc within noise;
-// profiles/r02_probe_hot_first.log).
+// (round 1: from 2, against hot-lock livelocks at one TPC-C warehouse).  It lengthens every
+// retried critical section by one round trip, and with the retry queues the herds no
+// longer need it from the start: from 2 restarts vs never, configs[1] tile 16, exec ms:
+// tpl_nw theta 0.6 0.51 -> 0.45, theta 0.8 5.9 -> 5.2; TPC-C one warehouse tpl_nw 0.21 ->
+// 0.23 M txn/s; Silo / TicToc within noise (profiles/r02_probe_hot_first.log).  It stays
+// as a livelock breaker for long-starved transactions: a small batch with extreme
+// contention (2,053 x 16 ops on 1,024 rows, too few transactions for a herd) livelocked
+// without it.
 #ifndef GC_HOT_FIRST_AFTER
-#define GC_HOT_FIRST_AFTER 0xFFFFFFFFu
+#define GC_HOT_FIRST_AFTER 64
 #endif
 template <int S, class WL, class Tile>
 GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
@@ -1374,7 +1390,12 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         // (tile mode at theta=0.99: 5 K txn/s).  After TO_SEQ_AFTER restarts a transaction
         // steps one lane at a time in access order and stops at the first conflict, as the
         // paper's one-thread-per-transaction launch does.
-        const bool seq = S == CC_TO && th.attempt >= TO_SEQ_AFTER;
+        bool seq = S == CC_TO && th.attempt >= TO_SEQ_AFTER;
+        if (S == CC_TO && GC_TO_SEQ_HERD > 0 && !seq && th.attempt >= (u32)GC_TO_SEQ_HERD) {
+            u64 n = 0;   // in a herd (many backing off) step one lane at a time sooner
+            if (li == 0) n = ld_relaxed(&p.ctl->pacing.v);
+            seq = tile.shfl(n, 0) >= 1024;
+        }
         Spin sp;
         for (;;) {
             int st = ST_DONE;

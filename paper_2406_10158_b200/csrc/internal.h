@@ -72,6 +72,7 @@ struct ExecParams {
     void *ws;                    // thread mode: per-worker access workspace in global memory when
                                  // it does not fit shared memory (else null: dynamic smem)
     uint32_t ring_cap;
+    uint32_t rq_herd_2pl;        // 2PL: pacing transactions from which exclusive retriers queue
     unsigned long long *rq;      // retry queues (GC_RETRY_FIFO): GC_RQ_N words after the ring,
                                  // ticket (low 32) | serving (high 32), hashed by control word
     // per-transaction internal results
@@ -269,6 +270,8 @@ cudaError_t launch_tree_level(const unsigned long long *in, uint64_t n_in, unsig
 cudaError_t launch_index_lookup(const YcsbParams &y, const unsigned long long *keys, uint64_t n,
                                 unsigned long long *out, cudaStream_t s);
 cudaError_t launch_fill_u64(unsigned long long *p, unsigned long long v, uint64_t n, cudaStream_t s);
+// zero `words` u64 words (background a2 of a used CC word set): evict-first stores
+cudaError_t launch_zero_words(unsigned long long *p, uint64_t words, cudaStream_t s);
 cudaError_t launch_ycsb_gen(uint32_t *keys, uint8_t *ops, uint32_t n_txn, uint32_t K,
                             uint64_t n_rows, double W, uint64_t seed,
                             const unsigned long long *T, uint64_t mult, unsigned long long *err,

@@ -46,6 +46,26 @@ __global__ void a2_kernel(u64 *ring, uint32_t ring_words, Ctl *ctl, uint8_t *com
     }
 }
 
+// The background zeroing of a used word set (a2, reset stream): 32 B evict-first stores
+// (st.global.cs), so the 84-168 MB it writes beside the next submit's executor do not
+// displace that executor's control words and hot rows from L2 (GC_ZERO_CS=0: memset).
+#ifndef GC_ZERO_CS
+#define GC_ZERO_CS 1
+#endif
+__global__ void zero_cs_kernel(u64 *p, uint64_t n4) {   // n4: 32 B units
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+        asm volatile("st.global.cs.v4.u64 [%0], {%1, %1, %1, %1};" ::"l"(p + 4 * i), "l"(0ull) : "memory");
+}
+cudaError_t launch_zero_words(u64 *p, uint64_t words, cudaStream_t s) {
+    if (!GC_ZERO_CS || (words & 3)) return cudaMemsetAsync(p, 0, words * 8, s);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    zero_cs_kernel<<<sms * 2, 512, 0, s>>>(p, words / 4);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_a2(u64 *ring, uint32_t ring_words, Ctl *ctl, uint8_t *committed, uint32_t *restarts, u64 *ohi,
                       u64 *olo, uint32_t n_txn, const u64 *batch_err, cudaStream_t s) {
     const uint64_t work = ring_words > n_txn ? ring_words : n_txn;
@@ -522,7 +542,7 @@ static void preload1(F f) {
     cudaFuncGetAttributes(&a, f);
 }
 void preload_prep_kernels() {
-    preload1(a2_kernel); preload1(a3_marks_kernel); preload1(positions_kernel);
+    preload1(a2_kernel); preload1(zero_cs_kernel); preload1(a3_marks_kernel); preload1(positions_kernel);
     preload1(gputx_rank_kernel<16>); preload1(gputx_rank_kernel<32>); preload1(fill_u32_kernel); preload1(iota_kernel);
     preload1(rank_bounds_kernel); preload1(rank_count_kernel); preload1(keys_iota_kernel); preload1(copy_u32_kernel);
     preload1(commit_pos_kernel); preload1(gather_hi_kernel); preload1(copy_out_kernel); preload1(stages_reduce_kernel);
