@@ -45,7 +45,7 @@ def parse():
                     help="tuned: per-scheme warps per SM measured best at configs[1] theta=0.6 "
                          "(profiles/r01_tune_bs.jsonl; one block per SM); fixed: --wd/--bs for "
                          "every scheme with a full-occupancy grid")
-    ap.add_argument("--lanes", type=int, default=16)      # 16 = tile mode (lane i owns op i); 1 = thread per txn (paper)
+    ap.add_argument("--lanes", type=int, default=32)      # tile mode: lane i owns op i (32: one txn per warp); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
     ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary", "eytz"],
                     help="dense = direct addressing on the dense YCSB key range (default); tree = cache-line "
@@ -264,11 +264,15 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-# YCSB tile mode: warps per SM with the lowest exec time at the bench workload
-# (configs[1], theta 0.6, 2 seeds; profiles/r01_tune_bs.jsonl).  Fewer resident transactions
-# collide less (TO: 0.54 -> 0.44 ms) and GPUTx's K-set chain runs faster with fewer
-# waiting tiles (0.97 -> 0.73 ms).
-TUNED_BS = {"tpl_nw": 16, "tpl_wd": 16, "to": 16, "mvcc": 16, "silo": 16, "tictoc": 12, "gputx": 8, "gacco": 24}
+# YCSB tile mode: warps per SM (one block per SM) with the lowest exec time at the bench
+# workload (configs[1], theta 0.6, 2 seeds).  Round 2: one transaction per warp (32-lane
+# tiles, lanes 16-31 idle for K = 16) beats two 16-lane tiles per warp for every scheme
+# (sum of the best exec times 3.99 -> 3.60 ms, GPUTx 0.74 -> 0.66, GaccO 0.78 -> 0.70):
+# a tile that waits or paces no longer shares its warp's issue slots and sleeps with
+# another transaction (profiles/r02_tune_lanes32.jsonl vs r02_tune_lanes16.jsonl).
+# Round 1 (16 lanes): profiles/r01_tune_bs.jsonl.
+TUNED_BS = {"tpl_nw": 32, "tpl_wd": 32, "to": 16, "mvcc": 24, "silo": 24, "tictoc": 24, "gputx": 8, "gacco": 8}
+TUNED_BS_16 = {"tpl_nw": 20, "tpl_wd": 20, "to": 8, "mvcc": 20, "silo": 12, "tictoc": 16, "gputx": 8, "gacco": 24}
 
 
 # TPC-C tile mode (32 lanes), configs[4] shape on one GPU (512 warehouses, 64K batch;
@@ -293,7 +297,7 @@ def tpcc_launch(args, scheme, n_sms, loopback=False):
 
 def launch_of(args, scheme, n_sms):
     if args.launch == "tuned" and args.lanes > 1 and args.wd == 0:
-        return {"wd": 0, "bs": TUNED_BS[scheme], "grid": n_sms}
+        return {"wd": 0, "bs": (TUNED_BS if args.lanes == 32 else TUNED_BS_16)[scheme], "grid": n_sms}
     return {"wd": args.wd, "bs": args.bs, "grid": 0}
 
 

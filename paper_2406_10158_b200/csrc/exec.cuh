@@ -392,9 +392,12 @@ GC_DEV bool gacco_access(Th &th, const typename WL::Params &y, typename WL::Lane
 #ifndef GC_KSET_MAX_SLEEP_NS
 #define GC_KSET_MAX_SLEEP_NS 50000u
 #endif
+#ifndef GC_KSET_TIGHT_DIST
+#define GC_KSET_TIGHT_DIST 1   // distances polled tightly (kdone lags the last finisher by a round trip)
+#endif
 GC_DEV unsigned kset_sleep_ns(u64 dist) {
-    if (dist <= 1) return 32u;
-    const u64 ns = 1500ull * (dist - 1);
+    if (dist <= GC_KSET_TIGHT_DIST) return 32u;
+    const u64 ns = 1500ull * (dist - GC_KSET_TIGHT_DIST);
     return ns < GC_KSET_MAX_SLEEP_NS ? (unsigned)ns : GC_KSET_MAX_SLEEP_NS;
 }
 // wait until K-set k-1 is the frontier (every earlier K-set complete)
@@ -441,13 +444,26 @@ GC_DEV bool kset_wait(Th &th, const ExecParams &p, u32 k) {
     if (th.timing) th.st[STAGE_WAIT] += clk64() - t0;
     return ok;
 }
+// Experiment builds (-DGC_TRACE_COMMIT=1, tools/trace_kset.py): trace[2050 + k] = when
+// K-set k completed, trace[4098 + k] = when the first member of K-set k passed its gate.
+GC_DEV void kset_trace(const ExecParams &p, u32 k, int what) {
+#if defined(GC_TRACE_COMMIT) && GC_TRACE_COMMIT
+    if (!p.trace || k >= 2048) return;
+    const u64 t = globaltimer_ns();
+    if (what == 0) p.trace[2050 + k] = t;
+    else atomicMin(&p.trace[4098 + k], t);
+#endif
+}
 GC_DEV void kset_done(const ExecParams &p, u32 k) {
     if (GC_KSET_KDONE) {
         const u32 old = atom_add_acqrel32(&p.rank_done[k], 1u);
         if (old + 1 == p.rank_count[k]) st_release(&p.ctl->kdone.v, (u64)k + 1);   // K-sets finish in order
     } else {
         const u32 old = atom_add_release32(&p.rank_done[k], 1u);
-        if (old + 1 == p.rank_count[k]) atomicMax(&p.ctl->kdone.v, (u64)k + 1);
+        if (old + 1 == p.rank_count[k]) {
+            atomicMax(&p.ctl->kdone.v, (u64)k + 1);
+            kset_trace(p, k, 0);
+        }
     }
 }
 
@@ -1539,6 +1555,7 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
             if (li == 0 && !kset_near(th, p, k)) st = ST_ABORT;
             if (tile.shfl(st, 0) == ST_DONE && act) WL::prefetch_access(p, y, L);
             if (li == 0 && st == ST_DONE && !kset_wait(th, p, k)) st = ST_ABORT;
+            if (li == 0 && st == ST_DONE) kset_trace(p, k, 1);
         }
         tile.sync();          // the leader's acquire orders every lane's accesses (warp barrier)
         if (tile.any(st != ST_DONE)) return RES_FATAL;

@@ -48,7 +48,9 @@ __global__ void a2_kernel(u64 *ring, uint32_t ring_words, Ctl *ctl, uint8_t *com
 
 // The background zeroing of a used word set (a2, reset stream): 32 B evict-first stores
 // (st.global.cs), so the 84-168 MB it writes beside the next submit's executor do not
-// displace that executor's control words and hot rows from L2 (GC_ZERO_CS=0: memset).
+// displace that executor's control words and hot rows from L2 (GC_ZERO_CS=0: memset;
+// measured neutral on the bench, 100.6 / 101.0 vs 101.3 / 99.5 M txn/s, profiles/
+// r02_bench_v21_zero_ab.txt).
 #ifndef GC_ZERO_CS
 #define GC_ZERO_CS 1
 #endif

@@ -51,7 +51,7 @@ def test_a1_generator_bitexact(c1, orc, seed):
 
 
 # (wd, bs, lanes): thread mode corners of the paper's launch grid + tile modes
-CORNERS = [(0, 32, 1), (5, 1, 1), (0, 1, 1), (5, 32, 1), (2, 8, 1), (0, 32, 4), (0, 8, 8), (0, 32, 16)]
+CORNERS = [(0, 32, 1), (5, 1, 1), (0, 1, 1), (5, 32, 1), (2, 8, 1), (0, 32, 4), (0, 8, 8), (0, 32, 16), (0, 8, 32)]
 
 
 @pytest.mark.parametrize("scheme", SCHEMES)
@@ -197,12 +197,13 @@ def test_c2_full_size_parity(c2, orc, scheme, theta, lanes):
                                         (0.95, False), (0.99, False)])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta, warm):
-    """configs[1] at full size in exactly the launch bench.py times (bench.launch_of: tile
-    16, per-scheme warps per SM, one block per SM), at the bench's theta and above."""
+    """configs[1] at full size in exactly the launch bench.py times (bench.launch_of: one
+    transaction per warp -- 32-lane tiles, 16 lanes idle at K = 16 -- per-scheme warps per
+    SM, one block per SM), at the bench's theta and above."""
     import types
     import bench
     db, S0, n = c2
-    a = types.SimpleNamespace(launch="tuned", lanes=16, wd=0, bs=32)
+    a = types.SimpleNamespace(launch="tuned", lanes=32, wd=0, bs=32)
     la = bench.launch_of(a, scheme, db.num_sms)
     assert la["grid"] == db.num_sms
     T = inputs.zipf_thresholds(n, theta)
@@ -212,7 +213,7 @@ def test_c2_full_size_parity_bench_launch(c2, orc, scheme, theta, warm):
     keys, ops = orc.ycsb_gen(79, n, B, K, W, T, A)
     db.snapshot(False)
     from paper_2406_10158_b200.gcctb import CC_FLAG_WARM
-    res = db.submit(b, scheme, lanes=16, watchdog_s=60, flags=CC_FLAG_WARM if warm else 0, **la)
+    res = db.submit(b, scheme, lanes=32, watchdog_s=60, flags=CC_FLAG_WARM if warm else 0, **la)
     st = db.sync()
     assert st.commits == B
     orc.check_ycsb(scheme, S0, keys, ops, K, res.host(db.stream), db.read_table(0))

@@ -35,7 +35,7 @@ def main():
         b = db.gen_ycsb(1 << 16, 16, 0.1, 3, T, A)
         for s in a.schemes.split(","):
             for mode in a.modes.split(","):
-                la = dict(lanes=1, wd=0, bs=32) if mode == "thread" else dict(lanes=16, wd=0, bs=bench.TUNED_BS[s],
+                la = dict(lanes=1, wd=0, bs=32) if mode == "thread" else dict(lanes=32, wd=0, bs=bench.TUNED_BS[s],
                                                                               grid=db.num_sms)
                 db.submit(b, s, watchdog_s=120, flags=a.flags, **la)
                 db.sync()

@@ -35,7 +35,7 @@ def main():
     for th in (0.0, 0.6):
         b = db.gen_ycsb(1 << 16, 16, 0.1, 3, inputs.zipf_thresholds(n, th), A)
         for s in SCHEMES:
-            la = dict(lanes=16, wd=0, bs=bench.TUNED_BS[s], grid=db.num_sms)
+            la = dict(lanes=32, wd=0, bs=bench.TUNED_BS[s], grid=db.num_sms)
             for pad in (0, 1):
                 ms = timed(db, b, s, CC_FLAG_META_PAD if pad else 0, **la)
                 print(json.dumps({"workload": f"ycsb theta={th}", "scheme": s, "pad": pad, "exec_ms": ms}), flush=True)
