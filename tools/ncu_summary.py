@@ -86,7 +86,7 @@ def main():
     except Exception:
         entries = []
     entries = [e for e in entries if e.get("config") != a.config]
-    entries.append({"config": a.config, "kernel": "exec_tile_kernel<*,YcsbWL,16> (8 schemes, mean)",
+    entries.append({"config": a.config, "kernel": "exec_tile_kernel<*,YcsbWL,%s> (8 schemes, mean)" % (a.config.split("lanes=")[1].split()[0] if "lanes=" in a.config else "?"),
                     "dram_bytes_per_launch": mean, "source": os.path.relpath(a.out, ROOT)})
     json.dump(entries, open(path, "w"), indent=1)
     print("\n".join(lines))

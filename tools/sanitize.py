@@ -34,7 +34,7 @@ def main():
     b = db.gen_ycsb(B, K, W, 5, T, A)
     keys, ops = oracle.ycsb_gen(5, n_rows, B, K, W, T, A)
     for scheme in only:
-        for lanes, wd, bs in ((1, 5, 8), (1, 5, 32), (1, 0, 32), (4, 0, 8), (16, 0, 4)):
+        for lanes, wd, bs in ((1, 5, 8), (1, 5, 32), (1, 0, 32), (4, 0, 8), (16, 0, 4), (32, 0, 4)):
             db.snapshot(False)
             db.prepare(b, scheme)
             res = db.submit(b, scheme, wd=wd, bs=bs, lanes=lanes, watchdog_s=600)
