@@ -165,7 +165,7 @@ class DB:
     def gen_ycsb(self, n_txn: int, K: int, W: float, seed: int, thresholds, mult: int) -> Batch:
         """thresholds: torch uint64/int64 cuda tensor or numpy uint64 array."""
         if isinstance(thresholds, torch.Tensor):
-            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            self._use(thresholds)
             ptr, on_dev = thresholds.data_ptr(), 1
             keep = thresholds
         else:
@@ -184,7 +184,7 @@ class DB:
         h = ctypes.c_void_p()
         keep = None
         if isinstance(keys, torch.Tensor) and keys.is_cuda:
-            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            self._use(keys, ops)
             st = G.lib().cc_batch_import_ycsb(self.h, keys.data_ptr(), ops.data_ptr(),
                                               keys.numel() // K, K, 1, ctypes.byref(h))
         else:
@@ -290,6 +290,17 @@ class DB:
         self._chk(G.lib().cc_prepare(self.h, batch.h, sid, flags))
 
     # ----------------------------------------------------------- partitioned TPC-C (a8)
+    def _use(self, *tensors):
+        """The db stream waits for the current stream, and each caller tensor is marked as
+        in use by the db stream: the caching allocator must not hand its memory to a later
+        allocation (e.g. the next torch.cat of a loopback round) before the library's
+        kernels on the db stream have read it -- otherwise a temporary freed right after
+        the call (a concatenated decision buffer) could be overwritten under them."""
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        for t in tensors:
+            if t is not None and t.is_cuda and t.numel():
+                t.record_stream(self.stream)
+
     def part_send(self):
         """(device uint8 tensor of the phase-B requests grouped by destination, counts list)."""
         ptr = ctypes.c_void_p()
@@ -304,13 +315,13 @@ class DB:
         n = recv.numel() // G.PART_REC_BYTES
         with torch.cuda.stream(self.stream):
             resp = torch.empty(n * G.PART_REC_BYTES, dtype=torch.uint8, device=recv.device)
-        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._use(recv)
         self._chk(G.lib().cc_part_apply(self.h, recv.data_ptr() if n else None, n, resp.data_ptr() if n else None))
         return resp
 
     def part_finish(self, resp: torch.Tensor):
         n = resp.numel() // G.PART_REC_BYTES
-        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._use(resp)
         self._chk(G.lib().cc_part_finish(self.h, resp.data_ptr() if n else None, n))
 
     # in-library exchange over peer memory (CC_FLAG_PART_P2P)
@@ -336,7 +347,7 @@ class DB:
         """Home: decide this round from the returned responses; device u64 decisions
         aligned with this round's send buffer (as a uint8 tensor of 8 bytes each)."""
         n = back.numel() // G.PART_REC_BYTES
-        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._use(back)
         ptr = ctypes.c_void_p()
         self._chk(G.lib().cc_part_decide(self.h, back.data_ptr() if n else None, n, ctypes.byref(ptr)))
         if n == 0:
@@ -345,7 +356,7 @@ class DB:
 
     def part_commit(self, recv: torch.Tensor, dec: torch.Tensor):
         n = dec.numel() // 8
-        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self._use(recv, dec)
         self._chk(G.lib().cc_part_commit(self.h, recv.data_ptr() if n else None, dec.data_ptr() if n else None, n))
 
     def part_next(self) -> int:
