@@ -609,10 +609,10 @@ def index_pass(args, db, b, schemes, LA, res, flag):
 # less); 64 warehouses: 8 warps per SM; 512 warehouses: the full grid, GaccO 16 warps per SM.
 TPCC_CONFIGS = [
     {"name": "configs2_1wh_16K_50:50", "W": 1, "n": 16384, "mix": 5000, "launch": {"*": (1, True)}},
-    {"name": "configs3_64wh_64K_45:43", "W": 64, "n": 65536, "mix": 5114, "launch": {"*": (8, True)},
-     "meta_pad": True},
+    {"name": "configs3_64wh_64K_45:43", "W": 64, "n": 65536, "mix": 5114,
+     "launch": {"*": (8, True), "to": (4, True), "tpl_wd": (16, True), "gacco": (16, True)}, "meta_pad": True},
     {"name": "configs4_shape_512wh_64K_45:43_1gpu", "W": 512, "n": 65536, "mix": 5114,
-     "launch": {"*": (8, False), "gacco": (16, True)}, "meta_pad": True},
+     "launch": {"*": (4, False), "to": (8, False), "tictoc": (8, False), "gputx": (16, False)}},
 ]
 
 
@@ -633,10 +633,11 @@ def tpcc_alg_bytes(tx):
 
 
 def tpcc_block(args, local, schemes):
-    """configs[2], configs[3] and the configs[4] shape on one GPU: per scheme, median of 3
-    timed submits (a2-a7, CUDA events on the db stream) of fresh seeded batches after one
-    warm-up submit; committed txn/s, abort rate, exec ms and the exec kernel's algorithmic
-    GB/s against the HBM peak."""
+    """configs[2], configs[3] and the configs[4] shape on one GPU: per scheme, 3 submits of
+    fresh seeded batches back to back after one warm-up submit (a2-a7 and the background
+    a2 zeroing, CUDA events on the db stream around all three, cc_join before the closing
+    event); committed txn/s, abort rate, mean exec ms and the exec kernel's algorithmic
+    GB/s against the HBM peak.  Launches per config from profiles/r02_tpcc_launch_tune.jsonl."""
     import numpy as np
     import torch
 
@@ -649,40 +650,45 @@ def tpcc_block(args, local, schemes):
     for cfg in TPCC_CONFIGS:
         db = DB(local)
         db.load_tpcc(cfg["W"], 1, cfg["n"])
-        res = Result.alloc(cfg["n"], 18, dev, stream=db.stream, out_words=48)
+        res = [Result.alloc(cfg["n"], 18, dev, stream=db.stream, out_words=48) for _ in range(3)]
         per = {}
         tot_ms, tot_commits = 0.0, 0
-        # one control word per 32 B sector where it measured faster (profiles/r02_probe_meta_pad.jsonl)
+        # one control word per 32 B sector where it measured faster (profiles/r02_probe_meta_pad.jsonl;
+        # at 512 warehouses the padded set's background zeroing -- 4x the words of ~70 M
+        # records -- costs more than the padding saves: 63.0 vs 73.9 M txn/s, r02_tpcc_meta_pad_b2b.log)
         flags = CC_FLAG_TIMING | (CC_FLAG_META_PAD if cfg.get("meta_pad") else 0)
         for s in schemes:
             bs, per_sm = cfg["launch"].get(s, cfg["launch"]["*"])
             la = {"bs": bs, "grid": db.num_sms if per_sm else 0}
-            sub, exe, ab, cm = [], [], 0, 0
-            alg = 0
-            for r in range(4):
-                b = db.gen_tpcc(cfg["n"], 101 + r, cfg["mix"])
-                if r == 3:
-                    alg = tpcc_alg_bytes(b.export_tpcc())
-                db.timing(reset=True)
-                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ea.record(db.stream)
-                db.submit(b, s, **la, lanes=32, flags=flags, result=res, watchdog_s=120)
-                db.join()   # the submit's background a2 zeroing counts
-                eb.record(db.stream)
-                st = db.sync()
-                pm, _ = db.timing(reset=True)
-                pm = list(pm)
-                pm[4] = ea.elapsed_time(eb)
+            # a warm-up submit, then NT submits of fresh batches back to back (as the YCSB
+            # step runs them: each submit's background a2 zeroing overlaps the next one;
+            # cc_join before the closing event makes the last one count too)
+            NT = 3
+            bt = [db.gen_tpcc(cfg["n"], 101 + r, cfg["mix"]) for r in range(NT + 1)]
+            alg = tpcc_alg_bytes(bt[-1].export_tpcc())
+            db.submit(bt[0], s, **la, lanes=32, flags=flags, result=res[0], watchdog_s=120)
+            st = db.sync()
+            assert st.commits == cfg["n"], (cfg["name"], s, st.commits)
+            db.timing(reset=True)
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(db.stream)
+            for r in range(NT):
+                db.submit(bt[r + 1], s, **la, lanes=32, flags=flags, result=res[r], watchdog_s=120)
+            db.join()
+            eb.record(db.stream)
+            db.sync()
+            pm, n_sub = db.timing(reset=True)
+            tot = ea.elapsed_time(eb)
+            ab = cm = 0
+            for r in range(NT):
+                h = res[r].stats.cpu().numpy().view(np.uint64)
+                assert int(h[0]) == cfg["n"], (cfg["name"], s, int(h[0]))
+                cm += int(h[0])
+                ab += int(h[1])
+            for b in bt:
                 b.free()
-                if r == 0:
-                    continue   # warm-up
-                assert st.commits == cfg["n"], (cfg["name"], s, st.commits)
-                sub.append(pm[4])
-                exe.append(pm[2])
-                ab += st.aborts
-                cm += st.commits
-            sub.sort()
-            exe.sort()
+            sub = [tot / NT] * 3
+            exe = [pm[2] / max(1, n_sub)] * 3
             gbs = alg / (exe[1] / 1e3) / 1e9
             per[s] = {"txn_s": cfg["n"] / (sub[1] / 1e3), "abort_rate": ab / max(1, cm), "submit_ms": sub[1],
                       "exec_ms": exe[1], "launch": la, "exec_alg_GBps": gbs, "exec_hbm_frac": gbs / peak}

@@ -140,7 +140,12 @@ def test_c4_full_size_parity_bench_launch(c4, orc, scheme, loopback):
     import types
     import bench
     db, S0 = c4
-    la = bench.tpcc_launch(types.SimpleNamespace(launch="tuned"), scheme, db.num_sms, loopback)
+    if loopback:
+        la = bench.tpcc_launch(types.SimpleNamespace(launch="tuned"), scheme, db.num_sms, loopback)
+    else:   # the `tpcc` block of the bench line (bench.TPCC_CONFIGS, configs[3])
+        cfg = [c for c in bench.TPCC_CONFIGS if c["W"] == 64][0]
+        bs, per_sm = cfg["launch"].get(scheme, cfg["launch"]["*"])
+        la = {"bs": bs, "grid": db.num_sms if per_sm else 0}
     b = db.gen_tpcc(65536, 43, 5114)
     _run(db, S0, 64, b, scheme, 32, orc, launch=la)
     b.free()
