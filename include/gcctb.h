@@ -350,7 +350,13 @@ typedef struct {
 
 /* Run batch b under desc->scheme: reset the scheme's CC state (a2), preprocess
  * (GPUTx/GaccO, a3), execute with compaction of aborts into a retry queue until every
- * transaction commits (a4-a6), then emit results (a7).  Asynchronous on the db stream. */
+ * transaction commits (a4-a6), then emit results (a7).  Asynchronous on the db stream.
+ * a2 (reading Z19): the db keeps two sets of control words, all zeros in
+ * the initial state of every scheme; a submit executes on a clean set and, once its
+ * executor is done, the set is zeroed on a background (reset) stream while the next
+ * submit runs on the other set (a partitioned submit zeroes its set in stream before the
+ * set's next use instead).  The db stream waits for that zeroing only when the set is
+ * reused; cc_join / cc_sync cover it. */
 cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_result *res);
 
 /* Pipelined preprocessing (GaccO's preprocessing

@@ -27,7 +27,15 @@ import inputs  # noqa: E402
 from paper_2406_10158_b200.api import DB  # noqa: E402
 from paper_2406_10158_b200.gcctb import CC_FLAG_TIMING, SCHEMES  # noqa: E402
 
-MODES = {"paper_wd0_bs32": dict(lanes=1, wd=0, bs=32), "tile16": dict(lanes=16, wd=0, bs=32)}
+MODES = {"paper_wd0_bs32": dict(lanes=1, wd=0, bs=32), "tile16": dict(lanes=16, wd=0, bs=32),
+         "bench_tile32": "bench"}   # the bench's launch: 32-lane tiles, bench.TUNED_BS warps, one block per SM
+
+
+def mode_kw(kw, scheme, db):
+    if kw == "bench":
+        import bench
+        return dict(lanes=32, wd=0, bs=bench.TUNED_BS[scheme], grid=db.num_sms)
+    return kw
 
 
 def cell(db, b, scheme, reps, watchdog, **kw):
@@ -69,7 +77,7 @@ def sweep_theta(a, out):
                 if (mode, s) in dead:
                     continue
                 try:
-                    r = cell(db, b, s, a.reps, a.watchdog, **kw)
+                    r = cell(db, b, s, a.reps, a.watchdog, **mode_kw(kw, s, db))
                 except Exception as e:   # watchdog / overflow: recorded, not fatal
                     r = dict(error=str(e)[:120])
                     dead.add((mode, s))
@@ -94,7 +102,7 @@ def sweep_presets(a, out):
         for mode, kw in MODES.items():
             for s in SCHEMES:
                 try:
-                    r = cell(db, b, s, a.reps, a.watchdog, **kw)
+                    r = cell(db, b, s, a.reps, a.watchdog, **mode_kw(kw, s, db))
                 except Exception as e:
                     r = dict(error=str(e)[:120])
                     db.close()
@@ -121,7 +129,8 @@ def sweep_stages(a, out):
             for s in SCHEMES:
                 try:
                     db.timing(reset=True)
-                    db.submit(b, s, flags=CC_FLAG_STAGES | CC_FLAG_TIMING | IDXF[a.index], watchdog_s=a.watchdog, **kw)
+                    db.submit(b, s, flags=CC_FLAG_STAGES | CC_FLAG_TIMING | IDXF[a.index], watchdog_s=a.watchdog,
+                              **mode_kw(kw, s, db))
                     st = db.sync()
                     ms, _ = db.timing(reset=True)
                     ns_per_cycle = 1e6 / max(st.sm_clock_khz, 1)
@@ -151,7 +160,7 @@ def sweep_latch(a, out):
             for s in SCHEMES[:6]:
                 for latched in (False, True):
                     try:
-                        k2 = dict(kw)
+                        k2 = dict(mode_kw(kw, s, db))
                         r = cell(db, b, s, a.reps, a.watchdog, **k2) if not latched else \
                             cell_flags(db, b, s, a.reps, a.watchdog, CC_FLAG_LATCHED, **k2)
                     except Exception as e:
