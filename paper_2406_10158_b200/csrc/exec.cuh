@@ -454,6 +454,9 @@ GC_DEV void kset_trace(const ExecParams &p, u32 k, int what) {
     else atomicMin(&p.trace[4098 + k], t);
 #endif
 }
+#ifndef GC_GPUTX_EARLY
+#define GC_GPUTX_EARLY 1
+#endif
 GC_DEV void kset_done(const ExecParams &p, u32 k) {
     if (GC_KSET_KDONE) {
         const u32 old = atom_add_acqrel32(&p.rank_done[k], 1u);
@@ -1548,12 +1551,33 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
     } else {   // GPUTx
         const u32 k = p.rank_of[gid];
         int st = ST_DONE;
+        // Early reads (GC_GPUTX_EARLY): an access whose item was last written (in id order)
+        // by a K-set before k-1 reads its row before the gate, once that K-set is complete
+        // -- nothing writes the item between then and this transaction (later writes of it
+        // rank above k).  Only the rows written by K-set k-1 are read after the gate, and
+        // those were just installed (L2).  The gate still orders every install.
+        bool done_rd = false;
+        if (GC_GPUTX_EARLY && act && k > 0) {
+            const u32 dep = p.acc_rdy[(u64)gid * p.K + li];
+            if (dep < k) {   // K-set dep - 1 <= k - 2 (or no earlier write)
+                if (dep > 0) {
+                    Spin sp(256);
+                    while (ld_acquire32(&p.rank_done[dep - 1]) < p.rank_count[dep - 1])
+                        if (!sp.wait(th)) { st = ST_ABORT; break; }
+                }
+                if (st == ST_DONE) {
+                    rd<WL>(th, y, L, gid, li, WL::row(y, L));
+                    done_rd = true;
+                }
+            }
+        }
+        if (tile.any(st != ST_DONE)) return RES_FATAL;
         if (k > 0) {
             // The rows were prefetched at claim time, often long before the gate opens, and
             // the L2 has turned over since: fetch them again once K-set k-1 is the frontier,
             // so the reads after the gate -- on the K-set chain's critical path -- hit L2.
             if (li == 0 && !kset_near(th, p, k)) st = ST_ABORT;
-            if (tile.shfl(st, 0) == ST_DONE && act) WL::prefetch_access(p, y, L);
+            if (tile.shfl(st, 0) == ST_DONE && act && !done_rd) WL::prefetch_access(p, y, L);
             if (li == 0 && st == ST_DONE && !kset_wait(th, p, k)) st = ST_ABORT;
             if (li == 0 && st == ST_DONE) kset_trace(p, k, 1);
         }
@@ -1561,8 +1585,12 @@ GC_DEV int run_tile(Tile &tile, Th &th, u32 gid, typename WL::Lane &L,
         if (tile.any(st != ST_DONE)) return RES_FATAL;
         if (act) {
             u64 *row = WL::row(y, L);
-            rd<WL>(th, y, L, gid, li, row);
+#if defined(GC_EXP_NOREAD) && GC_EXP_NOREAD   // timing experiment only (wrong results)
             if (L.w) inst<WL>(th, y, L, row);
+#else
+            if (!done_rd) rd<WL>(th, y, L, gid, li, row);
+            if (L.w) inst<WL>(th, y, L, row);
+#endif
         }
         tile.sync();   // every lane's install precedes the K-set release
         if (li == 0) kset_done(p, k);

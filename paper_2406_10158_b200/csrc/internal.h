@@ -86,7 +86,8 @@ struct ExecParams {
     const uint32_t *acc_seg;     // GaccO: segment (item) id of each access
     const uint32_t *acc_pos;     // GaccO: queue position of each access
     const uint32_t *acc_rdy;     // GaccO: cursor value at which the item's last earlier write
-                                 // has installed (0: none before it in the queue)
+                                 // has installed (0: none before it in the queue); GPUTx:
+                                 // 1 + the K-set of that write (0: none)
     uint32_t *cursor;            // GaccO: per-segment owner cursor
     const uint32_t *rank_order;  // GPUTx: transactions sorted by rank
     const uint32_t *rank_of;     // GPUTx: rank of each transaction

@@ -120,7 +120,7 @@ template <int G>
 __global__ void __launch_bounds__(1024) gputx_rank_kernel(
     const u64 *keys, const uint32_t *sorted_pos, const uint32_t *seg_of,
     const uint32_t *lw, uint32_t *rank, uint32_t n_txn, uint32_t K, Ctl *ctl,
-    u64 watchdog_ns, uint32_t poll_cap_ns) {
+    u64 watchdog_ns, uint32_t poll_cap_ns, uint32_t *acc_dep) {
     // a tile of G lanes per transaction, lane i resolves the predecessors of access i
     auto tile = cg::tiled_partition<G>(cg::this_thread_block());
     const uint32_t li = tile.thread_rank();
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
         s = tile.shfl(s, 0);
         if (s >= n_txn) return;
         const uint32_t gid = (uint32_t)s;
-        uint32_t r = 0;
+        uint32_t r = 0, dep = 0;
         bool fail = false;
         if (li < K) {
             const uint32_t p = sorted_pos[(u64)gid * K + li];
@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
             // (A write after a long run of reads -- a hot item -- otherwise paid one
             // dependent L2 round trip per read.)
             constexpr int B = 8;
+            bool first = has_q;   // the chunk at lo starts with the item's last earlier write
             for (uint32_t x = lo; x < hi && !fail; x += B) {
                 uint32_t u[B], ru[B];
 #pragma unroll
@@ -169,7 +170,14 @@ __global__ void __launch_bounds__(1024) gputx_rank_kernel(
                     }
                     if (u[j] != 0xFFFFFFFFu) r = max(r, ru[j] + 1);
                 }
+                if (first) {   // dependency of the access's row read: that write's K-set, + 1
+                    dep = ru[0] + 1;
+                    first = false;
+                }
             }
+            // (the executor may read the row once K-set dep - 1 has completed, before its
+            // own gate: only reads sit between that write and this access in id order)
+            acc_dep[(u64)gid * K + li] = dep;
         }
         if (tile.any(fail)) return;
         r = cg::reduce(tile, r, cg::greater<uint32_t>());
@@ -269,10 +277,10 @@ cudaError_t launch_prep_common(const ExecParams &p, PrepBufs &b, uint64_t n_reco
     if (grid_div > 1) grid = grid / grid_div > 0 ? grid / grid_div : 1;
     if (p.K <= 16)
         gputx_rank_kernel<16><<<grid, rank_block, 0, s>>>(sk, b.sorted_pos, b.seg_start, b.seg_id, b.rank, p.n_txn,
-                                                          p.K, p.ctl, p.watchdog_ns, poll_cap);
+                                                          p.K, p.ctl, p.watchdog_ns, poll_cap, b.acc_rdy);
     else
         gputx_rank_kernel<32><<<grid, rank_block, 0, s>>>(sk, b.sorted_pos, b.seg_start, b.seg_id, b.rank, p.n_txn,
-                                                          p.K, p.ctl, p.watchdog_ns, poll_cap);
+                                                          p.K, p.ctl, p.watchdog_ns, poll_cap, b.acc_rdy);
     // K-sets: transactions sorted by rank (stable: ids ascending inside a K-set)
     const unsigned gt = (p.n_txn + blk - 1) / blk;
     u64 *k1 = sk == b.keys_in ? b.keys_out : b.keys_in, *k2 = sk;   // the access keys are dead now

@@ -32,7 +32,7 @@ def main():
     for th in [float(x) for x in a.thetas.split(",")]:
         T = torch.from_numpy(inputs.zipf_thresholds(a.rows, th).view(np.int64)).to(dev)
         b = db.gen_ycsb(1 << 16, 16, 0.1, 3, T, A)
-        kw = dict(wd=0, bs=a.bs, lanes=16, grid=db.num_sms, watchdog_s=30)
+        kw = dict(wd=0, bs=a.bs, lanes=32, grid=db.num_sms, watchdog_s=30)
         db.submit(b, "gputx", **kw)
         db.sync()
         tr = torch.zeros(6146, dtype=torch.int64, device=dev)
