@@ -714,19 +714,20 @@ def launches_per_step(schemes, pipelined=False, a3_passes=3):
     """Kernel launches libgcctb issues per step (memsets excluded -- the CC words are zeroed
     by a kernel on the reset stream, counted: 1 per non-deterministic scheme): 1 generator;
     per scheme a2 = one prologue kernel (ring, retry queues, control block,
-    per-transaction results, batch error), the executor (1), a7 = commit positions +
-    copy_out + stats: 2PL dense tickets 1; TO / MVCC / Silo bitmap 5; TicToc ticket inverse
-    + gather + one cooperative sort + commit_pos = 4; GPUTx / GaccO iota + commit_pos 2 (+ 1
-    error merge when prepared).  a3 (GaccO: gather, a3_passes radix passes x 4 (the access
-    table has more than 128 tiles: the multi-kernel sort), marks, 3-kernel max-scan,
-    positions; GPUTx + fill, rank pass, keys, one cooperative rank sort, copy, bounds,
-    count) inline or on the prep stream when pipelined."""
+    per-transaction results, batch error), the executor (1), a7 = commit positions + one
+    copy-out kernel that also writes the stats: 2PL 0 (the dense ticket is the position);
+    TO / MVCC / Silo bitmap 5; TicToc ticket inverse + gather + one cooperative sort +
+    commit_pos = 4; GPUTx / GaccO iota + commit_pos 2 (+ 1 error merge when prepared).  a3
+    (GaccO: gather, a3_passes radix passes x 4 (the access table has more than 128 tiles:
+    the multi-kernel sort), marks, 3-kernel max-scan, positions; GPUTx + fill, rank pass,
+    keys, one cooperative rank sort, copy, bounds, count) inline or on the prep stream when
+    pipelined."""
     a3 = 1 + 4 * a3_passes + 1 + 3 + 1
     n = 1
     for s in schemes:
-        n += 1 + 1 + 2
+        n += 1 + 1 + 1
         if s in ("tpl_nw", "tpl_wd"):
-            n += 1 + 1
+            n += 1
         elif s in ("to", "mvcc", "silo"):
             n += 5 + 1
         elif s == "tictoc":

@@ -36,6 +36,7 @@ struct Ctl {
     Counter kdone;      // GPUTx: K-sets completed so far (they complete in order)
     Counter pacing_lk;  // transactions in post-lock-wait jitter right now (adaptive cap)
     Counter warm_hits;  // CC_FLAG_WARM: sink for the warm loads (practically never incremented)
+    Counter fin;        // a7: blocks of the copy-out launch that have finished (last one: stats)
 };
 // one event of the debug log: 24 bytes
 struct Event {

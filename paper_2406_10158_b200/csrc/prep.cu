@@ -310,6 +310,12 @@ __global__ void gather_hi_kernel(const u64 *hi, const uint32_t *perm, u64 *out, 
     if (p < n) out[p] = hi[perm[p]];
 }
 
+// a7 copy-out, one launch: per transaction the results (commit positions from `pos`, or --
+// 2PL, pos == null -- the dense lock-point ticket itself, see dense_ticket_pos_kernel),
+// the committed / restart totals; the last block to finish writes the stats words
+// (stats_body).  (Round 1 used three launches: positions, copy-out, stats.)
+__device__ void stats_body(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
+                           unsigned long long *sticky);
 __global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t *pos) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t c = 0, a = 0;
@@ -322,13 +328,23 @@ __global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t 
         if (r.restarts) r.restarts[i] = a;
         if (r.order_hi) r.order_hi[i] = p.order_hi[i];
         if (r.order_lo) r.order_lo[i] = p.order_lo[i];
-        if (r.commit_pos) r.commit_pos[i] = pos[i];
+        if (r.commit_pos) r.commit_pos[i] = pos ? pos[i] : (c ? (uint32_t)p.order_lo[i] : 0xFFFFFFFFu);
     }
     c = __reduce_add_sync(0xFFFFFFFFu, c);
     a = __reduce_add_sync(0xFFFFFFFFu, a);
     if ((threadIdx.x & 31) == 0) {
         if (c) atomicAdd(&p.ctl->done.v, (u64)c);
         if (a) atomicAdd(&p.ctl->aborts.v, (u64)a);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();   // this block's totals before its finish count
+        const u64 f = atomicAdd(&p.ctl->fin.v, 1ull);
+        if (f == gridDim.x - 1) {   // every block's totals are in
+            __threadfence();
+            st_relaxed(&p.ctl->fin.v, 0ull);   // (for a later copy-out of the same control block)
+            if (r.stats) stats_body(p.ctl, r.stats, p.stages, p.sticky);
+        }
     }
 }
 
@@ -351,8 +367,8 @@ cudaError_t launch_stages_reduce(unsigned long long *stages, uint64_t n_threads,
     return cudaGetLastError();
 }
 
-__global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
-                             unsigned long long *sticky) {
+__device__ void stats_body(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
+                           unsigned long long *sticky) {
     if (c->err.v && sticky) atomicCAS(sticky, 0ull, c->err.v);   // survives the next submit's reset
     stats[0] = c->done.v;
     stats[1] = c->aborts.v;
@@ -363,6 +379,10 @@ __global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long 
     for (int k = 6; k < CC_STATS_WORDS; k++) stats[k] = 0;
     if (stages)
         for (int k = 0; k < 7; k++) stats[8 + k] = stages[k];
+}
+__global__ void stats_kernel(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
+                             unsigned long long *sticky) {
+    stats_body(c, stats, stages, sticky);
 }
 
 // 2PL: the lock-point ticket is drawn only by attempts that commit, so the committed
@@ -487,7 +507,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
     // commit positions: a stable radix sort of the order keys (lo, then hi when used)
     uint32_t *pos = b.acc_pos;   // reuse as n-sized scratch after execution
     if (dense_ticket) {
-        dense_ticket_pos_kernel<<<g, blk, 0, s>>>(p.order_lo, p.committed, pos, n);
+        pos = nullptr;   // copy_out takes the ticket as the position
     } else if (deterministic) {
         iota_kernel<<<g, blk, 0, s>>>(b.rank_order, n);
         commit_pos_kernel<<<g, blk, 0, s>>>(b.rank_order, p.committed, pos, n);
@@ -525,8 +545,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         }
         commit_pos_kernel<<<g, blk, 0, s>>>(perm, p.committed, pos, n);
     }
-    copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);
-    stats_kernel<<<1, 1, 0, s>>>(p.ctl, res.stats, p.stages, p.sticky);
+    copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);   // + the stats words (last block; res.stats is set)
     return cudaGetLastError();
 }
 

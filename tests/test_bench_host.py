@@ -30,13 +30,13 @@ def test_tpcc_configs_cover_every_scheme():
 
 
 def test_launch_count_follows_the_submit_sequence():
-    # a1 generator + per scheme: a2 (1) + exec (1) + copy_out + stats (2) + commit positions
-    # + the background zeroing kernel of the non-deterministic schemes
+    # a1 generator + per scheme: a2 (1) + exec (1) + copy-out with stats (1) + commit
+    # positions + the background zeroing kernel of the non-deterministic schemes
     s2 = bench.launches_per_step(["tpl_nw"])
-    assert s2 == 1 + 1 + 1 + 2 + 1 + 1
-    assert bench.launches_per_step(["to"]) == 1 + 1 + 1 + 2 + 5 + 1
-    assert bench.launches_per_step(["tictoc"]) == 1 + 1 + 1 + 2 + 4 + 1
-    assert bench.launches_per_step(["tpl_nw", "to"]) == s2 + (1 + 1 + 2 + 5 + 1)
+    assert s2 == 1 + 1 + 1 + 1 + 0 + 1
+    assert bench.launches_per_step(["to"]) == 1 + 1 + 1 + 1 + 5 + 1
+    assert bench.launches_per_step(["tictoc"]) == 1 + 1 + 1 + 1 + 4 + 1
+    assert bench.launches_per_step(["tpl_nw", "to"]) == s2 + (1 + 1 + 1 + 5 + 1)
     # a prepared (pipelined) deterministic submit adds one error merge; its a3 still runs
     # inside the step (on the prep stream)
     assert bench.launches_per_step(["gacco"], pipelined=True) == bench.launches_per_step(["gacco"]) + 1
