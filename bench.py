@@ -553,6 +553,7 @@ def tpcc_partitioned_block(args, rank, world, local, schemes, steps=3):
         if db is not None:
             db.close()
         return out
+    ms_local = -1.0
     try:
         res = {s: Result.alloc(n, 18, dev, stream=db.stream, out_words=48) for s in schemes}
 
@@ -572,14 +573,24 @@ def tpcc_partitioned_block(args, rank, world, local, schemes, steps=3):
             step(1 + i)
         e1.record(db.stream)
         db.sync()
-        ms = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms_local = e0.elapsed_time(e1)
+    except Exception as e:   # reported, never fatal for the headline line
+        out["error"] = f"{type(e).__name__}: {e}"
+    # every rank reaches these collectives, also after an error (no rank waits forever)
+    ok = torch.tensor([0 if "error" in out else 1], device=dev, dtype=torch.int32)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    ms = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if int(ok.item()) == 1:
         ms = float(ms.item())
         out.update({"value": steps * n * len(schemes) * world / (ms / 1e3), "unit": "txn/s",
                     "ms_per_step": ms / steps, "steps": steps})
+    elif "error" not in out:
+        out["error"] = "another rank failed"
+    try:
         db.close()
-    except Exception as e:   # reported, never fatal for the headline line
-        out["error"] = f"{type(e).__name__}: {e}"
+    except Exception:
+        pass
     return out
 
 
