@@ -1403,10 +1403,8 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
         if (timing) CUDA_TRY(db, cudaEventRecord(ev.ev[3], db->stream));
         cc_result r = *res;
         if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
-        CUDA_TRY(db, launch_finalize(p, r, db->prep, false, true, db->stream));
-        if ((void *)r.stats != (void *)db->stats_scratch)
-            CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS, cudaMemcpyDeviceToDevice,
-                                         db->stream));
+        CUDA_TRY(db, launch_finalize(p, r, db->prep, false, true, db->stream, false, false, nullptr,
+                                     (uint64_t *)db->stats_scratch));
         if (rkind == 1) {
             cc_status st1 = copy_results_out(db, hk, res_in, b->n_txn, out_words);
             if (st1) return st1;
@@ -1441,14 +1439,12 @@ cc_status cc_submit(cc_db db, cc_batch b, const cc_exec_desc *desc, const cc_res
     }
     CUDA_TRY(db, launch_finalize(p, r, db->prep, det, scheme == CC_TICTOC, db->stream,
                                  scheme == CC_TPL_NW || scheme == CC_TPL_WD, scheme == CC_TICTOC,
-                                 bitmap_rank ? &db->rank_bm : nullptr));
+                                 bitmap_rank ? &db->rank_bm : nullptr, (uint64_t *)db->stats_scratch));
     if (used) {   // a later cc_prepare of this batch may overwrite the buffers after this point
         CUDA_TRY(db, cudaEventRecord(used->consumed, db->stream));
         used->has_consumer = true;
     }
-    if ((void *)r.stats != (void *)db->stats_scratch)
-        CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS,
-                                     cudaMemcpyDeviceToDevice, db->stream));
+
     if (rkind == 1) {
         cc_status st1 = copy_results_out(db, hk, res_in, b->n_txn, out_words);
         if (st1) return st1;
@@ -1598,10 +1594,8 @@ cc_status cc_part_finish(cc_db db, const void *resp, uint64_t n_sent) {
     if (P.timing) CUDA_TRY(db, cudaEventRecord(P.ev.ev[3], db->stream));
     cc_result r = P.res;
     if (!r.stats) r.stats = (uint64_t *)db->stats_scratch;
-    CUDA_TRY(db, launch_finalize(P.p, r, db->prep, false, true, db->stream));
-    if ((void *)r.stats != (void *)db->stats_scratch)
-        CUDA_TRY(db, cudaMemcpyAsync(db->stats_scratch, r.stats, 8 * CC_STATS_WORDS, cudaMemcpyDeviceToDevice,
-                                     db->stream));
+    CUDA_TRY(db, launch_finalize(P.p, r, db->prep, false, true, db->stream, false, false, nullptr,
+                                 (uint64_t *)db->stats_scratch));
     if (P.timing) {
         CUDA_TRY(db, cudaEventRecord(P.ev.ev[4], db->stream));
         db->pending.push_back(P.ev);

@@ -379,6 +379,11 @@ GC_DEV bool gacco_access(Th &th, const typename WL::Params &y, typename WL::Lane
         rd<WL>(th, y, L, gid, i, row);
     }
     if (L.w) inst<WL>(th, y, L, row);
+#if defined(GC_EXP_GACCO_RELAXED_READ) && GC_EXP_GACCO_RELAXED_READ
+    // timing ablation only: a read's hand-off without release semantics (the PTX model
+    // does not order the row load before a relaxed store; never shipped)
+    if (!L.w) { st_relaxed32(cur, pos + 1); return true; }
+#endif
     st_release32(cur, pos + 1);
     return true;
 }

@@ -185,7 +185,8 @@ struct RankBitmap {
 constexpr unsigned long long RANK_BITMAP_BITS = 1ull << 31;   // 31-bit timestamps
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket = false,
-                            bool lo_dense = false, const RankBitmap *rb = nullptr);
+                            bool lo_dense = false, const RankBitmap *rb = nullptr,
+                            uint64_t *stats_mirror = nullptr);   // also written with the stats
 size_t prep_cub_bytes(uint64_t n_acc, uint64_t n_txn);
 // sort.cu: stable LSD radix sort of u64 keys (+ optional u32 values) on bits [lo, hi),
 // keys_alt / vals_alt the ping-pong buffers, n = *n_dev if given (device-resident count,

@@ -316,7 +316,7 @@ __global__ void gather_hi_kernel(const u64 *hi, const uint32_t *perm, u64 *out, 
 // (stats_body).  (Round 1 used three launches: positions, copy-out, stats.)
 __device__ void stats_body(const Ctl *c, uint64_t *stats, const unsigned long long *stages,
                            unsigned long long *sticky);
-__global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t *pos) {
+__global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t *pos, uint64_t *mirror) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t c = 0, a = 0;
     if (i < p.n_txn) {
@@ -344,6 +344,7 @@ __global__ void copy_out_kernel(const ExecParams p, cc_result r, const uint32_t 
             __threadfence();
             st_relaxed(&p.ctl->fin.v, 0ull);   // (for a later copy-out of the same control block)
             if (r.stats) stats_body(p.ctl, r.stats, p.stages, p.sticky);
+            if (mirror && mirror != r.stats) stats_body(p.ctl, mirror, p.stages, nullptr);   // cc_sync's copy
         }
     }
 }
@@ -500,7 +501,7 @@ __global__ void ticket_perm_kernel(const u64 *lo, const uint8_t *committed, uint
 
 cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs &b,
                             bool deterministic, bool two_pass, cudaStream_t s, bool dense_ticket, bool lo_dense,
-                            const RankBitmap *rb) {
+                            const RankBitmap *rb, uint64_t *stats_mirror) {
     const uint32_t n = p.n_txn;
     const int blk = 256;
     const unsigned g = (n + blk - 1) / blk;
@@ -545,7 +546,7 @@ cudaError_t launch_finalize(const ExecParams &p, const cc_result &res, PrepBufs 
         }
         commit_pos_kernel<<<g, blk, 0, s>>>(perm, p.committed, pos, n);
     }
-    copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos);   // + the stats words (last block; res.stats is set)
+    copy_out_kernel<<<g, blk, 0, s>>>(p, res, pos, stats_mirror);   // + the stats words (last block; res.stats is set)
     return cudaGetLastError();
 }
 
