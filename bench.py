@@ -45,6 +45,12 @@ def parse():
                     help="tuned: per-scheme warps per SM measured best at configs[1] theta=0.6 "
                          "(profiles/r01_tune_bs.jsonl; one block per SM); fixed: --wd/--bs for "
                          "every scheme with a full-occupancy grid")
+    ap.add_argument("--phase-events", action=argparse.BooleanOptionalAction, default=False,
+                    help="CC_FLAG_TIMING (library phase events) on the timed submits: five CUDA "
+                         "events per submit, ~2 %% of the step (off: the exec share comes from the "
+                         "per-scheme pass)")
+    ap.add_argument("--scheme-events", action=argparse.BooleanOptionalAction, default=True,
+                    help="a CUDA event between the schemes of each timed step (step_scheme_ms)")
     ap.add_argument("--lanes", type=int, default=32)      # tile mode: lane i owns op i (32: one txn per warp); 1 = thread per txn (paper)
     ap.add_argument("--schemes", default=",".join(SCHEMES))
     ap.add_argument("--index", default="dense", choices=["dense", "tree", "binary", "eytz"],
@@ -353,14 +359,15 @@ def run_ours(args, rank, world, local):
         step's generation reuses them in stream order; cc_batch_free never blocks)."""
         b = db.gen_ycsb(args.batch, args.ops, args.write_frac, 1000 * (rank + 1) + i, T, A)
         prepare(b)
-        evs = ev_pool[len(scheme_ev)] if timing else None   # created before the timed region
+        sev = timing and args.scheme_events
+        evs = ev_pool[len(scheme_ev)] if sev else None   # created before the timed region
         for k, s in enumerate(schemes):
-            if timing:
+            if sev:
                 evs[k].record(stream)
-            db.submit(b, s, **LA[s], flags=xflags | (CC_FLAG_TIMING if timing else 0),
+            db.submit(b, s, **LA[s], flags=xflags | (CC_FLAG_TIMING if timing and args.phase_events else 0),
                       result=res[s], watchdog_s=60, lanes=args.lanes)
         db.join()   # the last submit's a2 zeroing (reset stream) belongs to this step
-        if timing:
+        if sev:
             evs[-1].record(stream)
             scheme_ev.append(evs)
         if keep:
@@ -475,7 +482,9 @@ def run_ours(args, rank, world, local):
         for tr in load_traffic() or []:   # ncu --set full DRAM bytes per launch, this exact config
             if tr.get("config") == config_key(args):
                 traffic = tr.get("dram_bytes_per_launch")
-        exec_share = phase_ms[2] / phase_ms[4] if phase_ms[4] else None
+        # exec share of the step: the timed submits' own phase events when on, else the
+        # per-scheme pass's exec times against the step time
+        exec_share = (phase_ms[2] / phase_ms[4]) if phase_ms[4] else exec_ms_total / (ms_max / args.steps)
         line = {
             "metric": METRIC, "value": value, "unit": "txn/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

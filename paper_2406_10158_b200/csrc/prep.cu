@@ -54,6 +54,12 @@ __global__ void a2_kernel(u64 *ring, uint32_t ring_words, Ctl *ctl, uint8_t *com
 #ifndef GC_ZERO_CS
 #define GC_ZERO_CS 1
 #endif
+#ifndef GC_ZERO_BLOCKS_PER_SM_X4
+#define GC_ZERO_BLOCKS_PER_SM_X4 2   // blocks per SM x 4 (2: one block per two SMs)
+#endif
+#ifndef GC_ZERO_THREADS
+#define GC_ZERO_THREADS 256
+#endif
 __global__ void zero_cs_kernel(u64 *p, uint64_t n4) {   // n4: 32 B units
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
@@ -64,7 +70,10 @@ cudaError_t launch_zero_words(u64 *p, uint64_t words, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    zero_cs_kernel<<<sms * 2, 512, 0, s>>>(p, words / 4);
+    // a small grid: the zeroing runs beside the next submit's executor and has ~two submits
+    // to finish; a full-GPU grid competes with that executor for issue slots
+    zero_cs_kernel<<<(unsigned)(sms * GC_ZERO_BLOCKS_PER_SM_X4 / 4 > 0 ? sms * GC_ZERO_BLOCKS_PER_SM_X4 / 4 : 1),
+                     GC_ZERO_THREADS, 0, s>>>(p, words / 4);
     return cudaGetLastError();
 }
 
