@@ -277,7 +277,9 @@ def run_reference(args, rank, world):
 # a tile that waits or paces no longer shares its warp's issue slots and sleeps with
 # another transaction (profiles/r02_tune_lanes32.jsonl vs r02_tune_lanes16.jsonl).
 # Round 1 (16 lanes): profiles/r01_tune_bs.jsonl.
-TUNED_BS = {"tpl_nw": 32, "tpl_wd": 32, "to": 16, "mvcc": 24, "silo": 24, "tictoc": 24, "gputx": 8, "gacco": 8}
+# GPUTx re-tuned after its reads moved before the gate (more transactions in flight now
+# pay: 0.57 ms at 8 warps -> 0.49 at 20, profiles/r02_tune_gputx_early.log).
+TUNED_BS = {"tpl_nw": 32, "tpl_wd": 32, "to": 16, "mvcc": 24, "silo": 24, "tictoc": 24, "gputx": 20, "gacco": 8}
 TUNED_BS_16 = {"tpl_nw": 20, "tpl_wd": 20, "to": 8, "mvcc": 20, "silo": 12, "tictoc": 16, "gputx": 8, "gacco": 24}
 
 
